@@ -1,0 +1,104 @@
+/*
+ * coxmoe.h — C ABI of libcoxmoe.so, the B200 (sm_100a) coalesced MoE expert stage.
+ *
+ * The reference (arxiv/paper_2605_17889, package `moeplan`) has no FFI layer: its
+ * expert stage exists only as the analytical row
+ *     expert_stage_parts(strategy, phase, system, model, batch, activation_map, coalesced)
+ *         (pkg/src/moeplan/costmodel.py:225-275)
+ * and its OP3 accounting (workload.py:156-165).  Each entry point below is one
+ * stage of the execution that row models; the Python host layer
+ * (paper_2605_17889_b200/executor.py) binds them with ctypes and mirrors the
+ * reference's types and error behaviour (ValueError on invalid input,
+ * costmodel.py:92-97, workload.py:157-158).  See INTEGRATION.md.
+ *
+ * Conventions
+ *   - All tensor arguments are DEVICE pointers owned by the caller; the library
+ *     never allocates device memory on these paths.  Work is stream-ordered on
+ *     the given cudaStream_t (passed as void* so no CUDA header is required).
+ *   - Row-major, contiguous.  bf16 = IEEE bfloat16 bit pattern (uint16).
+ *   - Return 0 on success, COX_EINVAL (-1) for invalid shapes/alignment,
+ *     COX_ECUDA (-2) for a CUDA error, COX_EUNSUPPORTED (-3) for an unsupported
+ *     device (anything but sm_100).  cox_last_error() returns a thread-local
+ *     message for the last failure.
+ */
+#ifndef COXMOE_H
+#define COXMOE_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define COX_OK 0
+#define COX_EINVAL (-1)
+#define COX_ECUDA (-2)
+#define COX_EUNSUPPORTED (-3)
+
+#define COX_DTYPE_F32 0
+#define COX_DTYPE_BF16 1
+
+#define COX_ROUTE_MIXTRAL 0  /* softmax over the k selected logits (renormalised) */
+#define COX_ROUTE_DEEPSEEK 1 /* softmax over all E, selected probabilities, no renorm */
+
+/* Library / device checks. */
+const char* cox_last_error(void);
+int cox_version(void);
+/* 0 if the current device is sm_100 (B200) and the kernels can launch. */
+int cox_device_check(void);
+
+/* K1 — router.  Replaces the top-k routing of PAPER.md:67 that the reference
+ * only accounts for analytically (workload.py:156-165 — OP3's D_X term).
+ *   x      [T, d]  (x_dtype: COX_DTYPE_BF16 or COX_DTYPE_F32), d % 8 == 0
+ *   wg     [E, d]  fp32 router weight
+ *   idx    [T, k]  int32 expert ids, descending logit, ties -> lower index
+ *                  (eas.py:364-374 convention)
+ *   w      [T, k]  fp32 routing weights
+ *   counts [E]     int32 tokens per expert (the per-batch analogue of eas.probe,
+ *                  eas.py:346-356)
+ * 1 <= k <= min(E, 8), E <= 256.  Logits are fp32 in the canonical order shared
+ * with the CPU oracle, so idx is bit-exact. */
+int cox_router_topk(const void* x, int x_dtype, const float* wg, int T, int d, int E, int k, int mode,
+                    int32_t* idx, float* w, int32_t* counts, void* stream);
+
+/* K2 — stable permutation by expert (coalesced dispatch).
+ *   x        [T, d] bf16, d % 8 == 0
+ *   offsets  [E+1]  int32 segment starts (segments padded to tile_m rows)
+ *   dst      [T, k] int32 row of x_perm that holds (t, j)
+ *   x_perm   [rows_cap, d] bf16, rows_cap >= T*k + E*(tile_m-1)
+ *   workspace of cox_permute_workspace_bytes(T, E) bytes. */
+size_t cox_permute_workspace_bytes(int T, int E);
+int cox_permute(const int32_t* idx, int T, int k, int E, int tile_m, const void* x, int d, int32_t* offsets,
+                int32_t* dst, void* x_perm, long long rows_cap, void* workspace, void* stream);
+
+/* K3 — grouped SwiGLU expert GEMM over the coalesced batch:
+ *   h[r, :] = silu(x_perm[r] W1_e^T) * (x_perm[r] W3_e^T) for r in segment e.
+ * Runs the groups group_experts[0..n_groups) (<= 64); w13[g] is the DEVICE
+ * pointer of that group's interleaved weight [2*ff, d] bf16 (128-row blocks:
+ * W1 rows 128i..128i+127, then W3 rows 128i..128i+127; see
+ * cox_interleave_w13).  Resident and streamed (cold) experts are just
+ * different groups/pointers, so a cold expert's GEMM can be issued separately
+ * once its copy has landed.  d % 64 == 0, ff % 128 == 0. */
+int cox_grouped_swiglu(const void* x_perm, long long rows_cap, const int32_t* offsets, int n_groups,
+                       const int32_t* group_experts, const void* const* w13, int d, int ff, void* h, void* stream);
+
+/* K4 — grouped down projection: y_perm[r] = h[r] W2_e^T.  w2[g]: [d, ff] bf16.
+ * ff % 64 == 0, d % 256 == 0. */
+int cox_grouped_down(const void* h, long long rows_cap, const int32_t* offsets, int n_groups,
+                     const int32_t* group_experts, const void* const* w2, int ff, int d, void* y_perm, void* stream);
+
+/* K5 — weighted top-k combine back to token order (+ optional shared-expert
+ * output, DeepSeek-V2):  out[t] = sum_j w[t,j] * y_perm[dst[t,j]] (+ shared[t]).
+ * out/shared dtype = out_dtype (bf16 or fp32). */
+int cox_combine(const void* y_perm, const int32_t* dst, const float* w, int T, int k, int d, const void* shared_out,
+                void* out, int out_dtype, void* stream);
+
+/* Layout helper: interleave W1 [ff, d] and W3 [ff, d] (bf16, device) into the
+ * K3 layout [2*ff, d] (device).  ff % 128 == 0. */
+int cox_interleave_w13(const void* w1, const void* w3, int ff, int d, void* w13, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* COXMOE_H */

@@ -1,0 +1,102 @@
+"""ctypes binding of libcoxmoe.so (include/coxmoe.h).
+
+There is deliberately no fallback: if the library is missing or the device is
+not sm_100, every op raises.  Error behaviour mirrors the reference: invalid
+shapes raise ValueError (moeplan raises ValueError for invalid input,
+costmodel.py:92-97, workload.py:157-158); CUDA failures raise RuntimeError.
+"""
+from __future__ import annotations
+
+import ctypes
+import threading
+from pathlib import Path
+
+_PKG = Path(__file__).resolve().parent
+LIB_PATH = _PKG / "libcoxmoe.so"
+
+COX_OK = 0
+COX_EINVAL = -1
+COX_ECUDA = -2
+COX_EUNSUPPORTED = -3
+DTYPE_F32 = 0
+DTYPE_BF16 = 1
+ROUTE_MIXTRAL = 0
+ROUTE_DEEPSEEK = 1
+
+# Every symbol include/coxmoe.h declares (tests check the .so exports them all).
+EXPORTS = (
+    "cox_last_error", "cox_version", "cox_device_check", "cox_router_topk", "cox_permute_workspace_bytes",
+    "cox_permute", "cox_grouped_swiglu", "cox_grouped_down", "cox_combine", "cox_interleave_w13",
+)
+
+_lock = threading.Lock()
+_lib = None
+_device_ok = None
+
+
+class CoxError(RuntimeError):
+    pass
+
+
+def _declare(L):
+    c_int, c_void_p, c_ll, c_size_t = ctypes.c_int, ctypes.c_void_p, ctypes.c_longlong, ctypes.c_size_t
+    L.cox_last_error.restype = ctypes.c_char_p
+    L.cox_last_error.argtypes = []
+    L.cox_version.restype = c_int
+    L.cox_device_check.restype = c_int
+    L.cox_router_topk.restype = c_int
+    L.cox_router_topk.argtypes = [c_void_p, c_int, c_void_p, c_int, c_int, c_int, c_int, c_int,
+                                  c_void_p, c_void_p, c_void_p, c_void_p]
+    L.cox_permute_workspace_bytes.restype = c_size_t
+    L.cox_permute_workspace_bytes.argtypes = [c_int, c_int]
+    L.cox_permute.restype = c_int
+    L.cox_permute.argtypes = [c_void_p, c_int, c_int, c_int, c_int, c_void_p, c_int, c_void_p, c_void_p,
+                              c_void_p, c_ll, c_void_p, c_void_p]
+    L.cox_grouped_swiglu.restype = c_int
+    L.cox_grouped_swiglu.argtypes = [c_void_p, c_ll, c_void_p, c_int, c_void_p, c_void_p, c_int, c_int,
+                                     c_void_p, c_void_p]
+    L.cox_grouped_down.restype = c_int
+    L.cox_grouped_down.argtypes = [c_void_p, c_ll, c_void_p, c_int, c_void_p, c_void_p, c_int, c_int,
+                                   c_void_p, c_void_p]
+    L.cox_combine.restype = c_int
+    L.cox_combine.argtypes = [c_void_p, c_void_p, c_void_p, c_int, c_int, c_int, c_void_p, c_void_p, c_int,
+                              c_void_p]
+    L.cox_interleave_w13.restype = c_int
+    L.cox_interleave_w13.argtypes = [c_void_p, c_void_p, c_int, c_int, c_void_p, c_void_p]
+
+
+def load(path: Path | None = None):
+    """Load (without touching the GPU) and declare the C ABI."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            p = Path(path) if path else LIB_PATH
+            if not p.exists():
+                raise CoxError(f"{p} is missing: run __graft_entry__.build() (no CPU fallback exists)")
+            L = ctypes.CDLL(str(p))
+            _declare(L)
+            _lib = L
+    return _lib
+
+
+def lib():
+    """The loaded library, after checking once that the device is sm_100."""
+    global _device_ok
+    L = load()
+    if _device_ok is None:
+        rc = L.cox_device_check()
+        _device_ok = rc == 0
+        if not _device_ok:
+            raise CoxError(L.cox_last_error().decode())
+    elif not _device_ok:
+        raise CoxError("libcoxmoe: unsupported device")
+    return L
+
+
+def check(rc: int, fn: str) -> None:
+    if rc == COX_OK:
+        return
+    msg = _lib.cox_last_error().decode() if _lib is not None else fn
+    if rc == COX_EINVAL:
+        raise ValueError(msg)
+    raise CoxError(msg)

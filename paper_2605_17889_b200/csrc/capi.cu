@@ -1,0 +1,158 @@
+// C ABI (include/coxmoe.h): argument validation, error reporting, dispatch.
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "../../include/coxmoe.h"
+#include "common.cuh"
+
+namespace cox {
+int launch_router(const void* x, int x_is_bf16, const float* wg, int T, int d, int E, int k, int mode, int32_t* idx,
+                  float* w, int32_t* counts, cudaStream_t s);
+size_t permute_workspace_bytes(int T, int E);
+int launch_permute(const int32_t* idx, int T, int k, int E, int tile_m, const void* x, int d, int32_t* offsets,
+                   int32_t* dst, void* x_perm, void* workspace, cudaStream_t s);
+int launch_grouped_gemm(int epi, const void* A, long long rows_cap, int K, const int32_t* offsets, int n_groups,
+                        const int32_t* group_expert, const void* const* B, int N, void* out, long long ldo,
+                        cudaStream_t s);
+int launch_combine(const void* y_perm, const int32_t* dst, const float* w, int T, int k, int d, const void* shared,
+                   void* out, int out_is_bf16, cudaStream_t s);
+
+__global__ void interleave_w13_kernel(const uint4* __restrict__ w1, const uint4* __restrict__ w3, int ff, int d,
+                                      uint4* __restrict__ w13) {
+  // row r of w13: block b = r / 128; source = (b even ? w1 : w3), row (b/2)*128 + r%128
+  const long vec_per_row = d / 8;
+  const long total = 2L * ff * vec_per_row;
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (long)gridDim.x * blockDim.x) {
+    const long r = i / vec_per_row, c = i % vec_per_row;
+    const long b = r / 128, rr = (b / 2) * 128 + (r % 128);
+    const uint4* src = (b & 1) ? w3 : w1;
+    w13[i] = src[rr * vec_per_row + c];
+  }
+}
+}  // namespace cox
+
+static thread_local std::string g_err;
+
+static int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+static int cuda_status(int rc, const char* what) {
+  if (rc == 0) return 0;
+  if (rc == COX_ECUDA) {
+    cudaError_t e = cudaGetLastError();
+    return fail(COX_ECUDA, "%s: CUDA error: %s", what, cudaGetErrorString(e));
+  }
+  if (rc == COX_EINVAL) return fail(COX_EINVAL, "%s: invalid argument (tensor map encode rejected the operand)", what);
+  return fail(rc, "%s: error %d", what, rc);
+}
+
+static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+extern "C" {
+
+const char* cox_last_error(void) { return g_err.c_str(); }
+
+int cox_version(void) { return 1; }
+
+int cox_device_check(void) {
+  int dev = 0, major = 0, minor = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return fail(COX_ECUDA, "no CUDA device");
+  cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+  cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
+  if (major != 10 || minor != 0)
+    return fail(COX_EUNSUPPORTED, "libcoxmoe is built for sm_100a only; device is sm_%d%d", major, minor);
+  return 0;
+}
+
+int cox_router_topk(const void* x, int x_dtype, const float* wg, int T, int d, int E, int k, int mode,
+                    int32_t* idx, float* w, int32_t* counts, void* stream) {
+  if (T < 0 || d <= 0 || d % 8 || E <= 0 || E > 256 || k < 1 || k > E || k > 8)
+    return fail(COX_EINVAL, "cox_router_topk: need T>=0, d%%8==0, 1<=k<=min(E,8), E<=256 (T=%d d=%d E=%d k=%d)", T, d,
+                E, k);
+  if (mode != COX_ROUTE_MIXTRAL && mode != COX_ROUTE_DEEPSEEK) return fail(COX_EINVAL, "cox_router_topk: bad mode %d", mode);
+  if (x_dtype != COX_DTYPE_BF16 && x_dtype != COX_DTYPE_F32) return fail(COX_EINVAL, "cox_router_topk: bad x_dtype");
+  if (T > 0 && (!x || !wg || !idx || !w || !counts)) return fail(COX_EINVAL, "cox_router_topk: null pointer");
+  if (!aligned16(x) || !aligned16(wg)) return fail(COX_EINVAL, "cox_router_topk: x and wg must be 16-byte aligned");
+  int rc = cox::launch_router(x, x_dtype == COX_DTYPE_BF16, wg, T, d, E, k, mode, idx, w, counts,
+                              static_cast<cudaStream_t>(stream));
+  return cuda_status(rc, "cox_router_topk");
+}
+
+size_t cox_permute_workspace_bytes(int T, int E) { return cox::permute_workspace_bytes(T, E); }
+
+int cox_permute(const int32_t* idx, int T, int k, int E, int tile_m, const void* x, int d, int32_t* offsets,
+                int32_t* dst, void* x_perm, long long rows_cap, void* workspace, void* stream) {
+  if (T < 0 || k < 1 || k > 8 || E < 1 || E > 256 || tile_m < 1 || d <= 0 || d % 8)
+    return fail(COX_EINVAL, "cox_permute: need 1<=k<=8, 1<=E<=256, tile_m>=1, d%%8==0");
+  if (rows_cap < (long long)T * k + (long long)E * (tile_m - 1))
+    return fail(COX_EINVAL, "cox_permute: rows_cap %lld < T*k + E*(tile_m-1) = %lld", rows_cap,
+                (long long)T * k + (long long)E * (tile_m - 1));
+  if (!aligned16(x) || !aligned16(x_perm)) return fail(COX_EINVAL, "cox_permute: x/x_perm must be 16-byte aligned");
+  if (!workspace || !offsets) return fail(COX_EINVAL, "cox_permute: null workspace/offsets");
+  int rc = cox::launch_permute(idx, T, k, E, tile_m, x, d, offsets, dst, x_perm, workspace,
+                               static_cast<cudaStream_t>(stream));
+  return cuda_status(rc, "cox_permute");
+}
+
+static int check_groups(const char* fn, int n_groups, const int32_t* group_experts, const void* const* w) {
+  if (n_groups < 0 || n_groups > 64) return fail(COX_EINVAL, "%s: n_groups must be in [0, 64]", fn);
+  for (int g = 0; g < n_groups; ++g) {
+    if (group_experts[g] < 0) return fail(COX_EINVAL, "%s: negative expert id", fn);
+    if (!w[g] || !aligned16(w[g])) return fail(COX_EINVAL, "%s: weight pointer %d null or unaligned", fn, g);
+  }
+  return 0;
+}
+
+int cox_grouped_swiglu(const void* x_perm, long long rows_cap, const int32_t* offsets, int n_groups,
+                       const int32_t* group_experts, const void* const* w13, int d, int ff, void* h, void* stream) {
+  if (d <= 0 || d % 64 || ff <= 0 || ff % 128)
+    return fail(COX_EINVAL, "cox_grouped_swiglu: need d%%64==0 and ff%%128==0 (d=%d ff=%d)", d, ff);
+  if (rows_cap < 1) return fail(COX_EINVAL, "cox_grouped_swiglu: rows_cap < 1");
+  if (!aligned16(x_perm) || !aligned16(h)) return fail(COX_EINVAL, "cox_grouped_swiglu: unaligned x_perm/h");
+  if (int rc = check_groups("cox_grouped_swiglu", n_groups, group_experts, w13)) return rc;
+  int rc = cox::launch_grouped_gemm(0, x_perm, rows_cap, d, offsets, n_groups, group_experts, w13, 2 * ff, h, ff,
+                                    static_cast<cudaStream_t>(stream));
+  return cuda_status(rc, "cox_grouped_swiglu");
+}
+
+int cox_grouped_down(const void* h, long long rows_cap, const int32_t* offsets, int n_groups,
+                     const int32_t* group_experts, const void* const* w2, int ff, int d, void* y_perm, void* stream) {
+  if (d <= 0 || d % 256 || ff <= 0 || ff % 64)
+    return fail(COX_EINVAL, "cox_grouped_down: need d%%256==0 and ff%%64==0 (d=%d ff=%d)", d, ff);
+  if (rows_cap < 1) return fail(COX_EINVAL, "cox_grouped_down: rows_cap < 1");
+  if (!aligned16(h) || !aligned16(y_perm)) return fail(COX_EINVAL, "cox_grouped_down: unaligned h/y_perm");
+  if (int rc = check_groups("cox_grouped_down", n_groups, group_experts, w2)) return rc;
+  int rc = cox::launch_grouped_gemm(1, h, rows_cap, ff, offsets, n_groups, group_experts, w2, d, y_perm, d,
+                                    static_cast<cudaStream_t>(stream));
+  return cuda_status(rc, "cox_grouped_down");
+}
+
+int cox_combine(const void* y_perm, const int32_t* dst, const float* w, int T, int k, int d, const void* shared_out,
+                void* out, int out_dtype, void* stream) {
+  if (T < 0 || k < 1 || k > 8 || d <= 0 || d % 8) return fail(COX_EINVAL, "cox_combine: need 1<=k<=8, d%%8==0");
+  if (out_dtype != COX_DTYPE_BF16 && out_dtype != COX_DTYPE_F32) return fail(COX_EINVAL, "cox_combine: bad out_dtype");
+  if (!aligned16(y_perm) || !aligned16(out) || !aligned16(shared_out))
+    return fail(COX_EINVAL, "cox_combine: unaligned operand");
+  int rc = cox::launch_combine(y_perm, dst, w, T, k, d, shared_out, out, out_dtype == COX_DTYPE_BF16,
+                               static_cast<cudaStream_t>(stream));
+  return cuda_status(rc, "cox_combine");
+}
+
+int cox_interleave_w13(const void* w1, const void* w3, int ff, int d, void* w13, void* stream) {
+  if (ff <= 0 || ff % 128 || d <= 0 || d % 8) return fail(COX_EINVAL, "cox_interleave_w13: need ff%%128==0, d%%8==0");
+  if (!aligned16(w1) || !aligned16(w3) || !aligned16(w13)) return fail(COX_EINVAL, "cox_interleave_w13: unaligned");
+  cox::interleave_w13_kernel<<<1184, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<const uint4*>(w1), static_cast<const uint4*>(w3), ff, d, static_cast<uint4*>(w13));
+  return cuda_status(cudaGetLastError() == cudaSuccess ? 0 : COX_ECUDA, "cox_interleave_w13");
+}
+
+}  // extern "C"

@@ -1,0 +1,387 @@
+// K3/K4 — coalesced grouped expert GEMM on 5th-gen tensor cores (sm_100a).
+//
+// The paper's OP3 ("gated FFN execution per expert") run over
+// the WHOLE ordinary batch of each expert at once (the
+// coalesced_expert_batch contract of costmodel.py:45-73): one persistent launch
+// covers every (expert, m-tile, n-tile) of every group.
+//
+//   K3 (EPI_SWIGLU): h[rows, ff]  = silu(A W1^T) * (A W3^T), W13 interleaved in
+//                    128-row blocks (gate block, up block, ...) so that one
+//                    256-wide accumulator tile holds matching gate/up columns.
+//   K4 (EPI_STORE) : y[rows, d]   = h W2^T.
+//
+// Machine mapping:
+//   * 2-CTA pairs (cluster 2x1): tcgen05.mma.cta_group::2, M=256 (128 A rows per
+//     CTA), N=256 (128 B rows per CTA), K=16 per instruction, fp32 accumulators
+//     in TMEM (2 x 256 columns: the epilogue of tile i overlaps the MMAs of i+1).
+//   * TMA (cp.async.bulk.tensor, 128B swizzle) streams 64-wide K slices of A and
+//     B into a 6-stage smem ring guarded by mbarriers; both CTAs' loads complete
+//     on the leader's "full" barrier, the leader's MMA commit frees the slot in
+//     both CTAs (multicast commit).
+//   * Warp roles: w0 TMA producer, w1 MMA issuer (leader CTA, one thread),
+//     w2 TMEM allocator, w4..w7 epilogue (TMEM -> registers -> global).
+//   * Persistent static schedule: 74 pairs on 148 SMs walk the tile list;
+//     tiles are rasterised in bands of `band` n-tiles so that concurrently
+//     running pairs share A rows and B bands in L2.
+// Expert segments need no padding: rows of a partial m-tile that belong to the
+// next segment are computed but never stored.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <mutex>
+#include <unordered_map>
+
+#include "common.cuh"
+
+namespace cox {
+
+constexpr int GM_BM = 128;  // A rows per CTA (pair: 256)
+constexpr int GM_BN = 256;  // MMA N per pair (B rows per CTA: 128)
+constexpr int GM_BK = 64;   // one 128-byte swizzle atom of bf16
+constexpr int GM_STAGES = 6;
+constexpr int GM_MAXG = 64;
+constexpr int GM_THREADS = 256;
+constexpr uint32_t GM_A_BYTES = GM_BM * GM_BK * 2;         // 16 KB
+constexpr uint32_t GM_B_BYTES = (GM_BN / 2) * GM_BK * 2;   // 16 KB
+constexpr uint32_t GM_TMEM_COLS = 512;
+constexpr int EPI_SWIGLU = 0;
+constexpr int EPI_STORE = 1;
+
+struct alignas(64) GemmParams {
+  CUtensorMap a_map;
+  CUtensorMap b_map[GM_MAXG];
+  const int32_t* offsets;
+  void* out;
+  long long ldo;
+  int group_expert[GM_MAXG];
+  int n_groups;
+  int K;
+  int n_tiles;
+  int band;
+};
+
+constexpr size_t GM_SMEM_BYTES = 1024 + GM_STAGES * (GM_A_BYTES + GM_B_BYTES) + 256 + 4 * (3 * GM_MAXG + 4);
+
+struct TileCoord {
+  int g, m, n;
+};
+
+COX_DEV TileCoord decode_tile(int t, const int* s_prefix, const int* s_rows, int band) {
+  TileCoord c;
+  int g = 0;
+  while (t >= s_prefix[g + 1]) ++g;
+  const int local = t - s_prefix[g];
+  const int mt = (s_rows[g] + 2 * GM_BM - 1) / (2 * GM_BM);
+  const int per_band = mt * band;
+  const int b = local / per_band;
+  const int r = local - b * per_band;
+  c.g = g;
+  c.m = r / band;
+  c.n = b * band + (r - c.m * band);
+  return c;
+}
+
+COX_DEV float silu_f(float g) { return g * __frcp_rn(1.0f + __expf(-g)); }
+
+template <int EPI>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GM_THREADS, 1)
+    grouped_gemm_kernel(const __grid_constant__ GemmParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + GM_STAGES * GM_A_BYTES;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sB + GM_STAGES * GM_B_BYTES);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + GM_STAGES;
+  uint64_t* tfull = bars + 2 * GM_STAGES;
+  uint64_t* tempty = bars + 2 * GM_STAGES + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * GM_STAGES + 4);
+  int* s_prefix = reinterpret_cast<int*>(tmem_slot + 4);
+  int* s_rows = s_prefix + GM_MAXG + 1;
+  int* s_row0 = s_rows + GM_MAXG;
+
+  const uint32_t rank = cluster_ctarank();
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < GM_STAGES; ++s) {
+      mbar_init(smem_u32(&full[s]), 1);
+      mbar_init(smem_u32(&empty[s]), 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(smem_u32(&tfull[a]), 1);
+      mbar_init(smem_u32(&tempty[a]), 8);  // 4 epilogue warps x 2 CTAs
+    }
+    fence_mbar_init();
+    int acc = 0;
+    for (int g = 0; g < p.n_groups; ++g) {
+      const int e = p.group_expert[g];
+      const int r0 = p.offsets[e];
+      const int rows = p.offsets[e + 1] - r0;
+      s_row0[g] = r0;
+      s_rows[g] = rows;
+      s_prefix[g] = acc;
+      acc += ((rows + 2 * GM_BM - 1) / (2 * GM_BM)) * p.n_tiles;
+    }
+    s_prefix[p.n_groups] = acc;
+  }
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&p.a_map);
+    for (int g = 0; g < p.n_groups; ++g) tma_prefetch_desc(&p.b_map[g]);
+  }
+  if (warp == 2) tmem_alloc<2>(smem_u32(tmem_slot), GM_TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  tc_fence_after();
+
+  const uint32_t tmem_base = *tmem_slot;
+  const int total = s_prefix[p.n_groups];
+  const int cid = blockIdx.x >> 1;
+  const int ncl = gridDim.x >> 1;
+  const int nk = p.K / GM_BK;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer
+    if (lane == 0) {
+      uint32_t stage = 0, phase = 0;
+      for (int t = cid; t < total; t += ncl) {
+        const TileCoord c = decode_tile(t, s_prefix, s_rows, p.band);
+        const int a_row = s_row0[c.g] + c.m * 2 * GM_BM + (int)rank * GM_BM;
+        const int b_row = c.n * GM_BN + (int)rank * (GM_BN / 2);
+        const CUtensorMap* bmap = &p.b_map[c.g];
+        for (int kb = 0; kb < nk; ++kb) {
+          mbar_wait(smem_u32(&empty[stage]), phase ^ 1);
+          const uint32_t fb_local = smem_u32(&full[stage]);
+          if (rank == 0) mbar_arrive_expect_tx(fb_local, 2 * (GM_A_BYTES + GM_B_BYTES));
+          const uint32_t fb = mapa(fb_local, 0);
+          tma_load_2d_pair(smem_u32(sA + stage * GM_A_BYTES), &p.a_map, fb, kb * GM_BK, a_row);
+          tma_load_2d_pair(smem_u32(sB + stage * GM_B_BYTES), bmap, fb, kb * GM_BK, b_row);
+          if (++stage == GM_STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer (leader CTA)
+    if (rank == 0 && lane == 0) {
+      const uint32_t idesc = idesc_bf16_f32(2 * GM_BM, GM_BN);
+      uint32_t stage = 0, phase = 0;
+      int it = 0;
+      for (int t = cid; t < total; t += ncl, ++it) {
+        const int acc = it & 1;
+        const uint32_t acc_phase = (it >> 1) & 1;
+        mbar_wait(smem_u32(&tempty[acc]), acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * GM_BN;
+        for (int kb = 0; kb < nk; ++kb) {
+          mbar_wait(smem_u32(&full[stage]), phase);
+          tc_fence_after();
+          const uint32_t a_base = smem_u32(sA + stage * GM_A_BYTES);
+          const uint32_t b_base = smem_u32(sB + stage * GM_B_BYTES);
+#pragma unroll
+          for (int k = 0; k < GM_BK / 16; ++k) {
+            mma_bf16_ss<2>(d_tmem, sdesc_kmajor_sw128(a_base + k * 32), sdesc_kmajor_sw128(b_base + k * 32), idesc,
+                           (kb | k) != 0 ? 1u : 0u);
+          }
+          mma_commit<2>(smem_u32(&empty[stage]));
+          if (++stage == GM_STAGES) { stage = 0; phase ^= 1; }
+        }
+        mma_commit<2>(smem_u32(&tfull[acc]));
+      }
+    }
+    __syncwarp();
+  } else if (warp >= 4) {
+    // ------------------------------------------------------------ epilogue
+    const int ew = warp - 4;
+    const int row_in_cta = ew * 32 + lane;
+    const uint32_t tempty_leader0 = mapa(smem_u32(&tempty[0]), 0);
+    const uint32_t tempty_leader1 = mapa(smem_u32(&tempty[1]), 0);
+    __nv_bfloat16* out = static_cast<__nv_bfloat16*>(p.out);
+    int it = 0;
+    for (int t = cid; t < total; t += ncl, ++it) {
+      const TileCoord c = decode_tile(t, s_prefix, s_rows, p.band);
+      const int acc = it & 1;
+      const uint32_t acc_phase = (it >> 1) & 1;
+      mbar_wait(smem_u32(&tfull[acc]), acc_phase);
+      tc_fence_after();
+      const int local_row = c.m * 2 * GM_BM + (int)rank * GM_BM + row_in_cta;
+      const bool valid = local_row < s_rows[c.g];
+      const long long grow = (long long)s_row0[c.g] + local_row;
+      const uint32_t tbase = tmem_base + ((uint32_t)(ew * 32) << 16) + acc * GM_BN;
+      if constexpr (EPI == EPI_SWIGLU) {
+        __nv_bfloat16* orow = out + grow * p.ldo + (long long)c.n * (GM_BN / 2);
+#pragma unroll 1
+        for (int cc = 0; cc < (GM_BN / 2) / 32; ++cc) {
+          uint32_t gr[32], ur[32];
+          tmem_ld_32x32b_x32(tbase + cc * 32, gr);
+          tmem_ld_32x32b_x32(tbase + (GM_BN / 2) + cc * 32, ur);
+          tmem_ld_wait();
+          uint32_t pk[16];
+#pragma unroll
+          for (int q = 0; q < 16; ++q) {
+            const float g0 = __uint_as_float(gr[2 * q]), g1 = __uint_as_float(gr[2 * q + 1]);
+            const float u0 = __uint_as_float(ur[2 * q]), u1 = __uint_as_float(ur[2 * q + 1]);
+            pk[q] = pack_bf16x2(silu_f(g0) * u0, silu_f(g1) * u1);
+          }
+          if (valid) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              st_global_v4(orow + cc * 32 + q * 8, pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+          }
+        }
+      } else {
+        __nv_bfloat16* orow = out + grow * p.ldo + (long long)c.n * GM_BN;
+#pragma unroll 1
+        for (int cc = 0; cc < GM_BN / 32; ++cc) {
+          uint32_t r[32];
+          tmem_ld_32x32b_x32(tbase + cc * 32, r);
+          tmem_ld_wait();
+          uint32_t pk[16];
+#pragma unroll
+          for (int q = 0; q < 16; ++q) pk[q] = pack_bf16x2(__uint_as_float(r[2 * q]), __uint_as_float(r[2 * q + 1]));
+          if (valid) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              st_global_v4(orow + cc * 32 + q * 8, pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(acc ? tempty_leader1 : tempty_leader0);
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc<2>(tmem_base, GM_TMEM_COLS);
+  }
+}
+
+// ------------------------------------------------------------------ host side
+
+static PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void* f = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  });
+  return fn;
+}
+
+struct MapKey {
+  const void* ptr;
+  unsigned long long rows, cols;
+  unsigned box_rows;
+  bool operator==(const MapKey& o) const {
+    return ptr == o.ptr && rows == o.rows && cols == o.cols && box_rows == o.box_rows;
+  }
+};
+struct MapKeyHash {
+  size_t operator()(const MapKey& k) const {
+    return std::hash<const void*>()(k.ptr) ^ (k.rows * 1000003ull) ^ (k.cols * 998244353ull) ^ k.box_rows;
+  }
+};
+
+// bf16 row-major [rows, cols] -> TMA map with a {64 cols, box_rows rows} box, 128B swizzle.
+static int get_map(CUtensorMap* out, const void* ptr, unsigned long long rows, unsigned long long cols,
+                   unsigned box_rows) {
+  static std::mutex mu;
+  static std::unordered_map<MapKey, CUtensorMap, MapKeyHash> cache;
+  MapKey key{ptr, rows, cols, box_rows};
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find(key);
+    if (it != cache.end()) {
+      *out = it->second;
+      return 0;
+    }
+  }
+  auto enc = get_encode_fn();
+  if (!enc) return -2;
+  CUtensorMap m;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {cols * 2};
+  cuuint32_t box[2] = {64, box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return -1;
+  std::lock_guard<std::mutex> lk(mu);
+  if (cache.size() > 4096) cache.clear();
+  cache.emplace(key, m);
+  *out = m;
+  return 0;
+}
+
+static int pick_band(int n_tiles) {
+  for (int b : {8, 4, 2, 1})
+    if (n_tiles % b == 0) return b;
+  return 1;
+}
+
+static int g_num_sms = 0;
+
+// epi: EPI_SWIGLU (B = W13 interleaved [2ff, K], out = h [rows_cap, ff])
+//      EPI_STORE  (B = W2 [N, K],                out = y [rows_cap, N])
+int launch_grouped_gemm(int epi, const void* A, long long rows_cap, int K, const int32_t* offsets, int n_groups,
+                        const int32_t* group_expert, const void* const* B, int N, void* out, long long ldo,
+                        cudaStream_t s) {
+  if (n_groups <= 0) return 0;
+  static GemmParams p;  // large (8.6 KB): built in static storage, copied at launch
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lk(mu);
+  int rc = get_map(&p.a_map, A, (unsigned long long)rows_cap, (unsigned long long)K, GM_BM);
+  if (rc) return rc;
+  for (int g = 0; g < n_groups; ++g) {
+    rc = get_map(&p.b_map[g], B[g], (unsigned long long)N, (unsigned long long)K, GM_BN / 2);
+    if (rc) return rc;
+    p.group_expert[g] = group_expert[g];
+  }
+  p.offsets = offsets;
+  p.out = out;
+  p.ldo = ldo;
+  p.n_groups = n_groups;
+  p.K = K;
+  p.n_tiles = N / GM_BN;
+  p.band = pick_band(p.n_tiles);
+  if (g_num_sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (g_num_sms <= 0) g_num_sms = 148;
+  }
+  const int grid = (g_num_sms / 2) * 2;
+  cudaError_t err;
+  if (epi == EPI_SWIGLU) {
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(grouped_gemm_kernel<EPI_SWIGLU>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)GM_SMEM_BYTES);
+      attr = true;
+    }
+    grouped_gemm_kernel<EPI_SWIGLU><<<grid, GM_THREADS, GM_SMEM_BYTES, s>>>(p);
+  } else {
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(grouped_gemm_kernel<EPI_STORE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)GM_SMEM_BYTES);
+      attr = true;
+    }
+    grouped_gemm_kernel<EPI_STORE><<<grid, GM_THREADS, GM_SMEM_BYTES, s>>>(p);
+  }
+  err = cudaGetLastError();
+  return err == cudaSuccess ? 0 : -2;
+}
+
+}  // namespace cox

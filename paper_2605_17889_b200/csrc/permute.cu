@@ -1,0 +1,179 @@
+// K2 — deterministic, stable token permutation by expert (the coalesced
+// dispatch of PAPER.md:191,282: every expert sees its whole-batch token set
+// as one contiguous row block).
+//
+// Order contract (shared with oracle/oracle_router.c:oracle_permute): the
+// (token, slot) pairs of expert e occupy rows [offsets[e], offsets[e]+n_e) in
+// ascending token order; segments are padded to a multiple of tile_m rows
+// (padding rows are zero-filled).  No atomics decide placement:
+//   1. perm_hist    — per-block (256 tokens) expert histogram (smem atomics on
+//                     integers: order-independent result);
+//   2. perm_scan    — per-expert exclusive scan over blocks (one warp per
+//                     expert, shuffle scan) and the padded segment offsets;
+//   3. perm_scatter — in-block ranks from warp ballots (lane = token, so
+//                     popc(ballot & lanemask_lt) is the ascending-token rank),
+//                     then each token row is read ONCE (16 B vector loads) and
+//                     written to its k destinations.
+#include "common.cuh"
+
+namespace cox {
+
+constexpr int PM_TB = 256;  // tokens per block
+
+__global__ void __launch_bounds__(PM_TB) perm_hist(const int32_t* __restrict__ idx, int T, int k, int E,
+                                                    int32_t* __restrict__ block_counts) {
+  __shared__ int s_h[1024];
+  for (int i = threadIdx.x; i < E; i += blockDim.x) s_h[i] = 0;
+  __syncthreads();
+  long t = (long)blockIdx.x * PM_TB + threadIdx.x;
+  if (t < T)
+    for (int j = 0; j < k; ++j) atomicAdd(&s_h[idx[t * k + j]], 1);
+  __syncthreads();
+  for (int i = threadIdx.x; i < E; i += blockDim.x) block_counts[(long)blockIdx.x * E + i] = s_h[i];
+}
+
+// One block of 1024 threads; warp w scans experts w, w+32, ...
+__global__ void __launch_bounds__(1024) perm_scan(const int32_t* __restrict__ block_counts, int nb, int E, int tile_m,
+                                                  int32_t* __restrict__ block_base, int32_t* __restrict__ offsets,
+                                                  int32_t* __restrict__ seg_counts) {
+  __shared__ int s_tot[1024];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int per = (nb + 31) / 32;
+  for (int e = warp; e < E; e += 32) {
+    const int b0 = lane * per, b1 = min(nb, b0 + per);
+    int local = 0;
+    for (int b = b0; b < b1; ++b) local += block_counts[(long)b * E + e];
+    int incl = local;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      int v = __shfl_up_sync(0xffffffffu, incl, off);
+      if (lane >= off) incl += v;
+    }
+    int run = incl - local;
+    for (int b = b0; b < b1; ++b) {
+      block_base[(long)b * E + e] = run;
+      run += block_counts[(long)b * E + e];
+    }
+    if (lane == 31) s_tot[e] = incl;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int o = 0;
+    offsets[0] = 0;
+    for (int e = 0; e < E; ++e) {
+      seg_counts[e] = s_tot[e];
+      o += ((s_tot[e] + tile_m - 1) / tile_m) * tile_m;
+      offsets[e + 1] = o;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(PM_TB) perm_scatter(const int32_t* __restrict__ idx, int T, int k, int E,
+                                                       const int32_t* __restrict__ block_base,
+                                                       const int32_t* __restrict__ offsets,
+                                                       const __nv_bfloat16* __restrict__ x, int d,
+                                                       int32_t* __restrict__ dst, __nv_bfloat16* __restrict__ x_perm) {
+  __shared__ int s_wcnt[PM_TB / 32][256];
+  __shared__ int s_wbase[PM_TB / 32][256];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long t = (long)blockIdx.x * PM_TB + threadIdx.x;
+  const bool valid = t < T;
+  int ej[8], rj[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    ej[j] = (valid && j < k) ? idx[t * k + j] : -1;
+    rj[j] = 0;
+  }
+  const uint32_t lt = (1u << lane) - 1u;
+  for (int e = 0; e < E; ++e) {
+    bool has = false;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) has |= (ej[j] == e);
+    uint32_t bal = __ballot_sync(0xffffffffu, has);
+    if (lane == 0) s_wcnt[warp][e] = __popc(bal);
+    int r = __popc(bal & lt);
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      if (ej[j] == e) rj[j] = r;
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < E; e += blockDim.x) {
+    int run = offsets[e] + block_base[(long)blockIdx.x * E + e];
+    for (int w = 0; w < PM_TB / 32; ++w) {
+      s_wbase[w][e] = run;
+      run += s_wcnt[w][e];
+    }
+  }
+  __syncthreads();
+  int dj[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    dj[j] = (ej[j] >= 0) ? s_wbase[warp][ej[j]] + rj[j] : -1;
+    if (j < k && valid) dst[t * k + j] = dj[j];
+  }
+  // Row copies: the warp walks its 32 tokens; each row is read once, written k times.
+  const long tw0 = (long)blockIdx.x * PM_TB + warp * 32;
+  for (int i = 0; i < 32; ++i) {
+    const long ti = tw0 + i;
+    if (ti >= T) break;
+    int di[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) di[j] = __shfl_sync(0xffffffffu, dj[j], i);
+    const __nv_bfloat16* src = x + ti * (long)d;
+    for (int c0 = lane * 8; c0 < d; c0 += 32 * 8 * 4) {
+      uint4 v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        int c = c0 + u * 256;
+        if (c < d) v[u] = ld_nc_v4(src + c);
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        if (j >= k) break;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          int c = c0 + u * 256;
+          if (c < d) *reinterpret_cast<uint4*>(x_perm + (long)di[j] * d + c) = v[u];
+        }
+      }
+    }
+  }
+}
+
+// Zero the padding rows [offsets[e] + n_e, offsets[e+1]) of every segment.
+__global__ void perm_zero_pad(const int32_t* __restrict__ offsets, const int32_t* __restrict__ seg_counts, int E,
+                              int d, __nv_bfloat16* __restrict__ x_perm) {
+  const int e = blockIdx.y;
+  const long r0 = offsets[e] + seg_counts[e], r1 = offsets[e + 1];
+  const long n = (r1 - r0) * (long)d / 8;
+  uint4 z = make_uint4(0, 0, 0, 0);
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x)
+    reinterpret_cast<uint4*>(x_perm + r0 * d)[i] = z;
+}
+
+size_t permute_workspace_bytes(int T, int E) {
+  long nb = (T + PM_TB - 1) / PM_TB;
+  if (nb < 1) nb = 1;
+  return sizeof(int32_t) * (size_t)(2 * nb * E + E);
+}
+
+int launch_permute(const int32_t* idx, int T, int k, int E, int tile_m, const void* x, int d, int32_t* offsets,
+                   int32_t* dst, void* x_perm, void* workspace, cudaStream_t s) {
+  long nb = (T + PM_TB - 1) / PM_TB;
+  int32_t* block_counts = static_cast<int32_t*>(workspace);
+  int32_t* block_base = block_counts + (nb > 0 ? nb : 1) * E;
+  int32_t* seg_counts = block_base + (nb > 0 ? nb : 1) * E;
+  if (nb == 0) {
+    if (cudaMemsetAsync(offsets, 0, sizeof(int32_t) * (E + 1), s) != cudaSuccess) return -2;
+    return 0;
+  }
+  perm_hist<<<(int)nb, PM_TB, 0, s>>>(idx, T, k, E, block_counts);
+  perm_scan<<<1, 1024, 0, s>>>(block_counts, (int)nb, E, tile_m, block_base, offsets, seg_counts);
+  perm_scatter<<<(int)nb, PM_TB, 0, s>>>(idx, T, k, E, block_base, offsets,
+                                          static_cast<const __nv_bfloat16*>(x), d, dst,
+                                          static_cast<__nv_bfloat16*>(x_perm));
+  if (tile_m > 1) perm_zero_pad<<<dim3(8, E), 256, 0, s>>>(offsets, seg_counts, E, d, static_cast<__nv_bfloat16*>(x_perm));
+  return cudaGetLastError() == cudaSuccess ? 0 : -2;
+}
+
+}  // namespace cox

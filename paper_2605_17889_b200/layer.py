@@ -1,0 +1,123 @@
+"""The coalesced MoE expert stage on one B200: router -> permute -> grouped
+SwiGLU -> grouped down -> combine, all in libcoxmoe.so.
+
+``MoELayer.forward`` is the single-GPU, all-resident path (the reference's
+``AllocationStrategy(exp_r=E, exp_m=0, exp_c=0)``).  Residency/streaming and
+expert parallelism build on the same stage functions (executor.py, ep.py).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import torch
+
+from . import _lib, ops
+from .synthetic import LayerWeights
+
+MODES = {"mixtral": _lib.ROUTE_MIXTRAL, "deepseek": _lib.ROUTE_DEEPSEEK}
+
+
+@dataclass
+class StageBuffers:
+    T: int
+    idx: torch.Tensor
+    w: torch.Tensor
+    counts: torch.Tensor
+    offsets: torch.Tensor
+    dst: torch.Tensor
+    x_perm: torch.Tensor
+    h: torch.Tensor
+    y: torch.Tensor
+    out: torch.Tensor
+    workspace: torch.Tensor
+    shared_offsets: torch.Tensor | None = None
+    shared_h: torch.Tensor | None = None
+    shared_y: torch.Tensor | None = None
+
+
+def alloc_buffers(T: int, d: int, ff: int, E: int, k: int, tile_m: int, device, out_dtype=torch.bfloat16,
+                  shared_ff: int = 0) -> StageBuffers:
+    cap = ops.rows_capacity(T, k, E, tile_m)
+    bf = torch.bfloat16
+    b = StageBuffers(
+        T=T,
+        idx=torch.empty((T, k), dtype=torch.int32, device=device),
+        w=torch.empty((T, k), dtype=torch.float32, device=device),
+        counts=torch.empty((E,), dtype=torch.int32, device=device),
+        offsets=torch.empty((E + 1,), dtype=torch.int32, device=device),
+        dst=torch.empty((T, k), dtype=torch.int32, device=device),
+        x_perm=torch.empty((cap, d), dtype=bf, device=device),
+        h=torch.empty((cap, ff), dtype=bf, device=device),
+        y=torch.empty((cap, d), dtype=bf, device=device),
+        out=torch.empty((T, d), dtype=out_dtype, device=device),
+        workspace=torch.empty((max(16, ops.permute_workspace_bytes(T, E)),), dtype=torch.uint8, device=device),
+    )
+    if shared_ff:
+        b.shared_offsets = torch.tensor([0, T], dtype=torch.int32, device=device)
+        b.shared_h = torch.empty((max(T, 1), shared_ff), dtype=bf, device=device)
+        b.shared_y = torch.empty((max(T, 1), d), dtype=bf, device=device)
+    return b
+
+
+class MoELayer:
+    """One MoE layer's expert stage with every expert resident in HBM."""
+
+    def __init__(self, weights: LayerWeights, top_k: int, mode: str = "mixtral", tile_m: int = 1,
+                 out_dtype=torch.bfloat16):
+        if mode not in MODES:
+            raise ValueError(f"mode must be one of {sorted(MODES)}")
+        self.wts = weights
+        self.k = int(top_k)
+        self.mode = MODES[mode]
+        self.tile_m = int(tile_m)
+        self.out_dtype = out_dtype
+        self.E = weights.num_experts
+        self.d = weights.hidden_dim
+        self.ff = weights.expert_dim
+        if not (1 <= self.k <= self.E):
+            raise ValueError("top_k must satisfy 1 <= top_k <= experts_per_layer")
+        self.groups = list(range(self.E))
+        self.w13_list = [weights.w13[e] for e in range(self.E)]
+        self.w2_list = [weights.w2[e] for e in range(self.E)]
+        self.shared_ff = weights.shared_w2.shape[1] if weights.shared_w2 is not None else 0
+        if self.shared_ff and out_dtype != torch.bfloat16:
+            raise ValueError("shared experts require a bf16 output")
+        self._bufs: StageBuffers | None = None
+
+    def buffers(self, T: int, device) -> StageBuffers:
+        if self._bufs is None or self._bufs.T != T:
+            self._bufs = None
+            self._bufs = alloc_buffers(T, self.d, self.ff, self.E, self.k, self.tile_m, device, self.out_dtype,
+                                       self.shared_ff)
+        return self._bufs
+
+    # --- stages (all stream-ordered on the current stream) -------------------
+    def route(self, x: torch.Tensor, b: StageBuffers):
+        ops.router_topk(x, self.wts.wg, self.k, self.mode, out=(b.idx, b.w, b.counts))
+        ops.permute(b.idx, x, self.E, self.tile_m, out=(b.offsets, b.dst, b.x_perm), workspace=b.workspace)
+
+    def experts(self, b: StageBuffers, groups=None, w13=None, w2=None):
+        groups = self.groups if groups is None else groups
+        ops.grouped_swiglu(b.x_perm, b.offsets, groups, self.w13_list if w13 is None else w13, self.ff, h=b.h)
+        ops.grouped_down(b.h, b.offsets, groups, self.w2_list if w2 is None else w2, self.d, y=b.y)
+
+    def shared_expert(self, x: torch.Tensor, b: StageBuffers):
+        if not self.shared_ff:
+            return None
+        ops.grouped_swiglu(x, b.shared_offsets, [0], [self.wts.shared_w13], self.shared_ff, h=b.shared_h)
+        ops.grouped_down(b.shared_h, b.shared_offsets, [0], [self.wts.shared_w2], self.d, y=b.shared_y)
+        return b.shared_y
+
+    def finish(self, b: StageBuffers, shared=None):
+        return ops.combine(b.y, b.dst, b.w, shared, out=b.out)
+
+    def forward(self, x: torch.Tensor) -> torch.Tensor:
+        if x.dtype != torch.bfloat16 or x.dim() != 2 or x.shape[1] != self.d:
+            raise ValueError(f"x must be bf16 [T, {self.d}]")
+        b = self.buffers(x.shape[0], x.device)
+        self.route(x, b)
+        self.experts(b)
+        sh = self.shared_expert(x, b)
+        return self.finish(b, sh)
+
+    __call__ = forward

@@ -1,0 +1,179 @@
+"""Torch-tensor front end of the C ABI: one function per kernel stage.
+
+Tensors are plain device memory here (torch is the allocator and the stream
+owner); every computation happens in libcoxmoe.so.  Functions validate the
+tensor metadata, then call the corresponding ``cox_*`` entry point on the
+current torch stream.
+"""
+from __future__ import annotations
+
+import ctypes
+from typing import Sequence
+
+import torch
+
+from . import _lib
+
+_BF16 = torch.bfloat16
+
+
+def _stream(stream=None) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+def _need(t: torch.Tensor, name: str, dtype=None, ndim=None):
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    if dtype is not None and t.dtype != dtype:
+        raise ValueError(f"{name} must be {dtype}, got {t.dtype}")
+    if ndim is not None and t.dim() != ndim:
+        raise ValueError(f"{name} must be {ndim}-D")
+
+
+def _ptrs(ts: Sequence[torch.Tensor]):
+    arr = (ctypes.c_void_p * max(1, len(ts)))()
+    for i, t in enumerate(ts):
+        arr[i] = t.data_ptr()
+    return arr
+
+
+def _ids(ids: Sequence[int]):
+    arr = (ctypes.c_int32 * max(1, len(ids)))()
+    for i, e in enumerate(ids):
+        arr[i] = int(e)
+    return arr
+
+
+def router_topk(x: torch.Tensor, wg: torch.Tensor, k: int, mode: int = _lib.ROUTE_MIXTRAL, out=None, stream=None):
+    """K1: -> (idx [T,k] int32, w [T,k] fp32, counts [E] int32)."""
+    _need(x, "x", ndim=2)
+    _need(wg, "wg", torch.float32, 2)
+    T, d = x.shape
+    E = wg.shape[0]
+    if wg.shape[1] != d:
+        raise ValueError("wg must be [E, d]")
+    if x.dtype == _BF16:
+        xdt = _lib.DTYPE_BF16
+    elif x.dtype == torch.float32:
+        xdt = _lib.DTYPE_F32
+    else:
+        raise ValueError("x must be bf16 or fp32")
+    if out is None:
+        idx = torch.empty((T, k), dtype=torch.int32, device=x.device)
+        w = torch.empty((T, k), dtype=torch.float32, device=x.device)
+        counts = torch.empty((E,), dtype=torch.int32, device=x.device)
+    else:
+        idx, w, counts = out
+    L = _lib.lib()
+    _lib.check(L.cox_router_topk(x.data_ptr(), xdt, wg.data_ptr(), T, d, E, k, mode, idx.data_ptr(), w.data_ptr(),
+                                 counts.data_ptr(), _stream(stream)), "cox_router_topk")
+    return idx, w, counts
+
+
+def permute_workspace_bytes(T: int, E: int) -> int:
+    return int(_lib.load().cox_permute_workspace_bytes(T, E))
+
+
+def rows_capacity(T: int, k: int, E: int, tile_m: int = 1) -> int:
+    return max(1, T * k + E * (tile_m - 1))
+
+
+def permute(idx: torch.Tensor, x: torch.Tensor, E: int, tile_m: int = 1, out=None, workspace=None, stream=None):
+    """K2: -> (offsets [E+1] int32, dst [T,k] int32, x_perm [rows_cap, d] bf16)."""
+    _need(idx, "idx", torch.int32, 2)
+    _need(x, "x", _BF16, 2)
+    T, k = idx.shape
+    d = x.shape[1]
+    if x.shape[0] != T:
+        raise ValueError("idx and x disagree on T")
+    cap = rows_capacity(T, k, E, tile_m)
+    if out is None:
+        offsets = torch.empty((E + 1,), dtype=torch.int32, device=x.device)
+        dst = torch.empty((T, k), dtype=torch.int32, device=x.device)
+        x_perm = torch.empty((cap, d), dtype=_BF16, device=x.device)
+    else:
+        offsets, dst, x_perm = out
+    if workspace is None:
+        workspace = torch.empty((permute_workspace_bytes(T, E),), dtype=torch.uint8, device=x.device)
+    L = _lib.lib()
+    _lib.check(L.cox_permute(idx.data_ptr(), T, k, E, tile_m, x.data_ptr(), d, offsets.data_ptr(), dst.data_ptr(),
+                             x_perm.data_ptr(), x_perm.shape[0], workspace.data_ptr(), _stream(stream)),
+               "cox_permute")
+    return offsets, dst, x_perm
+
+
+def grouped_swiglu(x_perm: torch.Tensor, offsets: torch.Tensor, group_experts: Sequence[int],
+                   w13: Sequence[torch.Tensor], ff: int, h: torch.Tensor | None = None, stream=None):
+    """K3: h[r] = silu(x_perm[r] W1_e^T) * (x_perm[r] W3_e^T) for the listed groups."""
+    _need(x_perm, "x_perm", _BF16, 2)
+    _need(offsets, "offsets", torch.int32, 1)
+    rows, d = x_perm.shape
+    for i, w in enumerate(w13):
+        _need(w, f"w13[{i}]", _BF16, 2)
+        if tuple(w.shape) != (2 * ff, d):
+            raise ValueError(f"w13[{i}] must be [2*ff, d] = [{2 * ff}, {d}]")
+    if len(w13) != len(group_experts):
+        raise ValueError("one weight per group")
+    if h is None:
+        h = torch.empty((rows, ff), dtype=_BF16, device=x_perm.device)
+    L = _lib.lib()
+    _lib.check(L.cox_grouped_swiglu(x_perm.data_ptr(), rows, offsets.data_ptr(), len(group_experts),
+                                    _ids(group_experts), _ptrs(w13), d, ff, h.data_ptr(), _stream(stream)),
+               "cox_grouped_swiglu")
+    return h
+
+
+def grouped_down(h: torch.Tensor, offsets: torch.Tensor, group_experts: Sequence[int], w2: Sequence[torch.Tensor],
+                 d: int, y: torch.Tensor | None = None, stream=None):
+    """K4: y[r] = h[r] W2_e^T for the listed groups."""
+    _need(h, "h", _BF16, 2)
+    _need(offsets, "offsets", torch.int32, 1)
+    rows, ff = h.shape
+    for i, w in enumerate(w2):
+        _need(w, f"w2[{i}]", _BF16, 2)
+        if tuple(w.shape) != (d, ff):
+            raise ValueError(f"w2[{i}] must be [d, ff] = [{d}, {ff}]")
+    if len(w2) != len(group_experts):
+        raise ValueError("one weight per group")
+    if y is None:
+        y = torch.empty((rows, d), dtype=_BF16, device=h.device)
+    L = _lib.lib()
+    _lib.check(L.cox_grouped_down(h.data_ptr(), rows, offsets.data_ptr(), len(group_experts), _ids(group_experts),
+                                  _ptrs(w2), ff, d, y.data_ptr(), _stream(stream)), "cox_grouped_down")
+    return y
+
+
+def combine(y_perm: torch.Tensor, dst: torch.Tensor, w: torch.Tensor, shared: torch.Tensor | None = None,
+            out: torch.Tensor | None = None, out_dtype=_BF16, stream=None):
+    """K5: out[t] = sum_j w[t,j] y_perm[dst[t,j]] (+ shared[t])."""
+    _need(y_perm, "y_perm", _BF16, 2)
+    _need(dst, "dst", torch.int32, 2)
+    _need(w, "w", torch.float32, 2)
+    T, k = dst.shape
+    d = y_perm.shape[1]
+    if out is None:
+        out = torch.empty((T, d), dtype=out_dtype, device=y_perm.device)
+    odt = _lib.DTYPE_BF16 if out.dtype == _BF16 else _lib.DTYPE_F32
+    if shared is not None:
+        _need(shared, "shared", out.dtype, 2)
+    L = _lib.lib()
+    _lib.check(L.cox_combine(y_perm.data_ptr(), dst.data_ptr(), w.data_ptr(), T, k, d,
+                             shared.data_ptr() if shared is not None else None, out.data_ptr(), odt, _stream(stream)),
+               "cox_combine")
+    return out
+
+
+def interleave_w13(w1: torch.Tensor, w3: torch.Tensor, out: torch.Tensor | None = None, stream=None):
+    """[ff,d] x 2 -> K3 layout [2ff, d] (128-row gate/up blocks)."""
+    _need(w1, "w1", _BF16, 2)
+    _need(w3, "w3", _BF16, 2)
+    ff, d = w1.shape
+    if out is None:
+        out = torch.empty((2 * ff, d), dtype=_BF16, device=w1.device)
+    L = _lib.lib()
+    _lib.check(L.cox_interleave_w13(w1.data_ptr(), w3.data_ptr(), ff, d, out.data_ptr(), _stream(stream)),
+               "cox_interleave_w13")
+    return out

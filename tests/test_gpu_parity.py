@@ -1,0 +1,167 @@
+"""GPU parity: every kernel through the C ABI against the CPU oracle / fp32 torch.
+
+Bars: routing indices, weights-order, counts, offsets and dst BIT-EXACT vs the
+oracle; x_perm rows bit-exact copies; grouped GEMMs within bf16 rounding of a
+torch fp32 reference (max |err| <= 2e-2 * max|ref|, rel-L2 <= 1e-2); whole
+layer rel-L2 <= 1e-2 vs the fp32 oracle.
+"""
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+from oracle import oracle as O  # noqa: E402  (test infrastructure)
+from paper_2605_17889_b200 import ops, _lib  # noqa: E402
+from paper_2605_17889_b200.layer import MoELayer  # noqa: E402
+from paper_2605_17889_b200.synthetic import make_layer_weights, make_tokens, split_w13  # noqa: E402
+
+DEV = "cuda"
+
+
+def rel_l2(a, b):
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30))
+
+
+@pytest.mark.parametrize("T,d,E,k,mode,dtype", [
+    (1000, 256, 8, 2, 0, torch.bfloat16),
+    (777, 1024, 8, 2, 0, torch.float32),
+    (513, 2048, 64, 6, 1, torch.bfloat16),
+    (37, 64, 4, 2, 0, torch.float32),
+    (1, 264, 5, 3, 1, torch.bfloat16),
+])
+def test_router_bitexact(T, d, E, k, mode, dtype):
+    x = make_tokens(T, d, seed=3, device=DEV, dtype=dtype)
+    g = torch.Generator(device=DEV).manual_seed(5)
+    wg = ((torch.rand((E, d), generator=g, device=DEV) * 2 - 1) / d ** 0.5).to(torch.bfloat16).float()
+    idx, w, counts = ops.router_topk(x, wg, k, mode)
+    torch.cuda.synchronize()
+    oi, ow, oc = O.router_topk(x.float().cpu().numpy(), wg.cpu().numpy(), k, mode)
+    assert np.array_equal(idx.cpu().numpy(), oi)
+    assert np.array_equal(counts.cpu().numpy(), oc)
+    np.testing.assert_allclose(w.cpu().numpy(), ow, rtol=2e-6, atol=1e-7)
+
+
+def test_router_ties_go_to_lower_index():
+    T, d, E, k = 64, 256, 8, 2
+    x = make_tokens(T, d, seed=4, device=DEV)
+    wg = torch.zeros((E, d), device=DEV)  # all logits equal -> experts 0, 1
+    idx, w, counts = ops.router_topk(x, wg, k, 0)
+    assert (idx.cpu().numpy() == np.array([0, 1])).all()
+    assert torch.allclose(w, torch.full_like(w, 0.5))
+    wg[3] = wg[5] = 1.0 / d  # duplicate rows: identical logits, lower index wins
+    idx, _, _ = ops.router_topk(x.abs(), wg, k, 0)
+    assert (idx.cpu().numpy() == np.array([3, 5])).all()
+
+
+@pytest.mark.parametrize("T,d,E,k,tile_m,skew", [
+    (1000, 256, 8, 2, 1, False),
+    (257, 512, 8, 2, 128, True),
+    (3000, 256, 64, 6, 1, True),
+    (5, 256, 16, 2, 1, False),
+])
+def test_permute_bitexact(T, d, E, k, tile_m, skew):
+    rng = np.random.default_rng(T)
+    if skew:  # ragged + empty experts
+        p = rng.zipf(1.5, size=E).astype(float)
+        p[E // 2:] = 0
+        p /= p.sum()
+    else:
+        p = np.full(E, 1.0 / E)
+    idx = np.stack([rng.choice(E, size=k, replace=False, p=None if not skew else None) for _ in range(T)])
+    if skew:
+        nz = max(k, int((p > 0).sum()))
+        idx = np.stack([rng.choice(nz, size=k, replace=False) for _ in range(T)])
+    idx = idx.astype(np.int32)
+    x = make_tokens(T, d, seed=7, device=DEV)
+    idx_t = torch.from_numpy(idx).to(DEV)
+    offsets, dst, x_perm = ops.permute(idx_t, x, E, tile_m)
+    torch.cuda.synchronize()
+    oo, od = O.permute(idx, E, tile_m)
+    assert np.array_equal(offsets.cpu().numpy(), oo)
+    assert np.array_equal(dst.cpu().numpy(), od)
+    xp = x_perm.view(torch.int16).cpu().numpy()
+    xs = x.view(torch.int16).cpu().numpy()
+    for t in range(T):
+        for j in range(k):
+            assert np.array_equal(xp[od[t, j]], xs[t])
+    if tile_m > 1:  # padding rows zero-filled
+        used = np.zeros(xp.shape[0], bool)
+        used[od.ravel()] = True
+        assert (xp[: oo[-1]][~used[: oo[-1]]] == 0).all()
+
+
+def _gemm_case(E, d, ff, counts, seed=0):
+    offs = np.concatenate([[0], np.cumsum(counts)]).astype(np.int32)
+    rows = int(offs[-1])
+    wts = make_layer_weights(E, d, ff, seed=seed, device=DEV)
+    x = make_tokens(max(rows, 1), d, seed=seed + 1, device=DEV)
+    return wts, x, torch.from_numpy(offs).to(DEV), offs
+
+
+@pytest.mark.parametrize("E,d,ff,counts", [
+    (2, 256, 256, [300, 17]),
+    (4, 512, 384, [0, 256, 1, 700]),
+    (3, 1024, 512, [1000, 513, 255]),
+])
+def test_grouped_gemms_vs_torch_fp32(E, d, ff, counts):
+    wts, x, offs_t, offs = _gemm_case(E, d, ff, counts)
+    h = ops.grouped_swiglu(x, offs_t, list(range(E)), [wts.w13[e] for e in range(E)], ff)
+    y = ops.grouped_down(h, offs_t, list(range(E)), [wts.w2[e] for e in range(E)], d)
+    torch.cuda.synchronize()
+    w1, w3 = split_w13(wts.w13)
+    for e in range(E):
+        r0, r1 = int(offs[e]), int(offs[e + 1])
+        if r1 == r0:
+            continue
+        xe = x[r0:r1].float()
+        href = torch.nn.functional.silu(xe @ w1[e].float().T) * (xe @ w3[e].float().T)
+        he = h[r0:r1].float()
+        assert rel_l2(he.cpu(), href.cpu()) < 1e-2, f"h expert {e}"
+        yref = he @ wts.w2[e].float().T
+        assert rel_l2(y[r0:r1].float().cpu(), yref.cpu()) < 1e-2, f"y expert {e}"
+
+
+def test_grouped_subset_groups_only_touch_their_rows():
+    E, d, ff = 4, 256, 256
+    wts, x, offs_t, offs = _gemm_case(E, d, ff, [100, 200, 300, 50])
+    h = torch.full((x.shape[0], ff), 7.0, dtype=torch.bfloat16, device=DEV)
+    ops.grouped_swiglu(x, offs_t, [1, 3], [wts.w13[1], wts.w13[3]], ff, h=h)
+    torch.cuda.synchronize()
+    assert (h[0:100] == 7).all() and (h[300:600] == 7).all()
+    assert not (h[100:300] == 7).all()
+
+
+@pytest.mark.parametrize("T,d,ff,E,k,mode,shared_ff", [
+    (4096, 1024, 3584, 8, 2, "mixtral", 0),   # C1 shape (bf16 inputs on the GPU)
+    (999, 512, 256, 8, 2, "mixtral", 0),
+    (700, 512, 256, 16, 6, "deepseek", 512),  # fine-grained + shared experts
+])
+def test_layer_vs_oracle(T, d, ff, E, k, mode, shared_ff):
+    wts = make_layer_weights(E, d, ff, seed=0, device=DEV, shared_ff=shared_ff, keep_split=True)
+    x = make_tokens(T, d, seed=1, device=DEV)
+    layer = MoELayer(wts, k, mode)
+    out = layer(x)
+    torch.cuda.synchronize()
+    b = layer.buffers(T, DEV)
+    f = lambda t: t.float().cpu().numpy()  # noqa: E731
+    shared = (f(wts.shared_w1), f(wts.shared_w3), f(wts.shared_w2)) if shared_ff else None
+    ref = O.moe_layer(f(x), f(wts.wg), f(wts.w1), f(wts.w3), f(wts.w2), k, 0 if mode == "mixtral" else 1,
+                      shared=shared)
+    assert np.array_equal(b.idx.cpu().numpy(), ref["idx"])
+    assert np.array_equal(b.dst.cpu().numpy(), ref["dst"])
+    assert np.array_equal(b.offsets.cpu().numpy(), ref["offsets"])
+    err = rel_l2(f(out), ref["out"])
+    assert err <= 1e-2, err
+
+
+def test_invalid_shapes_raise_valueerror():
+    x = make_tokens(8, 100, device=DEV)  # d % 8 != 0
+    wg = torch.zeros((4, 100), device=DEV)
+    with pytest.raises(ValueError):
+        ops.router_topk(x, wg, 2)
+    x = make_tokens(8, 256, device=DEV)
+    with pytest.raises(ValueError):
+        ops.router_topk(x, torch.zeros((4, 256), device=DEV), 5)
