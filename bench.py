@@ -1,0 +1,344 @@
+#!/usr/bin/env python
+"""Benchmark of the coalesced MoE expert stage (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config C2|C1|C3L|C4]
+
+One "step" = one full expert stage (router -> permute -> grouped SwiGLU ->
+grouped down -> combine) over one batch of synthetic tokens.  Default workload
+= BASELINE.json configs[1] (C2): Mixtral-8x7B-shaped layer, E=8, top-2,
+d=4096, ff=14336, batch 64x4096 = 262,144 tokens per GPU, bf16.
+
+N > 1 (torchrun, one process per GPU): expert parallelism — each rank holds its
+own 64x4096 batch (weak scaling) and E/N experts; tokens travel by NCCL
+all-to-all (ep.py).  Time = max over ranks of CUDA-event time.
+
+Prints ONE JSON line on rank 0.  `value` is device-resident throughput; `e2e`
+is the same metric through the public API (MoELayer / EP layer) with the
+tokens copied from pinned host memory and the output copied back inside the
+timed region.  `cpu_baseline` times the fp32 CPU oracle (oracle/, the
+"reference CPU path": moeplan ships no executable expert stage) on a bounded
+token slice on this host.
+
+--impl reference: times that CPU oracle alone (rank 0; other ranks exit 0).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+CONFIGS = {
+    # name: (T per GPU, d, ff, E, k, mode, shared_ff, description)
+    "C2": (64 * 4096, 4096, 14336, 8, 2, "mixtral", 0,
+           "C2 Mixtral-8x7B MoE layer (E=8, top-2, d=4096, ff=14336), prefill batch 64x4096 per GPU"),
+    "C1": (16 * 256, 1024, 3584, 8, 2, "mixtral", 0,
+           "C1 tiny Mixtral-style MoE layer (E=8, top-2, d=1024, ff=3584), batch 16x256 (bf16 on GPU)"),
+    "C3L": (64 * 4096, 6144, 16384, 8, 2, "mixtral", 0,
+            "C3/C5 Mixtral-8x22B MoE layer (E=8, top-2, d=6144, ff=16384), batch 64x4096 per GPU"),
+    "C4": (64 * 4096, 2048, 1408, 64, 6, "deepseek", 2816,
+           "C4 DeepSeek-V2-Lite MoE layer (64 routed top-6 + 2 shared, d=2048, ff=1408), batch 64x4096"),
+}
+
+
+def metric_name(config: str) -> str:
+    if config == "C2":
+        return "MoE layer tokens/s, Mixtral-8x7B layer, b64x4096"
+    return f"MoE layer tokens/s, {config}"
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        j = json.loads(p.read_text())
+        return dict(hbm=j["hbm_gbs"], bf16=j["bf16_tflops"], bf16_sus=j.get("bf16_tflops_sustained", j["bf16_tflops"]),
+                    src="measured")
+    return dict(hbm=6650.0, bf16=1590.0, bf16_sus=1400.0, src="fallback (B200_PROFILING.md)")
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap,power.draw")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        self.lines = []
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+                out, _ = self.proc.communicate()
+            self.lines = [l for l in out.splitlines() if l.strip()]
+
+    def summary(self):
+        sm, mx, reasons, pw = [], 0.0, set(), []
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for l in getattr(self, "lines", []):
+            f = [x.strip() for x in l.split(",")]
+            try:
+                sm.append(float(f[0]))
+                mx = max(mx, float(f[1]))
+                for n, v in zip(names, f[2:6]):
+                    if v.lower().startswith("active"):
+                        reasons.add(n)
+                pw.append(float(f[6]))
+            except (ValueError, IndexError):
+                continue
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "power_w_max": max(pw) if pw else None, "samples": len(sm)}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def cpu_baseline(wts_host, x_host, k, mode_id, shared_host, n_tokens):
+    """fp32 CPU oracle over the first n_tokens tokens (routed exactly as in the full batch)."""
+    from oracle import oracle as O
+    O.lib()
+    threads = len(os.sched_getaffinity(0))
+    O.set_num_threads(threads)
+    xs = x_host[:n_tokens]
+    t0 = time.perf_counter()
+    O.moe_layer(xs, wts_host["wg"], wts_host["w1"], wts_host["w3"], wts_host["w2"], k, mode_id, shared=shared_host)
+    dt = time.perf_counter() - t0
+    return n_tokens / dt, threads, dt
+
+
+def host_weights(wts):
+    import numpy as np  # noqa: F401
+    from paper_2605_17889_b200.synthetic import split_w13
+    w1, w3 = split_w13(wts.w13)
+    f = lambda t: t.float().cpu().numpy()  # noqa: E731
+    hw = {"wg": f(wts.wg), "w1": f(w1), "w3": f(w3), "w2": f(wts.w2)}
+    shared = None
+    if wts.shared_w13 is not None:
+        s1, s3 = split_w13(wts.shared_w13)
+        shared = (f(s1), f(s3), f(wts.shared_w2))
+    return hw, shared
+
+
+def cpu_model_name():
+    try:
+        for l in open("/proc/cpuinfo"):
+            if l.startswith("model name"):
+                return l.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def run_reference(args, cfg):
+    """--impl reference: the fp32 CPU oracle (the reference ships no executable expert stage)."""
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    import numpy as np
+    import torch
+    from oracle import oracle as O
+    from paper_2605_17889_b200.synthetic import make_layer_weights, make_tokens
+    T, d, ff, E, k, mode, shared_ff, desc = cfg
+    sample = min(T, args.ref_tokens)
+    wts = make_layer_weights(E, d, ff, seed=0, device="cpu", shared_ff=shared_ff)
+    x = make_tokens(sample, d, seed=1, device="cpu").float().numpy()
+    hw, shared = host_weights(wts)
+    del wts
+    threads = len(os.sched_getaffinity(0))
+    O.set_num_threads(threads)
+    mode_id = 0 if mode == "mixtral" else 1
+    for _ in range(args.warmup):
+        O.moe_layer(x[: max(8, sample // 8)], hw["wg"], hw["w1"], hw["w3"], hw["w2"], k, mode_id, shared=shared)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        O.moe_layer(x, hw["wg"], hw["w1"], hw["w3"], hw["w2"], k, mode_id, shared=shared)
+    dt = time.perf_counter() - t0
+    value = sample * args.steps / dt
+    line = {
+        "impl": "reference", "metric": metric_name(args.config), "value": value, "unit": "tokens/s",
+        "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": desc, "tokens_per_step": sample, "d": d, "ff": ff, "E": E, "k": k},
+        "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": threads, "kind": "port",
+                         "sample": f"first {sample} of {T} tokens per step, full-size weights, fp32 oracle "
+                                   f"(oracle/, OpenMP x{threads}) on {cpu_model_name()}"},
+        "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C2", choices=sorted(CONFIGS))
+    ap.add_argument("--cpu-tokens", type=int, default=2048, help="token slice for the CPU-oracle baseline")
+    ap.add_argument("--ref-tokens", type=int, default=512, help="tokens per step for --impl reference")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        return run_reference(args, cfg)
+
+    import torch
+    import torch.distributed as dist
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    T, d, ff, E, k, mode, shared_ff, desc = cfg
+
+    from paper_2605_17889_b200.synthetic import make_layer_weights, make_tokens
+    from paper_2605_17889_b200.layer import MoELayer
+
+    wts = make_layer_weights(E, d, ff, seed=0, device=dev, shared_ff=shared_ff)
+    x = make_tokens(T, d, seed=1 + rank, device=dev)
+    if ws > 1:
+        from paper_2605_17889_b200.ep import EPMoELayer
+        layer = EPMoELayer(wts, k, mode, dist.group.WORLD)
+    else:
+        layer = MoELayer(wts, k, mode)
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        if ws > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # --- device-resident throughput ------------------------------------------
+    for _ in range(args.warmup):
+        layer(x)
+    barrier()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    k3 = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    k4 = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    layer.profile_events = None
+    start = torch.cuda.Event(enable_timing=True)
+    stop = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        barrier()
+        start.record(stream)
+        for i in range(args.steps):
+            layer.profile_events = {"k3": k3[i], "k4": k4[i]}
+            ev[i][0].record(stream)
+            layer(x)
+            ev[i][1].record(stream)
+        stop.record(stream)
+        barrier()
+    layer.profile_events = None
+    ms_total = start.elapsed_time(stop)
+    t_local = torch.tensor([ms_total], dtype=torch.float64, device=dev)
+    if ws > 1:
+        dist.all_reduce(t_local, op=dist.ReduceOp.MAX)
+    ms_total = float(t_local.item())
+    ms_step = ms_total / args.steps
+    tokens_all = T * ws * args.steps
+    value = tokens_all / (ms_total / 1e3)
+    k3_ms = sum(a.elapsed_time(b) for a, b in k3) / args.steps
+    k4_ms = sum(a.elapsed_time(b) for a, b in k4) / args.steps
+
+    # --- end-to-end through the public API with host buffers ------------------
+    e2e = None
+    if not args.no_e2e:
+        x_host = x.cpu().pin_memory()
+        out_host = torch.empty((T, d), dtype=torch.bfloat16).pin_memory()
+        xd = torch.empty_like(x)
+        for _ in range(2):
+            xd.copy_(x_host, non_blocking=True)
+            out_host.copy_(layer(xd), non_blocking=True)
+        barrier()
+        s0 = torch.cuda.Event(enable_timing=True)
+        s1 = torch.cuda.Event(enable_timing=True)
+        s0.record(stream)
+        for _ in range(args.steps):
+            xd.copy_(x_host, non_blocking=True)
+            out_host.copy_(layer(xd), non_blocking=True)
+        s1.record(stream)
+        barrier()
+        e_ms = torch.tensor([s0.elapsed_time(s1)], dtype=torch.float64, device=dev)
+        if ws > 1:
+            dist.all_reduce(e_ms, op=dist.ReduceOp.MAX)
+        e2e = {"value": tokens_all / (float(e_ms.item()) / 1e3), "unit": "tokens/s",
+               "h2d_bytes_per_step": x.numel() * 2 * ws, "d2h_bytes_per_step": T * d * 2 * ws}
+
+    # --- per-stage breakdown (one extra step, not part of `value`) ------------
+    stages = layer.stage_times(x) if hasattr(layer, "stage_times") else None
+
+    if rank == 0:
+        pk = peaks()
+        flops_k3 = 4.0 * T * k * d * ff
+        flops_k4 = 2.0 * T * k * d * ff
+        flops_layer = 6.0 * T * k * d * ff + 2.0 * T * d * E + (6.0 * T * d * shared_ff if shared_ff else 0.0)
+        achieved = flops_k3 / (k3_ms / 1e3) / 1e12
+        cpu = None
+        if not args.no_cpu_baseline and ws == 1:
+            hw, shared = host_weights(wts)
+            x_host_f = x[: args.cpu_tokens].float().cpu().numpy()
+            cps, threads, dt = cpu_baseline(hw, x_host_f, k, 0 if mode == "mixtral" else 1, shared, args.cpu_tokens)
+            cpu = {"value": cps, "unit": "tokens/s", "cores": threads, "kind": "port",
+                   "sample": f"first {args.cpu_tokens} of {T} tokens (routed as in the full batch), full-size "
+                             f"weights, fp32 oracle (oracle/, OpenMP x{threads}) on {cpu_model_name()}: {dt:.1f} s"}
+        line = {
+            "metric": metric_name(args.config),
+            "value": value, "unit": "tokens/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "bf16", "data": "synthetic (seeded N(0,1) tokens, nn.Linear-style U(+-1/sqrt(fan_in)) weights)",
+            "config": {"workload": desc, "tokens_per_gpu": T, "global_batch_tokens": T * ws, "d": d, "ff": ff,
+                       "E": E, "k": k, "routing": mode, "parallelism": f"ep{ws}" if ws > 1 else "single",
+                       "l2": "inputs > L2 (x 2.1 GB, x_perm 4.3 GB, h 15 GB vs 126 MB L2); no flush"},
+            "layer_tflops": flops_layer / (ms_step / 1e3) / 1e12,
+            "frac_layer_of_bf16_sustained": flops_layer / (ms_step / 1e3) / 1e12 / pk["bf16_sus"],
+            "frac_layer_of_bf16_burst": flops_layer / (ms_step / 1e3) / 1e12 / pk["bf16"],
+            "roofline": {"kernel": "grouped_gemm_kernel<EPI_SWIGLU> (K3)", "bound": "tensor",
+                         "achieved": achieved, "peak": pk["bf16_sus"], "unit": "TFLOP/s",
+                         "frac": achieved / pk["bf16_sus"], "traffic": None,
+                         "peak_kind": f"bf16_tflops_sustained ({pk['src']}); burst {pk['bf16']}",
+                         "k3_ms": k3_ms, "k4_ms": k4_ms,
+                         "k4_tflops": flops_k4 / (k4_ms / 1e3) / 1e12},
+            "stages_ms": stages,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": layer.launches_per_step * args.steps,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -50,12 +50,29 @@ COX_DEV void mbar_wait(uint32_t bar, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred P1;\n"
       "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, 10000000;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
       "@P1 bra DONE_%=;\n\t"
       "bra WAIT_%=;\n"
       "DONE_%=:\n\t}" ::"r"(bar),
       "r"(parity)
       : "memory");
+}
+
+// Cluster-scope acquire: pairs with a remote mbarrier.arrive.release.cluster.
+COX_DEV void mbar_wait_cluster(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "WAITC_%=:\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@P1 bra DONEC_%=;\n\t"
+      "bra WAITC_%=;\n"
+      "DONEC_%=:\n\t}" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+
+COX_DEV void st_shared_cluster_u32(uint32_t cluster_addr, uint32_t v) {
+  asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(cluster_addr), "r"(v) : "memory");
 }
 
 COX_DEV void mbar_arrive_expect_tx(uint32_t bar, uint32_t bytes) {

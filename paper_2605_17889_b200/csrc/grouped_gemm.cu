@@ -20,14 +20,16 @@
 //     both CTAs (multicast commit).
 //   * Warp roles: w0 TMA producer, w1 MMA issuer (leader CTA, one thread),
 //     w2 TMEM allocator, w4..w7 epilogue (TMEM -> registers -> global).
-//   * Persistent static schedule: 74 pairs on 148 SMs walk the tile list;
-//     tiles are rasterised in bands of `band` n-tiles so that concurrently
-//     running pairs share A rows and B bands in L2.
+//   * Persistent kernel, 74 pairs on 148 SMs, dynamic tile scheduler (warp 3 of
+//     the leader: global atomic counter -> tile-id ring in both CTAs); tiles
+//     are rasterised in bands of `band` n-tiles so that concurrently running
+//     pairs share A rows and B bands in L2.
 // Expert segments need no padding: rows of a partial m-tile that belong to the
 // next segment are computed but never stored.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <cstdlib>
 #include <mutex>
 #include <unordered_map>
 
@@ -44,6 +46,7 @@ constexpr int GM_THREADS = 256;
 constexpr uint32_t GM_A_BYTES = GM_BM * GM_BK * 2;         // 16 KB
 constexpr uint32_t GM_B_BYTES = (GM_BN / 2) * GM_BK * 2;   // 16 KB
 constexpr uint32_t GM_TMEM_COLS = 512;
+constexpr int GM_SCHED_DEPTH = 4;  // tile-id ring between the scheduler and the roles
 constexpr int EPI_SWIGLU = 0;
 constexpr int EPI_STORE = 1;
 
@@ -51,6 +54,7 @@ struct alignas(64) GemmParams {
   CUtensorMap a_map;
   CUtensorMap b_map[GM_MAXG];
   const int32_t* offsets;
+  int* tile_counter;  // zeroed before launch; dynamic tile scheduler
   void* out;
   long long ldo;
   int group_expert[GM_MAXG];
@@ -60,7 +64,7 @@ struct alignas(64) GemmParams {
   int band;
 };
 
-constexpr size_t GM_SMEM_BYTES = 1024 + GM_STAGES * (GM_A_BYTES + GM_B_BYTES) + 256 + 4 * (3 * GM_MAXG + 4);
+constexpr size_t GM_SMEM_BYTES = 1024 + GM_STAGES * (GM_A_BYTES + GM_B_BYTES) + 512 + 4 * (3 * GM_MAXG + 4);
 
 struct TileCoord {
   int g, m, n;
@@ -95,7 +99,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GM_THREADS, 1)
   uint64_t* empty = bars + GM_STAGES;
   uint64_t* tfull = bars + 2 * GM_STAGES;
   uint64_t* tempty = bars + 2 * GM_STAGES + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * GM_STAGES + 4);
+  uint64_t* sfull = bars + 2 * GM_STAGES + 4;                   // [DEPTH] tile id published
+  uint64_t* sempty = sfull + GM_SCHED_DEPTH;                     // [DEPTH] (leader) slot consumed
+  int* s_tile = reinterpret_cast<int*>(sempty + GM_SCHED_DEPTH);  // [DEPTH]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_tile + GM_SCHED_DEPTH);
   int* s_prefix = reinterpret_cast<int*>(tmem_slot + 4);
   int* s_rows = s_prefix + GM_MAXG + 1;
   int* s_row0 = s_rows + GM_MAXG;
@@ -112,6 +119,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GM_THREADS, 1)
     for (int a = 0; a < 2; ++a) {
       mbar_init(smem_u32(&tfull[a]), 1);
       mbar_init(smem_u32(&tempty[a]), 8);  // 4 epilogue warps x 2 CTAs
+    }
+    for (int i = 0; i < GM_SCHED_DEPTH; ++i) {
+      mbar_init(smem_u32(&sfull[i]), 1);
+      mbar_init(smem_u32(&sempty[i]), 11);  // producers x2 + MMA + epilogue warps x8
     }
     fence_mbar_init();
     int acc = 0;
@@ -142,11 +153,45 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GM_THREADS, 1)
   const int ncl = gridDim.x >> 1;
   const int nk = p.K / GM_BK;
 
-  if (warp == 0) {
+  // Dynamic tile scheduler.  The leader's warp 3 publishes tile ids into a
+  // ring replicated in both CTAs (first wave static, then a global atomic
+  // counter) so that concurrently running pairs always work on neighbouring
+  // tiles of the rasterised order and keep sharing A/B in L2 — a static
+  // round-robin lets pairs drift apart by whole waves.  Every role consumes
+  // the same sequence; a value >= total terminates.
+  auto fetch_tile = [&](int& si) -> int {
+    const int slot = si % GM_SCHED_DEPTH;
+    mbar_wait_cluster(smem_u32(&sfull[slot]), (si / GM_SCHED_DEPTH) & 1);
+    const int t = reinterpret_cast<volatile int*>(s_tile)[slot];
+    mbar_arrive_cluster(mapa(smem_u32(&sempty[slot]), 0));
+    ++si;
+    return t;
+  };
+
+  if (warp == 3) {
+    // ------------------------------------------------------------ tile scheduler (leader)
+    if (rank == 0 && lane == 0) {
+      for (int i = 0;; ++i) {
+        const int slot = i % GM_SCHED_DEPTH;
+        mbar_wait_cluster(smem_u32(&sempty[slot]), ((i / GM_SCHED_DEPTH) & 1) ^ 1);
+        int t = (i == 0) ? cid : ncl + atomicAdd(p.tile_counter, 1);
+        if (t > total) t = total;
+        s_tile[slot] = t;
+        st_shared_cluster_u32(mapa(smem_u32(&s_tile[slot]), 1), (uint32_t)t);
+        mbar_arrive_cluster(mapa(smem_u32(&sfull[slot]), 0));
+        mbar_arrive_cluster(mapa(smem_u32(&sfull[slot]), 1));
+        if (t >= total) break;
+      }
+    }
+    __syncwarp();
+  } else if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
     if (lane == 0) {
       uint32_t stage = 0, phase = 0;
-      for (int t = cid; t < total; t += ncl) {
+      int si = 0;
+      for (;;) {
+        const int t = fetch_tile(si);
+        if (t >= total) break;
         const TileCoord c = decode_tile(t, s_prefix, s_rows, p.band);
         const int a_row = s_row0[c.g] + c.m * 2 * GM_BM + (int)rank * GM_BM;
         const int b_row = c.n * GM_BN + (int)rank * (GM_BN / 2);
@@ -168,8 +213,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GM_THREADS, 1)
     if (rank == 0 && lane == 0) {
       const uint32_t idesc = idesc_bf16_f32(2 * GM_BM, GM_BN);
       uint32_t stage = 0, phase = 0;
-      int it = 0;
-      for (int t = cid; t < total; t += ncl, ++it) {
+      int si = 0;
+      for (int it = 0;; ++it) {
+        const int t = fetch_tile(si);
+        if (t >= total) break;
         const int acc = it & 1;
         const uint32_t acc_phase = (it >> 1) & 1;
         mbar_wait(smem_u32(&tempty[acc]), acc_phase ^ 1);
@@ -199,8 +246,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GM_THREADS, 1)
     const uint32_t tempty_leader0 = mapa(smem_u32(&tempty[0]), 0);
     const uint32_t tempty_leader1 = mapa(smem_u32(&tempty[1]), 0);
     __nv_bfloat16* out = static_cast<__nv_bfloat16*>(p.out);
-    int it = 0;
-    for (int t = cid; t < total; t += ncl, ++it) {
+    int si = 0;
+    for (int it = 0;; ++it) {
+      int t;
+      {
+        const int slot = si % GM_SCHED_DEPTH;
+        mbar_wait_cluster(smem_u32(&sfull[slot]), (si / GM_SCHED_DEPTH) & 1);
+        t = reinterpret_cast<volatile int*>(s_tile)[slot];
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(mapa(smem_u32(&sempty[slot]), 0));
+        ++si;
+      }
+      if (t >= total) break;
       const TileCoord c = decode_tile(t, s_prefix, s_rows, p.band);
       const int acc = it & 1;
       const uint32_t acc_phase = (it >> 1) & 1;
@@ -325,6 +382,11 @@ static int get_map(CUtensorMap* out, const void* ptr, unsigned long long rows, u
 }
 
 static int pick_band(int n_tiles) {
+  static int env_band = [] {
+    const char* e = getenv("COX_GEMM_BAND");
+    return e ? atoi(e) : 0;
+  }();
+  if (env_band > 0 && n_tiles % env_band == 0) return env_band;
   for (int b : {8, 4, 2, 1})
     if (n_tiles % b == 0) return b;
   return 1;
@@ -348,6 +410,15 @@ int launch_grouped_gemm(int epi, const void* A, long long rows_cap, int K, const
     if (rc) return rc;
     p.group_expert[g] = group_expert[g];
   }
+  static int* counters = nullptr;
+  static unsigned seq = 0;
+  if (!counters) {
+    if (cudaMalloc(&counters, 1024 * sizeof(int)) != cudaSuccess) return -2;
+    if (cudaMemset(counters, 0, 1024 * sizeof(int)) != cudaSuccess) return -2;
+  }
+  int* counter = counters + (seq++ % 1024);
+  if (cudaMemsetAsync(counter, 0, sizeof(int), s) != cudaSuccess) return -2;
+  p.tile_counter = counter;
   p.offsets = offsets;
   p.out = out;
   p.ldo = ldo;

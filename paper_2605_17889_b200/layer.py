@@ -83,6 +83,12 @@ class MoELayer:
         if self.shared_ff and out_dtype != torch.bfloat16:
             raise ValueError("shared experts require a bf16 output")
         self._bufs: StageBuffers | None = None
+        self.profile_events = None  # optional {"k3": (ev0, ev1), "k4": (ev0, ev1)} recorded around K3/K4
+
+    @property
+    def launches_per_step(self) -> int:
+        # router 1 + permute 3 (+1 pad) + K3 + K4 + combine (+ shared K3/K4)
+        return 1 + 3 + (1 if self.tile_m > 1 else 0) + 2 + 1 + (2 if self.shared_ff else 0)
 
     def buffers(self, T: int, device) -> StageBuffers:
         if self._bufs is None or self._bufs.T != T:
@@ -98,8 +104,16 @@ class MoELayer:
 
     def experts(self, b: StageBuffers, groups=None, w13=None, w2=None):
         groups = self.groups if groups is None else groups
+        pe = self.profile_events
+        if pe:
+            pe["k3"][0].record()
         ops.grouped_swiglu(b.x_perm, b.offsets, groups, self.w13_list if w13 is None else w13, self.ff, h=b.h)
+        if pe:
+            pe["k3"][1].record()
+            pe["k4"][0].record()
         ops.grouped_down(b.h, b.offsets, groups, self.w2_list if w2 is None else w2, self.d, y=b.y)
+        if pe:
+            pe["k4"][1].record()
 
     def shared_expert(self, x: torch.Tensor, b: StageBuffers):
         if not self.shared_ff:
@@ -121,3 +135,26 @@ class MoELayer:
         return self.finish(b, sh)
 
     __call__ = forward
+
+    def stage_times(self, x: torch.Tensor | None = None) -> dict:
+        """One instrumented step (CUDA events between stages), in ms."""
+        b = self._bufs
+        if x is None:
+            raise ValueError("stage_times needs the step's input")
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(7)]
+        ev[0].record()
+        ops.router_topk(x, self.wts.wg, self.k, self.mode, out=(b.idx, b.w, b.counts))
+        ev[1].record()
+        ops.permute(b.idx, x, self.E, self.tile_m, out=(b.offsets, b.dst, b.x_perm), workspace=b.workspace)
+        ev[2].record()
+        ops.grouped_swiglu(b.x_perm, b.offsets, self.groups, self.w13_list, self.ff, h=b.h)
+        ev[3].record()
+        ops.grouped_down(b.h, b.offsets, self.groups, self.w2_list, self.d, y=b.y)
+        ev[4].record()
+        sh = self.shared_expert(x, b)
+        ev[5].record()
+        ops.combine(b.y, b.dst, b.w, sh, out=b.out)
+        ev[6].record()
+        torch.cuda.synchronize()
+        names = ["router", "permute", "swiglu_k3", "down_k4", "shared", "combine"]
+        return {n: ev[i].elapsed_time(ev[i + 1]) for i, n in enumerate(names)}
