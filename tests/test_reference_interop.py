@@ -1,0 +1,37 @@
+"""Drop-in check against the REAL reference objects (build container only):
+the executor-side API accepts moeplan's own instances and reproduces moeplan."""
+import numpy as np
+import pytest
+
+from paper_2605_17889_b200 import costmodel as CM
+from paper_2605_17889_b200 import eas
+
+
+def test_expert_stage_parts_accepts_reference_objects(moeplan):
+    from moeplan.costmodel import AllocationStrategy, expert_stage_parts
+    from moeplan.eas import ActivationMap
+    from moeplan.hardware import Device, DeviceSpec, LinkSpec, SystemSpec
+    from moeplan.workload import BatchConfig, ModelConfig, Phase
+    system = SystemSpec(DeviceSpec("gpu", 6.5e12, 1.36e15, 183e9), DeviceSpec("cpu", 3e11, 2e12, 1e12), LinkSpec(55e9))
+    model = ModelConfig(56, 6144, 16384, 8, 2, 2)
+    batch = BatchConfig(64, 4096, 0)
+    amap = ActivationMap(np.arange(1, 1 + 56 * 8, dtype=float).reshape(56, 8))
+    for part in [(8, 0, 0), (4, 4, 0), (2, 3, 3)]:
+        strat = AllocationStrategy((Device.GPU, Device.CPU, Device.GPU), *part, m=16)
+        ph = Phase.prefill(4096)
+        ref = expert_stage_parts(strat, ph, system, model, batch, amap)
+        ours = CM.expert_stage_parts(strat, ph, system, model, batch, amap)
+        assert (ours.act_load, ours.mig_load, ours.lat_gpu, ours.lat_cpu, ours.return_store) == \
+               (ref.act_load, ref.mig_load, ref.lat_gpu, ref.lat_cpu, ref.return_store)
+
+
+def test_residency_on_reference_map_and_trace(moeplan):
+    from moeplan import eas as R
+    trace = R.generate_synthetic_trace(1500, 8, 3, 16, 2, 5, 1.1, seed=9)
+    amap = R.stratified_activation_map(trace, R.StratificationConfig(5, 0.1, seed=9))
+    for cap in (0, 3, 8, 16):
+        assert eas.select_resident_experts(amap, cap).resident == R.select_resident_experts(amap, cap).resident
+        plan = R.select_resident_experts(amap, cap)
+        counts = np.zeros((3, 16))
+        np.add.at(counts, (trace.layer_idx, trace.expert_idx), trace.token_counts)
+        assert eas.hit_ratio_from_counts(counts, plan) == pytest.approx(R.hit_ratio(trace, plan), abs=0, rel=1e-15)
