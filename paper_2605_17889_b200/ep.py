@@ -1,0 +1,149 @@
+"""Expert parallelism across the GPUs of one box.
+
+One process per GPU.  Rank r owns experts [r*E/G, (r+1)*E/G) and its own
+batch of tokens (weak scaling: every rank routes its own ordinary batch, the
+coalesced per-expert batch on the owner is the union over all ranks).
+
+Per layer, on every rank (stream-ordered, CUDA kernels from libcoxmoe.so):
+  1. K1 route + K2 permute the local tokens by GLOBAL expert id — with
+     tile_m=1 the permuted rows are destination-rank-major, so they are the
+     all-to-all send buffer as is;
+  2. counts exchange: all_to_all of the E/G per-expert counts (one small
+     device->host read per layer to size the payload exchange);
+  3. dispatch: all_to_all_single (NCCL over NVLink/NVSwitch) of token rows;
+     the receive buffer holds, per source rank, that source's rows for each
+     local expert — every (source, expert) segment becomes one group of the
+     grouped GEMM (same weights, own row range), so no re-permute pass;
+  4. K3/K4 grouped expert GEMMs on the received rows;
+  5. combine: the reverse all_to_all_single returns y rows to their source;
+  6. K5 weighted combine on the home rank.
+Order contract: a source's rows arrive in that source's (expert, token)
+order, so the per-expert row order on the owner is (source rank, token) —
+the global token order when tokens are sharded contiguously — and results
+are bit-identical to a single-rank run (tests/test_ep.py checks this with
+the gloo backend and the CPU oracle standing in for the kernels).
+"""
+from __future__ import annotations
+
+import torch
+import torch.distributed as dist
+
+from . import ops
+from .layer import MODES
+from .synthetic import LayerWeights
+
+
+class CudaStage:
+    """The per-rank compute of the EP layer, on libcoxmoe.so kernels."""
+
+    def __init__(self, weights: LayerWeights, k: int, mode: int, local_experts: range):
+        self.w = weights
+        self.k = k
+        self.mode = mode
+        self.E = weights.num_experts
+        self.d = weights.hidden_dim
+        self.ff = weights.expert_dim
+        self.local = list(local_experts)
+        self.w13 = [weights.w13[e] for e in self.local]
+        self.w2 = [weights.w2[e] for e in self.local]
+        self._ws = None
+        self._h = None
+
+    def route_and_permute(self, x):
+        idx, w, counts = ops.router_topk(x, self.w.wg, self.k, self.mode)
+        T = x.shape[0]
+        if self._ws is None or self._ws.numel() < ops.permute_workspace_bytes(T, self.E):
+            self._ws = torch.empty((max(16, ops.permute_workspace_bytes(T, self.E)),), dtype=torch.uint8,
+                                   device=x.device)
+        offsets, dst, x_perm = ops.permute(idx, x, self.E, 1, workspace=self._ws)
+        return idx, w, counts, dst, x_perm
+
+    def experts(self, rows, seg_offsets, n_src, out=None):
+        L = len(self.local)
+        groups = list(range(n_src * L))
+        w13 = [self.w13[g % L] for g in groups]
+        w2 = [self.w2[g % L] for g in groups]
+        n = rows.shape[0]
+        if self._h is None or self._h.shape[0] < n:
+            self._h = torch.empty((max(n, 1), self.ff), dtype=torch.bfloat16, device=rows.device)
+        h = self._h[: max(n, 1)]
+        ops.grouped_swiglu(rows, seg_offsets, groups, w13, self.ff, h=h)
+        return ops.grouped_down(h, seg_offsets, groups, w2, self.d, y=out)
+
+    def combine(self, y_back, dst, w):
+        return ops.combine(y_back, dst, w)
+
+    def empty_rows(self, n, like):
+        return torch.empty((max(n, 1), self.d), dtype=like.dtype, device=like.device)
+
+
+def _a2a(out: torch.Tensor, inp: torch.Tensor, out_rows, in_rows, group):
+    """Row all-to-all; rows are moved as int32 words (bf16/fp32 payloads alike)."""
+    w = inp.shape[1] * inp.element_size() // 4
+    o = out.view(torch.int32).view(-1, w) if out.numel() else out.view(torch.int32)
+    i = inp.view(torch.int32).view(-1, w) if inp.numel() else inp.view(torch.int32)
+    dist.all_to_all_single(o, i, [int(v) for v in out_rows], [int(v) for v in in_rows], group=group)
+
+
+class EPMoELayer:
+    """MoE expert stage with experts sharded over the ranks of `group`."""
+
+    def __init__(self, weights: LayerWeights, top_k: int, mode: str = "mixtral", group=None, stage=None):
+        if mode not in MODES:
+            raise ValueError(f"mode must be one of {sorted(MODES)}")
+        self.group = group if group is not None else dist.group.WORLD
+        self.G = dist.get_world_size(self.group)
+        self.rank = dist.get_rank(self.group)
+        self.E = weights.num_experts if hasattr(weights, "num_experts") else weights["E"]
+        if self.E % self.G:
+            raise ValueError(f"{self.E} experts cannot be sharded evenly over {self.G} ranks")
+        self.L = self.E // self.G
+        if self.G * self.L > 64:
+            raise ValueError("at most 64 (source, expert) groups per grouped GEMM")
+        self.k = int(top_k)
+        local = range(self.rank * self.L, (self.rank + 1) * self.L)
+        self.stage = stage if stage is not None else CudaStage(weights, self.k, MODES[mode], local)
+        self._recv = None
+        self._yrecv = None
+        self._yback = None
+        self.last_split = None
+        self.profile_events = None
+
+    @property
+    def launches_per_step(self) -> int:
+        return 1 + 3 + 2 + 1
+
+    def _buf(self, name, n, like):
+        b = getattr(self, name)
+        if b is None or b.shape[0] < max(n, 1) or b.dtype != like.dtype:
+            b = self.stage.empty_rows(n, like)
+            setattr(self, name, b)
+        return b[:n]
+
+    def forward(self, x: torch.Tensor) -> torch.Tensor:
+        G, L, k = self.G, self.L, self.k
+        T = x.shape[0]
+        idx, w, counts, dst, x_perm = self.stage.route_and_permute(x)
+        # counts exchange: counts[e] for e owned by rank q go to rank q
+        recv_counts = torch.empty_like(counts)
+        dist.all_to_all_single(recv_counts, counts, group=self.group)
+        both = torch.cat([counts, recv_counts]).cpu()  # the one host sync per layer
+        send_seg = both[: self.E].view(G, L)
+        recv_seg = both[self.E:].view(G, L)  # [source rank, local expert]
+        send_rows = send_seg.sum(1).tolist()
+        recv_rows = recv_seg.sum(1).tolist()
+        n_recv = int(sum(recv_rows))
+        seg = torch.zeros(G * L + 1, dtype=torch.int32)
+        seg[1:] = torch.cumsum(recv_seg.reshape(-1), 0)
+        seg_offsets = seg.to(x.device, non_blocking=True)
+        self.last_split = (send_rows, recv_rows)
+
+        recv = self._buf("_recv", n_recv, x_perm)
+        _a2a(recv, x_perm[: T * k], recv_rows, send_rows, self.group)
+        yrecv = self._buf("_yrecv", n_recv, x_perm)
+        y = self.stage.experts(recv, seg_offsets, G, out=yrecv) if n_recv else yrecv
+        yback = self._buf("_yback", T * k, x_perm)
+        _a2a(yback, y[:n_recv], send_rows, recv_rows, self.group)
+        return self.stage.combine(yback, dst, w)
+
+    __call__ = forward

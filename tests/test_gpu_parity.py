@@ -204,3 +204,28 @@ def test_c2_scale_routing_and_permutation_bitexact_on_slice():
     assert np.array_equal(dst.cpu().numpy(), od)
     rows = torch.from_numpy(od[sl].reshape(-1)).to(DEV).long()
     assert torch.equal(x_perm[rows].view(-1, 2, d), x[sl].unsqueeze(1).expand(-1, 2, -1))
+
+
+def test_ep_layer_single_rank_nccl_matches_moelayer():
+    """EPMoELayer over NCCL with world_size 1 (the (source, expert) segment
+    groups, the all-to-all plumbing and the CUDA stage) == MoELayer bit-for-bit."""
+    import os
+    import socket
+    import torch.distributed as dist
+    from paper_2605_17889_b200.ep import EPMoELayer
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device(DEV, 0))
+    try:
+        T, d, ff, E, k = 3000, 512, 256, 8, 2
+        wts = make_layer_weights(E, d, ff, seed=0, device=DEV)
+        x = make_tokens(T, d, seed=1, device=DEV)
+        a = MoELayer(wts, k)(x).clone()
+        b = EPMoELayer(wts, k, "mixtral")(x)
+        torch.cuda.synchronize()
+        assert torch.equal(a, b)
+    finally:
+        dist.destroy_process_group()
