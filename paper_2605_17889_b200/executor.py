@@ -1,0 +1,276 @@
+"""Stratified multi-layer expert stage: hot experts pinned in HBM under a
+budget, cold experts streamed from pinned host memory, overlapped with the
+resident experts' GEMMs (BASELINE.json configs[2]; SURVEY.md §8a rows a4,
+a9-a12, a18).
+
+Reference mapping:
+  * AllocationStrategy.exp_r / exp_m (costmodel.py:45-89): per layer, the
+    residency plan's experts are exp_r (weights in HBM), the rest exp_m
+    (migrated every pass); exp_c must be 0 (no CPU expert path).
+  * vram_usage resident term (costmodel.py:460): resident bytes =
+    exp_r * 3*dt*d*ff * N; `capacity_per_layer` turns an HBM budget into exp_r.
+  * eas.select_resident_experts + probe (eas.py:346-374): `calibrate()` runs
+    prototype batches through the stack and accumulates the router's own
+    histograms (K1) into an ActivationMap, then picks the resident sets.
+  * sim.build_task_graph expert tasks (sim.py:149-202): measured timeline
+    records with the same {name, res, ts, dur} schema (sim.py:356-361), with
+    finer tasks: expert:gather (route+permute), expert:gpu:resident,
+    expert:migrate:L<l> (copy stream), expert:gpu:cold, expert:merge.
+    Unlike the reference's `expert:gpu` (which waits for the whole
+    migration), resident GEMMs start immediately; only the cold groups wait
+    for their copy events.
+
+Synthetic-model caveat (stated in DESIGN.md): expert weights are drawn from a
+pool of P distinct experts (expert (l, e) := pool[(l*E + e) % P]) so that the
+cold set fits in this host's pinned RAM; resident experts are real, distinct
+HBM copies and every cold expert crosses PCIe on every pass.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib, ops
+from .config import ExpertStageParts, ResidencyPlan
+from .eas import Calibrator, select_resident_experts
+from .layer import MODES
+from .streaming import HostExpertPool, SlotRing
+
+
+@dataclass
+class _Bufs:
+    T: int
+    idx: torch.Tensor
+    w: torch.Tensor
+    counts: torch.Tensor
+    offsets: torch.Tensor
+    dst: torch.Tensor
+    x_perm: torch.Tensor  # also receives y (K4 output) — x_perm is dead after K3
+    h: torch.Tensor
+    ping: torch.Tensor
+    pong: torch.Tensor
+    ws: torch.Tensor
+
+
+class StratifiedMoEStack:
+    def __init__(self, num_layers: int, wg: torch.Tensor, pool: HostExpertPool, top_k: int,
+                 residency: ResidencyPlan, mode: str = "mixtral", pool_map=None):
+        """wg: [N, E, d] fp32 router weights on the device; pool: host experts."""
+        self.N = int(num_layers)
+        self.wg = wg
+        self.E = wg.shape[1]
+        self.d = wg.shape[2]
+        self.ff = pool.w2.shape[2]
+        self.k = int(top_k)
+        self.mode = MODES[mode]
+        self.pool = pool
+        self.pool_map = pool_map or (lambda l, e: (l * self.E + e) % pool.size)
+        self.device = wg.device
+        self.res_w13: list[dict[int, torch.Tensor]] = []
+        self.res_w2: list[dict[int, torch.Tensor]] = []
+        self.ring = None
+        self._bufs = None
+        self.set_residency(residency)
+
+    # ------------------------------------------------------------ residency
+    def set_residency(self, plan: ResidencyPlan) -> None:
+        if plan.num_layers != self.N:
+            raise ValueError("residency plan must cover every layer")
+        self.plan = plan
+        self.res_w13, self.res_w2 = [], []
+        torch.cuda.empty_cache()
+        for l in range(self.N):
+            d13, d2 = {}, {}
+            for e in plan.resident[l]:
+                if not (0 <= e < self.E):
+                    raise ValueError("resident expert id out of range")
+                p = self.pool_map(l, e)
+                d13[e] = self.pool.w13[p].to(self.device, non_blocking=True)
+                d2[e] = self.pool.w2[p].to(self.device, non_blocking=True)
+            self.res_w13.append(d13)
+            self.res_w2.append(d2)
+        self.cold = [[e for e in range(self.E) if e not in set(plan.resident[l])] for l in range(self.N)]
+        C = max((len(c) for c in self.cold), default=0)
+        self.C = C
+        self.ring = SlotRing(2 * C, self.d, self.ff, self.device) if C else None
+        torch.cuda.synchronize()
+
+    @property
+    def resident_bytes(self) -> int:
+        per = self.pool.nbytes_per_expert()
+        return per * sum(len(r) for r in self.plan.resident)
+
+    @property
+    def launches_per_step(self) -> int:
+        per = 1 + 3 + 1  # router, permute x3, combine
+        return sum(per + (2 if self.plan.resident[l] else 0) + (2 if self.cold[l] else 0) for l in range(self.N))
+
+    def _buffers(self, T: int) -> _Bufs:
+        if self._bufs is None or self._bufs.T != T:
+            self._bufs = None
+            torch.cuda.empty_cache()
+            dev, bf = self.device, torch.bfloat16
+            cap = ops.rows_capacity(T, self.k, self.E, 1)
+            self._bufs = _Bufs(
+                T=T, idx=torch.empty((T, self.k), dtype=torch.int32, device=dev),
+                w=torch.empty((T, self.k), dtype=torch.float32, device=dev),
+                counts=torch.empty((self.E,), dtype=torch.int32, device=dev),
+                offsets=torch.empty((self.E + 1,), dtype=torch.int32, device=dev),
+                dst=torch.empty((T, self.k), dtype=torch.int32, device=dev),
+                x_perm=torch.empty((cap, self.d), dtype=bf, device=dev),
+                h=torch.empty((cap, self.ff), dtype=bf, device=dev),
+                ping=torch.empty((T, self.d), dtype=bf, device=dev),
+                pong=torch.empty((T, self.d), dtype=bf, device=dev),
+                ws=torch.empty((max(16, ops.permute_workspace_bytes(T, self.E)),), dtype=torch.uint8, device=dev))
+        return self._bufs
+
+    # ------------------------------------------------------------ forward
+    def _stage_layer(self, l: int, timing: bool):
+        base = (l % 2) * self.C
+        return [self.ring.stage(self.pool, self.pool_map(l, e), base + j, timing) for j, e in enumerate(self.cold[l])]
+
+    def forward(self, x: torch.Tensor, timeline: bool = False, counts_out: torch.Tensor | None = None):
+        """Run all N layers; returns the last layer's output (a view of an internal buffer).
+
+        counts_out: optional [N, E] int32 device tensor receiving each layer's
+        routed-token histogram (calibration / hit-ratio accounting)."""
+        if x.dtype != torch.bfloat16 or x.shape[1] != self.d:
+            raise ValueError(f"x must be bf16 [T, {self.d}]")
+        T = x.shape[0]
+        b = self._buffers(T)
+        s = torch.cuda.current_stream()
+        if self.ring is not None:
+            self.ring.copy_events = []
+        evs = [] if timeline else None
+        mk = (lambda: torch.cuda.Event(enable_timing=True)) if timeline else None
+        copy_done = {}
+        if self.C:
+            for l in range(min(2, self.N)):
+                copy_done[l] = self._stage_layer(l, timeline)
+        cur = x
+        for l in range(self.N):
+            out = b.ping if (l % 2 == 0) else b.pong
+            if timeline:
+                e0 = mk(); e0.record(s)
+            ops.router_topk(cur, self.wg[l], self.k, self.mode, out=(b.idx, b.w, b.counts))
+            ops.permute(b.idx, cur, self.E, 1, out=(b.offsets, b.dst, b.x_perm), workspace=b.ws)
+            if counts_out is not None:
+                counts_out[l].copy_(b.counts)
+            if timeline:
+                e1 = mk(); e1.record(s)
+            res = list(self.plan.resident[l])
+            if res:
+                ops.grouped_swiglu(b.x_perm, b.offsets, res, [self.res_w13[l][e] for e in res], self.ff, h=b.h)
+            if timeline:
+                e2 = mk(); e2.record(s)
+            cold = self.cold[l]
+            if cold:
+                for ev in copy_done.pop(l):
+                    s.wait_event(ev)
+                base = (l % 2) * self.C
+                slots = [base + j for j in range(len(cold))]
+                ops.grouped_swiglu(b.x_perm, b.offsets, cold, [self.ring.w13[i] for i in slots], self.ff, h=b.h)
+                ops.grouped_down(b.h, b.offsets, cold, [self.ring.w2[i] for i in slots], self.d, y=b.x_perm)
+                for i in slots:
+                    self.ring.release(i, s)
+                if l + 2 < self.N:
+                    copy_done[l + 2] = self._stage_layer(l + 2, timeline)
+            if timeline:
+                e3 = mk(); e3.record(s)
+            if res:
+                ops.grouped_down(b.h, b.offsets, res, [self.res_w2[l][e] for e in res], self.d, y=b.x_perm)
+            if timeline:
+                e4 = mk(); e4.record(s)
+            ops.combine(b.x_perm, b.dst, b.w, out=out)
+            if timeline:
+                e5 = mk(); e5.record(s)
+                evs.append((e0, e1, e2, e3, e4, e5))
+            cur = out
+        self._timeline_events = evs
+        return cur
+
+    __call__ = forward
+
+    # ------------------------------------------------------------ reporting
+    def timeline_records(self) -> list[dict]:
+        """Measured timeline in sim.timeline_records' schema (sim.py:356-361):
+        [{"name", "res", "ts", "dur"}] in seconds from the first event."""
+        torch.cuda.synchronize()
+        evs = self._timeline_events or []
+        if not evs:
+            return []
+        t0 = evs[0][0]
+        rec = []
+        ms = lambda a, b: a.elapsed_time(b) / 1e3  # noqa: E731
+        for l, (e0, e1, e2, e3, e4, e5) in enumerate(evs):
+            rec.append({"name": f"expert:gather:L{l}", "res": "gpu", "ts": ms(t0, e0), "dur": ms(e0, e1)})
+            rec.append({"name": f"expert:gpu:resident:L{l}", "res": "gpu", "ts": ms(t0, e1),
+                        "dur": ms(e1, e2) + ms(e3, e4)})
+            rec.append({"name": f"expert:gpu:cold:L{l}", "res": "gpu", "ts": ms(t0, e2), "dur": ms(e2, e3)})
+            rec.append({"name": f"expert:merge:L{l}", "res": "gpu", "ts": ms(t0, e4), "dur": ms(e4, e5)})
+        if self.ring is not None:
+            for i, (slot, a, b) in enumerate(self.ring.copy_events):
+                rec.append({"name": f"expert:migrate:slot{slot}:{i}", "res": "h2d", "ts": ms(t0, a), "dur": ms(a, b)})
+        return sorted(rec, key=lambda r: r["ts"])
+
+    def measured_parts(self) -> ExpertStageParts:
+        """Per-layer mean of the measured timeline, in ExpertStageParts' fields
+        (costmodel.py:199-222): act_load 0 (activations stay in HBM),
+        mig_load = copy-engine busy time, lat_gpu = stage GPU time."""
+        rec = self.timeline_records()
+        n = max(1, self.N)
+        mig = sum(r["dur"] for r in rec if r["res"] == "h2d") / n
+        gpu = sum(r["dur"] for r in rec if r["res"] == "gpu") / n
+        return ExpertStageParts(act_load=0.0, mig_load=mig, lat_gpu=gpu, lat_cpu=0.0, return_store=0.0)
+
+    # ------------------------------------------------------------ calibration
+    def calibrate(self, batches, capacity_per_layer: int) -> ResidencyPlan:
+        """Prefill-only probing: run prototype batches through the
+        stack, accumulate K1 histograms per layer, choose the hot set per layer
+        (eas.select_resident_experts) and re-place the resident copies."""
+        cal = Calibrator(self.N, self.E)
+        counts = torch.zeros((self.N, self.E), dtype=torch.int32, device=self.device)
+        for xb in batches:
+            self.forward(xb, counts_out=counts)
+            torch.cuda.synchronize()
+            c = counts.cpu().numpy()
+            for l in range(self.N):
+                cal.observe(l, c[l])
+        plan = select_resident_experts(cal.activation_map(), capacity_per_layer)
+        self._bufs = None
+        self.set_residency(plan)
+        self.calibration_map = cal.activation_map()
+        return plan
+
+
+def make_pool(P: int, d: int, ff: int, seed: int = 0, device="cuda") -> HostExpertPool:
+    """P distinct random experts generated on the device, copied to pinned host memory."""
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+    w13 = torch.empty((P, 2 * ff, d), dtype=torch.bfloat16, device=device)
+    w2 = torch.empty((P, d, ff), dtype=torch.bfloat16, device=device)
+    for p in range(P):
+        w13[p].uniform_(-d ** -0.5, d ** -0.5, generator=g)
+        w2[p].uniform_(-ff ** -0.5, ff ** -0.5, generator=g)
+    pool = HostExpertPool.from_device(w13, w2)
+    del w13, w2
+    torch.cuda.empty_cache()
+    return pool
+
+
+def make_router_weights(N: int, E: int, d: int, seed: int = 7, device="cuda") -> torch.Tensor:
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+    wg = torch.empty((N, E, d), dtype=torch.float32, device=device)
+    wg.uniform_(-d ** -0.5, d ** -0.5, generator=g)
+    return wg.to(torch.bfloat16).float()
+
+
+def hit_ratio_of_counts(counts: np.ndarray, plan: ResidencyPlan) -> float:
+    from .eas import hit_ratio_from_counts
+    return hit_ratio_from_counts(counts, plan)
+
+
+__all__ = ["StratifiedMoEStack", "make_pool", "make_router_weights", "HostExpertPool", "hit_ratio_of_counts", "_lib"]
