@@ -45,7 +45,11 @@ CONFIGS = {
             "C3/C5 Mixtral-8x22B MoE layer (E=8, top-2, d=6144, ff=16384), batch 64x4096 per GPU"),
     "C4": (64 * 4096, 2048, 1408, 64, 6, "deepseek", 2816,
            "C4 DeepSeek-V2-Lite MoE layer (64 routed top-6 + 2 shared, d=2048, ff=1408), batch 64x4096"),
+    "C3": (64 * 4096, 6144, 16384, 8, 2, "mixtral", 0,
+           "C3 Mixtral-8x22B-shaped 56-layer MoE stack, batch 64x4096, HBM budget -> calibrated hot experts "
+           "resident, cold experts streamed from pinned host memory"),
 }
+STACK_LAYERS = 56
 
 
 def metric_name(config: str) -> str:
@@ -195,6 +199,79 @@ def run_reference(args, cfg):
     print(json.dumps(line), flush=True)
 
 
+def run_stack(args, cfg):
+    """C3: the 56-layer stratified stack on one GPU (BASELINE.json configs[2])."""
+    import torch
+    from paper_2605_17889_b200 import costmodel as CM
+    from paper_2605_17889_b200.config import ModelConfig, ResidencyPlan, AllocationStrategy, Device, BatchConfig, Phase
+    from paper_2605_17889_b200.executor import StratifiedMoEStack, make_pool, make_router_weights
+    from paper_2605_17889_b200.eas import hit_ratio_from_counts
+    from paper_2605_17889_b200.synthetic import make_tokens
+
+    T, d, ff, E, k, mode, _, desc = cfg
+    N = args.layers
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    model = ModelConfig(N, d, ff, E, k, 2)
+    pool = make_pool(args.pool, d, ff, seed=0, device=dev)
+    wg = make_router_weights(N, E, d, seed=7, device=dev)
+    stack = StratifiedMoEStack(N, wg, pool, k, ResidencyPlan(tuple(() for _ in range(N)), 0), mode)
+    # calibration: prototype batches through the all-cold stack (prefill-only probing)
+    protos = [make_tokens(args.proto_tokens, d, seed=100 + i, device=dev) for i in range(2)]
+    # capacity from the HBM budget is computed after calibration frees its buffers
+    stack.calibrate(protos, 0)
+    del protos
+    cap = stack.max_capacity(T)
+    from paper_2605_17889_b200.eas import select_resident_experts
+    plan = select_resident_experts(stack.calibration_map, cap)
+    stack.set_residency(plan)
+    x = make_tokens(T, d, seed=1, device=dev)
+    counts = torch.zeros((N, E), dtype=torch.int32, device=dev)
+    for _ in range(args.warmup):
+        stack(x)
+    torch.cuda.synchronize()
+    s = torch.cuda.current_stream()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(0) as clk:
+        torch.cuda.synchronize()
+        a.record(s)
+        for i in range(args.steps):
+            stack(x, counts_out=counts if i == args.steps - 1 else None)
+        b.record(s)
+        torch.cuda.synchronize()
+    ms = a.elapsed_time(b) / args.steps
+    stack(x, timeline=True)
+    parts = stack.measured_parts()
+    hit = hit_ratio_from_counts(counts.cpu().numpy().astype(float), plan)
+    pk = peaks()
+    flops = N * (6.0 * T * k * d * ff + 2.0 * T * d * E)
+    n_cold = sum(len(c) for c in stack.cold)
+    mig_bytes = n_cold * pool.nbytes_per_expert()
+    strat = AllocationStrategy((Device.GPU,) * 3, cap, E - cap, 0, m=64)
+    ana = CM.expert_stage_parts(strat, Phase.prefill(4096), CM.b200_system(), model, BatchConfig(64, 4096, 0),
+                                stack.calibration_map, count_top_k=True)
+    line = {
+        "metric": metric_name("C3"), "value": T / (ms / 1e3), "unit": "tokens/s", "n_gpus": 1,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic; expert (l,e) weights = pool[(l*E+e) % P] (P distinct experts in pinned host RAM)",
+        "config": {"workload": desc, "layers": N, "tokens": T, "d": d, "ff": ff, "E": E, "k": k,
+                   "resident_per_layer": cap, "resident_bytes": stack.resident_bytes, "host_pool_experts": args.pool,
+                   "cold_experts_per_step": n_cold, "h2d_bytes_per_step": mig_bytes},
+        "stack_tflops": flops / (ms / 1e3) / 1e12,
+        "frac_of_bf16_sustained": flops / (ms / 1e3) / 1e12 / pk["bf16_sus"],
+        "hit_ratio": hit,
+        "measured_parts_per_layer_s": {"act_load": parts.act_load, "mig_load": parts.mig_load,
+                                       "lat_gpu": parts.lat_gpu},
+        "analytical_parts_per_layer_s": {"act_load": ana.act_load, "mig_load": ana.mig_load, "lat_gpu": ana.lat_gpu,
+                                         "system": "b200 measured peaks, 55 GB/s link, k counted"},
+        "h2d_gbs": mig_bytes / max(1e-9, parts.mig_load * N) / 1e9,
+        "gpu_launches": stack.launches_per_step * args.steps,
+        "clocks": clk.summary(),
+    }
+    print(json.dumps(line), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -206,11 +283,16 @@ def main():
     ap.add_argument("--ref-tokens", type=int, default=512, help="tokens per step for --impl reference")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--layers", type=int, default=STACK_LAYERS, help="C3 stack depth")
+    ap.add_argument("--pool", type=int, default=16, help="C3 distinct host-pool experts")
+    ap.add_argument("--proto-tokens", type=int, default=8192, help="C3 calibration batch size")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     cfg = CONFIGS[args.config]
     if args.impl == "reference":
         return run_reference(args, cfg)
+    if args.config == "C3":
+        return run_stack(args, cfg)
 
     import torch
     import torch.distributed as dist

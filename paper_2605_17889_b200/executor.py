@@ -56,8 +56,10 @@ class _Bufs:
 
 class StratifiedMoEStack:
     def __init__(self, num_layers: int, wg: torch.Tensor, pool: HostExpertPool, top_k: int,
-                 residency: ResidencyPlan, mode: str = "mixtral", pool_map=None):
-        """wg: [N, E, d] fp32 router weights on the device; pool: host experts."""
+                 residency: ResidencyPlan, mode: str = "mixtral", pool_map=None, residual: bool = True):
+        """wg: [N, E, d] fp32 router weights on the device; pool: host experts.
+        residual: layer l+1 consumes x_l + MoE_l(x_l) (the residual stream, added
+        inside K5) instead of MoE_l(x_l) alone."""
         self.N = int(num_layers)
         self.wg = wg
         self.E = wg.shape[1]
@@ -68,6 +70,7 @@ class StratifiedMoEStack:
         self.pool = pool
         self.pool_map = pool_map or (lambda l, e: (l * self.E + e) % pool.size)
         self.device = wg.device
+        self.residual = bool(residual)
         self.res_w13: list[dict[int, torch.Tensor]] = []
         self.res_w2: list[dict[int, torch.Tensor]] = []
         self.ring = None
@@ -80,6 +83,7 @@ class StratifiedMoEStack:
             raise ValueError("residency plan must cover every layer")
         self.plan = plan
         self.res_w13, self.res_w2 = [], []
+        self.ring = None
         torch.cuda.empty_cache()
         for l in range(self.N):
             d13, d2 = {}, {}
@@ -183,7 +187,8 @@ class StratifiedMoEStack:
                 ops.grouped_down(b.h, b.offsets, res, [self.res_w2[l][e] for e in res], self.d, y=b.x_perm)
             if timeline:
                 e4 = mk(); e4.record(s)
-            ops.combine(b.x_perm, b.dst, b.w, out=out)
+            # residual stream: out = x_l + sum_j w_j y_j, fused into K5 (shared_out = x_l)
+            ops.combine(b.x_perm, b.dst, b.w, shared=cur if self.residual else None, out=out)
             if timeline:
                 e5 = mk(); e5.record(s)
                 evs.append((e0, e1, e2, e3, e4, e5))
@@ -226,6 +231,23 @@ class StratifiedMoEStack:
         return ExpertStageParts(act_load=0.0, mig_load=mig, lat_gpu=gpu, lat_cpu=0.0, return_store=0.0)
 
     # ------------------------------------------------------------ calibration
+    def max_capacity(self, T: int, slack_bytes: int = 4 << 30) -> int:
+        """Largest exp_r whose resident copies + the T-token activations + the
+        2*(E - exp_r) slot ring fit in the free HBM (x, ping, pong, x_perm, h) (the vram_usage feasibility
+        test, costmodel.py:440-489, with measured free memory)."""
+        self.ring = None
+        self._bufs = None
+        self.res_w13, self.res_w2 = [], []
+        torch.cuda.empty_cache()
+        free, _ = torch.cuda.mem_get_info(self.device)
+        per = self.pool.nbytes_per_expert()
+        act = T * self.d * 2 * 3 + ops.rows_capacity(T, self.k, self.E) * (self.d + self.ff) * 2
+        for cap in range(self.E, -1, -1):
+            need = cap * per * self.N + 2 * (self.E - cap) * per + act + slack_bytes
+            if need <= free:
+                return cap
+        return 0
+
     def calibrate(self, batches, capacity_per_layer: int) -> ResidencyPlan:
         """Prefill-only probing: run prototype batches through the
         stack, accumulate K1 histograms per layer, choose the hot set per layer
