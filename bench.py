@@ -45,6 +45,9 @@ CONFIGS = {
             "C3/C5 Mixtral-8x22B MoE layer (E=8, top-2, d=6144, ff=16384), batch 64x4096 per GPU"),
     "C4": (64 * 4096, 2048, 1408, 64, 6, "deepseek", 2816,
            "C4 DeepSeek-V2-Lite MoE layer (64 routed top-6 + 2 shared, d=2048, ff=1408), batch 64x4096"),
+    "C4D": (64, 2048, 1408, 64, 6, "deepseek", 2816,
+            "C4 DeepSeek-V2-Lite MoE layer decode step: 64 sequences x 1 token (64 routed top-6 + 2 shared), "
+            "CUDA-graph replay"),
     "C3": (64 * 4096, 6144, 16384, 8, 2, "mixtral", 0,
            "C3 Mixtral-8x22B-shaped 56-layer MoE stack, batch 64x4096, HBM budget -> calibrated hot experts "
            "resident, cold experts streamed from pinned host memory"),
@@ -283,6 +286,8 @@ def main():
     ap.add_argument("--ref-tokens", type=int, default=512, help="tokens per step for --impl reference")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--microbatch", type=int, default=0,
+                    help="ablation: run the expert stage per micro-batch of this many tokens (not coalesced)")
     ap.add_argument("--layers", type=int, default=STACK_LAYERS, help="C3 stack depth")
     ap.add_argument("--pool", type=int, default=16, help="C3 distinct host-pool experts")
     ap.add_argument("--proto-tokens", type=int, default=8192, help="C3 calibration batch size")
@@ -315,6 +320,14 @@ def main():
     else:
         layer = MoELayer(wts, k, mode)
     stream = torch.cuda.current_stream()
+    graph = args.config == "C4D" and ws == 1
+    if graph:
+        replay, _ = layer.capture(x)
+        step = lambda: replay()  # noqa: E731
+    elif args.microbatch:
+        step = lambda: layer.forward_microbatched(x, args.microbatch)  # noqa: E731
+    else:
+        step = lambda: layer(x)  # noqa: E731
 
     def barrier():
         if ws > 1:
@@ -323,7 +336,7 @@ def main():
 
     # --- device-resident throughput ------------------------------------------
     for _ in range(args.warmup):
-        layer(x)
+        step()
     barrier()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     k3 = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
@@ -337,7 +350,7 @@ def main():
         for i in range(args.steps):
             layer.profile_events = {"k3": k3[i], "k4": k4[i]}
             ev[i][0].record(stream)
-            layer(x)
+            step()
             ev[i][1].record(stream)
         stop.record(stream)
         barrier()
@@ -350,42 +363,64 @@ def main():
     ms_step = ms_total / args.steps
     tokens_all = T * ws * args.steps
     value = tokens_all / (ms_total / 1e3)
-    k3_ms = sum(a.elapsed_time(b) for a, b in k3) / args.steps
-    k4_ms = sum(a.elapsed_time(b) for a, b in k4) / args.steps
+    k3_ms = sum(a.elapsed_time(b) for a, b in k3) / args.steps if not (graph or args.microbatch) else None
+    k4_ms = sum(a.elapsed_time(b) for a, b in k4) / args.steps if not (graph or args.microbatch) else None
 
     # --- end-to-end through the public API with host buffers ------------------
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and not args.microbatch:
+        # pinned host batches; each step = H2D of its tokens + expert stage + D2H of its output,
+        # pipelined across steps (ws == 1: MoELayer.run_host_batches; EP: sequential per step)
         x_host = x.cpu().pin_memory()
-        out_host = torch.empty((T, d), dtype=torch.bfloat16).pin_memory()
-        xd = torch.empty_like(x)
-        for _ in range(2):
-            xd.copy_(x_host, non_blocking=True)
-            out_host.copy_(layer(xd), non_blocking=True)
+        outs = [torch.empty((T, d), dtype=torch.bfloat16).pin_memory() for _ in range(2)]
+        if hasattr(layer, "run_host_batches"):
+            layer.run_host_batches([x_host] * 2, outs)
         barrier()
         s0 = torch.cuda.Event(enable_timing=True)
         s1 = torch.cuda.Event(enable_timing=True)
         s0.record(stream)
-        for _ in range(args.steps):
-            xd.copy_(x_host, non_blocking=True)
-            out_host.copy_(layer(xd), non_blocking=True)
+        if hasattr(layer, "run_host_batches"):
+            layer.run_host_batches([x_host] * args.steps, [outs[i % 2] for i in range(args.steps)])
+        else:
+            xd = torch.empty_like(x)
+            for i in range(args.steps):
+                xd.copy_(x_host, non_blocking=True)
+                outs[i % 2].copy_(layer(xd), non_blocking=True)
         s1.record(stream)
         barrier()
         e_ms = torch.tensor([s0.elapsed_time(s1)], dtype=torch.float64, device=dev)
         if ws > 1:
             dist.all_reduce(e_ms, op=dist.ReduceOp.MAX)
         e2e = {"value": tokens_all / (float(e_ms.item()) / 1e3), "unit": "tokens/s",
-               "h2d_bytes_per_step": x.numel() * 2 * ws, "d2h_bytes_per_step": T * d * 2 * ws}
+               "h2d_bytes_per_step": x.numel() * 2 * ws, "d2h_bytes_per_step": T * d * 2 * ws,
+               "api": "MoELayer.run_host_batches (pinned host in/out, copies overlapped across steps)"
+               if ws == 1 else "EPMoELayer per step with H2D/D2H copies"}
 
     # --- per-stage breakdown (one extra step, not part of `value`) ------------
-    stages = layer.stage_times(x) if hasattr(layer, "stage_times") else None
+    stages = layer.stage_times(x) if hasattr(layer, "stage_times") and not args.microbatch else None
+    touched = int((layer.buffers(T, dev).counts > 0).sum().item()) if hasattr(layer, "buffers") else E
 
     if rank == 0:
         pk = peaks()
         flops_k3 = 4.0 * T * k * d * ff
         flops_k4 = 2.0 * T * k * d * ff
         flops_layer = 6.0 * T * k * d * ff + 2.0 * T * d * E + (6.0 * T * d * shared_ff if shared_ff else 0.0)
-        achieved = flops_k3 / (k3_ms / 1e3) / 1e12
+        if k3_ms:
+            achieved = flops_k3 / (k3_ms / 1e3) / 1e12
+            roof = {"kernel": "grouped_gemm_kernel<EPI_SWIGLU> (K3)", "bound": "tensor", "achieved": achieved,
+                    "peak": pk["bf16_sus"], "unit": "TFLOP/s", "frac": achieved / pk["bf16_sus"], "traffic": None,
+                    "peak_kind": f"bf16_tflops_sustained ({pk['src']}); burst {pk['bf16']}", "k3_ms": k3_ms,
+                    "k4_ms": k4_ms, "k4_tflops": flops_k4 / (k4_ms / 1e3) / 1e12}
+        else:
+            # decode / micro-batched: whole step vs the HBM bound of the weights it must read
+            per_exp = 3 * d * ff * 2
+            wbytes = touched * per_exp + (3 * d * shared_ff * 2 if shared_ff else 0)
+            abytes = T * d * 2 * (2 + 2 * k)
+            achieved = (wbytes + abytes) / (ms_step / 1e3) / 1e9
+            roof = {"kernel": "whole expert stage (CUDA graph)" if graph else "whole expert stage (micro-batched)",
+                    "bound": "hbm", "achieved": achieved, "peak": pk["hbm"], "unit": "GB/s",
+                    "frac": achieved / pk["hbm"], "traffic": None,
+                    "bytes_per_step": wbytes + abytes, "experts_touched": touched}
         cpu = None
         if not args.no_cpu_baseline and ws == 1:
             hw, shared = host_weights(wts)
@@ -394,27 +429,26 @@ def main():
             cpu = {"value": cps, "unit": "tokens/s", "cores": threads, "kind": "port",
                    "sample": f"first {args.cpu_tokens} of {T} tokens (routed as in the full batch), full-size "
                              f"weights, fp32 oracle (oracle/, OpenMP x{threads}) on {cpu_model_name()}: {dt:.1f} s"}
+        if args.microbatch:
+            desc_mb = f" [ABLATION: micro-batched, {args.microbatch} tokens per expert-stage launch]"
+        else:
+            desc_mb = ""
         line = {
             "metric": metric_name(args.config),
             "value": value, "unit": "tokens/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "bf16", "data": "synthetic (seeded N(0,1) tokens, nn.Linear-style U(+-1/sqrt(fan_in)) weights)",
-            "config": {"workload": desc, "tokens_per_gpu": T, "global_batch_tokens": T * ws, "d": d, "ff": ff,
+            "config": {"workload": desc + desc_mb, "tokens_per_gpu": T, "global_batch_tokens": T * ws, "d": d, "ff": ff,
                        "E": E, "k": k, "routing": mode, "parallelism": f"ep{ws}" if ws > 1 else "single",
                        "l2": "inputs > L2 (x 2.1 GB, x_perm 4.3 GB, h 15 GB vs 126 MB L2); no flush"},
             "layer_tflops": flops_layer / (ms_step / 1e3) / 1e12,
             "frac_layer_of_bf16_sustained": flops_layer / (ms_step / 1e3) / 1e12 / pk["bf16_sus"],
             "frac_layer_of_bf16_burst": flops_layer / (ms_step / 1e3) / 1e12 / pk["bf16"],
-            "roofline": {"kernel": "grouped_gemm_kernel<EPI_SWIGLU> (K3)", "bound": "tensor",
-                         "achieved": achieved, "peak": pk["bf16_sus"], "unit": "TFLOP/s",
-                         "frac": achieved / pk["bf16_sus"], "traffic": None,
-                         "peak_kind": f"bf16_tflops_sustained ({pk['src']}); burst {pk['bf16']}",
-                         "k3_ms": k3_ms, "k4_ms": k4_ms,
-                         "k4_tflops": flops_k4 / (k4_ms / 1e3) / 1e12},
+            "roofline": roof,
             "stages_ms": stages,
             "cpu_baseline": cpu,
             "e2e": e2e,
-            "gpu_launches": layer.launches_per_step * args.steps,
+            "gpu_launches": layer.launches_per_step * args.steps * (-(-T // args.microbatch) if args.microbatch else 1),
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)

@@ -12,7 +12,10 @@ import threading
 from pathlib import Path
 
 _PKG = Path(__file__).resolve().parent
-LIB_PATH = _PKG / "libcoxmoe.so"
+import os as _os
+
+# COXMOE_LIB overrides the in-tree library (A/B experiments between builds).
+LIB_PATH = Path(_os.environ["COXMOE_LIB"]) if _os.environ.get("COXMOE_LIB") else _PKG / "libcoxmoe.so"
 
 COX_OK = 0
 COX_EINVAL = -1

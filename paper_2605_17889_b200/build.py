@@ -36,11 +36,14 @@ def needs_build() -> bool:
     return any(p.stat().st_mtime > t for p in deps if p.exists())
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
-    if not force and not needs_build():
+def build(force: bool = False, verbose: bool = False, out: Path | None = None, csrc: Path | None = None) -> Path:
+    """Compile the sources in `csrc` (default: csrc/) into `out` (default: libcoxmoe.so)."""
+    lib = Path(out) if out else LIB
+    src_dir = Path(csrc) if csrc else CSRC
+    if not force and out is None and csrc is None and not needs_build():
         return LIB
-    objdir = PKG / "build"
-    objdir.mkdir(exist_ok=True)
+    objdir = PKG / "build" / lib.stem
+    objdir.mkdir(parents=True, exist_ok=True)
     common = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v" if verbose else "-O3",
               "-I", str(ROOT / "include")]
     objs = []
@@ -48,7 +51,8 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     for s in SOURCES:
         o = objdir / (Path(s).stem + ".o")
         objs.append(o)
-        procs.append((s, subprocess.Popen([*common, "-c", str(CSRC / s), "-o", str(o)], stdout=subprocess.PIPE,
+        procs.append((s, subprocess.Popen([*common, "-I", str(CSRC), "-c", str(src_dir / s), "-o", str(o)],
+                                          stdout=subprocess.PIPE,
                                           stderr=subprocess.STDOUT, text=True)))
     for s, p in procs:
         out, _ = p.communicate()
@@ -56,10 +60,10 @@ def build(force: bool = False, verbose: bool = False) -> Path:
             sys.stderr.write(out)
         if p.returncode:
             raise RuntimeError(f"nvcc failed on {s}")
-    tmp = LIB.with_suffix(".so.tmp")
+    tmp = lib.with_suffix(".so.tmp")
     subprocess.run([nvcc(), *ARCH, "-shared", "-o", str(tmp), *map(str, objs), "-cudart", "static"], check=True)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":

@@ -159,11 +159,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GM_THREADS, 1)
   // tiles of the rasterised order and keep sharing A/B in L2 — a static
   // round-robin lets pairs drift apart by whole waves.  Every role consumes
   // the same sequence; a value >= total terminates.
-  auto fetch_tile = [&](int& si) -> int {
+  // Leader-CTA consumers use CTA-scope wait/arrive (cheap); the peer CTA needs
+  // cluster scope (its tile id was written remotely by the leader).
+  auto fetch_tile = [&](int& si, bool do_arrive) -> int {
     const int slot = si % GM_SCHED_DEPTH;
-    mbar_wait_cluster(smem_u32(&sfull[slot]), (si / GM_SCHED_DEPTH) & 1);
-    const int t = reinterpret_cast<volatile int*>(s_tile)[slot];
-    mbar_arrive_cluster(mapa(smem_u32(&sempty[slot]), 0));
+    const uint32_t ph = (si / GM_SCHED_DEPTH) & 1;
+    int t;
+    if (rank == 0) {
+      mbar_wait(smem_u32(&sfull[slot]), ph);
+      t = reinterpret_cast<volatile int*>(s_tile)[slot];
+      __syncwarp(__activemask());
+      if (do_arrive) mbar_arrive(smem_u32(&sempty[slot]));
+    } else {
+      mbar_wait_cluster(smem_u32(&sfull[slot]), ph);
+      t = reinterpret_cast<volatile int*>(s_tile)[slot];
+      __syncwarp(__activemask());
+      if (do_arrive) mbar_arrive_cluster(mapa(smem_u32(&sempty[slot]), 0));
+    }
     ++si;
     return t;
   };
@@ -173,12 +185,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GM_THREADS, 1)
     if (rank == 0 && lane == 0) {
       for (int i = 0;; ++i) {
         const int slot = i % GM_SCHED_DEPTH;
-        mbar_wait_cluster(smem_u32(&sempty[slot]), ((i / GM_SCHED_DEPTH) & 1) ^ 1);
+        mbar_wait(smem_u32(&sempty[slot]), ((i / GM_SCHED_DEPTH) & 1) ^ 1);
         int t = (i == 0) ? cid : ncl + atomicAdd(p.tile_counter, 1);
         if (t > total) t = total;
         s_tile[slot] = t;
         st_shared_cluster_u32(mapa(smem_u32(&s_tile[slot]), 1), (uint32_t)t);
-        mbar_arrive_cluster(mapa(smem_u32(&sfull[slot]), 0));
+        mbar_arrive(smem_u32(&sfull[slot]));
         mbar_arrive_cluster(mapa(smem_u32(&sfull[slot]), 1));
         if (t >= total) break;
       }
@@ -189,13 +201,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GM_THREADS, 1)
     if (lane == 0) {
       uint32_t stage = 0, phase = 0;
       int si = 0;
-      for (;;) {
-        const int t = fetch_tile(si);
-        if (t >= total) break;
+      int t = fetch_tile(si, true);
+      while (t < total) {
         const TileCoord c = decode_tile(t, s_prefix, s_rows, p.band);
         const int a_row = s_row0[c.g] + c.m * 2 * GM_BM + (int)rank * GM_BM;
         const int b_row = c.n * GM_BN + (int)rank * (GM_BN / 2);
         const CUtensorMap* bmap = &p.b_map[c.g];
+        int t_next = total;
         for (int kb = 0; kb < nk; ++kb) {
           mbar_wait(smem_u32(&empty[stage]), phase ^ 1);
           const uint32_t fb_local = smem_u32(&full[stage]);
@@ -204,7 +216,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GM_THREADS, 1)
           tma_load_2d_pair(smem_u32(sA + stage * GM_A_BYTES), &p.a_map, fb, kb * GM_BK, a_row);
           tma_load_2d_pair(smem_u32(sB + stage * GM_B_BYTES), bmap, fb, kb * GM_BK, b_row);
           if (++stage == GM_STAGES) { stage = 0; phase ^= 1; }
+          if (kb == 0) t_next = fetch_tile(si, true);  // look ahead: hide the fetch behind this tile
         }
+        t = t_next;
       }
     }
     __syncwarp();
@@ -214,9 +228,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GM_THREADS, 1)
       const uint32_t idesc = idesc_bf16_f32(2 * GM_BM, GM_BN);
       uint32_t stage = 0, phase = 0;
       int si = 0;
-      for (int it = 0;; ++it) {
-        const int t = fetch_tile(si);
-        if (t >= total) break;
+      int t = fetch_tile(si, true);
+      for (int it = 0; t < total; ++it) {
+        int t_next = total;
         const int acc = it & 1;
         const uint32_t acc_phase = (it >> 1) & 1;
         mbar_wait(smem_u32(&tempty[acc]), acc_phase ^ 1);
@@ -234,8 +248,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GM_THREADS, 1)
           }
           mma_commit<2>(smem_u32(&empty[stage]));
           if (++stage == GM_STAGES) { stage = 0; phase ^= 1; }
+          if (kb == 0) t_next = fetch_tile(si, true);  // look ahead while the tensor pipe is busy
         }
         mma_commit<2>(smem_u32(&tfull[acc]));
+        t = t_next;
       }
     }
     __syncwarp();
@@ -248,15 +264,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GM_THREADS, 1)
     __nv_bfloat16* out = static_cast<__nv_bfloat16*>(p.out);
     int si = 0;
     for (int it = 0;; ++it) {
-      int t;
-      {
-        const int slot = si % GM_SCHED_DEPTH;
-        mbar_wait_cluster(smem_u32(&sfull[slot]), (si / GM_SCHED_DEPTH) & 1);
-        t = reinterpret_cast<volatile int*>(s_tile)[slot];
-        __syncwarp();
-        if (lane == 0) mbar_arrive_cluster(mapa(smem_u32(&sempty[slot]), 0));
-        ++si;
-      }
+      const int t = fetch_tile(si, lane == 0);
       if (t >= total) break;
       const TileCoord c = decode_tile(t, s_prefix, s_rows, p.band);
       const int acc = it & 1;
@@ -381,12 +389,18 @@ static int get_map(CUtensorMap* out, const void* ptr, unsigned long long rows, u
   return 0;
 }
 
-static int pick_band(int n_tiles) {
-  static int env_band = [] {
-    const char* e = getenv("COX_GEMM_BAND");
-    return e ? atoi(e) : 0;
-  }();
-  if (env_band > 0 && n_tiles % env_band == 0) return env_band;
+// Raster band (n-tiles per band).  Defaults chosen by measurement; the
+// COX_GEMM_BAND_K3 / COX_GEMM_BAND_K4 environment variables override them
+// for experiments.
+static int pick_band(int epi, int n_tiles) {
+  static int env_band[2] = {
+      [] { const char* e = getenv("COX_GEMM_BAND_K3"); return e ? atoi(e) : 0; }(),
+      [] { const char* e = getenv("COX_GEMM_BAND_K4"); return e ? atoi(e) : 0; }()};
+  const int want = env_band[epi ? 1 : 0];
+  if (want > 0 && n_tiles % want == 0) return want;
+  // K3 (SwiGLU, K = d): 16-wide bands halve the A re-reads with the B band
+  // still L2-resident (C2: 32 MB); K4 (K = ff, 3.5x longer tiles): 8.
+  if (!epi && n_tiles % 16 == 0) return 16;
   for (int b : {8, 4, 2, 1})
     if (n_tiles % b == 0) return b;
   return 1;
@@ -425,7 +439,7 @@ int launch_grouped_gemm(int epi, const void* A, long long rows_cap, int K, const
   p.n_groups = n_groups;
   p.K = K;
   p.n_tiles = N / GM_BN;
-  p.band = pick_band(p.n_tiles);
+  p.band = pick_band(epi, p.n_tiles);
   if (g_num_sms == 0) {
     int dev = 0;
     cudaGetDevice(&dev);

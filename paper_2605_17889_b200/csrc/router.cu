@@ -10,68 +10,96 @@
 // oracle (oracle/oracle_router.c) replays exactly: lane l owns the 8-element
 // chunks c = 32*j + l, accumulating fmaf(x, w, acc) with j then q ascending,
 // followed by an xor butterfly 16,8,4,2,1 of __fadd_rn.  CUDA cores only — no
-// tensor cores — so the order is fixed.  HBM-bound: x is read exactly once with
-// 16-byte vector loads; router weights stay L1/L2-resident.
+// tensor cores — so the order is fixed.
+//
+// Work decomposition: a block of 8 warps covers RT_TPW*NTG tokens x all E
+// experts; warp w owns an RT_TPW-token x 8-expert register tile (token group
+// w / EGN, expert group w % EGN, EGN = expert groups per block pass).  The
+// warps of a block that share tokens read the same x chunks (L1 hits), so x
+// is read from HBM once.  The kernel is bound by the fp32 FMA pipe
+// (T*E*d FMAs: 8.6 G for C2, 34 G for C4), so x is widened once per chunk and
+// each loaded router weight feeds RT_TPW FMAs.  Top-k is a warp-parallel
+// argmax (lane-local scan + shuffle reduction, ties to the lower index).
 #include "common.cuh"
 
 namespace cox {
 
-constexpr int RT_TPW = 4;   // tokens per warp (register-blocked)
-constexpr int RT_EG = 8;    // experts per register group
-constexpr int RT_WARPS = 8;
+constexpr int RT_TPW = 4;    // tokens per warp tile
+constexpr int RT_EG = 8;     // experts per warp tile
+constexpr int RT_WARPS = 8;  // warps per block
 
 template <typename XT>
-COX_DEV void load_x8(const XT* p, float (&f)[8]);
-
+struct XChunk;
 template <>
-COX_DEV void load_x8<__nv_bfloat16>(const __nv_bfloat16* p, float (&f)[8]) {
-  uint4 v = ld_nc_v4(p);
-  bf16x8_to_f32(v, f);
-}
+struct XChunk<__nv_bfloat16> {
+  uint4 v;
+  COX_DEV void load(const __nv_bfloat16* p) { v = ld_nc_v4(p); }
+  COX_DEV void zero() { v = make_uint4(0, 0, 0, 0); }
+  COX_DEV float get(int q) const {
+    const uint32_t w = q < 2 ? v.x : q < 4 ? v.y : q < 6 ? v.z : v.w;
+    return (q & 1) ? __uint_as_float(w & 0xFFFF0000u) : __uint_as_float(w << 16);
+  }
+};
 template <>
-COX_DEV void load_x8<float>(const float* p, float (&f)[8]) {
-  float4 a = __ldg(reinterpret_cast<const float4*>(p));
-  float4 b = __ldg(reinterpret_cast<const float4*>(p) + 1);
-  f[0] = a.x; f[1] = a.y; f[2] = a.z; f[3] = a.w;
-  f[4] = b.x; f[5] = b.y; f[6] = b.z; f[7] = b.w;
-}
+struct XChunk<float> {
+  float4 a, b;
+  COX_DEV void load(const float* p) {
+    a = __ldg(reinterpret_cast<const float4*>(p));
+    b = __ldg(reinterpret_cast<const float4*>(p) + 1);
+  }
+  COX_DEV void zero() { a = b = make_float4(0.f, 0.f, 0.f, 0.f); }
+  COX_DEV float get(int q) const {
+    switch (q) {
+      case 0: return a.x; case 1: return a.y; case 2: return a.z; case 3: return a.w;
+      case 4: return b.x; case 5: return b.y; case 6: return b.z; default: return b.w;
+    }
+  }
+};
 
+// Tokens per block = RT_TPW * (RT_WARPS / egn); egn in {1,2,4,8}: expert groups
+// handled concurrently by the warps of one block (E > 8*egn loops over passes).
 template <typename XT>
 __global__ void __launch_bounds__(RT_WARPS * 32, 2)
 router_topk_kernel(const XT* __restrict__ x, const float* __restrict__ wg, int T, int d, int E, int k, int mode,
-                   int32_t* __restrict__ idx, float* __restrict__ wout, int32_t* __restrict__ counts) {
-  extern __shared__ float s_logits[];  // [RT_WARPS][RT_TPW][E]
+                   int egn, int32_t* __restrict__ idx, float* __restrict__ wout, int32_t* __restrict__ counts) {
+  extern __shared__ float s_logits[];  // [tokens_per_block][E]
   __shared__ int s_hist[256];
+  __shared__ int s_sel[RT_WARPS][8];
+  __shared__ float s_selv[RT_WARPS][8];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ntg = RT_WARPS / egn;
+  const int tpb = RT_TPW * ntg;
+  const int tg = warp / egn, eg = warp % egn;
   for (int i = threadIdx.x; i < E; i += blockDim.x) s_hist[i] = 0;
   __syncthreads();
-  float* my_logits = s_logits + warp * RT_TPW * E;
 
-  const long n_groups = (T + RT_TPW - 1) / RT_TPW;
-  for (long tg = (long)blockIdx.x * RT_WARPS + warp; tg < n_groups; tg += (long)gridDim.x * RT_WARPS) {
-    const long t0 = tg * RT_TPW;
-    for (int e0 = 0; e0 < E; e0 += RT_EG) {
+  const long nblk = (T + tpb - 1) / tpb;
+  for (long blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
+    const long tb0 = blk * tpb;
+    const long t0 = tb0 + (long)tg * RT_TPW;
+    for (int e0 = eg * RT_EG; e0 < E; e0 += egn * RT_EG) {
       float acc[RT_TPW][RT_EG];
 #pragma unroll
       for (int t = 0; t < RT_TPW; ++t)
 #pragma unroll
         for (int e = 0; e < RT_EG; ++e) acc[t][e] = 0.0f;
       for (int s = 8 * lane; s < d; s += 256) {
-        float xv[RT_TPW][8];
+        float xv[RT_TPW][8];  // widened once per chunk (the FMA pipe is the bound)
 #pragma unroll
         for (int t = 0; t < RT_TPW; ++t) {
-          if (t0 + t < T) {
-            load_x8<XT>(x + (t0 + t) * (long)d + s, xv[t]);
-          } else {
+          XChunk<XT> c;
+          if (t0 + t < T)
+            c.load(x + (t0 + t) * (long)d + s);
+          else
+            c.zero();
 #pragma unroll
-            for (int q = 0; q < 8; ++q) xv[t][q] = 0.0f;
-          }
+          for (int q = 0; q < 8; ++q) xv[t][q] = c.get(q);
         }
 #pragma unroll
         for (int e = 0; e < RT_EG; ++e) {
           if (e0 + e < E) {
             const float4* wp = reinterpret_cast<const float4*>(wg + (long)(e0 + e) * d + s);
-            float4 wa = __ldg(wp), wb = __ldg(wp + 1);
+            const float4 wa = __ldg(wp), wb = __ldg(wp + 1);
             const float w8[8] = {wa.x, wa.y, wa.z, wa.w, wb.x, wb.y, wb.z, wb.w};
 #pragma unroll
             for (int t = 0; t < RT_TPW; ++t)
@@ -87,43 +115,58 @@ router_topk_kernel(const XT* __restrict__ x, const float* __restrict__ wg, int T
           float v = acc[t][e];
 #pragma unroll
           for (int off = 16; off >= 1; off >>= 1) v = __fadd_rn(v, __shfl_xor_sync(0xffffffffu, v, off));
-          if (lane == 0 && e0 + e < E) my_logits[t * E + e0 + e] = v;
+          if (lane == 0 && e0 + e < E) s_logits[(tg * RT_TPW + t) * E + e0 + e] = v;
         }
     }
-    __syncwarp();
-    if (lane < RT_TPW && t0 + lane < T) {
-      const float* lg = my_logits + lane * E;
-      const long t = t0 + lane;
-      uint32_t taken[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // up to 256 experts
-      int sel[8];
-      float selv[8];
+    __syncthreads();
+    // top-k: one warp per token, warp-parallel argmax (ties -> lower index)
+    for (int tl = warp; tl < tpb; tl += RT_WARPS) {
+      const long t = tb0 + tl;
+      if (t >= T) break;
+      const float* lg = s_logits + tl * E;
+      uint32_t taken = 0;  // bit i: expert lane + 32*i already selected (E <= 256)
       for (int j = 0; j < k; ++j) {
-        int best = -1;
         float bv = 0.0f;
-        for (int e = 0; e < E; ++e) {
-          if (taken[e >> 5] & (1u << (e & 31))) continue;
-          float v = lg[e];
-          if (best < 0 || v > bv) { best = e; bv = v; }
+        int bi = -1;
+        for (int i = 0; lane + 32 * i < E; ++i) {
+          const int e = lane + 32 * i;
+          if (taken & (1u << i)) continue;
+          const float v = lg[e];
+          if (bi < 0 || v > bv) { bv = v; bi = e; }
         }
-        taken[best >> 5] |= 1u << (best & 31);
-        sel[j] = best;
-        selv[j] = bv;
-        idx[t * k + j] = best;
-        atomicAdd(&s_hist[best], 1);
+#pragma unroll
+        for (int off = 16; off >= 1; off >>= 1) {
+          const float ov = __shfl_xor_sync(0xffffffffu, bv, off);
+          const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
+          const bool better = (oi >= 0) && (bi < 0 || ov > bv || (ov == bv && oi < bi));
+          if (better) { bv = ov; bi = oi; }
+        }
+        if ((bi & 31) == lane) taken |= 1u << (bi >> 5);
+        if (lane == 0) {
+          s_sel[warp][j] = bi;
+          s_selv[warp][j] = bv;
+        }
       }
-      const float m = selv[0];
-      float ssum = 0.0f;
-      if (mode == 0) {
-        for (int j = 0; j < k; ++j) ssum = __fadd_rn(ssum, expf(__fsub_rn(selv[j], m)));
-      } else {
-        for (int e = 0; e < E; ++e) ssum = __fadd_rn(ssum, expf(__fsub_rn(lg[e], m)));
+      __syncwarp();
+      if (lane == 0) {
+        const int* sel = s_sel[warp];
+        const float* selv = s_selv[warp];
+        const float m = selv[0];
+        float ssum = 0.0f;
+        if (mode == 0) {
+          for (int j = 0; j < k; ++j) ssum = __fadd_rn(ssum, expf(__fsub_rn(selv[j], m)));
+        } else {
+          for (int e = 0; e < E; ++e) ssum = __fadd_rn(ssum, expf(__fsub_rn(lg[e], m)));
+        }
+        for (int j = 0; j < k; ++j) {
+          idx[t * k + j] = sel[j];
+          wout[t * k + j] = __fdiv_rn(expf(__fsub_rn(selv[j], m)), ssum);
+          atomicAdd(&s_hist[sel[j]], 1);
+        }
       }
-      for (int j = 0; j < k; ++j) wout[t * k + j] = __fdiv_rn(expf(__fsub_rn(selv[j], m)), ssum);
-      (void)sel;
     }
-    __syncwarp();
+    __syncthreads();
   }
-  __syncthreads();
   for (int i = threadIdx.x; i < E; i += blockDim.x)
     if (s_hist[i]) atomicAdd(&counts[i], s_hist[i]);
 }
@@ -133,17 +176,24 @@ int launch_router(const void* x, int x_is_bf16, const float* wg, int T, int d, i
   cudaError_t err = cudaMemsetAsync(counts, 0, sizeof(int32_t) * E, s);
   if (err != cudaSuccess) return -2;
   if (T == 0) return 0;
-  const int threads = RT_WARPS * 32;
-  long groups = (T + RT_TPW - 1) / RT_TPW;
-  long blocks = (groups + RT_WARPS - 1) / RT_WARPS;
+  int groups = (E + RT_EG - 1) / RT_EG;
+  int egn = 1;
+  while (egn < groups && egn < RT_WARPS) egn <<= 1;
+  const int tpb = RT_TPW * (RT_WARPS / egn);
+  long blocks = (T + tpb - 1) / tpb;
   if (blocks > 148L * 16) blocks = 148L * 16;
-  size_t smem = sizeof(float) * RT_WARPS * RT_TPW * E;
-  if (x_is_bf16)
-    router_topk_kernel<__nv_bfloat16><<<(int)blocks, threads, smem, s>>>(
-        static_cast<const __nv_bfloat16*>(x), wg, T, d, E, k, mode, idx, w, counts);
-  else
-    router_topk_kernel<float><<<(int)blocks, threads, smem, s>>>(static_cast<const float*>(x), wg, T, d, E, k,
-                                                                 mode, idx, w, counts);
+  const size_t smem = sizeof(float) * (size_t)tpb * E;
+  if (x_is_bf16) {
+    if (smem > 48 * 1024)
+      cudaFuncSetAttribute(router_topk_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    router_topk_kernel<__nv_bfloat16><<<(int)blocks, RT_WARPS * 32, smem, s>>>(
+        static_cast<const __nv_bfloat16*>(x), wg, T, d, E, k, mode, egn, idx, w, counts);
+  } else {
+    if (smem > 48 * 1024)
+      cudaFuncSetAttribute(router_topk_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    router_topk_kernel<float><<<(int)blocks, RT_WARPS * 32, smem, s>>>(static_cast<const float*>(x), wg, T, d, E, k,
+                                                                       mode, egn, idx, w, counts);
+  }
   return cudaGetLastError() == cudaSuccess ? 0 : -2;
 }
 

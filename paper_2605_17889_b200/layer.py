@@ -122,17 +122,97 @@ class MoELayer:
         ops.grouped_down(b.shared_h, b.shared_offsets, [0], [self.wts.shared_w2], self.d, y=b.shared_y)
         return b.shared_y
 
-    def finish(self, b: StageBuffers, shared=None):
-        return ops.combine(b.y, b.dst, b.w, shared, out=b.out)
+    def finish(self, b: StageBuffers, shared=None, out=None):
+        return ops.combine(b.y, b.dst, b.w, shared, out=b.out if out is None else out)
 
-    def forward(self, x: torch.Tensor) -> torch.Tensor:
+    def forward(self, x: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
         if x.dtype != torch.bfloat16 or x.dim() != 2 or x.shape[1] != self.d:
             raise ValueError(f"x must be bf16 [T, {self.d}]")
         b = self.buffers(x.shape[0], x.device)
         self.route(x, b)
         self.experts(b)
         sh = self.shared_expert(x, b)
-        return self.finish(b, sh)
+        return self.finish(b, sh, out)
+
+    def capture(self, x_static: torch.Tensor):
+        """Capture one forward over `x_static` into a CUDA graph (launch-bound
+        small-T steps such as decode).  Returns (replay_fn, out_tensor); refill
+        x_static in place and call replay_fn() for each step."""
+        self.forward(x_static)  # allocate buffers / tensor maps outside capture
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            out = self.forward(x_static)
+        return g.replay, out
+
+    def forward_microbatched(self, x: torch.Tensor, m_tokens: int) -> torch.Tensor:
+        """Ablation (costmodel.expert_stage_time(coalesced=False), planner.py:309-366):
+        run the expert stage separately per micro-batch of `m_tokens` tokens, so
+        every micro-batch re-reads the expert weights and each expert sees only
+        its share of the micro-batch.  Same results; for measuring the cost of
+        NOT coalescing."""
+        T = x.shape[0]
+        out = torch.empty((T, self.d), dtype=self.out_dtype, device=x.device)
+        subs = {}
+        for s0 in range(0, T, m_tokens):
+            xs = x[s0:s0 + m_tokens]
+            n = xs.shape[0]
+            if n not in subs:
+                subs[n] = MoELayer(self.wts, self.k, "mixtral" if self.mode == 0 else "deepseek", self.tile_m,
+                                   self.out_dtype)
+            subs[n].forward(xs, out=out[s0:s0 + n])
+        return out
+
+    def run_host_batches(self, xs_host, outs_host) -> None:
+        """End-to-end serving loop over host batches (pinned memory).
+
+        Batch i's H2D copy (copy engine, own stream) overlaps batch i-1's expert
+        stage, and batch i's D2H copy overlaps batch i+1's stage: two device
+        input and two device output buffers, event-ordered.  Every batch still
+        crosses PCIe both ways; only the waiting is hidden.  Returns once all
+        work is enqueued; the current stream is ordered after the last copy."""
+        if len(xs_host) != len(outs_host):
+            raise ValueError("one output buffer per input batch")
+        if not xs_host:
+            return
+        dev = self.wts.w13.device
+        T = xs_host[0].shape[0]
+        comp = torch.cuda.current_stream(dev)
+        st = self._host_state(T, dev)
+        h2d, d2h, xin, yout = st["h2d"], st["d2h"], st["xin"], st["yout"]
+        in_free, out_done = st["in_free"], st["out_done"]
+        for i, xh in enumerate(xs_host):
+            slot = i % 2
+            with torch.cuda.stream(h2d):
+                if in_free[slot] is not None:
+                    h2d.wait_event(in_free[slot])
+                xin[slot].copy_(xh, non_blocking=True)
+                ready = torch.cuda.Event()
+                ready.record(h2d)
+            comp.wait_event(ready)
+            if out_done[slot] is not None:
+                comp.wait_event(out_done[slot])
+            self.forward(xin[slot], out=yout[slot])
+            ev_c = torch.cuda.Event()
+            ev_c.record(comp)
+            in_free[slot] = ev_c
+            with torch.cuda.stream(d2h):
+                d2h.wait_event(ev_c)
+                outs_host[i].copy_(yout[slot], non_blocking=True)
+                ev_o = torch.cuda.Event()
+                ev_o.record(d2h)
+                out_done[slot] = ev_o
+        comp.wait_stream(d2h)
+
+    def _host_state(self, T, dev):
+        st = getattr(self, "_hs", None)
+        if st is None or st["T"] != T:
+            st = {"T": T, "h2d": torch.cuda.Stream(dev), "d2h": torch.cuda.Stream(dev),
+                  "xin": [torch.empty((T, self.d), dtype=torch.bfloat16, device=dev) for _ in range(2)],
+                  "yout": [torch.empty((T, self.d), dtype=self.out_dtype, device=dev) for _ in range(2)],
+                  "in_free": [None, None], "out_done": [None, None]}
+            self._hs = st
+        return st
 
     __call__ = forward
 

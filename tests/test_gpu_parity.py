@@ -229,3 +229,17 @@ def test_ep_layer_single_rank_nccl_matches_moelayer():
         assert torch.equal(a, b)
     finally:
         dist.destroy_process_group()
+
+
+def test_run_host_batches_matches_forward():
+    T, d, ff, E, k = 2000, 512, 256, 8, 2
+    wts = make_layer_weights(E, d, ff, seed=0, device=DEV)
+    layer = MoELayer(wts, k)
+    xs = [make_tokens(T, d, seed=s, device=DEV) for s in (1, 2, 3)]
+    ref = [layer(x).clone() for x in xs]
+    xh = [x.cpu().pin_memory() for x in xs]
+    oh = [torch.empty((T, d), dtype=torch.bfloat16).pin_memory() for _ in xs]
+    layer.run_host_batches(xh, oh)
+    torch.cuda.synchronize()
+    for r, o in zip(ref, oh):
+        assert torch.equal(r.cpu(), o)
