@@ -405,10 +405,16 @@ def main():
         flops_k3 = 4.0 * T * k * d * ff
         flops_k4 = 2.0 * T * k * d * ff
         flops_layer = 6.0 * T * k * d * ff + 2.0 * T * d * E + (6.0 * T * d * shared_ff if shared_ff else 0.0)
+        traffic = None
+        tp = ROOT / "profiles" / "ncu_traffic.json"
+        if tp.exists() and args.config == "C2":
+            traffic = json.loads(tp.read_text()).get("grouped_gemm_kernel<0>", {}).get("dram_bytes_per_launch")
         if k3_ms:
             achieved = flops_k3 / (k3_ms / 1e3) / 1e12
             roof = {"kernel": "grouped_gemm_kernel<EPI_SWIGLU> (K3)", "bound": "tensor", "achieved": achieved,
-                    "peak": pk["bf16_sus"], "unit": "TFLOP/s", "frac": achieved / pk["bf16_sus"], "traffic": None,
+                    "peak": pk["bf16_sus"], "unit": "TFLOP/s", "frac": achieved / pk["bf16_sus"], "traffic": traffic,
+                    "traffic_note": "DRAM bytes per K3 launch from one ncu --set full capture (profiles/r01); "
+                                    "algorithmic A+B+h = 21.2 GB, A re-read once per 16-wide n-band",
                     "peak_kind": f"bf16_tflops_sustained ({pk['src']}); burst {pk['bf16']}", "k3_ms": k3_ms,
                     "k4_ms": k4_ms, "k4_tflops": flops_k4 / (k4_ms / 1e3) / 1e12}
         else:
