@@ -48,6 +48,7 @@ class CudaStage:
         self.w2 = [weights.w2[e] for e in self.local]
         self._ws = None
         self._h = None
+        self.profile_events = None
 
     def route_and_permute(self, x):
         idx, w, counts = ops.router_topk(x, self.w.wg, self.k, self.mode)
@@ -67,8 +68,17 @@ class CudaStage:
         if self._h is None or self._h.shape[0] < n:
             self._h = torch.empty((max(n, 1), self.ff), dtype=torch.bfloat16, device=rows.device)
         h = self._h[: max(n, 1)]
+        pe = self.profile_events
+        if pe:
+            pe["k3"][0].record()
         ops.grouped_swiglu(rows, seg_offsets, groups, w13, self.ff, h=h)
-        return ops.grouped_down(h, seg_offsets, groups, w2, self.d, y=out)
+        if pe:
+            pe["k3"][1].record()
+            pe["k4"][0].record()
+        y = ops.grouped_down(h, seg_offsets, groups, w2, self.d, y=out)
+        if pe:
+            pe["k4"][1].record()
+        return y
 
     def combine(self, y_back, dst, w):
         return ops.combine(y_back, dst, w)
@@ -78,11 +88,22 @@ class CudaStage:
 
 
 def _a2a(out: torch.Tensor, inp: torch.Tensor, out_rows, in_rows, group):
-    """Row all-to-all; rows are moved as int32 words (bf16/fp32 payloads alike)."""
+    """Row all-to-all; rows are moved as int32 words (bf16/fp32 payloads alike).
+
+    NCCL moves device rows directly over NVLink/NVSwitch.  Under gloo (CPU
+    tests, or several ranks sharing one GPU in tests) device rows are staged
+    through host memory."""
     w = inp.shape[1] * inp.element_size() // 4
-    o = out.view(torch.int32).view(-1, w) if out.numel() else out.view(torch.int32)
-    i = inp.view(torch.int32).view(-1, w) if inp.numel() else inp.view(torch.int32)
-    dist.all_to_all_single(o, i, [int(v) for v in out_rows], [int(v) for v in in_rows], group=group)
+    o = out.view(torch.int32).view(-1, w)
+    i = inp.view(torch.int32).view(-1, w)
+    oc = [int(v) for v in out_rows]
+    ic = [int(v) for v in in_rows]
+    if o.is_cuda and dist.get_backend(group) != "nccl":
+        oh = torch.empty(o.shape, dtype=o.dtype)
+        dist.all_to_all_single(oh, i.cpu(), oc, ic, group=group)
+        o.copy_(oh)
+    else:
+        dist.all_to_all_single(o, i, oc, ic, group=group)
 
 
 class EPMoELayer:
@@ -126,7 +147,13 @@ class EPMoELayer:
         idx, w, counts, dst, x_perm = self.stage.route_and_permute(x)
         # counts exchange: counts[e] for e owned by rank q go to rank q
         recv_counts = torch.empty_like(counts)
-        dist.all_to_all_single(recv_counts, counts, group=self.group)
+        if counts.is_cuda and dist.get_backend(self.group) != "nccl":
+            rc = torch.empty(counts.shape, dtype=counts.dtype)
+            dist.all_to_all_single(rc, counts.cpu(), group=self.group)
+            recv_counts.copy_(rc)
+        else:
+            dist.all_to_all_single(recv_counts, counts, group=self.group)
+        self.stage.profile_events = self.profile_events
         both = torch.cat([counts, recv_counts]).cpu()  # the one host sync per layer
         send_seg = both[: self.E].view(G, L)
         recv_seg = both[self.E:].view(G, L)  # [source rank, local expert]
