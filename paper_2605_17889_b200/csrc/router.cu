@@ -171,11 +171,169 @@ router_topk_kernel(const XT* __restrict__ x, const float* __restrict__ wg, int T
     if (s_hist[i]) atomicAdd(&counts[i], s_hist[i]);
 }
 
+// Staged variant for E > 8 (fine-grained MoE, e.g. C4: E=64, d=2048): the
+// block's 32-token x tile is copied once into shared memory (cp.async) and
+// reused by all E/8 expert-group passes; each warp owns 4 tokens x 8 experts.
+// Router weights stream through L1/L2 once per 32 tokens (vs once per 4).
+// Same canonical per-(t,e) summation order as router_topk_kernel.
+constexpr int RS_TB = 32;
+
+COX_DEV void cp_async16(uint32_t dst, const void* src, uint32_t src_bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(src_bytes) : "memory");
+}
+COX_DEV void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+__global__ void __launch_bounds__(RT_WARPS * 32, 1)
+router_topk_staged_kernel(const __nv_bfloat16* __restrict__ x, const float* __restrict__ wg, int T, int d, int E,
+                          int k, int mode, int32_t* __restrict__ idx, float* __restrict__ wout,
+                          int32_t* __restrict__ counts) {
+  extern __shared__ __align__(16) uint8_t rs_smem[];
+  __nv_bfloat16* sx = reinterpret_cast<__nv_bfloat16*>(rs_smem);                    // [RS_TB][d]
+  float* s_logits = reinterpret_cast<float*>(rs_smem + (size_t)RS_TB * d * 2);      // [RS_TB][E]
+  __shared__ int s_hist[256];
+  __shared__ int s_sel[RT_WARPS][8];
+  __shared__ float s_selv[RT_WARPS][8];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int i = threadIdx.x; i < E; i += blockDim.x) s_hist[i] = 0;
+  const int vec_per_row = d / 8;
+  const long nblk = (T + RS_TB - 1) / RS_TB;
+  for (long blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
+    const long tb0 = blk * RS_TB;
+    __syncthreads();  // previous block's readers of sx / s_logits are done
+    for (int i = threadIdx.x; i < RS_TB * vec_per_row; i += blockDim.x) {
+      const int row = i / vec_per_row, c = i - row * vec_per_row;
+      const bool ok = tb0 + row < T;
+      const __nv_bfloat16* src = x + (ok ? (tb0 + row) * (long)d + 8 * c : 0);
+      cp_async16(smem_u32(sx + (size_t)row * d + 8 * c), src, ok ? 16u : 0u);
+    }
+    cp_async_wait_all();
+    __syncthreads();
+    const int tl0 = warp * RT_TPW;
+    for (int e0 = 0; e0 < E; e0 += RT_EG) {
+      float acc[RT_TPW][RT_EG];
+#pragma unroll
+      for (int t = 0; t < RT_TPW; ++t)
+#pragma unroll
+        for (int e = 0; e < RT_EG; ++e) acc[t][e] = 0.0f;
+      // register double-buffering: chunk j+1's operands are in flight while chunk j's FMAs issue
+      uint4 xn[RT_TPW];
+      float4 wna[RT_EG], wnb[RT_EG];
+      auto load_chunk = [&](int s) {
+#pragma unroll
+        for (int t = 0; t < RT_TPW; ++t) xn[t] = *reinterpret_cast<const uint4*>(sx + (size_t)(tl0 + t) * d + s);
+#pragma unroll
+        for (int e = 0; e < RT_EG; ++e) {
+          const int ee = min(e0 + e, E - 1);
+          const float4* wp = reinterpret_cast<const float4*>(wg + (long)ee * d + s);
+          wna[e] = __ldg(wp);
+          wnb[e] = __ldg(wp + 1);
+        }
+      };
+      if (8 * lane < d) load_chunk(8 * lane);
+      for (int s = 8 * lane; s < d; s += 256) {
+        uint4 xc[RT_TPW];
+        float4 wca[RT_EG], wcb[RT_EG];
+#pragma unroll
+        for (int t = 0; t < RT_TPW; ++t) xc[t] = xn[t];
+#pragma unroll
+        for (int e = 0; e < RT_EG; ++e) {
+          wca[e] = wna[e];
+          wcb[e] = wnb[e];
+        }
+        if (s + 256 < d) load_chunk(s + 256);
+        float xv[RT_TPW][8];
+#pragma unroll
+        for (int t = 0; t < RT_TPW; ++t) bf16x8_to_f32(xc[t], xv[t]);
+#pragma unroll
+        for (int e = 0; e < RT_EG; ++e) {
+          const float w8[8] = {wca[e].x, wca[e].y, wca[e].z, wca[e].w, wcb[e].x, wcb[e].y, wcb[e].z, wcb[e].w};
+#pragma unroll
+          for (int t = 0; t < RT_TPW; ++t)
+#pragma unroll
+            for (int q = 0; q < 8; ++q) acc[t][e] = __fmaf_rn(xv[t][q], w8[q], acc[t][e]);
+        }
+      }
+#pragma unroll
+      for (int t = 0; t < RT_TPW; ++t)
+#pragma unroll
+        for (int e = 0; e < RT_EG; ++e) {
+          float v = acc[t][e];
+#pragma unroll
+          for (int off = 16; off >= 1; off >>= 1) v = __fadd_rn(v, __shfl_xor_sync(0xffffffffu, v, off));
+          if (lane == 0 && e0 + e < E) s_logits[(tl0 + t) * E + e0 + e] = v;
+        }
+    }
+    __syncthreads();
+    for (int tl = warp; tl < RS_TB; tl += RT_WARPS) {
+      const long t = tb0 + tl;
+      if (t >= T) break;
+      const float* lg = s_logits + tl * E;
+      uint32_t taken = 0;
+      for (int j = 0; j < k; ++j) {
+        float bv = 0.0f;
+        int bi = -1;
+        for (int i = 0; lane + 32 * i < E; ++i) {
+          const int e = lane + 32 * i;
+          if (taken & (1u << i)) continue;
+          const float v = lg[e];
+          if (bi < 0 || v > bv) { bv = v; bi = e; }
+        }
+#pragma unroll
+        for (int off = 16; off >= 1; off >>= 1) {
+          const float ov = __shfl_xor_sync(0xffffffffu, bv, off);
+          const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
+          const bool better = (oi >= 0) && (bi < 0 || ov > bv || (ov == bv && oi < bi));
+          if (better) { bv = ov; bi = oi; }
+        }
+        if ((bi & 31) == lane) taken |= 1u << (bi >> 5);
+        if (lane == 0) {
+          s_sel[warp][j] = bi;
+          s_selv[warp][j] = bv;
+        }
+      }
+      __syncwarp();
+      if (lane == 0) {
+        const int* sel = s_sel[warp];
+        const float* selv = s_selv[warp];
+        const float m = selv[0];
+        float ssum = 0.0f;
+        if (mode == 0) {
+          for (int j = 0; j < k; ++j) ssum = __fadd_rn(ssum, expf(__fsub_rn(selv[j], m)));
+        } else {
+          for (int e = 0; e < E; ++e) ssum = __fadd_rn(ssum, expf(__fsub_rn(lg[e], m)));
+        }
+        for (int j = 0; j < k; ++j) {
+          idx[t * k + j] = sel[j];
+          wout[t * k + j] = __fdiv_rn(expf(__fsub_rn(selv[j], m)), ssum);
+          atomicAdd(&s_hist[sel[j]], 1);
+        }
+      }
+      __syncwarp();
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < E; i += blockDim.x)
+    if (s_hist[i]) atomicAdd(&counts[i], s_hist[i]);
+}
+
 int launch_router(const void* x, int x_is_bf16, const float* wg, int T, int d, int E, int k, int mode, int32_t* idx,
                   float* w, int32_t* counts, cudaStream_t s) {
   cudaError_t err = cudaMemsetAsync(counts, 0, sizeof(int32_t) * E, s);
   if (err != cudaSuccess) return -2;
   if (T == 0) return 0;
+  const size_t staged_smem = (size_t)RS_TB * d * 2 + (size_t)RS_TB * E * 4;
+  if (x_is_bf16 && E > RT_EG && staged_smem <= 200 * 1024) {
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(router_topk_staged_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      attr = true;
+    }
+    long blocks = (T + RS_TB - 1) / RS_TB;
+    if (blocks > 148L * 8) blocks = 148L * 8;
+    router_topk_staged_kernel<<<(int)blocks, RT_WARPS * 32, staged_smem, s>>>(
+        static_cast<const __nv_bfloat16*>(x), wg, T, d, E, k, mode, idx, w, counts);
+    return cudaGetLastError() == cudaSuccess ? 0 : -2;
+  }
   int groups = (E + RT_EG - 1) / RT_EG;
   int egn = 1;
   while (egn < groups && egn < RT_WARPS) egn <<= 1;
