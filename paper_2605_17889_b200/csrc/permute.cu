@@ -11,9 +11,9 @@
 //   2. perm_scan    — per-expert exclusive scan over blocks (one warp per
 //                     expert, shuffle scan) and the padded segment offsets;
 //   3. perm_scatter — in-block ranks from warp ballots (lane = token, so
-//                     popc(ballot & lanemask_lt) is the ascending-token rank),
-//                     then each token row is read ONCE (16 B vector loads) and
-//                     written to its k destinations.
+//                     popc(ballot & lanemask_lt) is the ascending-token rank);
+//   4. perm_copy    — grid-wide, one warp per token: each row is read ONCE
+//                     (16 B vector loads) and written to its k destinations.
 #include "common.cuh"
 
 namespace cox {
@@ -71,8 +71,7 @@ __global__ void __launch_bounds__(1024) perm_scan(const int32_t* __restrict__ bl
 __global__ void __launch_bounds__(PM_TB) perm_scatter(const int32_t* __restrict__ idx, int T, int k, int E,
                                                        const int32_t* __restrict__ block_base,
                                                        const int32_t* __restrict__ offsets,
-                                                       const __nv_bfloat16* __restrict__ x, int d,
-                                                       int32_t* __restrict__ dst, __nv_bfloat16* __restrict__ x_perm) {
+                                                       int32_t* __restrict__ dst) {
   __shared__ int s_wcnt[PM_TB / 32][256];
   __shared__ int s_wbase[PM_TB / 32][256];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -111,20 +110,25 @@ __global__ void __launch_bounds__(PM_TB) perm_scatter(const int32_t* __restrict_
     dj[j] = (ej[j] >= 0) ? s_wbase[warp][ej[j]] + rj[j] : -1;
     if (j < k && valid) dst[t * k + j] = dj[j];
   }
-  // Row copies: the warp walks its 32 tokens; each row is read once, written k times.
-  const long tw0 = (long)blockIdx.x * PM_TB + warp * 32;
-  for (int i = 0; i < 32; ++i) {
-    const long ti = tw0 + i;
-    if (ti >= T) break;
+}
+
+// Row copies, grid-wide: one warp per token; each row is read once (16 B
+// vectors, 4 chunks in flight per lane) and written to its k destinations.
+__global__ void __launch_bounds__(256) perm_copy(const int32_t* __restrict__ dst, int T, int k,
+                                                 const __nv_bfloat16* __restrict__ x, int d,
+                                                 __nv_bfloat16* __restrict__ x_perm) {
+  const int lane = threadIdx.x & 31;
+  const long nwarps = (long)gridDim.x * (blockDim.x >> 5);
+  for (long t = (long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); t < T; t += nwarps) {
     int di[8];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) di[j] = __shfl_sync(0xffffffffu, dj[j], i);
-    const __nv_bfloat16* src = x + ti * (long)d;
+    for (int j = 0; j < 8; ++j) di[j] = j < k ? dst[t * k + j] : 0;
+    const __nv_bfloat16* src = x + t * (long)d;
     for (int c0 = lane * 8; c0 < d; c0 += 32 * 8 * 4) {
       uint4 v[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
-        int c = c0 + u * 256;
+        const int c = c0 + u * 256;
         if (c < d) v[u] = ld_nc_v4(src + c);
       }
 #pragma unroll
@@ -132,7 +136,7 @@ __global__ void __launch_bounds__(PM_TB) perm_scatter(const int32_t* __restrict_
         if (j >= k) break;
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-          int c = c0 + u * 256;
+          const int c = c0 + u * 256;
           if (c < d) *reinterpret_cast<uint4*>(x_perm + (long)di[j] * d + c) = v[u];
         }
       }
@@ -169,9 +173,11 @@ int launch_permute(const int32_t* idx, int T, int k, int E, int tile_m, const vo
   }
   perm_hist<<<(int)nb, PM_TB, 0, s>>>(idx, T, k, E, block_counts);
   perm_scan<<<1, 1024, 0, s>>>(block_counts, (int)nb, E, tile_m, block_base, offsets, seg_counts);
-  perm_scatter<<<(int)nb, PM_TB, 0, s>>>(idx, T, k, E, block_base, offsets,
-                                          static_cast<const __nv_bfloat16*>(x), d, dst,
-                                          static_cast<__nv_bfloat16*>(x_perm));
+  perm_scatter<<<(int)nb, PM_TB, 0, s>>>(idx, T, k, E, block_base, offsets, dst);
+  long cb = (T + 7) / 8;
+  if (cb > 148L * 16) cb = 148L * 16;
+  perm_copy<<<(int)cb, 256, 0, s>>>(dst, T, k, static_cast<const __nv_bfloat16*>(x), d,
+                                    static_cast<__nv_bfloat16*>(x_perm));
   if (tile_m > 1) perm_zero_pad<<<dim3(8, E), 256, 0, s>>>(offsets, seg_counts, E, d, static_cast<__nv_bfloat16*>(x_perm));
   return cudaGetLastError() == cudaSuccess ? 0 : -2;
 }

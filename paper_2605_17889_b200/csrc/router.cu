@@ -58,7 +58,7 @@ struct XChunk<float> {
 
 // Tokens per block = RT_TPW * (RT_WARPS / egn); egn in {1,2,4,8}: expert groups
 // handled concurrently by the warps of one block (E > 8*egn loops over passes).
-template <typename XT>
+template <typename XT, int TPW>
 __global__ void __launch_bounds__(RT_WARPS * 32, 2)
 router_topk_kernel(const XT* __restrict__ x, const float* __restrict__ wg, int T, int d, int E, int k, int mode,
                    int egn, int32_t* __restrict__ idx, float* __restrict__ wout, int32_t* __restrict__ counts) {
@@ -68,7 +68,7 @@ router_topk_kernel(const XT* __restrict__ x, const float* __restrict__ wg, int T
   __shared__ float s_selv[RT_WARPS][8];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ntg = RT_WARPS / egn;
-  const int tpb = RT_TPW * ntg;
+  const int tpb = TPW * ntg;
   const int tg = warp / egn, eg = warp % egn;
   for (int i = threadIdx.x; i < E; i += blockDim.x) s_hist[i] = 0;
   __syncthreads();
@@ -76,17 +76,17 @@ router_topk_kernel(const XT* __restrict__ x, const float* __restrict__ wg, int T
   const long nblk = (T + tpb - 1) / tpb;
   for (long blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
     const long tb0 = blk * tpb;
-    const long t0 = tb0 + (long)tg * RT_TPW;
+    const long t0 = tb0 + (long)tg * TPW;
     for (int e0 = eg * RT_EG; e0 < E; e0 += egn * RT_EG) {
-      float acc[RT_TPW][RT_EG];
+      float acc[TPW][RT_EG];
 #pragma unroll
-      for (int t = 0; t < RT_TPW; ++t)
+      for (int t = 0; t < TPW; ++t)
 #pragma unroll
         for (int e = 0; e < RT_EG; ++e) acc[t][e] = 0.0f;
       for (int s = 8 * lane; s < d; s += 256) {
-        float xv[RT_TPW][8];  // widened once per chunk (the FMA pipe is the bound)
+        float xv[TPW][8];  // widened once per chunk (the FMA pipe is the bound)
 #pragma unroll
-        for (int t = 0; t < RT_TPW; ++t) {
+        for (int t = 0; t < TPW; ++t) {
           XChunk<XT> c;
           if (t0 + t < T)
             c.load(x + (t0 + t) * (long)d + s);
@@ -102,20 +102,20 @@ router_topk_kernel(const XT* __restrict__ x, const float* __restrict__ wg, int T
             const float4 wa = __ldg(wp), wb = __ldg(wp + 1);
             const float w8[8] = {wa.x, wa.y, wa.z, wa.w, wb.x, wb.y, wb.z, wb.w};
 #pragma unroll
-            for (int t = 0; t < RT_TPW; ++t)
+            for (int t = 0; t < TPW; ++t)
 #pragma unroll
               for (int q = 0; q < 8; ++q) acc[t][e] = __fmaf_rn(xv[t][q], w8[q], acc[t][e]);
           }
         }
       }
 #pragma unroll
-      for (int t = 0; t < RT_TPW; ++t)
+      for (int t = 0; t < TPW; ++t)
 #pragma unroll
         for (int e = 0; e < RT_EG; ++e) {
           float v = acc[t][e];
 #pragma unroll
           for (int off = 16; off >= 1; off >>= 1) v = __fadd_rn(v, __shfl_xor_sync(0xffffffffu, v, off));
-          if (lane == 0 && e0 + e < E) s_logits[(tg * RT_TPW + t) * E + e0 + e] = v;
+          if (lane == 0 && e0 + e < E) s_logits[(tg * TPW + t) * E + e0 + e] = v;
         }
     }
     __syncthreads();
@@ -322,7 +322,7 @@ int launch_router(const void* x, int x_is_bf16, const float* wg, int T, int d, i
   if (err != cudaSuccess) return -2;
   if (T == 0) return 0;
   const size_t staged_smem = (size_t)RS_TB * d * 2 + (size_t)RS_TB * E * 4;
-  if (x_is_bf16 && E > RT_EG && staged_smem <= 200 * 1024) {
+  if (x_is_bf16 && E > RT_EG && staged_smem <= 200 * 1024 && (long)T >= 148L * RS_TB) {
     static bool attr = false;
     if (!attr) {
       cudaFuncSetAttribute(router_topk_staged_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
@@ -337,21 +337,22 @@ int launch_router(const void* x, int x_is_bf16, const float* wg, int T, int d, i
   int groups = (E + RT_EG - 1) / RT_EG;
   int egn = 1;
   while (egn < groups && egn < RT_WARPS) egn <<= 1;
-  const int tpb = RT_TPW * (RT_WARPS / egn);
+  // Small batches (decode): one token per warp tile so that T*E/8 warps exist.
+  const bool small = (long)T * egn < 148L * 16 * RT_TPW;
+  const int tpw = small ? 1 : RT_TPW;
+  const int tpb = tpw * (RT_WARPS / egn);
   long blocks = (T + tpb - 1) / tpb;
   if (blocks > 148L * 16) blocks = 148L * 16;
   const size_t smem = sizeof(float) * (size_t)tpb * E;
+#define RT_LAUNCH(XT, TP) \
+  router_topk_kernel<XT, TP><<<(int)blocks, RT_WARPS * 32, smem, s>>>(static_cast<const XT*>(x), wg, T, d, E, k, \
+                                                                      mode, egn, idx, w, counts)
   if (x_is_bf16) {
-    if (smem > 48 * 1024)
-      cudaFuncSetAttribute(router_topk_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    router_topk_kernel<__nv_bfloat16><<<(int)blocks, RT_WARPS * 32, smem, s>>>(
-        static_cast<const __nv_bfloat16*>(x), wg, T, d, E, k, mode, egn, idx, w, counts);
+    if (small) RT_LAUNCH(__nv_bfloat16, 1); else RT_LAUNCH(__nv_bfloat16, RT_TPW);
   } else {
-    if (smem > 48 * 1024)
-      cudaFuncSetAttribute(router_topk_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    router_topk_kernel<float><<<(int)blocks, RT_WARPS * 32, smem, s>>>(static_cast<const float*>(x), wg, T, d, E, k,
-                                                                       mode, egn, idx, w, counts);
+    if (small) RT_LAUNCH(float, 1); else RT_LAUNCH(float, RT_TPW);
   }
+#undef RT_LAUNCH
   return cudaGetLastError() == cudaSuccess ? 0 : -2;
 }
 
