@@ -314,9 +314,32 @@ def main():
 
     wts = make_layer_weights(E, d, ff, seed=0, device=dev, shared_ff=shared_ff)
     x = make_tokens(T, d, seed=1 + rank, device=dev)
+    ep_used = None
     if ws > 1:
-        from paper_2605_17889_b200.ep import EPMoELayer
-        layer = EPMoELayer(wts, k, mode, dist.group.WORLD)
+        from paper_2605_17889_b200.ep import EPMoELayer, FusedEPMoELayer
+        want = os.environ.get("COX_EP", "auto")  # auto | fused | nccl
+        layer = None
+        if want in ("auto", "fused"):
+            # probe: the fused peer-memory path must agree bit-for-bit with the NCCL path
+            try:
+                px = x[: min(T, 8192)].contiguous()
+                a = EPMoELayer(wts, k, mode, dist.group.WORLD)(px).clone()
+                probe = FusedEPMoELayer(wts, k, mode, dist.group.WORLD)
+                b = probe(px).clone()
+                probe.check()
+                ok = torch.tensor([int(torch.equal(a, b))], device=dev)
+                dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+                del probe
+                if ok.item() == 1:
+                    layer = FusedEPMoELayer(wts, k, mode, dist.group.WORLD)
+                    ep_used = "fused NVLink peer-memory dispatch/combine (probe == NCCL path)"
+                else:
+                    ep_used = "nccl all_to_all (fused probe mismatch)"
+            except Exception as exc:  # noqa: BLE001
+                ep_used = f"nccl all_to_all (fused unavailable: {type(exc).__name__})"
+        if layer is None:
+            layer = EPMoELayer(wts, k, mode, dist.group.WORLD)
+            ep_used = ep_used or "nccl all_to_all"
     else:
         layer = MoELayer(wts, k, mode)
     stream = torch.cuda.current_stream()
@@ -446,6 +469,7 @@ def main():
             "dtype": "bf16", "data": "synthetic (seeded N(0,1) tokens, nn.Linear-style U(+-1/sqrt(fan_in)) weights)",
             "config": {"workload": desc + desc_mb, "tokens_per_gpu": T, "global_batch_tokens": T * ws, "d": d, "ff": ff,
                        "E": E, "k": k, "routing": mode, "parallelism": f"ep{ws}" if ws > 1 else "single",
+                       "ep_path": ep_used,
                        "l2": "inputs > L2 (x 2.1 GB, x_perm 4.3 GB, h 15 GB vs 126 MB L2); no flush"},
             "layer_tflops": flops_layer / (ms_step / 1e3) / 1e12,
             "frac_layer_of_bf16_sustained": flops_layer / (ms_step / 1e3) / 1e12 / pk["bf16_sus"],
@@ -459,6 +483,8 @@ def main():
         }
         print(json.dumps(line), flush=True)
     if ws > 1:
+        if hasattr(layer, "check"):
+            layer.check()
         dist.destroy_process_group()
 
 

@@ -67,7 +67,9 @@ int cox_router_topk(const void* x, int x_dtype, const float* wg, int T, int d, i
  *   offsets  [E+1]  int32 segment starts (segments padded to tile_m rows)
  *   dst      [T, k] int32 row of x_perm that holds (t, j)
  *   x_perm   [rows_cap, d] bf16, rows_cap >= T*k + E*(tile_m-1)
- *   workspace of cox_permute_workspace_bytes(T, E) bytes. */
+ *   workspace of cox_permute_workspace_bytes(T, E) bytes.
+ * x_perm == NULL: compute offsets and dst only (the fused EP dispatch moves
+ * the rows itself). */
 size_t cox_permute_workspace_bytes(int T, int E);
 int cox_permute(const int32_t* idx, int T, int k, int E, int tile_m, const void* x, int d, int32_t* offsets,
                 int32_t* dst, void* x_perm, long long rows_cap, void* workspace, void* stream);
@@ -93,6 +95,30 @@ int cox_grouped_down(const void* h, long long rows_cap, const int32_t* offsets, 
  * out/shared dtype = out_dtype (bf16 or fp32). */
 int cox_combine(const void* y_perm, const int32_t* dst, const float* w, int T, int k, int d, const void* shared_out,
                 void* out, int out_dtype, void* stream);
+
+/* K7' — fused expert-parallel dispatch/combine over NVLink peer memory
+ * (replaces the NCCL all-to-all pair of the EP path; see csrc/ep.cu).  Rank r
+ * of `world` owns experts [r*E/world, (r+1)*E/world).  Pointer tables are
+ * DEVICE arrays of `world` peer addresses (e.g. CUDA symmetric memory).
+ *   cox_ep_counts_put: counts[E] -> counts_all[rank][E] on every peer.
+ *   cox_ep_offsets:    counts_all[world][E] -> my receive segments
+ *                      recv_seg[world*E/world + 1] ((source, local expert)
+ *                      order) and send_base[E] (row of my first pair of
+ *                      expert e on its owner); overflow[0] = 1 if any owner
+ *                      would receive more than cap rows.
+ *   cox_ep_dispatch:   stores x[t] into the owners' receive buffers at
+ *                      send_base[e] + (dst_local - offsets_local[e]);
+ *                      route_row[T,k] records the row for the combine.
+ *   cox_ep_combine:    out[t] = sum_j w[t,j] * y_owner[route_row[t,j]] (bf16).
+ * dst_local/offsets_local come from cox_permute (x_perm may be NULL then). */
+int cox_ep_counts_put(const int32_t* counts, int E, int rank, int world, int32_t* const* peer_counts, void* stream);
+int cox_ep_offsets(const int32_t* counts_all, int world, int E, int rank, long long cap, int32_t* recv_seg,
+                   int32_t* send_base, int32_t* overflow, void* stream);
+int cox_ep_dispatch(const int32_t* idx, const int32_t* dst_local, const int32_t* offsets_local,
+                    const int32_t* send_base, int T, int k, int E, int world, long long cap, const void* x, int d,
+                    void* const* peer_recv, int32_t* route_row, void* stream);
+int cox_ep_combine(const int32_t* idx, const int32_t* route_row, const float* w, int T, int k, int d, int E,
+                   int world, const void* const* peer_y, void* out, void* stream);
 
 /* Layout helper: interleave W1 [ff, d] and W3 [ff, d] (bf16, device) into the
  * K3 layout [2*ff, d] (device).  ff % 128 == 0. */

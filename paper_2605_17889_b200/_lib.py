@@ -30,6 +30,7 @@ ROUTE_DEEPSEEK = 1
 EXPORTS = (
     "cox_last_error", "cox_version", "cox_device_check", "cox_router_topk", "cox_permute_workspace_bytes",
     "cox_permute", "cox_grouped_swiglu", "cox_grouped_down", "cox_combine", "cox_interleave_w13",
+    "cox_ep_counts_put", "cox_ep_offsets", "cox_ep_dispatch", "cox_ep_combine",
 )
 
 _lock = threading.Lock()
@@ -64,6 +65,16 @@ def _declare(L):
     L.cox_combine.restype = c_int
     L.cox_combine.argtypes = [c_void_p, c_void_p, c_void_p, c_int, c_int, c_int, c_void_p, c_void_p, c_int,
                               c_void_p]
+    L.cox_ep_counts_put.restype = c_int
+    L.cox_ep_counts_put.argtypes = [c_void_p, c_int, c_int, c_int, c_void_p, c_void_p]
+    L.cox_ep_offsets.restype = c_int
+    L.cox_ep_offsets.argtypes = [c_void_p, c_int, c_int, c_int, c_ll, c_void_p, c_void_p, c_void_p, c_void_p]
+    L.cox_ep_dispatch.restype = c_int
+    L.cox_ep_dispatch.argtypes = [c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_int, c_int, c_int, c_ll,
+                                  c_void_p, c_int, c_void_p, c_void_p, c_void_p]
+    L.cox_ep_combine.restype = c_int
+    L.cox_ep_combine.argtypes = [c_void_p, c_void_p, c_void_p, c_int, c_int, c_int, c_int, c_int, c_void_p,
+                                 c_void_p, c_void_p]
     L.cox_interleave_w13.restype = c_int
     L.cox_interleave_w13.argtypes = [c_void_p, c_void_p, c_int, c_int, c_void_p, c_void_p]
 

@@ -19,6 +19,16 @@ int launch_grouped_gemm(int epi, const void* A, long long rows_cap, int K, const
 int launch_combine(const void* y_perm, const int32_t* dst, const float* w, int T, int k, int d, const void* shared,
                    void* out, int out_is_bf16, cudaStream_t s);
 
+int launch_ep_counts_put(const int32_t* counts, int E, int rank, int world, int32_t* const* peer_counts,
+                         cudaStream_t s);
+int launch_ep_offsets(const int32_t* counts_all, int G, int E, int rank, long long cap, int32_t* recv_seg,
+                      int32_t* send_base, int32_t* overflow, cudaStream_t s);
+int launch_ep_dispatch(const int32_t* idx, const int32_t* dst_local, const int32_t* offsets_local,
+                       const int32_t* send_base, int T, int k, int L, long long cap, const void* x, int d,
+                       void* const* peer_recv, int32_t* route_row, cudaStream_t s);
+int launch_ep_combine(const int32_t* idx, const int32_t* route_row, const float* w, int T, int k, int d, int L,
+                      const void* const* peer_y, void* out, cudaStream_t s);
+
 __global__ void interleave_w13_kernel(const uint4* __restrict__ w1, const uint4* __restrict__ w3, int ff, int d,
                                       uint4* __restrict__ w13) {
   // row r of w13: block b = r / 128; source = (b even ? w1 : w3), row (b/2)*128 + r%128
@@ -96,7 +106,8 @@ int cox_permute(const int32_t* idx, int T, int k, int E, int tile_m, const void*
   if (rows_cap < (long long)T * k + (long long)E * (tile_m - 1))
     return fail(COX_EINVAL, "cox_permute: rows_cap %lld < T*k + E*(tile_m-1) = %lld", rows_cap,
                 (long long)T * k + (long long)E * (tile_m - 1));
-  if (!aligned16(x) || !aligned16(x_perm)) return fail(COX_EINVAL, "cox_permute: x/x_perm must be 16-byte aligned");
+  if (!aligned16(x) || (x_perm && !aligned16(x_perm)))
+    return fail(COX_EINVAL, "cox_permute: x/x_perm must be 16-byte aligned");
   if (!workspace || !offsets) return fail(COX_EINVAL, "cox_permute: null workspace/offsets");
   int rc = cox::launch_permute(idx, T, k, E, tile_m, x, d, offsets, dst, x_perm, workspace,
                                static_cast<cudaStream_t>(stream));
@@ -145,6 +156,49 @@ int cox_combine(const void* y_perm, const int32_t* dst, const float* w, int T, i
   int rc = cox::launch_combine(y_perm, dst, w, T, k, d, shared_out, out, out_dtype == COX_DTYPE_BF16,
                                static_cast<cudaStream_t>(stream));
   return cuda_status(rc, "cox_combine");
+}
+
+static int check_ep(const char* fn, int E, int world, int rank) {
+  if (world < 1 || E < 1 || E % world || rank < 0 || rank >= world || E > 256)
+    return fail(COX_EINVAL, "%s: need 1 <= world, E %% world == 0, 0 <= rank < world, E <= 256", fn);
+  return 0;
+}
+
+int cox_ep_counts_put(const int32_t* counts, int E, int rank, int world, int32_t* const* peer_counts, void* stream) {
+  if (int rc = check_ep("cox_ep_counts_put", E, world, rank)) return rc;
+  if (!counts || !peer_counts) return fail(COX_EINVAL, "cox_ep_counts_put: null pointer");
+  return cuda_status(cox::launch_ep_counts_put(counts, E, rank, world, peer_counts, static_cast<cudaStream_t>(stream)),
+                     "cox_ep_counts_put");
+}
+
+int cox_ep_offsets(const int32_t* counts_all, int world, int E, int rank, long long cap, int32_t* recv_seg,
+                   int32_t* send_base, int32_t* overflow, void* stream) {
+  if (int rc = check_ep("cox_ep_offsets", E, world, rank)) return rc;
+  if (cap < 1) return fail(COX_EINVAL, "cox_ep_offsets: cap < 1");
+  return cuda_status(cox::launch_ep_offsets(counts_all, world, E, rank, cap, recv_seg, send_base, overflow,
+                                            static_cast<cudaStream_t>(stream)),
+                     "cox_ep_offsets");
+}
+
+int cox_ep_dispatch(const int32_t* idx, const int32_t* dst_local, const int32_t* offsets_local,
+                    const int32_t* send_base, int T, int k, int E, int world, long long cap, const void* x, int d,
+                    void* const* peer_recv, int32_t* route_row, void* stream) {
+  if (int rc = check_ep("cox_ep_dispatch", E, world, 0)) return rc;
+  if (T < 0 || k < 1 || k > 8 || d <= 0 || d % 8) return fail(COX_EINVAL, "cox_ep_dispatch: need 1<=k<=8, d%%8==0");
+  if (!aligned16(x)) return fail(COX_EINVAL, "cox_ep_dispatch: x must be 16-byte aligned");
+  return cuda_status(cox::launch_ep_dispatch(idx, dst_local, offsets_local, send_base, T, k, E / world, cap, x, d,
+                                             peer_recv, route_row, static_cast<cudaStream_t>(stream)),
+                     "cox_ep_dispatch");
+}
+
+int cox_ep_combine(const int32_t* idx, const int32_t* route_row, const float* w, int T, int k, int d, int E,
+                   int world, const void* const* peer_y, void* out, void* stream) {
+  if (int rc = check_ep("cox_ep_combine", E, world, 0)) return rc;
+  if (T < 0 || k < 1 || k > 8 || d <= 0 || d % 8) return fail(COX_EINVAL, "cox_ep_combine: need 1<=k<=8, d%%8==0");
+  if (!aligned16(out)) return fail(COX_EINVAL, "cox_ep_combine: out must be 16-byte aligned");
+  return cuda_status(cox::launch_ep_combine(idx, route_row, w, T, k, d, E / world, peer_y, out,
+                                            static_cast<cudaStream_t>(stream)),
+                     "cox_ep_combine");
 }
 
 int cox_interleave_w13(const void* w1, const void* w3, int ff, int d, void* w13, void* stream) {

@@ -174,3 +174,133 @@ class EPMoELayer:
         return self.stage.combine(yback, dst, w)
 
     __call__ = forward
+
+
+class SymmMemTransport:
+    """Peer-mapped buffers from CUDA symmetric memory + its stream-ordered barrier."""
+
+    def __init__(self, group):
+        self.group = group
+        self.hdl = None
+
+    def alloc(self, spec: dict, dev) -> dict:
+        """spec: name -> (shape, dtype); returns name -> (local tensor, device int64 [world] peer addresses)."""
+        import torch.distributed._symmetric_memory as symm
+        out = {}
+        for name, (shape, dtype) in spec.items():
+            t = symm.empty(shape, dtype=dtype, device=dev)
+            h = symm.rendezvous(t, self.group)
+            if self.hdl is None:
+                self.hdl = h
+            out[name] = (t, torch.tensor(list(h.buffer_ptrs), dtype=torch.int64, device=dev))
+        return out
+
+    def barrier(self) -> None:
+        self.hdl.barrier(channel=0, timeout_ms=120000)
+
+
+class FusedEPMoELayer:
+    """EP expert stage with dispatch/combine fused into kernels that store/load
+    token rows directly in the peers' memory (csrc/ep.cu) — no NCCL
+    all-to-all, no x_perm/y_back round trip through local HBM, no host sync
+    (the receive layout is computed on the device from all-gathered counts).
+
+    Buffers are CUDA symmetric memory (torch.distributed._symmetric_memory):
+    every rank maps every peer's receive buffer, output buffer and count
+    matrix; the symmetric-memory barrier (stream-ordered, system-scope
+    release/acquire on signal pads) separates the phases:
+        K1 route -> K2 ranks -> counts put -> barrier -> offsets + dispatch
+        -> barrier -> K3/K4 on received rows -> barrier -> fused combine.
+    The next layer's counts put is ordered after this combine on every rank,
+    so buffers are never overwritten while a peer still reads them.
+    """
+
+    def __init__(self, weights: LayerWeights, top_k: int, mode: str = "mixtral", group=None,
+                 capacity_factor: float = 1.25, transport=None):
+        if mode not in MODES:
+            raise ValueError(f"mode must be one of {sorted(MODES)}")
+        self.group = group if group is not None else dist.group.WORLD
+        self.transport = transport if transport is not None else SymmMemTransport(self.group)
+        self.G = dist.get_world_size(self.group)
+        self.rank = dist.get_rank(self.group)
+        self.E = weights.num_experts
+        if self.E % self.G:
+            raise ValueError(f"{self.E} experts cannot be sharded evenly over {self.G} ranks")
+        self.L = self.E // self.G
+        if self.G * self.L > 64:
+            raise ValueError("at most 64 (source, expert) groups per grouped GEMM")
+        self.k = int(top_k)
+        self.mode = MODES[mode]
+        self.w = weights
+        self.d = weights.hidden_dim
+        self.ff = weights.expert_dim
+        local = range(self.rank * self.L, (self.rank + 1) * self.L)
+        self.w13 = [weights.w13[e] for e in local]
+        self.w2 = [weights.w2[e] for e in local]
+        self.cap_factor = float(capacity_factor)
+        self._T = None
+        self.profile_events = None
+
+    @property
+    def launches_per_step(self) -> int:
+        return 1 + 3 + 1 + 1 + 1 + 2 + 1 + 3  # router, permute ranks, put, offsets, dispatch, K3/K4, combine, 3 barriers
+
+    def _setup(self, T: int, dev):
+        G, E, k, d = self.G, self.E, self.k, self.d
+        cap = int(T * k * self.cap_factor) + 256
+        self.cap = cap
+        bufs = self.transport.alloc({"recv": ((cap, d), torch.bfloat16), "y": ((cap, d), torch.bfloat16),
+                                     "counts": ((G, E), torch.int32)}, dev)
+        (self.recv, self.peer_recv), (self.ysym, self.peer_y), (self.counts_all, self.peer_counts) = \
+            bufs["recv"], bufs["y"], bufs["counts"]
+        i32 = dict(dtype=torch.int32, device=dev)
+        self.idx = torch.empty((T, k), **i32)
+        self.wts = torch.empty((T, k), dtype=torch.float32, device=dev)
+        self.counts = torch.empty((E,), **i32)
+        self.offsets = torch.empty((E + 1,), **i32)
+        self.dst = torch.empty((T, k), **i32)
+        self.route_row = torch.empty((T, k), **i32)
+        self.recv_seg = torch.empty((G * self.L + 1,), **i32)
+        self.send_base = torch.empty((E,), **i32)
+        self.overflow = torch.zeros((1,), **i32)
+        self.ws = torch.empty((max(16, ops.permute_workspace_bytes(T, E)),), dtype=torch.uint8, device=dev)
+        self.h = torch.empty((cap, self.ff), dtype=torch.bfloat16, device=dev)
+        self.out = torch.empty((T, d), dtype=torch.bfloat16, device=dev)
+        self._T = T
+
+    def _barrier(self):
+        self.transport.barrier()
+
+    def forward(self, x: torch.Tensor) -> torch.Tensor:
+        T = x.shape[0]
+        if self._T != T:
+            self._setup(T, x.device)
+        G, L = self.G, self.L
+        ops.router_topk(x, self.w.wg, self.k, self.mode, out=(self.idx, self.wts, self.counts))
+        ops.permute(self.idx, x, self.E, 1, out=(self.offsets, self.dst, None), workspace=self.ws, copy_rows=False)
+        ops.ep_counts_put(self.counts, self.rank, G, self.peer_counts)
+        self._barrier()
+        ops.ep_offsets(self.counts_all, self.rank, self.cap, self.recv_seg, self.send_base, self.overflow)
+        ops.ep_dispatch(self.idx, self.dst, self.offsets, self.send_base, x, G, self.cap, self.peer_recv,
+                        self.route_row)
+        self._barrier()
+        groups = list(range(G * L))
+        pe = self.profile_events
+        if pe:
+            pe["k3"][0].record()
+        ops.grouped_swiglu(self.recv, self.recv_seg, groups, [self.w13[g % L] for g in groups], self.ff, h=self.h)
+        if pe:
+            pe["k3"][1].record()
+            pe["k4"][0].record()
+        ops.grouped_down(self.h, self.recv_seg, groups, [self.w2[g % L] for g in groups], self.d, y=self.ysym)
+        if pe:
+            pe["k4"][1].record()
+        self._barrier()
+        return ops.ep_combine(self.idx, self.route_row, self.wts, self.E, G, self.peer_y, self.out)
+
+    __call__ = forward
+
+    def check(self) -> None:
+        """Raise if any owner's receive buffer overflowed (capacity_factor too small)."""
+        if self._T is not None and int(self.overflow.item()) != 0:
+            raise RuntimeError(f"EP receive capacity {self.cap} rows exceeded; raise capacity_factor")

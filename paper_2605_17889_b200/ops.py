@@ -81,8 +81,11 @@ def rows_capacity(T: int, k: int, E: int, tile_m: int = 1) -> int:
     return max(1, T * k + E * (tile_m - 1))
 
 
-def permute(idx: torch.Tensor, x: torch.Tensor, E: int, tile_m: int = 1, out=None, workspace=None, stream=None):
-    """K2: -> (offsets [E+1] int32, dst [T,k] int32, x_perm [rows_cap, d] bf16)."""
+def permute(idx: torch.Tensor, x: torch.Tensor, E: int, tile_m: int = 1, out=None, workspace=None, stream=None,
+            copy_rows: bool = True):
+    """K2: -> (offsets [E+1] int32, dst [T,k] int32, x_perm [rows_cap, d] bf16 or None).
+
+    copy_rows=False computes offsets/dst only (the fused EP dispatch moves the rows)."""
     _need(idx, "idx", torch.int32, 2)
     _need(x, "x", _BF16, 2)
     T, k = idx.shape
@@ -93,14 +96,17 @@ def permute(idx: torch.Tensor, x: torch.Tensor, E: int, tile_m: int = 1, out=Non
     if out is None:
         offsets = torch.empty((E + 1,), dtype=torch.int32, device=x.device)
         dst = torch.empty((T, k), dtype=torch.int32, device=x.device)
-        x_perm = torch.empty((cap, d), dtype=_BF16, device=x.device)
+        x_perm = torch.empty((cap, d), dtype=_BF16, device=x.device) if copy_rows else None
     else:
         offsets, dst, x_perm = out
+        if not copy_rows:
+            x_perm = None
     if workspace is None:
         workspace = torch.empty((permute_workspace_bytes(T, E),), dtype=torch.uint8, device=x.device)
     L = _lib.lib()
     _lib.check(L.cox_permute(idx.data_ptr(), T, k, E, tile_m, x.data_ptr(), d, offsets.data_ptr(), dst.data_ptr(),
-                             x_perm.data_ptr(), x_perm.shape[0], workspace.data_ptr(), _stream(stream)),
+                             x_perm.data_ptr() if x_perm is not None else None,
+                             x_perm.shape[0] if x_perm is not None else cap, workspace.data_ptr(), _stream(stream)),
                "cox_permute")
     return offsets, dst, x_perm
 
@@ -176,4 +182,37 @@ def interleave_w13(w1: torch.Tensor, w3: torch.Tensor, out: torch.Tensor | None 
     L = _lib.lib()
     _lib.check(L.cox_interleave_w13(w1.data_ptr(), w3.data_ptr(), ff, d, out.data_ptr(), _stream(stream)),
                "cox_interleave_w13")
+    return out
+
+
+# --------------------------------------------------------------------------- fused EP (K7')
+def ep_counts_put(counts: torch.Tensor, rank: int, world: int, peer_counts: torch.Tensor, stream=None):
+    """counts[E] -> counts_all[rank] on every peer (peer_counts: device int64 [world] addresses)."""
+    L = _lib.lib()
+    _lib.check(L.cox_ep_counts_put(counts.data_ptr(), counts.numel(), rank, world, peer_counts.data_ptr(),
+                                   _stream(stream)), "cox_ep_counts_put")
+
+
+def ep_offsets(counts_all: torch.Tensor, rank: int, cap: int, recv_seg, send_base, overflow, stream=None):
+    world, E = counts_all.shape
+    L = _lib.lib()
+    _lib.check(L.cox_ep_offsets(counts_all.data_ptr(), world, E, rank, cap, recv_seg.data_ptr(), send_base.data_ptr(),
+                                overflow.data_ptr(), _stream(stream)), "cox_ep_offsets")
+
+
+def ep_dispatch(idx, dst_local, offsets_local, send_base, x, world: int, cap: int, peer_recv, route_row,
+                stream=None):
+    T, k = idx.shape
+    E = send_base.numel()
+    L = _lib.lib()
+    _lib.check(L.cox_ep_dispatch(idx.data_ptr(), dst_local.data_ptr(), offsets_local.data_ptr(), send_base.data_ptr(),
+                                 T, k, E, world, cap, x.data_ptr(), x.shape[1], peer_recv.data_ptr(),
+                                 route_row.data_ptr(), _stream(stream)), "cox_ep_dispatch")
+
+
+def ep_combine(idx, route_row, w, E: int, world: int, peer_y, out, stream=None):
+    T, k = idx.shape
+    L = _lib.lib()
+    _lib.check(L.cox_ep_combine(idx.data_ptr(), route_row.data_ptr(), w.data_ptr(), T, k, out.shape[1], E, world,
+                                peer_y.data_ptr(), out.data_ptr(), _stream(stream)), "cox_ep_combine")
     return out
