@@ -1,0 +1,34 @@
+"""Small-shape run of every kernel for compute-sanitizer (memcheck / racecheck / synccheck).
+
+    compute-sanitizer --tool memcheck python tools/sanitize.py
+"""
+import sys
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+import torch  # noqa: E402
+
+from paper_2605_17889_b200.layer import MoELayer  # noqa: E402
+from paper_2605_17889_b200.synthetic import make_layer_weights, make_tokens  # noqa: E402
+
+
+def main():
+    dev = torch.device("cuda", 0)
+    for (T, d, ff, E, k, mode, shared) in [(300, 256, 256, 8, 2, "mixtral", 0), (97, 512, 128, 16, 6, "deepseek", 256),
+                                           (5000, 256, 128, 64, 6, "deepseek", 0)]:
+        wts = make_layer_weights(E, d, ff, seed=0, device=dev, shared_ff=shared)
+        x = make_tokens(T, d, seed=1, device=dev)
+        out = MoELayer(wts, k, mode)(x)
+        torch.cuda.synchronize()
+        assert torch.isfinite(out.float()).all()
+    # small-T router paths (fp32 input, 1-token warp tiles) and the staged router (E > 8, T >= 148*32)
+    from paper_2605_17889_b200 import ops
+    wg = torch.randn(64, 256, device=dev) / 16
+    ops.router_topk(make_tokens(5000, 256, device=dev), wg, 6, 1)
+    ops.router_topk(make_tokens(33, 256, device=dev, dtype=torch.float32), wg[:8].contiguous(), 2, 0)
+    torch.cuda.synchronize()
+    print("sanitize run ok")
+
+
+if __name__ == "__main__":
+    main()
