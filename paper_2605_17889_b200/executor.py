@@ -230,6 +230,29 @@ class StratifiedMoEStack:
         gpu = sum(r["dur"] for r in rec if r["res"] == "gpu") / n
         return ExpertStageParts(act_load=0.0, mig_load=mig, lat_gpu=gpu, lat_cpu=0.0, return_store=0.0)
 
+    # ------------------------------------------------------------ orchestrator bridge
+    def apply_strategy(self, strategy, model=None, activation_map=None) -> ResidencyPlan:
+        """Adopt the expert partition an orchestrator chose — a moeplan
+        `AllocationStrategy` or `Plan` (planner.plan, planner.py:246-272; its
+        `prefill_strategy` is used): exp_r experts per layer stay resident
+        (the hottest ones of `activation_map`, default: the calibration map),
+        exp_m are streamed; exp_c must be 0 (no CPU expert path)."""
+        strategy = getattr(strategy, "prefill_strategy", strategy)
+        total = strategy.exp_r + strategy.exp_m + strategy.exp_c
+        if total != self.E:
+            raise ValueError(f"expert partition {strategy.exp_r}+{strategy.exp_m}+{strategy.exp_c} "
+                             f"does not cover the {self.E} activated experts")
+        if strategy.exp_c != 0:
+            raise ValueError("the B200 executor runs every expert on the GPU: exp_c must be 0")
+        amap = activation_map if activation_map is not None else getattr(self, "calibration_map", None)
+        if amap is None:
+            from .config import ActivationMap
+            amap = ActivationMap.uniform(self.N, self.E)
+        plan = select_resident_experts(amap, strategy.exp_r)
+        self._bufs = None
+        self.set_residency(plan)
+        return plan
+
     # ------------------------------------------------------------ calibration
     def max_capacity(self, T: int, slack_bytes: int = 4 << 30) -> int:
         """Largest exp_r whose resident copies + the T-token activations + the

@@ -69,3 +69,17 @@ def test_calibration_picks_the_hot_experts():
     out = stack(x)
     torch.cuda.synchronize()
     assert torch.isfinite(out.float()).all()
+
+
+def test_apply_strategy_from_orchestrator():
+    from paper_2605_17889_b200.config import AllocationStrategy, Device
+    stack, pool, wg = _stack(ResidencyPlan(tuple(() for _ in range(N)), 0))
+    x = make_tokens(500, d, seed=5, device=DEV)
+    ref = stack(x).clone()
+    plan = stack.apply_strategy(AllocationStrategy((Device.GPU,) * 3, exp_r=5, exp_m=3, exp_c=0, m=4))
+    assert all(len(r) == 5 for r in plan.resident)
+    out = stack(x)
+    torch.cuda.synchronize()
+    assert torch.equal(ref, out)
+    with pytest.raises(ValueError):
+        stack.apply_strategy(AllocationStrategy((Device.GPU,) * 3, exp_r=4, exp_m=2, exp_c=2, m=4))

@@ -35,3 +35,26 @@ def test_residency_on_reference_map_and_trace(moeplan):
         counts = np.zeros((3, 16))
         np.add.at(counts, (trace.layer_idx, trace.expert_idx), trace.token_counts)
         assert eas.hit_ratio_from_counts(counts, plan) == pytest.approx(R.hit_ratio(trace, plan), abs=0, rel=1e-15)
+
+
+def test_planner_plan_drives_residency(moeplan):
+    """moeplan.planner.plan on a B200 system spec -> exp_r/exp_m -> our residency
+    selection (the executor's apply_strategy uses exactly this rule)."""
+    from moeplan.hardware import DeviceSpec, LinkSpec, SystemSpec
+    from moeplan.planner import PlanRequest, plan
+    from moeplan.workload import BatchConfig, ModelConfig
+    from moeplan.eas import ActivationMap
+    b2 = CM.b200_system()
+    system = SystemSpec(DeviceSpec("gpu", b2.gpu.mem_bandwidth, b2.gpu.peak_compute, b2.gpu.mem_capacity),
+                        DeviceSpec("cpu", 3e11, 2e12, 1e12), LinkSpec(55e9))
+    model = ModelConfig(56, 6144, 16384, 8, 2, 2)
+    amap = ActivationMap(np.random.default_rng(0).integers(1, 100, size=(56, 8)).astype(float))
+    p = plan(PlanRequest(system=system, model=model, batch=BatchConfig(64, 4096, 16), activation_map=amap))
+    s = p.prefill_strategy
+    assert s.exp_r + s.exp_m + s.exp_c == 8 and s.exp_r >= 1
+    ours = eas.select_resident_experts(amap, s.exp_r)
+    assert all(len(layer) == s.exp_r for layer in ours.resident)
+    # the hottest experts of every layer are the resident ones
+    for layer, res in enumerate(ours.resident):
+        order = np.argsort(-amap.counts[layer], kind="stable")[: s.exp_r]
+        assert set(res) == set(int(e) for e in order)
