@@ -272,3 +272,20 @@ def test_fused_ep_single_rank_matches_moelayer():
             assert torch.equal(a, b) and torch.equal(a, b2)
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("T,E,k", [(0, 8, 2), (1, 8, 2), (3, 4, 4), (50, 1, 1)])
+def test_layer_edge_cases(T, E, k):
+    """Empty batch, single token, k == E (every expert gets every token), one expert."""
+    d, ff = 256, 128
+    wts = make_layer_weights(E, d, ff, seed=2, device=DEV, keep_split=True)
+    x = make_tokens(max(T, 1), d, seed=3, device=DEV)[:T]
+    layer = MoELayer(wts, k)
+    out = layer(x)
+    torch.cuda.synchronize()
+    assert out.shape == (T, d)
+    if T:
+        f = lambda t: t.float().cpu().numpy()  # noqa: E731
+        ref = O.moe_layer(f(x), f(wts.wg), f(wts.w1), f(wts.w3), f(wts.w2), k, 0)
+        assert np.array_equal(layer.buffers(T, DEV).idx.cpu().numpy(), ref["idx"])
+        assert rel_l2(f(out), ref["out"]) <= 1e-2
