@@ -289,3 +289,30 @@ def test_layer_edge_cases(T, E, k):
         ref = O.moe_layer(f(x), f(wts.wg), f(wts.w1), f(wts.w3), f(wts.w2), k, 0)
         assert np.array_equal(layer.buffers(T, DEV).idx.cpu().numpy(), ref["idx"])
         assert rel_l2(f(out), ref["out"]) <= 1e-2
+
+
+@pytest.mark.parametrize("cfg", ["C3L", "C4"])
+def test_full_size_layer_slice_vs_oracle(cfg):
+    """Full-size C3-layer / C4 batches (262,144 tokens) through the GPU layer; the
+    fp32 oracle recomputes a 512-token slice with the full-size weights (the
+    coalesced per-expert GEMM of a row depends only on that row)."""
+    T, d, ff, E, k, mode, sff = {"C3L": (262144, 6144, 16384, 8, 2, "mixtral", 0),
+                                 "C4": (262144, 2048, 1408, 64, 6, "deepseek", 2816)}[cfg]
+    wts = make_layer_weights(E, d, ff, seed=0, device=DEV, shared_ff=sff)
+    x = make_tokens(T, d, seed=1, device=DEV)
+    layer = MoELayer(wts, k, mode)
+    out = layer(x)
+    torch.cuda.synchronize()
+    sl = slice(123456, 123456 + 512)
+    w1, w3 = split_w13(wts.w13)
+    f = lambda t: t.float().cpu().numpy()  # noqa: E731
+    shared = None
+    if sff:
+        s1, s3 = split_w13(wts.shared_w13)
+        shared = (f(s1), f(s3), f(wts.shared_w2))
+    ref = O.moe_layer(f(x[sl]), f(wts.wg), f(w1), f(w3), f(wts.w2), k, 0 if mode == "mixtral" else 1, shared=shared)
+    b = layer.buffers(T, DEV)
+    assert np.array_equal(b.idx[sl].cpu().numpy(), ref["idx"])
+    assert rel_l2(f(out[sl]), ref["out"]) <= 1e-2
+    counts = b.counts.cpu().numpy()
+    assert counts.sum() == T * k and np.array_equal(np.diff(b.offsets.cpu().numpy()), counts)
