@@ -16,7 +16,6 @@ own golden values (tests/test_reference_interop.py).
 from __future__ import annotations
 
 import ctypes
-import os
 import subprocess
 from pathlib import Path
 

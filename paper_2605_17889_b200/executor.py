@@ -32,7 +32,7 @@ from dataclasses import dataclass
 import numpy as np
 import torch
 
-from . import _lib, ops
+from . import ops
 from .config import ExpertStageParts, ResidencyPlan
 from .eas import Calibrator, select_resident_experts
 from .layer import MODES
@@ -318,4 +318,4 @@ def hit_ratio_of_counts(counts: np.ndarray, plan: ResidencyPlan) -> float:
     return hit_ratio_from_counts(counts, plan)
 
 
-__all__ = ["StratifiedMoEStack", "make_pool", "make_router_weights", "HostExpertPool", "hit_ratio_of_counts", "_lib"]
+__all__ = ["StratifiedMoEStack", "make_pool", "make_router_weights", "HostExpertPool", "hit_ratio_of_counts"]
