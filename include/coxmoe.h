@@ -85,10 +85,21 @@ int cox_permute(const int32_t* idx, int T, int k, int E, int tile_m, const void*
 int cox_grouped_swiglu(const void* x_perm, long long rows_cap, const int32_t* offsets, int n_groups,
                        const int32_t* group_experts, const void* const* w13, int d, int ff, void* h, void* stream);
 
+/* Same, with a CTA budget: the persistent kernel uses at most max_ctas SMs
+ * (even, >= 2; 0 = all), so that two grouped GEMMs can run concurrently on
+ * different streams (e.g. the shared expert beside the routed experts in a
+ * decode step). */
+int cox_grouped_swiglu_ex(const void* x_perm, long long rows_cap, const int32_t* offsets, int n_groups,
+                          const int32_t* group_experts, const void* const* w13, int d, int ff, void* h,
+                          int max_ctas, void* stream);
+
 /* K4 — grouped down projection: y_perm[r] = h[r] W2_e^T.  w2[g]: [d, ff] bf16.
  * ff % 64 == 0, d % 256 == 0. */
 int cox_grouped_down(const void* h, long long rows_cap, const int32_t* offsets, int n_groups,
                      const int32_t* group_experts, const void* const* w2, int ff, int d, void* y_perm, void* stream);
+int cox_grouped_down_ex(const void* h, long long rows_cap, const int32_t* offsets, int n_groups,
+                        const int32_t* group_experts, const void* const* w2, int ff, int d, void* y_perm,
+                        int max_ctas, void* stream);
 
 /* K5 — weighted top-k combine back to token order (+ optional shared-expert
  * output, DeepSeek-V2):  out[t] = sum_j w[t,j] * y_perm[dst[t,j]] (+ shared[t]).

@@ -30,7 +30,8 @@ ROUTE_DEEPSEEK = 1
 EXPORTS = (
     "cox_last_error", "cox_version", "cox_device_check", "cox_router_topk", "cox_permute_workspace_bytes",
     "cox_permute", "cox_grouped_swiglu", "cox_grouped_down", "cox_combine", "cox_interleave_w13",
-    "cox_ep_counts_put", "cox_ep_offsets", "cox_ep_dispatch", "cox_ep_combine",
+    "cox_ep_counts_put", "cox_ep_offsets", "cox_ep_dispatch", "cox_ep_combine", "cox_grouped_swiglu_ex",
+    "cox_grouped_down_ex",
 )
 
 _lock = threading.Lock()
@@ -62,6 +63,12 @@ def _declare(L):
     L.cox_grouped_down.restype = c_int
     L.cox_grouped_down.argtypes = [c_void_p, c_ll, c_void_p, c_int, c_void_p, c_void_p, c_int, c_int,
                                    c_void_p, c_void_p]
+    L.cox_grouped_swiglu_ex.restype = c_int
+    L.cox_grouped_swiglu_ex.argtypes = [c_void_p, c_ll, c_void_p, c_int, c_void_p, c_void_p, c_int, c_int,
+                                        c_void_p, c_int, c_void_p]
+    L.cox_grouped_down_ex.restype = c_int
+    L.cox_grouped_down_ex.argtypes = [c_void_p, c_ll, c_void_p, c_int, c_void_p, c_void_p, c_int, c_int,
+                                      c_void_p, c_int, c_void_p]
     L.cox_combine.restype = c_int
     L.cox_combine.argtypes = [c_void_p, c_void_p, c_void_p, c_int, c_int, c_int, c_void_p, c_void_p, c_int,
                               c_void_p]

@@ -15,7 +15,7 @@ int launch_permute(const int32_t* idx, int T, int k, int E, int tile_m, const vo
                    int32_t* dst, void* x_perm, void* workspace, cudaStream_t s);
 int launch_grouped_gemm(int epi, const void* A, long long rows_cap, int K, const int32_t* offsets, int n_groups,
                         const int32_t* group_expert, const void* const* B, int N, void* out, long long ldo,
-                        cudaStream_t s);
+                        int max_ctas, cudaStream_t s);
 int launch_combine(const void* y_perm, const int32_t* dst, const float* w, int T, int k, int d, const void* shared,
                    void* out, int out_is_bf16, cudaStream_t s);
 
@@ -123,28 +123,42 @@ static int check_groups(const char* fn, int n_groups, const int32_t* group_exper
   return 0;
 }
 
-int cox_grouped_swiglu(const void* x_perm, long long rows_cap, const int32_t* offsets, int n_groups,
-                       const int32_t* group_experts, const void* const* w13, int d, int ff, void* h, void* stream) {
+int cox_grouped_swiglu_ex(const void* x_perm, long long rows_cap, const int32_t* offsets, int n_groups,
+                          const int32_t* group_experts, const void* const* w13, int d, int ff, void* h,
+                          int max_ctas, void* stream) {
   if (d <= 0 || d % 64 || ff <= 0 || ff % 128)
     return fail(COX_EINVAL, "cox_grouped_swiglu: need d%%64==0 and ff%%128==0 (d=%d ff=%d)", d, ff);
   if (rows_cap < 1) return fail(COX_EINVAL, "cox_grouped_swiglu: rows_cap < 1");
+  if (max_ctas < 0 || max_ctas == 1) return fail(COX_EINVAL, "cox_grouped_swiglu: max_ctas must be 0 or >= 2");
   if (!aligned16(x_perm) || !aligned16(h)) return fail(COX_EINVAL, "cox_grouped_swiglu: unaligned x_perm/h");
   if (int rc = check_groups("cox_grouped_swiglu", n_groups, group_experts, w13)) return rc;
   int rc = cox::launch_grouped_gemm(0, x_perm, rows_cap, d, offsets, n_groups, group_experts, w13, 2 * ff, h, ff,
-                                    static_cast<cudaStream_t>(stream));
+                                    max_ctas, static_cast<cudaStream_t>(stream));
   return cuda_status(rc, "cox_grouped_swiglu");
+}
+
+int cox_grouped_swiglu(const void* x_perm, long long rows_cap, const int32_t* offsets, int n_groups,
+                       const int32_t* group_experts, const void* const* w13, int d, int ff, void* h, void* stream) {
+  return cox_grouped_swiglu_ex(x_perm, rows_cap, offsets, n_groups, group_experts, w13, d, ff, h, 0, stream);
+}
+
+int cox_grouped_down_ex(const void* h, long long rows_cap, const int32_t* offsets, int n_groups,
+                        const int32_t* group_experts, const void* const* w2, int ff, int d, void* y_perm,
+                        int max_ctas, void* stream) {
+  if (d <= 0 || d % 256 || ff <= 0 || ff % 64)
+    return fail(COX_EINVAL, "cox_grouped_down: need d%%256==0 and ff%%64==0 (d=%d ff=%d)", d, ff);
+  if (rows_cap < 1) return fail(COX_EINVAL, "cox_grouped_down: rows_cap < 1");
+  if (max_ctas < 0 || max_ctas == 1) return fail(COX_EINVAL, "cox_grouped_down: max_ctas must be 0 or >= 2");
+  if (!aligned16(h) || !aligned16(y_perm)) return fail(COX_EINVAL, "cox_grouped_down: unaligned h/y_perm");
+  if (int rc = check_groups("cox_grouped_down", n_groups, group_experts, w2)) return rc;
+  int rc = cox::launch_grouped_gemm(1, h, rows_cap, ff, offsets, n_groups, group_experts, w2, d, y_perm, d, max_ctas,
+                                    static_cast<cudaStream_t>(stream));
+  return cuda_status(rc, "cox_grouped_down");
 }
 
 int cox_grouped_down(const void* h, long long rows_cap, const int32_t* offsets, int n_groups,
                      const int32_t* group_experts, const void* const* w2, int ff, int d, void* y_perm, void* stream) {
-  if (d <= 0 || d % 256 || ff <= 0 || ff % 64)
-    return fail(COX_EINVAL, "cox_grouped_down: need d%%256==0 and ff%%64==0 (d=%d ff=%d)", d, ff);
-  if (rows_cap < 1) return fail(COX_EINVAL, "cox_grouped_down: rows_cap < 1");
-  if (!aligned16(h) || !aligned16(y_perm)) return fail(COX_EINVAL, "cox_grouped_down: unaligned h/y_perm");
-  if (int rc = check_groups("cox_grouped_down", n_groups, group_experts, w2)) return rc;
-  int rc = cox::launch_grouped_gemm(1, h, rows_cap, ff, offsets, n_groups, group_experts, w2, d, y_perm, d,
-                                    static_cast<cudaStream_t>(stream));
-  return cuda_status(rc, "cox_grouped_down");
+  return cox_grouped_down_ex(h, rows_cap, offsets, n_groups, group_experts, w2, ff, d, y_perm, 0, stream);
 }
 
 int cox_combine(const void* y_perm, const int32_t* dst, const float* w, int T, int k, int d, const void* shared_out,

@@ -412,7 +412,7 @@ static int g_num_sms = 0;
 //      EPI_STORE  (B = W2 [N, K],                out = y [rows_cap, N])
 int launch_grouped_gemm(int epi, const void* A, long long rows_cap, int K, const int32_t* offsets, int n_groups,
                         const int32_t* group_expert, const void* const* B, int N, void* out, long long ldo,
-                        cudaStream_t s) {
+                        int max_ctas, cudaStream_t s) {
   if (n_groups <= 0) return 0;
   static GemmParams p;  // large (8.6 KB): built in static storage, copied at launch
   static std::mutex mu;
@@ -446,7 +446,8 @@ int launch_grouped_gemm(int epi, const void* A, long long rows_cap, int K, const
     cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
     if (g_num_sms <= 0) g_num_sms = 148;
   }
-  const int grid = (g_num_sms / 2) * 2;
+  int grid = (g_num_sms / 2) * 2;
+  if (max_ctas >= 2 && max_ctas < grid) grid = (max_ctas / 2) * 2;
   cudaError_t err;
   if (epi == EPI_SWIGLU) {
     static bool attr = false;

@@ -125,14 +125,44 @@ class MoELayer:
     def finish(self, b: StageBuffers, shared=None, out=None):
         return ops.combine(b.y, b.dst, b.w, shared, out=b.out if out is None else out)
 
+    # decode-size batches: the shared expert runs beside the routed experts on a
+    # side stream with a slice of the SMs (its GEMMs are tiny and would
+    # otherwise serialise behind the HBM-bound routed GEMMs)
+    SHARED_SIDE_MAX_ROWS = 8192
+    SHARED_SIDE_CTAS = 16
+
     def forward(self, x: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
         if x.dtype != torch.bfloat16 or x.dim() != 2 or x.shape[1] != self.d:
             raise ValueError(f"x must be bf16 [T, {self.d}]")
-        b = self.buffers(x.shape[0], x.device)
+        T = x.shape[0]
+        b = self.buffers(T, x.device)
+        if self.shared_ff and 0 < T * self.k <= self.SHARED_SIDE_MAX_ROWS:
+            main = torch.cuda.current_stream(x.device)
+            side = self._side_stream(x.device)
+            side.wait_stream(main)
+            with torch.cuda.stream(side):
+                ops.grouped_swiglu(x, b.shared_offsets, [0], [self.wts.shared_w13], self.shared_ff, h=b.shared_h,
+                                   max_ctas=self.SHARED_SIDE_CTAS)
+                ops.grouped_down(b.shared_h, b.shared_offsets, [0], [self.wts.shared_w2], self.d, y=b.shared_y,
+                                 max_ctas=self.SHARED_SIDE_CTAS)
+            self.route(x, b)
+            ops.grouped_swiglu(b.x_perm, b.offsets, self.groups, self.w13_list, self.ff, h=b.h,
+                               max_ctas=-(-(148 - self.SHARED_SIDE_CTAS) // 2) * 2)
+            ops.grouped_down(b.h, b.offsets, self.groups, self.w2_list, self.d, y=b.y,
+                             max_ctas=-(-(148 - self.SHARED_SIDE_CTAS) // 2) * 2)
+            main.wait_stream(side)
+            return self.finish(b, b.shared_y, out)
         self.route(x, b)
         self.experts(b)
         sh = self.shared_expert(x, b)
         return self.finish(b, sh, out)
+
+    def _side_stream(self, dev):
+        st = getattr(self, "_side", None)
+        if st is None:
+            st = torch.cuda.Stream(dev)
+            self._side = st
+        return st
 
     def capture(self, x_static: torch.Tensor):
         """Capture one forward over `x_static` into a CUDA graph (launch-bound

@@ -112,7 +112,8 @@ def permute(idx: torch.Tensor, x: torch.Tensor, E: int, tile_m: int = 1, out=Non
 
 
 def grouped_swiglu(x_perm: torch.Tensor, offsets: torch.Tensor, group_experts: Sequence[int],
-                   w13: Sequence[torch.Tensor], ff: int, h: torch.Tensor | None = None, stream=None):
+                   w13: Sequence[torch.Tensor], ff: int, h: torch.Tensor | None = None, stream=None,
+                   max_ctas: int = 0):
     """K3: h[r] = silu(x_perm[r] W1_e^T) * (x_perm[r] W3_e^T) for the listed groups."""
     _need(x_perm, "x_perm", _BF16, 2)
     _need(offsets, "offsets", torch.int32, 1)
@@ -126,14 +127,14 @@ def grouped_swiglu(x_perm: torch.Tensor, offsets: torch.Tensor, group_experts: S
     if h is None:
         h = torch.empty((rows, ff), dtype=_BF16, device=x_perm.device)
     L = _lib.lib()
-    _lib.check(L.cox_grouped_swiglu(x_perm.data_ptr(), rows, offsets.data_ptr(), len(group_experts),
-                                    _ids(group_experts), _ptrs(w13), d, ff, h.data_ptr(), _stream(stream)),
-               "cox_grouped_swiglu")
+    _lib.check(L.cox_grouped_swiglu_ex(x_perm.data_ptr(), rows, offsets.data_ptr(), len(group_experts),
+                                       _ids(group_experts), _ptrs(w13), d, ff, h.data_ptr(), max_ctas,
+                                       _stream(stream)), "cox_grouped_swiglu")
     return h
 
 
 def grouped_down(h: torch.Tensor, offsets: torch.Tensor, group_experts: Sequence[int], w2: Sequence[torch.Tensor],
-                 d: int, y: torch.Tensor | None = None, stream=None):
+                 d: int, y: torch.Tensor | None = None, stream=None, max_ctas: int = 0):
     """K4: y[r] = h[r] W2_e^T for the listed groups."""
     _need(h, "h", _BF16, 2)
     _need(offsets, "offsets", torch.int32, 1)
@@ -147,8 +148,9 @@ def grouped_down(h: torch.Tensor, offsets: torch.Tensor, group_experts: Sequence
     if y is None:
         y = torch.empty((rows, d), dtype=_BF16, device=h.device)
     L = _lib.lib()
-    _lib.check(L.cox_grouped_down(h.data_ptr(), rows, offsets.data_ptr(), len(group_experts), _ids(group_experts),
-                                  _ptrs(w2), ff, d, y.data_ptr(), _stream(stream)), "cox_grouped_down")
+    _lib.check(L.cox_grouped_down_ex(h.data_ptr(), rows, offsets.data_ptr(), len(group_experts),
+                                     _ids(group_experts), _ptrs(w2), ff, d, y.data_ptr(), max_ctas, _stream(stream)),
+               "cox_grouped_down")
     return y
 
 
