@@ -132,7 +132,7 @@ class EPMoELayer:
 
     @property
     def launches_per_step(self) -> int:
-        return 1 + 3 + 2 + 1
+        return 1 + 4 + 2 + 1
 
     def _buf(self, name, n, like):
         b = getattr(self, name)

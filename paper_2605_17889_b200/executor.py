@@ -108,7 +108,7 @@ class StratifiedMoEStack:
 
     @property
     def launches_per_step(self) -> int:
-        per = 1 + 3 + 1  # router, permute x3, combine
+        per = 1 + 4 + 1  # router, permute x4, combine
         return sum(per + (2 if self.plan.resident[l] else 0) + (2 if self.cold[l] else 0) for l in range(self.N))
 
     def _buffers(self, T: int) -> _Bufs:

@@ -87,8 +87,8 @@ class MoELayer:
 
     @property
     def launches_per_step(self) -> int:
-        # router 1 + permute 3 (+1 pad) + K3 + K4 + combine (+ shared K3/K4)
-        return 1 + 3 + (1 if self.tile_m > 1 else 0) + 2 + 1 + (2 if self.shared_ff else 0)
+        # router 1 + permute 4 (hist, scan, scatter, copy; +1 pad) + K3 + K4 + combine (+ shared K3/K4)
+        return 1 + 4 + (1 if self.tile_m > 1 else 0) + 2 + 1 + (2 if self.shared_ff else 0)
 
     def buffers(self, T: int, device) -> StageBuffers:
         if self._bufs is None or self._bufs.T != T:
