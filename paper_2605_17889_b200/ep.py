@@ -243,7 +243,8 @@ class FusedEPMoELayer:
 
     @property
     def launches_per_step(self) -> int:
-        return 1 + 3 + 1 + 1 + 1 + 2 + 1 + 3  # router, permute ranks, put, offsets, dispatch, K3/K4, combine, 3 barriers
+        # ours: router, permute ranks x3, counts put, offsets, dispatch, K3, K4, combine (+3 symm-mem barriers, not ours)
+        return 1 + 3 + 1 + 1 + 1 + 2 + 1
 
     def _setup(self, T: int, dev):
         G, E, k, d = self.G, self.E, self.k, self.d
