@@ -389,19 +389,22 @@ static int get_map(CUtensorMap* out, const void* ptr, unsigned long long rows, u
   return 0;
 }
 
-// Raster band (n-tiles per band).  Defaults chosen by measurement; the
-// COX_GEMM_BAND_K3 / COX_GEMM_BAND_K4 environment variables override them
-// for experiments.
-static int pick_band(int epi, int n_tiles) {
+// Raster band (n-tiles per band): tiles run expert -> n-band -> m -> n, so the
+// B band (band x 256 rows x K) is shared by every m-tile of the expert and A
+// is re-read once per band.  Pick the widest band that divides n_tiles and
+// whose B band stays within an L2 budget (~32 MB); e.g. C2 K3 (K=4096): 16,
+// C2 K4 (K=14336): 4, C4 K3 (11 n-tiles, K=2048): 11.  COX_GEMM_BAND_K3 /
+// COX_GEMM_BAND_K4 override for experiments.
+static int pick_band(int epi, int n_tiles, int K) {
   static int env_band[2] = {
       [] { const char* e = getenv("COX_GEMM_BAND_K3"); return e ? atoi(e) : 0; }(),
       [] { const char* e = getenv("COX_GEMM_BAND_K4"); return e ? atoi(e) : 0; }()};
   const int want = env_band[epi ? 1 : 0];
   if (want > 0 && n_tiles % want == 0) return want;
-  // K3 (SwiGLU, K = d): 16-wide bands halve the A re-reads with the B band
-  // still L2-resident (C2: 32 MB); K4 (K = ff, 3.5x longer tiles): 8.
-  if (!epi && n_tiles % 16 == 0) return 16;
-  for (int b : {8, 4, 2, 1})
+  const long long per_tile = (long long)GM_BN * K * 2;
+  long long max_band = (32LL << 20) / per_tile;
+  if (max_band < 1) max_band = 1;
+  for (int b = (int)(max_band < n_tiles ? max_band : n_tiles); b >= 1; --b)
     if (n_tiles % b == 0) return b;
   return 1;
 }
@@ -439,7 +442,7 @@ int launch_grouped_gemm(int epi, const void* A, long long rows_cap, int K, const
   p.n_groups = n_groups;
   p.K = K;
   p.n_tiles = N / GM_BN;
-  p.band = pick_band(epi, p.n_tiles);
+  p.band = pick_band(epi, p.n_tiles, K);
   if (g_num_sms == 0) {
     int dev = 0;
     cudaGetDevice(&dev);
