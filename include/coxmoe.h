@@ -61,6 +61,12 @@ int cox_device_check(void);
  * with the CPU oracle, so idx is bit-exact. */
 int cox_router_topk(const void* x, int x_dtype, const float* wg, int T, int d, int E, int k, int mode,
                     int32_t* idx, float* w, int32_t* counts, void* stream);
+/* Same with the router weight dtype explicit (COX_DTYPE_BF16 or COX_DTYPE_F32).
+ * A bf16 wg (the checkpoint dtype of Mixtral/DeepSeek routers) is staged in
+ * shared memory by the fine-grained (E > 8) kernel; the logits are identical
+ * to passing the same values as fp32 (bf16 x bf16 products are exact). */
+int cox_router_topk_ex(const void* x, int x_dtype, const void* wg, int wg_dtype, int T, int d, int E, int k,
+                       int mode, int32_t* idx, float* w, int32_t* counts, void* stream);
 
 /* K2 — stable permutation by expert (coalesced dispatch).
  *   x        [T, d] bf16, d % 8 == 0

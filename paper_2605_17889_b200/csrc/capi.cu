@@ -8,8 +8,8 @@
 #include "common.cuh"
 
 namespace cox {
-int launch_router(const void* x, int x_is_bf16, const float* wg, int T, int d, int E, int k, int mode, int32_t* idx,
-                  float* w, int32_t* counts, cudaStream_t s);
+int launch_router(const void* x, int x_is_bf16, const void* wg, int wg_is_bf16, int T, int d, int E, int k,
+                  int mode, int32_t* idx, float* w, int32_t* counts, cudaStream_t s);
 size_t permute_workspace_bytes(int T, int E);
 int launch_permute(const int32_t* idx, int T, int k, int E, int tile_m, const void* x, int d, int32_t* offsets,
                    int32_t* dst, void* x_perm, void* workspace, cudaStream_t s);
@@ -83,18 +83,24 @@ int cox_device_check(void) {
   return 0;
 }
 
-int cox_router_topk(const void* x, int x_dtype, const float* wg, int T, int d, int E, int k, int mode,
-                    int32_t* idx, float* w, int32_t* counts, void* stream) {
+int cox_router_topk_ex(const void* x, int x_dtype, const void* wg, int wg_dtype, int T, int d, int E, int k,
+                       int mode, int32_t* idx, float* w, int32_t* counts, void* stream) {
   if (T < 0 || d <= 0 || d % 8 || E <= 0 || E > 256 || k < 1 || k > E || k > 8)
     return fail(COX_EINVAL, "cox_router_topk: need T>=0, d%%8==0, 1<=k<=min(E,8), E<=256 (T=%d d=%d E=%d k=%d)", T, d,
                 E, k);
   if (mode != COX_ROUTE_MIXTRAL && mode != COX_ROUTE_DEEPSEEK) return fail(COX_EINVAL, "cox_router_topk: bad mode %d", mode);
   if (x_dtype != COX_DTYPE_BF16 && x_dtype != COX_DTYPE_F32) return fail(COX_EINVAL, "cox_router_topk: bad x_dtype");
+  if (wg_dtype != COX_DTYPE_BF16 && wg_dtype != COX_DTYPE_F32) return fail(COX_EINVAL, "cox_router_topk: bad wg_dtype");
   if (T > 0 && (!x || !wg || !idx || !w || !counts)) return fail(COX_EINVAL, "cox_router_topk: null pointer");
   if (!aligned16(x) || !aligned16(wg)) return fail(COX_EINVAL, "cox_router_topk: x and wg must be 16-byte aligned");
-  int rc = cox::launch_router(x, x_dtype == COX_DTYPE_BF16, wg, T, d, E, k, mode, idx, w, counts,
-                              static_cast<cudaStream_t>(stream));
+  int rc = cox::launch_router(x, x_dtype == COX_DTYPE_BF16, wg, wg_dtype == COX_DTYPE_BF16, T, d, E, k, mode, idx, w,
+                              counts, static_cast<cudaStream_t>(stream));
   return cuda_status(rc, "cox_router_topk");
+}
+
+int cox_router_topk(const void* x, int x_dtype, const float* wg, int T, int d, int E, int k, int mode,
+                    int32_t* idx, float* w, int32_t* counts, void* stream) {
+  return cox_router_topk_ex(x, x_dtype, wg, COX_DTYPE_F32, T, d, E, k, mode, idx, w, counts, stream);
 }
 
 size_t cox_permute_workspace_bytes(int T, int E) { return cox::permute_workspace_bytes(T, E); }

@@ -191,6 +191,18 @@ COX_DEV void tmem_ld_32x32b_x32(uint32_t taddr, uint32_t (&r)[32]) {
 }
 COX_DEV void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
+// Two independent fp32 FMAs in one FFMA2 (fma.rn.f32x2, sm_100): a0 = fma(x, w0, a0),
+// a1 = fma(x, w1, a1), each correctly rounded — bit-identical to two fmaf.  ptxas
+// folds the duplicated x into a broadcast operand.
+COX_DEV void ffma2(float& a0, float& a1, float x, float w0, float w1) {
+  unsigned long long acc, ww, xx;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(acc) : "f"(a0), "f"(a1));
+  asm("mov.b64 %0, {%1, %2};" : "=l"(ww) : "f"(w0), "f"(w1));
+  asm("mov.b64 %0, {%1, %1};" : "=l"(xx) : "f"(x));
+  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc) : "l"(xx), "l"(ww));
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a0), "=f"(a1) : "l"(acc));
+}
+
 // ---------------------------------------------------------------- misc
 COX_DEV uint32_t pack_bf16x2(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);

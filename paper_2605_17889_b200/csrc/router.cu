@@ -10,7 +10,9 @@
 // oracle (oracle/oracle_router.c) replays exactly: lane l owns the 8-element
 // chunks c = 32*j + l, accumulating fmaf(x, w, acc) with j then q ascending,
 // followed by an xor butterfly 16,8,4,2,1 of __fadd_rn.  CUDA cores only — no
-// tensor cores — so the order is fixed.
+// tensor cores — so the order is fixed.  Two experts' accumulators share one
+// FFMA2 (fma.rn.f32x2: two independently rounded FMAs), which halves the FMA
+// instruction count without changing any logit's operation sequence.
 //
 // Work decomposition: a block of 8 warps covers RT_TPW*NTG tokens x all E
 // experts; warp w owns an RT_TPW-token x 8-expert register tile (token group
@@ -58,9 +60,21 @@ struct XChunk<float> {
 
 // Tokens per block = RT_TPW * (RT_WARPS / egn); egn in {1,2,4,8}: expert groups
 // handled concurrently by the warps of one block (E > 8*egn loops over passes).
-template <typename XT, int TPW>
+template <typename WT>
+COX_DEV void load_w8(const WT* p, float (&w8)[8]);
+template <>
+COX_DEV void load_w8<float>(const float* p, float (&w8)[8]) {
+  const float4 wa = __ldg(reinterpret_cast<const float4*>(p)), wb = __ldg(reinterpret_cast<const float4*>(p) + 1);
+  w8[0] = wa.x; w8[1] = wa.y; w8[2] = wa.z; w8[3] = wa.w; w8[4] = wb.x; w8[5] = wb.y; w8[6] = wb.z; w8[7] = wb.w;
+}
+template <>
+COX_DEV void load_w8<__nv_bfloat16>(const __nv_bfloat16* p, float (&w8)[8]) {
+  bf16x8_to_f32(__ldg(reinterpret_cast<const uint4*>(p)), w8);
+}
+
+template <typename XT, int TPW, typename WT>
 __global__ void __launch_bounds__(RT_WARPS * 32, 2)
-router_topk_kernel(const XT* __restrict__ x, const float* __restrict__ wg, int T, int d, int E, int k, int mode,
+router_topk_kernel(const XT* __restrict__ x, const WT* __restrict__ wg, int T, int d, int E, int k, int mode,
                    int egn, int32_t* __restrict__ idx, float* __restrict__ wout, int32_t* __restrict__ counts) {
   extern __shared__ float s_logits[];  // [tokens_per_block][E]
   __shared__ int s_hist[256];
@@ -96,16 +110,15 @@ router_topk_kernel(const XT* __restrict__ x, const float* __restrict__ wg, int T
           for (int q = 0; q < 8; ++q) xv[t][q] = c.get(q);
         }
 #pragma unroll
-        for (int e = 0; e < RT_EG; ++e) {
-          if (e0 + e < E) {
-            const float4* wp = reinterpret_cast<const float4*>(wg + (long)(e0 + e) * d + s);
-            const float4 wa = __ldg(wp), wb = __ldg(wp + 1);
-            const float w8[8] = {wa.x, wa.y, wa.z, wa.w, wb.x, wb.y, wb.z, wb.w};
+        for (int e = 0; e < RT_EG; e += 2) {  // expert pairs -> FFMA2
+          float wa[8], wb[8];
+          const int ea = min(e0 + e, E - 1), eb = min(e0 + e + 1, E - 1);  // clamped rows are never stored
+          load_w8<WT>(wg + (long)ea * d + s, wa);
+          load_w8<WT>(wg + (long)eb * d + s, wb);
 #pragma unroll
-            for (int t = 0; t < TPW; ++t)
+          for (int t = 0; t < TPW; ++t)
 #pragma unroll
-              for (int q = 0; q < 8; ++q) acc[t][e] = __fmaf_rn(xv[t][q], w8[q], acc[t][e]);
-          }
+            for (int q = 0; q < 8; ++q) ffma2(acc[t][e], acc[t][e + 1], xv[t][q], wa[q], wb[q]);
         }
       }
 #pragma unroll
@@ -245,12 +258,14 @@ router_topk_staged_kernel(const __nv_bfloat16* __restrict__ x, const float* __re
 #pragma unroll
         for (int t = 0; t < RT_TPW; ++t) bf16x8_to_f32(xc[t], xv[t]);
 #pragma unroll
-        for (int e = 0; e < RT_EG; ++e) {
-          const float w8[8] = {wca[e].x, wca[e].y, wca[e].z, wca[e].w, wcb[e].x, wcb[e].y, wcb[e].z, wcb[e].w};
+        for (int e = 0; e < RT_EG; e += 2) {
+          const float wa[8] = {wca[e].x, wca[e].y, wca[e].z, wca[e].w, wcb[e].x, wcb[e].y, wcb[e].z, wcb[e].w};
+          const float wb[8] = {wca[e + 1].x, wca[e + 1].y, wca[e + 1].z, wca[e + 1].w,
+                               wcb[e + 1].x, wcb[e + 1].y, wcb[e + 1].z, wcb[e + 1].w};
 #pragma unroll
           for (int t = 0; t < RT_TPW; ++t)
 #pragma unroll
-            for (int q = 0; q < 8; ++q) acc[t][e] = __fmaf_rn(xv[t][q], w8[q], acc[t][e]);
+            for (int q = 0; q < 8; ++q) ffma2(acc[t][e], acc[t][e + 1], xv[t][q], wa[q], wb[q]);
         }
       }
 #pragma unroll
@@ -316,13 +331,175 @@ router_topk_staged_kernel(const __nv_bfloat16* __restrict__ x, const float* __re
     if (s_hist[i]) atomicAdd(&counts[i], s_hist[i]);
 }
 
-int launch_router(const void* x, int x_is_bf16, const float* wg, int T, int d, int E, int k, int mode, int32_t* idx,
-                  float* w, int32_t* counts, cudaStream_t s) {
+// bf16 router weights (the checkpoint dtype of Mixtral / DeepSeek routers):
+// the block's 32-token x tile AND the current 8-expert slice of wg are both
+// staged in shared memory (wg double-buffered: group g+1 streams in with
+// cp.async while group g is consumed), so every warp reads conflict-free
+// LDS.128 and the router weights cross L2 once per 32 tokens at half the
+// bytes.  Products bf16 x bf16 -> fp32 FMA in the canonical order: results are
+// identical to the fp32-weight kernels whenever wg is bf16-exact.
+constexpr int RB_TB = 32;
+
+__global__ void __launch_bounds__(RT_WARPS * 32, 1)
+router_topk_staged_bf16w_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ wg, int T,
+                                int d, int E, int k, int mode, int32_t* __restrict__ idx, float* __restrict__ wout,
+                                int32_t* __restrict__ counts) {
+  extern __shared__ __align__(16) uint8_t rb_smem[];
+  __nv_bfloat16* sx = reinterpret_cast<__nv_bfloat16*>(rb_smem);                         // [RB_TB][d]
+  __nv_bfloat16* sw = sx + (size_t)RB_TB * d;                                             // [2][RT_EG][d]
+  float* s_logits = reinterpret_cast<float*>(sw + (size_t)2 * RT_EG * d);                // [RB_TB][E]
+  __shared__ int s_hist[256];
+  __shared__ int s_sel[RT_WARPS][8];
+  __shared__ float s_selv[RT_WARPS][8];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int i = threadIdx.x; i < E; i += blockDim.x) s_hist[i] = 0;
+  const int vec_per_row = d / 8;
+  const int ngroups = (E + RT_EG - 1) / RT_EG;
+  auto stage_w = [&](int g, int buf) {
+    for (int i = threadIdx.x; i < RT_EG * vec_per_row; i += blockDim.x) {
+      const int r = i / vec_per_row, c = i - r * vec_per_row;
+      const int e = g * RT_EG + r;
+      const bool ok = e < E;
+      cp_async16(smem_u32(sw + ((size_t)buf * RT_EG + r) * d + 8 * c), wg + (ok ? (long)e * d + 8 * c : 0),
+                 ok ? 16u : 0u);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  const long nblk = (T + RB_TB - 1) / RB_TB;
+  for (long blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
+    const long tb0 = blk * RB_TB;
+    __syncthreads();
+    for (int i = threadIdx.x; i < RB_TB * vec_per_row; i += blockDim.x) {
+      const int row = i / vec_per_row, c = i - row * vec_per_row;
+      const bool ok = tb0 + row < T;
+      cp_async16(smem_u32(sx + (size_t)row * d + 8 * c), x + (ok ? (tb0 + row) * (long)d + 8 * c : 0),
+                 ok ? 16u : 0u);
+    }
+    stage_w(0, 0);  // commits x tile + group 0 together
+    const int tl0 = warp * RT_TPW;
+    for (int g = 0; g < ngroups; ++g) {
+      if (g + 1 < ngroups) {
+        stage_w(g + 1, (g + 1) & 1);
+        asm volatile("cp.async.wait_group 1;" ::: "memory");
+      } else {
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+      }
+      __syncthreads();
+      const __nv_bfloat16* swg = sw + (size_t)(g & 1) * RT_EG * d;
+      const int e0 = g * RT_EG;
+      float acc[RT_TPW][RT_EG];
+#pragma unroll
+      for (int t = 0; t < RT_TPW; ++t)
+#pragma unroll
+        for (int e = 0; e < RT_EG; ++e) acc[t][e] = 0.0f;
+      for (int s = 8 * lane; s < d; s += 256) {
+        float xv[RT_TPW][8];
+#pragma unroll
+        for (int t = 0; t < RT_TPW; ++t)
+          bf16x8_to_f32(*reinterpret_cast<const uint4*>(sx + (size_t)(tl0 + t) * d + s), xv[t]);
+#pragma unroll
+        for (int e = 0; e < RT_EG; e += 2) {
+          float wa[8], wb[8];
+          bf16x8_to_f32(*reinterpret_cast<const uint4*>(swg + (size_t)e * d + s), wa);
+          bf16x8_to_f32(*reinterpret_cast<const uint4*>(swg + (size_t)(e + 1) * d + s), wb);
+#pragma unroll
+          for (int t = 0; t < RT_TPW; ++t)
+#pragma unroll
+            for (int q = 0; q < 8; ++q) ffma2(acc[t][e], acc[t][e + 1], xv[t][q], wa[q], wb[q]);
+        }
+      }
+#pragma unroll
+      for (int t = 0; t < RT_TPW; ++t)
+#pragma unroll
+        for (int e = 0; e < RT_EG; ++e) {
+          float v = acc[t][e];
+#pragma unroll
+          for (int off = 16; off >= 1; off >>= 1) v = __fadd_rn(v, __shfl_xor_sync(0xffffffffu, v, off));
+          if (lane == 0 && e0 + e < E) s_logits[(tl0 + t) * E + e0 + e] = v;
+        }
+      __syncthreads();  // all warps done with buffer (g & 1) before it is refilled
+    }
+    for (int tl = warp; tl < RB_TB; tl += RT_WARPS) {
+      const long t = tb0 + tl;
+      if (t >= T) break;
+      const float* lg = s_logits + tl * E;
+      uint32_t taken = 0;
+      for (int j = 0; j < k; ++j) {
+        float bv = 0.0f;
+        int bi = -1;
+        for (int i = 0; lane + 32 * i < E; ++i) {
+          const int e = lane + 32 * i;
+          if (taken & (1u << i)) continue;
+          const float v = lg[e];
+          if (bi < 0 || v > bv) { bv = v; bi = e; }
+        }
+#pragma unroll
+        for (int off = 16; off >= 1; off >>= 1) {
+          const float ov = __shfl_xor_sync(0xffffffffu, bv, off);
+          const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
+          const bool better = (oi >= 0) && (bi < 0 || ov > bv || (ov == bv && oi < bi));
+          if (better) { bv = ov; bi = oi; }
+        }
+        if ((bi & 31) == lane) taken |= 1u << (bi >> 5);
+        if (lane == 0) {
+          s_sel[warp][j] = bi;
+          s_selv[warp][j] = bv;
+        }
+      }
+      __syncwarp();
+      if (lane == 0) {
+        const int* sel = s_sel[warp];
+        const float* selv = s_selv[warp];
+        const float m = selv[0];
+        float ssum = 0.0f;
+        if (mode == 0) {
+          for (int j = 0; j < k; ++j) ssum = __fadd_rn(ssum, expf(__fsub_rn(selv[j], m)));
+        } else {
+          for (int e = 0; e < E; ++e) ssum = __fadd_rn(ssum, expf(__fsub_rn(lg[e], m)));
+        }
+        for (int j = 0; j < k; ++j) {
+          idx[t * k + j] = sel[j];
+          wout[t * k + j] = __fdiv_rn(expf(__fsub_rn(selv[j], m)), ssum);
+          atomicAdd(&s_hist[sel[j]], 1);
+        }
+      }
+      __syncwarp();
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < E; i += blockDim.x)
+    if (s_hist[i]) atomicAdd(&counts[i], s_hist[i]);
+}
+
+int launch_router_bf16w(const void* x, const void* wg, int T, int d, int E, int k, int mode, int32_t* idx, float* w,
+                        int32_t* counts, cudaStream_t s) {
+  const size_t smem = (size_t)RB_TB * d * 2 + (size_t)2 * RT_EG * d * 2 + (size_t)RB_TB * E * 4;
+  if (smem > 220 * 1024) return -1;
+  if (cudaMemsetAsync(counts, 0, sizeof(int32_t) * E, s) != cudaSuccess) return -2;
+  if (T == 0) return 0;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(router_topk_staged_bf16w_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    attr = true;
+  }
+  long blocks = (T + RB_TB - 1) / RB_TB;
+  if (blocks > 148L * 8) blocks = 148L * 8;
+  router_topk_staged_bf16w_kernel<<<(int)blocks, RT_WARPS * 32, smem, s>>>(
+      static_cast<const __nv_bfloat16*>(x), static_cast<const __nv_bfloat16*>(wg), T, d, E, k, mode, idx, w, counts);
+  return cudaGetLastError() == cudaSuccess ? 0 : -2;
+}
+
+int launch_router(const void* x, int x_is_bf16, const void* wg, int wg_is_bf16, int T, int d, int E, int k,
+                  int mode, int32_t* idx, float* w, int32_t* counts, cudaStream_t s) {
+  if (wg_is_bf16 && x_is_bf16 && E > RT_EG && (long)T >= 148L * RB_TB) {
+    const int rc = launch_router_bf16w(x, wg, T, d, E, k, mode, idx, w, counts, s);
+    if (rc != -1) return rc;  // -1: tile does not fit in smem -> generic kernels below
+  }
   cudaError_t err = cudaMemsetAsync(counts, 0, sizeof(int32_t) * E, s);
   if (err != cudaSuccess) return -2;
   if (T == 0) return 0;
   const size_t staged_smem = (size_t)RS_TB * d * 2 + (size_t)RS_TB * E * 4;
-  if (x_is_bf16 && E > RT_EG && staged_smem <= 200 * 1024 && (long)T >= 148L * RS_TB) {
+  if (!wg_is_bf16 && x_is_bf16 && E > RT_EG && staged_smem <= 200 * 1024 && (long)T >= 148L * RS_TB) {
     static bool attr = false;
     if (!attr) {
       cudaFuncSetAttribute(router_topk_staged_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
@@ -331,7 +508,7 @@ int launch_router(const void* x, int x_is_bf16, const float* wg, int T, int d, i
     long blocks = (T + RS_TB - 1) / RS_TB;
     if (blocks > 148L * 8) blocks = 148L * 8;
     router_topk_staged_kernel<<<(int)blocks, RT_WARPS * 32, staged_smem, s>>>(
-        static_cast<const __nv_bfloat16*>(x), wg, T, d, E, k, mode, idx, w, counts);
+        static_cast<const __nv_bfloat16*>(x), static_cast<const float*>(wg), T, d, E, k, mode, idx, w, counts);
     return cudaGetLastError() == cudaSuccess ? 0 : -2;
   }
   int groups = (E + RT_EG - 1) / RT_EG;
@@ -344,14 +521,17 @@ int launch_router(const void* x, int x_is_bf16, const float* wg, int T, int d, i
   long blocks = (T + tpb - 1) / tpb;
   if (blocks > 148L * 16) blocks = 148L * 16;
   const size_t smem = sizeof(float) * (size_t)tpb * E;
-#define RT_LAUNCH(XT, TP) \
-  router_topk_kernel<XT, TP><<<(int)blocks, RT_WARPS * 32, smem, s>>>(static_cast<const XT*>(x), wg, T, d, E, k, \
-                                                                      mode, egn, idx, w, counts)
+#define RT_LAUNCH(XT, TP, WT)                                                                                   \
+  router_topk_kernel<XT, TP, WT><<<(int)blocks, RT_WARPS * 32, smem, s>>>(                                      \
+      static_cast<const XT*>(x), static_cast<const WT*>(wg), T, d, E, k, mode, egn, idx, w, counts)
+#define RT_BY_W(XT, TP) \
+  if (wg_is_bf16) RT_LAUNCH(XT, TP, __nv_bfloat16); else RT_LAUNCH(XT, TP, float)
   if (x_is_bf16) {
-    if (small) RT_LAUNCH(__nv_bfloat16, 1); else RT_LAUNCH(__nv_bfloat16, RT_TPW);
+    if (small) { RT_BY_W(__nv_bfloat16, 1); } else { RT_BY_W(__nv_bfloat16, RT_TPW); }
   } else {
-    if (small) RT_LAUNCH(float, 1); else RT_LAUNCH(float, RT_TPW);
+    if (small) { RT_BY_W(float, 1); } else { RT_BY_W(float, RT_TPW); }
   }
+#undef RT_BY_W
 #undef RT_LAUNCH
   return cudaGetLastError() == cudaSuccess ? 0 : -2;
 }

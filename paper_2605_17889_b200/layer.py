@@ -77,6 +77,9 @@ class MoELayer:
         if not (1 <= self.k <= self.E):
             raise ValueError("top_k must satisfy 1 <= top_k <= experts_per_layer")
         self.groups = list(range(self.E))
+        # router weight in bf16 when that is exact (bf16 checkpoints): half the bytes, smem-staged for E > 8
+        wgb = weights.wg.to(torch.bfloat16)
+        self.wg_router = wgb if torch.equal(wgb.float(), weights.wg) else weights.wg
         self.w13_list = [weights.w13[e] for e in range(self.E)]
         self.w2_list = [weights.w2[e] for e in range(self.E)]
         self.shared_ff = weights.shared_w2.shape[1] if weights.shared_w2 is not None else 0
@@ -99,7 +102,7 @@ class MoELayer:
 
     # --- stages (all stream-ordered on the current stream) -------------------
     def route(self, x: torch.Tensor, b: StageBuffers):
-        ops.router_topk(x, self.wts.wg, self.k, self.mode, out=(b.idx, b.w, b.counts))
+        ops.router_topk(x, self.wg_router, self.k, self.mode, out=(b.idx, b.w, b.counts))
         ops.permute(b.idx, x, self.E, self.tile_m, out=(b.offsets, b.dst, b.x_perm), workspace=b.workspace)
 
     def experts(self, b: StageBuffers, groups=None, w13=None, w2=None):
@@ -253,7 +256,7 @@ class MoELayer:
             raise ValueError("stage_times needs the step's input")
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(7)]
         ev[0].record()
-        ops.router_topk(x, self.wts.wg, self.k, self.mode, out=(b.idx, b.w, b.counts))
+        ops.router_topk(x, self.wg_router, self.k, self.mode, out=(b.idx, b.w, b.counts))
         ev[1].record()
         ops.permute(b.idx, x, self.E, self.tile_m, out=(b.offsets, b.dst, b.x_perm), workspace=b.workspace)
         ev[2].record()

@@ -48,9 +48,11 @@ def _ids(ids: Sequence[int]):
 
 
 def router_topk(x: torch.Tensor, wg: torch.Tensor, k: int, mode: int = _lib.ROUTE_MIXTRAL, out=None, stream=None):
-    """K1: -> (idx [T,k] int32, w [T,k] fp32, counts [E] int32)."""
+    """K1: -> (idx [T,k] int32, w [T,k] fp32, counts [E] int32).  wg: fp32 or bf16 [E, d]."""
     _need(x, "x", ndim=2)
-    _need(wg, "wg", torch.float32, 2)
+    _need(wg, "wg", None, 2)
+    if wg.dtype not in (torch.float32, _BF16):
+        raise ValueError("wg must be fp32 or bf16")
     T, d = x.shape
     E = wg.shape[0]
     if wg.shape[1] != d:
@@ -68,8 +70,9 @@ def router_topk(x: torch.Tensor, wg: torch.Tensor, k: int, mode: int = _lib.ROUT
     else:
         idx, w, counts = out
     L = _lib.lib()
-    _lib.check(L.cox_router_topk(x.data_ptr(), xdt, wg.data_ptr(), T, d, E, k, mode, idx.data_ptr(), w.data_ptr(),
-                                 counts.data_ptr(), _stream(stream)), "cox_router_topk")
+    wdt = _lib.DTYPE_BF16 if wg.dtype == _BF16 else _lib.DTYPE_F32
+    _lib.check(L.cox_router_topk_ex(x.data_ptr(), xdt, wg.data_ptr(), wdt, T, d, E, k, mode, idx.data_ptr(),
+                                    w.data_ptr(), counts.data_ptr(), _stream(stream)), "cox_router_topk")
     return idx, w, counts
 
 

@@ -316,3 +316,18 @@ def test_full_size_layer_slice_vs_oracle(cfg):
     assert rel_l2(f(out[sl]), ref["out"]) <= 1e-2
     counts = b.counts.cpu().numpy()
     assert counts.sum() == T * k and np.array_equal(np.diff(b.offsets.cpu().numpy()), counts)
+
+
+@pytest.mark.parametrize("T,d,E,k,mode", [(148 * 32 + 77, 2048, 64, 6, 1), (5000, 1024, 8, 2, 0), (40, 512, 16, 4, 1)])
+def test_router_bf16_weights_identical_to_fp32(T, d, E, k, mode):
+    """bf16 router weights (smem-staged kernel for E > 8) give exactly the fp32-weight results."""
+    x = make_tokens(T, d, seed=8, device=DEV)
+    g = torch.Generator(device=DEV).manual_seed(9)
+    wgb = ((torch.rand((E, d), generator=g, device=DEV) * 2 - 1) / d ** 0.5).to(torch.bfloat16)
+    a = ops.router_topk(x, wgb.float(), k, mode)
+    b = ops.router_topk(x, wgb, k, mode)
+    torch.cuda.synchronize()
+    for u, v in zip(a, b):
+        assert torch.equal(u, v)
+    oi, ow, _ = O.router_topk(x[:999].float().cpu().numpy(), wgb.float().cpu().numpy(), k, mode)
+    assert np.array_equal(b[0][:999].cpu().numpy(), oi)
