@@ -331,3 +331,29 @@ def test_router_bf16_weights_identical_to_fp32(T, d, E, k, mode):
         assert torch.equal(u, v)
     oi, ow, _ = O.router_topk(x[:999].float().cpu().numpy(), wgb.float().cpu().numpy(), k, mode)
     assert np.array_equal(b[0][:999].cpu().numpy(), oi)
+
+
+def test_fused_ep_full_size_c2_single_rank():
+    """C2-size batch (262,144 tokens, d=4096, ff=14336) through the fused EP layer
+    at world size 1 == MoELayer bit-for-bit (receive buffers of 655k rows)."""
+    import os
+    import socket
+    import torch.distributed as dist
+    from paper_2605_17889_b200.ep import FusedEPMoELayer
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device(DEV, 0))
+    try:
+        wts = make_layer_weights(8, 4096, 14336, seed=0, device=DEV)
+        x = make_tokens(64 * 4096, 4096, seed=1, device=DEV)
+        a = MoELayer(wts, 2)(x).clone()
+        lay = FusedEPMoELayer(wts, 2, "mixtral")
+        b = lay(x)
+        torch.cuda.synchronize()
+        lay.check()
+        assert torch.equal(a, b)
+    finally:
+        dist.destroy_process_group()
