@@ -128,16 +128,18 @@ def dist_env():
 
 
 def cpu_baseline(wts_host, x_host, k, mode_id, shared_host, n_tokens):
-    """fp32 CPU oracle over the first n_tokens tokens (routed exactly as in the full batch)."""
+    """fp32 CPU oracle over the first n_tokens tokens (routed exactly as in the full batch).
+    Returns (tokens/s, threads, seconds, oracle result dict)."""
     from oracle import oracle as O
     O.lib()
     threads = len(os.sched_getaffinity(0))
     O.set_num_threads(threads)
     xs = x_host[:n_tokens]
     t0 = time.perf_counter()
-    O.moe_layer(xs, wts_host["wg"], wts_host["w1"], wts_host["w3"], wts_host["w2"], k, mode_id, shared=shared_host)
+    ref = O.moe_layer(xs, wts_host["wg"], wts_host["w1"], wts_host["w3"], wts_host["w2"], k, mode_id,
+                      shared=shared_host)
     dt = time.perf_counter() - t0
-    return n_tokens / dt, threads, dt
+    return n_tokens / dt, threads, dt, ref
 
 
 def host_weights(wts):
@@ -451,13 +453,23 @@ def main():
                     "frac": achieved / pk["hbm"], "traffic": None,
                     "bytes_per_step": wbytes + abytes, "experts_touched": touched}
         cpu = None
-        if not args.no_cpu_baseline and ws == 1:
+        parity = None
+        if not args.no_cpu_baseline and ws == 1 and not graph and not args.microbatch:
             hw, shared = host_weights(wts)
             x_host_f = x[: args.cpu_tokens].float().cpu().numpy()
-            cps, threads, dt = cpu_baseline(hw, x_host_f, k, 0 if mode == "mixtral" else 1, shared, args.cpu_tokens)
+            cps, threads, dt, ref = cpu_baseline(hw, x_host_f, k, 0 if mode == "mixtral" else 1, shared,
+                                                 args.cpu_tokens)
             cpu = {"value": cps, "unit": "tokens/s", "cores": threads, "kind": "port",
                    "sample": f"first {args.cpu_tokens} of {T} tokens (routed as in the full batch), full-size "
                              f"weights, fp32 oracle (oracle/, OpenMP x{threads}) on {cpu_model_name()}: {dt:.1f} s"}
+            # parity of the timed GPU path on the same tokens (same inputs, same weights)
+            import numpy as np
+            n = args.cpu_tokens
+            gout = layer(x)[:n].float().cpu().numpy().astype(np.float64)
+            gidx = layer.buffers(T, dev).idx[:n].cpu().numpy()
+            err = float(np.linalg.norm(gout - ref["out"]) / max(np.linalg.norm(ref["out"]), 1e-30))
+            parity = {"tokens_checked": n, "routing_indices_bitexact": bool(np.array_equal(gidx, ref["idx"])),
+                      "out_rel_l2_vs_fp32_oracle": err, "tolerance": 1e-2, "pass": bool(err <= 1e-2)}
         if args.microbatch:
             desc_mb = f" [ABLATION: micro-batched, {args.microbatch} tokens per expert-stage launch]"
         else:
@@ -477,6 +489,7 @@ def main():
             "roofline": roof,
             "stages_ms": stages,
             "cpu_baseline": cpu,
+            "parity": parity,
             "e2e": e2e,
             "gpu_launches": layer.launches_per_step * args.steps * (-(-T // args.microbatch) if args.microbatch else 1),
             "clocks": clk.summary(),
