@@ -64,7 +64,8 @@ struct alignas(64) GemmParams {
   int band;
 };
 
-constexpr size_t GM_SMEM_BYTES = 1024 + GM_STAGES * (GM_A_BYTES + GM_B_BYTES) + 512 + 4 * (3 * GM_MAXG + 4);
+constexpr size_t GM_SMEM_BYTES =
+    1024 + GM_STAGES * (GM_A_BYTES + GM_B_BYTES) + 512 + 4 * (3 * GM_MAXG + 4) + 16 + 4 * 32 * 128;
 
 struct TileCoord {
   int g, m, n;
@@ -106,6 +107,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GM_THREADS, 1)
   int* s_prefix = reinterpret_cast<int*>(tmem_slot + 4);
   int* s_rows = s_prefix + GM_MAXG + 1;
   int* s_row0 = s_rows + GM_MAXG;
+  uint32_t* s_stage = reinterpret_cast<uint32_t*>(
+      (reinterpret_cast<uintptr_t>(s_row0 + GM_MAXG) + 15) & ~uintptr_t(15));  // 4 warps x 32 rows x 128 B
 
   const uint32_t rank = cluster_ctarank();
   const int warp = threadIdx.x >> 5;
@@ -275,8 +278,32 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GM_THREADS, 1)
       const bool valid = local_row < s_rows[c.g];
       const long long grow = (long long)s_row0[c.g] + local_row;
       const uint32_t tbase = tmem_base + ((uint32_t)(ew * 32) << 16) + acc * GM_BN;
+      // Epilogue stores are coalesced through a per-warp 4 KB staging tile:
+      // each lane packs 64 bf16 columns of its row (XOR-swizzled 16 B chunks,
+      // conflict-free), then every st.global.v4 instruction of the warp writes
+      // 4 rows x 128 contiguous bytes (full lines) instead of 32 scattered
+      // 16-byte pieces.
+      const int wrow0 = c.m * 2 * GM_BM + (int)rank * GM_BM + ew * 32;  // first row of this warp in the group
+      const int vrows = s_rows[c.g] - wrow0;                               // rows of the warp that are stored
+      const long long grow0 = (long long)s_row0[c.g] + wrow0;
+      uint32_t* stg = s_stage + ew * (32 * 32);
+      auto stage16 = [&](int j, uint32_t a, uint32_t b, uint32_t c2, uint32_t d2) {  // chunk j (0..7) of my row
+        *reinterpret_cast<uint4*>(stg + lane * 32 + ((j ^ (lane & 7)) * 4)) = make_uint4(a, b, c2, d2);
+      };
+      auto flush64 = [&](__nv_bfloat16* col0) {  // write the staged 32 rows x 64 cols
+        __syncwarp();
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int r = i * 4 + (lane >> 3), j = lane & 7;
+          const uint4 v = *reinterpret_cast<const uint4*>(stg + r * 32 + ((j ^ (r & 7)) * 4));
+          if (r < vrows) st_global_v4(col0 + (grow0 + r) * p.ldo + j * 8, v.x, v.y, v.z, v.w);
+        }
+        __syncwarp();
+      };
+      (void)valid;
+      (void)grow;
       if constexpr (EPI == EPI_SWIGLU) {
-        __nv_bfloat16* orow = out + grow * p.ldo + (long long)c.n * (GM_BN / 2);
+        __nv_bfloat16* ocol = out + (long long)c.n * (GM_BN / 2);
 #pragma unroll 1
         for (int cc = 0; cc < (GM_BN / 2) / 32; ++cc) {
           uint32_t gr[32], ur[32];
@@ -290,14 +317,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GM_THREADS, 1)
             const float u0 = __uint_as_float(ur[2 * q]), u1 = __uint_as_float(ur[2 * q + 1]);
             pk[q] = pack_bf16x2(silu_f(g0) * u0, silu_f(g1) * u1);
           }
-          if (valid) {
 #pragma unroll
-            for (int q = 0; q < 4; ++q)
-              st_global_v4(orow + cc * 32 + q * 8, pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
-          }
+          for (int q = 0; q < 4; ++q) stage16((cc & 1) * 4 + q, pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+          if (cc & 1) flush64(ocol + (cc >> 1) * 64);
         }
       } else {
-        __nv_bfloat16* orow = out + grow * p.ldo + (long long)c.n * GM_BN;
+        __nv_bfloat16* ocol = out + (long long)c.n * GM_BN;
 #pragma unroll 1
         for (int cc = 0; cc < GM_BN / 32; ++cc) {
           uint32_t r[32];
@@ -306,11 +331,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GM_THREADS, 1)
           uint32_t pk[16];
 #pragma unroll
           for (int q = 0; q < 16; ++q) pk[q] = pack_bf16x2(__uint_as_float(r[2 * q]), __uint_as_float(r[2 * q + 1]));
-          if (valid) {
 #pragma unroll
-            for (int q = 0; q < 4; ++q)
-              st_global_v4(orow + cc * 32 + q * 8, pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
-          }
+          for (int q = 0; q < 4; ++q) stage16((cc & 1) * 4 + q, pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+          if (cc & 1) flush64(ocol + (cc >> 1) * 64);
         }
       }
       tc_fence_before();
