@@ -29,8 +29,11 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <algorithm>
+#include <cmath>
 #include <cstdlib>
 #include <mutex>
+#include <vector>
 #include <unordered_map>
 
 #include "common.cuh"
@@ -55,6 +58,8 @@ struct alignas(64) GemmParams {
   CUtensorMap b_map[GM_MAXG];
   const int32_t* offsets;
   int* tile_counter;  // zeroed before launch; dynamic tile scheduler
+  unsigned long long* tile_word;  // die-aware mode: (claimed from head) | (claimed from tail) << 32
+  const int* die_map;             // SM id -> die (0/1), nullptr = die-agnostic
   void* out;
   long long ldo;
   int group_expert[GM_MAXG];
@@ -186,10 +191,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GM_THREADS, 1)
   if (warp == 3) {
     // ------------------------------------------------------------ tile scheduler (leader)
     if (rank == 0 && lane == 0) {
+      uint32_t smid;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+      const int my_die = p.die_map ? p.die_map[smid] : 0;
       for (int i = 0;; ++i) {
         const int slot = i % GM_SCHED_DEPTH;
         mbar_wait(smem_u32(&sempty[slot]), ((i / GM_SCHED_DEPTH) & 1) ^ 1);
-        int t = (i == 0) ? cid : ncl + atomicAdd(p.tile_counter, 1);
+        int t;
+        if (p.die_map) {
+          // Two-ended queue: die 0 walks the tile list from the front, die 1 from the
+          // back; both claims go through one 64-bit atomic, so they meet exactly.
+          const unsigned long long old = atomicAdd(p.tile_word, my_die ? (1ull << 32) : 1ull);
+          const int head = (int)(old & 0xffffffffu), tailc = (int)(old >> 32);
+          if (my_die == 0)
+            t = (head < total - tailc) ? head : total;
+          else
+            t = (total - 1 - tailc >= head) ? total - 1 - tailc : total;
+        } else {
+          t = (i == 0) ? cid : ncl + atomicAdd(p.tile_counter, 1);
+        }
         if (t > total) t = total;
         s_tile[slot] = t;
         st_shared_cluster_u32(mapa(smem_u32(&s_tile[slot]), 1), (uint32_t)t);
@@ -432,6 +452,114 @@ static int pick_band(int epi, int n_tiles, int K) {
   return 1;
 }
 
+// ------------------------------------------------------------------ die discovery
+// B200 has two dies, each with half of the L2; an operand used by SMs of both
+// dies is fetched into both halves (the L2 fabric counters show it).  The SM ->
+// die map is per GPU (yield-dependent), so it is measured once per process: each
+// SM times L2 hits to 256 lines; lines homed on its own die are faster, so SMs
+// of one die share a latency pattern (within-group correlation ~0.9, between
+// ~ -0.7 on the measured boards).  OFF by default (COX_DIE_AWARE=1 enables):
+// measured on C2 it RAISES K3's DRAM reads 33 -> 138 GB and the L2 fabric
+// traffic 4x (1.71 vs 1.86 M tok/s) — operands shared by both dies are served
+// better than disjoint per-die working sets; C4 gains ~1.5%.  Kept as an
+// experiment switch, see DESIGN.md.
+__global__ void die_probe_kernel(const int* __restrict__ buf, int nlines, int stride_ints, unsigned* lat,
+                                 int* smid_out) {
+  unsigned smid;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+  if (threadIdx.x) return;
+  smid_out[blockIdx.x] = (int)smid;
+  int sink = 0;
+  for (int i = 0; i < nlines; ++i) {
+    int v;
+    asm volatile("ld.global.cg.s32 %0, [%1];" : "=r"(v) : "l"(buf + (long)i * stride_ints));
+    sink += v;
+  }
+  for (int i = 0; i < nlines; ++i) {
+    const long long t0 = clock64();
+    int v;
+    asm volatile("ld.global.cg.s32 %0, [%1];" : "=r"(v) : "l"(buf + (long)i * stride_ints + (sink & 1)));
+    sink += v;
+    const long long t1 = clock64();
+    lat[blockIdx.x * nlines + i] = (unsigned)(t1 - t0);
+  }
+  if (sink == 123456789) lat[0] = 0;
+}
+
+static const int* die_map_device(int num_sms) {
+  static int* d_map = nullptr;
+  static bool tried = false;
+  if (tried) return d_map;
+  tried = true;
+  const char* env = getenv("COX_DIE_AWARE");
+  if (!env || atoi(env) == 0) return nullptr;
+  const int nlines = 256, stride = 1536, nb = num_sms * 4;
+  int* buf = nullptr;
+  unsigned* lat = nullptr;
+  int* sm = nullptr;
+  bool ok = cudaMalloc(&buf, (size_t)nlines * stride * 4 + 64) == cudaSuccess &&
+            cudaMalloc(&lat, (size_t)nb * nlines * 4) == cudaSuccess && cudaMalloc(&sm, nb * 4) == cudaSuccess &&
+            cudaMemset(buf, 0, (size_t)nlines * stride * 4 + 64) == cudaSuccess;
+  std::vector<unsigned> h((size_t)nb * nlines);
+  std::vector<int> hs(nb);
+  if (ok) {
+    die_probe_kernel<<<nb, 32>>>(buf, nlines, stride, lat, sm);
+    die_probe_kernel<<<nb, 32>>>(buf, nlines, stride, lat, sm);
+    ok = cudaDeviceSynchronize() == cudaSuccess &&
+         cudaMemcpy(h.data(), lat, h.size() * 4, cudaMemcpyDeviceToHost) == cudaSuccess &&
+         cudaMemcpy(hs.data(), sm, nb * 4, cudaMemcpyDeviceToHost) == cudaSuccess;
+  }
+  cudaFree(buf);
+  cudaFree(lat);
+  cudaFree(sm);
+  if (!ok) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  // per-SM mean latency vector (centred), correlation with SM 0's vector
+  std::vector<double> M((size_t)num_sms * nlines, 0.0);
+  std::vector<int> n(num_sms, 0);
+  for (int b = 0; b < nb; ++b) {
+    const int id = hs[b];
+    if (id < 0 || id >= num_sms) return nullptr;
+    n[id]++;
+    for (int i = 0; i < nlines; ++i) M[(size_t)id * nlines + i] += h[(size_t)b * nlines + i];
+  }
+  for (int id = 0; id < num_sms; ++id) {
+    if (!n[id]) return nullptr;
+    double mean = 0;
+    for (int i = 0; i < nlines; ++i) mean += (M[(size_t)id * nlines + i] /= n[id]);
+    mean /= nlines;
+    for (int i = 0; i < nlines; ++i) M[(size_t)id * nlines + i] -= mean;
+  }
+  auto corr = [&](int a, int b) {
+    double ab = 0, aa = 0, bb = 0;
+    for (int i = 0; i < nlines; ++i) {
+      const double x = M[(size_t)a * nlines + i], y = M[(size_t)b * nlines + i];
+      ab += x * y;
+      aa += x * x;
+      bb += y * y;
+    }
+    return ab / std::sqrt(aa * bb + 1e-30);
+  };
+  std::vector<int> die(num_sms);
+  int n1 = 0;
+  double worst = 1.0;
+  for (int id = 0; id < num_sms; ++id) {
+    const double c = corr(0, id);
+    die[id] = c > 0 ? 0 : 1;
+    n1 += die[id];
+    worst = std::min(worst, std::fabs(c));
+  }
+  // a clean two-way split is required; otherwise stay die-agnostic
+  if (worst < 0.3 || n1 < num_sms / 4 || n1 > 3 * num_sms / 4) return nullptr;
+  for (int id = 0; id + 1 < num_sms; id += 2)  // CTA pairs (clusters) never straddle dies
+    if (die[id] != die[id + 1]) return nullptr;
+  if (cudaMalloc(&d_map, num_sms * sizeof(int)) != cudaSuccess) return d_map = nullptr;
+  cudaMemcpy(d_map, die.data(), num_sms * sizeof(int), cudaMemcpyHostToDevice);
+  return d_map;
+}
+
 static int g_num_sms = 0;
 
 // epi: EPI_SWIGLU (B = W13 interleaved [2ff, K], out = h [rows_cap, ff])
@@ -456,9 +584,16 @@ int launch_grouped_gemm(int epi, const void* A, long long rows_cap, int K, const
     if (cudaMalloc(&counters, 1024 * sizeof(int)) != cudaSuccess) return -2;
     if (cudaMemset(counters, 0, 1024 * sizeof(int)) != cudaSuccess) return -2;
   }
-  int* counter = counters + (seq++ % 1024);
+  const unsigned slot = seq++ % 1024;
+  int* counter = counters + slot;
   if (cudaMemsetAsync(counter, 0, sizeof(int), s) != cudaSuccess) return -2;
   p.tile_counter = counter;
+  static unsigned long long* words = nullptr;
+  if (!words) {
+    if (cudaMalloc(&words, 1024 * sizeof(unsigned long long)) != cudaSuccess) return -2;
+  }
+  p.tile_word = words + slot;
+  if (cudaMemsetAsync(p.tile_word, 0, sizeof(unsigned long long), s) != cudaSuccess) return -2;
   p.offsets = offsets;
   p.out = out;
   p.ldo = ldo;
@@ -472,6 +607,7 @@ int launch_grouped_gemm(int epi, const void* A, long long rows_cap, int K, const
     cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
     if (g_num_sms <= 0) g_num_sms = 148;
   }
+  p.die_map = die_map_device(g_num_sms);
   int grid = (g_num_sms / 2) * 2;
   if (max_ctas >= 2 && max_ctas < grid) grid = (max_ctas / 2) * 2;
   cudaError_t err;
