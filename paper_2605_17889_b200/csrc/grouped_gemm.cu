@@ -435,8 +435,8 @@ static int get_map(CUtensorMap* out, const void* ptr, unsigned long long rows, u
 // Raster band (n-tiles per band): tiles run expert -> n-band -> m -> n, so the
 // B band (band x 256 rows x K) is shared by every m-tile of the expert and A
 // is re-read once per band.  Pick the widest band that divides n_tiles and
-// whose B band stays within an L2 budget (~32 MB); e.g. C2 K3 (K=4096): 16,
-// C2 K4 (K=14336): 4, C4 K3 (11 n-tiles, K=2048): 11.  COX_GEMM_BAND_K3 /
+// whose B band stays within an L2 budget (32 MB for K3, 64 MB for K4); e.g.
+// C2 K3 (K=4096): 16, C2 K4 (K=14336): 8, C4 K3 (11 n-tiles, K=2048): 11.  COX_GEMM_BAND_K3 /
 // COX_GEMM_BAND_K4 override for experiments.
 static int pick_band(int epi, int n_tiles, int K) {
   static int env_band[2] = {
@@ -445,7 +445,10 @@ static int pick_band(int epi, int n_tiles, int K) {
   const int want = env_band[epi ? 1 : 0];
   if (want > 0 && n_tiles % want == 0) return want;
   const long long per_tile = (long long)GM_BN * K * 2;
-  long long max_band = (32LL << 20) / per_tile;
+  // measured (ncu dram__bytes_read, C2): K3 band 16 -> 33 GB (28 -> 57 GB);
+  // K4 band 4/8/16 -> 77/69/143 GB, so the long-K down projection gets a larger budget
+  const long long budget = epi ? (64LL << 20) : (32LL << 20);
+  long long max_band = budget / per_tile;
   if (max_band < 1) max_band = 1;
   for (int b = (int)(max_band < n_tiles ? max_band : n_tiles); b >= 1; --b)
     if (n_tiles % b == 0) return b;
