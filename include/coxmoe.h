@@ -119,10 +119,11 @@ int cox_combine(const void* y_perm, const int32_t* dst, const float* w, int T, i
  * DEVICE arrays of `world` peer addresses (e.g. CUDA symmetric memory).
  *   cox_ep_counts_put: counts[E] -> counts_all[rank][E] on every peer.
  *   cox_ep_offsets:    counts_all[world][E] -> my receive segments
- *                      recv_seg[world*E/world + 1] ((source, local expert)
- *                      order) and send_base[E] (row of my first pair of
- *                      expert e on its owner); overflow[0] = 1 if any owner
- *                      would receive more than cap rows.
+ *                      recv_seg[E/world + 1] (one per local expert: all
+ *                      sources' rows, source-rank order) and send_base[E]
+ *                      (row of my first pair of expert e on its owner);
+ *                      overflow[0] = 1 if any owner would receive more than
+ *                      cap rows.
  *   cox_ep_dispatch:   stores x[t] into the owners' receive buffers at
  *                      send_base[e] + (dst_local - offsets_local[e]);
  *                      route_row[T,k] records the row for the combine.

@@ -9,10 +9,11 @@
 // HBM disappear, and no host synchronisation is needed (the receive layout is
 // computed on the device from an all-gathered count matrix).
 //
-// Receive layout on owner r (identical to the NCCL path, ep.py): segments in
-// (source rank s, local expert l) order, g = s*L + l; inside a segment the
-// rows are in the source's ascending token order — so per-expert row order
-// is the global token order and results are bit-identical to one GPU.
+// Receive layout on owner r: one contiguous segment per local expert l, made
+// of every source's rows in source-rank order, each source's rows in its
+// ascending token order — so the per-expert row order is the global token
+// order (results bit-identical to one GPU) and each local expert is ONE
+// grouped-GEMM group (its weights stream once per layer).
 #include "common.cuh"
 
 namespace cox {
@@ -26,9 +27,11 @@ __global__ void ep_counts_put_kernel(const int32_t* __restrict__ counts, int E, 
   }
 }
 
-// From counts_all [G][E]: my receive segments (G*L+1 offsets) and, for each of
-// my experts e (owned by r = e / L), the row where my first (t, e) pair lands
-// on r.  overflow[0] is set if any owner would receive more than `cap` rows.
+// From counts_all [G][E]: my receive segments (L+1 offsets, one per local
+// expert: every source's rows of local expert l are contiguous, sources in
+// rank order) and, for each of my experts e (owned by r = e / L, l = e % L),
+// the row where my first (t, e) pair lands on r.  overflow[0] is set if any
+// owner would receive more than `cap` rows.
 __global__ void ep_offsets_kernel(const int32_t* __restrict__ counts_all, int G, int E, int rank, long long cap,
                                   int32_t* __restrict__ recv_seg, int32_t* __restrict__ send_base,
                                   int32_t* __restrict__ overflow) {
@@ -36,18 +39,16 @@ __global__ void ep_offsets_kernel(const int32_t* __restrict__ counts_all, int G,
   const int L = E / G;
   long long run = 0;
   recv_seg[0] = 0;
-  for (int s = 0; s < G; ++s)
-    for (int l = 0; l < L; ++l) {
-      run += counts_all[s * E + rank * L + l];
-      recv_seg[s * L + l + 1] = (int32_t)run;
-    }
+  for (int l = 0; l < L; ++l) {
+    for (int s = 0; s < G; ++s) run += counts_all[s * E + rank * L + l];
+    recv_seg[l + 1] = (int32_t)run;
+  }
   for (int r = 0; r < G; ++r) {
     long long base = 0;
-    for (int s = 0; s < G; ++s)
-      for (int l = 0; l < L; ++l) {
-        const int c = counts_all[s * E + r * L + l];
+    for (int l = 0; l < L; ++l)
+      for (int s = 0; s < G; ++s) {
         if (s == rank) send_base[r * L + l] = (int32_t)base;
-        base += c;
+        base += counts_all[s * E + r * L + l];
       }
     if (base > cap) overflow[0] = 1;
   }

@@ -210,7 +210,8 @@ class FusedEPMoELayer:
     matrix; the symmetric-memory barrier (stream-ordered, system-scope
     release/acquire on signal pads) separates the phases:
         K1 route -> K2 ranks -> counts put -> barrier -> offsets + dispatch
-        -> barrier -> K3/K4 on received rows -> barrier -> fused combine.
+        -> barrier -> K3/K4 on received rows (one group per local expert)
+        -> barrier -> fused combine.
     The next layer's counts put is ordered after this combine on every rank,
     so buffers are never overwritten while a peer still reads them.
     """
@@ -227,8 +228,8 @@ class FusedEPMoELayer:
         if self.E % self.G:
             raise ValueError(f"{self.E} experts cannot be sharded evenly over {self.G} ranks")
         self.L = self.E // self.G
-        if self.G * self.L > 64:
-            raise ValueError("at most 64 (source, expert) groups per grouped GEMM")
+        if self.L > 64:
+            raise ValueError("at most 64 local experts per grouped GEMM")
         self.k = int(top_k)
         self.mode = MODES[mode]
         self.w = weights
@@ -261,7 +262,7 @@ class FusedEPMoELayer:
         self.offsets = torch.empty((E + 1,), **i32)
         self.dst = torch.empty((T, k), **i32)
         self.route_row = torch.empty((T, k), **i32)
-        self.recv_seg = torch.empty((G * self.L + 1,), **i32)
+        self.recv_seg = torch.empty((self.L + 1,), **i32)
         self.send_base = torch.empty((E,), **i32)
         self.overflow = torch.zeros((1,), **i32)
         self.ws = torch.empty((max(16, ops.permute_workspace_bytes(T, E)),), dtype=torch.uint8, device=dev)
@@ -285,15 +286,15 @@ class FusedEPMoELayer:
         ops.ep_dispatch(self.idx, self.dst, self.offsets, self.send_base, x, G, self.cap, self.peer_recv,
                         self.route_row)
         self._barrier()
-        groups = list(range(G * L))
+        groups = list(range(L))  # one group per local expert (all sources' rows contiguous)
         pe = self.profile_events
         if pe:
             pe["k3"][0].record()
-        ops.grouped_swiglu(self.recv, self.recv_seg, groups, [self.w13[g % L] for g in groups], self.ff, h=self.h)
+        ops.grouped_swiglu(self.recv, self.recv_seg, groups, self.w13, self.ff, h=self.h)
         if pe:
             pe["k3"][1].record()
             pe["k4"][0].record()
-        ops.grouped_down(self.h, self.recv_seg, groups, [self.w2[g % L] for g in groups], self.d, y=self.ysym)
+        ops.grouped_down(self.h, self.recv_seg, groups, self.w2, self.d, y=self.ysym)
         if pe:
             pe["k4"][1].record()
         self._barrier()
