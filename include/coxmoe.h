@@ -79,6 +79,11 @@ int cox_router_topk_ex(const void* x, int x_dtype, const void* wg, int wg_dtype,
 size_t cox_permute_workspace_bytes(int T, int E);
 int cox_permute(const int32_t* idx, int T, int k, int E, int tile_m, const void* x, int d, int32_t* offsets,
                 int32_t* dst, void* x_perm, long long rows_cap, void* workspace, void* stream);
+/* Same, optionally emitting row_tokens[rows_cap]: the source token of every
+ * permuted row (for cox_grouped_swiglu_gather; x_perm may then be NULL). */
+int cox_permute_ex(const int32_t* idx, int T, int k, int E, int tile_m, const void* x, int d, int32_t* offsets,
+                   int32_t* dst, void* x_perm, long long rows_cap, int32_t* row_tokens, void* workspace,
+                   void* stream);
 
 /* K3 — grouped SwiGLU expert GEMM over the coalesced batch:
  *   h[r, :] = silu(x_perm[r] W1_e^T) * (x_perm[r] W3_e^T) for r in segment e.
@@ -98,6 +103,13 @@ int cox_grouped_swiglu(const void* x_perm, long long rows_cap, const int32_t* of
 int cox_grouped_swiglu_ex(const void* x_perm, long long rows_cap, const int32_t* offsets, int n_groups,
                           const int32_t* group_experts, const void* const* w13, int d, int ff, void* h,
                           int max_ctas, void* stream);
+
+/* K3 with gather-fused A loads: permuted row r is read straight from x[T, d]
+ * at row row_tokens[r] (TMA tile::gather4, 4 rows per load), so x_perm is
+ * never materialised.  Same results as cox_grouped_swiglu on x_perm. */
+int cox_grouped_swiglu_gather(const void* x, long long T, const int32_t* row_tokens, long long rows_cap,
+                              const int32_t* offsets, int n_groups, const int32_t* group_experts,
+                              const void* const* w13, int d, int ff, void* h, int max_ctas, void* stream);
 
 /* K4 — grouped down projection: y_perm[r] = h[r] W2_e^T.  w2[g]: [d, ff] bf16.
  * ff % 64 == 0, d % 256 == 0. */

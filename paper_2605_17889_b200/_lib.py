@@ -31,7 +31,7 @@ EXPORTS = (
     "cox_last_error", "cox_version", "cox_device_check", "cox_router_topk", "cox_permute_workspace_bytes",
     "cox_permute", "cox_grouped_swiglu", "cox_grouped_down", "cox_combine", "cox_interleave_w13",
     "cox_ep_counts_put", "cox_ep_offsets", "cox_ep_dispatch", "cox_ep_combine", "cox_grouped_swiglu_ex",
-    "cox_grouped_down_ex", "cox_router_topk_ex",
+    "cox_grouped_down_ex", "cox_router_topk_ex", "cox_permute_ex", "cox_grouped_swiglu_gather",
 )
 
 _lock = threading.Lock()
@@ -55,6 +55,12 @@ def _declare(L):
     L.cox_router_topk_ex.restype = c_int
     L.cox_router_topk_ex.argtypes = [c_void_p, c_int, c_void_p, c_int, c_int, c_int, c_int, c_int, c_int,
                                      c_void_p, c_void_p, c_void_p, c_void_p]
+    L.cox_permute_ex.restype = c_int
+    L.cox_permute_ex.argtypes = [c_void_p, c_int, c_int, c_int, c_int, c_void_p, c_int, c_void_p, c_void_p,
+                                 c_void_p, c_ll, c_void_p, c_void_p, c_void_p]
+    L.cox_grouped_swiglu_gather.restype = c_int
+    L.cox_grouped_swiglu_gather.argtypes = [c_void_p, c_ll, c_void_p, c_ll, c_void_p, c_int, c_void_p, c_void_p,
+                                            c_int, c_int, c_void_p, c_int, c_void_p]
     L.cox_permute_workspace_bytes.restype = c_size_t
     L.cox_permute_workspace_bytes.argtypes = [c_int, c_int]
     L.cox_permute.restype = c_int

@@ -12,10 +12,11 @@ int launch_router(const void* x, int x_is_bf16, const void* wg, int wg_is_bf16, 
                   int mode, int32_t* idx, float* w, int32_t* counts, cudaStream_t s);
 size_t permute_workspace_bytes(int T, int E);
 int launch_permute(const int32_t* idx, int T, int k, int E, int tile_m, const void* x, int d, int32_t* offsets,
-                   int32_t* dst, void* x_perm, void* workspace, cudaStream_t s);
+                   int32_t* dst, void* x_perm, void* workspace, cudaStream_t s, int32_t* row_tokens = nullptr,
+                   long long rows_cap = 0);
 int launch_grouped_gemm(int epi, const void* A, long long rows_cap, int K, const int32_t* offsets, int n_groups,
                         const int32_t* group_expert, const void* const* B, int N, void* out, long long ldo,
-                        int max_ctas, cudaStream_t s);
+                        int max_ctas, cudaStream_t s, const int32_t* a_rows = nullptr, long long a_rows_cap = 0);
 int launch_combine(const void* y_perm, const int32_t* dst, const float* w, int T, int k, int d, const void* shared,
                    void* out, int out_is_bf16, cudaStream_t s);
 
@@ -105,8 +106,8 @@ int cox_router_topk(const void* x, int x_dtype, const float* wg, int T, int d, i
 
 size_t cox_permute_workspace_bytes(int T, int E) { return cox::permute_workspace_bytes(T, E); }
 
-int cox_permute(const int32_t* idx, int T, int k, int E, int tile_m, const void* x, int d, int32_t* offsets,
-                int32_t* dst, void* x_perm, long long rows_cap, void* workspace, void* stream) {
+int cox_permute_ex(const int32_t* idx, int T, int k, int E, int tile_m, const void* x, int d, int32_t* offsets,
+                   int32_t* dst, void* x_perm, long long rows_cap, int32_t* row_tokens, void* workspace, void* stream) {
   if (T < 0 || k < 1 || k > 8 || E < 1 || E > 256 || tile_m < 1 || d <= 0 || d % 8)
     return fail(COX_EINVAL, "cox_permute: need 1<=k<=8, 1<=E<=256, tile_m>=1, d%%8==0");
   if (rows_cap < (long long)T * k + (long long)E * (tile_m - 1))
@@ -116,8 +117,13 @@ int cox_permute(const int32_t* idx, int T, int k, int E, int tile_m, const void*
     return fail(COX_EINVAL, "cox_permute: x/x_perm must be 16-byte aligned");
   if (!workspace || !offsets) return fail(COX_EINVAL, "cox_permute: null workspace/offsets");
   int rc = cox::launch_permute(idx, T, k, E, tile_m, x, d, offsets, dst, x_perm, workspace,
-                               static_cast<cudaStream_t>(stream));
+                               static_cast<cudaStream_t>(stream), row_tokens, rows_cap);
   return cuda_status(rc, "cox_permute");
+}
+
+int cox_permute(const int32_t* idx, int T, int k, int E, int tile_m, const void* x, int d, int32_t* offsets,
+                int32_t* dst, void* x_perm, long long rows_cap, void* workspace, void* stream) {
+  return cox_permute_ex(idx, T, k, E, tile_m, x, d, offsets, dst, x_perm, rows_cap, nullptr, workspace, stream);
 }
 
 static int check_groups(const char* fn, int n_groups, const int32_t* group_experts, const void* const* w) {
@@ -141,6 +147,20 @@ int cox_grouped_swiglu_ex(const void* x_perm, long long rows_cap, const int32_t*
   int rc = cox::launch_grouped_gemm(0, x_perm, rows_cap, d, offsets, n_groups, group_experts, w13, 2 * ff, h, ff,
                                     max_ctas, static_cast<cudaStream_t>(stream));
   return cuda_status(rc, "cox_grouped_swiglu");
+}
+
+int cox_grouped_swiglu_gather(const void* x, long long T, const int32_t* row_tokens, long long rows_cap,
+                              const int32_t* offsets, int n_groups, const int32_t* group_experts,
+                              const void* const* w13, int d, int ff, void* h, int max_ctas, void* stream) {
+  if (d <= 0 || d % 64 || ff <= 0 || ff % 128)
+    return fail(COX_EINVAL, "cox_grouped_swiglu_gather: need d%%64==0 and ff%%128==0 (d=%d ff=%d)", d, ff);
+  if (T < 1 || rows_cap < 1 || !row_tokens) return fail(COX_EINVAL, "cox_grouped_swiglu_gather: empty input");
+  if (max_ctas < 0 || max_ctas == 1) return fail(COX_EINVAL, "cox_grouped_swiglu_gather: bad max_ctas");
+  if (!aligned16(x) || !aligned16(h)) return fail(COX_EINVAL, "cox_grouped_swiglu_gather: unaligned x/h");
+  if (int rc = check_groups("cox_grouped_swiglu_gather", n_groups, group_experts, w13)) return rc;
+  int rc = cox::launch_grouped_gemm(0, x, T, d, offsets, n_groups, group_experts, w13, 2 * ff, h, ff, max_ctas,
+                                    static_cast<cudaStream_t>(stream), row_tokens, rows_cap);
+  return cuda_status(rc, "cox_grouped_swiglu_gather");
 }
 
 int cox_grouped_swiglu(const void* x_perm, long long rows_cap, const int32_t* offsets, int n_groups,

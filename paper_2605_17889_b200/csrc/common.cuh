@@ -103,6 +103,17 @@ COX_DEV void tma_load_2d_pair(uint32_t dst, const void* map, uint32_t bar, int32
       : "memory");
 }
 
+// 4 arbitrary rows (row coordinates r0..r3) x one box of columns, into this CTA's
+// smem, completing on a barrier of the 2-CTA pair (tile::gather4, sm_100).
+COX_DEV void tma_gather4_pair(uint32_t dst, const void* map, uint32_t bar, int32_t col, int32_t r0, int32_t r1,
+                              int32_t r2, int32_t r3) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(col), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(bar)
+      : "memory");
+}
+
 COX_DEV void tma_load_2d(uint32_t dst, const void* map, uint32_t bar, int32_t c0, int32_t c1) {
   asm volatile(
       "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"

@@ -57,6 +57,8 @@ struct alignas(64) GemmParams {
   CUtensorMap a_map;
   CUtensorMap b_map[GM_MAXG];
   const int32_t* offsets;
+  const int32_t* a_rows;  // gather mode: A row r = x[a_rows[r]] (tile::gather4); nullptr = tiled A
+  long long a_rows_cap;   // entries of a_rows
   int* tile_counter;  // zeroed before launch; dynamic tile scheduler
   unsigned long long* tile_word;  // die-aware mode: (claimed from head) | (claimed from tail) << 32
   const int* die_map;             // SM id -> die (0/1), nullptr = die-agnostic
@@ -221,28 +223,50 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GM_THREADS, 1)
     __syncwarp();
   } else if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
-    if (lane == 0) {
-      uint32_t stage = 0, phase = 0;
-      int si = 0;
-      int t = fetch_tile(si, true);
-      while (t < total) {
-        const TileCoord c = decode_tile(t, s_prefix, s_rows, p.band);
-        const int a_row = s_row0[c.g] + c.m * 2 * GM_BM + (int)rank * GM_BM;
-        const int b_row = c.n * GM_BN + (int)rank * (GM_BN / 2);
-        const CUtensorMap* bmap = &p.b_map[c.g];
-        int t_next = total;
-        for (int kb = 0; kb < nk; ++kb) {
-          mbar_wait(smem_u32(&empty[stage]), phase ^ 1);
-          const uint32_t fb_local = smem_u32(&full[stage]);
-          if (rank == 0) mbar_arrive_expect_tx(fb_local, 2 * (GM_A_BYTES + GM_B_BYTES));
-          const uint32_t fb = mapa(fb_local, 0);
-          tma_load_2d_pair(smem_u32(sA + stage * GM_A_BYTES), &p.a_map, fb, kb * GM_BK, a_row);
-          tma_load_2d_pair(smem_u32(sB + stage * GM_B_BYTES), bmap, fb, kb * GM_BK, b_row);
-          if (++stage == GM_STAGES) { stage = 0; phase ^= 1; }
-          if (kb == 0) t_next = fetch_tile(si, true);  // look ahead: hide the fetch behind this tile
+    // Tiled A: lane 0 issues one A box and one B box per stage.  Gather A
+    // (p.a_rows): the whole warp issues 32 tile::gather4 loads per stage, lane i
+    // fetching token rows a_rows[4i..4i+3] of this CTA's 128 permuted rows
+    // straight from x — no materialised x_perm.  Correct but ~3x slower at C2
+    // (gather issue rate; A re-fetched per n-tile), so it is opt-in only.
+    const bool gather = p.a_rows != nullptr;
+    uint32_t stage = 0, phase = 0;
+    int si = 0;
+    int t = lane == 0 ? fetch_tile(si, true) : 0;
+    t = __shfl_sync(0xffffffffu, t, 0);
+    while (t < total) {
+      const TileCoord c = decode_tile(t, s_prefix, s_rows, p.band);
+      const int a_row = s_row0[c.g] + c.m * 2 * GM_BM + (int)rank * GM_BM;
+      const int b_row = c.n * GM_BN + (int)rank * (GM_BN / 2);
+      const CUtensorMap* bmap = &p.b_map[c.g];
+      int rr[4] = {0, 0, 0, 0};
+      if (gather) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const long long r = (long long)a_row + lane * 4 + q;
+          rr[q] = r < p.a_rows_cap ? p.a_rows[r] : 0;
         }
-        t = t_next;
       }
+      int t_next = total;
+      for (int kb = 0; kb < nk; ++kb) {
+        if (lane == 0) mbar_wait(smem_u32(&empty[stage]), phase ^ 1);
+        __syncwarp();
+        const uint32_t fb_local = smem_u32(&full[stage]);
+        const uint32_t fb = mapa(fb_local, 0);
+        if (lane == 0) {
+          if (rank == 0) mbar_arrive_expect_tx(fb_local, 2 * (GM_A_BYTES + GM_B_BYTES));
+          if (!gather) tma_load_2d_pair(smem_u32(sA + stage * GM_A_BYTES), &p.a_map, fb, kb * GM_BK, a_row);
+          tma_load_2d_pair(smem_u32(sB + stage * GM_B_BYTES), bmap, fb, kb * GM_BK, b_row);
+        }
+        if (gather)
+          tma_gather4_pair(smem_u32(sA + stage * GM_A_BYTES) + lane * 512, &p.a_map, fb, kb * GM_BK, rr[0], rr[1],
+                           rr[2], rr[3]);
+        if (++stage == GM_STAGES) { stage = 0; phase ^= 1; }
+        if (kb == 0) {  // look ahead: hide the fetch behind this tile
+          int tn = lane == 0 ? fetch_tile(si, true) : 0;
+          t_next = __shfl_sync(0xffffffffu, tn, 0);
+        }
+      }
+      t = t_next;
     }
     __syncwarp();
   } else if (warp == 1) {
@@ -569,12 +593,13 @@ static int g_num_sms = 0;
 //      EPI_STORE  (B = W2 [N, K],                out = y [rows_cap, N])
 int launch_grouped_gemm(int epi, const void* A, long long rows_cap, int K, const int32_t* offsets, int n_groups,
                         const int32_t* group_expert, const void* const* B, int N, void* out, long long ldo,
-                        int max_ctas, cudaStream_t s) {
+                        int max_ctas, cudaStream_t s, const int32_t* a_rows, long long a_rows_cap) {
   if (n_groups <= 0) return 0;
   static GemmParams p;  // large (8.6 KB): built in static storage, copied at launch
   static std::mutex mu;
   std::lock_guard<std::mutex> lk(mu);
-  int rc = get_map(&p.a_map, A, (unsigned long long)rows_cap, (unsigned long long)K, GM_BM);
+  // gather mode: A is x [rows_cap = T, K] read row by row (box of 1 row x 64 cols)
+  int rc = get_map(&p.a_map, A, (unsigned long long)rows_cap, (unsigned long long)K, a_rows ? 1u : (unsigned)GM_BM);
   if (rc) return rc;
   for (int g = 0; g < n_groups; ++g) {
     rc = get_map(&p.b_map[g], B[g], (unsigned long long)N, (unsigned long long)K, GM_BN / 2);
@@ -598,6 +623,8 @@ int launch_grouped_gemm(int epi, const void* A, long long rows_cap, int K, const
   p.tile_word = words + slot;
   if (cudaMemsetAsync(p.tile_word, 0, sizeof(unsigned long long), s) != cudaSuccess) return -2;
   p.offsets = offsets;
+  p.a_rows = a_rows;
+  p.a_rows_cap = a_rows_cap;
   p.out = out;
   p.ldo = ldo;
   p.n_groups = n_groups;

@@ -71,7 +71,7 @@ __global__ void __launch_bounds__(1024) perm_scan(const int32_t* __restrict__ bl
 __global__ void __launch_bounds__(PM_TB) perm_scatter(const int32_t* __restrict__ idx, int T, int k, int E,
                                                        const int32_t* __restrict__ block_base,
                                                        const int32_t* __restrict__ offsets,
-                                                       int32_t* __restrict__ dst) {
+                                                       int32_t* __restrict__ dst, int32_t* __restrict__ row_tokens) {
   __shared__ int s_wcnt[PM_TB / 32][256];
   __shared__ int s_wbase[PM_TB / 32][256];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -108,7 +108,10 @@ __global__ void __launch_bounds__(PM_TB) perm_scatter(const int32_t* __restrict_
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
     dj[j] = (ej[j] >= 0) ? s_wbase[warp][ej[j]] + rj[j] : -1;
-    if (j < k && valid) dst[t * k + j] = dj[j];
+    if (j < k && valid) {
+      dst[t * k + j] = dj[j];
+      if (row_tokens) row_tokens[dj[j]] = (int32_t)t;
+    }
   }
 }
 
@@ -162,7 +165,8 @@ size_t permute_workspace_bytes(int T, int E) {
 }
 
 int launch_permute(const int32_t* idx, int T, int k, int E, int tile_m, const void* x, int d, int32_t* offsets,
-                   int32_t* dst, void* x_perm, void* workspace, cudaStream_t s) {
+                   int32_t* dst, void* x_perm, void* workspace, cudaStream_t s, int32_t* row_tokens,
+                   long long rows_cap) {
   long nb = (T + PM_TB - 1) / PM_TB;
   int32_t* block_counts = static_cast<int32_t*>(workspace);
   int32_t* block_base = block_counts + (nb > 0 ? nb : 1) * E;
@@ -173,7 +177,9 @@ int launch_permute(const int32_t* idx, int T, int k, int E, int tile_m, const vo
   }
   perm_hist<<<(int)nb, PM_TB, 0, s>>>(idx, T, k, E, block_counts);
   perm_scan<<<1, 1024, 0, s>>>(block_counts, (int)nb, E, tile_m, block_base, offsets, seg_counts);
-  perm_scatter<<<(int)nb, PM_TB, 0, s>>>(idx, T, k, E, block_base, offsets, dst);
+  if (row_tokens && tile_m > 1)  // padding rows gather token 0 (computed, never combined)
+    if (cudaMemsetAsync(row_tokens, 0, sizeof(int32_t) * rows_cap, s) != cudaSuccess) return -2;
+  perm_scatter<<<(int)nb, PM_TB, 0, s>>>(idx, T, k, E, block_base, offsets, dst, row_tokens);
   long cb = (T + 7) / 8;
   if (cb > 148L * 16) cb = 148L * 16;
   if (x_perm) perm_copy<<<(int)cb, 256, 0, s>>>(dst, T, k, static_cast<const __nv_bfloat16*>(x), d,

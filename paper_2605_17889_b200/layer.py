@@ -7,6 +7,7 @@ expert parallelism build on the same stage functions (executor.py, ep.py).
 """
 from __future__ import annotations
 
+import os
 from dataclasses import dataclass
 
 import torch
@@ -30,13 +31,15 @@ class StageBuffers:
     y: torch.Tensor
     out: torch.Tensor
     workspace: torch.Tensor
+    row_tokens: torch.Tensor | None = None  # gather mode: source token of every permuted row
+    x_ref: torch.Tensor | None = None       # gather mode: the step's input (A source of K3)
     shared_offsets: torch.Tensor | None = None
     shared_h: torch.Tensor | None = None
     shared_y: torch.Tensor | None = None
 
 
 def alloc_buffers(T: int, d: int, ff: int, E: int, k: int, tile_m: int, device, out_dtype=torch.bfloat16,
-                  shared_ff: int = 0) -> StageBuffers:
+                  shared_ff: int = 0, gather_a: bool = False) -> StageBuffers:
     cap = ops.rows_capacity(T, k, E, tile_m)
     bf = torch.bfloat16
     b = StageBuffers(
@@ -46,12 +49,14 @@ def alloc_buffers(T: int, d: int, ff: int, E: int, k: int, tile_m: int, device, 
         counts=torch.empty((E,), dtype=torch.int32, device=device),
         offsets=torch.empty((E + 1,), dtype=torch.int32, device=device),
         dst=torch.empty((T, k), dtype=torch.int32, device=device),
-        x_perm=torch.empty((cap, d), dtype=bf, device=device),
+        x_perm=torch.empty((1 if gather_a else cap, d), dtype=bf, device=device),
         h=torch.empty((cap, ff), dtype=bf, device=device),
         y=torch.empty((cap, d), dtype=bf, device=device),
         out=torch.empty((T, d), dtype=out_dtype, device=device),
         workspace=torch.empty((max(16, ops.permute_workspace_bytes(T, E)),), dtype=torch.uint8, device=device),
     )
+    if gather_a:
+        b.row_tokens = torch.empty((cap,), dtype=torch.int32, device=device)
     if shared_ff:
         b.shared_offsets = torch.tensor([0, T], dtype=torch.int32, device=device)
         b.shared_h = torch.empty((max(T, 1), shared_ff), dtype=bf, device=device)
@@ -63,7 +68,7 @@ class MoELayer:
     """One MoE layer's expert stage with every expert resident in HBM."""
 
     def __init__(self, weights: LayerWeights, top_k: int, mode: str = "mixtral", tile_m: int = 1,
-                 out_dtype=torch.bfloat16):
+                 out_dtype=torch.bfloat16, gather_a: bool | None = None):
         if mode not in MODES:
             raise ValueError(f"mode must be one of {sorted(MODES)}")
         self.wts = weights
@@ -71,6 +76,10 @@ class MoELayer:
         self.mode = MODES[mode]
         self.tile_m = int(tile_m)
         self.out_dtype = out_dtype
+        # gather-fused A loads (TMA tile::gather4): K3 reads token rows from x directly
+        if gather_a is None:
+            gather_a = os.environ.get("COX_GATHER_A", "0") == "1"
+        self.gather_a = bool(gather_a)
         self.E = weights.num_experts
         self.d = weights.hidden_dim
         self.ff = weights.expert_dim
@@ -97,20 +106,32 @@ class MoELayer:
         if self._bufs is None or self._bufs.T != T:
             self._bufs = None
             self._bufs = alloc_buffers(T, self.d, self.ff, self.E, self.k, self.tile_m, device, self.out_dtype,
-                                       self.shared_ff)
+                                       self.shared_ff, self.gather_a)
         return self._bufs
 
     # --- stages (all stream-ordered on the current stream) -------------------
     def route(self, x: torch.Tensor, b: StageBuffers):
         ops.router_topk(x, self.wg_router, self.k, self.mode, out=(b.idx, b.w, b.counts))
-        ops.permute(b.idx, x, self.E, self.tile_m, out=(b.offsets, b.dst, b.x_perm), workspace=b.workspace)
+        if self.gather_a:
+            ops.permute(b.idx, x, self.E, self.tile_m, out=(b.offsets, b.dst, None), workspace=b.workspace,
+                        copy_rows=False, row_tokens=b.row_tokens)
+            b.x_ref = x
+        else:
+            ops.permute(b.idx, x, self.E, self.tile_m, out=(b.offsets, b.dst, b.x_perm), workspace=b.workspace)
+
+    def _k3(self, b: StageBuffers, groups, w13, max_ctas: int = 0):
+        if self.gather_a:
+            ops.grouped_swiglu_gather(b.x_ref, b.row_tokens, b.offsets, groups, w13, self.ff, h=b.h,
+                                      max_ctas=max_ctas)
+        else:
+            ops.grouped_swiglu(b.x_perm, b.offsets, groups, w13, self.ff, h=b.h, max_ctas=max_ctas)
 
     def experts(self, b: StageBuffers, groups=None, w13=None, w2=None):
         groups = self.groups if groups is None else groups
         pe = self.profile_events
         if pe:
             pe["k3"][0].record()
-        ops.grouped_swiglu(b.x_perm, b.offsets, groups, self.w13_list if w13 is None else w13, self.ff, h=b.h)
+        self._k3(b, groups, self.w13_list if w13 is None else w13)
         if pe:
             pe["k3"][1].record()
             pe["k4"][0].record()
@@ -149,8 +170,7 @@ class MoELayer:
                 ops.grouped_down(b.shared_h, b.shared_offsets, [0], [self.wts.shared_w2], self.d, y=b.shared_y,
                                  max_ctas=self.SHARED_SIDE_CTAS)
             self.route(x, b)
-            ops.grouped_swiglu(b.x_perm, b.offsets, self.groups, self.w13_list, self.ff, h=b.h,
-                               max_ctas=-(-(148 - self.SHARED_SIDE_CTAS) // 2) * 2)
+            self._k3(b, self.groups, self.w13_list, max_ctas=-(-(148 - self.SHARED_SIDE_CTAS) // 2) * 2)
             ops.grouped_down(b.h, b.offsets, self.groups, self.w2_list, self.d, y=b.y,
                              max_ctas=-(-(148 - self.SHARED_SIDE_CTAS) // 2) * 2)
             main.wait_stream(side)
@@ -192,7 +212,7 @@ class MoELayer:
             n = xs.shape[0]
             if n not in subs:
                 subs[n] = MoELayer(self.wts, self.k, "mixtral" if self.mode == 0 else "deepseek", self.tile_m,
-                                   self.out_dtype)
+                                   self.out_dtype, self.gather_a)
             subs[n].forward(xs, out=out[s0:s0 + n])
         return out
 
@@ -258,9 +278,14 @@ class MoELayer:
         ev[0].record()
         ops.router_topk(x, self.wg_router, self.k, self.mode, out=(b.idx, b.w, b.counts))
         ev[1].record()
-        ops.permute(b.idx, x, self.E, self.tile_m, out=(b.offsets, b.dst, b.x_perm), workspace=b.workspace)
+        if self.gather_a:
+            ops.permute(b.idx, x, self.E, self.tile_m, out=(b.offsets, b.dst, None), workspace=b.workspace,
+                        copy_rows=False, row_tokens=b.row_tokens)
+            b.x_ref = x
+        else:
+            ops.permute(b.idx, x, self.E, self.tile_m, out=(b.offsets, b.dst, b.x_perm), workspace=b.workspace)
         ev[2].record()
-        ops.grouped_swiglu(b.x_perm, b.offsets, self.groups, self.w13_list, self.ff, h=b.h)
+        self._k3(b, self.groups, self.w13_list)
         ev[3].record()
         ops.grouped_down(b.h, b.offsets, self.groups, self.w2_list, self.d, y=b.y)
         ev[4].record()

@@ -85,7 +85,7 @@ def rows_capacity(T: int, k: int, E: int, tile_m: int = 1) -> int:
 
 
 def permute(idx: torch.Tensor, x: torch.Tensor, E: int, tile_m: int = 1, out=None, workspace=None, stream=None,
-            copy_rows: bool = True):
+            copy_rows: bool = True, row_tokens: torch.Tensor | None = None):
     """K2: -> (offsets [E+1] int32, dst [T,k] int32, x_perm [rows_cap, d] bf16 or None).
 
     copy_rows=False computes offsets/dst only (the fused EP dispatch moves the rows)."""
@@ -107,10 +107,15 @@ def permute(idx: torch.Tensor, x: torch.Tensor, E: int, tile_m: int = 1, out=Non
     if workspace is None:
         workspace = torch.empty((permute_workspace_bytes(T, E),), dtype=torch.uint8, device=x.device)
     L = _lib.lib()
-    _lib.check(L.cox_permute(idx.data_ptr(), T, k, E, tile_m, x.data_ptr(), d, offsets.data_ptr(), dst.data_ptr(),
-                             x_perm.data_ptr() if x_perm is not None else None,
-                             x_perm.shape[0] if x_perm is not None else cap, workspace.data_ptr(), _stream(stream)),
-               "cox_permute")
+    if row_tokens is not None:
+        _need(row_tokens, "row_tokens", torch.int32, 1)
+        if row_tokens.numel() < cap:
+            raise ValueError(f"row_tokens needs {cap} entries")
+    _lib.check(L.cox_permute_ex(idx.data_ptr(), T, k, E, tile_m, x.data_ptr(), d, offsets.data_ptr(), dst.data_ptr(),
+                                x_perm.data_ptr() if x_perm is not None else None,
+                                x_perm.shape[0] if x_perm is not None else cap,
+                                row_tokens.data_ptr() if row_tokens is not None else None, workspace.data_ptr(),
+                                _stream(stream)), "cox_permute")
     return offsets, dst, x_perm
 
 
@@ -133,6 +138,29 @@ def grouped_swiglu(x_perm: torch.Tensor, offsets: torch.Tensor, group_experts: S
     _lib.check(L.cox_grouped_swiglu_ex(x_perm.data_ptr(), rows, offsets.data_ptr(), len(group_experts),
                                        _ids(group_experts), _ptrs(w13), d, ff, h.data_ptr(), max_ctas,
                                        _stream(stream)), "cox_grouped_swiglu")
+    return h
+
+
+def grouped_swiglu_gather(x: torch.Tensor, row_tokens: torch.Tensor, offsets: torch.Tensor,
+                          group_experts: Sequence[int], w13: Sequence[torch.Tensor], ff: int, h: torch.Tensor,
+                          stream=None, max_ctas: int = 0):
+    """K3 with gather-fused A loads: row r of the grouped GEMM is x[row_tokens[r]]."""
+    _need(x, "x", _BF16, 2)
+    _need(row_tokens, "row_tokens", torch.int32, 1)
+    _need(offsets, "offsets", torch.int32, 1)
+    _need(h, "h", _BF16, 2)
+    T, d = x.shape
+    for i, w in enumerate(w13):
+        _need(w, f"w13[{i}]", _BF16, 2)
+        if tuple(w.shape) != (2 * ff, d):
+            raise ValueError(f"w13[{i}] must be [2*ff, d] = [{2 * ff}, {d}]")
+    if len(w13) != len(group_experts):
+        raise ValueError("one weight per group")
+    L = _lib.lib()
+    _lib.check(L.cox_grouped_swiglu_gather(x.data_ptr(), T, row_tokens.data_ptr(), row_tokens.numel(),
+                                           offsets.data_ptr(), len(group_experts), _ids(group_experts), _ptrs(w13),
+                                           d, ff, h.data_ptr(), max_ctas, _stream(stream)),
+               "cox_grouped_swiglu_gather")
     return h
 
 
