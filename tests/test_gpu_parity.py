@@ -375,3 +375,32 @@ def test_gather_a_identical_to_materialised_permute(T, d, ff, E, k, mode, shared
     dst = g.buffers(T, DEV).dst.cpu().numpy()
     for t in range(0, T, max(1, T // 50)):
         assert (rt[dst[t]] == t).all()
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_random_configs_vs_oracle(seed):
+    """Seeded random configurations: d in {256..1024}, ff in multiples of 128, E in
+    {2..32}, k in 1..min(E,6), ragged T, both routing modes, optional skew (a mean
+    direction that concentrates routing on a few experts -> ragged and empty segments)."""
+    rng = np.random.default_rng(1000 + seed)
+    d = int(rng.choice([256, 512, 768, 1024]))
+    ff = 128 * int(rng.integers(1, 5))
+    E = int(rng.choice([2, 3, 4, 8, 16, 32]))
+    k = int(rng.integers(1, min(E, 6) + 1))
+    T = int(rng.integers(1, 1500))
+    mode = "mixtral" if rng.random() < 0.5 else "deepseek"
+    wts = make_layer_weights(E, d, ff, seed=seed, device=DEV, keep_split=True)
+    x = make_tokens(T, d, seed=seed + 7, device=DEV).float()
+    if rng.random() < 0.5:  # skew toward one expert's router direction
+        x += 2.0 * d ** 0.5 * wts.wg[int(rng.integers(0, E))]
+    x = x.to(torch.bfloat16)
+    layer = MoELayer(wts, k, mode)
+    out = layer(x)
+    torch.cuda.synchronize()
+    f = lambda t: t.float().cpu().numpy()  # noqa: E731
+    ref = O.moe_layer(f(x), f(wts.wg), f(wts.w1), f(wts.w3), f(wts.w2), k, 0 if mode == "mixtral" else 1)
+    b = layer.buffers(T, DEV)
+    assert np.array_equal(b.idx.cpu().numpy(), ref["idx"])
+    assert np.array_equal(b.dst.cpu().numpy(), ref["dst"])
+    assert np.array_equal(b.offsets.cpu().numpy(), ref["offsets"])
+    assert rel_l2(f(out), ref["out"]) <= 1e-2
