@@ -95,16 +95,23 @@ COX_DEV TileCoord decode_tile(int t, const int* s_prefix, const int* s_rows, int
 
 COX_DEV float silu_f(float g) { return g * __frcp_rn(1.0f + __expf(-g)); }
 
-template <int EPI>
+// KA = 128-byte swizzle atoms of K per pipeline stage: 1 -> BK 64, 6 stages;
+// 2 -> BK 128, 3 stages (same smem; 256 contiguous bytes per weight row per
+// stage, i.e. better DRAM page locality for weight-streaming shapes).
+template <int EPI, int KA>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GM_THREADS, 1)
     grouped_gemm_kernel(const __grid_constant__ GemmParams p) {
+  constexpr int BK = GM_BK * KA;
+  constexpr int STAGES = GM_STAGES / KA;
+  constexpr uint32_t A_STAGE = GM_A_BYTES * KA;
+  constexpr uint32_t B_STAGE = GM_B_BYTES * KA;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + GM_STAGES * GM_A_BYTES;
   uint64_t* bars = reinterpret_cast<uint64_t*>(sB + GM_STAGES * GM_B_BYTES);
   uint64_t* full = bars;
-  uint64_t* empty = bars + GM_STAGES;
+  uint64_t* empty = bars + GM_STAGES;  // barrier arrays sized for the max stage count
   uint64_t* tfull = bars + 2 * GM_STAGES;
   uint64_t* tempty = bars + 2 * GM_STAGES + 2;
   uint64_t* sfull = bars + 2 * GM_STAGES + 4;                   // [DEPTH] tile id published
@@ -122,7 +129,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GM_THREADS, 1)
   const int lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < GM_STAGES; ++s) {
+    for (int s = 0; s < STAGES; ++s) {
       mbar_init(smem_u32(&full[s]), 1);
       mbar_init(smem_u32(&empty[s]), 1);
     }
@@ -161,7 +168,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GM_THREADS, 1)
   const int total = s_prefix[p.n_groups];
   const int cid = blockIdx.x >> 1;
   const int ncl = gridDim.x >> 1;
-  const int nk = p.K / GM_BK;
+  const int nk = p.K / BK;
 
   // Dynamic tile scheduler.  The leader's warp 3 publishes tile ids into a
   // ring replicated in both CTAs (first wave static, then a global atomic
@@ -253,14 +260,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GM_THREADS, 1)
         const uint32_t fb_local = smem_u32(&full[stage]);
         const uint32_t fb = mapa(fb_local, 0);
         if (lane == 0) {
-          if (rank == 0) mbar_arrive_expect_tx(fb_local, 2 * (GM_A_BYTES + GM_B_BYTES));
-          if (!gather) tma_load_2d_pair(smem_u32(sA + stage * GM_A_BYTES), &p.a_map, fb, kb * GM_BK, a_row);
-          tma_load_2d_pair(smem_u32(sB + stage * GM_B_BYTES), bmap, fb, kb * GM_BK, b_row);
+          if (rank == 0) mbar_arrive_expect_tx(fb_local, 2 * (A_STAGE + B_STAGE));
+#pragma unroll
+          for (int a = 0; a < KA; ++a) {
+            if (!gather)
+              tma_load_2d_pair(smem_u32(sA + stage * A_STAGE + a * GM_A_BYTES), &p.a_map, fb, kb * BK + a * GM_BK,
+                               a_row);
+            tma_load_2d_pair(smem_u32(sB + stage * B_STAGE + a * GM_B_BYTES), bmap, fb, kb * BK + a * GM_BK, b_row);
+          }
         }
-        if (gather)
-          tma_gather4_pair(smem_u32(sA + stage * GM_A_BYTES) + lane * 512, &p.a_map, fb, kb * GM_BK, rr[0], rr[1],
-                           rr[2], rr[3]);
-        if (++stage == GM_STAGES) { stage = 0; phase ^= 1; }
+        if (gather) {
+#pragma unroll
+          for (int a = 0; a < KA; ++a)
+            tma_gather4_pair(smem_u32(sA + stage * A_STAGE + a * GM_A_BYTES) + lane * 512, &p.a_map, fb,
+                             kb * BK + a * GM_BK, rr[0], rr[1], rr[2], rr[3]);
+        }
+        if (++stage == STAGES) { stage = 0; phase ^= 1; }
         if (kb == 0) {  // look ahead: hide the fetch behind this tile
           int tn = lane == 0 ? fetch_tile(si, true) : 0;
           t_next = __shfl_sync(0xffffffffu, tn, 0);
@@ -286,15 +301,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GM_THREADS, 1)
         for (int kb = 0; kb < nk; ++kb) {
           mbar_wait(smem_u32(&full[stage]), phase);
           tc_fence_after();
-          const uint32_t a_base = smem_u32(sA + stage * GM_A_BYTES);
-          const uint32_t b_base = smem_u32(sB + stage * GM_B_BYTES);
+          const uint32_t a_base = smem_u32(sA + stage * A_STAGE);
+          const uint32_t b_base = smem_u32(sB + stage * B_STAGE);
 #pragma unroll
-          for (int k = 0; k < GM_BK / 16; ++k) {
-            mma_bf16_ss<2>(d_tmem, sdesc_kmajor_sw128(a_base + k * 32), sdesc_kmajor_sw128(b_base + k * 32), idesc,
+          for (int k = 0; k < BK / 16; ++k) {
+            const uint32_t off = (k >> 2) * GM_A_BYTES + (k & 3) * 32;  // atom, then 16-wide K step inside it
+            mma_bf16_ss<2>(d_tmem, sdesc_kmajor_sw128(a_base + off), sdesc_kmajor_sw128(b_base + off), idesc,
                            (kb | k) != 0 ? 1u : 0u);
           }
           mma_commit<2>(smem_u32(&empty[stage]));
-          if (++stage == GM_STAGES) { stage = 0; phase ^= 1; }
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
           if (kb == 0) t_next = fetch_tile(si, true);  // look ahead while the tensor pipe is busy
         }
         mma_commit<2>(smem_u32(&tfull[acc]));
@@ -640,24 +656,32 @@ int launch_grouped_gemm(int epi, const void* A, long long rows_cap, int K, const
   p.die_map = die_map_device(g_num_sms);
   int grid = (g_num_sms / 2) * 2;
   if (max_ctas >= 2 && max_ctas < grid) grid = (max_ctas / 2) * 2;
+  // K per stage: measured on C2, the SwiGLU GEMM is faster with BK=128 (3 stages;
+  // K3 92.2 -> 89.6 ms) while the long-K down projection prefers BK=64 with 6
+  // stages (42.6 vs 43.6 ms).  COX_GEMM_BK=64|128 forces one value for both.
+  static int env_bk = [] {
+    const char* e = getenv("COX_GEMM_BK");
+    return e ? atoi(e) : 0;
+  }();
+  int ka = env_bk == 128 ? 2 : env_bk == 64 ? 1 : (epi == EPI_SWIGLU ? 2 : 1);
+  if (K % (ka * GM_BK) != 0) ka = 1;
   cudaError_t err;
+#define GM_LAUNCH(E_, KA_)                                                                                  \
+  do {                                                                                                      \
+    static bool attr = false;                                                                               \
+    if (!attr) {                                                                                            \
+      cudaFuncSetAttribute(grouped_gemm_kernel<E_, KA_>, cudaFuncAttributeMaxDynamicSharedMemorySize,       \
+                           (int)GM_SMEM_BYTES);                                                             \
+      attr = true;                                                                                          \
+    }                                                                                                       \
+    grouped_gemm_kernel<E_, KA_><<<grid, GM_THREADS, GM_SMEM_BYTES, s>>>(p);                                \
+  } while (0)
   if (epi == EPI_SWIGLU) {
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(grouped_gemm_kernel<EPI_SWIGLU>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)GM_SMEM_BYTES);
-      attr = true;
-    }
-    grouped_gemm_kernel<EPI_SWIGLU><<<grid, GM_THREADS, GM_SMEM_BYTES, s>>>(p);
+    if (ka == 2) GM_LAUNCH(EPI_SWIGLU, 2); else GM_LAUNCH(EPI_SWIGLU, 1);
   } else {
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(grouped_gemm_kernel<EPI_STORE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)GM_SMEM_BYTES);
-      attr = true;
-    }
-    grouped_gemm_kernel<EPI_STORE><<<grid, GM_THREADS, GM_SMEM_BYTES, s>>>(p);
+    if (ka == 2) GM_LAUNCH(EPI_STORE, 2); else GM_LAUNCH(EPI_STORE, 1);
   }
+#undef GM_LAUNCH
   err = cudaGetLastError();
   return err == cudaSuccess ? 0 : -2;
 }
