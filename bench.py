@@ -470,6 +470,11 @@ def main():
             err = float(np.linalg.norm(gout - ref["out"]) / max(np.linalg.norm(ref["out"]), 1e-30))
             parity = {"tokens_checked": n, "routing_indices_bitexact": bool(np.array_equal(gidx, ref["idx"])),
                       "out_rel_l2_vs_fp32_oracle": err, "tolerance": 1e-2, "pass": bool(err <= 1e-2)}
+        if graph:
+            l2_note = (f"expert weights read per step ({(touched * 3 * d * ff * 2 + 3 * d * shared_ff * 2) / 1e9:.2f} GB)"
+                       " > 126 MB L2, so every step streams them from HBM; no flush")
+        else:
+            l2_note = "inputs > L2 (x 2.1 GB, x_perm 4.3 GB, h 15 GB vs 126 MB L2); no flush"
         if args.microbatch:
             desc_mb = f" [ABLATION: micro-batched, {args.microbatch} tokens per expert-stage launch]"
         else:
@@ -482,7 +487,7 @@ def main():
             "config": {"workload": desc + desc_mb, "tokens_per_gpu": T, "global_batch_tokens": T * ws, "d": d, "ff": ff,
                        "E": E, "k": k, "routing": mode, "parallelism": f"ep{ws}" if ws > 1 else "single",
                        "ep_path": ep_used,
-                       "l2": "inputs > L2 (x 2.1 GB, x_perm 4.3 GB, h 15 GB vs 126 MB L2); no flush"},
+                       "l2": l2_note},
             "layer_tflops": flops_layer / (ms_step / 1e3) / 1e12,
             "frac_layer_of_bf16_sustained": flops_layer / (ms_step / 1e3) / 1e12 / pk["bf16_sus"],
             "frac_layer_of_bf16_burst": flops_layer / (ms_step / 1e3) / 1e12 / pk["bf16"],
@@ -491,7 +496,8 @@ def main():
             "cpu_baseline": cpu,
             "parity": parity,
             "e2e": e2e,
-            "gpu_launches": layer.launches_per_step * args.steps * (-(-T // args.microbatch) if args.microbatch else 1),
+            "gpu_launches": launches_per_step(layer, args.microbatch or T) * args.steps
+            * (-(-T // args.microbatch) if args.microbatch else 1),
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)
@@ -499,6 +505,11 @@ def main():
         if hasattr(layer, "check"):
             layer.check()
         dist.destroy_process_group()
+
+
+def launches_per_step(layer, T: int) -> int:
+    lp = layer.launches_per_step
+    return lp(T) if callable(lp) else lp
 
 
 if __name__ == "__main__":

@@ -119,6 +119,24 @@ int cox_grouped_down_ex(const void* h, long long rows_cap, const int32_t* offset
                         const int32_t* group_experts, const void* const* w2, int ff, int d, void* y_perm,
                         int max_ctas, void* stream);
 
+/* K3+K4 for decode-size batches: ONE
+ * persistent, weight-streaming launch runs the SwiGLU and the down projection
+ * of every group, plus (x_shared != NULL) the shared experts of a
+ * DeepSeek-style layer as one more dense group.  Swap-AB tcgen05 tiles: 128
+ * weight rows x up to 64 tokens, so the weights stream from HBM once while
+ * the tensor pipe idles; a group's down tiles start as soon as its SwiGLU
+ * tiles are stored (device-side counters, no launch boundary).
+ *   x_perm/h/y_perm/offsets/w13/w2 as for cox_grouped_swiglu / cox_grouped_down
+ *   x_shared [Ts, d], w13_shared [2*ff_shared, d] (interleaved),
+ *   w2_shared [d, ff_shared], h_shared [Ts, ff_shared], y_shared [Ts, d]
+ * Same results as cox_grouped_swiglu + cox_grouped_down for any segment
+ * length; efficient while segments have <= 64 rows (decode steps).
+ * d % 128 == 0, ff % 128 == 0, ff_shared % 128 == 0, n_groups <= 64. */
+int cox_small_expert_ffn(const void* x_perm, long long rows_cap, const int32_t* offsets, int n_groups,
+                         const int32_t* group_experts, const void* const* w13, const void* const* w2, int d, int ff,
+                         void* h, void* y_perm, const void* x_shared, int Ts, const void* w13_shared,
+                         const void* w2_shared, int ff_shared, void* h_shared, void* y_shared, void* stream);
+
 /* K5 — weighted top-k combine back to token order (+ optional shared-expert
  * output, DeepSeek-V2):  out[t] = sum_j w[t,j] * y_perm[dst[t,j]] (+ shared[t]).
  * out/shared dtype = out_dtype (bf16 or fp32). */

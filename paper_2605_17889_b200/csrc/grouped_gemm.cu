@@ -441,7 +441,7 @@ struct MapKeyHash {
 };
 
 // bf16 row-major [rows, cols] -> TMA map with a {64 cols, box_rows rows} box, 128B swizzle.
-static int get_map(CUtensorMap* out, const void* ptr, unsigned long long rows, unsigned long long cols,
+int get_map(CUtensorMap* out, const void* ptr, unsigned long long rows, unsigned long long cols,
                    unsigned box_rows) {
   static std::mutex mu;
   static std::unordered_map<MapKey, CUtensorMap, MapKeyHash> cache;

@@ -97,10 +97,13 @@ class MoELayer:
         self._bufs: StageBuffers | None = None
         self.profile_events = None  # optional {"k3": (ev0, ev1), "k4": (ev0, ev1)} recorded around K3/K4
 
-    @property
-    def launches_per_step(self) -> int:
-        # router 1 + permute 4 (hist, scan, scatter, copy; +1 pad) + K3 + K4 + combine (+ shared K3/K4)
-        return 1 + 4 + (1 if self.tile_m > 1 else 0) + 2 + 1 + (2 if self.shared_ff else 0)
+    def launches_per_step(self, T: int | None = None) -> int:
+        # router 1 + permute 4 (hist, scan, scatter, copy; +1 pad) + K3 + K4 + combine (+ shared K3/K4);
+        # decode-size batches: K3, K4 and the shared experts are one launch
+        perm = 4 + (1 if self.tile_m > 1 else 0)
+        if T is not None and self.uses_small_path(T):
+            return 1 + perm + 1 + 1
+        return 1 + perm + 2 + 1 + (2 if self.shared_ff else 0)
 
     def buffers(self, T: int, device) -> StageBuffers:
         if self._bufs is None or self._bufs.T != T:
@@ -155,11 +158,25 @@ class MoELayer:
     SHARED_SIDE_MAX_ROWS = 8192
     SHARED_SIDE_CTAS = 16
 
+    # decode-size batches: one weight-streaming launch for K3+K4 (+ shared
+    # experts), csrc/small_gemm.cu; COX_SMALL_T_MAX overrides the crossover
+    SMALL_T_MAX = int(os.environ.get("COX_SMALL_T_MAX", "256"))
+
+    def uses_small_path(self, T: int) -> bool:
+        return (0 < T <= self.SMALL_T_MAX and not self.gather_a and self.d % 128 == 0 and self.ff % 128 == 0
+                and self.E <= 64 and (not self.shared_ff or self.shared_ff % 128 == 0))
+
     def forward(self, x: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
         if x.dtype != torch.bfloat16 or x.dim() != 2 or x.shape[1] != self.d:
             raise ValueError(f"x must be bf16 [T, {self.d}]")
         T = x.shape[0]
         b = self.buffers(T, x.device)
+        if self.uses_small_path(T):
+            self.route(x, b)
+            shared = ((x, self.wts.shared_w13, self.wts.shared_w2, b.shared_h, b.shared_y)
+                      if self.shared_ff else None)
+            ops.small_expert_ffn(b.x_perm, b.offsets, self.groups, self.w13_list, self.w2_list, b.h, b.y, shared)
+            return self.finish(b, b.shared_y if self.shared_ff else None, out)
         if self.shared_ff and 0 < T * self.k <= self.SHARED_SIDE_MAX_ROWS:
             main = torch.cuda.current_stream(x.device)
             side = self._side_stream(x.device)
@@ -285,6 +302,16 @@ class MoELayer:
         else:
             ops.permute(b.idx, x, self.E, self.tile_m, out=(b.offsets, b.dst, b.x_perm), workspace=b.workspace)
         ev[2].record()
+        if self.uses_small_path(x.shape[0]):
+            shared = ((x, self.wts.shared_w13, self.wts.shared_w2, b.shared_h, b.shared_y)
+                      if self.shared_ff else None)
+            ops.small_expert_ffn(b.x_perm, b.offsets, self.groups, self.w13_list, self.w2_list, b.h, b.y, shared)
+            ev[3].record()
+            ops.combine(b.y, b.dst, b.w, b.shared_y if self.shared_ff else None, out=b.out)
+            ev[4].record()
+            torch.cuda.synchronize()
+            names = ["router", "permute", "expert_ffn_k3k4_shared", "combine"]
+            return {n: ev[i].elapsed_time(ev[i + 1]) for i, n in enumerate(names)}
         self._k3(b, self.groups, self.w13_list)
         ev[3].record()
         ops.grouped_down(b.h, b.offsets, self.groups, self.w2_list, self.d, y=b.y)

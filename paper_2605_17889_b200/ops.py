@@ -185,6 +185,48 @@ def grouped_down(h: torch.Tensor, offsets: torch.Tensor, group_experts: Sequence
     return y
 
 
+def small_expert_ffn(x_perm: torch.Tensor, offsets: torch.Tensor, group_experts: Sequence[int],
+                     w13: Sequence[torch.Tensor], w2: Sequence[torch.Tensor], h: torch.Tensor, y: torch.Tensor,
+                     shared=None, stream=None):
+    """K3+K4 in one weight-streaming launch for decode-size batches.
+
+    shared = (x, w13_shared, w2_shared, h_shared, y_shared) adds the dense
+    shared-expert MLP over all rows of x as one more group of the launch."""
+    _need(x_perm, "x_perm", _BF16, 2)
+    _need(offsets, "offsets", torch.int32, 1)
+    _need(h, "h", _BF16, 2)
+    _need(y, "y", _BF16, 2)
+    rows, d = x_perm.shape
+    ff = h.shape[1]
+    if h.shape[0] != rows or tuple(y.shape) != (rows, d):
+        raise ValueError("h must be [rows, ff] and y [rows, d] with the rows of x_perm")
+    if len(w13) != len(group_experts) or len(w2) != len(group_experts):
+        raise ValueError("one weight pair per group")
+    for i, (a, b) in enumerate(zip(w13, w2)):
+        _need(a, f"w13[{i}]", _BF16, 2)
+        _need(b, f"w2[{i}]", _BF16, 2)
+        if tuple(a.shape) != (2 * ff, d) or tuple(b.shape) != (d, ff):
+            raise ValueError(f"group {i}: need w13 [2*ff, d] and w2 [d, ff] with ff={ff}, d={d}")
+    sx = sw13 = sw2 = sh = sy = None
+    Ts = ffs = 0
+    if shared is not None:
+        sx, sw13, sw2, sh, sy = shared
+        for t, n in ((sx, "x_shared"), (sw13, "w13_shared"), (sw2, "w2_shared"), (sh, "h_shared"), (sy, "y_shared")):
+            _need(t, n, _BF16, 2)
+        Ts, ffs = sx.shape[0], sh.shape[1]
+        if (sx.shape[1] != d or tuple(sw13.shape) != (2 * ffs, d) or tuple(sw2.shape) != (d, ffs)
+                or sh.shape[0] < Ts or sy.shape[0] < Ts or sy.shape[1] != d):
+            raise ValueError("shared expert operands have inconsistent shapes")
+    L = _lib.lib()
+    _lib.check(L.cox_small_expert_ffn(
+        x_perm.data_ptr(), rows, offsets.data_ptr(), len(group_experts), _ids(group_experts), _ptrs(w13), _ptrs(w2),
+        d, ff, h.data_ptr(), y.data_ptr(),
+        sx.data_ptr() if sx is not None else None, Ts, sw13.data_ptr() if sw13 is not None else None,
+        sw2.data_ptr() if sw2 is not None else None, ffs, sh.data_ptr() if sh is not None else None,
+        sy.data_ptr() if sy is not None else None, _stream(stream)), "cox_small_expert_ffn")
+    return y
+
+
 def combine(y_perm: torch.Tensor, dst: torch.Tensor, w: torch.Tensor, shared: torch.Tensor | None = None,
             out: torch.Tensor | None = None, out_dtype=_BF16, stream=None):
     """K5: out[t] = sum_j w[t,j] y_perm[dst[t,j]] (+ shared[t])."""

@@ -1,0 +1,136 @@
+"""GPU parity of the decode-size expert FFN (csrc/small_gemm.cu, cox_small_expert_ffn).
+
+One weight-streaming launch computes K3 (SwiGLU) and K4 (down) of every
+group, plus the shared experts: checked per expert against a torch fp32
+reference (rel-L2 <= 1e-2, the bar of the prefill GEMMs), against the prefill
+kernels on the same operands, and through MoELayer (which takes this path for
+T <= SMALL_T_MAX) against the fp32 CPU oracle with routing bit-exact.
+"""
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+from oracle import oracle as O  # noqa: E402  (test infrastructure)
+from paper_2605_17889_b200 import ops  # noqa: E402
+from paper_2605_17889_b200.layer import MoELayer  # noqa: E402
+from paper_2605_17889_b200.synthetic import make_layer_weights, make_tokens, split_w13  # noqa: E402
+
+DEV = "cuda"
+
+
+def rel_l2(a, b):
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30))
+
+
+def _swiglu_ref(xe, w13e, w2e):
+    w1, w3 = split_w13(w13e[None])
+    h = torch.nn.functional.silu(xe @ w1[0].float().T) * (xe @ w3[0].float().T)
+    return h, h.to(torch.bfloat16).float() @ w2e.float().T
+
+
+@pytest.mark.parametrize("E,d,ff,counts,shared_ff", [
+    (4, 256, 256, [0, 1, 16, 17], 0),
+    (3, 512, 384, [64, 65, 150], 256),        # 65 and 150 rows: 64-row chunks
+    (8, 1024, 512, [6, 0, 9, 3, 12, 5, 1, 30], 0),
+    (64, 2048, 1408, None, 2816),             # C4 decode shape, T = 64 tokens x top-6
+])
+def test_small_ffn_vs_torch_fp32(E, d, ff, counts, shared_ff):
+    if counts is None:
+        counts = np.random.default_rng(0).multinomial(64 * 6, np.ones(E) / E).tolist()
+    offs = np.concatenate([[0], np.cumsum(counts)]).astype(np.int32)
+    rows = int(offs[-1])
+    wts = make_layer_weights(E, d, ff, seed=3, device=DEV, shared_ff=shared_ff)
+    x = make_tokens(max(rows, 1), d, seed=4, device=DEV)
+    offs_t = torch.from_numpy(offs).to(DEV)
+    h = torch.full((max(rows, 1), ff), 3.0, dtype=torch.bfloat16, device=DEV)
+    y = torch.full((max(rows, 1), d), 3.0, dtype=torch.bfloat16, device=DEV)
+    shared = None
+    Ts = 40
+    if shared_ff:
+        xs = make_tokens(Ts, d, seed=5, device=DEV)
+        shared = (xs, wts.shared_w13, wts.shared_w2, torch.empty((Ts, shared_ff), dtype=torch.bfloat16, device=DEV),
+                  torch.empty((Ts, d), dtype=torch.bfloat16, device=DEV))
+    ops.small_expert_ffn(x, offs_t, list(range(E)), [wts.w13[e] for e in range(E)],
+                         [wts.w2[e] for e in range(E)], h, y, shared)
+    torch.cuda.synchronize()
+    for e in range(E):
+        r0, r1 = int(offs[e]), int(offs[e + 1])
+        if r1 == r0:
+            continue
+        href, yref = _swiglu_ref(x[r0:r1].float(), wts.w13[e], wts.w2[e])
+        assert rel_l2(h[r0:r1].float().cpu(), href.cpu()) < 1e-2, f"h expert {e}"
+        assert rel_l2(y[r0:r1].float().cpu(), yref.cpu()) < 1e-2, f"y expert {e}"
+    if rows == 0:
+        assert (h == 3).all() and (y == 3).all()
+    if shared_ff:
+        href, yref = _swiglu_ref(shared[0].float(), wts.shared_w13, wts.shared_w2)
+        assert rel_l2(shared[3].float().cpu(), href.cpu()) < 1e-2
+        assert rel_l2(shared[4].float().cpu(), yref.cpu()) < 1e-2
+
+
+def test_small_ffn_close_to_prefill_kernels():
+    """Same operands through the prefill kernels (M=256 x N=256 tiles): the two
+    paths differ only in fp32 summation order, so the bf16 outputs agree to a
+    few bf16 ulps."""
+    E, d, ff = 8, 1024, 1024
+    counts = [5, 0, 33, 64, 70, 1, 9, 2]
+    offs = np.concatenate([[0], np.cumsum(counts)]).astype(np.int32)
+    rows = int(offs[-1])
+    wts = make_layer_weights(E, d, ff, seed=6, device=DEV)
+    x = make_tokens(rows, d, seed=7, device=DEV)
+    offs_t = torch.from_numpy(offs).to(DEV)
+    g = list(range(E))
+    w13 = [wts.w13[e] for e in g]
+    w2 = [wts.w2[e] for e in g]
+    h1 = ops.grouped_swiglu(x, offs_t, g, w13, ff)
+    y1 = ops.grouped_down(h1, offs_t, g, w2, d)
+    h2 = torch.empty_like(h1)
+    y2 = torch.empty_like(y1)
+    ops.small_expert_ffn(x, offs_t, g, w13, w2, h2, y2)
+    torch.cuda.synchronize()
+    assert rel_l2(h2.float().cpu(), h1.float().cpu()) < 4e-3
+    assert rel_l2(y2.float().cpu(), y1.float().cpu()) < 4e-3
+
+
+@pytest.mark.parametrize("T,d,ff,E,k,mode,shared_ff", [
+    (64, 2048, 1408, 64, 6, "deepseek", 2816),   # C4 decode step
+    (64, 4096, 14336, 8, 2, "mixtral", 0),       # Mixtral-8x7B decode step
+    (200, 1024, 512, 16, 4, "deepseek", 256),
+    (1, 256, 128, 8, 2, "mixtral", 0),
+])
+def test_decode_layer_vs_oracle(T, d, ff, E, k, mode, shared_ff):
+    wts = make_layer_weights(E, d, ff, seed=0, device=DEV, shared_ff=shared_ff, keep_split=True)
+    x = make_tokens(T, d, seed=1, device=DEV)
+    layer = MoELayer(wts, k, mode)
+    assert layer.uses_small_path(T)
+    out = layer(x)
+    torch.cuda.synchronize()
+    b = layer.buffers(T, DEV)
+    f = lambda t: t.float().cpu().numpy()  # noqa: E731
+    shared = (f(wts.shared_w1), f(wts.shared_w3), f(wts.shared_w2)) if shared_ff else None
+    ref = O.moe_layer(f(x), f(wts.wg), f(wts.w1), f(wts.w3), f(wts.w2), k, 0 if mode == "mixtral" else 1,
+                      shared=shared)
+    assert np.array_equal(b.idx.cpu().numpy(), ref["idx"])
+    assert np.array_equal(b.dst.cpu().numpy(), ref["dst"])
+    err = rel_l2(f(out), ref["out"])
+    assert err <= 1e-2, err
+
+
+def test_decode_graph_replay_matches_eager():
+    T, d, ff, E, k, sff = 64, 2048, 1408, 64, 6, 2816
+    wts = make_layer_weights(E, d, ff, seed=0, device=DEV, shared_ff=sff)
+    layer = MoELayer(wts, k, "deepseek")
+    x_static = make_tokens(T, d, seed=1, device=DEV)
+    replay, out = layer.capture(x_static)
+    for s in (2, 3):
+        x_new = make_tokens(T, d, seed=s, device=DEV)
+        x_static.copy_(x_new)
+        replay()
+        torch.cuda.synchronize()
+        eager = MoELayer(wts, k, "deepseek")(x_new)
+        torch.cuda.synchronize()
+        assert torch.equal(out, eager)
