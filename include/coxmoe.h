@@ -119,23 +119,35 @@ int cox_grouped_down_ex(const void* h, long long rows_cap, const int32_t* offset
                         const int32_t* group_experts, const void* const* w2, int ff, int d, void* y_perm,
                         int max_ctas, void* stream);
 
-/* K3+K4 for decode-size batches: ONE
+/* K3+K4(+K5) for decode-size batches: ONE
  * persistent, weight-streaming launch runs the SwiGLU and the down projection
- * of every group, plus (x_shared != NULL) the shared experts of a
- * DeepSeek-style layer as one more dense group.  Swap-AB tcgen05 tiles: 128
- * weight rows x up to 64 tokens, so the weights stream from HBM once while
- * the tensor pipe idles; a group's down tiles start as soon as its SwiGLU
- * tiles are stored (device-side counters, no launch boundary).
- *   x_perm/h/y_perm/offsets/w13/w2 as for cox_grouped_swiglu / cox_grouped_down
- *   x_shared [Ts, d], w13_shared [2*ff_shared, d] (interleaved),
- *   w2_shared [d, ff_shared], h_shared [Ts, ff_shared], y_shared [Ts, d]
- * Same results as cox_grouped_swiglu + cox_grouped_down for any segment
- * length; efficient while segments have <= 64 rows (decode steps).
- * d % 128 == 0, ff % 128 == 0, ff_shared % 128 == 0, n_groups <= 64. */
-int cox_small_expert_ffn(const void* x_perm, long long rows_cap, const int32_t* offsets, int n_groups,
-                         const int32_t* group_experts, const void* const* w13, const void* const* w2, int d, int ff,
-                         void* h, void* y_perm, const void* x_shared, int Ts, const void* w13_shared,
-                         const void* w2_shared, int ff_shared, void* h_shared, void* y_shared, void* stream);
+ * of every group, the shared experts of a DeepSeek-style layer (one more
+ * dense group over x) and, optionally, the weighted combine.  Swap-AB tcgen05
+ * tiles: 128 weight rows x up to 64 tokens, so the weights stream from HBM
+ * once while the tensor pipe idles; a group's down tiles start as soon as its
+ * SwiGLU tiles are stored, and the CTA that stores the last down tile of a
+ * 128-column block combines that block for every token (device-side
+ * counters, no launch boundaries).
+ *   x [T, d]             the step's tokens (shared-expert input; gather source)
+ *   row_tokens           source token of every permuted row (cox_permute_ex);
+ *                        used when x_perm == NULL: the routed rows are gathered
+ *                        from x by TMA tile::gather4, no x_perm copy
+ *   x_perm [rows_cap, d] materialised permuted rows (or NULL, see above)
+ *   offsets/w13/w2/h/y_perm as for cox_grouped_swiglu / cox_grouped_down
+ *   w13_shared [2*ff_shared, d] (interleaved), w2_shared [d, ff_shared],
+ *   h_shared [T, ff_shared], y_shared [T, d]   (w13_shared == NULL: none)
+ *   dst [T, k], w [T, k], out [T, d] bf16: fused combine
+ *                        out[t] = sum_j w[t,j] y_perm[dst[t,j]] (+ y_shared[t]),
+ *                        bit-identical to cox_combine (out == NULL: skipped)
+ * Same results as cox_grouped_swiglu + cox_grouped_down (+ cox_combine) up to
+ * fp32 summation order, for any segment length; efficient while segments
+ * have <= 64 rows.  d % 128 == 0, ff % 128 == 0, ff_shared % 128 == 0,
+ * n_groups <= 64. */
+int cox_small_expert_ffn(const void* x, int T, const int32_t* row_tokens, const void* x_perm, long long rows_cap,
+                         const int32_t* offsets, int n_groups, const int32_t* group_experts, const void* const* w13,
+                         const void* const* w2, int d, int ff, void* h, void* y_perm, const void* w13_shared,
+                         const void* w2_shared, int ff_shared, void* h_shared, void* y_shared, const int32_t* dst,
+                         const float* w, int k, void* out, void* stream);
 
 /* K5 — weighted top-k combine back to token order (+ optional shared-expert
  * output, DeepSeek-V2):  out[t] = sum_j w[t,j] * y_perm[dst[t,j]] (+ shared[t]).

@@ -80,9 +80,9 @@ def _declare(L):
     L.cox_grouped_down_ex.argtypes = [c_void_p, c_ll, c_void_p, c_int, c_void_p, c_void_p, c_int, c_int,
                                       c_void_p, c_int, c_void_p]
     L.cox_small_expert_ffn.restype = c_int
-    L.cox_small_expert_ffn.argtypes = [c_void_p, c_ll, c_void_p, c_int, c_void_p, c_void_p, c_void_p, c_int, c_int,
-                                       c_void_p, c_void_p, c_void_p, c_int, c_void_p, c_void_p, c_int, c_void_p,
-                                       c_void_p, c_void_p]
+    L.cox_small_expert_ffn.argtypes = [c_void_p, c_int, c_void_p, c_void_p, c_ll, c_void_p, c_int, c_void_p,
+                                       c_void_p, c_void_p, c_int, c_int, c_void_p, c_void_p, c_void_p, c_void_p,
+                                       c_int, c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_void_p, c_void_p]
     L.cox_combine.restype = c_int
     L.cox_combine.argtypes = [c_void_p, c_void_p, c_void_p, c_int, c_int, c_int, c_void_p, c_void_p, c_int,
                               c_void_p]

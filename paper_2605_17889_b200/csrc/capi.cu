@@ -17,10 +17,11 @@ int launch_permute(const int32_t* idx, int T, int k, int E, int tile_m, const vo
 int launch_grouped_gemm(int epi, const void* A, long long rows_cap, int K, const int32_t* offsets, int n_groups,
                         const int32_t* group_expert, const void* const* B, int N, void* out, long long ldo,
                         int max_ctas, cudaStream_t s, const int32_t* a_rows = nullptr, long long a_rows_cap = 0);
-int launch_small_ffn(const void* act, long long rows_cap, const int32_t* offsets, int n_groups,
-                     const int32_t* group_expert, const void* const* w13, const void* const* w2, int d, int ff,
-                     void* h, void* y, const void* xs, int Ts, const void* w13s, const void* w2s, int ffs, void* hs,
-                     void* ys, int phases, cudaStream_t s);
+int launch_small_ffn(const void* x, int T, const int32_t* row_tokens, const void* act, long long rows_cap,
+                     const int32_t* offsets, int n_groups, const int32_t* group_expert, const void* const* w13,
+                     const void* const* w2, int d, int ff, void* h, void* y, const void* w13s, const void* w2s,
+                     int ffs, void* hs, void* ys, const int32_t* cdst, const float* cw, int k, void* out,
+                     int phases, cudaStream_t s);
 int launch_combine(const void* y_perm, const int32_t* dst, const float* w, int T, int k, int d, const void* shared,
                    void* out, int out_is_bf16, cudaStream_t s);
 
@@ -191,28 +192,35 @@ int cox_grouped_down(const void* h, long long rows_cap, const int32_t* offsets, 
   return cox_grouped_down_ex(h, rows_cap, offsets, n_groups, group_experts, w2, ff, d, y_perm, 0, stream);
 }
 
-int cox_small_expert_ffn(const void* x_perm, long long rows_cap, const int32_t* offsets, int n_groups,
-                         const int32_t* group_experts, const void* const* w13, const void* const* w2, int d, int ff,
-                         void* h, void* y_perm, const void* x_shared, int Ts, const void* w13_shared,
-                         const void* w2_shared, int ff_shared, void* h_shared, void* y_shared, void* stream) {
+int cox_small_expert_ffn(const void* x, int T, const int32_t* row_tokens, const void* x_perm, long long rows_cap,
+                         const int32_t* offsets, int n_groups, const int32_t* group_experts, const void* const* w13,
+                         const void* const* w2, int d, int ff, void* h, void* y_perm, const void* w13_shared,
+                         const void* w2_shared, int ff_shared, void* h_shared, void* y_shared, const int32_t* dst,
+                         const float* w, int k, void* out, void* stream) {
   const char* fn = "cox_small_expert_ffn";
-  if (d <= 0 || d % 128) return fail(COX_EINVAL, "%s: need d %% 128 == 0 (d=%d)", fn, d);
-  if (n_groups > 0 && (ff <= 0 || ff % 128)) return fail(COX_EINVAL, "%s: need ff %% 128 == 0 (ff=%d)", fn, ff);
-  if (n_groups > 0 && rows_cap < 1) return fail(COX_EINVAL, "%s: rows_cap < 1", fn);
-  if (n_groups > 0 && (!offsets || !aligned16(x_perm) || !aligned16(h) || !aligned16(y_perm) || !x_perm || !h || !y_perm))
-    return fail(COX_EINVAL, "%s: null or unaligned x_perm/h/y_perm/offsets", fn);
+  if (T < 0 || d <= 0 || d % 128) return fail(COX_EINVAL, "%s: need T >= 0 and d %% 128 == 0 (d=%d)", fn, d);
+  if (T > 0 && (!x || !aligned16(x))) return fail(COX_EINVAL, "%s: x null or unaligned", fn);
+  if (n_groups > 0) {
+    if (ff <= 0 || ff % 128) return fail(COX_EINVAL, "%s: need ff %% 128 == 0 (ff=%d)", fn, ff);
+    if (rows_cap < 1 || !offsets) return fail(COX_EINVAL, "%s: rows_cap < 1 or null offsets", fn);
+    if (!x_perm && !row_tokens) return fail(COX_EINVAL, "%s: need x_perm or row_tokens", fn);
+    if (!h || !y_perm || !aligned16(x_perm) || !aligned16(h) || !aligned16(y_perm))
+      return fail(COX_EINVAL, "%s: null or unaligned x_perm/h/y_perm", fn);
+  }
   if (int rc = check_groups(fn, n_groups, group_experts, w13)) return rc;
   if (int rc = check_groups(fn, n_groups, group_experts, w2)) return rc;
-  if (x_shared) {
-    if (Ts < 0 || ff_shared <= 0 || ff_shared % 128)
-      return fail(COX_EINVAL, "%s: need Ts >= 0 and ff_shared %% 128 == 0 (ff_shared=%d)", fn, ff_shared);
-    if (!w13_shared || !w2_shared || !h_shared || !y_shared || !aligned16(x_shared) || !aligned16(w13_shared) ||
-        !aligned16(w2_shared) || !aligned16(h_shared) || !aligned16(y_shared))
+  if (w13_shared) {
+    if (ff_shared <= 0 || ff_shared % 128)
+      return fail(COX_EINVAL, "%s: need ff_shared %% 128 == 0 (ff_shared=%d)", fn, ff_shared);
+    if (!w2_shared || !h_shared || !y_shared || !aligned16(w13_shared) || !aligned16(w2_shared) ||
+        !aligned16(h_shared) || !aligned16(y_shared))
       return fail(COX_EINVAL, "%s: null or unaligned shared-expert operand", fn);
-    if (Ts == 0) x_shared = nullptr;
   }
-  int rc = cox::launch_small_ffn(x_perm, rows_cap, offsets, n_groups, group_experts, w13, w2, d, ff, h, y_perm,
-                                 x_shared, Ts, w13_shared, w2_shared, ff_shared, h_shared, y_shared, 3,
+  if (out) {
+    if (k < 1 || k > 8 || !dst || !w || !aligned16(out)) return fail(COX_EINVAL, "%s: fused combine needs 1<=k<=8, dst, w", fn);
+  }
+  int rc = cox::launch_small_ffn(x, T, row_tokens, x_perm, rows_cap, offsets, n_groups, group_experts, w13, w2, d, ff,
+                                 h, y_perm, w13_shared, w2_shared, ff_shared, h_shared, y_shared, dst, w, k, out, 3,
                                  static_cast<cudaStream_t>(stream));
   return cuda_status(rc, fn);
 }

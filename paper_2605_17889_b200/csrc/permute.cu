@@ -115,6 +115,101 @@ __global__ void __launch_bounds__(PM_TB) perm_scatter(const int32_t* __restrict_
   }
 }
 
+// Small batches (decode: T*k <= PS_MAX_PAIRS): histogram, scan and stable
+// scatter in ONE single-CTA launch instead of three.  Same order contract:
+// tokens are processed in chunks of 1024 (thread = token), in-warp ranks from
+// ballots, warp prefix per expert in shared memory, running per-expert base
+// across chunks.
+constexpr int PS_THREADS = 1024;
+constexpr long PS_MAX_PAIRS = 16384;
+
+__global__ void __launch_bounds__(PS_THREADS) perm_small(const int32_t* __restrict__ idx, int T, int k, int E,
+                                                         int tile_m, int32_t* __restrict__ offsets,
+                                                         int32_t* __restrict__ dst, int32_t* __restrict__ row_tokens,
+                                                         int32_t* __restrict__ seg_counts) {
+  __shared__ int s_cnt[256];
+  __shared__ int s_base[256];
+  __shared__ int s_wcnt[PS_THREADS / 32][256];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int e = threadIdx.x; e < E; e += PS_THREADS) s_cnt[e] = 0;
+  __syncthreads();
+  for (long i = threadIdx.x; i < (long)T * k; i += PS_THREADS) atomicAdd(&s_cnt[idx[i]], 1);
+  __syncthreads();
+  if (warp == 0) {  // padded segment offsets: warp scan over E <= 256 (8 experts per lane)
+    int loc[8], sum = 0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int e = lane * 8 + q;
+      const int n = e < E ? s_cnt[e] : 0;
+      loc[q] = ((n + tile_m - 1) / tile_m) * tile_m;
+      sum += loc[q];
+    }
+    int incl = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
+    }
+    int run = incl - sum;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int e = lane * 8 + q;
+      if (e < E) {
+        s_base[e] = run;
+        offsets[e] = run;
+        seg_counts[e] = s_cnt[e];
+      }
+      run += loc[q];
+    }
+    if (lane == 31) offsets[E] = incl;
+  }
+  __syncthreads();
+  const uint32_t lt = (1u << lane) - 1u;
+  for (int c0 = 0; c0 < T; c0 += PS_THREADS) {
+    const long t = c0 + threadIdx.x;
+    const bool valid = t < T;
+    int ej[8], rj[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      ej[j] = (valid && j < k) ? idx[t * k + j] : -1;
+      rj[j] = 0;
+    }
+    const int nlive = min(PS_THREADS / 32, (T - c0 + 31) / 32);  // warps holding tokens of this chunk
+    if (warp < nlive) {
+      for (int e = 0; e < E; ++e) {
+        bool has = false;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) has |= (ej[j] == e);
+        const uint32_t bal = __ballot_sync(0xffffffffu, has);
+        if (lane == 0) s_wcnt[warp][e] = __popc(bal);
+        const int r = __popc(bal & lt);
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          if (ej[j] == e) rj[j] = r;
+      }
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < E; e += PS_THREADS) {  // exclusive prefix over warps, per expert
+      int run = s_base[e];
+      for (int w = 0; w < nlive; ++w) {
+        const int n = s_wcnt[w][e];
+        s_wcnt[w][e] = run;
+        run += n;
+      }
+      s_base[e] = run;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      if (j < k && valid) {
+        const int dj = s_wcnt[warp][ej[j]] + rj[j];
+        dst[t * k + j] = dj;
+        if (row_tokens) row_tokens[dj] = (int32_t)t;
+      }
+    __syncthreads();
+  }
+}
+
 // Row copies, grid-wide: one warp per token; each row is read once (16 B
 // vectors, 4 chunks in flight per lane) and written to its k destinations.
 __global__ void __launch_bounds__(256) perm_copy(const int32_t* __restrict__ dst, int T, int k,
@@ -175,11 +270,15 @@ int launch_permute(const int32_t* idx, int T, int k, int E, int tile_m, const vo
     if (cudaMemsetAsync(offsets, 0, sizeof(int32_t) * (E + 1), s) != cudaSuccess) return -2;
     return 0;
   }
-  perm_hist<<<(int)nb, PM_TB, 0, s>>>(idx, T, k, E, block_counts);
-  perm_scan<<<1, 1024, 0, s>>>(block_counts, (int)nb, E, tile_m, block_base, offsets, seg_counts);
   if (row_tokens && tile_m > 1)  // padding rows gather token 0 (computed, never combined)
     if (cudaMemsetAsync(row_tokens, 0, sizeof(int32_t) * rows_cap, s) != cudaSuccess) return -2;
-  perm_scatter<<<(int)nb, PM_TB, 0, s>>>(idx, T, k, E, block_base, offsets, dst, row_tokens);
+  if ((long)T * k <= PS_MAX_PAIRS) {
+    perm_small<<<1, PS_THREADS, 0, s>>>(idx, T, k, E, tile_m, offsets, dst, row_tokens, seg_counts);
+  } else {
+    perm_hist<<<(int)nb, PM_TB, 0, s>>>(idx, T, k, E, block_counts);
+    perm_scan<<<1, 1024, 0, s>>>(block_counts, (int)nb, E, tile_m, block_base, offsets, seg_counts);
+    perm_scatter<<<(int)nb, PM_TB, 0, s>>>(idx, T, k, E, block_base, offsets, dst, row_tokens);
+  }
   long cb = (T + 7) / 8;
   if (cb > 148L * 16) cb = 148L * 16;
   if (x_perm) perm_copy<<<(int)cb, 256, 0, s>>>(dst, T, k, static_cast<const __nv_bfloat16*>(x), d,

@@ -35,7 +35,7 @@ struct XChunk;
 template <>
 struct XChunk<__nv_bfloat16> {
   uint4 v;
-  COX_DEV void load(const __nv_bfloat16* p) { v = ld_nc_v4(p); }
+  COX_DEV void load(const __nv_bfloat16* p) { v = ld_nc_v4_ordered(p); }
   COX_DEV void zero() { v = make_uint4(0, 0, 0, 0); }
   COX_DEV float get(int q) const {
     const uint32_t w = q < 2 ? v.x : q < 4 ? v.y : q < 6 ? v.z : v.w;
@@ -136,7 +136,7 @@ router_topk_kernel(const XT* __restrict__ x, const WT* __restrict__ wg, int T, i
     for (int tl = warp; tl < tpb; tl += RT_WARPS) {
       const long t = tb0 + tl;
       if (t >= T) break;
-      const float* lg = s_logits + tl * E;
+      float* lg = s_logits + tl * E;
       uint32_t taken = 0;  // bit i: expert lane + 32*i already selected (E <= 256)
       for (int j = 0; j < k; ++j) {
         float bv = 0.0f;
@@ -161,6 +161,11 @@ router_topk_kernel(const XT* __restrict__ x, const WT* __restrict__ wg, int T, i
         }
       }
       __syncwarp();
+      if (mode != 0) {  // full softmax: every expf in parallel (in place; the logits are no longer needed)
+        const float m0 = s_selv[warp][0];
+        for (int e = lane; e < E; e += 32) lg[e] = expf(__fsub_rn(lg[e], m0));
+        __syncwarp();
+      }
       if (lane == 0) {
         const int* sel = s_sel[warp];
         const float* selv = s_selv[warp];
@@ -169,7 +174,7 @@ router_topk_kernel(const XT* __restrict__ x, const WT* __restrict__ wg, int T, i
         if (mode == 0) {
           for (int j = 0; j < k; ++j) ssum = __fadd_rn(ssum, expf(__fsub_rn(selv[j], m)));
         } else {
-          for (int e = 0; e < E; ++e) ssum = __fadd_rn(ssum, expf(__fsub_rn(lg[e], m)));
+          for (int e = 0; e < E; ++e) ssum = __fadd_rn(ssum, lg[e]);  // ascending e, as the oracle
         }
         for (int j = 0; j < k; ++j) {
           idx[t * k + j] = sel[j];
@@ -282,7 +287,7 @@ router_topk_staged_kernel(const __nv_bfloat16* __restrict__ x, const float* __re
     for (int tl = warp; tl < RS_TB; tl += RT_WARPS) {
       const long t = tb0 + tl;
       if (t >= T) break;
-      const float* lg = s_logits + tl * E;
+      float* lg = s_logits + tl * E;
       uint32_t taken = 0;
       for (int j = 0; j < k; ++j) {
         float bv = 0.0f;
@@ -307,6 +312,11 @@ router_topk_staged_kernel(const __nv_bfloat16* __restrict__ x, const float* __re
         }
       }
       __syncwarp();
+      if (mode != 0) {  // full softmax: every expf in parallel (in place; the logits are no longer needed)
+        const float m0 = s_selv[warp][0];
+        for (int e = lane; e < E; e += 32) lg[e] = expf(__fsub_rn(lg[e], m0));
+        __syncwarp();
+      }
       if (lane == 0) {
         const int* sel = s_sel[warp];
         const float* selv = s_selv[warp];
@@ -315,7 +325,7 @@ router_topk_staged_kernel(const __nv_bfloat16* __restrict__ x, const float* __re
         if (mode == 0) {
           for (int j = 0; j < k; ++j) ssum = __fadd_rn(ssum, expf(__fsub_rn(selv[j], m)));
         } else {
-          for (int e = 0; e < E; ++e) ssum = __fadd_rn(ssum, expf(__fsub_rn(lg[e], m)));
+          for (int e = 0; e < E; ++e) ssum = __fadd_rn(ssum, lg[e]);  // ascending e, as the oracle
         }
         for (int j = 0; j < k; ++j) {
           idx[t * k + j] = sel[j];
@@ -422,7 +432,7 @@ router_topk_staged_bf16w_kernel(const __nv_bfloat16* __restrict__ x, const __nv_
     for (int tl = warp; tl < RB_TB; tl += RT_WARPS) {
       const long t = tb0 + tl;
       if (t >= T) break;
-      const float* lg = s_logits + tl * E;
+      float* lg = s_logits + tl * E;
       uint32_t taken = 0;
       for (int j = 0; j < k; ++j) {
         float bv = 0.0f;
@@ -447,6 +457,11 @@ router_topk_staged_bf16w_kernel(const __nv_bfloat16* __restrict__ x, const __nv_
         }
       }
       __syncwarp();
+      if (mode != 0) {  // full softmax: every expf in parallel (in place; the logits are no longer needed)
+        const float m0 = s_selv[warp][0];
+        for (int e = lane; e < E; e += 32) lg[e] = expf(__fsub_rn(lg[e], m0));
+        __syncwarp();
+      }
       if (lane == 0) {
         const int* sel = s_sel[warp];
         const float* selv = s_selv[warp];
@@ -455,7 +470,7 @@ router_topk_staged_bf16w_kernel(const __nv_bfloat16* __restrict__ x, const __nv_
         if (mode == 0) {
           for (int j = 0; j < k; ++j) ssum = __fadd_rn(ssum, expf(__fsub_rn(selv[j], m)));
         } else {
-          for (int e = 0; e < E; ++e) ssum = __fadd_rn(ssum, expf(__fsub_rn(lg[e], m)));
+          for (int e = 0; e < E; ++e) ssum = __fadd_rn(ssum, lg[e]);  // ascending e, as the oracle
         }
         for (int j = 0; j < k; ++j) {
           idx[t * k + j] = sel[j];

@@ -33,6 +33,8 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <cstdio>
+#include <cstdlib>
 #include <mutex>
 
 #include "common.cuh"
@@ -40,18 +42,32 @@
 namespace cox {
 
 int get_map(CUtensorMap* out, const void* ptr, unsigned long long rows, unsigned long long cols, unsigned box_rows);
+int launch_combine(const void* y_perm, const int32_t* dst, const float* w, int T, int k, int d, const void* shared,
+                   void* out, int out_is_bf16, cudaStream_t s);
 
 constexpr int SG_BM = 128;     // weight rows per unit (MMA M, TMEM lanes)
-constexpr int SG_BK = 64;      // K per stage: one 128-byte swizzle atom of bf16
-constexpr int SG_NMAX = 64;    // tokens per MMA chunk (MMA N <= 64)
-constexpr int SG_STAGES = 8;
+constexpr int SG_ATOM = 64;    // K of one 128-byte swizzle atom of bf16
+constexpr uint32_t SG_RING_BYTES = 200 * 1024;  // smem for the TMA ring
 constexpr int SG_MAXG = 66;    // 64 routed groups + shared
 constexpr int SG_THREADS = 256;
 constexpr int SG_DEPTH = 4;    // unit-id ring between the scheduler and the roles
-constexpr uint32_t SG_A_BYTES = SG_BM * SG_BK * 2;    // 16 KB
-constexpr uint32_t SG_B_BYTES = SG_NMAX * SG_BK * 2;  // 8 KB
-constexpr int SG_PITCH = 33;                          // fp32 staging row pitch (conflict-free)
-constexpr uint32_t SG_TMEM_COLS = 2 * SG_NMAX;
+constexpr uint32_t SG_A_ATOM = SG_BM * SG_ATOM * 2;  // 16 KB: one K atom of the weight tile
+constexpr int SG_PITCH = 33;                         // fp32 staging row pitch (conflict-free)
+
+// KA = K atoms per pipeline stage (BK = 64 KA: contiguous bytes per weight row
+// per stage), NMAX = tokens per MMA chunk (MMA N <= NMAX).
+template <int KA, int NMAX>
+struct SgCfg {
+  static constexpr int BK = SG_ATOM * KA;
+  static constexpr uint32_t A_STAGE = SG_A_ATOM * KA;
+  static constexpr uint32_t B_ATOM = NMAX * SG_ATOM * 2;
+  static constexpr uint32_t B_STAGE = B_ATOM * KA;
+  static constexpr int STAGES = (int)(SG_RING_BYTES / (A_STAGE + B_STAGE)) > 12 ? 12
+                                                                               : (int)(SG_RING_BYTES / (A_STAGE + B_STAGE));
+  static constexpr uint32_t TMEM_COLS = 2 * NMAX < 64 ? 64 : 2 * NMAX;
+  static constexpr size_t SMEM = 1024 + STAGES * (A_STAGE + B_STAGE) + 512 + 24 * (SG_MAXG + 2) +
+                                 4 * SG_BM * SG_PITCH + 64;
+};
 
 struct alignas(64) SmallParams {
   CUtensorMap act3[2];  // SwiGLU B operand: [0] routed rows (x_perm), [1] shared-expert input (x)
@@ -62,6 +78,16 @@ struct alignas(64) SmallParams {
   int* counters;  // [0] unit counter, [1 + g] SwiGLU units of group g whose h columns are stored
   __nv_bfloat16* h[2];
   __nv_bfloat16* y[2];
+  const int32_t* row_tokens;  // gather mode: routed row r of the SwiGLU pass is x[row_tokens[r]] (act3[0] = x)
+  long long rows_cap;
+  // fused combine (out != nullptr): out[t, cols of block i] = sum_j w[t,j] y[dst[t,j]] (+ y_shared[t]),
+  // done by the CTA that stores the last down tile of column block i
+  const int32_t* cdst;
+  const float* cw;
+  __nv_bfloat16* out;
+  int k;
+  int T;
+  int k4_colmajor;
   int group_expert[SG_MAXG];  // >= 0: routed expert (segment from offsets); -1: shared (rows [0, Ts))
   int group_ff[SG_MAXG];
   int n_groups;
@@ -69,9 +95,9 @@ struct alignas(64) SmallParams {
   int d;
   int phases;  // bit 0: SwiGLU pass, bit 1: down pass
 };
+constexpr int SG_CB_BASE = 1 + SG_MAXG;  // counters[SG_CB_BASE + i]: down tiles stored in column block i
+constexpr int SG_COUNTERS = 256;
 
-constexpr size_t SG_SMEM_BYTES = 1024 + SG_STAGES * (SG_A_BYTES + SG_B_BYTES) + 512 + 16 * (SG_MAXG + 2) +
-                                 4 * SG_BM * SG_PITCH + 64;
 
 COX_DEV void mbar_spin_ge(const int* p, int want) {
   int v;
@@ -81,8 +107,29 @@ COX_DEV void mbar_spin_ge(const int* p, int want) {
 }
 COX_DEV void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
 COX_DEV void named_bar_epi() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+COX_DEV void tma_gather4(uint32_t dst, const void* map, uint32_t bar, int32_t col, int32_t r0, int32_t r1, int32_t r2,
+                         int32_t r3) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(col), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(bar)
+      : "memory");
+}
+COX_DEV uint4 ld_cg_v4(const void* p) {
+  uint4 r;
+  asm volatile("ld.global.cg.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+  return r;
+}
 
+template <int KA, int NMAX>
 __global__ void __launch_bounds__(SG_THREADS, 1) small_ffn_kernel(const __grid_constant__ SmallParams p) {
+  using C = SgCfg<KA, NMAX>;
+  constexpr int SG_STAGES = C::STAGES;
+  constexpr int SG_BK = C::BK;
+  constexpr int SG_NMAX = NMAX;
+  constexpr uint32_t SG_A_BYTES = C::A_STAGE;
+  constexpr uint32_t SG_B_BYTES = C::B_STAGE;
+  constexpr uint32_t SG_TMEM_COLS = C::TMEM_COLS;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
@@ -99,7 +146,9 @@ __global__ void __launch_bounds__(SG_THREADS, 1) small_ffn_kernel(const __grid_c
   int* s_row0 = s_rows + SG_MAXG;
   int* s_p3 = s_row0 + SG_MAXG;      // [G+1] prefix of SwiGLU units
   int* s_p4 = s_p3 + SG_MAXG + 1;    // [G+1] prefix of down units
-  float* stg = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(s_p4 + SG_MAXG + 1) + 15) & ~uintptr_t(15));
+  int* s_misc = s_p4 + SG_MAXG + 1;  // [0] groups with rows, [1] combine flag
+  int* s_act = s_misc + 4;            // [G] active groups (rows > 0), in group order
+  float* stg = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(s_act + SG_MAXG) + 15) & ~uintptr_t(15));
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -119,22 +168,46 @@ __global__ void __launch_bounds__(SG_THREADS, 1) small_ffn_kernel(const __grid_c
       mbar_init(smem_u32(&sempty[i]), 6);  // producer + MMA + 4 epilogue warps
     }
     fence_mbar_init();
-    int a3 = 0, a4 = 0;
-    for (int g = 0; g < G; ++g) {
-      const int e = p.group_expert[g];
-      const int r0 = e >= 0 ? p.offsets[e] : 0;
-      const int rows = e >= 0 ? p.offsets[e + 1] - r0 : p.Ts;
-      s_row0[g] = r0;
-      s_rows[g] = rows;
-      s_p3[g] = a3;
-      s_p4[g] = a4;
-      if (rows > 0) {
-        if (p.phases & 1) a3 += p.group_ff[g] / 64;
-        if (p.phases & 2) a4 += p.d / SG_BM;
+  }
+  if (warp == 0) {
+    // group table: rows / first row per group and the unit prefix sums, one
+    // group per lane (a serial loop would pay one L2 round trip per group)
+    int c3 = 0, c4 = 0, nact = 0;
+    for (int base = 0; base < G; base += 32) {
+      const int g = base + lane;
+      int rows = 0, r0 = 0;
+      if (g < G) {
+        const int e = p.group_expert[g];
+        r0 = e >= 0 ? p.offsets[e] : 0;
+        rows = e >= 0 ? p.offsets[e + 1] - r0 : p.Ts;
+        s_row0[g] = r0;
+        s_rows[g] = rows;
       }
+      const uint32_t live = __ballot_sync(0xffffffffu, g < G && rows > 0);
+      if (g < G && rows > 0) s_act[nact + __popc(live & ((1u << lane) - 1u))] = g;
+      nact += __popc(live);
+      int u3 = (g < G && rows > 0 && (p.phases & 1)) ? p.group_ff[g < G ? g : 0] / 64 : 0;
+      int u4 = (g < G && rows > 0 && (p.phases & 2)) ? p.d / SG_BM : 0;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {  // inclusive warp scans
+        const int a = __shfl_up_sync(0xffffffffu, u3, o), b = __shfl_up_sync(0xffffffffu, u4, o);
+        if (lane >= o) {
+          u3 += a;
+          u4 += b;
+        }
+      }
+      if (g < G) {
+        s_p3[g + 1] = c3 + u3;
+        s_p4[g + 1] = c4 + u4;
+      }
+      c3 += __shfl_sync(0xffffffffu, u3, 31);
+      c4 += __shfl_sync(0xffffffffu, u4, 31);
     }
-    s_p3[G] = a3;
-    s_p4[G] = a4;
+    if (lane == 0) {
+      s_p3[0] = 0;
+      s_p4[0] = 0;
+      s_misc[0] = nact;
+    }
   }
   if (warp == 2) tmem_alloc<1>(smem_u32(tmem_slot), SG_TMEM_COLS);
   tc_fence_before();
@@ -163,8 +236,21 @@ __global__ void __launch_bounds__(SG_THREADS, 1) small_ffn_kernel(const __grid_c
       pre = s_p4;
       pass = 1;
     }
-    g = 0;
-    while (t >= pre[g + 1]) ++g;
+    if (pass == 1 && p.k4_colmajor) {
+      // down tiles run column-block-major (block i of every group, then i+1):
+      // the blocks complete one after another during the pass, so the fused
+      // combine of a block overlaps the streaming of later ones
+      const int nact = s_misc[0];
+      i = t / nact;
+      g = s_act[t - i * nact];
+      return;
+    }
+    int lo = 0, hi = G;  // largest g with pre[g] <= t (empty groups have pre[g] == pre[g + 1])
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (pre[mid] <= t) lo = mid; else hi = mid;
+    }
+    g = lo;
     i = t - pre[g];
   };
 
@@ -186,42 +272,121 @@ __global__ void __launch_bounds__(SG_THREADS, 1) small_ffn_kernel(const __grid_c
     __syncwarp();
   } else if (warp == 0) {
     // ------------------------------------------------------------ TMA producer
-    if (lane == 0) {
-      uint32_t stage = 0, phase = 0;
-      int si = 0;
-      for (int t = fetch(si, true); t < total; t = fetch(si, true)) {
-        int pass, g, i;
-        decode(t, pass, g, i);
-        const int rows = s_rows[g], row0 = s_row0[g];
-        const int src = p.group_expert[g] < 0 ? 1 : 0;
-        const CUtensorMap* wmap = pass == 0 ? &p.w13[g] : &p.w2[g];
-        const CUtensorMap* amap = pass == 0 ? &p.act3[src] : &p.act4[src];
-        const int nk = (pass == 0 ? p.d : p.group_ff[g]) / SG_BK;
-        // weight rows of the two 64-row halves of the A tile
-        const int wr0 = pass == 0 ? 256 * (i >> 1) + 64 * (i & 1) : SG_BM * i;
-        const int wr1 = pass == 0 ? wr0 + 128 : wr0 + 64;
-        bool dep_ok = !(pass == 1 && (p.phases & 1));
-        for (int c0 = 0; c0 < rows; c0 += SG_NMAX) {
-          const int nb = (min(SG_NMAX, rows - c0) + 15) >> 4;  // 16-row B boxes
-          for (int kb = 0; kb < nk; ++kb) {
-            mbar_wait(smem_u32(&empty[stage]), phase ^ 1);
-            const uint32_t fb = smem_u32(&full[stage]);
-            mbar_arrive_expect_tx(fb, SG_A_BYTES + nb * 2048u);
+    // Lane 0 issues the weight tiles and tiled activation boxes; in gather mode
+    // lanes 0..4nb-1 each issue one tile::gather4 (4 token rows of x) per atom.
+    uint32_t stage = 0, phase = 0;
+    int si = 0;
+    for (;;) {
+      int t = lane == 0 ? fetch(si, true) : 0;
+      t = __shfl_sync(0xffffffffu, t, 0);
+      if (t >= total) break;
+      int pass, g, i;
+      decode(t, pass, g, i);
+      const int rows = s_rows[g], row0 = s_row0[g];
+      const int src = p.group_expert[g] < 0 ? 1 : 0;
+      const bool gat = pass == 0 && src == 0 && p.row_tokens != nullptr;
+      const CUtensorMap* wmap = pass == 0 ? &p.w13[g] : &p.w2[g];
+      const CUtensorMap* amap = pass == 0 ? &p.act3[src] : &p.act4[src];
+      const int K = pass == 0 ? p.d : p.group_ff[g];
+      const int nk = (K + SG_BK - 1) / SG_BK;  // the last stage may hold fewer than KA atoms
+      // weight rows of the two 64-row halves of the A tile
+      const int wr0 = pass == 0 ? 256 * (i >> 1) + 64 * (i & 1) : SG_BM * i;
+      const int wr1 = pass == 0 ? wr0 + 128 : wr0 + 64;
+      bool dep_ok = !(pass == 1 && (p.phases & 1));
+      for (int c0 = 0; c0 < rows; c0 += SG_NMAX) {
+        const int nb = (min(SG_NMAX, rows - c0) + 15) >> 4;  // 16-row B boxes
+        int rr[4] = {0, 0, 0, 0};
+        if (gat) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const long long r = (long long)row0 + c0 + 4 * lane + q;
+            rr[q] = (lane < 4 * nb && r < p.rows_cap) ? p.row_tokens[r] : 0;
+          }
+        }
+        // Down tile whose h rows may still be in production: stream the first
+        // weight stages (A only) while waiting, then add their B boxes.
+        int npre = 0;
+        if (!dep_ok && lane == 0) {
+          const int* cnt = p.counters + 1 + g;
+          const int want = p.group_ff[g] / 64;
+          int v;
+          asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(cnt) : "memory");
+          if (v < want) {
+            npre = min(nk, SG_STAGES);
+            uint32_t st0 = stage, ph0 = phase;
+            for (int kb = 0; kb < npre; ++kb) {
+              mbar_wait(smem_u32(&empty[stage]), phase ^ 1);
+              const uint32_t fb = smem_u32(&full[stage]);
+              const int na = min(KA, (K - kb * SG_BK) / SG_ATOM);
+              mbar_arrive_expect_tx(fb, na * (SG_A_ATOM + nb * 2048u));
+              const uint32_t a_dst = smem_u32(sA + stage * SG_A_BYTES);
+              for (int a = 0; a < na; ++a) {
+                tma_load_2d(a_dst + a * SG_A_ATOM, wmap, fb, kb * SG_BK + a * SG_ATOM, wr0);
+                tma_load_2d(a_dst + a * SG_A_ATOM + SG_A_ATOM / 2, wmap, fb, kb * SG_BK + a * SG_ATOM, wr1);
+              }
+              if (++stage == SG_STAGES) {
+                stage = 0;
+                phase ^= 1;
+              }
+            }
+            mbar_spin_ge(cnt, want);
+            fence_proxy_async_global();
+            for (int kb = 0; kb < npre; ++kb) {
+              const uint32_t fb = smem_u32(&full[st0]);
+              const int na = min(KA, (K - kb * SG_BK) / SG_ATOM);
+              const uint32_t b_dst = smem_u32(sB + st0 * SG_B_BYTES);
+              for (int a = 0; a < na; ++a)
+                for (int b = 0; b < nb; ++b)
+                  tma_load_2d(b_dst + a * C::B_ATOM + b * 2048u, amap, fb, kb * SG_BK + a * SG_ATOM,
+                              row0 + c0 + 16 * b);
+              if (++st0 == SG_STAGES) {
+                st0 = 0;
+                ph0 ^= 1;
+              }
+            }
+          } else {
+            fence_proxy_async_global();
+          }
+        }
+        dep_ok = true;
+        npre = __shfl_sync(0xffffffffu, npre, 0);
+        stage = __shfl_sync(0xffffffffu, stage, 0);
+        phase = __shfl_sync(0xffffffffu, phase, 0);
+        for (int kb = npre; kb < nk; ++kb) {
+          if (lane == 0) mbar_wait(smem_u32(&empty[stage]), phase ^ 1);
+          __syncwarp();
+          const uint32_t fb = smem_u32(&full[stage]);
+          const int na = min(KA, (K - kb * SG_BK) / SG_ATOM);
+          const uint32_t b_dst = smem_u32(sB + stage * SG_B_BYTES);
+          if (lane == 0) {
+            mbar_arrive_expect_tx(fb, na * (SG_A_ATOM + nb * 2048u));
             const uint32_t a_dst = smem_u32(sA + stage * SG_A_BYTES);
-            tma_load_2d(a_dst, wmap, fb, kb * SG_BK, wr0);
-            tma_load_2d(a_dst + SG_A_BYTES / 2, wmap, fb, kb * SG_BK, wr1);
-            if (!dep_ok) {
-              // h columns of this group come from SwiGLU units of this launch
-              mbar_spin_ge(p.counters + 1 + g, p.group_ff[g] / 64);
-              fence_proxy_async_global();
-              dep_ok = true;
+#pragma unroll
+            for (int a = 0; a < KA; ++a) {
+              if (a >= na) break;
+              tma_load_2d(a_dst + a * SG_A_ATOM, wmap, fb, kb * SG_BK + a * SG_ATOM, wr0);
+              tma_load_2d(a_dst + a * SG_A_ATOM + SG_A_ATOM / 2, wmap, fb, kb * SG_BK + a * SG_ATOM, wr1);
             }
-            const uint32_t b_dst = smem_u32(sB + stage * SG_B_BYTES);
-            for (int b = 0; b < nb; ++b) tma_load_2d(b_dst + b * 2048u, amap, fb, kb * SG_BK, row0 + c0 + 16 * b);
-            if (++stage == SG_STAGES) {
-              stage = 0;
-              phase ^= 1;
+            if (!gat) {
+#pragma unroll
+              for (int a = 0; a < KA; ++a)
+                for (int b = 0; b < nb && a < na; ++b)
+                  tma_load_2d(b_dst + a * C::B_ATOM + b * 2048u, amap, fb, kb * SG_BK + a * SG_ATOM,
+                              row0 + c0 + 16 * b);
             }
+          }
+          if (gat && lane < 4 * nb) {
+            __syncwarp(__activemask());
+#pragma unroll
+            for (int a = 0; a < KA; ++a)
+              if (a < na)
+                tma_gather4(b_dst + a * C::B_ATOM + lane * 512u, amap, fb, kb * SG_BK + a * SG_ATOM, rr[0], rr[1],
+                            rr[2], rr[3]);
+          }
+          __syncwarp();
+          if (++stage == SG_STAGES) {
+            stage = 0;
+            phase ^= 1;
           }
         }
       }
@@ -236,7 +401,8 @@ __global__ void __launch_bounds__(SG_THREADS, 1) small_ffn_kernel(const __grid_c
         int pass, g, i;
         decode(t, pass, g, i);
         const int rows = s_rows[g];
-        const int nk = (pass == 0 ? p.d : p.group_ff[g]) / SG_BK;
+        const int K = pass == 0 ? p.d : p.group_ff[g];
+        const int nk = (K + SG_BK - 1) / SG_BK;
         for (int c0 = 0; c0 < rows; c0 += SG_NMAX, ++job) {
           const int npad = ((min(SG_NMAX, rows - c0) + 15) >> 4) << 4;
           const uint32_t idesc = idesc_bf16_f32(SG_BM, npad);
@@ -249,9 +415,12 @@ __global__ void __launch_bounds__(SG_THREADS, 1) small_ffn_kernel(const __grid_c
             tc_fence_after();
             const uint32_t a_base = smem_u32(sA + stage * SG_A_BYTES);
             const uint32_t b_base = smem_u32(sB + stage * SG_B_BYTES);
+            const int nkk = min(KA, (K - kb * SG_BK) / SG_ATOM) * (SG_ATOM / 16);
 #pragma unroll
             for (int k = 0; k < SG_BK / 16; ++k)
-              mma_bf16_ss<1>(d_tmem, sdesc_kmajor_sw128(a_base + k * 32), sdesc_kmajor_sw128(b_base + k * 32), idesc,
+              if (k < nkk)
+                mma_bf16_ss<1>(d_tmem, sdesc_kmajor_sw128(a_base + (k >> 2) * SG_A_ATOM + (k & 3) * 32),
+                             sdesc_kmajor_sw128(b_base + (k >> 2) * C::B_ATOM + (k & 3) * 32), idesc,
                              (kb | k) != 0 ? 1u : 0u);
             mma_commit<1>(smem_u32(&empty[stage]));
             if (++stage == SG_STAGES) {
@@ -332,6 +501,79 @@ __global__ void __launch_bounds__(SG_THREADS, 1) small_ffn_kernel(const __grid_c
         __syncwarp();
         if (lane == 0) mbar_arrive(smem_u32(&tempty[acc]));
       }
+      if (pass == 1 && p.out) {
+        // fused combine: the CTA that stores the last down tile of column
+        // block i gathers the k rows of every token for those 128 columns
+        // (same operation order as combine_kernel, so the same bits)
+        named_bar_epi();
+        if (tid == 0) {
+          __threadfence();
+          const int old = atomicAdd(p.counters + SG_CB_BASE + i, 1);
+          __threadfence();
+          s_misc[1] = (old == s_misc[0] - 1);
+        }
+        named_bar_epi();
+        if (s_misc[1]) {
+          // dst / w of every token into shared memory (the staging tile is free
+          // here), then every (token, 8-column chunk) issues its k + 1 row loads
+          // at once; accumulation in ascending j as in combine_kernel
+          const int T = p.T, kk = p.k, d = p.d;
+          int* s_dst = reinterpret_cast<int*>(stg);
+          float* s_w = reinterpret_cast<float*>(stg) + T * kk;
+          __threadfence();
+          for (int e = tid; e < T * kk; e += 128) {
+            s_dst[e] = p.cdst[e];
+            s_w[e] = p.cw[e];
+          }
+          named_bar_epi();
+          const __nv_bfloat16* y0 = p.y[0];
+          const __nv_bfloat16* ys = p.y[1];
+          constexpr int CI = 4;  // items per batch: all their row loads are in flight together
+          for (int it0 = tid; it0 < T * 16; it0 += 128 * CI) {
+            uint4 v[CI][9];
+#pragma unroll
+            for (int c = 0; c < CI; ++c) {
+              const int it = it0 + c * 128;
+              if (it < T * 16) {
+                const int tt = it >> 4;
+                const int col = i * SG_BM + (it & 15) * 8;
+#pragma unroll
+                for (int j = 0; j < 8; ++j)
+                  if (j < kk) v[c][j] = ld_cg_v4(y0 + (long long)s_dst[tt * kk + j] * d + col);
+                if (ys) v[c][8] = ld_cg_v4(ys + (long long)tt * d + col);
+              }
+            }
+#pragma unroll
+            for (int c = 0; c < CI; ++c) {
+              const int it = it0 + c * 128;
+              if (it >= T * 16) break;
+              const int tt = it >> 4;
+              const int col = i * SG_BM + (it & 15) * 8;
+              float acc[8];
+#pragma unroll
+              for (int q = 0; q < 8; ++q) acc[q] = 0.0f;
+#pragma unroll
+              for (int j = 0; j < 8; ++j) {
+                if (j >= kk) break;
+                const float wj = s_w[tt * kk + j];
+                float f[8];
+                bf16x8_to_f32(v[c][j], f);
+#pragma unroll
+                for (int q = 0; q < 8; ++q) acc[q] = __fadd_rn(acc[q], __fmul_rn(wj, f[q]));
+              }
+              if (ys) {
+                float f[8];
+                bf16x8_to_f32(v[c][8], f);
+#pragma unroll
+                for (int q = 0; q < 8; ++q) acc[q] = __fadd_rn(acc[q], f[q]);
+              }
+              st_global_v4(p.out + (long long)tt * d + col, pack_bf16x2(acc[0], acc[1]), pack_bf16x2(acc[2], acc[3]),
+                           pack_bf16x2(acc[4], acc[5]), pack_bf16x2(acc[6], acc[7]));
+            }
+          }
+          named_bar_epi();  // the staging tile is reused by the next unit
+        }
+      }
       if (pass == 0 && (p.phases & 2)) {
         // publish this unit's h columns to the down units of group g (their
         // B operand is read by TMA, i.e. through the async proxy)
@@ -355,53 +597,76 @@ __global__ void __launch_bounds__(SG_THREADS, 1) small_ffn_kernel(const __grid_c
 
 static int g_sg_sms = 0;
 
-// act: routed rows [rows_cap, d] (x_perm); h: [rows_cap, ff]; y: [rows_cap, d].
-// Optional shared expert group (xs != nullptr): xs [Ts, d], w13s [2 ffs, d],
-// w2s [d, ffs], hs [Ts, ffs], ys [Ts, d].
-int launch_small_ffn(const void* act, long long rows_cap, const int32_t* offsets, int n_groups,
-                     const int32_t* group_expert, const void* const* w13, const void* const* w2, int d, int ff,
-                     void* h, void* y, const void* xs, int Ts, const void* w13s, const void* w2s, int ffs, void* hs,
-                     void* ys, int phases, cudaStream_t s) {
-  const int G = n_groups + (xs ? 1 : 0);
+// Routed B rows: x_perm [rows_cap, d] (act != nullptr), or gathered from
+// x [T, d] through row_tokens[rows_cap].  h: [rows_cap, ff]; y: [rows_cap, d].
+// Shared expert group (w13s != nullptr) over x: w13s [2 ffs, d], w2s [d, ffs],
+// hs [T, ffs], ys [T, d].  Fused combine when out != nullptr (bf16 [T, d]).
+int launch_small_ffn(const void* x, int T, const int32_t* row_tokens, const void* act, long long rows_cap,
+                     const int32_t* offsets, int n_groups, const int32_t* group_expert, const void* const* w13,
+                     const void* const* w2, int d, int ff, void* h, void* y, const void* w13s, const void* w2s,
+                     int ffs, void* hs, void* ys, const int32_t* cdst, const float* cw, int k, void* out,
+                     int phases, cudaStream_t s) {
+  const bool shared = w13s != nullptr && T > 0;
+  const int G = n_groups + (shared ? 1 : 0);
   if (G == 0) return 0;
   static SmallParams p;  // 17 KB of tensor maps: built in static storage, copied at launch
   static std::mutex mu;
   std::lock_guard<std::mutex> lk(mu);
   int rc = 0;
   if (n_groups > 0) {
-    if ((rc = get_map(&p.act3[0], act, rows_cap, d, 16))) return rc;
+    if (act) {
+      if ((rc = get_map(&p.act3[0], act, rows_cap, d, 16))) return rc;
+    } else {
+      if ((rc = get_map(&p.act3[0], x, T, d, 1))) return rc;  // tile::gather4 rows
+    }
     if ((rc = get_map(&p.act4[0], h, rows_cap, ff, 16))) return rc;
   }
+  // the shared group goes first: its SwiGLU tiles finish first, so the
+  // column-block-major down pass never waits on it
+  const int g0 = shared ? 1 : 0;
   for (int g = 0; g < n_groups; ++g) {
-    if ((rc = get_map(&p.w13[g], w13[g], 2ull * ff, d, 64))) return rc;
-    if ((rc = get_map(&p.w2[g], w2[g], d, ff, 64))) return rc;
-    p.group_expert[g] = group_expert[g];
-    p.group_ff[g] = ff;
+    if ((rc = get_map(&p.w13[g0 + g], w13[g], 2ull * ff, d, 64))) return rc;
+    if ((rc = get_map(&p.w2[g0 + g], w2[g], d, ff, 64))) return rc;
+    p.group_expert[g0 + g] = group_expert[g];
+    p.group_ff[g0 + g] = ff;
   }
-  if (xs) {
-    if ((rc = get_map(&p.act3[1], xs, Ts, d, 16))) return rc;
-    if ((rc = get_map(&p.act4[1], hs, Ts, ffs, 16))) return rc;
-    if ((rc = get_map(&p.w13[n_groups], w13s, 2ull * ffs, d, 64))) return rc;
-    if ((rc = get_map(&p.w2[n_groups], w2s, d, ffs, 64))) return rc;
-    p.group_expert[n_groups] = -1;
-    p.group_ff[n_groups] = ffs;
+  if (shared) {
+    if ((rc = get_map(&p.act3[1], x, T, d, 16))) return rc;
+    if ((rc = get_map(&p.act4[1], hs, T, ffs, 16))) return rc;
+    if ((rc = get_map(&p.w13[0], w13s, 2ull * ffs, d, 64))) return rc;
+    if ((rc = get_map(&p.w2[0], w2s, d, ffs, 64))) return rc;
+    p.group_expert[0] = -1;
+    p.group_ff[0] = ffs;
   }
+  // fused combine stages dst/w of all tokens in the 16.9 KB staging tile
+  const bool fuse = out != nullptr && (long long)T * k * 8 <= 4LL * SG_BM * SG_PITCH;
   static int* counters = nullptr;
   static unsigned seq = 0;
-  constexpr int SLOT = 128;
   if (!counters) {
-    if (cudaMalloc(&counters, 256 * SLOT * sizeof(int)) != cudaSuccess) return -2;
+    if (cudaMalloc(&counters, 256 * SG_COUNTERS * sizeof(int)) != cudaSuccess) return -2;
   }
-  int* c = counters + (seq++ % 256) * SLOT;
-  if (cudaMemsetAsync(c, 0, (1 + G) * sizeof(int), s) != cudaSuccess) return -2;
+  int* c = counters + (seq++ % 256) * SG_COUNTERS;
+  if (cudaMemsetAsync(c, 0, (SG_CB_BASE + d / SG_BM) * sizeof(int), s) != cudaSuccess) return -2;
+  p.row_tokens = act ? nullptr : row_tokens;
+  p.rows_cap = rows_cap;
+  p.cdst = cdst;
+  p.cw = cw;
+  p.out = fuse ? static_cast<__nv_bfloat16*>(out) : nullptr;
+  p.k = k;
+  p.T = T;
+  static const int colmajor = [] {
+    const char* e = getenv("COX_SMALL_K4_COLMAJOR");  // measured on C4D: 240 vs 232 us (group-major)
+    return e ? atoi(e) : 0;
+  }();
+  p.k4_colmajor = colmajor;
   p.counters = c;
   p.offsets = offsets;
   p.h[0] = static_cast<__nv_bfloat16*>(h);
   p.h[1] = static_cast<__nv_bfloat16*>(hs);
   p.y[0] = static_cast<__nv_bfloat16*>(y);
-  p.y[1] = static_cast<__nv_bfloat16*>(ys);
+  p.y[1] = shared ? static_cast<__nv_bfloat16*>(ys) : nullptr;
   p.n_groups = G;
-  p.Ts = Ts;
+  p.Ts = shared ? T : 0;
   p.d = d;
   p.phases = phases;
   if (g_sg_sms == 0) {
@@ -410,12 +675,37 @@ int launch_small_ffn(const void* act, long long rows_cap, const int32_t* offsets
     cudaDeviceGetAttribute(&g_sg_sms, cudaDevAttrMultiProcessorCount, dev);
     if (g_sg_sms <= 0) g_sg_sms = 148;
   }
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(small_ffn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SG_SMEM_BYTES);
-    attr = true;
+  // pipeline shape (K atoms per stage, tokens per chunk); COX_SMALL_VARIANT=KA,NMAX for experiments
+  static int variant = [] {
+    const char* e = getenv("COX_SMALL_VARIANT");
+    int ka = 2, nm = 64;  // measured best on C4 decode (tools/ab_small.sh)
+    if (e) sscanf(e, "%d,%d", &ka, &nm);
+    return ka * 1000 + nm;
+  }();
+#define SG_LAUNCH(KA_, NM_)                                                                                \
+  do {                                                                                                     \
+    static bool attr = false;                                                                              \
+    if (!attr) {                                                                                           \
+      cudaFuncSetAttribute(small_ffn_kernel<KA_, NM_>, cudaFuncAttributeMaxDynamicSharedMemorySize,        \
+                           (int)SgCfg<KA_, NM_>::SMEM);                                                    \
+      attr = true;                                                                                         \
+    }                                                                                                      \
+    small_ffn_kernel<KA_, NM_><<<g_sg_sms, SG_THREADS, SgCfg<KA_, NM_>::SMEM, s>>>(p);                     \
+  } while (0)
+  switch (variant) {
+    case 1032: SG_LAUNCH(1, 32); break;
+    case 2032: SG_LAUNCH(2, 32); break;
+    case 2016: SG_LAUNCH(2, 16); break;
+    case 4016: SG_LAUNCH(4, 16); break;
+    case 4032: SG_LAUNCH(4, 32); break;
+    case 1064: SG_LAUNCH(1, 64); break;
+    default: SG_LAUNCH(2, 64); break;
   }
-  small_ffn_kernel<<<g_sg_sms, SG_THREADS, SG_SMEM_BYTES, s>>>(p);
+#undef SG_LAUNCH
+  if (out && !fuse) {
+    if (cudaGetLastError() != cudaSuccess) return -2;
+    return launch_combine(y, cdst, cw, T, k, d, shared ? ys : nullptr, out, 1, s);
+  }
   return cudaGetLastError() == cudaSuccess ? 0 : -2;
 }
 

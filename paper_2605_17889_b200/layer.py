@@ -100,9 +100,12 @@ class MoELayer:
     def launches_per_step(self, T: int | None = None) -> int:
         # router 1 + permute 4 (hist, scan, scatter, copy; +1 pad) + K3 + K4 + combine (+ shared K3/K4);
         # decode-size batches: K3, K4 and the shared experts are one launch
-        perm = 4 + (1 if self.tile_m > 1 else 0)
+        # permute: single-CTA index kernel for T*k <= 16384 (else hist, scan, scatter) + row copy (+ pad)
+        small_perm = T is not None and T * self.k <= 16384
+        perm = (1 if small_perm else 3) + 1 + (1 if self.tile_m > 1 else 0)
         if T is not None and self.uses_small_path(T):
-            return 1 + perm + 1 + 1
+            # router + single-CTA permute (indices only) + one launch for K3/K4/shared/combine
+            return 1 + 1 + 1 + (1 if self.out_dtype != torch.bfloat16 else 0)
         return 1 + perm + 2 + 1 + (2 if self.shared_ff else 0)
 
     def buffers(self, T: int, device) -> StageBuffers:
@@ -110,6 +113,8 @@ class MoELayer:
             self._bufs = None
             self._bufs = alloc_buffers(T, self.d, self.ff, self.E, self.k, self.tile_m, device, self.out_dtype,
                                        self.shared_ff, self.gather_a)
+            if self.uses_small_path(T) and self._bufs.row_tokens is None:
+                self._bufs.row_tokens = torch.empty((self._bufs.h.shape[0],), dtype=torch.int32, device=device)
         return self._bufs
 
     # --- stages (all stream-ordered on the current stream) -------------------
@@ -172,11 +177,7 @@ class MoELayer:
         T = x.shape[0]
         b = self.buffers(T, x.device)
         if self.uses_small_path(T):
-            self.route(x, b)
-            shared = ((x, self.wts.shared_w13, self.wts.shared_w2, b.shared_h, b.shared_y)
-                      if self.shared_ff else None)
-            ops.small_expert_ffn(b.x_perm, b.offsets, self.groups, self.w13_list, self.w2_list, b.h, b.y, shared)
-            return self.finish(b, b.shared_y if self.shared_ff else None, out)
+            return self._forward_small(x, b, out)
         if self.shared_ff and 0 < T * self.k <= self.SHARED_SIDE_MAX_ROWS:
             main = torch.cuda.current_stream(x.device)
             side = self._side_stream(x.device)
@@ -196,6 +197,32 @@ class MoELayer:
         self.experts(b)
         sh = self.shared_expert(x, b)
         return self.finish(b, sh, out)
+
+    # experiment switches for the decode path (A/B): gathered vs materialised
+    # routed rows, fused vs separate combine
+    SMALL_GATHER = os.environ.get("COX_SMALL_GATHER", "1") == "1"
+    SMALL_FUSE = os.environ.get("COX_SMALL_FUSE", "1") == "1"
+
+    def _route_small(self, x: torch.Tensor, b: StageBuffers):
+        ops.router_topk(x, self.wg_router, self.k, self.mode, out=(b.idx, b.w, b.counts))
+        ops.permute(b.idx, x, self.E, self.tile_m, out=(b.offsets, b.dst, None if self.SMALL_GATHER else b.x_perm),
+                    workspace=b.workspace, copy_rows=not self.SMALL_GATHER, row_tokens=b.row_tokens)
+
+    def _ffn_small(self, x: torch.Tensor, b: StageBuffers, out: torch.Tensor):
+        shared = (self.wts.shared_w13, self.wts.shared_w2, b.shared_h, b.shared_y) if self.shared_ff else None
+        fuse = out.dtype == torch.bfloat16 and self.SMALL_FUSE
+        ops.small_expert_ffn(x, b.offsets, self.groups, self.w13_list, self.w2_list, b.h, b.y,
+                             x_perm=None if self.SMALL_GATHER else b.x_perm, row_tokens=b.row_tokens,
+                             shared=shared, combine=(b.dst, b.w, out) if fuse else None)
+        if not fuse:
+            ops.combine(b.y, b.dst, b.w, b.shared_y if self.shared_ff else None, out=out)
+        return out
+
+    def _forward_small(self, x: torch.Tensor, b: StageBuffers, out: torch.Tensor | None):
+        """Decode-size step: router, index-only permute (no row copy), then ONE
+        launch for K3 + K4 + shared experts + combine (csrc/small_gemm.cu)."""
+        self._route_small(x, b)
+        return self._ffn_small(x, b, b.out if out is None else out)
 
     def _side_stream(self, dev):
         st = getattr(self, "_side", None)
@@ -295,7 +322,10 @@ class MoELayer:
         ev[0].record()
         ops.router_topk(x, self.wg_router, self.k, self.mode, out=(b.idx, b.w, b.counts))
         ev[1].record()
-        if self.gather_a:
+        if self.uses_small_path(x.shape[0]):
+            ops.permute(b.idx, x, self.E, self.tile_m, out=(b.offsets, b.dst, None), workspace=b.workspace,
+                        copy_rows=False, row_tokens=b.row_tokens)
+        elif self.gather_a:
             ops.permute(b.idx, x, self.E, self.tile_m, out=(b.offsets, b.dst, None), workspace=b.workspace,
                         copy_rows=False, row_tokens=b.row_tokens)
             b.x_ref = x
@@ -303,14 +333,10 @@ class MoELayer:
             ops.permute(b.idx, x, self.E, self.tile_m, out=(b.offsets, b.dst, b.x_perm), workspace=b.workspace)
         ev[2].record()
         if self.uses_small_path(x.shape[0]):
-            shared = ((x, self.wts.shared_w13, self.wts.shared_w2, b.shared_h, b.shared_y)
-                      if self.shared_ff else None)
-            ops.small_expert_ffn(b.x_perm, b.offsets, self.groups, self.w13_list, self.w2_list, b.h, b.y, shared)
+            self._ffn_small(x, b, b.out)
             ev[3].record()
-            ops.combine(b.y, b.dst, b.w, b.shared_y if self.shared_ff else None, out=b.out)
-            ev[4].record()
             torch.cuda.synchronize()
-            names = ["router", "permute", "expert_ffn_k3k4_shared", "combine"]
+            names = ["router", "permute", "expert_ffn_k3k4_shared_combine"]
             return {n: ev[i].elapsed_time(ev[i + 1]) for i, n in enumerate(names)}
         self._k3(b, self.groups, self.w13_list)
         ev[3].record()

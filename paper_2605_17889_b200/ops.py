@@ -185,21 +185,34 @@ def grouped_down(h: torch.Tensor, offsets: torch.Tensor, group_experts: Sequence
     return y
 
 
-def small_expert_ffn(x_perm: torch.Tensor, offsets: torch.Tensor, group_experts: Sequence[int],
+def small_expert_ffn(x: torch.Tensor, offsets: torch.Tensor, group_experts: Sequence[int],
                      w13: Sequence[torch.Tensor], w2: Sequence[torch.Tensor], h: torch.Tensor, y: torch.Tensor,
-                     shared=None, stream=None):
-    """K3+K4 in one weight-streaming launch for decode-size batches.
+                     x_perm: torch.Tensor | None = None, row_tokens: torch.Tensor | None = None,
+                     shared=None, combine=None, stream=None):
+    """K3+K4 (+shared experts, +K5) in one weight-streaming launch for decode-size batches.
 
-    shared = (x, w13_shared, w2_shared, h_shared, y_shared) adds the dense
-    shared-expert MLP over all rows of x as one more group of the launch."""
-    _need(x_perm, "x_perm", _BF16, 2)
+    Routed rows come from ``x_perm`` or, if it is None, are gathered from ``x``
+    through ``row_tokens``.  ``shared = (w13_shared, w2_shared, h_shared,
+    y_shared)`` adds the dense shared-expert MLP over x; ``combine = (dst, w,
+    out)`` fuses the weighted combine (bf16 out, same bits as ops.combine)."""
+    _need(x, "x", _BF16, 2)
     _need(offsets, "offsets", torch.int32, 1)
     _need(h, "h", _BF16, 2)
     _need(y, "y", _BF16, 2)
-    rows, d = x_perm.shape
-    ff = h.shape[1]
-    if h.shape[0] != rows or tuple(y.shape) != (rows, d):
-        raise ValueError("h must be [rows, ff] and y [rows, d] with the rows of x_perm")
+    T, d = x.shape
+    rows, ff = h.shape
+    if tuple(y.shape) != (rows, d):
+        raise ValueError("y must be [rows, d] with the rows of h")
+    if x_perm is not None:
+        _need(x_perm, "x_perm", _BF16, 2)
+        if tuple(x_perm.shape) != (rows, d):
+            raise ValueError("x_perm must be [rows, d] with the rows of h")
+    elif row_tokens is not None:
+        _need(row_tokens, "row_tokens", torch.int32, 1)
+        if row_tokens.numel() < rows:
+            raise ValueError("row_tokens needs one entry per row of h")
+    elif len(group_experts):
+        raise ValueError("need x_perm or row_tokens")
     if len(w13) != len(group_experts) or len(w2) != len(group_experts):
         raise ValueError("one weight pair per group")
     for i, (a, b) in enumerate(zip(w13, w2)):
@@ -207,24 +220,33 @@ def small_expert_ffn(x_perm: torch.Tensor, offsets: torch.Tensor, group_experts:
         _need(b, f"w2[{i}]", _BF16, 2)
         if tuple(a.shape) != (2 * ff, d) or tuple(b.shape) != (d, ff):
             raise ValueError(f"group {i}: need w13 [2*ff, d] and w2 [d, ff] with ff={ff}, d={d}")
-    sx = sw13 = sw2 = sh = sy = None
-    Ts = ffs = 0
+    sw13 = sw2 = sh = sy = None
+    ffs = 0
     if shared is not None:
-        sx, sw13, sw2, sh, sy = shared
-        for t, n in ((sx, "x_shared"), (sw13, "w13_shared"), (sw2, "w2_shared"), (sh, "h_shared"), (sy, "y_shared")):
+        sw13, sw2, sh, sy = shared
+        for t, n in ((sw13, "w13_shared"), (sw2, "w2_shared"), (sh, "h_shared"), (sy, "y_shared")):
             _need(t, n, _BF16, 2)
-        Ts, ffs = sx.shape[0], sh.shape[1]
-        if (sx.shape[1] != d or tuple(sw13.shape) != (2 * ffs, d) or tuple(sw2.shape) != (d, ffs)
-                or sh.shape[0] < Ts or sy.shape[0] < Ts or sy.shape[1] != d):
+        ffs = sh.shape[1]
+        if (tuple(sw13.shape) != (2 * ffs, d) or tuple(sw2.shape) != (d, ffs) or sh.shape[0] < T
+                or sy.shape[0] < T or sy.shape[1] != d):
             raise ValueError("shared expert operands have inconsistent shapes")
+    dst = wt = out = None
+    k = 0
+    if combine is not None:
+        dst, wt, out = combine
+        _need(dst, "dst", torch.int32, 2)
+        _need(wt, "w", torch.float32, 2)
+        _need(out, "out", _BF16, 2)
+        k = dst.shape[1]
+        if dst.shape[0] != T or tuple(wt.shape) != tuple(dst.shape) or tuple(out.shape) != (T, d):
+            raise ValueError("combine operands must be dst/w [T, k] and out [T, d]")
+    ptr = lambda t: t.data_ptr() if t is not None else None  # noqa: E731
     L = _lib.lib()
     _lib.check(L.cox_small_expert_ffn(
-        x_perm.data_ptr(), rows, offsets.data_ptr(), len(group_experts), _ids(group_experts), _ptrs(w13), _ptrs(w2),
-        d, ff, h.data_ptr(), y.data_ptr(),
-        sx.data_ptr() if sx is not None else None, Ts, sw13.data_ptr() if sw13 is not None else None,
-        sw2.data_ptr() if sw2 is not None else None, ffs, sh.data_ptr() if sh is not None else None,
-        sy.data_ptr() if sy is not None else None, _stream(stream)), "cox_small_expert_ffn")
-    return y
+        x.data_ptr(), T, ptr(row_tokens), ptr(x_perm), rows, offsets.data_ptr(), len(group_experts),
+        _ids(group_experts), _ptrs(w13), _ptrs(w2), d, ff, h.data_ptr(), y.data_ptr(), ptr(sw13), ptr(sw2), ffs,
+        ptr(sh), ptr(sy), ptr(dst), ptr(wt), k, ptr(out), _stream(stream)), "cox_small_expert_ffn")
+    return out if out is not None else y
 
 
 def combine(y_perm: torch.Tensor, dst: torch.Tensor, w: torch.Tensor, shared: torch.Tensor | None = None,

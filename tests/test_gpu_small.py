@@ -50,12 +50,12 @@ def test_small_ffn_vs_torch_fp32(E, d, ff, counts, shared_ff):
     y = torch.full((max(rows, 1), d), 3.0, dtype=torch.bfloat16, device=DEV)
     shared = None
     Ts = 40
+    xs = make_tokens(Ts, d, seed=5, device=DEV)  # the step's tokens: shared-expert input
     if shared_ff:
-        xs = make_tokens(Ts, d, seed=5, device=DEV)
-        shared = (xs, wts.shared_w13, wts.shared_w2, torch.empty((Ts, shared_ff), dtype=torch.bfloat16, device=DEV),
+        shared = (wts.shared_w13, wts.shared_w2, torch.empty((Ts, shared_ff), dtype=torch.bfloat16, device=DEV),
                   torch.empty((Ts, d), dtype=torch.bfloat16, device=DEV))
-    ops.small_expert_ffn(x, offs_t, list(range(E)), [wts.w13[e] for e in range(E)],
-                         [wts.w2[e] for e in range(E)], h, y, shared)
+    ops.small_expert_ffn(xs, offs_t, list(range(E)), [wts.w13[e] for e in range(E)],
+                         [wts.w2[e] for e in range(E)], h, y, x_perm=x, shared=shared)
     torch.cuda.synchronize()
     for e in range(E):
         r0, r1 = int(offs[e]), int(offs[e + 1])
@@ -67,9 +67,9 @@ def test_small_ffn_vs_torch_fp32(E, d, ff, counts, shared_ff):
     if rows == 0:
         assert (h == 3).all() and (y == 3).all()
     if shared_ff:
-        href, yref = _swiglu_ref(shared[0].float(), wts.shared_w13, wts.shared_w2)
-        assert rel_l2(shared[3].float().cpu(), href.cpu()) < 1e-2
-        assert rel_l2(shared[4].float().cpu(), yref.cpu()) < 1e-2
+        href, yref = _swiglu_ref(xs.float(), wts.shared_w13, wts.shared_w2)
+        assert rel_l2(shared[2].float().cpu(), href.cpu()) < 1e-2
+        assert rel_l2(shared[3].float().cpu(), yref.cpu()) < 1e-2
 
 
 def test_small_ffn_close_to_prefill_kernels():
@@ -90,7 +90,7 @@ def test_small_ffn_close_to_prefill_kernels():
     y1 = ops.grouped_down(h1, offs_t, g, w2, d)
     h2 = torch.empty_like(h1)
     y2 = torch.empty_like(y1)
-    ops.small_expert_ffn(x, offs_t, g, w13, w2, h2, y2)
+    ops.small_expert_ffn(x, offs_t, g, w13, w2, h2, y2, x_perm=x)
     torch.cuda.synchronize()
     assert rel_l2(h2.float().cpu(), h1.float().cpu()) < 4e-3
     assert rel_l2(y2.float().cpu(), y1.float().cpu()) < 4e-3
@@ -134,3 +134,38 @@ def test_decode_graph_replay_matches_eager():
         eager = MoELayer(wts, k, "deepseek")(x_new)
         torch.cuda.synchronize()
         assert torch.equal(out, eager)
+
+
+@pytest.mark.parametrize("T,E,k,d,ff,shared_ff", [
+    (64, 64, 6, 2048, 1408, 2816),
+    (37, 8, 2, 512, 256, 0),
+    (150, 16, 4, 1024, 512, 256),   # segments > 64 rows: chunked
+])
+def test_gather_rows_and_fused_combine_match_separate_kernels(T, E, k, d, ff, shared_ff):
+    """Gather-mode B loads (row_tokens, no x_perm) and the fused combine give the
+    same bits as materialised x_perm rows + the separate combine kernel."""
+    wts = make_layer_weights(E, d, ff, seed=8, device=DEV, shared_ff=shared_ff)
+    x = make_tokens(T, d, seed=9, device=DEV)
+    idx, w, _ = ops.router_topk(x, wts.wg, k, 1)
+    cap = ops.rows_capacity(T, k, E)
+    rt = torch.empty((cap,), dtype=torch.int32, device=DEV)
+    offsets, dst, x_perm = ops.permute(idx, x, E, row_tokens=rt)
+    g = list(range(E))
+    w13 = [wts.w13[e] for e in g]
+    w2 = [wts.w2[e] for e in g]
+    bf = torch.bfloat16
+
+    def bufs():
+        sh = ((wts.shared_w13, wts.shared_w2, torch.empty((T, shared_ff), dtype=bf, device=DEV),
+               torch.empty((T, d), dtype=bf, device=DEV)) if shared_ff else None)
+        return torch.empty((cap, ff), dtype=bf, device=DEV), torch.empty((cap, d), dtype=bf, device=DEV), sh
+
+    h1, y1, sh1 = bufs()
+    ops.small_expert_ffn(x, offsets, g, w13, w2, h1, y1, x_perm=x_perm, shared=sh1)
+    out1 = ops.combine(y1, dst, w, sh1[3] if shared_ff else None)
+    h2, y2, sh2 = bufs()
+    out2 = torch.full((T, d), 5.0, dtype=bf, device=DEV)
+    ops.small_expert_ffn(x, offsets, g, w13, w2, h2, y2, row_tokens=rt, shared=sh2, combine=(dst, w, out2))
+    torch.cuda.synchronize()
+    assert torch.equal(h1, h2) and torch.equal(y1, y2)
+    assert torch.equal(out1, out2)
