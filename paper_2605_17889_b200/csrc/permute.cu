@@ -273,6 +273,12 @@ int launch_permute(const int32_t* idx, int T, int k, int E, int tile_m, const vo
   if (row_tokens && tile_m > 1)  // padding rows gather token 0 (computed, never combined)
     if (cudaMemsetAsync(row_tokens, 0, sizeof(int32_t) * rows_cap, s) != cudaSuccess) return -2;
   if ((long)T * k <= PS_MAX_PAIRS) {
+    static bool carve = false;
+    if (!carve) {
+      cudaFuncSetAttribute(perm_small, cudaFuncAttributePreferredSharedMemoryCarveout,
+                           (int)cudaSharedmemCarveoutMaxShared);
+      carve = true;
+    }
     perm_small<<<1, PS_THREADS, 0, s>>>(idx, T, k, E, tile_m, offsets, dst, row_tokens, seg_counts);
   } else {
     perm_hist<<<(int)nb, PM_TB, 0, s>>>(idx, T, k, E, block_counts);

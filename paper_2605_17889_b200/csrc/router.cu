@@ -537,8 +537,16 @@ int launch_router(const void* x, int x_is_bf16, const void* wg, int wg_is_bf16, 
   if (blocks > 148L * 16) blocks = 148L * 16;
   const size_t smem = sizeof(float) * (size_t)tpb * E;
 #define RT_LAUNCH(XT, TP, WT)                                                                                   \
-  router_topk_kernel<XT, TP, WT><<<(int)blocks, RT_WARPS * 32, smem, s>>>(                                      \
-      static_cast<const XT*>(x), static_cast<const WT*>(wg), T, d, E, k, mode, egn, idx, w, counts)
+  do {                                                                                                          \
+    static bool carve = false;                                                                                  \
+    if (!carve && small) { /* decode: same smem carveout as the expert kernel that follows (no reconfig) */    \
+      cudaFuncSetAttribute(router_topk_kernel<XT, TP, WT>, cudaFuncAttributePreferredSharedMemoryCarveout,     \
+                           (int)cudaSharedmemCarveoutMaxShared);                                                \
+      carve = true;                                                                                             \
+    }                                                                                                           \
+    router_topk_kernel<XT, TP, WT><<<(int)blocks, RT_WARPS * 32, smem, s>>>(                                    \
+        static_cast<const XT*>(x), static_cast<const WT*>(wg), T, d, E, k, mode, egn, idx, w, counts);          \
+  } while (0)
 #define RT_BY_W(XT, TP) \
   if (wg_is_bf16) RT_LAUNCH(XT, TP, __nv_bfloat16); else RT_LAUNCH(XT, TP, float)
   if (x_is_bf16) {

@@ -34,8 +34,11 @@
 #include <cudaTypedefs.h>
 
 #include <cstdio>
+#include <cstring>
 #include <cstdlib>
 #include <mutex>
+#include <unordered_map>
+#include <vector>
 
 #include "common.cuh"
 
@@ -69,13 +72,22 @@ struct SgCfg {
                                  4 * SG_BM * SG_PITCH + 64;
 };
 
-struct alignas(64) SmallParams {
-  CUtensorMap act3[2];  // SwiGLU B operand: [0] routed rows (x_perm), [1] shared-expert input (x)
+// Tensor maps live in a global-memory table (17 KB), not in the kernel
+// parameters: a 17 KB parameter block costs every launch; the table for a given
+// set of operands is uploaded once and reused (graph replays included).
+struct alignas(128) SmallMaps {
+  CUtensorMap act3[2];  // SwiGLU B operand: [0] routed rows (x_perm, or x for gather4), [1] shared-expert input (x)
   CUtensorMap act4[2];  // down B operand:   [0] h, [1] shared h
   CUtensorMap w13[SG_MAXG];
   CUtensorMap w2[SG_MAXG];
+};
+
+struct SmallParams {
+  const SmallMaps* maps;
   const int32_t* offsets;
-  int* counters;  // [0] unit counter, [1 + g] SwiGLU units of group g whose h columns are stored
+  int* counters;  // [0] unit counter, [1 + g] SwiGLU units of group g whose h columns are stored,
+                  // [SG_CB_BASE + i] down tiles of column block i, [SG_COUNTERS - 1] exit ticket;
+                  // zero at launch, reset by the last CTA to exit
   __nv_bfloat16* h[2];
   __nv_bfloat16* y[2];
   const int32_t* row_tokens;  // gather mode: routed row r of the SwiGLU pass is x[row_tokens[r]] (act3[0] = x)
@@ -285,8 +297,8 @@ __global__ void __launch_bounds__(SG_THREADS, 1) small_ffn_kernel(const __grid_c
       const int rows = s_rows[g], row0 = s_row0[g];
       const int src = p.group_expert[g] < 0 ? 1 : 0;
       const bool gat = pass == 0 && src == 0 && p.row_tokens != nullptr;
-      const CUtensorMap* wmap = pass == 0 ? &p.w13[g] : &p.w2[g];
-      const CUtensorMap* amap = pass == 0 ? &p.act3[src] : &p.act4[src];
+      const CUtensorMap* wmap = pass == 0 ? &p.maps->w13[g] : &p.maps->w2[g];
+      const CUtensorMap* amap = pass == 0 ? &p.maps->act3[src] : &p.maps->act4[src];
       const int K = pass == 0 ? p.d : p.group_ff[g];
       const int nk = (K + SG_BK - 1) / SG_BK;  // the last stage may hold fewer than KA atoms
       // weight rows of the two 64-row halves of the A tile
@@ -593,9 +605,45 @@ __global__ void __launch_bounds__(SG_THREADS, 1) small_ffn_kernel(const __grid_c
     tc_fence_after();
     tmem_dealloc<1>(tmem_base, SG_TMEM_COLS);
   }
+  if (threadIdx.x == 0) {
+    // the last CTA to exit zeroes the counters for the next launch (no memset node)
+    __threadfence();
+    const int ticket = atomicAdd(p.counters + SG_COUNTERS - 1, 1);
+    if (ticket == (int)gridDim.x - 1) {
+      __threadfence();
+      const int n = SG_CB_BASE + p.d / SG_BM;
+      for (int c = 0; c < n; ++c) p.counters[c] = 0;
+      p.counters[SG_COUNTERS - 1] = 0;
+    }
+  }
 }
 
 static int g_sg_sms = 0;
+
+// Device copies of map tables, keyed by content: a table is uploaded (stream-
+// ordered, from its own pinned host copy) the first time a set of operands is
+// seen and kept for the life of the process, so a kernel node captured in a
+// CUDA graph always finds its table unchanged (no eviction).
+static const SmallMaps* upload_maps(const SmallMaps& m, cudaStream_t s) {
+  struct Slot {
+    SmallMaps* host;
+    SmallMaps* dev;
+  };
+  static std::unordered_map<unsigned long long, std::vector<Slot>> pool;
+  unsigned long long h = 1469598103934665603ull;  // FNV-1a over the table
+  const unsigned char* b = reinterpret_cast<const unsigned char*>(&m);
+  for (size_t i = 0; i < sizeof(SmallMaps); ++i) h = (h ^ b[i]) * 1099511628211ull;
+  auto& v = pool[h];
+  for (const Slot& sl : v)
+    if (memcmp(sl.host, &m, sizeof(SmallMaps)) == 0) return sl.dev;
+  Slot sl{nullptr, nullptr};
+  if (cudaMallocHost(&sl.host, sizeof(SmallMaps)) != cudaSuccess) return nullptr;
+  if (cudaMalloc(&sl.dev, sizeof(SmallMaps)) != cudaSuccess) return nullptr;
+  *sl.host = m;
+  if (cudaMemcpyAsync(sl.dev, sl.host, sizeof(SmallMaps), cudaMemcpyHostToDevice, s) != cudaSuccess) return nullptr;
+  v.push_back(sl);
+  return sl.dev;
+}
 
 // Routed B rows: x_perm [rows_cap, d] (act != nullptr), or gathered from
 // x [T, d] through row_tokens[rows_cap].  h: [rows_cap, ff]; y: [rows_cap, d].
@@ -609,32 +657,34 @@ int launch_small_ffn(const void* x, int T, const int32_t* row_tokens, const void
   const bool shared = w13s != nullptr && T > 0;
   const int G = n_groups + (shared ? 1 : 0);
   if (G == 0) return 0;
-  static SmallParams p;  // 17 KB of tensor maps: built in static storage, copied at launch
+  static SmallParams p;
+  static SmallMaps m;
   static std::mutex mu;
   std::lock_guard<std::mutex> lk(mu);
+  memset(&m, 0, sizeof(m));
   int rc = 0;
   if (n_groups > 0) {
     if (act) {
-      if ((rc = get_map(&p.act3[0], act, rows_cap, d, 16))) return rc;
+      if ((rc = get_map(&m.act3[0], act, rows_cap, d, 16))) return rc;
     } else {
-      if ((rc = get_map(&p.act3[0], x, T, d, 1))) return rc;  // tile::gather4 rows
+      if ((rc = get_map(&m.act3[0], x, T, d, 1))) return rc;  // tile::gather4 rows
     }
-    if ((rc = get_map(&p.act4[0], h, rows_cap, ff, 16))) return rc;
+    if ((rc = get_map(&m.act4[0], h, rows_cap, ff, 16))) return rc;
   }
   // the shared group goes first: its SwiGLU tiles finish first, so the
   // column-block-major down pass never waits on it
   const int g0 = shared ? 1 : 0;
   for (int g = 0; g < n_groups; ++g) {
-    if ((rc = get_map(&p.w13[g0 + g], w13[g], 2ull * ff, d, 64))) return rc;
-    if ((rc = get_map(&p.w2[g0 + g], w2[g], d, ff, 64))) return rc;
+    if ((rc = get_map(&m.w13[g0 + g], w13[g], 2ull * ff, d, 64))) return rc;
+    if ((rc = get_map(&m.w2[g0 + g], w2[g], d, ff, 64))) return rc;
     p.group_expert[g0 + g] = group_expert[g];
     p.group_ff[g0 + g] = ff;
   }
   if (shared) {
-    if ((rc = get_map(&p.act3[1], x, T, d, 16))) return rc;
-    if ((rc = get_map(&p.act4[1], hs, T, ffs, 16))) return rc;
-    if ((rc = get_map(&p.w13[0], w13s, 2ull * ffs, d, 64))) return rc;
-    if ((rc = get_map(&p.w2[0], w2s, d, ffs, 64))) return rc;
+    if ((rc = get_map(&m.act3[1], x, T, d, 16))) return rc;
+    if ((rc = get_map(&m.act4[1], hs, T, ffs, 16))) return rc;
+    if ((rc = get_map(&m.w13[0], w13s, 2ull * ffs, d, 64))) return rc;
+    if ((rc = get_map(&m.w2[0], w2s, d, ffs, 64))) return rc;
     p.group_expert[0] = -1;
     p.group_ff[0] = ffs;
   }
@@ -644,9 +694,11 @@ int launch_small_ffn(const void* x, int T, const int32_t* row_tokens, const void
   static unsigned seq = 0;
   if (!counters) {
     if (cudaMalloc(&counters, 256 * SG_COUNTERS * sizeof(int)) != cudaSuccess) return -2;
+    if (cudaMemset(counters, 0, 256 * SG_COUNTERS * sizeof(int)) != cudaSuccess) return -2;
   }
   int* c = counters + (seq++ % 256) * SG_COUNTERS;
-  if (cudaMemsetAsync(c, 0, (SG_CB_BASE + d / SG_BM) * sizeof(int), s) != cudaSuccess) return -2;
+  p.maps = upload_maps(m, s);
+  if (!p.maps) return -2;
   p.row_tokens = act ? nullptr : row_tokens;
   p.rows_cap = rows_cap;
   p.cdst = cdst;

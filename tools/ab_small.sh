@@ -2,4 +2,3 @@
 run() { env "$@" timeout 120 python bench.py --config C4D --no-cpu-baseline --no-e2e --steps 3000 --warmup 20 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$*', round(d['ms_per_step']*1000,1), 'us', round(d['roofline']['frac'],3), d['clocks']['sm_mhz'])"; }
 run COX_SMALL_FUSE=1
 run COX_SMALL_FUSE=0
-run COX_SMALL_FUSE=1 COX_SMALL_GATHER=0

@@ -1,0 +1,137 @@
+"""Per-unit timeline of the decode expert FFN kernel (csrc/small_gemm.cu).
+
+Builds a TRACED copy of the library (the kernel source patched to stamp
+%globaltimer when the producer picks up a unit and when the epilogue finishes
+it) into paper_2605_17889_b200/build/trace/, runs one C4 decode step through it
+and prints where the time goes: start-up, per-pass unit durations, idle gaps
+and the tail.  Debug tool only; the product library is untouched.
+
+    python tools/trace_small.py            # on the GPU box (gpurun)
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import re
+import shutil
+import sys
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+TRACE_DIR = ROOT / "paper_2605_17889_b200" / "build" / "trace"
+LIB = TRACE_DIR / "libcoxmoe_trace.so"
+MAXU = 96  # units recorded per CTA
+
+
+def make_traced_sources() -> Path:
+    src = TRACE_DIR / "csrc"
+    if src.exists():
+        shutil.rmtree(src)
+    shutil.copytree(ROOT / "paper_2605_17889_b200" / "csrc", src)
+    f = src / "small_gemm.cu"
+    s = f.read_text()
+    s = s.replace("namespace cox {\n", f"""namespace cox {{
+__device__ unsigned long long g_trace[160 * {MAXU + 2} * 3];
+__device__ __forceinline__ unsigned long long gtimer() {{
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}}
+""", 1)
+    # kernel start / end stamps
+    s = s.replace("  const uint32_t tmem_base = *tmem_slot;\n",
+                  f"  const uint32_t tmem_base = *tmem_slot;\n"
+                  f"  if (threadIdx.x == 0) g_trace[(blockIdx.x * {MAXU + 2} + {MAXU}) * 3] = gtimer();\n", 1)
+    s = s.replace("  tc_fence_before();\n  __syncthreads();\n  if (warp == 2) {\n    tc_fence_after();\n    tmem_dealloc<1>",
+                  f"  tc_fence_before();\n  __syncthreads();\n"
+                  f"  if (threadIdx.x == 0) g_trace[(blockIdx.x * {MAXU + 2} + {MAXU}) * 3 + 1] = gtimer();\n"
+                  f"  if (warp == 2) {{\n    tc_fence_after();\n    tmem_dealloc<1>", 1)
+    # producer: unit pick-up
+    s = s.replace("      int t = lane == 0 ? fetch(si, true) : 0;\n      t = __shfl_sync(0xffffffffu, t, 0);\n      if (t >= total) break;\n",
+                  f"      int t = lane == 0 ? fetch(si, true) : 0;\n      t = __shfl_sync(0xffffffffu, t, 0);\n      if (t >= total) break;\n"
+                  f"      if (lane == 0 && si - 1 < {MAXU}) {{\n"
+                  f"        g_trace[(blockIdx.x * {MAXU + 2} + si - 1) * 3] = gtimer();\n"
+                  f"        g_trace[(blockIdx.x * {MAXU + 2} + si - 1) * 3 + 2] = t;\n      }}\n", 1)
+    # epilogue: unit finished (after its last accumulator is released)
+    pat = "        if (lane == 0) mbar_arrive(smem_u32(&tempty[acc]));\n      }\n"
+    assert pat in s
+    s = s.replace(pat, pat + f"      if (tid == 0 && si - 1 < {MAXU}) g_trace[(blockIdx.x * {MAXU + 2} + si - 1) * 3 + 1] = gtimer();\n", 1)
+    s += f"""
+extern "C" int cox_trace_dump(unsigned long long* host) {{
+  return (int)cudaMemcpyFromSymbol(host, cox::g_trace, sizeof(unsigned long long) * 160 * {MAXU + 2} * 3);
+}}
+extern "C" int cox_trace_clear() {{
+  static unsigned long long z[160 * {MAXU + 2} * 3];
+  return (int)cudaMemcpyToSymbol(cox::g_trace, z, sizeof(z));
+}}
+"""
+    f.write_text(s)
+    return src
+
+
+def build_traced():
+    from paper_2605_17889_b200 import build
+    src = make_traced_sources()
+    build.build(force=True, out=LIB, csrc=src)
+
+
+def run():
+    os.environ["COXMOE_LIB"] = str(LIB)
+    import torch
+    from paper_2605_17889_b200.layer import MoELayer
+    from paper_2605_17889_b200.synthetic import make_layer_weights, make_tokens
+    from paper_2605_17889_b200 import _lib
+    T, d, ff, E, k, sff = 64, 2048, 1408, 64, 6, 2816
+    wts = make_layer_weights(E, d, ff, seed=0, device="cuda", shared_ff=sff)
+    x = make_tokens(T, d, seed=1, device="cuda")
+    layer = MoELayer(wts, k, "deepseek")
+    for _ in range(5):
+        layer(x)
+    torch.cuda.synchronize()
+    L = _lib.load()
+    L.cox_trace_clear()
+    layer(x)
+    torch.cuda.synchronize()
+    n = 160 * (MAXU + 2) * 3
+    buf = (ctypes.c_ulonglong * n)()
+    assert L.cox_trace_dump(buf) == 0
+    import numpy as np
+    a = np.frombuffer(buf, dtype=np.uint64).reshape(160, MAXU + 2, 3).astype(np.int64)
+    nb = 148
+    starts, ends = a[:nb, MAXU, 0], a[:nb, MAXU, 1]
+    t0 = starts.min()
+    print(f"CTA start spread {(starts.max() - t0) / 1e3:.1f} us; kernel body {(ends.max() - t0) / 1e3:.1f} us; "
+          f"first CTA end {(ends.min() - t0) / 1e3:.1f} us")
+    rec = []
+    for b in range(nb):
+        for u in range(MAXU):
+            s, e, t = a[b, u]
+            if s == 0:
+                break
+            rec.append((b, u, (s - t0) / 1e3, (e - t0) / 1e3 if e else float("nan"), int(t)))
+    total3 = None
+    ids = sorted(r[4] for r in rec)
+    print(f"units traced {len(rec)} (max id {ids[-1]})")
+    durs = np.array([r[3] - r[2] for r in rec])
+    print(f"unit pick-up -> done: median {np.nanmedian(durs):.1f} us, p90 {np.nanpercentile(durs, 90):.1f}")
+    first = np.array([min(r[2] for r in rec if r[0] == b) for b in range(nb)])
+    last_pick = np.array([max(r[2] for r in rec if r[0] == b) for b in range(nb)])
+    last_done = np.array([np.nanmax([r[3] for r in rec if r[0] == b]) for b in range(nb)])
+    print(f"first pick-up per CTA: median {np.median(first):.1f} us, max {first.max():.1f}")
+    print(f"last unit done per CTA: min {last_done.min():.1f} median {np.median(last_done):.1f} max {last_done.max():.1f} us")
+    per = {}
+    for b, u, s, e, t in rec:
+        per.setdefault(b, []).append((s, e, t))
+    # time by pass: the id where the down pass starts is where ids jump in duration; report by id quartiles
+    by_id = sorted(rec, key=lambda r: r[4])
+    for q in range(0, len(by_id), max(1, len(by_id) // 12)):
+        chunk = by_id[q:q + max(1, len(by_id) // 12)]
+        print(f"  ids {chunk[0][4]:5d}-{chunk[-1][4]:5d}: picked {chunk[0][2]:7.1f}-{chunk[-1][2]:7.1f} us, "
+              f"median dur {np.nanmedian([c[3] - c[2] for c in chunk]):5.1f} us")
+
+
+if __name__ == "__main__":
+    if "--run-only" not in sys.argv:
+        build_traced()
+    run()
