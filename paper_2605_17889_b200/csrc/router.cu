@@ -22,6 +22,8 @@
 // (T*E*d FMAs: 8.6 G for C2, 34 G for C4), so x is widened once per chunk and
 // each loaded router weight feeds RT_TPW FMAs.  Top-k is a warp-parallel
 // argmax (lane-local scan + shuffle reduction, ties to the lower index).
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace cox {
@@ -350,7 +352,10 @@ router_topk_staged_kernel(const __nv_bfloat16* __restrict__ x, const float* __re
 // identical to the fp32-weight kernels whenever wg is bf16-exact.
 constexpr int RB_TB = 32;
 
-__global__ void __launch_bounds__(RT_WARPS * 32, 1)
+// NW = warps per block: 8 (each warp 4 tokens x 8 experts) or 16 (4 tokens x 4
+// experts: twice the warps per scheduler to hide the conversion/FMA latencies).
+template <int NW>
+__global__ void __launch_bounds__(NW * 32, 1)
 router_topk_staged_bf16w_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ wg, int T,
                                 int d, int E, int k, int mode, int32_t* __restrict__ idx, float* __restrict__ wout,
                                 int32_t* __restrict__ counts) {
@@ -359,8 +364,9 @@ router_topk_staged_bf16w_kernel(const __nv_bfloat16* __restrict__ x, const __nv_
   __nv_bfloat16* sw = sx + (size_t)RB_TB * d;                                             // [2][RT_EG][d]
   float* s_logits = reinterpret_cast<float*>(sw + (size_t)2 * RT_EG * d);                // [RB_TB][E]
   __shared__ int s_hist[256];
-  __shared__ int s_sel[RT_WARPS][8];
-  __shared__ float s_selv[RT_WARPS][8];
+  __shared__ int s_sel[NW][8];
+  __shared__ float s_selv[NW][8];
+  constexpr int EPW = RT_EG * RT_WARPS / NW;  // experts per warp tile
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int i = threadIdx.x; i < E; i += blockDim.x) s_hist[i] = 0;
   const int vec_per_row = d / 8;
@@ -386,7 +392,8 @@ router_topk_staged_bf16w_kernel(const __nv_bfloat16* __restrict__ x, const __nv_
                  ok ? 16u : 0u);
     }
     stage_w(0, 0);  // commits x tile + group 0 together
-    const int tl0 = warp * RT_TPW;
+    const int tl0 = (warp % RT_WARPS) * RT_TPW;
+    const int eh = (warp / RT_WARPS) * EPW;  // first expert of this warp within the 8-expert slice
     for (int g = 0; g < ngroups; ++g) {
       if (g + 1 < ngroups) {
         stage_w(g + 1, (g + 1) & 1);
@@ -395,20 +402,20 @@ router_topk_staged_bf16w_kernel(const __nv_bfloat16* __restrict__ x, const __nv_
         asm volatile("cp.async.wait_group 0;" ::: "memory");
       }
       __syncthreads();
-      const __nv_bfloat16* swg = sw + (size_t)(g & 1) * RT_EG * d;
-      const int e0 = g * RT_EG;
-      float acc[RT_TPW][RT_EG];
+      const __nv_bfloat16* swg = sw + (size_t)(g & 1) * RT_EG * d + (size_t)eh * d;
+      const int e0 = g * RT_EG + eh;
+      float acc[RT_TPW][EPW];
 #pragma unroll
       for (int t = 0; t < RT_TPW; ++t)
 #pragma unroll
-        for (int e = 0; e < RT_EG; ++e) acc[t][e] = 0.0f;
+        for (int e = 0; e < EPW; ++e) acc[t][e] = 0.0f;
       for (int s = 8 * lane; s < d; s += 256) {
         float xv[RT_TPW][8];
 #pragma unroll
         for (int t = 0; t < RT_TPW; ++t)
           bf16x8_to_f32(*reinterpret_cast<const uint4*>(sx + (size_t)(tl0 + t) * d + s), xv[t]);
 #pragma unroll
-        for (int e = 0; e < RT_EG; e += 2) {
+        for (int e = 0; e < EPW; e += 2) {
           float wa[8], wb[8];
           bf16x8_to_f32(*reinterpret_cast<const uint4*>(swg + (size_t)e * d + s), wa);
           bf16x8_to_f32(*reinterpret_cast<const uint4*>(swg + (size_t)(e + 1) * d + s), wb);
@@ -421,7 +428,7 @@ router_topk_staged_bf16w_kernel(const __nv_bfloat16* __restrict__ x, const __nv_
 #pragma unroll
       for (int t = 0; t < RT_TPW; ++t)
 #pragma unroll
-        for (int e = 0; e < RT_EG; ++e) {
+        for (int e = 0; e < EPW; ++e) {
           float v = acc[t][e];
 #pragma unroll
           for (int off = 16; off >= 1; off >>= 1) v = __fadd_rn(v, __shfl_xor_sync(0xffffffffu, v, off));
@@ -429,7 +436,7 @@ router_topk_staged_bf16w_kernel(const __nv_bfloat16* __restrict__ x, const __nv_
         }
       __syncthreads();  // all warps done with buffer (g & 1) before it is refilled
     }
-    for (int tl = warp; tl < RB_TB; tl += RT_WARPS) {
+    for (int tl = warp; tl < RB_TB; tl += NW) {
       const long t = tb0 + tl;
       if (t >= T) break;
       float* lg = s_logits + tl * E;
@@ -492,20 +499,54 @@ int launch_router_bf16w(const void* x, const void* wg, int T, int d, int E, int 
   if (smem > 220 * 1024) return -1;
   if (cudaMemsetAsync(counts, 0, sizeof(int32_t) * E, s) != cudaSuccess) return -2;
   if (T == 0) return 0;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(router_topk_staged_bf16w_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-    attr = true;
-  }
+  static const int nw = [] {
+    const char* e = getenv("COX_ROUTER_NW");
+    return e && atoi(e) == 8 ? 8 : 16;
+  }();
   long blocks = (T + RB_TB - 1) / RB_TB;
   if (blocks > 148L * 8) blocks = 148L * 8;
-  router_topk_staged_bf16w_kernel<<<(int)blocks, RT_WARPS * 32, smem, s>>>(
-      static_cast<const __nv_bfloat16*>(x), static_cast<const __nv_bfloat16*>(wg), T, d, E, k, mode, idx, w, counts);
+  if (nw == 16) {
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(router_topk_staged_bf16w_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           220 * 1024);
+      attr = true;
+    }
+    router_topk_staged_bf16w_kernel<16><<<(int)blocks, 16 * 32, smem, s>>>(
+        static_cast<const __nv_bfloat16*>(x), static_cast<const __nv_bfloat16*>(wg), T, d, E, k, mode, idx, w,
+        counts);
+  } else {
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(router_topk_staged_bf16w_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           220 * 1024);
+      attr = true;
+    }
+    router_topk_staged_bf16w_kernel<8><<<(int)blocks, 8 * 32, smem, s>>>(
+        static_cast<const __nv_bfloat16*>(x), static_cast<const __nv_bfloat16*>(wg), T, d, E, k, mode, idx, w,
+        counts);
+  }
   return cudaGetLastError() == cudaSuccess ? 0 : -2;
 }
 
+int launch_router_tc(const void* x, const void* wg, int T, int d, int E, int k, int mode, int32_t* idx, float* w,
+                     int32_t* counts, cudaStream_t s);
+
 int launch_router(const void* x, int x_is_bf16, const void* wg, int wg_is_bf16, int T, int d, int E, int k,
                   int mode, int32_t* idx, float* w, int32_t* counts, cudaStream_t s) {
+  // Large batches with bf16 x and router weights: tensor-core screening +
+  // exact re-scoring (router_tc.cu).  COX_ROUTER_TC=0 forces the all-CUDA-core
+  // kernels below (same indices).
+  static const bool use_tc = [] {
+    const char* e = getenv("COX_ROUTER_TC");
+    return !(e && atoi(e) == 0);
+  }();
+  // (fine-grained MoE only: with E = 8 the all-CUDA-core kernel is faster,
+  // tools/bench_router.py: C2 0.85 ms vs 0.39 + 1.15 ms; C4 3.11 vs 1.77 ms)
+  if (use_tc && x_is_bf16 && wg_is_bf16 && E >= 32 && (long)T >= 148L * 128) {
+    const int rc = launch_router_tc(x, wg, T, d, E, k, mode, idx, w, counts, s);
+    if (rc != -3) return rc;  // -3: shape not supported by the screen -> CUDA-core kernels
+  }
   if (wg_is_bf16 && x_is_bf16 && E > RT_EG && (long)T >= 148L * RB_TB) {
     const int rc = launch_router_bf16w(x, wg, T, d, E, k, mode, idx, w, counts, s);
     if (rc != -1) return rc;  // -1: tile does not fit in smem -> generic kernels below
