@@ -278,66 +278,55 @@ COX_DEV uint4 ldg_v4(const void* p) { return __ldg(reinterpret_cast<const uint4*
 
 // NCH = x chunks per lane held in registers (d <= 256 NCH): the token's whole
 // x row is requested at once, so a token costs one DRAM round trip.
-template <int NCH>
+template <int NCH, int NE>
 __global__ void __launch_bounds__(RR_WARPS * 32, NCH <= 8 ? 2 : 1) router_rescore_kernel(
     const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ wg, const float* __restrict__ approx,
     const float* __restrict__ margin, int T, int d, int E, int k, int mode, int32_t* __restrict__ idx,
     float* __restrict__ wout, int32_t* __restrict__ counts) {
   __shared__ float s_l[RR_WARPS][256];     // per warp: approx logits, exact for the candidates
   __shared__ uint8_t s_cand[RR_WARPS][256];
+  __shared__ int s_win[RR_WARPS][8];       // exact winners by rank
   __shared__ int s_hist[256];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int i = threadIdx.x; i < E; i += blockDim.x) s_hist[i] = 0;
   __syncthreads();
-  const int nE = (E + 31) / 32;
   float* lg = s_l[warp];
   uint8_t* cand = s_cand[warp];
   for (long long t = (long long)blockIdx.x * RR_WARPS + warp; t < T; t += (long long)gridDim.x * RR_WARPS) {
-    float av[8];
+    float av[NE];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
+    for (int i = 0; i < NE; ++i) {
       const int e = lane + 32 * i;
-      av[i] = (i < nE && e < E) ? approx[t * E + e] : -INFINITY;
-      if (i < nE && e < E) lg[e] = av[i];
+      av[i] = e < E ? approx[t * E + e] : -INFINITY;
+      if (e < E) lg[e] = av[i];
     }
-    // k-th largest approx value
-    float kth = 0.f;
+    // k-th largest approx VALUE: k rounds of a value-only warp max; equal
+    // values leave together (that can only lower the threshold: a superset)
+    float kth = -INFINITY;
     {
       uint32_t taken = 0;
       for (int j = 0; j < k; ++j) {
         float bv = -INFINITY;
-        int bi = -1;
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const int e = lane + 32 * i;
-          if (i < nE && e < E && !(taken & (1u << i)) && (bi < 0 || av[i] > bv)) {
-            bv = av[i];
-            bi = e;
-          }
-        }
+        for (int i = 0; i < NE; ++i)
+          if (!(taken & (1u << i))) bv = fmaxf(bv, av[i]);
 #pragma unroll
-        for (int off = 16; off >= 1; off >>= 1) {
-          const float ov = __shfl_xor_sync(0xffffffffu, bv, off);
-          const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
-          if (oi >= 0 && (bi < 0 || ov > bv || (ov == bv && oi < bi))) {
-            bv = ov;
-            bi = oi;
-          }
-        }
-        if (bi >= 0 && (bi & 31) == lane) taken |= 1u << (bi >> 5);
+        for (int off = 16; off >= 1; off >>= 1) bv = fmaxf(bv, __shfl_xor_sync(0xffffffffu, bv, off));
+#pragma unroll
+        for (int i = 0; i < NE; ++i)
+          if (av[i] == bv) taken |= 1u << i;
         kth = bv;
       }
     }
     const float thr = kth - 2.0f * margin[t];
     int nc = 0;
-    uint32_t cm[8];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
+    for (int i = 0; i < NE; ++i) {
       const int e = lane + 32 * i;
-      const bool c = i < nE && e < E && av[i] >= thr;
-      cm[i] = __ballot_sync(0xffffffffu, c);
-      if (c) cand[nc + __popc(cm[i] & ((1u << lane) - 1u))] = (uint8_t)e;
-      nc += __popc(cm[i]);
+      const bool c = e < E && av[i] >= thr;
+      const uint32_t bal = __ballot_sync(0xffffffffu, c);
+      if (c) cand[nc + __popc(bal & ((1u << lane) - 1u))] = (uint8_t)e;
+      nc += __popc(bal);
     }
     __syncwarp();
     const __nv_bfloat16* xr = x + t * d;
@@ -381,35 +370,30 @@ __global__ void __launch_bounds__(RR_WARPS * 32, NCH <= 8 ? 2 : 1) router_rescor
       }
     }
     __syncwarp();
-    // exact top-k among the candidates (ties -> lower index)
+    // exact top-k among the candidates: the rank of candidate slot c is the
+    // number of candidates with a larger exact logit, or an equal one and a
+    // lower expert index (the tie rule); slots are spread over the lanes
+    for (int c0 = 0; c0 < nc; c0 += 32) {
+      const int c = c0 + lane;
+      const int e = c < nc ? cand[c] : 0;
+      const float v = c < nc ? lg[e] : 0.f;
+      int rank = 0;
+      for (int o = 0; o < nc; ++o) {
+        const int eo = cand[o];
+        const float vo = lg[eo];
+        rank += (vo > v || (vo == v && eo < e)) ? 1 : 0;
+      }
+      if (c < nc && rank < k) s_win[warp][rank] = e;
+    }
+    __syncwarp();
     int sel[8];
     float selv[8];
-    uint32_t taken = 0;  // bit i: candidate e = lane + 32 i already selected
-    for (int j = 0; j < k; ++j) {
-      float bv = 0.f;
-      int bi = -1;
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const int e = lane + 32 * i;
-        if (!((cm[i] >> lane) & 1u) || (taken & (1u << i))) continue;
-        const float v = lg[e];
-        if (bi < 0 || v > bv) {
-          bv = v;
-          bi = e;
-        }
+    for (int j = 0; j < 8; ++j) {
+      if (j < k) {
+        sel[j] = s_win[warp][j];
+        selv[j] = lg[sel[j]];
       }
-#pragma unroll
-      for (int off = 16; off >= 1; off >>= 1) {
-        const float ov = __shfl_xor_sync(0xffffffffu, bv, off);
-        const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
-        if (oi >= 0 && (bi < 0 || ov > bv || (ov == bv && oi < bi))) {
-          bv = ov;
-          bi = oi;
-        }
-      }
-      if ((bi & 31) == lane) taken |= 1u << (bi >> 5);
-      sel[j] = bi;
-      selv[j] = bv;
     }
     __syncwarp();
     if (mode != 0) {  // full-softmax denominator terms in parallel
@@ -490,23 +474,31 @@ int launch_router_tc(const void* x, const void* wg, int T, int d, int E, int k, 
   router_screen_kernel<<<grid, RC_THREADS, smem, s>>>(p);
   long long blocks = ((long long)T + RR_WARPS - 1) / RR_WARPS;
   if (blocks > (long long)num_sms * 8) blocks = (long long)num_sms * 8;
-#define RR_LAUNCH(NCH_)                                                                                          \
+#define RR_LAUNCH(NCH_, NE_)                                                                                     \
   do {                                                                                                           \
     static bool carve = false;                                                                                   \
     if (!carve) { /* data flows through L1: keep the L1 share large */                                           \
-      cudaFuncSetAttribute(router_rescore_kernel<NCH_>, cudaFuncAttributePreferredSharedMemoryCarveout, 10);    \
+      cudaFuncSetAttribute(router_rescore_kernel<NCH_, NE_>, cudaFuncAttributePreferredSharedMemoryCarveout, 10); \
       carve = true;                                                                                              \
     }                                                                                                            \
-    router_rescore_kernel<NCH_><<<(int)blocks, RR_WARPS * 32, 0, s>>>(                                           \
+    router_rescore_kernel<NCH_, NE_><<<(int)blocks, RR_WARPS * 32, 0, s>>>(                                      \
         static_cast<const __nv_bfloat16*>(x), static_cast<const __nv_bfloat16*>(wg), p.approx, p.margin, T, d, E, \
         k, mode, idx, w, counts);                                                                                \
   } while (0)
+#define RR_BY_NE(NCH_)                          \
+  do {                                          \
+    if (E <= 32) RR_LAUNCH(NCH_, 1);            \
+    else if (E <= 64) RR_LAUNCH(NCH_, 2);       \
+    else if (E <= 128) RR_LAUNCH(NCH_, 4);      \
+    else RR_LAUNCH(NCH_, 8);                    \
+  } while (0)
   const int nch = (d + 255) / 256;
-  if (nch <= 4) RR_LAUNCH(4);
-  else if (nch <= 8) RR_LAUNCH(8);
-  else if (nch <= 16) RR_LAUNCH(16);
-  else if (nch <= 24) RR_LAUNCH(24);
+  if (nch <= 4) RR_BY_NE(4);
+  else if (nch <= 8) RR_BY_NE(8);
+  else if (nch <= 16) RR_BY_NE(16);
+  else if (nch <= 24) RR_BY_NE(24);
   else return -3;
+#undef RR_BY_NE
 #undef RR_LAUNCH
   return cudaGetLastError() == cudaSuccess ? 0 : -2;
 }
