@@ -64,7 +64,13 @@ int cox_router_topk(const void* x, int x_dtype, const float* wg, int T, int d, i
 /* Same with the router weight dtype explicit (COX_DTYPE_BF16 or COX_DTYPE_F32).
  * A bf16 wg (the checkpoint dtype of Mixtral/DeepSeek routers) is staged in
  * shared memory by the fine-grained (E > 8) kernel; the logits are identical
- * to passing the same values as fp32 (bf16 x bf16 products are exact). */
+ * to passing the same values as fp32 (bf16 x bf16 products are exact).
+ * bf16 x and wg, E >= 32, T >= 18944: the logits are screened on the tensor
+ * cores (fp32 accumulation, per-token error bound) and only the candidates
+ * that can reach the top-k are recomputed in the canonical order: same idx
+ * and counts; COX_ROUTE_MIXTRAL weights identical; COX_ROUTE_DEEPSEEK
+ * weights within ~1e-6 relative (their full-softmax denominator uses the
+ * screened logits of the non-candidates).  COX_ROUTER_TC=0 disables. */
 int cox_router_topk_ex(const void* x, int x_dtype, const void* wg, int wg_dtype, int T, int d, int E, int k,
                        int mode, int32_t* idx, float* w, int32_t* counts, void* stream);
 
