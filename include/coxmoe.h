@@ -155,6 +155,23 @@ int cox_small_expert_ffn(const void* x, int T, const int32_t* row_tokens, const 
                          const void* w2_shared, int ff_shared, void* h_shared, void* y_shared, const int32_t* dst,
                          const float* w, int k, void* out, void* stream);
 
+/* The whole MoE layer for a decode step (T <= 64 tokens, E <= 64 experts) in
+ * ONE launch: router (bf16 wg, canonical order: idx bit-exact with
+ * cox_router_topk), SwiGLU + down projection of EVERY expert over all T tokens
+ * (the step streams every expert's weights anyway; the idle tensor pipe
+ * computes the unrouted pairs, so routing is off the critical path), shared
+ * experts and the weighted combine of the routed pairs.
+ *   x [T, d] bf16; wg [E, d] bf16; w13[e] [2 ff, d] (interleaved), w2[e] [d, ff]
+ *   h [E*T, ff], y [E*T, d] bf16 scratch (expert e's rows at e*T)
+ *   optional shared experts: w13_shared [2 ff_shared, d], w2_shared [d, ff_shared],
+ *   h_shared [T, ff_shared], y_shared [T, d]
+ *   idx [T, k] int32, w [T, k] fp32: the routing; out [T, d] bf16.
+ * d % 128 == 0, ff % 128 == 0, ff_shared % 128 == 0. */
+int cox_decode_moe(const void* x, int T, const void* wg, int E, int k, int mode, const void* const* w13,
+                   const void* const* w2, int d, int ff, const void* w13_shared, const void* w2_shared, int ff_shared,
+                   void* h, void* y, void* h_shared, void* y_shared, int32_t* idx, float* w, void* out,
+                   void* stream);
+
 /* K5 — weighted top-k combine back to token order (+ optional shared-expert
  * output, DeepSeek-V2):  out[t] = sum_j w[t,j] * y_perm[dst[t,j]] (+ shared[t]).
  * out/shared dtype = out_dtype (bf16 or fp32). */

@@ -17,11 +17,17 @@ int launch_permute(const int32_t* idx, int T, int k, int E, int tile_m, const vo
 int launch_grouped_gemm(int epi, const void* A, long long rows_cap, int K, const int32_t* offsets, int n_groups,
                         const int32_t* group_expert, const void* const* B, int N, void* out, long long ldo,
                         int max_ctas, cudaStream_t s, const int32_t* a_rows = nullptr, long long a_rows_cap = 0);
+struct SmallDense {
+  const void* wg;
+  int E, mode;
+  int32_t* idx;
+  float* w;
+};
 int launch_small_ffn(const void* x, int T, const int32_t* row_tokens, const void* act, long long rows_cap,
                      const int32_t* offsets, int n_groups, const int32_t* group_expert, const void* const* w13,
                      const void* const* w2, int d, int ff, void* h, void* y, const void* w13s, const void* w2s,
                      int ffs, void* hs, void* ys, const int32_t* cdst, const float* cw, int k, void* out,
-                     int phases, cudaStream_t s);
+                     int phases, cudaStream_t s, const SmallDense* dense = nullptr);
 int launch_combine(const void* y_perm, const int32_t* dst, const float* w, int T, int k, int d, const void* shared,
                    void* out, int out_is_bf16, cudaStream_t s);
 
@@ -222,6 +228,32 @@ int cox_small_expert_ffn(const void* x, int T, const int32_t* row_tokens, const 
   int rc = cox::launch_small_ffn(x, T, row_tokens, x_perm, rows_cap, offsets, n_groups, group_experts, w13, w2, d, ff,
                                  h, y_perm, w13_shared, w2_shared, ff_shared, h_shared, y_shared, dst, w, k, out, 3,
                                  static_cast<cudaStream_t>(stream));
+  return cuda_status(rc, fn);
+}
+
+int cox_decode_moe(const void* x, int T, const void* wg, int E, int k, int mode, const void* const* w13,
+                   const void* const* w2, int d, int ff, const void* w13_shared, const void* w2_shared, int ff_shared,
+                   void* h, void* y, void* h_shared, void* y_shared, int32_t* idx, float* w, void* out,
+                   void* stream) {
+  const char* fn = "cox_decode_moe";
+  if (T < 1 || T > 64) return fail(COX_EINVAL, "%s: need 1 <= T <= 64 (T=%d)", fn, T);
+  if (E < 1 || E > 64 || k < 1 || k > 8 || k > E) return fail(COX_EINVAL, "%s: need 1 <= k <= min(E, 8), E <= 64", fn);
+  if (mode != COX_ROUTE_MIXTRAL && mode != COX_ROUTE_DEEPSEEK) return fail(COX_EINVAL, "%s: bad mode %d", fn, mode);
+  if (d <= 0 || d % 128 || ff <= 0 || ff % 128) return fail(COX_EINVAL, "%s: need d %% 128 == 0, ff %% 128 == 0", fn);
+  if (!x || !wg || !h || !y || !idx || !w || !out || !aligned16(x) || !aligned16(wg) || !aligned16(h) ||
+      !aligned16(y) || !aligned16(out))
+    return fail(COX_EINVAL, "%s: null or unaligned operand", fn);
+  if (w13_shared && (ff_shared <= 0 || ff_shared % 128 || !w2_shared || !h_shared || !y_shared ||
+                     !aligned16(h_shared) || !aligned16(y_shared)))
+    return fail(COX_EINVAL, "%s: bad shared-expert operands", fn);
+  int32_t ids[64];
+  for (int e = 0; e < E; ++e) ids[e] = e;
+  if (int rc = check_groups(fn, E, ids, w13)) return rc;
+  if (int rc = check_groups(fn, E, ids, w2)) return rc;
+  cox::SmallDense dn{wg, E, mode, idx, w};
+  int rc = cox::launch_small_ffn(x, T, nullptr, nullptr, (long long)E * T, nullptr, E, ids, w13, w2, d, ff, h, y,
+                                 w13_shared, w2_shared, ff_shared, h_shared, y_shared, nullptr, nullptr, k, out, 3,
+                                 static_cast<cudaStream_t>(stream), &dn);
   return cuda_status(rc, fn);
 }
 

@@ -68,7 +68,7 @@ struct SgCfg {
   static constexpr int STAGES = (int)(SG_RING_BYTES / (A_STAGE + B_STAGE)) > 12 ? 12
                                                                                : (int)(SG_RING_BYTES / (A_STAGE + B_STAGE));
   static constexpr uint32_t TMEM_COLS = 2 * NMAX < 64 ? 64 : 2 * NMAX;
-  static constexpr size_t SMEM = 1024 + STAGES * (A_STAGE + B_STAGE) + 512 + 24 * (SG_MAXG + 2) +
+  static constexpr size_t SMEM = 1024 + STAGES * (A_STAGE + B_STAGE) + 512 + 1024 + 24 * (SG_MAXG + 2) +
                                  4 * SG_BM * SG_PITCH + 64;
 };
 
@@ -100,6 +100,18 @@ struct SmallParams {
   int k;
   int T;
   int k4_colmajor;
+  // dense decode (dense != 0): every group runs over all T tokens (B = x rows
+  // [0, T); routed group g writes h/y rows [(g - g0) T, +T)) and warp 2 of CTA
+  // b routes token b (canonical order, like router_topk_kernel) into ridx/rw;
+  // the combine reads y[(expert_slot[e]) T + t]
+  int dense;
+  const __nv_bfloat16* wg;  // [E, d] bf16 router weight
+  const __nv_bfloat16* xtok;  // [T, d] the step's tokens
+  int E;
+  int mode;
+  int32_t* ridx;  // [T, k]
+  float* rw;      // [T, k]
+  int16_t expert_slot[256];  // routed expert -> its row block in h/y (dense)
   int group_expert[SG_MAXG];  // >= 0: routed expert (segment from offsets); -1: shared (rows [0, Ts))
   int group_ff[SG_MAXG];
   int n_groups;
@@ -109,6 +121,7 @@ struct SmallParams {
 };
 constexpr int SG_CB_BASE = 1 + SG_MAXG;  // counters[SG_CB_BASE + i]: down tiles stored in column block i
 constexpr int SG_COUNTERS = 256;
+constexpr int SG_ROUTED = SG_COUNTERS - 2;  // dense: tokens routed so far
 
 
 COX_DEV void mbar_spin_ge(const int* p, int want) {
@@ -160,7 +173,8 @@ __global__ void __launch_bounds__(SG_THREADS, 1) small_ffn_kernel(const __grid_c
   int* s_p4 = s_p3 + SG_MAXG + 1;    // [G+1] prefix of down units
   int* s_misc = s_p4 + SG_MAXG + 1;  // [0] groups with rows, [1] combine flag
   int* s_act = s_misc + 4;            // [G] active groups (rows > 0), in group order
-  float* stg = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(s_act + SG_MAXG) + 15) & ~uintptr_t(15));
+  float* s_route = reinterpret_cast<float*>(s_act + SG_MAXG);  // [256] dense: logits of the token being routed
+  float* stg = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(s_route + 256) + 15) & ~uintptr_t(15));
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -190,8 +204,13 @@ __global__ void __launch_bounds__(SG_THREADS, 1) small_ffn_kernel(const __grid_c
       int rows = 0, r0 = 0;
       if (g < G) {
         const int e = p.group_expert[g];
-        r0 = e >= 0 ? p.offsets[e] : 0;
-        rows = e >= 0 ? p.offsets[e + 1] - r0 : p.Ts;
+        if (p.dense) {
+          rows = p.T;
+          r0 = e >= 0 ? p.expert_slot[e] * p.T : 0;
+        } else {
+          r0 = e >= 0 ? p.offsets[e] : 0;
+          rows = e >= 0 ? p.offsets[e + 1] - r0 : p.Ts;
+        }
         s_row0[g] = r0;
         s_rows[g] = rows;
       }
@@ -296,9 +315,10 @@ __global__ void __launch_bounds__(SG_THREADS, 1) small_ffn_kernel(const __grid_c
       decode(t, pass, g, i);
       const int rows = s_rows[g], row0 = s_row0[g];
       const int src = p.group_expert[g] < 0 ? 1 : 0;
-      const bool gat = pass == 0 && src == 0 && p.row_tokens != nullptr;
+      const bool gat = pass == 0 && src == 0 && p.row_tokens != nullptr && !p.dense;
       const CUtensorMap* wmap = pass == 0 ? &p.maps->w13[g] : &p.maps->w2[g];
-      const CUtensorMap* amap = pass == 0 ? &p.maps->act3[src] : &p.maps->act4[src];
+      const CUtensorMap* amap = pass == 0 ? &p.maps->act3[p.dense ? 1 : src] : &p.maps->act4[src];
+      const int brow0 = (pass == 0 && p.dense) ? 0 : row0;  // dense SwiGLU: B = x rows [0, T)
       const int K = pass == 0 ? p.d : p.group_ff[g];
       const int nk = (K + SG_BK - 1) / SG_BK;  // the last stage may hold fewer than KA atoms
       // weight rows of the two 64-row halves of the A tile
@@ -350,7 +370,7 @@ __global__ void __launch_bounds__(SG_THREADS, 1) small_ffn_kernel(const __grid_c
               for (int a = 0; a < na; ++a)
                 for (int b = 0; b < nb; ++b)
                   tma_load_2d(b_dst + a * C::B_ATOM + b * 2048u, amap, fb, kb * SG_BK + a * SG_ATOM,
-                              row0 + c0 + 16 * b);
+                              brow0 + c0 + 16 * b);
               if (++st0 == SG_STAGES) {
                 st0 = 0;
                 ph0 ^= 1;
@@ -384,7 +404,7 @@ __global__ void __launch_bounds__(SG_THREADS, 1) small_ffn_kernel(const __grid_c
               for (int a = 0; a < KA; ++a)
                 for (int b = 0; b < nb && a < na; ++b)
                   tma_load_2d(b_dst + a * C::B_ATOM + b * 2048u, amap, fb, kb * SG_BK + a * SG_ATOM,
-                              row0 + c0 + 16 * b);
+                              brow0 + c0 + 16 * b);
             }
           }
           if (gat && lane < 4 * nb) {
@@ -445,6 +465,94 @@ __global__ void __launch_bounds__(SG_THREADS, 1) small_ffn_kernel(const __grid_c
       }
     }
     __syncwarp();
+  } else if (warp == 2) {
+    // ------------------------------------------------------------ dense decode: in-kernel router
+    // Token t = blockIdx.x (+ gridDim.x ...): logits in the canonical order of
+    // router_topk_kernel (lane chunks s = 8 lane + 256 j, fma ascending, xor
+    // butterfly; expert pairs share one FFMA2), top-k with ties to the lower
+    // index, Mixtral / DeepSeek weights.  Only the combine needs the result, so
+    // this runs beside the weight stream instead of before it.
+    if (p.dense) {
+      const int d = p.d, E = p.E, kk = p.k;
+      for (int t = blockIdx.x; t < p.T; t += gridDim.x) {
+        const __nv_bfloat16* xr = p.xtok + (long long)t * d;
+        for (int e0 = 0; e0 < E; e0 += 8) {
+          float acc[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) acc[u] = 0.f;
+#pragma unroll 2
+          for (int sc = 8 * lane; sc < d; sc += 256) {
+            float xv[8];
+            bf16x8_to_f32(ld_nc_v4(xr + sc), xv);
+#pragma unroll
+            for (int u = 0; u < 8; u += 2) {
+              float wa[8], wb[8];
+              const int ea = min(e0 + u, E - 1), eb = min(e0 + u + 1, E - 1);
+              bf16x8_to_f32(ld_nc_v4(p.wg + (long long)ea * d + sc), wa);
+              bf16x8_to_f32(ld_nc_v4(p.wg + (long long)eb * d + sc), wb);
+#pragma unroll
+              for (int q = 0; q < 8; ++q) ffma2(acc[u], acc[u + 1], xv[q], wa[q], wb[q]);
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            float v = acc[u];
+#pragma unroll
+            for (int off = 16; off >= 1; off >>= 1) v = __fadd_rn(v, __shfl_xor_sync(0xffffffffu, v, off));
+            if (lane == 0 && e0 + u < E) s_route[e0 + u] = v;
+          }
+        }
+        __syncwarp();
+        int sel[8];
+        float selv[8];
+        uint32_t taken = 0;
+        for (int j = 0; j < kk; ++j) {
+          float bv = 0.f;
+          int bi = -1;
+          for (int i = 0; lane + 32 * i < E; ++i) {
+            const int e = lane + 32 * i;
+            if (taken & (1u << i)) continue;
+            const float v = s_route[e];
+            if (bi < 0 || v > bv) {
+              bv = v;
+              bi = e;
+            }
+          }
+#pragma unroll
+          for (int off = 16; off >= 1; off >>= 1) {
+            const float ov = __shfl_xor_sync(0xffffffffu, bv, off);
+            const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
+            if (oi >= 0 && (bi < 0 || ov > bv || (ov == bv && oi < bi))) {
+              bv = ov;
+              bi = oi;
+            }
+          }
+          if ((bi & 31) == lane) taken |= 1u << (bi >> 5);
+          sel[j & 7] = bi;
+          selv[j & 7] = bv;
+        }
+        if (p.mode != 0) {
+          for (int e = lane; e < E; e += 32) s_route[e] = expf(__fsub_rn(s_route[e], selv[0]));
+          __syncwarp();
+        }
+        if (lane == 0) {
+          const float m = selv[0];
+          float ssum = 0.0f;
+          if (p.mode == 0) {
+            for (int j = 0; j < kk; ++j) ssum = __fadd_rn(ssum, expf(__fsub_rn(selv[j], m)));
+          } else {
+            for (int e = 0; e < E; ++e) ssum = __fadd_rn(ssum, s_route[e]);  // ascending e, as the oracle
+          }
+          for (int j = 0; j < kk; ++j) {
+            p.ridx[t * kk + j] = sel[j];
+            p.rw[t * kk + j] = __fdiv_rn(expf(__fsub_rn(selv[j], m)), ssum);
+          }
+          __threadfence();
+          atomicAdd(p.counters + SG_ROUTED, 1);
+        }
+        __syncwarp();
+      }
+    }
   } else if (warp >= 4) {
     // ------------------------------------------------------------ epilogue
     // Warp q reads TMEM lanes 32q..32q+31 (= weight rows of the unit), 32
@@ -532,10 +640,17 @@ __global__ void __launch_bounds__(SG_THREADS, 1) small_ffn_kernel(const __grid_c
           const int T = p.T, kk = p.k, d = p.d;
           int* s_dst = reinterpret_cast<int*>(stg);
           float* s_w = reinterpret_cast<float*>(stg) + T * kk;
+          if (p.dense && tid == 0) mbar_spin_ge(p.counters + SG_ROUTED, T);  // routing of every token done
+          named_bar_epi();
           __threadfence();
           for (int e = tid; e < T * kk; e += 128) {
-            s_dst[e] = p.cdst[e];
-            s_w[e] = p.cw[e];
+            if (p.dense) {
+              s_dst[e] = p.expert_slot[p.ridx[e]] * T + e / kk;
+              s_w[e] = p.rw[e];
+            } else {
+              s_dst[e] = p.cdst[e];
+              s_w[e] = p.cw[e];
+            }
           }
           named_bar_epi();
           const __nv_bfloat16* y0 = p.y[0];
@@ -613,6 +728,7 @@ __global__ void __launch_bounds__(SG_THREADS, 1) small_ffn_kernel(const __grid_c
       __threadfence();
       const int n = SG_CB_BASE + p.d / SG_BM;
       for (int c = 0; c < n; ++c) p.counters[c] = 0;
+      p.counters[SG_ROUTED] = 0;
       p.counters[SG_COUNTERS - 1] = 0;
     }
   }
@@ -649,11 +765,18 @@ static const SmallMaps* upload_maps(const SmallMaps& m, cudaStream_t s) {
 // x [T, d] through row_tokens[rows_cap].  h: [rows_cap, ff]; y: [rows_cap, d].
 // Shared expert group (w13s != nullptr) over x: w13s [2 ffs, d], w2s [d, ffs],
 // hs [T, ffs], ys [T, d].  Fused combine when out != nullptr (bf16 [T, d]).
+struct SmallDense {  // in-kernel routing (dense decode), see SmallParams::dense
+  const void* wg;
+  int E, mode;
+  int32_t* idx;
+  float* w;
+};
+
 int launch_small_ffn(const void* x, int T, const int32_t* row_tokens, const void* act, long long rows_cap,
                      const int32_t* offsets, int n_groups, const int32_t* group_expert, const void* const* w13,
                      const void* const* w2, int d, int ff, void* h, void* y, const void* w13s, const void* w2s,
                      int ffs, void* hs, void* ys, const int32_t* cdst, const float* cw, int k, void* out,
-                     int phases, cudaStream_t s) {
+                     int phases, cudaStream_t s, const SmallDense* dense = nullptr) {
   const bool shared = w13s != nullptr && T > 0;
   const int G = n_groups + (shared ? 1 : 0);
   if (G == 0) return 0;
@@ -663,7 +786,12 @@ int launch_small_ffn(const void* x, int T, const int32_t* row_tokens, const void
   std::lock_guard<std::mutex> lk(mu);
   memset(&m, 0, sizeof(m));
   int rc = 0;
-  if (n_groups > 0) {
+  if (dense) {
+    if ((rc = get_map(&m.act3[1], x, T, d, 16))) return rc;  // every group's SwiGLU B = x rows [0, T)
+    if ((rc = get_map(&m.act4[0], h, rows_cap, ff, 16))) return rc;
+    for (int e = 0; e < 256; ++e) p.expert_slot[e] = -1;
+    for (int g = 0; g < n_groups; ++g) p.expert_slot[group_expert[g]] = (int16_t)g;
+  } else if (n_groups > 0) {
     if (act) {
       if ((rc = get_map(&m.act3[0], act, rows_cap, d, 16))) return rc;
     } else {
@@ -681,7 +809,7 @@ int launch_small_ffn(const void* x, int T, const int32_t* row_tokens, const void
     p.group_ff[g0 + g] = ff;
   }
   if (shared) {
-    if ((rc = get_map(&m.act3[1], x, T, d, 16))) return rc;
+    if (!dense && (rc = get_map(&m.act3[1], x, T, d, 16))) return rc;
     if ((rc = get_map(&m.act4[1], hs, T, ffs, 16))) return rc;
     if ((rc = get_map(&m.w13[0], w13s, 2ull * ffs, d, 64))) return rc;
     if ((rc = get_map(&m.w2[0], w2s, d, ffs, 64))) return rc;
@@ -711,6 +839,15 @@ int launch_small_ffn(const void* x, int T, const int32_t* row_tokens, const void
     return e ? atoi(e) : 0;
   }();
   p.k4_colmajor = colmajor;
+  p.dense = dense ? 1 : 0;
+  if (dense) {
+    p.wg = static_cast<const __nv_bfloat16*>(dense->wg);
+    p.xtok = static_cast<const __nv_bfloat16*>(x);
+    p.E = dense->E;
+    p.mode = dense->mode;
+    p.ridx = dense->idx;
+    p.rw = dense->w;
+  }
   p.counters = c;
   p.offsets = offsets;
   p.h[0] = static_cast<__nv_bfloat16*>(h);

@@ -103,6 +103,8 @@ class MoELayer:
         # permute: single-CTA index kernel for T*k <= 16384 (else hist, scan, scatter) + row copy (+ pad)
         small_perm = T is not None and T * self.k <= 16384
         perm = (1 if small_perm else 3) + 1 + (1 if self.tile_m > 1 else 0)
+        if T is not None and self.uses_dense_decode(T):
+            return 1  # router + all experts + shared + combine in one launch
         if T is not None and self.uses_small_path(T):
             # router + single-CTA permute (indices only) + one launch for K3/K4/shared/combine
             return 1 + 1 + 1 + (1 if self.out_dtype != torch.bfloat16 else 0)
@@ -218,11 +220,40 @@ class MoELayer:
             ops.combine(b.y, b.dst, b.w, b.shared_y if self.shared_ff else None, out=out)
         return out
 
+    # Mid-size decode steps: router + every expert over all tokens + shared
+    # experts + combine in ONE launch (cox_decode_moe).  It streams EVERY
+    # expert, so it only pays when nearly all are touched anyway, and its token
+    # tiles grow with T: measured on C4 (tools/sweep_decode.py, us/step, dense
+    # vs routed): T=8 184/139, 16 186/179, 24 191/206, 32 192/212, 48 203/218,
+    # 64 227/221.  Used when T <= DENSE_T_MAX and P(expert untouched) =
+    # (1 - k/E)^T <= 0.1; COX_DECODE_DENSE=0 disables.
+    DENSE_T_MAX = 48 if os.environ.get("COX_DECODE_DENSE", "1") == "1" else 0
+
+    def uses_dense_decode(self, T: int) -> bool:
+        return (self.uses_small_path(T) and T <= self.DENSE_T_MAX and (1.0 - self.k / self.E) ** T <= 0.1
+                and self.wg_router.dtype == torch.bfloat16 and self.out_dtype == torch.bfloat16)
+
     def _forward_small(self, x: torch.Tensor, b: StageBuffers, out: torch.Tensor | None):
         """Decode-size step: router, index-only permute (no row copy), then ONE
-        launch for K3 + K4 + shared experts + combine (csrc/small_gemm.cu)."""
+        launch for K3 + K4 + shared experts + combine (csrc/small_gemm.cu).
+        At <= 64 tokens the router runs inside that launch too (dense decode)."""
+        out = b.out if out is None else out
+        T = x.shape[0]
+        if self.uses_dense_decode(T):
+            dh, dy = self._dense_scratch(T, x.device)
+            shared = (self.wts.shared_w13, self.wts.shared_w2, b.shared_h, b.shared_y) if self.shared_ff else None
+            return ops.decode_moe(x, self.wg_router, self.k, self.mode, self.w13_list, self.w2_list, dh, dy,
+                                  b.idx, b.w, out, shared)
         self._route_small(x, b)
-        return self._ffn_small(x, b, b.out if out is None else out)
+        return self._ffn_small(x, b, out)
+
+    def _dense_scratch(self, T: int, dev):
+        sc = getattr(self, "_dense", None)
+        if sc is None or sc[0].shape[0] != self.E * T:
+            sc = (torch.empty((self.E * T, self.ff), dtype=torch.bfloat16, device=dev),
+                  torch.empty((self.E * T, self.d), dtype=torch.bfloat16, device=dev))
+            self._dense = sc
+        return sc
 
     def _side_stream(self, dev):
         st = getattr(self, "_side", None)
@@ -319,6 +350,12 @@ class MoELayer:
         if x is None:
             raise ValueError("stage_times needs the step's input")
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(7)]
+        if self.uses_dense_decode(x.shape[0]):
+            ev[0].record()
+            self._forward_small(x, b, b.out)
+            ev[1].record()
+            torch.cuda.synchronize()
+            return {"decode_moe_one_launch": ev[0].elapsed_time(ev[1])}
         ev[0].record()
         ops.router_topk(x, self.wg_router, self.k, self.mode, out=(b.idx, b.w, b.counts))
         ev[1].record()

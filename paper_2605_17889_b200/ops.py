@@ -249,6 +249,37 @@ def small_expert_ffn(x: torch.Tensor, offsets: torch.Tensor, group_experts: Sequ
     return out if out is not None else y
 
 
+def decode_moe(x: torch.Tensor, wg: torch.Tensor, k: int, mode: int, w13: Sequence[torch.Tensor],
+               w2: Sequence[torch.Tensor], h: torch.Tensor, y: torch.Tensor, idx: torch.Tensor, w: torch.Tensor,
+               out: torch.Tensor, shared=None, stream=None):
+    """Whole decode-step MoE layer in one launch (router + every expert over all
+    T <= 64 tokens + shared experts + combine).  h [E*T, ff], y [E*T, d] scratch;
+    shared = (w13_shared, w2_shared, h_shared, y_shared)."""
+    _need(x, "x", _BF16, 2)
+    _need(wg, "wg", _BF16, 2)
+    T, d = x.shape
+    E = wg.shape[0]
+    ff = h.shape[1]
+    for t, n in ((h, "h"), (y, "y"), (out, "out")):
+        _need(t, n, _BF16, 2)
+    _need(idx, "idx", torch.int32, 2)
+    _need(w, "w", torch.float32, 2)
+    if (wg.shape[1] != d or h.shape[0] != E * T or tuple(y.shape) != (E * T, d) or tuple(out.shape) != (T, d)
+            or tuple(idx.shape) != (T, k) or tuple(w.shape) != (T, k) or len(w13) != E or len(w2) != E):
+        raise ValueError("decode_moe: inconsistent shapes")
+    sw13 = sw2 = sh = sy = None
+    ffs = 0
+    if shared is not None:
+        sw13, sw2, sh, sy = shared
+        ffs = sh.shape[1]
+    ptr = lambda t: t.data_ptr() if t is not None else None  # noqa: E731
+    L = _lib.lib()
+    _lib.check(L.cox_decode_moe(x.data_ptr(), T, wg.data_ptr(), E, k, mode, _ptrs(w13), _ptrs(w2), d, ff, ptr(sw13),
+                                ptr(sw2), ffs, h.data_ptr(), y.data_ptr(), ptr(sh), ptr(sy), idx.data_ptr(),
+                                w.data_ptr(), out.data_ptr(), _stream(stream)), "cox_decode_moe")
+    return out
+
+
 def combine(y_perm: torch.Tensor, dst: torch.Tensor, w: torch.Tensor, shared: torch.Tensor | None = None,
             out: torch.Tensor | None = None, out_dtype=_BF16, stream=None):
     """K5: out[t] = sum_j w[t,j] y_perm[dst[t,j]] (+ shared[t])."""

@@ -97,7 +97,8 @@ def test_small_ffn_close_to_prefill_kernels():
 
 
 @pytest.mark.parametrize("T,d,ff,E,k,mode,shared_ff", [
-    (64, 2048, 1408, 64, 6, "deepseek", 2816),   # C4 decode step
+    (64, 2048, 1408, 64, 6, "deepseek", 2816),   # C4 decode step (routed path)
+    (32, 2048, 1408, 64, 6, "deepseek", 2816),   # C4, 32 sequences (dense single-launch path)
     (64, 4096, 14336, 8, 2, "mixtral", 0),       # Mixtral-8x7B decode step
     (200, 1024, 512, 16, 4, "deepseek", 256),
     (1, 256, 128, 8, 2, "mixtral", 0),
@@ -115,9 +116,34 @@ def test_decode_layer_vs_oracle(T, d, ff, E, k, mode, shared_ff):
     ref = O.moe_layer(f(x), f(wts.wg), f(wts.w1), f(wts.w3), f(wts.w2), k, 0 if mode == "mixtral" else 1,
                       shared=shared)
     assert np.array_equal(b.idx.cpu().numpy(), ref["idx"])
-    assert np.array_equal(b.dst.cpu().numpy(), ref["dst"])
+    np.testing.assert_allclose(b.w.cpu().numpy(), ref["w"], rtol=2e-6, atol=1e-7)
+    if not layer.uses_dense_decode(T):  # the dense decode launch has no permutation
+        assert np.array_equal(b.dst.cpu().numpy(), ref["dst"])
     err = rel_l2(f(out), ref["out"])
     assert err <= 1e-2, err
+
+
+@pytest.mark.parametrize("T,d,ff,E,k,mode,shared_ff", [
+    (32, 2048, 1408, 64, 6, "deepseek", 2816),
+    (17, 4096, 14336, 8, 2, "mixtral", 0),
+    (33, 1024, 512, 40, 4, "deepseek", 256),
+])
+def test_dense_decode_matches_routed_decode(T, d, ff, E, k, mode, shared_ff):
+    """cox_decode_moe (router in the launch, every expert over every token)
+    against the routed decode path (router + permute + weight-streaming FFN):
+    identical routing, outputs equal up to fp32 summation order."""
+    wts = make_layer_weights(E, d, ff, seed=5, device=DEV, shared_ff=shared_ff)
+    x = make_tokens(T, d, seed=6, device=DEV)
+    dense = MoELayer(wts, k, mode)
+    routed = MoELayer(wts, k, mode)
+    routed.DENSE_T_MAX = 0
+    assert dense.uses_dense_decode(T) and not routed.uses_dense_decode(T)
+    a = dense(x).clone()
+    bb = routed(x).clone()
+    torch.cuda.synchronize()
+    assert torch.equal(dense.buffers(T, DEV).idx, routed.buffers(T, DEV).idx)
+    assert torch.equal(dense.buffers(T, DEV).w, routed.buffers(T, DEV).w)
+    assert rel_l2(a.float().cpu(), bb.float().cpu()) < 4e-3
 
 
 def test_decode_graph_replay_matches_eager():
