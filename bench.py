@@ -280,7 +280,8 @@ def run_stack(args, cfg):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=None,
+                    help="timed steps (default per config: ~4-6 s of device time; C3 5, C4D 2000)")
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="C2", choices=sorted(CONFIGS))
@@ -295,6 +296,12 @@ def main():
     ap.add_argument("--proto-tokens", type=int, default=8192, help="C3 calibration batch size")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    if args.steps is None:
+        # enough steps that the end-to-end pipeline's fill (first H2D) and drain
+        # (last D2H) are a small share of the e2e number, within ~5 s per arm
+        args.steps = {"C3": 5, "C4D": 2000, "C1": 200}.get(args.config, 30)
+        if args.impl == "reference":
+            args.steps = 10
     cfg = CONFIGS[args.config]
     if args.impl == "reference":
         return run_reference(args, cfg)
