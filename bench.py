@@ -218,7 +218,7 @@ def run_stack(args, cfg):
     dev = torch.device("cuda", 0)
     torch.cuda.set_device(dev)
     model = ModelConfig(N, d, ff, E, k, 2)
-    pool = make_pool(args.pool, d, ff, seed=0, device=dev)
+    pool = make_pool(args.pool, d, ff, seed=0, device=dev, residual_scale=(2.0 * N) ** -0.5)
     wg = make_router_weights(N, E, d, seed=7, device=dev)
     stack = StratifiedMoEStack(N, wg, pool, k, ResidencyPlan(tuple(() for _ in range(N)), 0), mode)
     # calibration: prototype batches through the all-cold stack (prefill-only probing)

@@ -66,6 +66,7 @@ int oracle_router_topk(const float* x, const float* wg, int T, int d, int E, int
     for (long t = 0; t < T; ++t) {
         for (int e = 0; e < E; ++e) {
             lg[e] = oracle_router_logit(x + t * (long)d, wg + (long)e * d, d);
+            if (isnan(lg[e])) lg[e] = -INFINITY; /* NaN ranks below every number (GPU: nan_low) */
             if (logits_out) logits_out[t * E + e] = lg[e];
             taken[e] = 0;
         }

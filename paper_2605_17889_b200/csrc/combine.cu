@@ -52,8 +52,9 @@ __global__ void __launch_bounds__(256) combine_kernel(const __nv_bfloat16* __res
     float wj[K];
 #pragma unroll
     for (int j = 0; j < K; ++j) {
-      rows[j] = y + (long)dst[t * K + j] * d;
-      wj[j] = w[t * K + j];
+      const int r = dst[t * K + j];
+      rows[j] = y + (long)(r < 0 ? 0 : r) * d;   // dst < 0 (invalid expert id): no contribution
+      wj[j] = r < 0 ? 0.0f : w[t * K + j];
     }
     for (int c0 = lane * 8; c0 < d; c0 += 256 * CB_UNROLL) {
       uint4 v[CB_UNROLL][K];

@@ -27,7 +27,10 @@ __global__ void __launch_bounds__(PM_TB) perm_hist(const int32_t* __restrict__ i
   __syncthreads();
   long t = (long)blockIdx.x * PM_TB + threadIdx.x;
   if (t < T)
-    for (int j = 0; j < k; ++j) atomicAdd(&s_h[idx[t * k + j]], 1);
+    for (int j = 0; j < k; ++j) {
+      const int e = idx[t * k + j];
+      if ((unsigned)e < (unsigned)E) atomicAdd(&s_h[e], 1);  // invalid ids are dropped (dst = -1)
+    }
   __syncthreads();
   for (int i = threadIdx.x; i < E; i += blockDim.x) block_counts[(long)blockIdx.x * E + i] = s_h[i];
 }
@@ -81,6 +84,7 @@ __global__ void __launch_bounds__(PM_TB) perm_scatter(const int32_t* __restrict_
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
     ej[j] = (valid && j < k) ? idx[t * k + j] : -1;
+    if ((unsigned)ej[j] >= (unsigned)E) ej[j] = -1;
     rj[j] = 0;
   }
   const uint32_t lt = (1u << lane) - 1u;
@@ -110,7 +114,7 @@ __global__ void __launch_bounds__(PM_TB) perm_scatter(const int32_t* __restrict_
     dj[j] = (ej[j] >= 0) ? s_wbase[warp][ej[j]] + rj[j] : -1;
     if (j < k && valid) {
       dst[t * k + j] = dj[j];
-      if (row_tokens) row_tokens[dj[j]] = (int32_t)t;
+      if (row_tokens && dj[j] >= 0) row_tokens[dj[j]] = (int32_t)t;
     }
   }
 }
@@ -133,7 +137,10 @@ __global__ void __launch_bounds__(PS_THREADS) perm_small(const int32_t* __restri
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int e = threadIdx.x; e < E; e += PS_THREADS) s_cnt[e] = 0;
   __syncthreads();
-  for (long i = threadIdx.x; i < (long)T * k; i += PS_THREADS) atomicAdd(&s_cnt[idx[i]], 1);
+  for (long i = threadIdx.x; i < (long)T * k; i += PS_THREADS) {
+    const int e = idx[i];
+    if ((unsigned)e < (unsigned)E) atomicAdd(&s_cnt[e], 1);  // invalid ids are dropped (dst = -1)
+  }
   __syncthreads();
   if (warp == 0) {  // padded segment offsets: warp scan over E <= 256 (8 experts per lane)
     int loc[8], sum = 0;
@@ -172,6 +179,7 @@ __global__ void __launch_bounds__(PS_THREADS) perm_small(const int32_t* __restri
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
       ej[j] = (valid && j < k) ? idx[t * k + j] : -1;
+      if ((unsigned)ej[j] >= (unsigned)E) ej[j] = -1;
       rj[j] = 0;
     }
     const int nlive = min(PS_THREADS / 32, (T - c0 + 31) / 32);  // warps holding tokens of this chunk
@@ -202,9 +210,9 @@ __global__ void __launch_bounds__(PS_THREADS) perm_small(const int32_t* __restri
 #pragma unroll
     for (int j = 0; j < 8; ++j)
       if (j < k && valid) {
-        const int dj = s_wcnt[warp][ej[j]] + rj[j];
+        const int dj = ej[j] >= 0 ? s_wcnt[warp][ej[j]] + rj[j] : -1;
         dst[t * k + j] = dj;
-        if (row_tokens) row_tokens[dj] = (int32_t)t;
+        if (row_tokens && dj >= 0) row_tokens[dj] = (int32_t)t;
       }
     __syncthreads();
   }
@@ -235,7 +243,7 @@ __global__ void __launch_bounds__(256) perm_copy(const int32_t* __restrict__ dst
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           const int c = c0 + u * 256;
-          if (c < d) *reinterpret_cast<uint4*>(x_perm + (long)di[j] * d + c) = v[u];
+          if (c < d && di[j] >= 0) *reinterpret_cast<uint4*>(x_perm + (long)di[j] * d + c) = v[u];
         }
       }
     }

@@ -28,6 +28,11 @@
 
 namespace cox {
 
+// NaN logits (e.g. from overflowing inputs) rank below every number, like
+// -inf, so the top-k always returns valid, distinct expert ids (ties and
+// equal -inf -> lower index); the oracle applies the same rule.
+COX_DEV float nan_low(float v) { return v != v ? -INFINITY : v; }
+
 constexpr int RT_TPW = 4;    // tokens per warp tile
 constexpr int RT_EG = 8;     // experts per warp tile
 constexpr int RT_WARPS = 8;  // warps per block
@@ -130,7 +135,7 @@ router_topk_kernel(const XT* __restrict__ x, const WT* __restrict__ wg, int T, i
           float v = acc[t][e];
 #pragma unroll
           for (int off = 16; off >= 1; off >>= 1) v = __fadd_rn(v, __shfl_xor_sync(0xffffffffu, v, off));
-          if (lane == 0 && e0 + e < E) s_logits[(tg * TPW + t) * E + e0 + e] = v;
+          if (lane == 0 && e0 + e < E) s_logits[(tg * TPW + t) * E + e0 + e] = nan_low(v);
         }
     }
     __syncthreads();
@@ -282,7 +287,7 @@ router_topk_staged_kernel(const __nv_bfloat16* __restrict__ x, const float* __re
           float v = acc[t][e];
 #pragma unroll
           for (int off = 16; off >= 1; off >>= 1) v = __fadd_rn(v, __shfl_xor_sync(0xffffffffu, v, off));
-          if (lane == 0 && e0 + e < E) s_logits[(tl0 + t) * E + e0 + e] = v;
+          if (lane == 0 && e0 + e < E) s_logits[(tl0 + t) * E + e0 + e] = nan_low(v);
         }
     }
     __syncthreads();
@@ -432,7 +437,7 @@ router_topk_staged_bf16w_kernel(const __nv_bfloat16* __restrict__ x, const __nv_
           float v = acc[t][e];
 #pragma unroll
           for (int off = 16; off >= 1; off >>= 1) v = __fadd_rn(v, __shfl_xor_sync(0xffffffffu, v, off));
-          if (lane == 0 && e0 + e < E) s_logits[(tl0 + t) * E + e0 + e] = v;
+          if (lane == 0 && e0 + e < E) s_logits[(tl0 + t) * E + e0 + e] = nan_low(v);
         }
       __syncthreads();  // all warps done with buffer (g & 1) before it is refilled
     }

@@ -298,6 +298,7 @@ __global__ void __launch_bounds__(RR_WARPS * 32, NCH <= 8 ? 2 : 1) router_rescor
     for (int i = 0; i < NE; ++i) {
       const int e = lane + 32 * i;
       av[i] = e < E ? approx[t * E + e] : -INFINITY;
+      av[i] = av[i] != av[i] ? -INFINITY : av[i];  // NaN ranks like -inf (router.cu nan_low)
       if (e < E) lg[e] = av[i];
     }
     // k-th largest approx VALUE: k rounds of a value-only warp max; equal
@@ -366,7 +367,7 @@ __global__ void __launch_bounds__(RR_WARPS * 32, NCH <= 8 ? 2 : 1) router_rescor
         for (int u = 0; u < CG; ++u) a[u] = __fadd_rn(a[u], __shfl_xor_sync(0xffffffffu, a[u], off));
       if (lane == 0) {
 #pragma unroll
-        for (int u = 0; u < CG; ++u) lg[ec[u]] = a[u];
+        for (int u = 0; u < CG; ++u) lg[ec[u]] = a[u] != a[u] ? -INFINITY : a[u];
       }
     }
     __syncwarp();

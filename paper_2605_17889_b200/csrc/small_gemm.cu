@@ -499,7 +499,7 @@ __global__ void __launch_bounds__(SG_THREADS, 1) small_ffn_kernel(const __grid_c
             float v = acc[u];
 #pragma unroll
             for (int off = 16; off >= 1; off >>= 1) v = __fadd_rn(v, __shfl_xor_sync(0xffffffffu, v, off));
-            if (lane == 0 && e0 + u < E) s_route[e0 + u] = v;
+            if (lane == 0 && e0 + u < E) s_route[e0 + u] = v != v ? -INFINITY : v;  // NaN ranks like -inf
           }
         }
         __syncwarp();

@@ -290,15 +290,21 @@ class StratifiedMoEStack:
         return plan
 
 
-def make_pool(P: int, d: int, ff: int, seed: int = 0, device="cuda") -> HostExpertPool:
-    """P distinct random experts generated on the device, copied to pinned host memory."""
+def make_pool(P: int, d: int, ff: int, seed: int = 0, device="cuda", residual_scale: float = 1.0) -> HostExpertPool:
+    """P distinct random experts generated on the device, copied to pinned host memory.
+
+    residual_scale multiplies the down projections (GPT-2-style 1/sqrt(2 N)
+    init of residual branches): the stack has no normalisation between layers,
+    and with unit-scaled random experts reused every P/E layers the residual
+    stream of a deep stack grows geometrically (overflow after ~50 layers)."""
     g = torch.Generator(device=device)
     g.manual_seed(seed)
     w13 = torch.empty((P, 2 * ff, d), dtype=torch.bfloat16, device=device)
     w2 = torch.empty((P, d, ff), dtype=torch.bfloat16, device=device)
+    a2 = residual_scale * ff ** -0.5
     for p in range(P):
         w13[p].uniform_(-d ** -0.5, d ** -0.5, generator=g)
-        w2[p].uniform_(-ff ** -0.5, ff ** -0.5, generator=g)
+        w2[p].uniform_(-a2, a2, generator=g)
     pool = HostExpertPool.from_device(w13, w2)
     del w13, w2
     torch.cuda.empty_cache()

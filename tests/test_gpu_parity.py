@@ -401,6 +401,7 @@ def test_random_configs_vs_oracle(seed):
     ref = O.moe_layer(f(x), f(wts.wg), f(wts.w1), f(wts.w3), f(wts.w2), k, 0 if mode == "mixtral" else 1)
     b = layer.buffers(T, DEV)
     assert np.array_equal(b.idx.cpu().numpy(), ref["idx"])
-    assert np.array_equal(b.dst.cpu().numpy(), ref["dst"])
-    assert np.array_equal(b.offsets.cpu().numpy(), ref["offsets"])
+    if not layer.uses_dense_decode(T):  # the single-launch dense decode materialises no permutation
+        assert np.array_equal(b.dst.cpu().numpy(), ref["dst"])
+        assert np.array_equal(b.offsets.cpu().numpy(), ref["offsets"])
     assert rel_l2(f(out), ref["out"]) <= 1e-2
