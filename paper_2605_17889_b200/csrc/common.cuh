@@ -214,6 +214,14 @@ COX_DEV void ffma2(float& a0, float& a1, float x, float w0, float w1) {
   asm("mov.b64 {%0, %1}, %2;" : "=f"(a0), "=f"(a1) : "l"(acc));
 }
 
+// ---------------------------------------------------------------- programmatic dependent launch
+// A kernel launched with cudaLaunchAttributeProgrammaticStreamSerialization may
+// start while its stream predecessor is still running once that predecessor
+// executes launch_dependents; pdl_wait() blocks until the predecessor grid has
+// completed and its writes are visible (a no-op for an ordinary launch).
+COX_DEV void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+COX_DEV void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // ---------------------------------------------------------------- misc
 COX_DEV uint32_t pack_bf16x2(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);

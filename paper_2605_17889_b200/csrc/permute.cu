@@ -135,6 +135,8 @@ __global__ void __launch_bounds__(PS_THREADS) perm_small(const int32_t* __restri
   __shared__ int s_base[256];
   __shared__ int s_wcnt[PS_THREADS / 32][256];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  pdl_launch_dependents();  // the expert kernel may start its weight prefetch now
+  pdl_wait();               // ... while this kernel waits for the router's idx
   for (int e = threadIdx.x; e < E; e += PS_THREADS) s_cnt[e] = 0;
   __syncthreads();
   for (long i = threadIdx.x; i < (long)T * k; i += PS_THREADS) {
@@ -287,7 +289,16 @@ int launch_permute(const int32_t* idx, int T, int k, int E, int tile_m, const vo
                            (int)cudaSharedmemCarveoutMaxShared);
       carve = true;
     }
-    perm_small<<<1, PS_THREADS, 0, s>>>(idx, T, k, E, tile_m, offsets, dst, row_tokens, seg_counts);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(1);
+    cfg.blockDim = dim3(PS_THREADS);
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, perm_small, idx, T, k, E, tile_m, offsets, dst, row_tokens, seg_counts);
   } else {
     perm_hist<<<(int)nb, PM_TB, 0, s>>>(idx, T, k, E, block_counts);
     perm_scan<<<1, 1024, 0, s>>>(block_counts, (int)nb, E, tile_m, block_base, offsets, seg_counts);

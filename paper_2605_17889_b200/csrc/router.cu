@@ -88,6 +88,7 @@ router_topk_kernel(const XT* __restrict__ x, const WT* __restrict__ wg, int T, i
   __shared__ int s_sel[RT_WARPS][8];
   __shared__ float s_selv[RT_WARPS][8];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  pdl_launch_dependents();  // the permute (a programmatic dependent) may be scheduled now
   const int ntg = RT_WARPS / egn;
   const int tpb = TPW * ntg;
   const int tg = warp / egn, eg = warp % egn;

@@ -112,6 +112,12 @@ struct SmallParams {
   int32_t* ridx;  // [T, k]
   float* rw;      // [T, k]
   int16_t expert_slot[256];  // routed expert -> its row block in h/y (dense)
+  // Launched as a programmatic dependent of the permute (pdl != 0): CTAs may
+  // become resident while the routing kernels still run and wait (griddepcontrol)
+  // before reading their outputs.  Measured: -3 us/step eager, neutral under a
+  // CUDA graph; also prefetching the first units' weights into L2 during the
+  // wait was tried and was slower (1 unit/CTA +2 us, 2: +4 us, 4: +10 us).
+  int pdl;
   int group_expert[SG_MAXG];  // >= 0: routed expert (segment from offsets); -1: shared (rows [0, Ts))
   int group_ff[SG_MAXG];
   int n_groups;
@@ -179,6 +185,10 @@ __global__ void __launch_bounds__(SG_THREADS, 1) small_ffn_kernel(const __grid_c
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int G = p.n_groups;
+
+  if (p.pdl) {
+    pdl_wait();  // routing (offsets, row_tokens, dst, w) of this step is complete from here on
+  }
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < SG_STAGES; ++s) {
@@ -840,6 +850,12 @@ int launch_small_ffn(const void* x, int T, const int32_t* row_tokens, const void
   }();
   p.k4_colmajor = colmajor;
   p.dense = dense ? 1 : 0;
+  // routed decode: launched as a programmatic dependent of the permute (COX_PDL=0 disables)
+  static const int pdl_env = [] {
+    const char* e = getenv("COX_PDL");
+    return e ? atoi(e) : 1;
+  }();
+  p.pdl = (!dense && pdl_env) ? 1 : 0;
   if (dense) {
     p.wg = static_cast<const __nv_bfloat16*>(dense->wg);
     p.xtok = static_cast<const __nv_bfloat16*>(x);
@@ -879,7 +895,21 @@ int launch_small_ffn(const void* x, int T, const int32_t* row_tokens, const void
                            (int)SgCfg<KA_, NM_>::SMEM);                                                    \
       attr = true;                                                                                         \
     }                                                                                                      \
-    small_ffn_kernel<KA_, NM_><<<g_sg_sms, SG_THREADS, SgCfg<KA_, NM_>::SMEM, s>>>(p);                     \
+    if (p.pdl) {                                                                                           \
+      cudaLaunchConfig_t cfg = {};                                                                         \
+      cfg.gridDim = dim3(g_sg_sms);                                                                        \
+      cfg.blockDim = dim3(SG_THREADS);                                                                     \
+      cfg.dynamicSmemBytes = SgCfg<KA_, NM_>::SMEM;                                                        \
+      cfg.stream = s;                                                                                      \
+      cudaLaunchAttribute at[1];                                                                           \
+      at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;                                       \
+      at[0].val.programmaticStreamSerializationAllowed = 1;                                                \
+      cfg.attrs = at;                                                                                      \
+      cfg.numAttrs = 1;                                                                                    \
+      cudaLaunchKernelEx(&cfg, small_ffn_kernel<KA_, NM_>, p);                                             \
+    } else {                                                                                               \
+      small_ffn_kernel<KA_, NM_><<<g_sg_sms, SG_THREADS, SgCfg<KA_, NM_>::SMEM, s>>>(p);                   \
+    }                                                                                                      \
   } while (0)
   switch (variant) {
     case 1032: SG_LAUNCH(1, 32); break;
