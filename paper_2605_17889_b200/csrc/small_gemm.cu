@@ -27,9 +27,20 @@
 // counter, so a waiting unit only ever waits on units already running.
 //
 // The shared experts of DeepSeek-style layers (dense MLP over all tokens) are
-// one more group (expert id -1, rows [0, Ts) of x), in the same launch.
-// Segments longer than 64 rows are processed in 64-row chunks (the weight tile
-// is then re-read from L2).
+// one more group (expert id -1, rows [0, Ts) of x), placed first.  Segments
+// longer than 64 rows are processed in 64-row chunks (the weight tile is then
+// re-read from L2).  Routed rows are gathered from x by TMA tile::gather4
+// (row_tokens) or read from a materialised x_perm.  The CTA that stores the
+// last down tile of a 128-column block combines that block for every token
+// (same operation order as combine_kernel).
+//
+// Dense mode (cox_decode_moe): every group runs over all T <= 64 tokens and
+// warp 2 routes token blockIdx.x in the canonical order, so the router is off
+// the critical path; only the combine waits for it.  Routed mode is launched
+// as a programmatic dependent of the permute (griddepcontrol).
+//
+// Host side: tensor maps in a content-keyed global table (not 17 KB of kernel
+// parameters), counters reset by the last CTA to exit (no memset node).
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
