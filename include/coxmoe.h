@@ -155,6 +155,19 @@ int cox_small_expert_ffn(const void* x, int T, const int32_t* row_tokens, const 
                          const void* w2_shared, int ff_shared, void* h_shared, void* y_shared, const int32_t* dst,
                          const float* w, int k, void* out, void* stream);
 
+/* Same decode-size expert stage straight from the router's output (no
+ * permute launch): segments from counts[E] (expert-ascending, written to
+ * offsets [E+1] if non-NULL), each routed SwiGLU tile collects its expert's
+ * tokens from idx [T, k] and gathers their rows from x, the combine rows are
+ * written to dst [T, k] (same order as cox_permute).  Experts 0..E-1 are the
+ * groups; h [T*k, ff], y_perm [T*k, d]; out [T, d] bf16 (fused combine).
+ * T <= 256, E <= 64, d % 128 == 0, ff % 128 == 0. */
+int cox_small_expert_ffn_idx(const void* x, int T, const int32_t* idx, const int32_t* counts, int E,
+                             const float* w, int k, const void* const* w13, const void* const* w2, int d, int ff,
+                             void* h, void* y_perm, const void* w13_shared, const void* w2_shared, int ff_shared,
+                             void* h_shared, void* y_shared, int32_t* dst, int32_t* offsets, void* out,
+                             void* stream);
+
 /* The whole MoE layer for a decode step (T <= 64 tokens, E <= 64 experts) in
  * ONE launch: router (bf16 wg, canonical order: idx bit-exact with
  * cox_router_topk), SwiGLU + down projection of EVERY expert over all T tokens

@@ -23,11 +23,19 @@ struct SmallDense {
   int32_t* idx;
   float* w;
 };
+struct SmallIdx {
+  const int32_t* idx;
+  const int32_t* counts;
+  int E;
+  int32_t* dst_out;
+  int32_t* offsets_out;
+};
 int launch_small_ffn(const void* x, int T, const int32_t* row_tokens, const void* act, long long rows_cap,
                      const int32_t* offsets, int n_groups, const int32_t* group_expert, const void* const* w13,
                      const void* const* w2, int d, int ff, void* h, void* y, const void* w13s, const void* w2s,
                      int ffs, void* hs, void* ys, const int32_t* cdst, const float* cw, int k, void* out,
-                     int phases, cudaStream_t s, const SmallDense* dense = nullptr);
+                     int phases, cudaStream_t s, const SmallDense* dense = nullptr,
+                     const SmallIdx* fromidx = nullptr);
 int launch_combine(const void* y_perm, const int32_t* dst, const float* w, int T, int k, int d, const void* shared,
                    void* out, int out_is_bf16, cudaStream_t s);
 
@@ -228,6 +236,32 @@ int cox_small_expert_ffn(const void* x, int T, const int32_t* row_tokens, const 
   int rc = cox::launch_small_ffn(x, T, row_tokens, x_perm, rows_cap, offsets, n_groups, group_experts, w13, w2, d, ff,
                                  h, y_perm, w13_shared, w2_shared, ff_shared, h_shared, y_shared, dst, w, k, out, 3,
                                  static_cast<cudaStream_t>(stream));
+  return cuda_status(rc, fn);
+}
+
+int cox_small_expert_ffn_idx(const void* x, int T, const int32_t* idx, const int32_t* counts, int E,
+                             const float* w, int k, const void* const* w13, const void* const* w2, int d, int ff,
+                             void* h, void* y_perm, const void* w13_shared, const void* w2_shared, int ff_shared,
+                             void* h_shared, void* y_shared, int32_t* dst, int32_t* offsets, void* out,
+                             void* stream) {
+  const char* fn = "cox_small_expert_ffn_idx";
+  if (T < 1 || T > 256) return fail(COX_EINVAL, "%s: need 1 <= T <= 256 (T=%d)", fn, T);
+  if (E < 1 || E > 64 || k < 1 || k > 8 || k > E) return fail(COX_EINVAL, "%s: need 1 <= k <= min(E, 8), E <= 64", fn);
+  if (d <= 0 || d % 128 || ff <= 0 || ff % 128) return fail(COX_EINVAL, "%s: need d %% 128 == 0, ff %% 128 == 0", fn);
+  if (!x || !idx || !counts || !w || !h || !y_perm || !dst || !out || !aligned16(x) || !aligned16(h) ||
+      !aligned16(y_perm) || !aligned16(out))
+    return fail(COX_EINVAL, "%s: null or unaligned operand", fn);
+  if (w13_shared && (ff_shared <= 0 || ff_shared % 128 || !w2_shared || !h_shared || !y_shared ||
+                     !aligned16(h_shared) || !aligned16(y_shared)))
+    return fail(COX_EINVAL, "%s: bad shared-expert operands", fn);
+  int32_t ids[64];
+  for (int e = 0; e < E; ++e) ids[e] = e;
+  if (int rc = check_groups(fn, E, ids, w13)) return rc;
+  if (int rc = check_groups(fn, E, ids, w2)) return rc;
+  cox::SmallIdx fi{idx, counts, E, dst, offsets};
+  int rc = cox::launch_small_ffn(x, T, nullptr, nullptr, (long long)T * k, nullptr, E, ids, w13, w2, d, ff, h,
+                                 y_perm, w13_shared, w2_shared, ff_shared, h_shared, y_shared, dst, w, k, out, 3,
+                                 static_cast<cudaStream_t>(stream), nullptr, &fi);
   return cuda_status(rc, fn);
 }
 

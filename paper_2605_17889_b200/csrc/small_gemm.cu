@@ -67,6 +67,7 @@ constexpr int SG_THREADS = 256;
 constexpr int SG_DEPTH = 4;    // unit-id ring between the scheduler and the roles
 constexpr uint32_t SG_A_ATOM = SG_BM * SG_ATOM * 2;  // 16 KB: one K atom of the weight tile
 constexpr int SG_PITCH = 33;                         // fp32 staging row pitch (conflict-free)
+constexpr int SG_MAX_PAIRS = 2048;                   // T*k of the from_idx path (T <= 256, k <= 8)
 
 // KA = K atoms per pipeline stage (BK = 64 KA: contiguous bytes per weight row
 // per stage), NMAX = tokens per MMA chunk (MMA N <= NMAX).
@@ -79,7 +80,8 @@ struct SgCfg {
   static constexpr int STAGES = (int)(SG_RING_BYTES / (A_STAGE + B_STAGE)) > 12 ? 12
                                                                                : (int)(SG_RING_BYTES / (A_STAGE + B_STAGE));
   static constexpr uint32_t TMEM_COLS = 2 * NMAX < 64 ? 64 : 2 * NMAX;
-  static constexpr size_t SMEM = 1024 + STAGES * (A_STAGE + B_STAGE) + 512 + 1024 + 24 * (SG_MAXG + 2) +
+  static constexpr size_t SMEM = 1024 + STAGES * (A_STAGE + B_STAGE) + 512 + 1040 + 4 * SG_MAX_PAIRS + 1024 + 32 +
+                                 24 * (SG_MAXG + 2) +
                                  4 * SG_BM * SG_PITCH + 64;
 };
 
@@ -129,6 +131,16 @@ struct SmallParams {
   // CUDA graph; also prefetching the first units' weights into L2 during the
   // wait was tried and was slower (1 unit/CTA +2 us, 2: +4 us, 4: +10 us).
   int pdl;
+  // from_idx != 0: no permute kernel ran.  Segments come from the router's
+  // counts (expert-ascending offsets, written to offsets_out by CTA 0), the
+  // producer of a routed SwiGLU unit collects its expert's tokens from ridx
+  // (ascending token order, like the permute) and gathers their rows from x,
+  // and the producer of unit 0 of each group writes the group's dst entries
+  // for the combine.
+  int from_idx;
+  const int32_t* rcounts;  // [E]
+  int32_t* dst_out;        // [T, k]
+  int32_t* offsets_out;    // [E + 1]
   int group_expert[SG_MAXG];  // >= 0: routed expert (segment from offsets); -1: shared (rows [0, Ts))
   int group_ff[SG_MAXG];
   int n_groups;
@@ -190,8 +202,16 @@ __global__ void __launch_bounds__(SG_THREADS, 1) small_ffn_kernel(const __grid_c
   int* s_p4 = s_p3 + SG_MAXG + 1;    // [G+1] prefix of down units
   int* s_misc = s_p4 + SG_MAXG + 1;  // [0] groups with rows, [1] combine flag
   int* s_act = s_misc + 4;            // [G] active groups (rows > 0), in group order
-  float* s_route = reinterpret_cast<float*>(s_act + SG_MAXG);  // [256] dense: logits of the token being routed
-  float* stg = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(s_route + 256) + 15) & ~uintptr_t(15));
+  float* s_route = reinterpret_cast<float*>(s_act + SG_MAXG);  // [260] dense: logits of the token being routed;
+  int* s_eoff = reinterpret_cast<int*>(s_route);                 //   from_idx: expert offsets [E + 1]
+  // from_idx: the stable permutation, computed once per CTA by warp 2:
+  // s_perm[row] = token of permuted row (expert-major, ascending tokens),
+  // s_pos[t*k + j] = permuted row of (t, j)
+  int16_t* s_perm = reinterpret_cast<int16_t*>(s_route + 260);   // [SG_MAX_PAIRS]
+  int16_t* s_pos = s_perm + SG_MAX_PAIRS;                         // [SG_MAX_PAIRS]
+  int* s_erun = reinterpret_cast<int*>(s_pos + SG_MAX_PAIRS);     // [256] running row per expert
+  uint64_t* perm_ready = reinterpret_cast<uint64_t*>(s_erun + 256);
+  float* stg = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(perm_ready + 1) + 15) & ~uintptr_t(15));
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -214,9 +234,37 @@ __global__ void __launch_bounds__(SG_THREADS, 1) small_ffn_kernel(const __grid_c
       mbar_init(smem_u32(&sfull[i]), 1);
       mbar_init(smem_u32(&sempty[i]), 6);  // producer + MMA + 4 epilogue warps
     }
+    mbar_init(smem_u32(perm_ready), 1);
     fence_mbar_init();
   }
   if (warp == 0) {
+    if (p.from_idx) {
+      // expert offsets from the router's counts (exclusive scan, 8 experts per lane)
+      int loc[8], sum = 0;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int e = lane * 8 + q;
+        loc[q] = e < p.E ? p.rcounts[e] : 0;
+        sum += loc[q];
+      }
+      int incl = sum;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += v;
+      }
+      int run = incl - sum;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int e = lane * 8 + q;
+        if (e <= p.E) {
+          s_eoff[e] = run;
+          if (blockIdx.x == 0 && p.offsets_out) p.offsets_out[e] = run;
+        }
+        run += loc[q];
+      }
+      __syncwarp();
+    }
     // group table: rows / first row per group and the unit prefix sums, one
     // group per lane (a serial loop would pay one L2 round trip per group)
     int c3 = 0, c4 = 0, nact = 0;
@@ -228,6 +276,9 @@ __global__ void __launch_bounds__(SG_THREADS, 1) small_ffn_kernel(const __grid_c
         if (p.dense) {
           rows = p.T;
           r0 = e >= 0 ? p.expert_slot[e] * p.T : 0;
+        } else if (p.from_idx) {
+          r0 = e >= 0 ? s_eoff[e] : 0;
+          rows = e >= 0 ? s_eoff[e + 1] - r0 : p.Ts;
         } else {
           r0 = e >= 0 ? p.offsets[e] : 0;
           rows = e >= 0 ? p.offsets[e + 1] - r0 : p.Ts;
@@ -328,6 +379,7 @@ __global__ void __launch_bounds__(SG_THREADS, 1) small_ffn_kernel(const __grid_c
     // lanes 0..4nb-1 each issue one tile::gather4 (4 token rows of x) per atom.
     uint32_t stage = 0, phase = 0;
     int si = 0;
+    bool perm_seen = false;
     for (;;) {
       int t = lane == 0 ? fetch(si, true) : 0;
       t = __shfl_sync(0xffffffffu, t, 0);
@@ -336,7 +388,11 @@ __global__ void __launch_bounds__(SG_THREADS, 1) small_ffn_kernel(const __grid_c
       decode(t, pass, g, i);
       const int rows = s_rows[g], row0 = s_row0[g];
       const int src = p.group_expert[g] < 0 ? 1 : 0;
-      const bool gat = pass == 0 && src == 0 && p.row_tokens != nullptr && !p.dense;
+      const bool gat = pass == 0 && src == 0 && !p.dense && (p.row_tokens != nullptr || p.from_idx);
+      if (gat && p.from_idx && !perm_seen) {
+        mbar_wait(smem_u32(perm_ready), 0);  // warp 2 has built this CTA's copy of the permutation
+        perm_seen = true;
+      }
       const CUtensorMap* wmap = pass == 0 ? &p.maps->w13[g] : &p.maps->w2[g];
       const CUtensorMap* amap = pass == 0 ? &p.maps->act3[p.dense ? 1 : src] : &p.maps->act4[src];
       const int brow0 = (pass == 0 && p.dense) ? 0 : row0;  // dense SwiGLU: B = x rows [0, T)
@@ -349,7 +405,13 @@ __global__ void __launch_bounds__(SG_THREADS, 1) small_ffn_kernel(const __grid_c
       for (int c0 = 0; c0 < rows; c0 += SG_NMAX) {
         const int nb = (min(SG_NMAX, rows - c0) + 15) >> 4;  // 16-row B boxes
         int rr[4] = {0, 0, 0, 0};
-        if (gat) {
+        if (gat && p.from_idx) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int r = c0 + 4 * lane + q;
+            rr[q] = (lane < 4 * nb && r < rows) ? (int)s_perm[row0 + r] : 0;
+          }
+        } else if (gat) {
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
             const long long r = (long long)row0 + c0 + 4 * lane + q;
@@ -487,6 +549,34 @@ __global__ void __launch_bounds__(SG_THREADS, 1) small_ffn_kernel(const __grid_c
     }
     __syncwarp();
   } else if (warp == 2) {
+    if (p.from_idx) {
+      // ---------------------------------------------------------- stable permutation (from_idx)
+      // Entries in (t, j) order, 32 at a time: rank among earlier entries of
+      // the same expert = running count + peers before me in this chunk
+      // (match_any), so rows are expert-major with ascending tokens -- the
+      // order of permute.cu / the oracle.  Every CTA keeps its own copy; CTA 0
+      // also publishes dst for the caller.
+      for (int e = lane; e < p.E; e += 32) s_erun[e] = s_eoff[e];
+      __syncwarp();
+      const int nent = p.T * p.k;
+      for (int c = 0; c < nent; c += 32) {
+        const int ent = c + lane;
+        const int e = ent < nent ? p.ridx[ent] : -1;
+        const uint32_t peers = __match_any_sync(0xffffffffu, e);
+        const int before = __popc(peers & ((1u << lane) - 1u));
+        int row = -1;
+        if (e >= 0 && e < p.E) row = s_erun[e] + before;
+        __syncwarp();
+        if (e >= 0 && e < p.E && before == 0) s_erun[e] += __popc(peers);
+        if (ent < nent) {
+          s_pos[ent] = (int16_t)row;
+          if (row >= 0) s_perm[row] = (int16_t)(ent / p.k);
+          if (blockIdx.x == 0) p.dst_out[ent] = row;
+        }
+        __syncwarp();
+      }
+      if (lane == 0) mbar_arrive(smem_u32(perm_ready));  // release: the arrays are visible to waiters
+    }
     // ------------------------------------------------------------ dense decode: in-kernel router
     // Token t = blockIdx.x (+ gridDim.x ...): logits in the canonical order of
     // router_topk_kernel (lane chunks s = 8 lane + 256 j, fma ascending, xor
@@ -662,12 +752,16 @@ __global__ void __launch_bounds__(SG_THREADS, 1) small_ffn_kernel(const __grid_c
           int* s_dst = reinterpret_cast<int*>(stg);
           float* s_w = reinterpret_cast<float*>(stg) + T * kk;
           if (p.dense && tid == 0) mbar_spin_ge(p.counters + SG_ROUTED, T);  // routing of every token done
+          if (p.from_idx) mbar_wait(smem_u32(perm_ready), 0);              // this CTA's permutation is built
           named_bar_epi();
           __threadfence();
           for (int e = tid; e < T * kk; e += 128) {
             if (p.dense) {
               s_dst[e] = p.expert_slot[p.ridx[e]] * T + e / kk;
               s_w[e] = p.rw[e];
+            } else if (p.from_idx) {
+              s_dst[e] = s_pos[e];  // this CTA's copy of the permutation (perm_ready long passed)
+              s_w[e] = p.cw[e];
             } else {
               s_dst[e] = p.cdst[e];
               s_w[e] = p.cw[e];
@@ -793,11 +887,20 @@ struct SmallDense {  // in-kernel routing (dense decode), see SmallParams::dense
   float* w;
 };
 
+struct SmallIdx {  // segments straight from the router (see SmallParams::from_idx)
+  const int32_t* idx;
+  const int32_t* counts;
+  int E;
+  int32_t* dst_out;
+  int32_t* offsets_out;
+};
+
 int launch_small_ffn(const void* x, int T, const int32_t* row_tokens, const void* act, long long rows_cap,
                      const int32_t* offsets, int n_groups, const int32_t* group_expert, const void* const* w13,
                      const void* const* w2, int d, int ff, void* h, void* y, const void* w13s, const void* w2s,
                      int ffs, void* hs, void* ys, const int32_t* cdst, const float* cw, int k, void* out,
-                     int phases, cudaStream_t s, const SmallDense* dense = nullptr) {
+                     int phases, cudaStream_t s, const SmallDense* dense = nullptr,
+                     const SmallIdx* fromidx = nullptr) {
   const bool shared = w13s != nullptr && T > 0;
   const int G = n_groups + (shared ? 1 : 0);
   if (G == 0) return 0;
@@ -861,6 +964,16 @@ int launch_small_ffn(const void* x, int T, const int32_t* row_tokens, const void
   }();
   p.k4_colmajor = colmajor;
   p.dense = dense ? 1 : 0;
+  p.from_idx = fromidx ? 1 : 0;
+  if (fromidx) {
+    p.ridx = const_cast<int32_t*>(fromidx->idx);
+    p.rcounts = fromidx->counts;
+    p.E = fromidx->E;
+    p.dst_out = fromidx->dst_out;
+    p.offsets_out = fromidx->offsets_out;
+    p.cdst = fromidx->dst_out;
+    p.row_tokens = nullptr;
+  }
   // routed decode: launched as a programmatic dependent of the permute (COX_PDL=0 disables)
   static const int pdl_env = [] {
     const char* e = getenv("COX_PDL");

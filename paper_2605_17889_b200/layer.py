@@ -105,6 +105,8 @@ class MoELayer:
         perm = (1 if small_perm else 3) + 1 + (1 if self.tile_m > 1 else 0)
         if T is not None and self.uses_dense_decode(T):
             return 1  # router + all experts + shared + combine in one launch
+        if T is not None and self.uses_idx_decode(T):
+            return 2  # router, then one launch for K3/K4/shared/combine reading the router's idx
         if T is not None and self.uses_small_path(T):
             # router + single-CTA permute (indices only) + one launch for K3/K4/shared/combine
             return 1 + 1 + 1 + (1 if self.out_dtype != torch.bfloat16 else 0)
@@ -224,8 +226,8 @@ class MoELayer:
     # experts + combine in ONE launch (cox_decode_moe).  It streams EVERY
     # expert, so it only pays when nearly all are touched anyway, and its token
     # tiles grow with T: measured on C4 (tools/sweep_decode.py, us/step, dense
-    # vs routed): T=8 184/139, 16 186/179, 24 191/206, 32 192/212, 48 203/218,
-    # 64 227/221.  Used when T <= DENSE_T_MAX and P(expert untouched) =
+    # vs routed): T=8 130/130, 16 171/171, 24 192/198, 32 193/204, 48 204/211,
+    # 64 213/212.  Used when T <= DENSE_T_MAX and P(expert untouched) =
     # (1 - k/E)^T <= 0.1; COX_DECODE_DENSE=0 disables.
     DENSE_T_MAX = 48 if os.environ.get("COX_DECODE_DENSE", "1") == "1" else 0
 
@@ -244,8 +246,25 @@ class MoELayer:
             shared = (self.wts.shared_w13, self.wts.shared_w2, b.shared_h, b.shared_y) if self.shared_ff else None
             return ops.decode_moe(x, self.wg_router, self.k, self.mode, self.w13_list, self.w2_list, dh, dy,
                                   b.idx, b.w, out, shared)
+        if self.uses_idx_decode(T, out):
+            ops.router_topk(x, self.wg_router, self.k, self.mode, out=(b.idx, b.w, b.counts))
+            return self._ffn_idx(x, b, out)
         self._route_small(x, b)
         return self._ffn_small(x, b, out)
+
+    # routed decode without a permute launch: the expert kernel reads the
+    # router's idx/counts directly (COX_SMALL_FROM_IDX=0: router + permute + FFN)
+    SMALL_FROM_IDX = os.environ.get("COX_SMALL_FROM_IDX", "1") == "1"
+
+    def uses_idx_decode(self, T: int, out: torch.Tensor | None = None) -> bool:
+        return (self.SMALL_FROM_IDX and self.uses_small_path(T) and self.tile_m == 1 and self.SMALL_FUSE
+                and self.SMALL_GATHER and (out is None or out.dtype == torch.bfloat16)
+                and self.out_dtype == torch.bfloat16)
+
+    def _ffn_idx(self, x: torch.Tensor, b: StageBuffers, out: torch.Tensor):
+        shared = (self.wts.shared_w13, self.wts.shared_w2, b.shared_h, b.shared_y) if self.shared_ff else None
+        return ops.small_expert_ffn_idx(x, b.idx, b.counts, b.w, self.w13_list, self.w2_list, b.h, b.y, b.dst, out,
+                                        offsets=b.offsets, shared=shared)
 
     def _dense_scratch(self, T: int, dev):
         sc = getattr(self, "_dense", None)
@@ -359,6 +378,11 @@ class MoELayer:
         ev[0].record()
         ops.router_topk(x, self.wg_router, self.k, self.mode, out=(b.idx, b.w, b.counts))
         ev[1].record()
+        if self.uses_idx_decode(x.shape[0]):
+            self._ffn_idx(x, b, b.out)
+            ev[2].record()
+            torch.cuda.synchronize()
+            return {"router": ev[0].elapsed_time(ev[1]), "expert_ffn_from_idx_shared_combine": ev[1].elapsed_time(ev[2])}
         if self.uses_small_path(x.shape[0]):
             ops.permute(b.idx, x, self.E, self.tile_m, out=(b.offsets, b.dst, None), workspace=b.workspace,
                         copy_rows=False, row_tokens=b.row_tokens)

@@ -249,6 +249,42 @@ def small_expert_ffn(x: torch.Tensor, offsets: torch.Tensor, group_experts: Sequ
     return out if out is not None else y
 
 
+def small_expert_ffn_idx(x: torch.Tensor, idx: torch.Tensor, counts: torch.Tensor, w: torch.Tensor,
+                         w13: Sequence[torch.Tensor], w2: Sequence[torch.Tensor], h: torch.Tensor, y: torch.Tensor,
+                         dst: torch.Tensor, out: torch.Tensor, offsets: torch.Tensor | None = None, shared=None,
+                         stream=None):
+    """Decode-size expert stage straight from the router output (no permute
+    launch); writes dst (and offsets) like ops.permute, out = combined result.
+    shared = (w13_shared, w2_shared, h_shared, y_shared)."""
+    _need(x, "x", _BF16, 2)
+    _need(idx, "idx", torch.int32, 2)
+    _need(counts, "counts", torch.int32, 1)
+    _need(w, "w", torch.float32, 2)
+    _need(dst, "dst", torch.int32, 2)
+    for t, n in ((h, "h"), (y, "y"), (out, "out")):
+        _need(t, n, _BF16, 2)
+    T, d = x.shape
+    k = idx.shape[1]
+    E = counts.shape[0]
+    ff = h.shape[1]
+    if (tuple(idx.shape) != (T, k) or tuple(w.shape) != (T, k) or tuple(dst.shape) != (T, k)
+            or h.shape[0] < T * k or y.shape[0] < T * k or y.shape[1] != d or tuple(out.shape) != (T, d)
+            or len(w13) != E or len(w2) != E):
+        raise ValueError("small_expert_ffn_idx: inconsistent shapes")
+    sw13 = sw2 = sh = sy = None
+    ffs = 0
+    if shared is not None:
+        sw13, sw2, sh, sy = shared
+        ffs = sh.shape[1]
+    ptr = lambda t: t.data_ptr() if t is not None else None  # noqa: E731
+    L = _lib.lib()
+    _lib.check(L.cox_small_expert_ffn_idx(
+        x.data_ptr(), T, idx.data_ptr(), counts.data_ptr(), E, w.data_ptr(), k, _ptrs(w13), _ptrs(w2), d, ff,
+        h.data_ptr(), y.data_ptr(), ptr(sw13), ptr(sw2), ffs, ptr(sh), ptr(sy), dst.data_ptr(), ptr(offsets),
+        out.data_ptr(), _stream(stream)), "cox_small_expert_ffn_idx")
+    return out
+
+
 def decode_moe(x: torch.Tensor, wg: torch.Tensor, k: int, mode: int, w13: Sequence[torch.Tensor],
                w2: Sequence[torch.Tensor], h: torch.Tensor, y: torch.Tensor, idx: torch.Tensor, w: torch.Tensor,
                out: torch.Tensor, shared=None, stream=None):

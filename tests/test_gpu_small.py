@@ -195,3 +195,29 @@ def test_gather_rows_and_fused_combine_match_separate_kernels(T, E, k, d, ff, sh
     torch.cuda.synchronize()
     assert torch.equal(h1, h2) and torch.equal(y1, y2)
     assert torch.equal(out1, out2)
+
+
+@pytest.mark.parametrize("T,d,ff,E,k,mode,shared_ff", [
+    (64, 2048, 1408, 64, 6, "deepseek", 2816),
+    (200, 1024, 512, 16, 4, "deepseek", 256),
+    (5, 512, 256, 8, 2, "mixtral", 0),
+])
+def test_decode_from_idx_matches_permute_path(T, d, ff, E, k, mode, shared_ff):
+    """The expert launch that reads the router's idx/counts directly (no permute
+    kernel) produces the permute's offsets and dst and the same output bits as
+    router + permute + gathered-row launch."""
+    wts = make_layer_weights(E, d, ff, seed=9, device=DEV, shared_ff=shared_ff)
+    x = make_tokens(T, d, seed=10, device=DEV)
+    a_l = MoELayer(wts, k, mode)
+    b_l = MoELayer(wts, k, mode)
+    b_l.SMALL_FROM_IDX = False
+    a_l.DENSE_T_MAX = b_l.DENSE_T_MAX = 0
+    assert a_l.uses_idx_decode(T) and not b_l.uses_idx_decode(T)
+    a = a_l(x).clone()
+    bo = b_l(x).clone()
+    torch.cuda.synchronize()
+    ba, bb = a_l.buffers(T, DEV), b_l.buffers(T, DEV)
+    assert torch.equal(ba.idx, bb.idx)
+    assert torch.equal(ba.offsets, bb.offsets)
+    assert torch.equal(ba.dst, bb.dst)
+    assert torch.equal(a, bo)

@@ -23,7 +23,7 @@ def test_decode_path_selection(c4_layer):
     assert L.uses_dense_decode(24) and L.uses_dense_decode(48)
     assert not L.uses_dense_decode(64)      # measured slower than the routed path
     assert L.launches_per_step(32) == 1
-    assert L.launches_per_step(64) == 3     # router, 1-CTA permute, FFN + combine
+    assert L.launches_per_step(64) == 2     # router, then FFN + combine straight from the router's idx
     assert L.launches_per_step(262144) == 1 + 3 + 1 + 2 + 1 + 2
 
 
