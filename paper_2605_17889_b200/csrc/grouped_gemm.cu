@@ -142,17 +142,32 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GM_THREADS, 1)
       mbar_init(smem_u32(&sempty[i]), 11);  // producers x2 + MMA + epilogue warps x8
     }
     fence_mbar_init();
+  }
+  if (warp == 1) {
+    // group table, one group per lane (a serial loop pays one L2 round trip per
+    // group: ~20 us at 64 groups)
     int acc = 0;
-    for (int g = 0; g < p.n_groups; ++g) {
-      const int e = p.group_expert[g];
-      const int r0 = p.offsets[e];
-      const int rows = p.offsets[e + 1] - r0;
-      s_row0[g] = r0;
-      s_rows[g] = rows;
-      s_prefix[g] = acc;
-      acc += ((rows + 2 * GM_BM - 1) / (2 * GM_BM)) * p.n_tiles;
+    for (int base = 0; base < p.n_groups; base += 32) {
+      const int g = base + lane;
+      int tiles = 0;
+      if (g < p.n_groups) {
+        const int e = p.group_expert[g];
+        const int r0 = p.offsets[e];
+        const int rows = p.offsets[e + 1] - r0;
+        s_row0[g] = r0;
+        s_rows[g] = rows;
+        tiles = ((rows + 2 * GM_BM - 1) / (2 * GM_BM)) * p.n_tiles;
+      }
+      int incl = tiles;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += v;
+      }
+      if (g < p.n_groups) s_prefix[g] = acc + incl - tiles;
+      acc += __shfl_sync(0xffffffffu, incl, 31);
     }
-    s_prefix[p.n_groups] = acc;
+    if (lane == 0) s_prefix[p.n_groups] = acc;
   }
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&p.a_map);
