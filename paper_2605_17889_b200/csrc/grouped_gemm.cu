@@ -98,23 +98,35 @@ COX_DEV float silu_f(float g) { return g * __frcp_rn(1.0f + __expf(-g)); }
 // KA = 128-byte swizzle atoms of K per pipeline stage: 1 -> BK 64, 6 stages;
 // 2 -> BK 128, 3 stages (same smem; 256 contiguous bytes per weight row per
 // stage, i.e. better DRAM page locality for weight-streaming shapes).
-template <int EPI, int KA>
+// STG: epilogue stores coalesced through a 16 KB smem staging tile (default);
+// without it the ring gets a 7th 32 KB stage (KA = 1): more operand bytes in
+// flight for feed-bound shapes.
+template <int KA, bool STG>
+struct GmRing {
+  static constexpr int STAGES = STG ? GM_STAGES / KA : (KA == 1 ? 7 : 3);
+  static constexpr int ATOMS = STAGES * KA;  // ring size in 16 KB (A) / 16 KB (B) atoms
+  static constexpr size_t SMEM = 1024 + (size_t)ATOMS * (GM_A_BYTES + GM_B_BYTES) + 512 + 4 * (3 * GM_MAXG + 4) + 16 +
+                                 (STG ? 4 * 32 * 128 : 0);
+};
+
+template <int EPI, int KA, bool STG>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GM_THREADS, 1)
     grouped_gemm_kernel(const __grid_constant__ GemmParams p) {
   constexpr int BK = GM_BK * KA;
-  constexpr int STAGES = GM_STAGES / KA;
+  constexpr int STAGES = GmRing<KA, STG>::STAGES;
+  constexpr int NB = GmRing<KA, STG>::ATOMS;  // barrier array length (>= STAGES)
   constexpr uint32_t A_STAGE = GM_A_BYTES * KA;
   constexpr uint32_t B_STAGE = GM_B_BYTES * KA;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
-  uint8_t* sB = smem + GM_STAGES * GM_A_BYTES;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sB + GM_STAGES * GM_B_BYTES);
+  uint8_t* sB = smem + NB * GM_A_BYTES;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sB + NB * GM_B_BYTES);
   uint64_t* full = bars;
-  uint64_t* empty = bars + GM_STAGES;  // barrier arrays sized for the max stage count
-  uint64_t* tfull = bars + 2 * GM_STAGES;
-  uint64_t* tempty = bars + 2 * GM_STAGES + 2;
-  uint64_t* sfull = bars + 2 * GM_STAGES + 4;                   // [DEPTH] tile id published
+  uint64_t* empty = bars + NB;  // barrier arrays sized for the max stage count
+  uint64_t* tfull = bars + 2 * NB;
+  uint64_t* tempty = bars + 2 * NB + 2;
+  uint64_t* sfull = bars + 2 * NB + 4;                           // [DEPTH] tile id published
   uint64_t* sempty = sfull + GM_SCHED_DEPTH;                     // [DEPTH] (leader) slot consumed
   int* s_tile = reinterpret_cast<int*>(sempty + GM_SCHED_DEPTH);  // [DEPTH]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_tile + GM_SCHED_DEPTH);
@@ -375,8 +387,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GM_THREADS, 1)
         }
         __syncwarp();
       };
-      (void)valid;
-      (void)grow;
       if constexpr (EPI == EPI_SWIGLU) {
         __nv_bfloat16* ocol = out + (long long)c.n * (GM_BN / 2);
 #pragma unroll 1
@@ -392,9 +402,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GM_THREADS, 1)
             const float u0 = __uint_as_float(ur[2 * q]), u1 = __uint_as_float(ur[2 * q + 1]);
             pk[q] = pack_bf16x2(silu_f(g0) * u0, silu_f(g1) * u1);
           }
+          if constexpr (STG) {
 #pragma unroll
-          for (int q = 0; q < 4; ++q) stage16((cc & 1) * 4 + q, pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
-          if (cc & 1) flush64(ocol + (cc >> 1) * 64);
+            for (int q = 0; q < 4; ++q) stage16((cc & 1) * 4 + q, pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+            if (cc & 1) flush64(ocol + (cc >> 1) * 64);
+          } else if (valid) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              st_global_v4(ocol + grow * p.ldo + cc * 32 + 8 * q, pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+          }
         }
       } else {
         __nv_bfloat16* ocol = out + (long long)c.n * GM_BN;
@@ -406,9 +422,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GM_THREADS, 1)
           uint32_t pk[16];
 #pragma unroll
           for (int q = 0; q < 16; ++q) pk[q] = pack_bf16x2(__uint_as_float(r[2 * q]), __uint_as_float(r[2 * q + 1]));
+          if constexpr (STG) {
 #pragma unroll
-          for (int q = 0; q < 4; ++q) stage16((cc & 1) * 4 + q, pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
-          if (cc & 1) flush64(ocol + (cc >> 1) * 64);
+            for (int q = 0; q < 4; ++q) stage16((cc & 1) * 4 + q, pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+            if (cc & 1) flush64(ocol + (cc >> 1) * 64);
+          } else if (valid) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              st_global_v4(ocol + grow * p.ldo + cc * 32 + 8 * q, pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+          }
         }
       }
       tc_fence_before();
@@ -681,20 +703,29 @@ int launch_grouped_gemm(int epi, const void* A, long long rows_cap, int K, const
   int ka = env_bk == 128 ? 2 : env_bk == 64 ? 1 : (epi == EPI_SWIGLU ? 2 : 1);
   if (K % (ka * GM_BK) != 0) ka = 1;
   cudaError_t err;
-#define GM_LAUNCH(E_, KA_)                                                                                  \
+#define GM_LAUNCH(E_, KA_, STG_)                                                                            \
   do {                                                                                                      \
     static bool attr = false;                                                                               \
     if (!attr) {                                                                                            \
-      cudaFuncSetAttribute(grouped_gemm_kernel<E_, KA_>, cudaFuncAttributeMaxDynamicSharedMemorySize,       \
-                           (int)GM_SMEM_BYTES);                                                             \
+      cudaFuncSetAttribute(grouped_gemm_kernel<E_, KA_, STG_>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                           (int)GmRing<KA_, STG_>::SMEM);                                                   \
       attr = true;                                                                                          \
     }                                                                                                       \
-    grouped_gemm_kernel<E_, KA_><<<grid, GM_THREADS, GM_SMEM_BYTES, s>>>(p);                                \
+    grouped_gemm_kernel<E_, KA_, STG_><<<grid, GM_THREADS, GmRing<KA_, STG_>::SMEM, s>>>(p);                \
   } while (0)
+  // COX_GEMM_NOSTG=1: BK = 64 kernels without the epilogue staging tile, 7 ring stages (experiment)
+  static const bool nostg = [] {
+    const char* e = getenv("COX_GEMM_NOSTG");
+    return e && atoi(e) == 1;
+  }();
   if (epi == EPI_SWIGLU) {
-    if (ka == 2) GM_LAUNCH(EPI_SWIGLU, 2); else GM_LAUNCH(EPI_SWIGLU, 1);
+    if (ka == 2) GM_LAUNCH(EPI_SWIGLU, 2, true);
+    else if (nostg) GM_LAUNCH(EPI_SWIGLU, 1, false);
+    else GM_LAUNCH(EPI_SWIGLU, 1, true);
   } else {
-    if (ka == 2) GM_LAUNCH(EPI_STORE, 2); else GM_LAUNCH(EPI_STORE, 1);
+    if (ka == 2) GM_LAUNCH(EPI_STORE, 2, true);
+    else if (nostg) GM_LAUNCH(EPI_STORE, 1, false);
+    else GM_LAUNCH(EPI_STORE, 1, true);
   }
 #undef GM_LAUNCH
   err = cudaGetLastError();
