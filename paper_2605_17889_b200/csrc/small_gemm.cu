@@ -81,7 +81,7 @@ struct SgCfg {
                                                                                : (int)(SG_RING_BYTES / (A_STAGE + B_STAGE));
   static constexpr uint32_t TMEM_COLS = 2 * NMAX < 64 ? 64 : 2 * NMAX;
   static constexpr size_t SMEM = 1024 + STAGES * (A_STAGE + B_STAGE) + 512 + 1040 + 4 * SG_MAX_PAIRS + 1024 + 32 +
-                                 24 * (SG_MAXG + 2) +
+                                 256 + 24 * (SG_MAXG + 2) +
                                  4 * SG_BM * SG_PITCH + 64;
 };
 
@@ -151,6 +151,7 @@ struct SmallParams {
 constexpr int SG_CB_BASE = 1 + SG_MAXG;  // counters[SG_CB_BASE + i]: down tiles stored in column block i
 constexpr int SG_COUNTERS = 256;
 constexpr int SG_ROUTED = SG_COUNTERS - 2;  // dense: tokens routed so far
+constexpr int SG_CTICKET = SG_COUNTERS - 3; // fused combine: work-item ticket
 
 
 COX_DEV void mbar_spin_ge(const int* p, int want) {
@@ -733,87 +734,12 @@ __global__ void __launch_bounds__(SG_THREADS, 1) small_ffn_kernel(const __grid_c
         if (lane == 0) mbar_arrive(smem_u32(&tempty[acc]));
       }
       if (pass == 1 && p.out) {
-        // fused combine: the CTA that stores the last down tile of column
-        // block i gathers the k rows of every token for those 128 columns
-        // (same operation order as combine_kernel, so the same bits)
+        // publish this down tile of column block i to the fused combine
+        // (end of the kernel): release after all epilogue threads' y stores
         named_bar_epi();
         if (tid == 0) {
           __threadfence();
-          const int old = atomicAdd(p.counters + SG_CB_BASE + i, 1);
-          __threadfence();
-          s_misc[1] = (old == s_misc[0] - 1);
-        }
-        named_bar_epi();
-        if (s_misc[1]) {
-          // dst / w of every token into shared memory (the staging tile is free
-          // here), then every (token, 8-column chunk) issues its k + 1 row loads
-          // at once; accumulation in ascending j as in combine_kernel
-          const int T = p.T, kk = p.k, d = p.d;
-          int* s_dst = reinterpret_cast<int*>(stg);
-          float* s_w = reinterpret_cast<float*>(stg) + T * kk;
-          if (p.dense && tid == 0) mbar_spin_ge(p.counters + SG_ROUTED, T);  // routing of every token done
-          if (p.from_idx) mbar_wait(smem_u32(perm_ready), 0);              // this CTA's permutation is built
-          named_bar_epi();
-          __threadfence();
-          for (int e = tid; e < T * kk; e += 128) {
-            if (p.dense) {
-              s_dst[e] = p.expert_slot[p.ridx[e]] * T + e / kk;
-              s_w[e] = p.rw[e];
-            } else if (p.from_idx) {
-              s_dst[e] = s_pos[e];  // this CTA's copy of the permutation (perm_ready long passed)
-              s_w[e] = p.cw[e];
-            } else {
-              s_dst[e] = p.cdst[e];
-              s_w[e] = p.cw[e];
-            }
-          }
-          named_bar_epi();
-          const __nv_bfloat16* y0 = p.y[0];
-          const __nv_bfloat16* ys = p.y[1];
-          constexpr int CI = 4;  // items per batch: all their row loads are in flight together
-          for (int it0 = tid; it0 < T * 16; it0 += 128 * CI) {
-            uint4 v[CI][9];
-#pragma unroll
-            for (int c = 0; c < CI; ++c) {
-              const int it = it0 + c * 128;
-              if (it < T * 16) {
-                const int tt = it >> 4;
-                const int col = i * SG_BM + (it & 15) * 8;
-#pragma unroll
-                for (int j = 0; j < 8; ++j)
-                  if (j < kk) v[c][j] = ld_cg_v4(y0 + (long long)s_dst[tt * kk + j] * d + col);
-                if (ys) v[c][8] = ld_cg_v4(ys + (long long)tt * d + col);
-              }
-            }
-#pragma unroll
-            for (int c = 0; c < CI; ++c) {
-              const int it = it0 + c * 128;
-              if (it >= T * 16) break;
-              const int tt = it >> 4;
-              const int col = i * SG_BM + (it & 15) * 8;
-              float acc[8];
-#pragma unroll
-              for (int q = 0; q < 8; ++q) acc[q] = 0.0f;
-#pragma unroll
-              for (int j = 0; j < 8; ++j) {
-                if (j >= kk) break;
-                const float wj = s_w[tt * kk + j];
-                float f[8];
-                bf16x8_to_f32(v[c][j], f);
-#pragma unroll
-                for (int q = 0; q < 8; ++q) acc[q] = __fadd_rn(acc[q], __fmul_rn(wj, f[q]));
-              }
-              if (ys) {
-                float f[8];
-                bf16x8_to_f32(v[c][8], f);
-#pragma unroll
-                for (int q = 0; q < 8; ++q) acc[q] = __fadd_rn(acc[q], f[q]);
-              }
-              st_global_v4(p.out + (long long)tt * d + col, pack_bf16x2(acc[0], acc[1]), pack_bf16x2(acc[2], acc[3]),
-                           pack_bf16x2(acc[4], acc[5]), pack_bf16x2(acc[6], acc[7]));
-            }
-          }
-          named_bar_epi();  // the staging tile is reused by the next unit
+          atomicAdd(p.counters + SG_CB_BASE + i, 1);
         }
       }
       if (pass == 0 && (p.phases & 2)) {
@@ -835,6 +761,82 @@ __global__ void __launch_bounds__(SG_THREADS, 1) small_ffn_kernel(const __grid_c
     tc_fence_after();
     tmem_dealloc<1>(tmem_base, SG_TMEM_COLS);
   }
+  // ------------------------------------------------------------ fused combine
+  // out[t, block] = sum_j w[t,j] y[row(t,j), block] (+ y_shared[t, block]) in
+  // ascending j with separately rounded mul/add -- combine_kernel's order, so
+  // the same bits.  Work items (column block, 16 tokens) are claimed from a
+  // global ticket by every CTA that has finished its units; an item waits
+  // (acquire) until all down tiles of its block are stored, so the combine of
+  // the last blocks is spread over all SMs instead of trailing on one CTA.
+  if (p.out) {
+    const int T = p.T, kk = p.k, d = p.d;
+    const int tid = threadIdx.x;
+    int* s_dst = reinterpret_cast<int*>(stg);
+    float* s_w = reinterpret_cast<float*>(stg) + T * kk;
+    int* s_item = s_misc + 3;
+    if (p.dense && tid == 0) mbar_spin_ge(p.counters + SG_ROUTED, T);  // routing of every token done
+    if (p.from_idx) mbar_wait(smem_u32(perm_ready), 0);              // this CTA's permutation is built
+    __syncthreads();
+    __threadfence();
+    for (int e = tid; e < T * kk; e += SG_THREADS) {
+      if (p.dense) {
+        s_dst[e] = p.expert_slot[p.ridx[e]] * T + e / kk;
+        s_w[e] = p.rw[e];
+      } else if (p.from_idx) {
+        s_dst[e] = s_pos[e];
+        s_w[e] = p.cw[e];
+      } else {
+        s_dst[e] = __ldcg(p.cdst + e);
+        s_w[e] = p.cw[e];
+      }
+    }
+    const int ngrp = (T + 15) / 16;
+    const int nitems = (d / SG_BM) * ngrp;
+    const __nv_bfloat16* y0 = p.y[0];
+    const __nv_bfloat16* ys = p.y[1];
+    for (;;) {
+      __syncthreads();  // staging done / previous item consumed
+      if (tid == 0) {
+        const int item = atomicAdd(p.counters + SG_CTICKET, 1);
+        if (item < nitems) mbar_spin_ge(p.counters + SG_CB_BASE + item / ngrp, s_misc[0]);
+        s_item[0] = item;
+      }
+      __syncthreads();
+      const int item = s_item[0];
+      if (item >= nitems) break;
+      __threadfence();
+      const int blk = item / ngrp;
+      const int tt = (item % ngrp) * 16 + (tid >> 4);
+      const int col = blk * SG_BM + (tid & 15) * 8;
+      if (tt < T) {
+        uint4 v[9];
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          if (j < kk) v[j] = ld_cg_v4(y0 + (long long)s_dst[tt * kk + j] * d + col);
+        if (ys) v[8] = ld_cg_v4(ys + (long long)tt * d + col);
+        float acc[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) acc[q] = 0.0f;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          if (j >= kk) break;
+          const float wj = s_w[tt * kk + j];
+          float f[8];
+          bf16x8_to_f32(v[j], f);
+#pragma unroll
+          for (int q = 0; q < 8; ++q) acc[q] = __fadd_rn(acc[q], __fmul_rn(wj, f[q]));
+        }
+        if (ys) {
+          float f[8];
+          bf16x8_to_f32(v[8], f);
+#pragma unroll
+          for (int q = 0; q < 8; ++q) acc[q] = __fadd_rn(acc[q], f[q]);
+        }
+        st_global_v4(p.out + (long long)tt * d + col, pack_bf16x2(acc[0], acc[1]), pack_bf16x2(acc[2], acc[3]),
+                     pack_bf16x2(acc[4], acc[5]), pack_bf16x2(acc[6], acc[7]));
+      }
+    }
+  }
   if (threadIdx.x == 0) {
     // the last CTA to exit zeroes the counters for the next launch (no memset node)
     __threadfence();
@@ -844,6 +846,7 @@ __global__ void __launch_bounds__(SG_THREADS, 1) small_ffn_kernel(const __grid_c
       const int n = SG_CB_BASE + p.d / SG_BM;
       for (int c = 0; c < n; ++c) p.counters[c] = 0;
       p.counters[SG_ROUTED] = 0;
+      p.counters[SG_CTICKET] = 0;
       p.counters[SG_COUNTERS - 1] = 0;
     }
   }

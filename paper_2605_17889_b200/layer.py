@@ -226,8 +226,8 @@ class MoELayer:
     # experts + combine in ONE launch (cox_decode_moe).  It streams EVERY
     # expert, so it only pays when nearly all are touched anyway, and its token
     # tiles grow with T: measured on C4 (tools/sweep_decode.py, us/step, dense
-    # vs routed): T=8 130/130, 16 171/171, 24 192/198, 32 193/204, 48 204/211,
-    # 64 213/212.  Used when T <= DENSE_T_MAX and P(expert untouched) =
+    # vs routed): T=8 129/129, 16 168/169, 24 188/195, 32 190/199, 48 198/204,
+    # 64 205/205.  Used when T <= DENSE_T_MAX and P(expert untouched) =
     # (1 - k/E)^T <= 0.1; COX_DECODE_DENSE=0 disables.
     DENSE_T_MAX = 48 if os.environ.get("COX_DECODE_DENSE", "1") == "1" else 0
 

@@ -47,6 +47,18 @@ __device__ __forceinline__ unsigned long long gtimer() {{
                   f"  tc_fence_before();\n  __syncthreads();\n"
                   f"  if (threadIdx.x == 0) g_trace[(blockIdx.x * {MAXU + 2} + {MAXU}) * 3 + 1] = gtimer();\n"
                   f"  if (warp == 2) {{\n    tc_fence_after();\n    tmem_dealloc<1>", 1)
+    # end of the deferred combine
+    pat_c = "  if (threadIdx.x == 0) {\n    // the last CTA to exit zeroes the counters"
+    if pat_c in s:
+        s = s.replace(pat_c, f"  if (threadIdx.x == 0) g_trace[(blockIdx.x * {MAXU + 2} + {MAXU + 1}) * 3] = gtimer();\n" + pat_c, 1)
+    # inside the combine: after the dst/w staging
+    pat_s = "    __syncthreads();\n    const __nv_bfloat16* y0 = p.y[0];"
+    if pat_s in s:
+        s = s.replace(pat_s, f"    __syncthreads();\n    if (threadIdx.x == 0) g_trace[(blockIdx.x * {MAXU + 2} + {MAXU + 1}) * 3 + 1] = gtimer();\n"
+                      "    const __nv_bfloat16* y0 = p.y[0];", 1)
+    pat_b = "  const int npend = s_misc[2];\n"
+    if pat_b in s:
+        s = s.replace(pat_b, pat_b + f"  if (threadIdx.x == 0) g_trace[(blockIdx.x * {MAXU + 2} + {MAXU + 1}) * 3 + 2] = gtimer();\n", 1)
     # producer: unit pick-up
     s = s.replace("      int t = lane == 0 ? fetch(si, true) : 0;\n      t = __shfl_sync(0xffffffffu, t, 0);\n      if (t >= total) break;\n",
                   f"      int t = lane == 0 ? fetch(si, true) : 0;\n      t = __shfl_sync(0xffffffffu, t, 0);\n      if (t >= total) break;\n"
@@ -103,6 +115,14 @@ def run():
     t0 = starts.min()
     print(f"CTA start spread {(starts.max() - t0) / 1e3:.1f} us; kernel body {(ends.max() - t0) / 1e3:.1f} us; "
           f"first CTA end {(ends.min() - t0) / 1e3:.1f} us")
+    cend = a[:nb, MAXU + 1, 0]
+    if cend.max() > 0:
+        print(f"after the deferred combine: last CTA {(cend.max() - t0) / 1e3:.1f} us, "
+              f"median {(np.median(cend) - t0) / 1e3:.1f} us")
+        b = int(np.argmax(cend))
+        cst, cbeg = a[b, MAXU + 1, 1], a[b, MAXU + 1, 2]
+        print(f"  last CTA {b}: combine begins {(cbeg - t0) / 1e3:.1f}, staged {(cst - t0) / 1e3:.1f}, "
+              f"done {(cend[b] - t0) / 1e3:.1f} us")
     rec = []
     for b in range(nb):
         for u in range(MAXU):
