@@ -25,6 +25,7 @@
 #include <cstdlib>
 
 #include "common.cuh"
+#include "route_common.cuh"
 
 namespace cox {
 
@@ -145,51 +146,7 @@ router_topk_kernel(const XT* __restrict__ x, const WT* __restrict__ wg, int T, i
       const long t = tb0 + tl;
       if (t >= T) break;
       float* lg = s_logits + tl * E;
-      uint32_t taken = 0;  // bit i: expert lane + 32*i already selected (E <= 256)
-      for (int j = 0; j < k; ++j) {
-        float bv = 0.0f;
-        int bi = -1;
-        for (int i = 0; lane + 32 * i < E; ++i) {
-          const int e = lane + 32 * i;
-          if (taken & (1u << i)) continue;
-          const float v = lg[e];
-          if (bi < 0 || v > bv) { bv = v; bi = e; }
-        }
-#pragma unroll
-        for (int off = 16; off >= 1; off >>= 1) {
-          const float ov = __shfl_xor_sync(0xffffffffu, bv, off);
-          const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
-          const bool better = (oi >= 0) && (bi < 0 || ov > bv || (ov == bv && oi < bi));
-          if (better) { bv = ov; bi = oi; }
-        }
-        if ((bi & 31) == lane) taken |= 1u << (bi >> 5);
-        if (lane == 0) {
-          s_sel[warp][j] = bi;
-          s_selv[warp][j] = bv;
-        }
-      }
-      __syncwarp();
-      if (mode != 0) {  // full softmax: every expf in parallel (in place; the logits are no longer needed)
-        const float m0 = s_selv[warp][0];
-        for (int e = lane; e < E; e += 32) lg[e] = expf(__fsub_rn(lg[e], m0));
-        __syncwarp();
-      }
-      if (lane == 0) {
-        const int* sel = s_sel[warp];
-        const float* selv = s_selv[warp];
-        const float m = selv[0];
-        float ssum = 0.0f;
-        if (mode == 0) {
-          for (int j = 0; j < k; ++j) ssum = __fadd_rn(ssum, expf(__fsub_rn(selv[j], m)));
-        } else {
-          for (int e = 0; e < E; ++e) ssum = __fadd_rn(ssum, lg[e]);  // ascending e, as the oracle
-        }
-        for (int j = 0; j < k; ++j) {
-          idx[t * k + j] = sel[j];
-          wout[t * k + j] = __fdiv_rn(expf(__fsub_rn(selv[j], m)), ssum);
-          atomicAdd(&s_hist[sel[j]], 1);
-        }
-      }
+      warp_route_token(lg, E, k, mode, lane, s_sel[warp], s_selv[warp], idx + t * k, wout + t * k, s_hist);
     }
     __syncthreads();
   }
@@ -296,51 +253,7 @@ router_topk_staged_kernel(const __nv_bfloat16* __restrict__ x, const float* __re
       const long t = tb0 + tl;
       if (t >= T) break;
       float* lg = s_logits + tl * E;
-      uint32_t taken = 0;
-      for (int j = 0; j < k; ++j) {
-        float bv = 0.0f;
-        int bi = -1;
-        for (int i = 0; lane + 32 * i < E; ++i) {
-          const int e = lane + 32 * i;
-          if (taken & (1u << i)) continue;
-          const float v = lg[e];
-          if (bi < 0 || v > bv) { bv = v; bi = e; }
-        }
-#pragma unroll
-        for (int off = 16; off >= 1; off >>= 1) {
-          const float ov = __shfl_xor_sync(0xffffffffu, bv, off);
-          const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
-          const bool better = (oi >= 0) && (bi < 0 || ov > bv || (ov == bv && oi < bi));
-          if (better) { bv = ov; bi = oi; }
-        }
-        if ((bi & 31) == lane) taken |= 1u << (bi >> 5);
-        if (lane == 0) {
-          s_sel[warp][j] = bi;
-          s_selv[warp][j] = bv;
-        }
-      }
-      __syncwarp();
-      if (mode != 0) {  // full softmax: every expf in parallel (in place; the logits are no longer needed)
-        const float m0 = s_selv[warp][0];
-        for (int e = lane; e < E; e += 32) lg[e] = expf(__fsub_rn(lg[e], m0));
-        __syncwarp();
-      }
-      if (lane == 0) {
-        const int* sel = s_sel[warp];
-        const float* selv = s_selv[warp];
-        const float m = selv[0];
-        float ssum = 0.0f;
-        if (mode == 0) {
-          for (int j = 0; j < k; ++j) ssum = __fadd_rn(ssum, expf(__fsub_rn(selv[j], m)));
-        } else {
-          for (int e = 0; e < E; ++e) ssum = __fadd_rn(ssum, lg[e]);  // ascending e, as the oracle
-        }
-        for (int j = 0; j < k; ++j) {
-          idx[t * k + j] = sel[j];
-          wout[t * k + j] = __fdiv_rn(expf(__fsub_rn(selv[j], m)), ssum);
-          atomicAdd(&s_hist[sel[j]], 1);
-        }
-      }
+      warp_route_token(lg, E, k, mode, lane, s_sel[warp], s_selv[warp], idx + t * k, wout + t * k, s_hist);
       __syncwarp();
     }
   }
@@ -446,51 +359,7 @@ router_topk_staged_bf16w_kernel(const __nv_bfloat16* __restrict__ x, const __nv_
       const long t = tb0 + tl;
       if (t >= T) break;
       float* lg = s_logits + tl * E;
-      uint32_t taken = 0;
-      for (int j = 0; j < k; ++j) {
-        float bv = 0.0f;
-        int bi = -1;
-        for (int i = 0; lane + 32 * i < E; ++i) {
-          const int e = lane + 32 * i;
-          if (taken & (1u << i)) continue;
-          const float v = lg[e];
-          if (bi < 0 || v > bv) { bv = v; bi = e; }
-        }
-#pragma unroll
-        for (int off = 16; off >= 1; off >>= 1) {
-          const float ov = __shfl_xor_sync(0xffffffffu, bv, off);
-          const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
-          const bool better = (oi >= 0) && (bi < 0 || ov > bv || (ov == bv && oi < bi));
-          if (better) { bv = ov; bi = oi; }
-        }
-        if ((bi & 31) == lane) taken |= 1u << (bi >> 5);
-        if (lane == 0) {
-          s_sel[warp][j] = bi;
-          s_selv[warp][j] = bv;
-        }
-      }
-      __syncwarp();
-      if (mode != 0) {  // full softmax: every expf in parallel (in place; the logits are no longer needed)
-        const float m0 = s_selv[warp][0];
-        for (int e = lane; e < E; e += 32) lg[e] = expf(__fsub_rn(lg[e], m0));
-        __syncwarp();
-      }
-      if (lane == 0) {
-        const int* sel = s_sel[warp];
-        const float* selv = s_selv[warp];
-        const float m = selv[0];
-        float ssum = 0.0f;
-        if (mode == 0) {
-          for (int j = 0; j < k; ++j) ssum = __fadd_rn(ssum, expf(__fsub_rn(selv[j], m)));
-        } else {
-          for (int e = 0; e < E; ++e) ssum = __fadd_rn(ssum, lg[e]);  // ascending e, as the oracle
-        }
-        for (int j = 0; j < k; ++j) {
-          idx[t * k + j] = sel[j];
-          wout[t * k + j] = __fdiv_rn(expf(__fsub_rn(selv[j], m)), ssum);
-          atomicAdd(&s_hist[sel[j]], 1);
-        }
-      }
+      warp_route_token(lg, E, k, mode, lane, s_sel[warp], s_selv[warp], idx + t * k, wout + t * k, s_hist);
       __syncwarp();
     }
   }

@@ -52,6 +52,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "route_common.cuh"
 
 namespace cox {
 
@@ -80,7 +81,7 @@ struct SgCfg {
   static constexpr int STAGES = (int)(SG_RING_BYTES / (A_STAGE + B_STAGE)) > 12 ? 12
                                                                                : (int)(SG_RING_BYTES / (A_STAGE + B_STAGE));
   static constexpr uint32_t TMEM_COLS = 2 * NMAX < 64 ? 64 : 2 * NMAX;
-  static constexpr size_t SMEM = 1024 + STAGES * (A_STAGE + B_STAGE) + 512 + 1040 + 4 * SG_MAX_PAIRS + 1024 + 32 +
+  static constexpr size_t SMEM = 1024 + STAGES * (A_STAGE + B_STAGE) + 512 + 1120 + 4 * SG_MAX_PAIRS + 1024 + 32 +
                                  256 + 24 * (SG_MAXG + 2) +
                                  4 * SG_BM * SG_PITCH + 64;
 };
@@ -203,12 +204,13 @@ __global__ void __launch_bounds__(SG_THREADS, 1) small_ffn_kernel(const __grid_c
   int* s_p4 = s_p3 + SG_MAXG + 1;    // [G+1] prefix of down units
   int* s_misc = s_p4 + SG_MAXG + 1;  // [0] groups with rows, [1] combine flag
   int* s_act = s_misc + 4;            // [G] active groups (rows > 0), in group order
-  float* s_route = reinterpret_cast<float*>(s_act + SG_MAXG);  // [260] dense: logits of the token being routed;
+  float* s_route = reinterpret_cast<float*>(s_act + SG_MAXG);  // [280] dense: logits of the token being routed
+                                                                 //   (+ top-k scratch at 264..279);
   int* s_eoff = reinterpret_cast<int*>(s_route);                 //   from_idx: expert offsets [E + 1]
   // from_idx: the stable permutation, computed once per CTA by warp 2:
   // s_perm[row] = token of permuted row (expert-major, ascending tokens),
   // s_pos[t*k + j] = permuted row of (t, j)
-  int16_t* s_perm = reinterpret_cast<int16_t*>(s_route + 260);   // [SG_MAX_PAIRS]
+  int16_t* s_perm = reinterpret_cast<int16_t*>(s_route + 280);   // [SG_MAX_PAIRS]
   int16_t* s_pos = s_perm + SG_MAX_PAIRS;                         // [SG_MAX_PAIRS]
   int* s_erun = reinterpret_cast<int*>(s_pos + SG_MAX_PAIRS);     // [256] running row per expert
   uint64_t* perm_ready = reinterpret_cast<uint64_t*>(s_erun + 256);
@@ -615,50 +617,9 @@ __global__ void __launch_bounds__(SG_THREADS, 1) small_ffn_kernel(const __grid_c
           }
         }
         __syncwarp();
-        int sel[8];
-        float selv[8];
-        uint32_t taken = 0;
-        for (int j = 0; j < kk; ++j) {
-          float bv = 0.f;
-          int bi = -1;
-          for (int i = 0; lane + 32 * i < E; ++i) {
-            const int e = lane + 32 * i;
-            if (taken & (1u << i)) continue;
-            const float v = s_route[e];
-            if (bi < 0 || v > bv) {
-              bv = v;
-              bi = e;
-            }
-          }
-#pragma unroll
-          for (int off = 16; off >= 1; off >>= 1) {
-            const float ov = __shfl_xor_sync(0xffffffffu, bv, off);
-            const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
-            if (oi >= 0 && (bi < 0 || ov > bv || (ov == bv && oi < bi))) {
-              bv = ov;
-              bi = oi;
-            }
-          }
-          if ((bi & 31) == lane) taken |= 1u << (bi >> 5);
-          sel[j & 7] = bi;
-          selv[j & 7] = bv;
-        }
-        if (p.mode != 0) {
-          for (int e = lane; e < E; e += 32) s_route[e] = expf(__fsub_rn(s_route[e], selv[0]));
-          __syncwarp();
-        }
+        warp_route_token(s_route, E, kk, p.mode, lane, reinterpret_cast<int*>(s_route + 264), s_route + 272,
+                         p.ridx + t * kk, p.rw + t * kk, nullptr);
         if (lane == 0) {
-          const float m = selv[0];
-          float ssum = 0.0f;
-          if (p.mode == 0) {
-            for (int j = 0; j < kk; ++j) ssum = __fadd_rn(ssum, expf(__fsub_rn(selv[j], m)));
-          } else {
-            for (int e = 0; e < E; ++e) ssum = __fadd_rn(ssum, s_route[e]);  // ascending e, as the oracle
-          }
-          for (int j = 0; j < kk; ++j) {
-            p.ridx[t * kk + j] = sel[j];
-            p.rw[t * kk + j] = __fdiv_rn(expf(__fsub_rn(selv[j], m)), ssum);
-          }
           __threadfence();
           atomicAdd(p.counters + SG_ROUTED, 1);
         }
