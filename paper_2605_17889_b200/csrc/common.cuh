@@ -88,6 +88,14 @@ COX_DEV void mbar_arrive_cluster(uint32_t cluster_bar) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_bar) : "memory");
 }
 
+// Relaxed arrive (no release fence, so no MEMBAR.GPU wait for this thread's
+// outstanding global stores).  For "TMEM accumulator drained" signals: the
+// tcgen05.ld results are already in registers (tcgen05.wait::ld) and the
+// consumer orders its MMAs with tcgen05.fence::after_thread_sync.
+COX_DEV void mbar_arrive_cluster_relaxed(uint32_t cluster_bar) {
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_bar) : "memory");
+}
+
 // ---------------------------------------------------------------- TMA
 COX_DEV void tma_prefetch_desc(const void* map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
