@@ -230,6 +230,14 @@ COX_DEV void ffma2(float& a0, float& a1, float x, float w0, float w1) {
 COX_DEV void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 COX_DEV void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
+// SiLU for the SwiGLU epilogues: g / (1 + exp(-g)) with the approximate
+// MUFU reciprocal (__fdividef, ~2 ulp fp32; the result is rounded to bf16).
+// Branch-free: the IEEE __frcp_rn carries a special-case branch per element
+// (BSSY/BSYNC), which serialised the 32 elements of a TMEM chunk and made the
+// K3 epilogue 11-14 us per 256x256 tile -- longer than the MMAs at K <= 2048.
+// Large negative g: exp(-g) = inf -> g / inf = -0.
+COX_DEV float silu_fast(float g) { return __fdividef(g, 1.0f + __expf(-g)); }
+
 // ---------------------------------------------------------------- misc
 COX_DEV uint32_t pack_bf16x2(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);

@@ -93,7 +93,7 @@ COX_DEV TileCoord decode_tile(int t, const int* s_prefix, const int* s_rows, int
   return c;
 }
 
-COX_DEV float silu_f(float g) { return g * __frcp_rn(1.0f + __expf(-g)); }
+COX_DEV float silu_f(float g) { return silu_fast(g); }
 
 // KA = 128-byte swizzle atoms of K per pipeline stage: 1 -> BK 64, 6 stages;
 // 2 -> BK 128, 3 stages (same smem; 256 contiguous bytes per weight row per

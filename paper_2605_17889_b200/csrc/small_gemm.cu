@@ -667,7 +667,7 @@ __global__ void __launch_bounds__(SG_THREADS, 1) small_ffn_kernel(const __grid_c
                   const int c = cg * 8 + 2 * j;
                   const float g0 = stg[c * SG_PITCH + tt], g1 = stg[(c + 1) * SG_PITCH + tt];
                   const float u0 = stg[(64 + c) * SG_PITCH + tt], u1 = stg[(65 + c) * SG_PITCH + tt];
-                  pk[j] = pack_bf16x2(g0 * __frcp_rn(1.0f + __expf(-g0)) * u0, g1 * __frcp_rn(1.0f + __expf(-g1)) * u1);
+                  pk[j] = pack_bf16x2(silu_fast(g0) * u0, silu_fast(g1) * u1);
                 }
                 st_global_v4(hbase + (tok0 + tt) * ff + cg * 8, pk[0], pk[1], pk[2], pk[3]);
               }
