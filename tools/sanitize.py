@@ -27,6 +27,23 @@ def main():
     ops.router_topk(make_tokens(5000, 256, device=dev), wg, 6, 1)
     ops.router_topk(make_tokens(33, 256, device=dev, dtype=torch.float32), wg[:8].contiguous(), 2, 0)
     torch.cuda.synchronize()
+    # decode-size paths: routed weight-streaming launch straight from idx (T=64,
+    # E=64), the dense single launch (T=40, E=16), and the x_perm / row-gather
+    # variants of cox_small_expert_ffn
+    for (T, d, ff, E, k, mode, shared) in [(64, 256, 128, 64, 6, "deepseek", 256), (40, 256, 128, 16, 4, "deepseek", 128),
+                                           (150, 256, 128, 8, 2, "mixtral", 0)]:
+        wts = make_layer_weights(E, d, ff, seed=2, device=dev, shared_ff=shared)
+        x = make_tokens(T, d, seed=3, device=dev)
+        layer = MoELayer(wts, k, mode)
+        out = layer(x)
+        layer.SMALL_FROM_IDX = False
+        out2 = layer(x)
+        torch.cuda.synchronize()
+        assert torch.isfinite(out.float()).all() and torch.isfinite(out2.float()).all()
+    # tensor-core screening router (E >= 32, T >= 148*128)
+    wg64 = (torch.rand(64, 256, device=dev) * 2 - 1).to(torch.bfloat16) / 16
+    ops.router_topk(make_tokens(148 * 128 + 9, 256, device=dev), wg64, 6, 1)
+    torch.cuda.synchronize()
     print("sanitize run ok")
 
 
