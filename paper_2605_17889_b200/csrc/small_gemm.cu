@@ -562,9 +562,20 @@ __global__ void __launch_bounds__(SG_THREADS, 1) small_ffn_kernel(const __grid_c
       for (int e = lane; e < p.E; e += 32) s_erun[e] = s_eoff[e];
       __syncwarp();
       const int nent = p.T * p.k;
-      for (int c = 0; c < nent; c += 32) {
+      constexpr int PB = 8;  // chunks whose idx loads are in flight together (one L2 round trip per 256 entries)
+      for (int c0 = 0; c0 < nent; c0 += 32 * PB) {
+      int ev[PB];
+#pragma unroll
+      for (int b = 0; b < PB; ++b) {
+        const int ent = c0 + 32 * b + lane;
+        ev[b] = ent < nent ? __ldg(p.ridx + ent) : -1;
+      }
+#pragma unroll
+      for (int b = 0; b < PB; ++b) {
+        const int c = c0 + 32 * b;
+        if (c >= nent) break;
         const int ent = c + lane;
-        const int e = ent < nent ? p.ridx[ent] : -1;
+        const int e = ev[b];
         const uint32_t peers = __match_any_sync(0xffffffffu, e);
         const int before = __popc(peers & ((1u << lane) - 1u));
         int row = -1;
@@ -577,6 +588,7 @@ __global__ void __launch_bounds__(SG_THREADS, 1) small_ffn_kernel(const __grid_c
           if (blockIdx.x == 0) p.dst_out[ent] = row;
         }
         __syncwarp();
+      }
       }
       if (lane == 0) mbar_arrive(smem_u32(perm_ready));  // release: the arrays are visible to waiters
     }
