@@ -14,12 +14,16 @@
 //   * 2-CTA pairs (cluster 2x1): tcgen05.mma.cta_group::2, M=256 (128 A rows per
 //     CTA), N=256 (128 B rows per CTA), K=16 per instruction, fp32 accumulators
 //     in TMEM (2 x 256 columns: the epilogue of tile i overlaps the MMAs of i+1).
-//   * TMA (cp.async.bulk.tensor, 128B swizzle) streams 64-wide K slices of A and
-//     B into a 6-stage smem ring guarded by mbarriers; both CTAs' loads complete
-//     on the leader's "full" barrier, the leader's MMA commit frees the slot in
-//     both CTAs (multicast commit).
+//   * TMA (cp.async.bulk.tensor, 128B swizzle) streams K slices of A and B into
+//     a 192 KB smem ring guarded by mbarriers (K3: 3 stages of K = 128; K4: 6
+//     stages of K = 64); both CTAs' loads complete on the leader's "full"
+//     barrier, the leader's MMA commit frees the slot in both CTAs (multicast
+//     commit).
 //   * Warp roles: w0 TMA producer, w1 MMA issuer (leader CTA, one thread),
-//     w2 TMEM allocator, w4..w7 epilogue (TMEM -> registers -> global).
+//     w2 TMEM allocator, w4..w7 epilogue (TMEM -> registers -> coalesced
+//     stores through a smem staging tile; branch-free SiLU for K3 -- see
+//     silu_fast -- and a relaxed "accumulator drained" arrive, so the epilogue
+//     stays shorter than one tile's MMAs even at K = 1024).
 //   * Persistent kernel, 74 pairs on 148 SMs, dynamic tile scheduler (warp 3 of
 //     the leader: global atomic counter -> tile-id ring in both CTAs); tiles
 //     are rasterised in bands of `band` n-tiles so that concurrently running
