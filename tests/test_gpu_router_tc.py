@@ -81,3 +81,16 @@ def test_tc_router_matches_cuda_core_router(monkeypatch):
     torch.cuda.synchronize()
     assert torch.equal(idx_big[:4096], idx_small)
     assert torch.equal(w_big[:4096], w_small)
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_tc_router_random_configs(seed):
+    rng = np.random.default_rng(3000 + seed)
+    d = 64 * int(rng.integers(2, 49))        # 128 .. 3072
+    E = int(rng.integers(32, 257))
+    k = int(rng.integers(1, 9))
+    mode = int(rng.integers(0, 2))
+    x = make_tokens(T_TC, d, seed=seed + 20, device=DEV)
+    if rng.random() < 0.5:  # skewed, near-tie-rich routing: scaled-down tokens
+        x = (x.float() * 0.05).to(torch.bfloat16)
+    _check(x, _wg(E, d, seed + 30), k, mode, 2e-6 if mode == 0 else 1e-5)

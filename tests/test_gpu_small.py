@@ -221,3 +221,37 @@ def test_decode_from_idx_matches_permute_path(T, d, ff, E, k, mode, shared_ff):
     assert torch.equal(ba.offsets, bb.offsets)
     assert torch.equal(ba.dst, bb.dst)
     assert torch.equal(a, bo)
+
+
+@pytest.mark.parametrize("seed", range(10))
+def test_random_decode_configs_vs_oracle(seed):
+    """Seeded random decode-size layers through MoELayer (whichever decode path
+    it picks: routed from idx, dense single launch): routing bit-exact and
+    rel-L2 <= 1e-2 against the fp32 oracle; skewed routing included."""
+    rng = np.random.default_rng(2000 + seed)
+    d = 128 * int(rng.integers(1, 9))
+    ff = 128 * int(rng.integers(1, 6))
+    E = int(rng.choice([2, 4, 8, 16, 32, 64]))
+    k = int(rng.integers(1, min(E, 8) + 1))
+    T = int(rng.integers(1, 257))
+    mode = "mixtral" if rng.random() < 0.5 else "deepseek"
+    sff = 128 * int(rng.integers(1, 4)) if rng.random() < 0.4 else 0
+    wts = make_layer_weights(E, d, ff, seed=seed, device=DEV, shared_ff=sff, keep_split=True)
+    x = make_tokens(T, d, seed=seed + 11, device=DEV).float()
+    if rng.random() < 0.4:  # skew toward one expert
+        x += 2.0 * d ** 0.5 * wts.wg[int(rng.integers(0, E))]
+    x = x.to(torch.bfloat16)
+    layer = MoELayer(wts, k, mode)
+    assert layer.uses_small_path(T)
+    out = layer(x)
+    torch.cuda.synchronize()
+    f = lambda t: t.float().cpu().numpy()  # noqa: E731
+    shared = (f(wts.shared_w1), f(wts.shared_w3), f(wts.shared_w2)) if sff else None
+    ref = O.moe_layer(f(x), f(wts.wg), f(wts.w1), f(wts.w3), f(wts.w2), k, 0 if mode == "mixtral" else 1,
+                      shared=shared)
+    b = layer.buffers(T, DEV)
+    assert np.array_equal(b.idx.cpu().numpy(), ref["idx"])
+    if not layer.uses_dense_decode(T):
+        assert np.array_equal(b.dst.cpu().numpy(), ref["dst"])
+        assert np.array_equal(b.offsets.cpu().numpy(), ref["offsets"])
+    assert rel_l2(f(out), ref["out"]) <= 1e-2
