@@ -248,11 +248,13 @@ COX_DEV void st_global_v4(void* p, uint32_t a, uint32_t b, uint32_t c, uint32_t 
   asm volatile("st.global.v4.b32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
 }
 
-// Read-only (for the whole kernel) 16-byte load.  Not volatile: the compiler
-// may batch these loads ahead of the arithmetic that consumes them.
+// Read-only (for the whole kernel) 16-byte load.  Volatile on purpose: callers
+// guard loads with bounds checks (`if (c < d) v = ld_nc_v4(...)`), and a
+// non-volatile asm load could be speculated past the guard, reading beyond
+// the end of an allocation.
 COX_DEV uint4 ld_nc_v4(const void* p) {
   uint4 r;
-  asm("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
                : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
                : "l"(p));
   return r;
