@@ -48,6 +48,9 @@ CONFIGS = {
     "C4D": (64, 2048, 1408, 64, 6, "deepseek", 2816,
             "C4 DeepSeek-V2-Lite MoE layer decode step: 64 sequences x 1 token (64 routed top-6 + 2 shared), "
             "CUDA-graph replay"),
+    "C2D": (64, 4096, 14336, 8, 2, "mixtral", 0,
+            "C2 Mixtral-8x7B MoE layer decode step: 64 sequences x 1 token (not a BASELINE config: the decode "
+            "kernel at 352 MB experts), CUDA-graph replay"),
     "C3": (64 * 4096, 6144, 16384, 8, 2, "mixtral", 0,
            "C3 Mixtral-8x22B-shaped 56-layer MoE stack, batch 64x4096, HBM budget -> calibrated hot experts "
            "resident, cold experts streamed from pinned host memory"),
@@ -299,7 +302,7 @@ def main():
     if args.steps is None:
         # enough steps that the end-to-end pipeline's fill (first H2D) and drain
         # (last D2H) are a small share of the e2e number, within ~5 s per arm
-        args.steps = {"C3": 5, "C4D": 2000, "C1": 200}.get(args.config, 30)
+        args.steps = {"C3": 5, "C4D": 2000, "C2D": 1000, "C1": 200}.get(args.config, 30)
         if args.impl == "reference":
             args.steps = 10
     cfg = CONFIGS[args.config]
@@ -352,7 +355,7 @@ def main():
     else:
         layer = MoELayer(wts, k, mode)
     stream = torch.cuda.current_stream()
-    graph = args.config == "C4D" and ws == 1
+    graph = args.config in ("C4D", "C2D") and ws == 1
     if graph:
         replay, _ = layer.capture(x)
         step = lambda: replay()  # noqa: E731
