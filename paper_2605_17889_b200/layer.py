@@ -310,14 +310,19 @@ class MoELayer:
             subs[n].forward(xs, out=out[s0:s0 + n])
         return out
 
+    # run_host_batches replays a captured step for batches up to this many tokens (COX_HOST_GRAPH_T_MAX)
+    HOST_GRAPH_T_MAX = int(os.environ.get("COX_HOST_GRAPH_T_MAX", "8192"))
+
     def run_host_batches(self, xs_host, outs_host) -> None:
         """End-to-end serving loop over host batches (pinned memory).
 
         Batch i's H2D copy (copy engine, own stream) overlaps batch i-1's expert
         stage, and batch i's D2H copy overlaps batch i+1's stage: two device
         input and two device output buffers, event-ordered.  Every batch still
-        crosses PCIe both ways; only the waiting is hidden.  Returns once all
-        work is enqueued; the current stream is ordered after the last copy."""
+        crosses PCIe both ways; only the waiting is hidden.  Batches of up to
+        HOST_GRAPH_T_MAX tokens replay a CUDA graph of the step (one per slot).
+        Returns once all work is enqueued; the current stream is ordered after
+        the last copy."""
         if len(xs_host) != len(outs_host):
             raise ValueError("one output buffer per input batch")
         if not xs_host:
@@ -339,7 +344,10 @@ class MoELayer:
             comp.wait_event(ready)
             if out_done[slot] is not None:
                 comp.wait_event(out_done[slot])
-            self.forward(xin[slot], out=yout[slot])
+            if st["graphs"] is not None:
+                st["graphs"][slot].replay()
+            else:
+                self.forward(xin[slot], out=yout[slot])
             ev_c = torch.cuda.Event()
             ev_c.record(comp)
             in_free[slot] = ev_c
@@ -357,7 +365,18 @@ class MoELayer:
             st = {"T": T, "h2d": torch.cuda.Stream(dev), "d2h": torch.cuda.Stream(dev),
                   "xin": [torch.empty((T, self.d), dtype=torch.bfloat16, device=dev) for _ in range(2)],
                   "yout": [torch.empty((T, self.d), dtype=self.out_dtype, device=dev) for _ in range(2)],
-                  "in_free": [None, None], "out_done": [None, None]}
+                  "in_free": [None, None], "out_done": [None, None], "graphs": None}
+            if T <= self.HOST_GRAPH_T_MAX:
+                # launch-bound batch sizes: one CUDA graph per (input, output) slot pair
+                st["graphs"] = []
+                for s in range(2):
+                    st["xin"][s].zero_()
+                    self.forward(st["xin"][s], out=st["yout"][s])  # buffers / tensor maps outside capture
+                    torch.cuda.synchronize(dev)
+                    g = torch.cuda.CUDAGraph()
+                    with torch.cuda.graph(g):
+                        self.forward(st["xin"][s], out=st["yout"][s])
+                    st["graphs"].append(g)
             self._hs = st
         return st
 

@@ -231,10 +231,15 @@ def test_ep_layer_single_rank_nccl_matches_moelayer():
         dist.destroy_process_group()
 
 
-def test_run_host_batches_matches_forward():
-    T, d, ff, E, k = 2000, 512, 256, 8, 2
+@pytest.mark.parametrize("T,graphed", [(2000, True), (2000, False), (40, True), (200, True)])
+def test_run_host_batches_matches_forward(T, graphed):
+    """Pipelined host-buffer loop (graph-replayed step for small batches, eager
+    otherwise; T=40 / 200 take the decode kernels) == forward bit-for-bit."""
+    d, ff, E, k = 512, 256, 8, 2
     wts = make_layer_weights(E, d, ff, seed=0, device=DEV)
     layer = MoELayer(wts, k)
+    if not graphed:
+        layer.HOST_GRAPH_T_MAX = 0
     xs = [make_tokens(T, d, seed=s, device=DEV) for s in (1, 2, 3)]
     ref = [layer(x).clone() for x in xs]
     xh = [x.cpu().pin_memory() for x in xs]
