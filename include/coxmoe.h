@@ -125,6 +125,20 @@ int cox_grouped_down_ex(const void* h, long long rows_cap, const int32_t* offset
                         const int32_t* group_experts, const void* const* w2, int ff, int d, void* y_perm,
                         int max_ctas, void* stream);
 
+/* Shared-expert down projection with K5 fused into its epilogue (prefill,
+ * DeepSeek-style layers): out[t] = sum_{j<k} w[t,j] * y_perm[dst[t,j]]
+ * + bf16(h_shared[t] W2s^T), the exact operation order of cox_combine with
+ * shared = the shared expert's bf16 output, so the result is bit-identical to
+ * cox_grouped_down(shared) followed by cox_combine — without writing and
+ * re-reading the shared output or running the combine as its own pass.
+ * Replaces `expert:merge` / `return_store` (sim.py:149-202,
+ * costmodel.py:266-273) for layers with shared experts.  shared_offsets:
+ * device int32 {0, T}; w2_shared [d, ff_shared]; y_perm/dst/w as cox_combine;
+ * out [T, d] bf16.  d % 256 == 0, ff_shared % 64 == 0, 1 <= k <= 8. */
+int cox_shared_down_combine(const void* h_shared, int T, const int32_t* shared_offsets, const void* w2_shared,
+                            int ff_shared, int d, const void* y_perm, const int32_t* dst, const float* w, int k,
+                            void* out, void* stream);
+
 /* K3+K4(+K5) for decode-size batches: ONE
  * persistent, weight-streaming launch runs the SwiGLU and the down projection
  * of every group, the shared experts of a DeepSeek-style layer (one more

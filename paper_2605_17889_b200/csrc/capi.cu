@@ -16,7 +16,8 @@ int launch_permute(const int32_t* idx, int T, int k, int E, int tile_m, const vo
                    long long rows_cap = 0);
 int launch_grouped_gemm(int epi, const void* A, long long rows_cap, int K, const int32_t* offsets, int n_groups,
                         const int32_t* group_expert, const void* const* B, int N, void* out, long long ldo,
-                        int max_ctas, cudaStream_t s, const int32_t* a_rows = nullptr, long long a_rows_cap = 0);
+                        int max_ctas, cudaStream_t s, const int32_t* a_rows = nullptr, long long a_rows_cap = 0,
+                        const GemmCombine* cmb = nullptr);
 struct SmallDense {
   const void* wg;
   int E, mode;
@@ -204,6 +205,26 @@ int cox_grouped_down_ex(const void* h, long long rows_cap, const int32_t* offset
 int cox_grouped_down(const void* h, long long rows_cap, const int32_t* offsets, int n_groups,
                      const int32_t* group_experts, const void* const* w2, int ff, int d, void* y_perm, void* stream) {
   return cox_grouped_down_ex(h, rows_cap, offsets, n_groups, group_experts, w2, ff, d, y_perm, 0, stream);
+}
+
+int cox_shared_down_combine(const void* h_shared, int T, const int32_t* shared_offsets, const void* w2_shared,
+                            int ff_shared, int d, const void* y_perm, const int32_t* dst, const float* w, int k,
+                            void* out, void* stream) {
+  const char* fn = "cox_shared_down_combine";
+  if (d <= 0 || d % 256 || ff_shared <= 0 || ff_shared % 64)
+    return fail(COX_EINVAL, "%s: need d%%256==0 and ff_shared%%64==0 (d=%d ff_shared=%d)", fn, d, ff_shared);
+  if (T < 0 || k < 1 || k > 8) return fail(COX_EINVAL, "%s: need T >= 0 and 1 <= k <= 8 (T=%d k=%d)", fn, T, k);
+  if (T == 0) return 0;
+  if (!h_shared || !shared_offsets || !w2_shared || !y_perm || !dst || !w || !out)
+    return fail(COX_EINVAL, "%s: null pointer", fn);
+  if (!aligned16(h_shared) || !aligned16(w2_shared) || !aligned16(y_perm) || !aligned16(out))
+    return fail(COX_EINVAL, "%s: unaligned h_shared/w2_shared/y_perm/out", fn);
+  const int32_t g0 = 0;
+  const void* b[1] = {w2_shared};
+  cox::GemmCombine cmb{y_perm, dst, w, k};
+  int rc = cox::launch_grouped_gemm(2, h_shared, T, ff_shared, shared_offsets, 1, &g0, b, d, out, d, 0,
+                                    static_cast<cudaStream_t>(stream), nullptr, 0, &cmb);
+  return cuda_status(rc, fn);
 }
 
 int cox_small_expert_ffn(const void* x, int T, const int32_t* row_tokens, const void* x_perm, long long rows_cap,

@@ -97,6 +97,9 @@ COX_DEV void mbar_arrive_cluster_relaxed(uint32_t cluster_bar) {
 }
 
 // ---------------------------------------------------------------- TMA
+COX_DEV void prefetch_l2(const void* p) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(reinterpret_cast<uint64_t>(p)));
+}
 COX_DEV void tma_prefetch_desc(const void* map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
 }
@@ -163,6 +166,14 @@ COX_DEV uint64_t sdesc_kmajor_sw128(uint32_t saddr) {
   d |= (uint64_t)2 << 61;              // SWIZZLE_128B
   return d;
 }
+
+// top-k combine fused into a down-projection epilogue (grouped_gemm.cu EPI_COMBINE)
+struct GemmCombine {
+  const void* y_perm;   // routed expert outputs [rows, N] bf16
+  const int32_t* dst;   // [T, k]
+  const float* w;       // [T, k]
+  int k;
+};
 
 // Instruction descriptor, kind::f16: BF16 x BF16 -> F32, both K-major.
 __host__ __device__ constexpr uint32_t idesc_bf16_f32(int M, int N) {

@@ -56,6 +56,12 @@ constexpr uint32_t GM_TMEM_COLS = 512;
 constexpr int GM_SCHED_DEPTH = 4;  // tile-id ring between the scheduler and the roles
 constexpr int EPI_SWIGLU = 0;
 constexpr int EPI_STORE = 1;
+// shared-expert down projection with the top-k combine fused into its epilogue:
+// out[t] = sum_j w[t,j] * y_perm[dst[t,j]] + bf16(h_shared W2s^T)[t]
+constexpr int EPI_COMBINE = 2;
+#ifndef CMB_U
+#define CMB_U 2  // EPI_COMBINE: rows per lane whose routed-row loads are in flight together (4: 255 regs, slower)
+#endif
 
 struct alignas(64) GemmParams {
   CUtensorMap a_map;
@@ -68,6 +74,10 @@ struct alignas(64) GemmParams {
   const int* die_map;             // SM id -> die (0/1), nullptr = die-agnostic
   void* out;
   long long ldo;
+  const __nv_bfloat16* cy;  // EPI_COMBINE: routed expert outputs y_perm [rows, N] (leading dim ldo)
+  const int32_t* cdst;      //   [T, ck] permuted row of (token, slot); < 0 = no contribution
+  const float* cw;          //   [T, ck] combine weights
+  int ck;                   //   top-k (<= 8)
   int group_expert[GM_MAXG];
   int n_groups;
   int K;
@@ -363,6 +373,30 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GM_THREADS, 1)
       const TileCoord c = decode_tile(t, s_prefix, s_rows, p.band);
       const int acc = it & 1;
       const uint32_t acc_phase = (it >> 1) & 1;
+      // EPI_COMBINE: this lane's token (row) — its top-k (row, weight) pairs,
+      // and an L2 prefetch of the routed rows' 256 columns while the MMA runs
+      int cd[8];
+      float cwt[8];
+      if constexpr (EPI == EPI_COMBINE) {
+        const int lrow = c.m * 2 * GM_BM + (int)rank * GM_BM + row_in_cta;
+        const bool v = lrow < s_rows[c.g];
+        const long long tok = (long long)s_row0[c.g] + lrow;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          cd[j] = 0;
+          cwt[j] = 0.0f;
+          if (j < p.ck && v) {
+            const int r = __ldg(p.cdst + tok * p.ck + j);
+            if (r >= 0) {
+              cd[j] = r;
+              cwt[j] = __ldg(p.cw + tok * p.ck + j);
+              const __nv_bfloat16* src = p.cy + (long long)r * p.ldo + (long long)c.n * GM_BN;
+#pragma unroll
+              for (int l = 0; l < 4; ++l) prefetch_l2(src + l * 64);
+            }
+          }
+        }
+      }
       mbar_wait(smem_u32(&tfull[acc]), acc_phase);
       tc_fence_after();
       const int local_row = c.m * 2 * GM_BM + (int)rank * GM_BM + row_in_cta;
@@ -388,6 +422,56 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GM_THREADS, 1)
           const int r = i * 4 + (lane >> 3), j = lane & 7;
           const uint4 v = *reinterpret_cast<const uint4*>(stg + r * 32 + ((j ^ (r & 7)) * 4));
           if (r < vrows) st_global_v4(col0 + (grow0 + r) * p.ldo + j * 8, v.x, v.y, v.z, v.w);
+        }
+        __syncwarp();
+      };
+      // EPI_COMBINE: the staged 32 rows x 64 cols are the shared expert's bf16
+      // output; add the routed rows in the order of combine.cu (ascending j,
+      // separately rounded fp32 multiply and add, shared last) and store `out`
+      auto flush64c = [&](__nv_bfloat16* col0, long long gcol) {
+        __syncwarp();
+        // CMB_U rows per lane per batch: all their routed-row loads are issued
+        // before any is consumed (the loads are volatile asm, so the compiler
+        // would not hoist them across the previous row's store by itself)
+#pragma unroll 1
+        for (int i0 = 0; i0 < 8; i0 += CMB_U) {
+          uint4 yv[CMB_U][8];
+          float wj[CMB_U][8];
+#pragma unroll
+          for (int u = 0; u < CMB_U; ++u) {
+            const int r = (i0 + u) * 4 + (lane >> 3), j = lane & 7;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              const int dr = __shfl_sync(0xffffffffu, cd[q], r);
+              wj[u][q] = __shfl_sync(0xffffffffu, cwt[q], r);
+              if (q < p.ck && r < vrows) yv[u][q] = ld_nc_v4(p.cy + (long long)dr * p.ldo + gcol + j * 8);
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < CMB_U; ++u) {
+            const int r = (i0 + u) * 4 + (lane >> 3), j = lane & 7;
+            if (r < vrows) {
+              float a[8];
+#pragma unroll
+              for (int e = 0; e < 8; ++e) a[e] = 0.0f;
+#pragma unroll
+              for (int q = 0; q < 8; ++q) {
+                if (q < p.ck) {
+                  float f[8];
+                  bf16x8_to_f32(yv[u][q], f);
+#pragma unroll
+                  for (int e = 0; e < 8; ++e) a[e] = __fadd_rn(a[e], __fmul_rn(wj[u][q], f[e]));
+                }
+              }
+              const uint4 v = *reinterpret_cast<const uint4*>(stg + r * 32 + ((j ^ (r & 7)) * 4));
+              float sh[8];
+              bf16x8_to_f32(v, sh);
+#pragma unroll
+              for (int e = 0; e < 8; ++e) a[e] = __fadd_rn(a[e], sh[e]);
+              st_global_v4(col0 + (grow0 + r) * p.ldo + j * 8, pack_bf16x2(a[0], a[1]), pack_bf16x2(a[2], a[3]),
+                           pack_bf16x2(a[4], a[5]), pack_bf16x2(a[6], a[7]));
+            }
+          }
         }
         __syncwarp();
       };
@@ -429,7 +513,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GM_THREADS, 1)
           if constexpr (STG) {
 #pragma unroll
             for (int q = 0; q < 4; ++q) stage16((cc & 1) * 4 + q, pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
-            if (cc & 1) flush64(ocol + (cc >> 1) * 64);
+            if (cc & 1) {
+              if constexpr (EPI == EPI_COMBINE)
+                flush64c(ocol + (cc >> 1) * 64, (long long)c.n * GM_BN + (cc >> 1) * 64);
+              else
+                flush64(ocol + (cc >> 1) * 64);
+            }
           } else if (valid) {
 #pragma unroll
             for (int q = 0; q < 4; ++q)
@@ -648,9 +737,11 @@ static int g_num_sms = 0;
 
 // epi: EPI_SWIGLU (B = W13 interleaved [2ff, K], out = h [rows_cap, ff])
 //      EPI_STORE  (B = W2 [N, K],                out = y [rows_cap, N])
+//      EPI_COMBINE (B = W2 of the shared expert, out = final [T, N]; cmb = routed y_perm / dst / w / k)
 int launch_grouped_gemm(int epi, const void* A, long long rows_cap, int K, const int32_t* offsets, int n_groups,
                         const int32_t* group_expert, const void* const* B, int N, void* out, long long ldo,
-                        int max_ctas, cudaStream_t s, const int32_t* a_rows, long long a_rows_cap) {
+                        int max_ctas, cudaStream_t s, const int32_t* a_rows, long long a_rows_cap,
+                        const GemmCombine* cmb) {
   if (n_groups <= 0) return 0;
   static GemmParams p;  // large (8.6 KB): built in static storage, copied at launch
   static std::mutex mu;
@@ -684,6 +775,10 @@ int launch_grouped_gemm(int epi, const void* A, long long rows_cap, int K, const
   p.a_rows_cap = a_rows_cap;
   p.out = out;
   p.ldo = ldo;
+  p.cy = cmb ? static_cast<const __nv_bfloat16*>(cmb->y_perm) : nullptr;
+  p.cdst = cmb ? cmb->dst : nullptr;
+  p.cw = cmb ? cmb->w : nullptr;
+  p.ck = cmb ? cmb->k : 0;
   p.n_groups = n_groups;
   p.K = K;
   p.n_tiles = N / GM_BN;
@@ -705,6 +800,7 @@ int launch_grouped_gemm(int epi, const void* A, long long rows_cap, int K, const
     return e ? atoi(e) : 0;
   }();
   int ka = env_bk == 128 ? 2 : env_bk == 64 ? 1 : (epi == EPI_SWIGLU ? 2 : 1);
+  if (epi == EPI_COMBINE) ka = 1;
   if (K % (ka * GM_BK) != 0) ka = 1;
   cudaError_t err;
 #define GM_LAUNCH(E_, KA_, STG_)                                                                            \
@@ -722,7 +818,9 @@ int launch_grouped_gemm(int epi, const void* A, long long rows_cap, int K, const
     const char* e = getenv("COX_GEMM_NOSTG");
     return e && atoi(e) == 1;
   }();
-  if (epi == EPI_SWIGLU) {
+  if (epi == EPI_COMBINE) {
+    GM_LAUNCH(EPI_COMBINE, 1, true);
+  } else if (epi == EPI_SWIGLU) {
     if (ka == 2) GM_LAUNCH(EPI_SWIGLU, 2, true);
     else if (nostg) GM_LAUNCH(EPI_SWIGLU, 1, false);
     else GM_LAUNCH(EPI_SWIGLU, 1, true);

@@ -110,6 +110,9 @@ class MoELayer:
         if T is not None and self.uses_small_path(T):
             # router + single-CTA permute (indices only) + one launch for K3/K4/shared/combine
             return 1 + 1 + 1 + (1 if self.out_dtype != torch.bfloat16 else 0)
+        if (self.shared_ff and self.SHARED_FUSED_COMBINE and self.k <= 8
+                and not (T is not None and 0 < T * self.k <= self.SHARED_SIDE_MAX_ROWS)):
+            return 1 + perm + 2 + 2  # shared K3 + shared down with the combine in its epilogue
         return 1 + perm + 2 + 1 + (2 if self.shared_ff else 0)
 
     def buffers(self, T: int, device) -> StageBuffers:
@@ -175,6 +178,12 @@ class MoELayer:
         return (0 < T <= self.SMALL_T_MAX and not self.gather_a and self.d % 128 == 0 and self.ff % 128 == 0
                 and self.E <= 64 and (not self.shared_ff or self.shared_ff % 128 == 0))
 
+    # prefill layers with shared experts: COX_SHARED_FUSE=1 runs the top-k combine
+    # in the shared down projection's epilogue (cox_shared_down_combine, bit-identical).
+    # Off by default: measured on C4 the fused epilogue is latency-bound on the k
+    # routed-row gathers (shared down + combine 3.51 ms fused vs 1.99 + 1.38 separate)
+    SHARED_FUSED_COMBINE = os.environ.get("COX_SHARED_FUSE", "0") == "1"
+
     def forward(self, x: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
         if x.dtype != torch.bfloat16 or x.dim() != 2 or x.shape[1] != self.d:
             raise ValueError(f"x must be bf16 [T, {self.d}]")
@@ -199,6 +208,11 @@ class MoELayer:
             return self.finish(b, b.shared_y, out)
         self.route(x, b)
         self.experts(b)
+        if self.shared_ff and self.SHARED_FUSED_COMBINE and self.k <= 8:
+            # shared expert K3, then its down projection with the combine in the epilogue
+            ops.grouped_swiglu(x, b.shared_offsets, [0], [self.wts.shared_w13], self.shared_ff, h=b.shared_h)
+            return ops.shared_down_combine(b.shared_h, b.shared_offsets, self.wts.shared_w2, b.y, b.dst, b.w,
+                                           out=b.out if out is None else out)
         sh = self.shared_expert(x, b)
         return self.finish(b, sh, out)
 
@@ -422,6 +436,14 @@ class MoELayer:
         ev[3].record()
         ops.grouped_down(b.h, b.offsets, self.groups, self.w2_list, self.d, y=b.y)
         ev[4].record()
+        if self.shared_ff and self.SHARED_FUSED_COMBINE and self.k <= 8:
+            ops.grouped_swiglu(x, b.shared_offsets, [0], [self.wts.shared_w13], self.shared_ff, h=b.shared_h)
+            ev[5].record()
+            ops.shared_down_combine(b.shared_h, b.shared_offsets, self.wts.shared_w2, b.y, b.dst, b.w, out=b.out)
+            ev[6].record()
+            torch.cuda.synchronize()
+            names = ["router", "permute", "swiglu_k3", "down_k4", "shared_k3", "shared_down_with_combine"]
+            return {n: ev[i].elapsed_time(ev[i + 1]) for i, n in enumerate(names)}
         sh = self.shared_expert(x, b)
         ev[5].record()
         ops.combine(b.y, b.dst, b.w, sh, out=b.out)

@@ -336,6 +336,35 @@ def combine(y_perm: torch.Tensor, dst: torch.Tensor, w: torch.Tensor, shared: to
     return out
 
 
+def shared_down_combine(h_shared: torch.Tensor, shared_offsets: torch.Tensor, w2_shared: torch.Tensor,
+                        y_perm: torch.Tensor, dst: torch.Tensor, w: torch.Tensor, out: torch.Tensor | None = None,
+                        stream=None):
+    """Shared-expert down projection with K5 fused into its epilogue:
+    out[t] = sum_j w[t,j] y_perm[dst[t,j]] + bf16(h_shared[t] W2s^T) — bit-identical
+    to grouped_down(shared) followed by combine(..., shared)."""
+    _need(h_shared, "h_shared", _BF16, 2)
+    _need(shared_offsets, "shared_offsets", torch.int32, 1)
+    _need(w2_shared, "w2_shared", _BF16, 2)
+    _need(y_perm, "y_perm", _BF16, 2)
+    _need(dst, "dst", torch.int32, 2)
+    _need(w, "w", torch.float32, 2)
+    T, k = dst.shape
+    d, ffs = w2_shared.shape
+    if h_shared.shape[1] != ffs or h_shared.shape[0] < T:
+        raise ValueError(f"h_shared must be [>= {T}, {ffs}]")
+    if y_perm.shape[1] != d:
+        raise ValueError(f"y_perm must have {d} columns")
+    if out is None:
+        out = torch.empty((T, d), dtype=_BF16, device=y_perm.device)
+    _need(out, "out", _BF16, 2)
+    L = _lib.lib()
+    _lib.check(L.cox_shared_down_combine(h_shared.data_ptr(), T, shared_offsets.data_ptr(), w2_shared.data_ptr(),
+                                         ffs, d, y_perm.data_ptr(), dst.data_ptr(), w.data_ptr(), k,
+                                         out.data_ptr(), _stream(stream)),
+               "cox_shared_down_combine")
+    return out
+
+
 def interleave_w13(w1: torch.Tensor, w3: torch.Tensor, out: torch.Tensor | None = None, stream=None):
     """[ff,d] x 2 -> K3 layout [2ff, d] (128-row gate/up blocks)."""
     _need(w1, "w1", _BF16, 2)
