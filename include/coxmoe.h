@@ -199,6 +199,21 @@ int cox_decode_moe(const void* x, int T, const void* wg, int E, int k, int mode,
                    void* h, void* y, void* h_shared, void* y_shared, int32_t* idx, float* w, void* out,
                    void* stream);
 
+/* The whole routed decode-step layer in ONE launch (T <= 256): the router
+ * runs in the kernel's prologue (warp 2 of CTA b routes tokens b, b + grid, ...
+ * in the canonical order of cox_router_topk, so idx/w are bit-identical) and
+ * publishes a per-expert histogram; every CTA then derives the expert
+ * segments, its copy of the stable permutation, and streams ONLY the touched
+ * experts' weights, as cox_small_expert_ffn_idx — without the router launch
+ * and its hand-off on the critical path.  Outputs idx/w [T, k] (router),
+ * counts [E], dst [T, k], offsets [E + 1] (as cox_permute), out [T, d].
+ * h [T*k, ff], y_perm [T*k, d] scratch; shared-expert operands optional.
+ * Replaces the decode-phase `expert_stage_parts` (costmodel.py:368). */
+int cox_decode_moe_routed(const void* x, int T, const void* wg, int E, int k, int mode, const void* const* w13,
+                          const void* const* w2, int d, int ff, const void* w13_shared, const void* w2_shared,
+                          int ff_shared, void* h, void* y_perm, void* h_shared, void* y_shared, int32_t* idx,
+                          float* w, int32_t* counts, int32_t* dst, int32_t* offsets, void* out, void* stream);
+
 /* K5 — weighted top-k combine back to token order (+ optional shared-expert
  * output, DeepSeek-V2):  out[t] = sum_j w[t,j] * y_perm[dst[t,j]] (+ shared[t]).
  * out/shared dtype = out_dtype (bf16 or fp32). */

@@ -33,6 +33,7 @@ EXPORTS = (
     "cox_ep_counts_put", "cox_ep_offsets", "cox_ep_dispatch", "cox_ep_combine", "cox_grouped_swiglu_ex",
     "cox_grouped_down_ex", "cox_router_topk_ex", "cox_permute_ex", "cox_grouped_swiglu_gather",
     "cox_small_expert_ffn", "cox_decode_moe", "cox_small_expert_ffn_idx", "cox_shared_down_combine",
+    "cox_decode_moe_routed",
 )
 
 _lock = threading.Lock()
@@ -79,6 +80,10 @@ def _declare(L):
     L.cox_grouped_down_ex.restype = c_int
     L.cox_grouped_down_ex.argtypes = [c_void_p, c_ll, c_void_p, c_int, c_void_p, c_void_p, c_int, c_int,
                                       c_void_p, c_int, c_void_p]
+    L.cox_decode_moe_routed.restype = c_int
+    L.cox_decode_moe_routed.argtypes = [c_void_p, c_int, c_void_p, c_int, c_int, c_int, c_void_p, c_void_p, c_int,
+                                        c_int, c_void_p, c_void_p, c_int, c_void_p, c_void_p, c_void_p, c_void_p,
+                                        c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]
     L.cox_shared_down_combine.restype = c_int
     L.cox_shared_down_combine.argtypes = [c_void_p, c_int, c_void_p, c_void_p, c_int, c_int, c_void_p, c_void_p,
                                           c_void_p, c_int, c_void_p, c_void_p]

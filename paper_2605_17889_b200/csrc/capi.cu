@@ -312,6 +312,34 @@ int cox_decode_moe(const void* x, int T, const void* wg, int E, int k, int mode,
   return cuda_status(rc, fn);
 }
 
+int cox_decode_moe_routed(const void* x, int T, const void* wg, int E, int k, int mode, const void* const* w13,
+                          const void* const* w2, int d, int ff, const void* w13_shared, const void* w2_shared,
+                          int ff_shared, void* h, void* y_perm, void* h_shared, void* y_shared, int32_t* idx,
+                          float* w, int32_t* counts, int32_t* dst, int32_t* offsets, void* out, void* stream) {
+  const char* fn = "cox_decode_moe_routed";
+  if (T < 1 || T > 256) return fail(COX_EINVAL, "%s: need 1 <= T <= 256 (T=%d)", fn, T);
+  if (E < 1 || E > 64 || k < 1 || k > 8 || k > E) return fail(COX_EINVAL, "%s: need 1 <= k <= min(E, 8), E <= 64", fn);
+  if (mode != COX_ROUTE_MIXTRAL && mode != COX_ROUTE_DEEPSEEK) return fail(COX_EINVAL, "%s: bad mode %d", fn, mode);
+  if (d <= 0 || d % 128 || d > 8192 || ff <= 0 || ff % 128)
+    return fail(COX_EINVAL, "%s: need d %% 128 == 0, d <= 8192, ff %% 128 == 0", fn);
+  if (!x || !wg || !h || !y_perm || !idx || !w || !counts || !dst || !out || !aligned16(x) || !aligned16(wg) ||
+      !aligned16(h) || !aligned16(y_perm) || !aligned16(out))
+    return fail(COX_EINVAL, "%s: null or unaligned operand", fn);
+  if (w13_shared && (ff_shared <= 0 || ff_shared % 128 || !w2_shared || !h_shared || !y_shared ||
+                     !aligned16(h_shared) || !aligned16(y_shared)))
+    return fail(COX_EINVAL, "%s: bad shared-expert operands", fn);
+  int32_t ids[64];
+  for (int e = 0; e < E; ++e) ids[e] = e;
+  if (int rc = check_groups(fn, E, ids, w13)) return rc;
+  if (int rc = check_groups(fn, E, ids, w2)) return rc;
+  cox::SmallDense dn{wg, E, mode, idx, w};
+  cox::SmallIdx fi{idx, counts, E, dst, offsets};
+  int rc = cox::launch_small_ffn(x, T, nullptr, nullptr, (long long)T * k, nullptr, E, ids, w13, w2, d, ff, h,
+                                 y_perm, w13_shared, w2_shared, ff_shared, h_shared, y_shared, dst, w, k, out, 3,
+                                 static_cast<cudaStream_t>(stream), &dn, &fi);
+  return cuda_status(rc, fn);
+}
+
 int cox_combine(const void* y_perm, const int32_t* dst, const float* w, int T, int k, int d, const void* shared_out,
                 void* out, int out_dtype, void* stream) {
   if (T < 0 || k < 1 || k > 8 || d <= 0 || d % 8) return fail(COX_EINVAL, "cox_combine: need 1<=k<=8, d%%8==0");

@@ -139,6 +139,13 @@ struct SmallParams {
   // and the producer of unit 0 of each group writes the group's dst entries
   // for the combine.
   int from_idx;
+  // route_in != 0 (with from_idx): no router kernel ran either.  Warp 2 of CTA
+  // b routes tokens b, b + grid, ... in the prologue (canonical order, as the
+  // dense path) into ridx/rw and the histogram counters[SG_HIST + e]; every CTA
+  // waits until all T tokens are routed, then proceeds as from_idx with those
+  // counts (CTA 0 copies them to counts_out).
+  int route_in;
+  int32_t* counts_out;     // [E] (route_in)
   const int32_t* rcounts;  // [E]
   int32_t* dst_out;        // [T, k]
   int32_t* offsets_out;    // [E + 1]
@@ -153,6 +160,7 @@ constexpr int SG_CB_BASE = 1 + SG_MAXG;  // counters[SG_CB_BASE + i]: down tiles
 constexpr int SG_COUNTERS = 256;
 constexpr int SG_ROUTED = SG_COUNTERS - 2;  // dense: tokens routed so far
 constexpr int SG_CTICKET = SG_COUNTERS - 3; // fused combine: work-item ticket
+constexpr int SG_HIST = 160;                // route_in: counters[SG_HIST + e] tokens routed to expert e (E <= 64)
 
 
 COX_DEV void mbar_spin_ge(const int* p, int want) {
@@ -220,10 +228,6 @@ __global__ void __launch_bounds__(SG_THREADS, 1) small_ffn_kernel(const __grid_c
   const int lane = threadIdx.x & 31;
   const int G = p.n_groups;
 
-  if (p.pdl) {
-    pdl_wait();  // routing (offsets, row_tokens, dst, w) of this step is complete from here on
-  }
-
   if (threadIdx.x == 0) {
     for (int s = 0; s < SG_STAGES; ++s) {
       mbar_init(smem_u32(&full[s]), 1);
@@ -240,14 +244,112 @@ __global__ void __launch_bounds__(SG_THREADS, 1) small_ffn_kernel(const __grid_c
     mbar_init(smem_u32(perm_ready), 1);
     fence_mbar_init();
   }
+  // canonical-order routing of tokens blockIdx.x, + gridDim.x, ... by one warp
+  // (dense decode: beside the weight stream; route_in: in the prologue)
+  auto route_tokens = [&](int* hist) {
+      const int d = p.d, E = p.E, kk = p.k;
+      for (int t = blockIdx.x; t < p.T; t += gridDim.x) {
+        const __nv_bfloat16* xr = p.xtok + (long long)t * d;
+        for (int e0 = 0; e0 < E; e0 += 8) {
+          float acc[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) acc[u] = 0.f;
+#pragma unroll 2
+          for (int sc = 8 * lane; sc < d; sc += 256) {
+            float xv[8];
+            bf16x8_to_f32(ld_nc_v4(xr + sc), xv);
+#pragma unroll
+            for (int u = 0; u < 8; u += 2) {
+              float wa[8], wb[8];
+              const int ea = min(e0 + u, E - 1), eb = min(e0 + u + 1, E - 1);
+              bf16x8_to_f32(ld_nc_v4(p.wg + (long long)ea * d + sc), wa);
+              bf16x8_to_f32(ld_nc_v4(p.wg + (long long)eb * d + sc), wb);
+#pragma unroll
+              for (int q = 0; q < 8; ++q) ffma2(acc[u], acc[u + 1], xv[q], wa[q], wb[q]);
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            float v = acc[u];
+#pragma unroll
+            for (int off = 16; off >= 1; off >>= 1) v = __fadd_rn(v, __shfl_xor_sync(0xffffffffu, v, off));
+            if (lane == 0 && e0 + u < E) s_route[e0 + u] = v != v ? -INFINITY : v;  // NaN ranks like -inf
+          }
+        }
+        __syncwarp();
+        warp_route_token(s_route, E, kk, p.mode, lane, reinterpret_cast<int*>(s_route + 264), s_route + 272,
+                         p.ridx + t * kk, p.rw + t * kk, hist);
+        if (lane == 0) {
+          __threadfence();
+          atomicAdd(p.counters + SG_ROUTED, 1);
+        }
+        __syncwarp();
+      }
+      };
+  // barrier init and the TMEM allocation do not depend on the routing: done
+  // while the router (the PDL primary) is still running
+  if (warp == 2) tmem_alloc<1>(smem_u32(tmem_slot), SG_TMEM_COLS);
+  if (p.pdl) {
+    pdl_wait();  // routing (offsets, row_tokens, dst, w) of this step is complete from here on
+  }
+  if (p.route_in) {
+    // prologue routing with the whole CTA: warp w computes the logits of
+    // experts 8w..8w+7 (each in the canonical order, so the split changes no
+    // bit), then warp 2 selects the top-k
+    const int d = p.d, E = p.E, kk = p.k;
+    for (int t = blockIdx.x; t < p.T; t += gridDim.x) {
+      const __nv_bfloat16* xr = p.xtok + (long long)t * d;
+      for (int e0 = 8 * warp; e0 < E; e0 += 8 * (SG_THREADS / 32)) {
+        float acc[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) acc[u] = 0.f;
+#pragma unroll 2
+        for (int sc = 8 * lane; sc < d; sc += 256) {
+          float xv[8];
+          bf16x8_to_f32(ld_nc_v4(xr + sc), xv);
+#pragma unroll
+          for (int u = 0; u < 8; u += 2) {
+            float wa[8], wb[8];
+            const int ea = min(e0 + u, E - 1), eb = min(e0 + u + 1, E - 1);
+            bf16x8_to_f32(ld_nc_v4(p.wg + (long long)ea * d + sc), wa);
+            bf16x8_to_f32(ld_nc_v4(p.wg + (long long)eb * d + sc), wb);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) ffma2(acc[u], acc[u + 1], xv[q], wa[q], wb[q]);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          float v = acc[u];
+#pragma unroll
+          for (int off = 16; off >= 1; off >>= 1) v = __fadd_rn(v, __shfl_xor_sync(0xffffffffu, v, off));
+          if (lane == 0 && e0 + u < E) s_route[e0 + u] = v != v ? -INFINITY : v;  // NaN ranks like -inf
+        }
+      }
+      __syncthreads();
+      if (warp == 2) {
+        warp_route_token(s_route, E, kk, p.mode, lane, reinterpret_cast<int*>(s_route + 264), s_route + 272,
+                         p.ridx + t * kk, p.rw + t * kk, p.counters + SG_HIST);
+        if (lane == 0) {
+          __threadfence();
+          atomicAdd(p.counters + SG_ROUTED, 1);
+        }
+      }
+      __syncthreads();
+    }
+  }
   if (warp == 0) {
     if (p.from_idx) {
       // expert offsets from the router's counts (exclusive scan, 8 experts per lane)
       int loc[8], sum = 0;
+      if (p.route_in) {
+        if (lane == 0) mbar_spin_ge(p.counters + SG_ROUTED, p.T);  // every CTA's tokens are routed
+        __syncwarp();
+      }
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
         const int e = lane * 8 + q;
-        loc[q] = e < p.E ? p.rcounts[e] : 0;
+        loc[q] = e < p.E ? (p.route_in ? __ldcg(p.counters + SG_HIST + e) : p.rcounts[e]) : 0;
+        if (p.route_in && blockIdx.x == 0 && e < p.E && p.counts_out) p.counts_out[e] = loc[q];
         sum += loc[q];
       }
       int incl = sum;
@@ -315,7 +417,6 @@ __global__ void __launch_bounds__(SG_THREADS, 1) small_ffn_kernel(const __grid_c
       s_misc[0] = nact;
     }
   }
-  if (warp == 2) tmem_alloc<1>(smem_u32(tmem_slot), SG_TMEM_COLS);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -568,7 +669,7 @@ __global__ void __launch_bounds__(SG_THREADS, 1) small_ffn_kernel(const __grid_c
 #pragma unroll
       for (int b = 0; b < PB; ++b) {
         const int ent = c0 + 32 * b + lane;
-        ev[b] = ent < nent ? __ldg(p.ridx + ent) : -1;
+        ev[b] = ent < nent ? (p.route_in ? __ldcg(p.ridx + ent) : __ldg(p.ridx + ent)) : -1;
       }
 #pragma unroll
       for (int b = 0; b < PB; ++b) {
@@ -598,46 +699,7 @@ __global__ void __launch_bounds__(SG_THREADS, 1) small_ffn_kernel(const __grid_c
     // butterfly; expert pairs share one FFMA2), top-k with ties to the lower
     // index, Mixtral / DeepSeek weights.  Only the combine needs the result, so
     // this runs beside the weight stream instead of before it.
-    if (p.dense) {
-      const int d = p.d, E = p.E, kk = p.k;
-      for (int t = blockIdx.x; t < p.T; t += gridDim.x) {
-        const __nv_bfloat16* xr = p.xtok + (long long)t * d;
-        for (int e0 = 0; e0 < E; e0 += 8) {
-          float acc[8];
-#pragma unroll
-          for (int u = 0; u < 8; ++u) acc[u] = 0.f;
-#pragma unroll 2
-          for (int sc = 8 * lane; sc < d; sc += 256) {
-            float xv[8];
-            bf16x8_to_f32(ld_nc_v4(xr + sc), xv);
-#pragma unroll
-            for (int u = 0; u < 8; u += 2) {
-              float wa[8], wb[8];
-              const int ea = min(e0 + u, E - 1), eb = min(e0 + u + 1, E - 1);
-              bf16x8_to_f32(ld_nc_v4(p.wg + (long long)ea * d + sc), wa);
-              bf16x8_to_f32(ld_nc_v4(p.wg + (long long)eb * d + sc), wb);
-#pragma unroll
-              for (int q = 0; q < 8; ++q) ffma2(acc[u], acc[u + 1], xv[q], wa[q], wb[q]);
-            }
-          }
-#pragma unroll
-          for (int u = 0; u < 8; ++u) {
-            float v = acc[u];
-#pragma unroll
-            for (int off = 16; off >= 1; off >>= 1) v = __fadd_rn(v, __shfl_xor_sync(0xffffffffu, v, off));
-            if (lane == 0 && e0 + u < E) s_route[e0 + u] = v != v ? -INFINITY : v;  // NaN ranks like -inf
-          }
-        }
-        __syncwarp();
-        warp_route_token(s_route, E, kk, p.mode, lane, reinterpret_cast<int*>(s_route + 264), s_route + 272,
-                         p.ridx + t * kk, p.rw + t * kk, nullptr);
-        if (lane == 0) {
-          __threadfence();
-          atomicAdd(p.counters + SG_ROUTED, 1);
-        }
-        __syncwarp();
-      }
-    }
+    if (p.dense) route_tokens(nullptr);
   } else if (warp >= 4) {
     // ------------------------------------------------------------ epilogue
     // Warp q reads TMEM lanes 32q..32q+31 (= weight rows of the unit), 32
@@ -757,7 +819,7 @@ __global__ void __launch_bounds__(SG_THREADS, 1) small_ffn_kernel(const __grid_c
         s_w[e] = p.rw[e];
       } else if (p.from_idx) {
         s_dst[e] = s_pos[e];
-        s_w[e] = p.cw[e];
+        s_w[e] = p.route_in ? __ldcg(p.cw + e) : p.cw[e];
       } else {
         s_dst[e] = __ldcg(p.cdst + e);
         s_w[e] = p.cw[e];
@@ -820,6 +882,8 @@ __global__ void __launch_bounds__(SG_THREADS, 1) small_ffn_kernel(const __grid_c
       for (int c = 0; c < n; ++c) p.counters[c] = 0;
       p.counters[SG_ROUTED] = 0;
       p.counters[SG_CTICKET] = 0;
+      if (p.route_in)
+        for (int e = 0; e < p.E; ++e) p.counters[SG_HIST + e] = 0;
       p.counters[SG_COUNTERS - 1] = 0;
     }
   }
@@ -886,6 +950,11 @@ int launch_small_ffn(const void* x, int T, const int32_t* row_tokens, const void
   std::lock_guard<std::mutex> lk(mu);
   memset(&m, 0, sizeof(m));
   int rc = 0;
+  // dense + fromidx: routed decode with the routing in the kernel's prologue
+  // (route_in); the groups, maps and combine are those of the from_idx path
+  const SmallDense* router = dense;
+  const bool route_in = dense != nullptr && fromidx != nullptr;
+  if (route_in) dense = nullptr;
   if (dense) {
     if ((rc = get_map(&m.act3[1], x, T, d, 16))) return rc;  // every group's SwiGLU B = x rows [0, T)
     if ((rc = get_map(&m.act4[0], h, rows_cap, ff, 16))) return rc;
@@ -956,6 +1025,16 @@ int launch_small_ffn(const void* x, int T, const int32_t* row_tokens, const void
     return e ? atoi(e) : 1;
   }();
   p.pdl = (!dense && pdl_env) ? 1 : 0;
+  p.route_in = route_in ? 1 : 0;
+  if (route_in) {
+    p.wg = static_cast<const __nv_bfloat16*>(router->wg);
+    p.xtok = static_cast<const __nv_bfloat16*>(x);
+    p.mode = router->mode;
+    p.ridx = router->idx;
+    p.rw = router->w;
+    p.cw = router->w;
+    p.counts_out = const_cast<int32_t*>(fromidx->counts);
+  }
   if (dense) {
     p.wg = static_cast<const __nv_bfloat16*>(dense->wg);
     p.xtok = static_cast<const __nv_bfloat16*>(x);

@@ -105,6 +105,8 @@ class MoELayer:
         perm = (1 if small_perm else 3) + 1 + (1 if self.tile_m > 1 else 0)
         if T is not None and self.uses_dense_decode(T):
             return 1  # router + all experts + shared + combine in one launch
+        if T is not None and self.uses_routed_one_launch(T):
+            return 1  # router in the prologue of the K3/K4/shared/combine launch
         if T is not None and self.uses_idx_decode(T):
             return 2  # router, then one launch for K3/K4/shared/combine reading the router's idx
         if T is not None and self.uses_small_path(T):
@@ -261,6 +263,10 @@ class MoELayer:
             return ops.decode_moe(x, self.wg_router, self.k, self.mode, self.w13_list, self.w2_list, dh, dy,
                                   b.idx, b.w, out, shared)
         if self.uses_idx_decode(T, out):
+            if self.uses_routed_one_launch(T):
+                shared = (self.wts.shared_w13, self.wts.shared_w2, b.shared_h, b.shared_y) if self.shared_ff else None
+                return ops.decode_moe_routed(x, self.wg_router, self.k, self.mode, self.w13_list, self.w2_list,
+                                             b.h, b.y, b.idx, b.w, b.counts, b.dst, b.offsets, out, shared)
             ops.router_topk(x, self.wg_router, self.k, self.mode, out=(b.idx, b.w, b.counts))
             return self._ffn_idx(x, b, out)
         self._route_small(x, b)
@@ -274,6 +280,14 @@ class MoELayer:
         return (self.SMALL_FROM_IDX and self.uses_small_path(T) and self.tile_m == 1 and self.SMALL_FUSE
                 and self.SMALL_GATHER and (out is None or out.dtype == torch.bfloat16)
                 and self.out_dtype == torch.bfloat16)
+
+    # routed decode in ONE launch: the router runs in the expert kernel's
+    # prologue (cox_decode_moe_routed); COX_DECODE_ROUTE_IN=0: router launch + FFN launch
+    DECODE_ROUTE_IN = os.environ.get("COX_DECODE_ROUTE_IN", "1") == "1"
+
+    def uses_routed_one_launch(self, T: int) -> bool:
+        return (self.DECODE_ROUTE_IN and self.uses_idx_decode(T) and self.wg_router.dtype == torch.bfloat16
+                and self.E <= 64 and self.d <= 8192)
 
     def _ffn_idx(self, x: torch.Tensor, b: StageBuffers, out: torch.Tensor):
         shared = (self.wts.shared_w13, self.wts.shared_w2, b.shared_h, b.shared_y) if self.shared_ff else None
@@ -402,12 +416,13 @@ class MoELayer:
         if x is None:
             raise ValueError("stage_times needs the step's input")
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(7)]
-        if self.uses_dense_decode(x.shape[0]):
+        if self.uses_dense_decode(x.shape[0]) or self.uses_routed_one_launch(x.shape[0]):
             ev[0].record()
             self._forward_small(x, b, b.out)
             ev[1].record()
             torch.cuda.synchronize()
-            return {"decode_moe_one_launch": ev[0].elapsed_time(ev[1])}
+            name = "decode_moe_one_launch" if self.uses_dense_decode(x.shape[0]) else "decode_moe_routed_one_launch"
+            return {name: ev[0].elapsed_time(ev[1])}
         ev[0].record()
         ops.router_topk(x, self.wg_router, self.k, self.mode, out=(b.idx, b.w, b.counts))
         ev[1].record()

@@ -316,6 +316,46 @@ def decode_moe(x: torch.Tensor, wg: torch.Tensor, k: int, mode: int, w13: Sequen
     return out
 
 
+def decode_moe_routed(x: torch.Tensor, wg: torch.Tensor, k: int, mode: int, w13: Sequence[torch.Tensor],
+                      w2: Sequence[torch.Tensor], h: torch.Tensor, y: torch.Tensor, idx: torch.Tensor,
+                      w: torch.Tensor, counts: torch.Tensor, dst: torch.Tensor, offsets: torch.Tensor,
+                      out: torch.Tensor, shared=None, stream=None):
+    """Whole routed decode-step layer in one launch (T <= 256): in-kernel router
+    (bit-identical idx/w), then only the touched experts + shared experts +
+    combine.  h [>= T*k, ff], y [>= T*k, d] scratch; writes idx/w/counts/dst/offsets
+    like router_topk + permute; shared = (w13_shared, w2_shared, h_shared, y_shared)."""
+    _need(x, "x", _BF16, 2)
+    _need(wg, "wg", _BF16, 2)
+    T, d = x.shape
+    E = wg.shape[0]
+    ff = h.shape[1]
+    for t, n in ((h, "h"), (y, "y"), (out, "out")):
+        _need(t, n, _BF16, 2)
+    for t, n in ((idx, "idx"), (dst, "dst")):
+        _need(t, n, torch.int32, 2)
+    _need(w, "w", torch.float32, 2)
+    _need(counts, "counts", torch.int32, 1)
+    _need(offsets, "offsets", torch.int32, 1)
+    if (wg.shape[1] != d or h.shape[0] < T * k or y.shape[0] < T * k or y.shape[1] != d
+            or tuple(out.shape) != (T, d) or tuple(idx.shape) != (T, k) or tuple(w.shape) != (T, k)
+            or tuple(dst.shape) != (T, k) or counts.shape[0] < E or offsets.shape[0] < E + 1
+            or len(w13) != E or len(w2) != E):
+        raise ValueError("decode_moe_routed: inconsistent shapes")
+    sw13 = sw2 = sh = sy = None
+    ffs = 0
+    if shared is not None:
+        sw13, sw2, sh, sy = shared
+        ffs = sh.shape[1]
+    ptr = lambda t: t.data_ptr() if t is not None else None  # noqa: E731
+    L = _lib.lib()
+    _lib.check(L.cox_decode_moe_routed(x.data_ptr(), T, wg.data_ptr(), E, k, mode, _ptrs(w13), _ptrs(w2), d, ff,
+                                       ptr(sw13), ptr(sw2), ffs, h.data_ptr(), y.data_ptr(), ptr(sh), ptr(sy),
+                                       idx.data_ptr(), w.data_ptr(), counts.data_ptr(), dst.data_ptr(),
+                                       offsets.data_ptr(), out.data_ptr(), _stream(stream)),
+               "cox_decode_moe_routed")
+    return out
+
+
 def combine(y_perm: torch.Tensor, dst: torch.Tensor, w: torch.Tensor, shared: torch.Tensor | None = None,
             out: torch.Tensor | None = None, out_dtype=_BF16, stream=None):
     """K5: out[t] = sum_j w[t,j] y_perm[dst[t,j]] (+ shared[t])."""

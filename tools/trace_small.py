@@ -6,7 +6,7 @@ it) into paper_2605_17889_b200/build/trace/, runs one C4 decode step through it
 and prints where the time goes: start-up, per-pass unit durations, idle gaps
 and the tail.  Debug tool only; the product library is untouched.
 
-    python tools/trace_small.py            # on the GPU box (gpurun)
+    python tools/trace_small.py [C4D|C2D]  # on the GPU box (gpurun)
 """
 from __future__ import annotations
 
@@ -21,7 +21,7 @@ ROOT = Path(__file__).resolve().parents[1]
 sys.path.insert(0, str(ROOT))
 TRACE_DIR = ROOT / "paper_2605_17889_b200" / "build" / "trace"
 LIB = TRACE_DIR / "libcoxmoe_trace.so"
-MAXU = 96  # units recorded per CTA
+MAXU = 96  # units recorded per CTA (C2D: ~14 per CTA)
 
 
 def make_traced_sources() -> Path:
@@ -39,6 +39,19 @@ __device__ __forceinline__ unsigned long long gtimer() {{
   return t;
 }}
 """, 1)
+    # kernel entry stamp (before barrier init / PDL wait / routing / group table)
+    ent = "  const int warp = threadIdx.x >> 5;\n  const int lane = threadIdx.x & 31;\n  const int G = p.n_groups;\n"
+    assert ent in s
+    s = s.replace(ent, ent + f"  if (threadIdx.x == 0) g_trace[(blockIdx.x * {MAXU + 2} + {MAXU}) * 3 + 2] = gtimer();\n", 1)
+    # route_in prologue: after this CTA's routing, after the grid-wide wait (row MAXU - 1)
+    a1 = "      __syncthreads();\n    }\n  }\n  if (warp == 0) {\n    if (p.from_idx) {\n"
+    if a1 in s:
+        s = s.replace(a1, "      __syncthreads();\n    }\n  }\n"
+                      f"  if (threadIdx.x == 0) g_trace[(blockIdx.x * {MAXU + 2} + {MAXU - 1}) * 3] = gtimer();\n"
+                      "  if (warp == 0) {\n    if (p.from_idx) {\n", 1)
+    a2 = "        if (lane == 0) mbar_spin_ge(p.counters + SG_ROUTED, p.T);  // every CTA's tokens are routed\n"
+    if a2 in s:
+        s = s.replace(a2, a2 + f"        if (lane == 0) g_trace[(blockIdx.x * {MAXU + 2} + {MAXU - 1}) * 3 + 1] = gtimer();\n", 1)
     # kernel start / end stamps
     s = s.replace("  const uint32_t tmem_base = *tmem_slot;\n",
                   f"  const uint32_t tmem_base = *tmem_slot;\n"
@@ -88,16 +101,17 @@ def build_traced():
     build.build(force=True, out=LIB, csrc=src)
 
 
-def run():
+def run(cfg: str = "C4D"):
     os.environ["COXMOE_LIB"] = str(LIB)
     import torch
     from paper_2605_17889_b200.layer import MoELayer
     from paper_2605_17889_b200.synthetic import make_layer_weights, make_tokens
     from paper_2605_17889_b200 import _lib
-    T, d, ff, E, k, sff = 64, 2048, 1408, 64, 6, 2816
+    T, d, ff, E, k, sff, mode = {"C4D": (64, 2048, 1408, 64, 6, 2816, "deepseek"),
+                                 "C2D": (64, 4096, 14336, 8, 2, 0, "mixtral")}[cfg]
     wts = make_layer_weights(E, d, ff, seed=0, device="cuda", shared_ff=sff)
     x = make_tokens(T, d, seed=1, device="cuda")
-    layer = MoELayer(wts, k, "deepseek")
+    layer = MoELayer(wts, k, mode)
     for _ in range(5):
         layer(x)
     torch.cuda.synchronize()
@@ -105,14 +119,37 @@ def run():
     L.cox_trace_clear()
     layer(x)
     torch.cuda.synchronize()
+    if os.environ.get("TRACE_GRAPH") == "1":
+        # steady state under graph replay: the traced buffers keep the LAST replay's stamps
+        replay, _ = layer.capture(x)
+        for _ in range(3):
+            replay()
+        torch.cuda.synchronize()
+        L.cox_trace_clear()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        replay()
+        ev0.record()
+        replay()
+        ev1.record()
+        torch.cuda.synchronize()
+        print(f"[{cfg}] graph replay step {ev0.elapsed_time(ev1) * 1e3:.1f} us")
     n = 160 * (MAXU + 2) * 3
     buf = (ctypes.c_ulonglong * n)()
     assert L.cox_trace_dump(buf) == 0
     import numpy as np
     a = np.frombuffer(buf, dtype=np.uint64).reshape(160, MAXU + 2, 3).astype(np.int64)
     nb = 148
-    starts, ends = a[:nb, MAXU, 0], a[:nb, MAXU, 1]
+    starts, ends, entry = a[:nb, MAXU, 0], a[:nb, MAXU, 1], a[:nb, MAXU, 2]
     t0 = starts.min()
+    r1, r2 = a[:nb, MAXU - 1, 0], a[:nb, MAXU - 1, 1]
+    if r2.max() > 0:
+        print(f"[{cfg}] route_in: own routing done median {np.median(r1 - entry) / 1e3:.1f} us after entry "
+              f"(max {(r1.max() - entry.min()) / 1e3:.1f} from first entry); grid-wide wait passed median "
+              f"{np.median(r2 - entry) / 1e3:.1f} us after entry")
+        a[:nb, MAXU - 1] = 0
+    print(f"[{cfg}] kernel entry: first {(entry.min() - t0) / 1e3:.1f} us, last {(entry.max() - t0) / 1e3:.1f} us "
+          f"(relative to the first CTA past the prologue); prologue per CTA median "
+          f"{np.median(starts - entry) / 1e3:.1f} us")
     print(f"CTA start spread {(starts.max() - t0) / 1e3:.1f} us; kernel body {(ends.max() - t0) / 1e3:.1f} us; "
           f"first CTA end {(ends.min() - t0) / 1e3:.1f} us")
     cend = a[:nb, MAXU + 1, 0]
@@ -154,4 +191,5 @@ def run():
 if __name__ == "__main__":
     if "--run-only" not in sys.argv:
         build_traced()
-    run()
+    for c in [a for a in sys.argv[1:] if not a.startswith("--")] or ["C4D"]:
+        run(c)
