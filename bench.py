@@ -333,23 +333,26 @@ def main():
         want = os.environ.get("COX_EP", "auto")  # auto | fused | nccl
         layer = None
         if want in ("auto", "fused"):
-            # probe: the fused peer-memory path must agree bit-for-bit with the NCCL path
+            # probe: the fused peer-memory path must agree bit-for-bit with the NCCL path;
+            # every rank reaches the same all_reduce whether or not its probe raised
+            px = x[: min(T, 8192)].contiguous()
+            a = EPMoELayer(wts, k, mode, dist.group.WORLD)(px).clone()
+            why = "probe mismatch"
             try:
-                px = x[: min(T, 8192)].contiguous()
-                a = EPMoELayer(wts, k, mode, dist.group.WORLD)(px).clone()
                 probe = FusedEPMoELayer(wts, k, mode, dist.group.WORLD)
                 b = probe(px).clone()
                 probe.check()
                 ok = torch.tensor([int(torch.equal(a, b))], device=dev)
-                dist.all_reduce(ok, op=dist.ReduceOp.MIN)
                 del probe
-                if ok.item() == 1:
-                    layer = FusedEPMoELayer(wts, k, mode, dist.group.WORLD)
-                    ep_used = "fused NVLink peer-memory dispatch/combine (probe == NCCL path)"
-                else:
-                    ep_used = "nccl all_to_all (fused probe mismatch)"
             except Exception as exc:  # noqa: BLE001
-                ep_used = f"nccl all_to_all (fused unavailable: {type(exc).__name__})"
+                ok = torch.tensor([0], device=dev)
+                why = f"unavailable: {type(exc).__name__}"
+            dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+            if ok.item() == 1:
+                layer = FusedEPMoELayer(wts, k, mode, dist.group.WORLD)
+                ep_used = "fused NVLink peer-memory dispatch/combine (probe == NCCL path)"
+            else:
+                ep_used = f"nccl all_to_all (fused {why})"
         if layer is None:
             layer = EPMoELayer(wts, k, mode, dist.group.WORLD)
             ep_used = ep_used or "nccl all_to_all"
