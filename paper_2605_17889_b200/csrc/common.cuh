@@ -97,6 +97,11 @@ COX_DEV void mbar_arrive_cluster_relaxed(uint32_t cluster_bar) {
 }
 
 // ---------------------------------------------------------------- TMA
+// release-add on a global counter: orders this thread's earlier writes (and,
+// by cumulativity, those of threads it synchronised with) before the add
+COX_DEV void red_release_add(int* p, int v) {
+  asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 COX_DEV void prefetch_l2(const void* p) {
   asm volatile("prefetch.global.L2 [%0];" ::"l"(reinterpret_cast<uint64_t>(p)));
 }
@@ -131,6 +136,22 @@ COX_DEV void tma_load_2d(uint32_t dst, const void* map, uint32_t bar, int32_t c0
       " [%0], [%1, {%3, %4}], [%2];" ::"r"(dst),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1)
       : "memory");
+}
+
+// same with an L2 cache policy (createpolicy): streamed-once operands use
+// evict_first so they do not push reusable lines (activations, router
+// weights, counters, code) out of L2
+COX_DEV void tma_load_2d_hint(uint32_t dst, const void* map, uint32_t bar, int32_t c0, int32_t c1, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1), "l"(pol)
+      : "memory");
+}
+COX_DEV uint64_t l2_policy_evict_first() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
 }
 
 // ---------------------------------------------------------------- tcgen05

@@ -51,19 +51,30 @@ COX_DEV void warp_route_token(float* lg, int E, int k, int mode, int lane, int* 
     for (int e = lane; e < E; e += 32) lg[e] = expf(__fsub_rn(lg[e], m0));
     __syncwarp();
   }
+  const float m = s_selv[0];
+  float ssum = 0.0f;
   if (lane == 0) {
-    const float m = s_selv[0];
-    float ssum = 0.0f;
     if (mode == 0) {
       for (int j = 0; j < k; ++j) ssum = __fadd_rn(ssum, expf(__fsub_rn(s_selv[j], m)));
     } else {
-      for (int e = 0; e < E; ++e) ssum = __fadd_rn(ssum, lg[e]);  // ascending e, as the oracle
+      // ascending e, as the oracle; eight shared loads in flight per step of the add chain
+      int e = 0;
+      for (; e + 8 <= E; e += 8) {
+        float v[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) v[q] = lg[e + q];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) ssum = __fadd_rn(ssum, v[q]);
+      }
+      for (; e < E; ++e) ssum = __fadd_rn(ssum, lg[e]);
     }
-    for (int j = 0; j < k; ++j) {
-      idx[j] = s_sel[j];
-      w[j] = __fdiv_rn(expf(__fsub_rn(s_selv[j], m)), ssum);
-      if (hist) atomicAdd(&hist[s_sel[j]], 1);
-    }
+  }
+  ssum = __shfl_sync(0xffffffffu, ssum, 0);
+  if (lane < k) {  // one selected expert per lane: the same expression per weight as a serial loop
+    const int e = s_sel[lane];
+    idx[lane] = e;
+    w[lane] = __fdiv_rn(expf(__fsub_rn(s_selv[lane], m)), ssum);
+    if (hist) atomicAdd(&hist[e], 1);
   }
   __syncwarp();
 }

@@ -279,10 +279,7 @@ __global__ void __launch_bounds__(SG_THREADS, 1) small_ffn_kernel(const __grid_c
         __syncwarp();
         warp_route_token(s_route, E, kk, p.mode, lane, reinterpret_cast<int*>(s_route + 264), s_route + 272,
                          p.ridx + t * kk, p.rw + t * kk, hist);
-        if (lane == 0) {
-          __threadfence();
-          atomicAdd(p.counters + SG_ROUTED, 1);
-        }
+        if (lane == 0) red_release_add(p.counters + SG_ROUTED, 1);  // after idx / w / histogram
         __syncwarp();
       }
       };
@@ -329,10 +326,7 @@ __global__ void __launch_bounds__(SG_THREADS, 1) small_ffn_kernel(const __grid_c
       if (warp == 2) {
         warp_route_token(s_route, E, kk, p.mode, lane, reinterpret_cast<int*>(s_route + 264), s_route + 272,
                          p.ridx + t * kk, p.rw + t * kk, p.counters + SG_HIST);
-        if (lane == 0) {
-          __threadfence();
-          atomicAdd(p.counters + SG_ROUTED, 1);
-        }
+        if (lane == 0) red_release_add(p.counters + SG_ROUTED, 1);  // after idx / w / histogram
       }
       __syncthreads();
     }
@@ -484,6 +478,9 @@ __global__ void __launch_bounds__(SG_THREADS, 1) small_ffn_kernel(const __grid_c
     uint32_t stage = 0, phase = 0;
     int si = 0;
     bool perm_seen = false;
+    // expert weights are read once per step: evict_first keeps x, h, y, the
+    // router weight and the counters in L2
+    const uint64_t wpol = l2_policy_evict_first();
     for (;;) {
       int t = lane == 0 ? fetch(si, true) : 0;
       t = __shfl_sync(0xffffffffu, t, 0);
@@ -540,8 +537,8 @@ __global__ void __launch_bounds__(SG_THREADS, 1) small_ffn_kernel(const __grid_c
               mbar_arrive_expect_tx(fb, na * (SG_A_ATOM + nb * 2048u));
               const uint32_t a_dst = smem_u32(sA + stage * SG_A_BYTES);
               for (int a = 0; a < na; ++a) {
-                tma_load_2d(a_dst + a * SG_A_ATOM, wmap, fb, kb * SG_BK + a * SG_ATOM, wr0);
-                tma_load_2d(a_dst + a * SG_A_ATOM + SG_A_ATOM / 2, wmap, fb, kb * SG_BK + a * SG_ATOM, wr1);
+                tma_load_2d_hint(a_dst + a * SG_A_ATOM, wmap, fb, kb * SG_BK + a * SG_ATOM, wr0, wpol);
+                tma_load_2d_hint(a_dst + a * SG_A_ATOM + SG_A_ATOM / 2, wmap, fb, kb * SG_BK + a * SG_ATOM, wr1, wpol);
               }
               if (++stage == SG_STAGES) {
                 stage = 0;
@@ -583,8 +580,8 @@ __global__ void __launch_bounds__(SG_THREADS, 1) small_ffn_kernel(const __grid_c
 #pragma unroll
             for (int a = 0; a < KA; ++a) {
               if (a >= na) break;
-              tma_load_2d(a_dst + a * SG_A_ATOM, wmap, fb, kb * SG_BK + a * SG_ATOM, wr0);
-              tma_load_2d(a_dst + a * SG_A_ATOM + SG_A_ATOM / 2, wmap, fb, kb * SG_BK + a * SG_ATOM, wr1);
+              tma_load_2d_hint(a_dst + a * SG_A_ATOM, wmap, fb, kb * SG_BK + a * SG_ATOM, wr0, wpol);
+              tma_load_2d_hint(a_dst + a * SG_A_ATOM + SG_A_ATOM / 2, wmap, fb, kb * SG_BK + a * SG_ATOM, wr1, wpol);
             }
             if (!gat) {
 #pragma unroll

@@ -52,6 +52,17 @@ __device__ __forceinline__ unsigned long long gtimer() {{
     a2 = "        if (lane == 0) mbar_spin_ge(p.counters + SG_ROUTED, p.T);  // every CTA's tokens are routed\n"
     if a2 in s:
         s = s.replace(a2, a2 + f"        if (lane == 0) g_trace[(blockIdx.x * {MAXU + 2} + {MAXU - 1}) * 3 + 1] = gtimer();\n", 1)
+    # route_in: after the logits of this CTA's first token, after its top-k (row MAXU - 2)
+    a3 = "      __syncthreads();\n      if (warp == 2) {\n        warp_route_token("
+    if a3 in s:
+        s = s.replace(a3, "      __syncthreads();\n"
+                      f"      if (threadIdx.x == 0 && t == (int)blockIdx.x) g_trace[(blockIdx.x * {MAXU + 2} + {MAXU - 2}) * 3] = gtimer();\n"
+                      "      if (warp == 2) {\n        warp_route_token(", 1)
+    a4 = "        if (lane == 0) red_release_add(p.counters + SG_ROUTED, 1);  // after idx / w / histogram\n      }\n"
+    if a4 in s:
+        s = s.replace(a4, "        if (lane == 0) red_release_add(p.counters + SG_ROUTED, 1);  // after idx / w / histogram\n"
+                      f"        if (lane == 0 && t == (int)blockIdx.x) g_trace[(blockIdx.x * {MAXU + 2} + {MAXU - 2}) * 3 + 1] = gtimer();\n"
+                      "      }\n", 1)
     # kernel start / end stamps
     s = s.replace("  const uint32_t tmem_base = *tmem_slot;\n",
                   f"  const uint32_t tmem_base = *tmem_slot;\n"
@@ -141,6 +152,13 @@ def run(cfg: str = "C4D"):
     nb = 148
     starts, ends, entry = a[:nb, MAXU, 0], a[:nb, MAXU, 1], a[:nb, MAXU, 2]
     t0 = starts.min()
+    l1, l2 = a[:nb, MAXU - 2, 0], a[:nb, MAXU - 2, 1]
+    if l2.max() > 0:
+        m = l2 > 0
+        print(f"[{cfg}] route_in first token: logits done median {np.median((l1 - entry)[m]) / 1e3:.1f} us after "
+              f"entry (max {np.max((l1 - entry)[m]) / 1e3:.1f}), top-k + publish done median "
+              f"{np.median((l2 - entry)[m]) / 1e3:.1f} (max {np.max((l2 - entry)[m]) / 1e3:.1f})")
+        a[:nb, MAXU - 2] = 0
     r1, r2 = a[:nb, MAXU - 1, 0], a[:nb, MAXU - 1, 1]
     if r2.max() > 0:
         print(f"[{cfg}] route_in: own routing done median {np.median(r1 - entry) / 1e3:.1f} us after entry "
