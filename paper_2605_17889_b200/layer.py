@@ -282,8 +282,12 @@ class MoELayer:
                 and self.out_dtype == torch.bfloat16)
 
     # routed decode in ONE launch: the router runs in the expert kernel's
-    # prologue (cox_decode_moe_routed); COX_DECODE_ROUTE_IN=0: router launch + FFN launch
-    DECODE_ROUTE_IN = os.environ.get("COX_DECODE_ROUTE_IN", "1") == "1"
+    # prologue (cox_decode_moe_routed), COX_DECODE_ROUTE_IN=1.  Off by default:
+    # measured on C4 (tools/sweep_decode.py, profiles/r01/sweep_decode_c4_v2.txt)
+    # the in-kernel routing of a token (~10 us on one CTA) is slower than the
+    # router kernel + PDL hand-off at small T (T=1: 82 vs 56 us) and within
+    # noise at T=64..256; C2D (E=8) gains ~1%
+    DECODE_ROUTE_IN = os.environ.get("COX_DECODE_ROUTE_IN", "0") == "1"
 
     def uses_routed_one_launch(self, T: int) -> bool:
         return (self.DECODE_ROUTE_IN and self.uses_idx_decode(T) and self.wg_router.dtype == torch.bfloat16

@@ -18,6 +18,7 @@ DEV = "cuda"
 def _pair(E, d, ff, k, mode, sff, seed=0):
     wts = make_layer_weights(E, d, ff, seed=seed, device=DEV, shared_ff=sff, keep_split=True)
     a = MoELayer(wts, k, mode)
+    a.DECODE_ROUTE_IN = True
     b = MoELayer(wts, k, mode)
     b.DECODE_ROUTE_IN = False
     b.DENSE_T_MAX = 0

@@ -1,6 +1,8 @@
-"""Decode-step latency vs batch size (C4 DeepSeek-V2-Lite layer), dense single-
-launch decode (cox_decode_moe) vs the routed path (router + permute + weight-
-streaming FFN launch), CUDA-graph replay, CUDA events, median of 200 steps.
+"""Decode-step latency vs batch size (C4 DeepSeek-V2-Lite layer): dense single-
+launch decode (cox_decode_moe, every expert over all tokens), routed single
+launch (cox_decode_moe_routed, router in the prologue) and routed two launches
+(router kernel + cox_small_expert_ffn_idx); CUDA-graph replay, CUDA events,
+median of 200 steps.
 
     python tools/sweep_decode.py        # on the GPU box
 """
@@ -38,14 +40,18 @@ def time_layer(layer, T, d):
 def main():
     d, ff, E, k, sff = 2048, 1408, 64, 6, 2816
     wts = make_layer_weights(E, d, ff, seed=0, device="cuda", shared_ff=sff)
-    for T in (1, 4, 8, 16, 24, 32, 48, 64):
+    for T in (1, 4, 8, 16, 24, 32, 48, 64, 128, 256):
         row = []
-        for dense in (True, False):
+        for variant in ("dense", "routed1", "routed2"):
             layer = MoELayer(wts, k, "deepseek")
-            if not dense:
-                layer.DENSE_T_MAX = 0
-            row.append(time_layer(layer, T, d))
-        print(f"T={T:3d}: dense {row[0]:7.1f} us   routed {row[1]:7.1f} us", flush=True)
+            if variant == "dense" and not layer.uses_small_path(T):
+                row.append(float("nan"))
+                continue
+            layer.DENSE_T_MAX = 256 if variant == "dense" else 0
+            layer.DECODE_ROUTE_IN = variant == "routed1"
+            row.append(time_layer(layer, T, d) if variant != "dense" or T <= 64 else float("nan"))
+        print(f"T={T:3d}: dense {row[0]:7.1f} us   routed, one launch {row[1]:7.1f} us   "
+              f"routed, router launch + FFN {row[2]:7.1f} us", flush=True)
 
 
 if __name__ == "__main__":
