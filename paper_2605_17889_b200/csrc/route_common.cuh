@@ -15,34 +15,44 @@ namespace cox {
 // mode 1); s_sel / s_selv: this warp's [8] shared scratch; idx / w: the
 // token's k outputs; hist: optional shared/global histogram (+1 per selected
 // expert).  E <= 256, k <= 8.
+// Order-preserving map of a float to an unsigned key (larger float -> larger
+// key; -inf -> 0x007fffff > 0 = "no candidate"; -0 and +0 share a key, so they
+// tie as under float comparison).  Logits are NaN-free here (callers map NaN
+// to -inf).
+COX_DEV uint32_t route_key(float v) {
+  const uint32_t b = v == 0.0f ? 0u : __float_as_uint(v);
+  return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+
 COX_DEV void warp_route_token(float* lg, int E, int k, int mode, int lane, int* s_sel, float* s_selv,
                               int32_t* idx, float* w, int* hist) {
-  uint32_t taken = 0;  // bit i: expert lane + 32 i already selected
-  for (int j = 0; j < k; ++j) {
-    float bv = 0.0f;
-    int bi = -1;
-    for (int i = 0; lane + 32 * i < E; ++i) {
-      const int e = lane + 32 * i;
-      if (taken & (1u << i)) continue;
-      const float v = lg[e];
-      if (bi < 0 || v > bv) {
-        bv = v;
-        bi = e;
-      }
-    }
+  // the lane's logits (experts lane + 32 i) in registers, selected ones knocked
+  // out; each round: the lane's best (lowest index among equals), then two
+  // warp-wide redux steps: max key, then min index among the lanes holding it
+  // (= the old shuffle butterfly's choice: largest value, ties -> lower index)
+  constexpr int NI = 8;  // E <= 256
+  uint32_t key[NI];
 #pragma unroll
-    for (int off = 16; off >= 1; off >>= 1) {
-      const float ov = __shfl_xor_sync(0xffffffffu, bv, off);
-      const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
-      if (oi >= 0 && (bi < 0 || ov > bv || (ov == bv && oi < bi))) {
-        bv = ov;
-        bi = oi;
+  for (int i = 0; i < NI; ++i) key[i] = (lane + 32 * i < E) ? route_key(lg[lane + 32 * i]) : 0u;
+  for (int j = 0; j < k; ++j) {
+    uint32_t bk = 0;
+    int bi = 0x7fffffff;
+#pragma unroll
+    for (int i = 0; i < NI; ++i)
+      if (key[i] > bk) {
+        bk = key[i];
+        bi = lane + 32 * i;
       }
+    const uint32_t mk = __reduce_max_sync(0xffffffffu, bk);
+    const int e = (int)__reduce_min_sync(0xffffffffu, (uint32_t)(bk == mk ? bi : 0x7fffffff));
+    if ((e & 31) == lane) {
+#pragma unroll
+      for (int i = 0; i < NI; ++i)
+        if (i == (e >> 5)) key[i] = 0;
     }
-    if ((bi & 31) == lane) taken |= 1u << (bi >> 5);
     if (lane == 0) {
-      s_sel[j] = bi;
-      s_selv[j] = bv;
+      s_sel[j] = e;
+      s_selv[j] = lg[e];
     }
   }
   __syncwarp();

@@ -72,3 +72,29 @@ def test_routed_one_launch_vs_oracle_and_replays(mode):
         got = f(out)
         err = np.linalg.norm(got - ref["out"]) / np.linalg.norm(ref["out"])
         assert err < 1e-2, err
+
+
+@pytest.mark.parametrize("route_in", [True, False])
+def test_decode_routing_exact_ties_vs_oracle(route_in):
+    """Duplicated router rows give exactly tied logits: the lower expert index
+    wins, in the decode router kernel and the in-kernel (prologue) router."""
+    from oracle import oracle as O
+    T, d, ff, E, k = 64, 256, 128, 64, 6
+    wts = make_layer_weights(E, d, ff, seed=7, device=DEV, keep_split=True)
+    wg = wts.wg.clone()
+    wg[1::2] = wg[0::2]  # experts 2i and 2i+1 tie on every token
+    wg[60:] = 0.0        # logits exactly +0
+    wts.wg = wg
+    layer = MoELayer(wts, k, "deepseek")
+    layer.DECODE_ROUTE_IN = route_in
+    layer.DENSE_T_MAX = 0
+    x = make_tokens(T, d, seed=8, device=DEV)
+    out = layer(x)
+    torch.cuda.synchronize()
+    f = lambda t: t.float().cpu().numpy()  # noqa: E731
+    ref = O.moe_layer(f(x), f(wg), f(wts.w1), f(wts.w3), f(wts.w2), k, 1)
+    b = layer.buffers(T, DEV)
+    assert np.array_equal(b.idx.cpu().numpy(), ref["idx"])
+    assert np.array_equal(b.w.cpu().numpy(), ref["w"]) or np.allclose(b.w.cpu().numpy(), ref["w"], rtol=1e-6)
+    err = np.linalg.norm(f(out) - ref["out"]) / np.linalg.norm(ref["out"])
+    assert err < 1e-2

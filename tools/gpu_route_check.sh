@@ -1,4 +1,5 @@
-# router changes: parity tests + decode trace + C4D/C2D bench (run under gpurun)
-timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_router_tc.py tests/test_gpu_small.py tests/test_gpu_decode_routed.py tests/test_gpu_robust.py -q -x 2>&1 | tail -2
-TRACE_GRAPH=1 timeout 300 python tools/trace_small.py --run-only C4D C2D 2>&1 | grep "^\["
-for c in C4D C2D; do timeout 300 python bench.py --config $c --no-cpu-baseline --no-e2e 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$c', round(d['ms_per_step']*1e3,1), 'us', round(d['roofline']['frac'],3))"; done
+# router changes: probe + parity tests + decode sweep points (run under gpurun)
+./tools/probes/route_probe
+timeout 1200 python -m pytest tests -m gpu -q -x 2>&1 | tail -2
+for c in C4D C2D; do for r in 0 1; do COX_DECODE_ROUTE_IN=$r timeout 300 python bench.py --config $c --no-cpu-baseline --no-e2e 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$c route_in=$r', round(d['ms_per_step']*1e3,1), 'us', round(d['roofline']['frac'],3), d['stages_ms'])"; done; done
+timeout 300 python bench.py --no-cpu-baseline --no-e2e --steps 10 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('C2', round(d['value']/1e6,4), d['stages_ms'])"
