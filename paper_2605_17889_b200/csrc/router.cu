@@ -404,6 +404,118 @@ int launch_router_bf16w(const void* x, const void* wg, int T, int d, int E, int 
   return cudaGetLastError() == cudaSuccess ? 0 : -2;
 }
 
+// ---------------------------------------------------------------- decode router
+// T <= 64 tokens: block (t, sp) computes the logits of token t for experts
+// [sp E/S, (sp + 1) E/S), one expert pair per warp and pass (the canonical
+// per-expert order of router_topk_kernel, so the same bits), into a global
+// scratch row; the last of the S blocks of token t (acq_rel ticket) selects
+// its top-k; the block that completes the last token writes the per-expert
+// counts from idx (no memset node, no count atomics) and resets the tickets.
+constexpr int RD_TMAX = 64;
+constexpr int RD_SLOTS = 16;  // scratch slots, rotated per launch
+
+COX_DEV int atom_add_acq_rel(int* p, int v) {
+  int old;
+  asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+
+template <typename XT, typename WT>
+__global__ void __launch_bounds__(RT_WARPS * 32)
+router_decode_kernel(const XT* __restrict__ x, const WT* __restrict__ wg, int T, int d, int E, int k, int mode,
+                     int S, int32_t* __restrict__ idx, float* __restrict__ wout, int32_t* __restrict__ counts,
+                     float* g_logits, int* g_cnt) {
+  __shared__ float lg[256];
+  __shared__ int s_hist[256];
+  __shared__ int s_sel[8];
+  __shared__ float s_selv[8];
+  __shared__ int s_last;
+  pdl_launch_dependents();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int t = blockIdx.x / S, sp = blockIdx.x - t * S;
+  const int ept = E / S, eb0 = sp * ept;
+  const XT* xr = x + (long)t * d;
+  for (int pr = warp; 2 * pr < ept; pr += RT_WARPS) {
+    const int ea = eb0 + 2 * pr, ebb = min(ea + 1, E - 1);
+    float acc0 = 0.0f, acc1 = 0.0f;
+#pragma unroll 8
+    for (int s = 8 * lane; s < d; s += 256) {
+      XChunk<XT> c;
+      c.load(xr + s);
+      float wa[8], wb[8];
+      load_w8<WT>(wg + (long)ea * d + s, wa);
+      load_w8<WT>(wg + (long)ebb * d + s, wb);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) ffma2(acc0, acc1, c.get(q), wa[q], wb[q]);
+    }
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) {
+      acc0 = __fadd_rn(acc0, __shfl_xor_sync(0xffffffffu, acc0, off));
+      acc1 = __fadd_rn(acc1, __shfl_xor_sync(0xffffffffu, acc1, off));
+    }
+    if (lane == 0) {
+      g_logits[(long)t * E + ea] = nan_low(acc0);
+      if (ea + 1 < E) g_logits[(long)t * E + ea + 1] = nan_low(acc1);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = atom_add_acq_rel(g_cnt + t, 1) == S - 1;
+  __syncthreads();
+  if (!s_last || warp != 0) return;
+  // last block of token t: its top-k
+  for (int e = lane; e < E; e += 32) lg[e] = __ldcg(g_logits + (long)t * E + e);
+  __syncwarp();
+  warp_route_token(lg, E, k, mode, lane, s_sel, s_selv, idx + (long)t * k, wout + (long)t * k, nullptr);
+  int last_tok = 0;
+  if (lane == 0) last_tok = atom_add_acq_rel(g_cnt + RD_TMAX, 1) == T - 1;
+  last_tok = __shfl_sync(0xffffffffu, last_tok, 0);
+  if (!last_tok) return;
+  // every token is routed: counts from idx, then reset the tickets
+  for (int e = lane; e < E; e += 32) s_hist[e] = 0;
+  __syncwarp();
+  for (int i = lane; i < T * k; i += 32) {
+    const int e = __ldcg(idx + i);
+    if (e >= 0 && e < E) atomicAdd(&s_hist[e], 1);
+  }
+  __syncwarp();
+  for (int e = lane; e < E; e += 32) counts[e] = s_hist[e];
+  for (int i = lane; i <= RD_TMAX; i += 32) g_cnt[i] = 0;
+}
+
+static int launch_router_decode(const void* x, int x_is_bf16, const void* wg, int wg_is_bf16, int T, int d, int E,
+                                int k, int mode, int32_t* idx, float* w, int32_t* counts, cudaStream_t s) {
+  static float* logits = nullptr;
+  static int* cnt = nullptr;
+  static unsigned seq = 0;
+  if (!logits) {
+    if (cudaMalloc(&logits, sizeof(float) * RD_SLOTS * RD_TMAX * 256) != cudaSuccess) return -2;
+    if (cudaMalloc(&cnt, sizeof(int) * RD_SLOTS * (RD_TMAX + 1)) != cudaSuccess) return -2;
+    if (cudaMemset(cnt, 0, sizeof(int) * RD_SLOTS * (RD_TMAX + 1)) != cudaSuccess) return -2;
+  }
+  const unsigned slot = seq++ % RD_SLOTS;
+  // splits per token: expert pairs spread over the warps of S blocks
+  int S = 1;
+  while (S < 4 && E % (4 * S) == 0 && E / (2 * S) >= 2 * RT_WARPS) S *= 2;
+  float* lgs = logits + (size_t)slot * RD_TMAX * 256;
+  int* cs = cnt + (size_t)slot * (RD_TMAX + 1);
+  static bool carve = false;
+  if (!carve) {  // decode: same smem carveout as the expert kernel that follows (no reconfig)
+    cudaFuncSetAttribute(router_decode_kernel<__nv_bfloat16, __nv_bfloat16>,
+                         cudaFuncAttributePreferredSharedMemoryCarveout, (int)cudaSharedmemCarveoutMaxShared);
+    carve = true;
+  }
+#define RD_LAUNCH(XT, WT)                                                                                        \
+  router_decode_kernel<XT, WT><<<T * S, RT_WARPS * 32, 0, s>>>(static_cast<const XT*>(x), static_cast<const WT*>(wg), \
+                                                               T, d, E, k, mode, S, idx, w, counts, lgs, cs)
+  if (x_is_bf16) {
+    if (wg_is_bf16) RD_LAUNCH(__nv_bfloat16, __nv_bfloat16); else RD_LAUNCH(__nv_bfloat16, float);
+  } else {
+    if (wg_is_bf16) RD_LAUNCH(float, __nv_bfloat16); else RD_LAUNCH(float, float);
+  }
+#undef RD_LAUNCH
+  return cudaGetLastError() == cudaSuccess ? 0 : -2;
+}
+
 int launch_router_tc(const void* x, const void* wg, int T, int d, int E, int k, int mode, int32_t* idx, float* w,
                      int32_t* counts, cudaStream_t s);
 
@@ -426,6 +538,13 @@ int launch_router(const void* x, int x_is_bf16, const void* wg, int wg_is_bf16, 
     const int rc = launch_router_bf16w(x, wg, T, d, E, k, mode, idx, w, counts, s);
     if (rc != -1) return rc;  // -1: tile does not fit in smem -> generic kernels below
   }
+  // decode batches: split-expert router, counts without a memset (COX_ROUTER_DECODE=0: generic kernel)
+  static const bool use_dec = [] {
+    const char* e = getenv("COX_ROUTER_DECODE");
+    return !(e && atoi(e) == 0);
+  }();
+  if (use_dec && T >= 1 && T <= RD_TMAX && E <= 256 && E % 2 == 0 && d % 8 == 0)
+    return launch_router_decode(x, x_is_bf16, wg, wg_is_bf16, T, d, E, k, mode, idx, w, counts, s);
   cudaError_t err = cudaMemsetAsync(counts, 0, sizeof(int32_t) * E, s);
   if (err != cudaSuccess) return -2;
   if (T == 0) return 0;

@@ -44,6 +44,29 @@ def test_router_bitexact(T, d, E, k, mode, dtype):
     np.testing.assert_allclose(w.cpu().numpy(), ow, rtol=2e-6, atol=1e-7)
 
 
+@pytest.mark.parametrize("T,d,E,k,mode,dtype,wbf16", [
+    (64, 2048, 64, 6, 1, torch.bfloat16, True),    # C4 decode: 4 blocks per token
+    (1, 4096, 8, 2, 0, torch.bfloat16, True),
+    (17, 512, 16, 4, 1, torch.float32, False),
+    (64, 1024, 160, 6, 1, torch.bfloat16, True),   # 20 expert pairs per block
+    (33, 200, 8, 8, 0, torch.bfloat16, False),     # d not a multiple of 256
+])
+def test_decode_router_bitexact(T, d, E, k, mode, dtype, wbf16):
+    """Split-expert decode router (T <= 64): idx / counts bit-exact vs the oracle,
+    repeated launches (self-resetting tickets), weights within 2 ulp of expf."""
+    g = torch.Generator(device=DEV).manual_seed(T + E)
+    wg = ((torch.rand((E, d), generator=g, device=DEV) * 2 - 1) / d ** 0.5).to(torch.bfloat16)
+    wg = wg if wbf16 else wg.float()
+    for rep in range(3):
+        x = make_tokens(T, d, seed=20 + rep, device=DEV, dtype=dtype)
+        idx, w, counts = ops.router_topk(x, wg, k, mode)
+        torch.cuda.synchronize()
+        oi, ow, oc = O.router_topk(x.float().cpu().numpy(), wg.float().cpu().numpy(), k, mode)
+        assert np.array_equal(idx.cpu().numpy(), oi)
+        assert np.array_equal(counts.cpu().numpy(), oc)
+        np.testing.assert_allclose(w.cpu().numpy(), ow, rtol=2e-6, atol=1e-7)
+
+
 def test_router_ties_go_to_lower_index():
     T, d, E, k = 64, 256, 8, 2
     x = make_tokens(T, d, seed=4, device=DEV)
