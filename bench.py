@@ -461,8 +461,9 @@ def main():
             achieved = flops_k3 / (k3_ms / 1e3) / 1e12
             roof = {"kernel": "grouped_gemm_kernel<EPI_SWIGLU> (K3)", "bound": "tensor", "achieved": achieved,
                     "peak": pk["bf16_sus"], "unit": "TFLOP/s", "frac": achieved / pk["bf16_sus"], "traffic": traffic,
-                    "traffic_note": "DRAM bytes per K3 launch from one ncu --set full capture (profiles/r01); "
-                                    "algorithmic A+B+h = 21.2 GB, A re-read once per 16-wide n-band",
+                    "traffic_note": ("DRAM bytes per K3 launch from one ncu --set full capture (profiles/r01); "
+                                     "algorithmic A+B+h = 21.2 GB, A re-read once per 16-wide n-band")
+                    if traffic is not None else "no ncu --set full capture for this config (traffic measured on C2)",
                     "peak_kind": f"bf16_tflops_sustained ({pk['src']}); burst {pk['bf16']}", "k3_ms": k3_ms,
                     "k4_ms": k4_ms, "k4_tflops": flops_k4 / (k4_ms / 1e3) / 1e12}
         else:
