@@ -110,8 +110,11 @@ class MoELayer:
         if T is not None and self.uses_idx_decode(T):
             return 2  # router, then one launch for K3/K4/shared/combine reading the router's idx
         if T is not None and self.uses_small_path(T):
-            # router + single-CTA permute (indices only) + one launch for K3/K4/shared/combine
-            return 1 + 1 + 1 + (1 if self.out_dtype != torch.bfloat16 else 0)
+            # router + single-CTA permute (indices only; + row copy above the gather
+            # threshold) + one launch for K3/K4/shared/combine
+            perm_small_path = 1 if small_perm else 3
+            return (1 + perm_small_path + (0 if self._small_gather(T) else 1) + 1
+                    + (1 if self.out_dtype != torch.bfloat16 else 0))
         if (self.shared_ff and self.SHARED_FUSED_COMBINE and self.k <= 8
                 and not (T is not None and 0 < T * self.k <= self.SHARED_SIDE_MAX_ROWS)):
             return 1 + perm + 2 + 2  # shared K3 + shared down with the combine in its epilogue
@@ -222,17 +225,26 @@ class MoELayer:
     # routed rows, fused vs separate combine
     SMALL_GATHER = os.environ.get("COX_SMALL_GATHER", "1") == "1"
     SMALL_FUSE = os.environ.get("COX_SMALL_FUSE", "1") == "1"
+    # Row gathers (TMA tile::gather4 of x rows) only up to this many tokens:
+    # above it the permute materialises x_perm and the kernel loads tiled B
+    # boxes.  Measured on C4 (tools/sweep_decode_large.py, us/step, gather vs
+    # x_perm): T=64 196.5/196.2, 128 222.0/210.9, 192 270.9/234.8, 256 323.4/262.1.
+    SMALL_GATHER_T_MAX = int(os.environ.get("COX_SMALL_GATHER_T_MAX", "64"))
+
+    def _small_gather(self, T: int) -> bool:
+        return self.SMALL_GATHER and T <= self.SMALL_GATHER_T_MAX
 
     def _route_small(self, x: torch.Tensor, b: StageBuffers):
+        gather = self._small_gather(x.shape[0])
         ops.router_topk(x, self.wg_router, self.k, self.mode, out=(b.idx, b.w, b.counts))
-        ops.permute(b.idx, x, self.E, self.tile_m, out=(b.offsets, b.dst, None if self.SMALL_GATHER else b.x_perm),
-                    workspace=b.workspace, copy_rows=not self.SMALL_GATHER, row_tokens=b.row_tokens)
+        ops.permute(b.idx, x, self.E, self.tile_m, out=(b.offsets, b.dst, None if gather else b.x_perm),
+                    workspace=b.workspace, copy_rows=not gather, row_tokens=b.row_tokens)
 
     def _ffn_small(self, x: torch.Tensor, b: StageBuffers, out: torch.Tensor):
         shared = (self.wts.shared_w13, self.wts.shared_w2, b.shared_h, b.shared_y) if self.shared_ff else None
         fuse = out.dtype == torch.bfloat16 and self.SMALL_FUSE
         ops.small_expert_ffn(x, b.offsets, self.groups, self.w13_list, self.w2_list, b.h, b.y,
-                             x_perm=None if self.SMALL_GATHER else b.x_perm, row_tokens=b.row_tokens,
+                             x_perm=None if self._small_gather(x.shape[0]) else b.x_perm, row_tokens=b.row_tokens,
                              shared=shared, combine=(b.dst, b.w, out) if fuse else None)
         if not fuse:
             ops.combine(b.y, b.dst, b.w, b.shared_y if self.shared_ff else None, out=out)
@@ -278,7 +290,7 @@ class MoELayer:
 
     def uses_idx_decode(self, T: int, out: torch.Tensor | None = None) -> bool:
         return (self.SMALL_FROM_IDX and self.uses_small_path(T) and self.tile_m == 1 and self.SMALL_FUSE
-                and self.SMALL_GATHER and (out is None or out.dtype == torch.bfloat16)
+                and self._small_gather(T) and (out is None or out.dtype == torch.bfloat16)
                 and self.out_dtype == torch.bfloat16)
 
     # routed decode in ONE launch: the router runs in the expert kernel's
@@ -436,8 +448,9 @@ class MoELayer:
             torch.cuda.synchronize()
             return {"router": ev[0].elapsed_time(ev[1]), "expert_ffn_from_idx_shared_combine": ev[1].elapsed_time(ev[2])}
         if self.uses_small_path(x.shape[0]):
-            ops.permute(b.idx, x, self.E, self.tile_m, out=(b.offsets, b.dst, None), workspace=b.workspace,
-                        copy_rows=False, row_tokens=b.row_tokens)
+            gather = self._small_gather(x.shape[0])
+            ops.permute(b.idx, x, self.E, self.tile_m, out=(b.offsets, b.dst, None if gather else b.x_perm),
+                        workspace=b.workspace, copy_rows=not gather, row_tokens=b.row_tokens)
         elif self.gather_a:
             ops.permute(b.idx, x, self.E, self.tile_m, out=(b.offsets, b.dst, None), workspace=b.workspace,
                         copy_rows=False, row_tokens=b.row_tokens)

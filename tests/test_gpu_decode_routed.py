@@ -23,6 +23,7 @@ def _pair(E, d, ff, k, mode, sff, seed=0):
     b.DECODE_ROUTE_IN = False
     b.DENSE_T_MAX = 0
     a.DENSE_T_MAX = 0
+    a.SMALL_GATHER_T_MAX = b.SMALL_GATHER_T_MAX = 256  # the idx paths gather rows at every T here
     return wts, a, b
 
 

@@ -212,6 +212,7 @@ def test_decode_from_idx_matches_permute_path(T, d, ff, E, k, mode, shared_ff):
     b_l = MoELayer(wts, k, mode)
     b_l.SMALL_FROM_IDX = False
     a_l.DENSE_T_MAX = b_l.DENSE_T_MAX = 0
+    a_l.SMALL_GATHER_T_MAX = b_l.SMALL_GATHER_T_MAX = 256  # gathered rows at every T here
     assert a_l.uses_idx_decode(T) and not b_l.uses_idx_decode(T)
     a = a_l(x).clone()
     bo = b_l(x).clone()
@@ -220,6 +221,26 @@ def test_decode_from_idx_matches_permute_path(T, d, ff, E, k, mode, shared_ff):
     assert torch.equal(ba.idx, bb.idx)
     assert torch.equal(ba.offsets, bb.offsets)
     assert torch.equal(ba.dst, bb.dst)
+    assert torch.equal(a, bo)
+
+
+@pytest.mark.parametrize("T", [65, 128, 256])
+def test_decode_x_perm_above_gather_threshold(T):
+    """Above SMALL_GATHER_T_MAX the decode step materialises x_perm (router +
+    permute copy + tiled-B launch): same routing and output bits as the
+    gathered-row path."""
+    d, ff, E, k, sff = 1024, 512, 16, 4, 256
+    wts = make_layer_weights(E, d, ff, seed=11, device=DEV, shared_ff=sff)
+    x = make_tokens(T, d, seed=12, device=DEV)
+    a_l = MoELayer(wts, k, "deepseek")
+    b_l = MoELayer(wts, k, "deepseek")
+    b_l.SMALL_GATHER_T_MAX = 256
+    assert not a_l._small_gather(T) and b_l._small_gather(T)
+    assert a_l.launches_per_step(T) == 4 and b_l.launches_per_step(T) == 2
+    a = a_l(x).clone()
+    bo = b_l(x).clone()
+    torch.cuda.synchronize()
+    assert torch.equal(a_l.buffers(T, DEV).idx, b_l.buffers(T, DEV).idx)
     assert torch.equal(a, bo)
 
 
