@@ -27,6 +27,8 @@ def main():
         for variant in ("gather", "x_perm", "prefill"):
             layer = MoELayer(wts, k, "deepseek")
             layer.DENSE_T_MAX = 0
+            if variant == "gather":
+                layer.SMALL_GATHER_T_MAX = 1 << 30  # row gathers at every T
             if variant == "x_perm":
                 layer.SMALL_GATHER = False
             if variant == "prefill":
