@@ -188,6 +188,9 @@ class MoELayer:
     # Off by default: measured on C4 the fused epilogue is latency-bound on the k
     # routed-row gathers (shared down + combine 3.51 ms fused vs 1.99 + 1.38 separate)
     SHARED_FUSED_COMBINE = os.environ.get("COX_SHARED_FUSE", "0") == "1"
+    # prefill layers with shared experts: shared-expert GEMMs on a side stream
+    # beside the permute (COX_SHARED_BESIDE=0: in sequence after the routed experts)
+    SHARED_BESIDE_PERMUTE = os.environ.get("COX_SHARED_BESIDE", "1") == "1"
 
     def forward(self, x: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
         if x.dtype != torch.bfloat16 or x.dim() != 2 or x.shape[1] != self.d:
@@ -211,6 +214,25 @@ class MoELayer:
                              max_ctas=-(-(148 - self.SHARED_SIDE_CTAS) // 2) * 2)
             main.wait_stream(side)
             return self.finish(b, b.shared_y, out)
+        if self.shared_ff and self.SHARED_BESIDE_PERMUTE and not self.SHARED_FUSED_COMBINE:
+            # the shared expert does not depend on the routing: its GEMMs run on a
+            # side stream right after the router, so the HBM-bound permute copy
+            # (a few registers, no shared memory) co-resides with them on the SMs
+            main = torch.cuda.current_stream(x.device)
+            side = self._side_stream(x.device)
+            ops.router_topk(x, self.wg_router, self.k, self.mode, out=(b.idx, b.w, b.counts))
+            side.wait_stream(main)
+            with torch.cuda.stream(side):
+                sh = self.shared_expert(x, b)
+            if self.gather_a:
+                ops.permute(b.idx, x, self.E, self.tile_m, out=(b.offsets, b.dst, None), workspace=b.workspace,
+                            copy_rows=False, row_tokens=b.row_tokens)
+                b.x_ref = x
+            else:
+                ops.permute(b.idx, x, self.E, self.tile_m, out=(b.offsets, b.dst, b.x_perm), workspace=b.workspace)
+            self.experts(b)
+            main.wait_stream(side)
+            return self.finish(b, sh, out)
         self.route(x, b)
         self.experts(b)
         if self.shared_ff and self.SHARED_FUSED_COMBINE and self.k <= 8:
