@@ -244,45 +244,45 @@ __global__ void __launch_bounds__(SG_THREADS, 1) small_ffn_kernel(const __grid_c
     mbar_init(smem_u32(perm_ready), 1);
     fence_mbar_init();
   }
-  // canonical-order routing of tokens blockIdx.x, + gridDim.x, ... by one warp
-  // (dense decode: beside the weight stream; route_in: in the prologue)
-  auto route_tokens = [&](int* hist) {
-      const int d = p.d, E = p.E, kk = p.k;
-      for (int t = blockIdx.x; t < p.T; t += gridDim.x) {
-        const __nv_bfloat16* xr = p.xtok + (long long)t * d;
-        for (int e0 = 0; e0 < E; e0 += 8) {
-          float acc[8];
+  // dense decode: warp 2 routes tokens blockIdx.x, + gridDim.x, ... in the
+  // canonical order, beside the weight stream (only the combine waits for it)
+  auto route_tokens = [&]() {
+    const int d = p.d, E = p.E, kk = p.k;
+    for (int t = blockIdx.x; t < p.T; t += gridDim.x) {
+      const __nv_bfloat16* xr = p.xtok + (long long)t * d;
+      for (int e0 = 0; e0 < E; e0 += 8) {
+        float acc[8];
 #pragma unroll
-          for (int u = 0; u < 8; ++u) acc[u] = 0.f;
+        for (int u = 0; u < 8; ++u) acc[u] = 0.f;
 #pragma unroll 2
-          for (int sc = 8 * lane; sc < d; sc += 256) {
-            float xv[8];
-            bf16x8_to_f32(ld_nc_v4(xr + sc), xv);
+        for (int sc = 8 * lane; sc < d; sc += 256) {
+          float xv[8];
+          bf16x8_to_f32(ld_nc_v4(xr + sc), xv);
 #pragma unroll
-            for (int u = 0; u < 8; u += 2) {
-              float wa[8], wb[8];
-              const int ea = min(e0 + u, E - 1), eb = min(e0 + u + 1, E - 1);
-              bf16x8_to_f32(ld_nc_v4(p.wg + (long long)ea * d + sc), wa);
-              bf16x8_to_f32(ld_nc_v4(p.wg + (long long)eb * d + sc), wb);
+          for (int u = 0; u < 8; u += 2) {
+            float wa[8], wb[8];
+            const int ea = min(e0 + u, E - 1), eb = min(e0 + u + 1, E - 1);
+            bf16x8_to_f32(ld_nc_v4(p.wg + (long long)ea * d + sc), wa);
+            bf16x8_to_f32(ld_nc_v4(p.wg + (long long)eb * d + sc), wb);
 #pragma unroll
-              for (int q = 0; q < 8; ++q) ffma2(acc[u], acc[u + 1], xv[q], wa[q], wb[q]);
-            }
-          }
-#pragma unroll
-          for (int u = 0; u < 8; ++u) {
-            float v = acc[u];
-#pragma unroll
-            for (int off = 16; off >= 1; off >>= 1) v = __fadd_rn(v, __shfl_xor_sync(0xffffffffu, v, off));
-            if (lane == 0 && e0 + u < E) s_route[e0 + u] = v != v ? -INFINITY : v;  // NaN ranks like -inf
+            for (int q = 0; q < 8; ++q) ffma2(acc[u], acc[u + 1], xv[q], wa[q], wb[q]);
           }
         }
-        __syncwarp();
-        warp_route_token(s_route, E, kk, p.mode, lane, reinterpret_cast<int*>(s_route + 264), s_route + 272,
-                         p.ridx + t * kk, p.rw + t * kk, hist);
-        if (lane == 0) red_release_add(p.counters + SG_ROUTED, 1);  // after idx / w / histogram
-        __syncwarp();
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          float v = acc[u];
+#pragma unroll
+          for (int off = 16; off >= 1; off >>= 1) v = __fadd_rn(v, __shfl_xor_sync(0xffffffffu, v, off));
+          if (lane == 0 && e0 + u < E) s_route[e0 + u] = v != v ? -INFINITY : v;  // NaN ranks like -inf
+        }
       }
-      };
+      __syncwarp();
+      warp_route_token(s_route, E, kk, p.mode, lane, reinterpret_cast<int*>(s_route + 264), s_route + 272,
+                       p.ridx + t * kk, p.rw + t * kk, nullptr);
+      if (lane == 0) red_release_add(p.counters + SG_ROUTED, 1);  // after idx / w / histogram
+      __syncwarp();
+    }
+  };
   // barrier init and the TMEM allocation do not depend on the routing: done
   // while the router (the PDL primary) is still running
   if (warp == 2) tmem_alloc<1>(smem_u32(tmem_slot), SG_TMEM_COLS);
@@ -696,7 +696,7 @@ __global__ void __launch_bounds__(SG_THREADS, 1) small_ffn_kernel(const __grid_c
     // butterfly; expert pairs share one FFMA2), top-k with ties to the lower
     // index, Mixtral / DeepSeek weights.  Only the combine needs the result, so
     // this runs beside the weight stream instead of before it.
-    if (p.dense) route_tokens(nullptr);
+    if (p.dense) route_tokens();
   } else if (warp >= 4) {
     // ------------------------------------------------------------ epilogue
     // Warp q reads TMEM lanes 32q..32q+31 (= weight rows of the unit), 32
