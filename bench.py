@@ -146,6 +146,63 @@ def cpu_baseline(wts_host, x_host, k, mode_id, shared_host, n_tokens):
     return n_tokens / dt, threads, dt, ref
 
 
+def gpu_routing(layer, x):
+    """(idx, counts, offsets, dst) the timed path produced for x (numpy; offsets
+    / dst None where the path materialises no permutation)."""
+    import torch
+    from paper_2605_17889_b200 import ops
+    T = x.shape[0]
+    c = lambda t: t.cpu().numpy() if t is not None else None  # noqa: E731
+    if hasattr(layer, "buffers"):  # MoELayer: buffers of its last step over x
+        b = layer.buffers(T, x.device)
+        perm = not layer.uses_dense_decode(T)
+        return c(b.idx), c(b.counts), c(b.offsets) if perm else None, c(b.dst) if perm else None
+    if hasattr(layer, "route_row"):  # fused EP: routing of the rank's own tokens
+        return c(layer.idx), c(layer.counts), c(layer.offsets), c(layer.dst)
+    # NCCL EP: the same router + permute kernels its stage runs
+    idx, _, counts, _, _ = layer.stage.route_and_permute(x)
+    offsets = torch.empty((layer.E + 1,), dtype=torch.int32, device=x.device)
+    dst = torch.empty_like(idx)
+    ops.permute(idx, x, layer.E, out=(offsets, dst, None))
+    return c(idx), c(counts), c(offsets), c(dst)
+
+
+def cpu_baseline_and_parity(args, layer, wts, x, out_full, k, mode):
+    """cpu_baseline: the fp32 oracle over the first n tokens of this rank's batch
+    (routed as in the full batch), timed on this host.  parity: (1) routing of
+    the FULL batch — idx, counts, offsets, dst — against the oracle router
+    (OpenMP over tokens) bit for bit; (2) the layer output of the first n tokens
+    against the fp32 oracle layer, rel-L2 <= 1e-2."""
+    import numpy as np
+    import torch
+    from oracle import oracle as O
+    T, d = x.shape
+    E = wts.num_experts
+    mode_id = 0 if mode == "mixtral" else 1
+    n = min(T, args.cpu_tokens)
+    hw, shared = host_weights(wts)
+    cps, threads, dt, ref = cpu_baseline(hw, x[:n].float().cpu().numpy(), k, mode_id, shared, n)
+    cpu = {"value": cps, "unit": "tokens/s", "cores": threads, "kind": "port",
+           "sample": (f"all {T} tokens of the step" if n == T else f"first {n} of {T} tokens (routed as in the full "
+                      "batch)") + f", full-size weights, fp32 oracle (oracle/, OpenMP x{threads}) on "
+                      f"{cpu_model_name()}: {dt:.2f} s"}
+    gi, gc, go, gd = gpu_routing(layer, x)
+    t0 = time.perf_counter()
+    oi, _, oc = O.router_topk_bf16(x.view(torch.int16).cpu().numpy().view(np.uint16), hw["wg"], k, mode_id)
+    oo, od = O.permute(oi, E, 1)
+    t_route = time.perf_counter() - t0
+    routing_ok = bool(np.array_equal(gi, oi) and np.array_equal(gc, oc)
+                      and (go is None or np.array_equal(go, oo)) and (gd is None or np.array_equal(gd, od)))
+    gout = out_full[:n].float().cpu().numpy().astype(np.float64)
+    err = float(np.linalg.norm(gout - ref["out"]) / max(np.linalg.norm(ref["out"]), 1e-30))
+    parity = {"routing_tokens_checked": T, "routing_bitexact": routing_ok,
+              "routing_checked": "idx, counts" + (", offsets, dst" if go is not None else ""),
+              "routing_oracle_s": round(t_route, 2),
+              "tokens_checked": n, "routing_indices_bitexact": bool(np.array_equal(gi[:n], ref["idx"])),
+              "out_rel_l2_vs_fp32_oracle": err, "tolerance": 1e-2, "pass": bool(routing_ok and err <= 1e-2)}
+    return cpu, parity
+
+
 def host_weights(wts):
     import numpy as np  # noqa: F401
     from paper_2605_17889_b200.synthetic import split_w13
@@ -418,22 +475,15 @@ def main():
     e2e = None
     if not args.no_e2e and not args.microbatch:
         # pinned host batches; each step = H2D of its tokens + expert stage + D2H of its output,
-        # pipelined across steps (ws == 1: MoELayer.run_host_batches; EP: sequential per step)
+        # pipelined across steps (MoELayer / EP layer .run_host_batches, every rank its own batches)
         x_host = x.cpu().pin_memory()
         outs = [torch.empty((T, d), dtype=torch.bfloat16).pin_memory() for _ in range(2)]
-        if hasattr(layer, "run_host_batches"):
-            layer.run_host_batches([x_host] * 2, outs)
+        layer.run_host_batches([x_host] * 2, outs)
         barrier()
         s0 = torch.cuda.Event(enable_timing=True)
         s1 = torch.cuda.Event(enable_timing=True)
         s0.record(stream)
-        if hasattr(layer, "run_host_batches"):
-            layer.run_host_batches([x_host] * args.steps, [outs[i % 2] for i in range(args.steps)])
-        else:
-            xd = torch.empty_like(x)
-            for i in range(args.steps):
-                xd.copy_(x_host, non_blocking=True)
-                outs[i % 2].copy_(layer(xd), non_blocking=True)
+        layer.run_host_batches([x_host] * args.steps, [outs[i % 2] for i in range(args.steps)])
         s1.record(stream)
         barrier()
         e_ms = torch.tensor([s0.elapsed_time(s1)], dtype=torch.float64, device=dev)
@@ -441,12 +491,32 @@ def main():
             dist.all_reduce(e_ms, op=dist.ReduceOp.MAX)
         e2e = {"value": tokens_all / (float(e_ms.item()) / 1e3), "unit": "tokens/s",
                "h2d_bytes_per_step": x.numel() * 2 * ws, "d2h_bytes_per_step": T * d * 2 * ws,
-               "api": "MoELayer.run_host_batches (pinned host in/out, copies overlapped across steps)"
-               if ws == 1 else "EPMoELayer per step with H2D/D2H copies"}
+               "api": f"{type(layer).__name__}.run_host_batches (pinned host in/out, copies overlapped across steps"
+                      + (", every rank its own batches)" if ws > 1 else ")")}
+        del x_host, outs
 
-    # --- per-stage breakdown (one extra step, not part of `value`) ------------
+    # --- per-stage breakdown (one extra step, not part of `value`; collective under EP) ---
     stages = layer.stage_times(x) if hasattr(layer, "stage_times") and not args.microbatch else None
     touched = int((layer.buffers(T, dev).counts > 0).sum().item()) if hasattr(layer, "buffers") else E
+    # one more (untimed) step of the timed path: its output and routing are what the parity checks
+    out_full = layer(x).clone() if not args.microbatch else None
+    ep_info = None
+    if ws > 1:
+        # EP output for this rank's batch == the single-GPU layer on the same batch (bit for bit)
+        exch = layer.exchange_bytes() if hasattr(layer, "exchange_bytes") else None
+        barrier()
+        ep_equal = None
+        if rank == 0:
+            ref_layer = MoELayer(wts, k, mode)
+            ep_equal = bool(torch.equal(ref_layer(x), out_full))
+            del ref_layer
+            torch.cuda.empty_cache()
+        ep_info = {"rank0_output_equals_single_gpu_layer": ep_equal}
+        if exch is not None and stages:
+            ep_info["rank0_nvlink_bytes"] = exch
+            ep_info["rank0_dispatch_gbs"] = exch["dispatch"] / max(1e-9, stages["dispatch_nvlink"] / 1e3) / 1e9
+            ep_info["rank0_combine_gbs"] = exch["combine"] / max(1e-9, stages["combine_nvlink"] / 1e3) / 1e9
+        barrier()
 
     if rank == 0:
         pk = peaks()
@@ -459,10 +529,10 @@ def main():
             traffic = json.loads(tp.read_text()).get("grouped_gemm_kernel<0>", {}).get("dram_bytes_per_launch")
         if k3_ms:
             achieved = flops_k3 / (k3_ms / 1e3) / 1e12
-            roof = {"kernel": "grouped_gemm_kernel<EPI_SWIGLU> (K3)", "bound": "tensor", "achieved": achieved,
+            roof = {"kernel": "grouped_gemm_kernel<EPI_SWIGLU> (K3)" + (" on rank 0" if ws > 1 else ""),
+                    "bound": "tensor", "achieved": achieved,
                     "peak": pk["bf16_sus"], "unit": "TFLOP/s", "frac": achieved / pk["bf16_sus"], "traffic": traffic,
-                    "traffic_note": ("DRAM bytes per K3 launch from one ncu --set full capture (profiles/r01); "
-                                     "algorithmic A+B+h = 21.2 GB, A re-read once per 16-wide n-band")
+                    "traffic_note": "DRAM bytes per K3 launch from one ncu --set full capture (profiles/ncu_traffic.json)"
                     if traffic is not None else "no ncu --set full capture for this config (traffic measured on C2)",
                     "peak_kind": f"bf16_tflops_sustained ({pk['src']}); burst {pk['bf16']}", "k3_ms": k3_ms,
                     "k4_ms": k4_ms, "k4_tflops": flops_k4 / (k4_ms / 1e3) / 1e12}
@@ -478,22 +548,11 @@ def main():
                     "bytes_per_step": wbytes + abytes, "experts_touched": touched}
         cpu = None
         parity = None
-        if not args.no_cpu_baseline and ws == 1 and not decode and not args.microbatch:
-            hw, shared = host_weights(wts)
-            x_host_f = x[: args.cpu_tokens].float().cpu().numpy()
-            cps, threads, dt, ref = cpu_baseline(hw, x_host_f, k, 0 if mode == "mixtral" else 1, shared,
-                                                 args.cpu_tokens)
-            cpu = {"value": cps, "unit": "tokens/s", "cores": threads, "kind": "port",
-                   "sample": f"first {args.cpu_tokens} of {T} tokens (routed as in the full batch), full-size "
-                             f"weights, fp32 oracle (oracle/, OpenMP x{threads}) on {cpu_model_name()}: {dt:.1f} s"}
-            # parity of the timed GPU path on the same tokens (same inputs, same weights)
-            import numpy as np
-            n = args.cpu_tokens
-            gout = layer(x)[:n].float().cpu().numpy().astype(np.float64)
-            gidx = layer.buffers(T, dev).idx[:n].cpu().numpy()
-            err = float(np.linalg.norm(gout - ref["out"]) / max(np.linalg.norm(ref["out"]), 1e-30))
-            parity = {"tokens_checked": n, "routing_indices_bitexact": bool(np.array_equal(gidx, ref["idx"])),
-                      "out_rel_l2_vs_fp32_oracle": err, "tolerance": 1e-2, "pass": bool(err <= 1e-2)}
+        if not args.no_cpu_baseline and not args.microbatch:
+            cpu, parity = cpu_baseline_and_parity(args, layer, wts, x, out_full, k, mode)
+        if ep_info is not None and parity is not None:
+            parity["ep"] = ep_info
+            parity["pass"] = bool(parity["pass"] and ep_info["rank0_output_equals_single_gpu_layer"])
         wgb = (touched * 3 * d * ff * 2 + 3 * d * shared_ff * 2) / 1e9
         if decode:
             l2_note = (f"expert weights read per step ({wgb:.2f} GB) > 126 MB L2, so every step streams them "

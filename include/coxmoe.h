@@ -51,93 +51,62 @@ int cox_device_check(void);
 /* K1 — router.  Replaces the top-k routing of PAPER.md:67 that the reference
  * only accounts for analytically (workload.py:156-165 — OP3's D_X term).
  *   x      [T, d]  (x_dtype: COX_DTYPE_BF16 or COX_DTYPE_F32), d % 8 == 0
- *   wg     [E, d]  fp32 router weight
+ *   wg     [E, d]  router weight (wg_dtype: COX_DTYPE_BF16 or COX_DTYPE_F32)
  *   idx    [T, k]  int32 expert ids, descending logit, ties -> lower index
  *                  (eas.py:364-374 convention)
  *   w      [T, k]  fp32 routing weights
  *   counts [E]     int32 tokens per expert (the per-batch analogue of eas.probe,
  *                  eas.py:346-356)
+ *   workspace      >= cox_router_workspace_bytes(T, E) bytes of device memory,
+ *                  ZEROED ONCE when allocated (the kernels leave it zeroed);
+ *                  one workspace per concurrently executing launch.
  * 1 <= k <= min(E, 8), E <= 256.  Logits are fp32 in the canonical order shared
- * with the CPU oracle, so idx is bit-exact. */
-int cox_router_topk(const void* x, int x_dtype, const float* wg, int T, int d, int E, int k, int mode,
-                    int32_t* idx, float* w, int32_t* counts, void* stream);
-/* Same with the router weight dtype explicit (COX_DTYPE_BF16 or COX_DTYPE_F32).
- * A bf16 wg (the checkpoint dtype of Mixtral/DeepSeek routers) is staged in
- * shared memory by the fine-grained (E > 8) kernel; the logits are identical
- * to passing the same values as fp32 (bf16 x bf16 products are exact).
- * bf16 x and wg, E >= 32, T >= 18944: the logits are screened on the tensor
- * cores (fp32 accumulation, per-token error bound) and only the candidates
- * that can reach the top-k are recomputed in the canonical order: same idx
- * and counts; COX_ROUTE_MIXTRAL weights identical; COX_ROUTE_DEEPSEEK
- * weights within ~1e-6 relative (their full-softmax denominator uses the
- * screened logits of the non-candidates).  COX_ROUTER_TC=0 disables. */
-int cox_router_topk_ex(const void* x, int x_dtype, const void* wg, int wg_dtype, int T, int d, int E, int k,
-                       int mode, int32_t* idx, float* w, int32_t* counts, void* stream);
+ * with the CPU oracle, so idx is bit-exact.  A bf16 wg (the checkpoint dtype of
+ * Mixtral/DeepSeek routers) gives the same logits as the same values in fp32
+ * (bf16 x bf16 products are exact).  bf16 x and wg, E >= 32, T >= 18944: the
+ * logits are screened on the tensor cores (fp32 accumulation, per-token error
+ * bound) and only the candidates that can reach the top-k are recomputed in the
+ * canonical order: same idx and counts; COX_ROUTE_MIXTRAL weights identical;
+ * COX_ROUTE_DEEPSEEK weights within ~1e-6 relative (their full-softmax
+ * denominator uses the screened logits of the non-candidates). */
+size_t cox_router_workspace_bytes(int T, int E);
+int cox_router_topk(const void* x, int x_dtype, const void* wg, int wg_dtype, int T, int d, int E, int k, int mode,
+                    int32_t* idx, float* w, int32_t* counts, void* workspace, size_t workspace_bytes, void* stream);
 
 /* K2 — stable permutation by expert (coalesced dispatch).
+ *   idx      [T, k] expert ids in [0, E) (anything else is dropped)
  *   x        [T, d] bf16, d % 8 == 0
  *   offsets  [E+1]  int32 segment starts (segments padded to tile_m rows)
  *   dst      [T, k] int32 row of x_perm that holds (t, j)
- *   x_perm   [rows_cap, d] bf16, rows_cap >= T*k + E*(tile_m-1)
- *   workspace of cox_permute_workspace_bytes(T, E) bytes.
- * x_perm == NULL: compute offsets and dst only (the fused EP dispatch moves
- * the rows itself). */
+ *   x_perm   [rows_cap, d] bf16, rows_cap >= T*k + E*(tile_m-1); NULL: compute
+ *            offsets and dst only (the fused EP dispatch moves the rows itself)
+ *   row_tokens [rows_cap] (nullable): the source token of every permuted row
+ *            (the gathered-B decode path of cox_small_expert_ffn)
+ *   workspace of cox_permute_workspace_bytes(T, E) bytes. */
 size_t cox_permute_workspace_bytes(int T, int E);
 int cox_permute(const int32_t* idx, int T, int k, int E, int tile_m, const void* x, int d, int32_t* offsets,
-                int32_t* dst, void* x_perm, long long rows_cap, void* workspace, void* stream);
-/* Same, optionally emitting row_tokens[rows_cap]: the source token of every
- * permuted row (for cox_grouped_swiglu_gather; x_perm may then be NULL). */
-int cox_permute_ex(const int32_t* idx, int T, int k, int E, int tile_m, const void* x, int d, int32_t* offsets,
-                   int32_t* dst, void* x_perm, long long rows_cap, int32_t* row_tokens, void* workspace,
-                   void* stream);
+                int32_t* dst, void* x_perm, long long rows_cap, int32_t* row_tokens, void* workspace, void* stream);
 
 /* K3 — grouped SwiGLU expert GEMM over the coalesced batch:
  *   h[r, :] = silu(x_perm[r] W1_e^T) * (x_perm[r] W3_e^T) for r in segment e.
- * Runs the groups group_experts[0..n_groups) (<= 64); w13[g] is the DEVICE
+ * offsets [E+1] are the segments of cox_permute.  Runs the groups
+ * group_experts[0..n_groups) (<= 64, each in [0, E)); w13[g] is the DEVICE
  * pointer of that group's interleaved weight [2*ff, d] bf16 (128-row blocks:
  * W1 rows 128i..128i+127, then W3 rows 128i..128i+127; see
  * cox_interleave_w13).  Resident and streamed (cold) experts are just
  * different groups/pointers, so a cold expert's GEMM can be issued separately
- * once its copy has landed.  d % 64 == 0, ff % 128 == 0. */
-int cox_grouped_swiglu(const void* x_perm, long long rows_cap, const int32_t* offsets, int n_groups,
-                       const int32_t* group_experts, const void* const* w13, int d, int ff, void* h, void* stream);
-
-/* Same, with a CTA budget: the persistent kernel uses at most max_ctas SMs
- * (even, >= 2; 0 = all), so that two grouped GEMMs can run concurrently on
- * different streams (e.g. the shared expert beside the routed experts in a
- * decode step). */
-int cox_grouped_swiglu_ex(const void* x_perm, long long rows_cap, const int32_t* offsets, int n_groups,
-                          const int32_t* group_experts, const void* const* w13, int d, int ff, void* h,
-                          int max_ctas, void* stream);
-
-/* K3 with gather-fused A loads: permuted row r is read straight from x[T, d]
- * at row row_tokens[r] (TMA tile::gather4, 4 rows per load), so x_perm is
- * never materialised.  Same results as cox_grouped_swiglu on x_perm. */
-int cox_grouped_swiglu_gather(const void* x, long long T, const int32_t* row_tokens, long long rows_cap,
-                              const int32_t* offsets, int n_groups, const int32_t* group_experts,
-                              const void* const* w13, int d, int ff, void* h, int max_ctas, void* stream);
+ * once its copy has landed.  max_ctas: the persistent kernel uses at most
+ * max_ctas SMs (even, >= 2; 0 = all), so two grouped GEMMs can run
+ * concurrently on different streams.  d % 64 == 0, ff % 128 == 0. */
+int cox_grouped_swiglu(const void* x_perm, long long rows_cap, const int32_t* offsets, int E, int n_groups,
+                       const int32_t* group_experts, const void* const* w13, int d, int ff, void* h, int max_ctas,
+                       void* stream);
 
 /* K4 — grouped down projection: y_perm[r] = h[r] W2_e^T.  w2[g]: [d, ff] bf16.
- * ff % 64 == 0, d % 256 == 0. */
-int cox_grouped_down(const void* h, long long rows_cap, const int32_t* offsets, int n_groups,
-                     const int32_t* group_experts, const void* const* w2, int ff, int d, void* y_perm, void* stream);
-int cox_grouped_down_ex(const void* h, long long rows_cap, const int32_t* offsets, int n_groups,
-                        const int32_t* group_experts, const void* const* w2, int ff, int d, void* y_perm,
-                        int max_ctas, void* stream);
-
-/* Shared-expert down projection with K5 fused into its epilogue (prefill,
- * DeepSeek-style layers): out[t] = sum_{j<k} w[t,j] * y_perm[dst[t,j]]
- * + bf16(h_shared[t] W2s^T), the exact operation order of cox_combine with
- * shared = the shared expert's bf16 output, so the result is bit-identical to
- * cox_grouped_down(shared) followed by cox_combine — without writing and
- * re-reading the shared output or running the combine as its own pass.
- * Replaces `expert:merge` / `return_store` (sim.py:149-202,
- * costmodel.py:266-273) for layers with shared experts.  shared_offsets:
- * device int32 {0, T}; w2_shared [d, ff_shared]; y_perm/dst/w as cox_combine;
- * out [T, d] bf16.  d % 256 == 0, ff_shared % 64 == 0, 1 <= k <= 8. */
-int cox_shared_down_combine(const void* h_shared, int T, const int32_t* shared_offsets, const void* w2_shared,
-                            int ff_shared, int d, const void* y_perm, const int32_t* dst, const float* w, int k,
-                            void* out, void* stream);
+ * Same grouping arguments as cox_grouped_swiglu.  ff % 64 == 0, d % 256 == 0. */
+int cox_grouped_down(const void* h, long long rows_cap, const int32_t* offsets, int E, int n_groups,
+                     const int32_t* group_experts, const void* const* w2, int ff, int d, void* y_perm, int max_ctas,
+                     void* stream);
 
 /* K3+K4(+K5) for decode-size batches: ONE
  * persistent, weight-streaming launch runs the SwiGLU and the down projection
@@ -149,11 +118,12 @@ int cox_shared_down_combine(const void* h_shared, int T, const int32_t* shared_o
  * 128-column block combines that block for every token (device-side
  * counters, no launch boundaries).
  *   x [T, d]             the step's tokens (shared-expert input; gather source)
- *   row_tokens           source token of every permuted row (cox_permute_ex);
+ *   row_tokens           source token of every permuted row (cox_permute);
  *                        used when x_perm == NULL: the routed rows are gathered
  *                        from x by TMA tile::gather4, no x_perm copy
  *   x_perm [rows_cap, d] materialised permuted rows (or NULL, see above)
- *   offsets/w13/w2/h/y_perm as for cox_grouped_swiglu / cox_grouped_down
+ *   offsets [E+1] / group_experts / w13 / w2 / h / y_perm as for
+ *                        cox_grouped_swiglu / cox_grouped_down
  *   w13_shared [2*ff_shared, d] (interleaved), w2_shared [d, ff_shared],
  *   h_shared [T, ff_shared], y_shared [T, d]   (w13_shared == NULL: none)
  *   dst [T, k], w [T, k], out [T, d] bf16: fused combine
@@ -164,10 +134,10 @@ int cox_shared_down_combine(const void* h_shared, int T, const int32_t* shared_o
  * have <= 64 rows.  d % 128 == 0, ff % 128 == 0, ff_shared % 128 == 0,
  * n_groups <= 64. */
 int cox_small_expert_ffn(const void* x, int T, const int32_t* row_tokens, const void* x_perm, long long rows_cap,
-                         const int32_t* offsets, int n_groups, const int32_t* group_experts, const void* const* w13,
-                         const void* const* w2, int d, int ff, void* h, void* y_perm, const void* w13_shared,
-                         const void* w2_shared, int ff_shared, void* h_shared, void* y_shared, const int32_t* dst,
-                         const float* w, int k, void* out, void* stream);
+                         const int32_t* offsets, int E, int n_groups, const int32_t* group_experts,
+                         const void* const* w13, const void* const* w2, int d, int ff, void* h, void* y_perm,
+                         const void* w13_shared, const void* w2_shared, int ff_shared, void* h_shared,
+                         void* y_shared, const int32_t* dst, const float* w, int k, void* out, void* stream);
 
 /* Same decode-size expert stage straight from the router's output (no
  * permute launch): segments from counts[E] (expert-ascending, written to
@@ -193,26 +163,12 @@ int cox_small_expert_ffn_idx(const void* x, int T, const int32_t* idx, const int
  *   optional shared experts: w13_shared [2 ff_shared, d], w2_shared [d, ff_shared],
  *   h_shared [T, ff_shared], y_shared [T, d]
  *   idx [T, k] int32, w [T, k] fp32: the routing; out [T, d] bf16.
+ * Replaces the decode-phase `expert_stage_parts` (costmodel.py:368).
  * d % 128 == 0, ff % 128 == 0, ff_shared % 128 == 0. */
 int cox_decode_moe(const void* x, int T, const void* wg, int E, int k, int mode, const void* const* w13,
                    const void* const* w2, int d, int ff, const void* w13_shared, const void* w2_shared, int ff_shared,
                    void* h, void* y, void* h_shared, void* y_shared, int32_t* idx, float* w, void* out,
                    void* stream);
-
-/* The whole routed decode-step layer in ONE launch (T <= 256): the router
- * runs in the kernel's prologue (warp 2 of CTA b routes tokens b, b + grid, ...
- * in the canonical order of cox_router_topk, so idx/w are bit-identical) and
- * publishes a per-expert histogram; every CTA then derives the expert
- * segments, its copy of the stable permutation, and streams ONLY the touched
- * experts' weights, as cox_small_expert_ffn_idx — without the router launch
- * and its hand-off on the critical path.  Outputs idx/w [T, k] (router),
- * counts [E], dst [T, k], offsets [E + 1] (as cox_permute), out [T, d].
- * h [T*k, ff], y_perm [T*k, d] scratch; shared-expert operands optional.
- * Replaces the decode-phase `expert_stage_parts` (costmodel.py:368). */
-int cox_decode_moe_routed(const void* x, int T, const void* wg, int E, int k, int mode, const void* const* w13,
-                          const void* const* w2, int d, int ff, const void* w13_shared, const void* w2_shared,
-                          int ff_shared, void* h, void* y_perm, void* h_shared, void* y_shared, int32_t* idx,
-                          float* w, int32_t* counts, int32_t* dst, int32_t* offsets, void* out, void* stream);
 
 /* K5 — weighted top-k combine back to token order (+ optional shared-expert
  * output, DeepSeek-V2):  out[t] = sum_j w[t,j] * y_perm[dst[t,j]] (+ shared[t]).
@@ -227,14 +183,17 @@ int cox_combine(const void* y_perm, const int32_t* dst, const float* w, int T, i
  *   cox_ep_counts_put: counts[E] -> counts_all[rank][E] on every peer.
  *   cox_ep_offsets:    counts_all[world][E] -> my receive segments
  *                      recv_seg[E/world + 1] (one per local expert: all
- *                      sources' rows, source-rank order) and send_base[E]
- *                      (row of my first pair of expert e on its owner);
- *                      overflow[0] = 1 if any owner would receive more than
- *                      cap rows.
+ *                      sources' rows, source-rank order; clamped to cap) and
+ *                      send_base[E] (row of my first pair of expert e on its
+ *                      owner); overflow[0] = the largest receive count of any
+ *                      owner if it exceeds cap, else 0 (rewritten per launch;
+ *                      identical on every rank).
  *   cox_ep_dispatch:   stores x[t] into the owners' receive buffers at
  *                      send_base[e] + (dst_local - offsets_local[e]);
- *                      route_row[T,k] records the row for the combine.
- *   cox_ep_combine:    out[t] = sum_j w[t,j] * y_owner[route_row[t,j]] (bf16).
+ *                      route_row[T,k] records the row for the combine (-1:
+ *                      beyond cap, dropped).
+ *   cox_ep_combine:    out[t] = sum_j w[t,j] * y_owner[route_row[t,j]] (bf16;
+ *                      route_row < 0 contributes nothing).
  * dst_local/offsets_local come from cox_permute (x_perm may be NULL then). */
 int cox_ep_counts_put(const int32_t* counts, int E, int rank, int world, int32_t* const* peer_counts, void* stream);
 int cox_ep_offsets(const int32_t* counts_all, int world, int E, int rank, long long cap, int32_t* recv_seg,

@@ -26,6 +26,7 @@ _LIB = None
 
 _f32p = np.ctypeslib.ndpointer(dtype=np.float32, flags="C_CONTIGUOUS")
 _i32p = np.ctypeslib.ndpointer(dtype=np.int32, flags="C_CONTIGUOUS")
+_u16p = np.ctypeslib.ndpointer(dtype=np.uint16, flags="C_CONTIGUOUS")
 
 
 def build() -> Path:
@@ -44,6 +45,9 @@ def lib():
         L.oracle_router_topk.restype = ctypes.c_int
         L.oracle_router_topk.argtypes = [_f32p, _f32p, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                          ctypes.c_int, ctypes.c_void_p, _i32p, _f32p, _i32p]
+        L.oracle_router_topk_bf16.restype = ctypes.c_int
+        L.oracle_router_topk_bf16.argtypes = [_u16p, _f32p, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                              ctypes.c_int, ctypes.c_void_p, _i32p, _f32p, _i32p]
         L.oracle_router_logit.restype = ctypes.c_float
         L.oracle_router_logit.argtypes = [_f32p, _f32p, ctypes.c_int]
         L.oracle_permute.restype = ctypes.c_int
@@ -92,6 +96,22 @@ def router_topk(x, wg, k: int, mode: int = 0, want_logits: bool = False):
     if rc != 0:
         raise ValueError("oracle_router_topk: invalid arguments (d must be a multiple of 8, 1<=k<=E<=256)")
     return (idx, w, counts, logits) if want_logits else (idx, w, counts)
+
+
+def router_topk_bf16(x_bits, wg, k: int, mode: int = 0):
+    """Router over bf16 tokens given as their uint16 bit patterns [T, d] (exact
+    widening; same arithmetic as router_topk on the fp32 copy) — for full
+    batches: -> (idx, w, counts)."""
+    x_bits = np.ascontiguousarray(x_bits, dtype=np.uint16)
+    wg = _f32(wg)
+    T, d = x_bits.shape
+    E = wg.shape[0]
+    idx = np.zeros((T, k), np.int32)
+    w = np.zeros((T, k), np.float32)
+    counts = np.zeros(E, np.int32)
+    if lib().oracle_router_topk_bf16(x_bits, wg, T, d, E, k, mode, None, idx, w, counts) != 0:
+        raise ValueError("oracle_router_topk_bf16: invalid arguments")
+    return idx, w, counts
 
 
 def permute(idx, E: int, tile_m: int = 1):

@@ -24,10 +24,13 @@
  * ascending, starting from +0.0f.  The 32 partials are then combined by an xor
  * butterfly: for off in 16,8,4,2,1: p[l] = p[l] + p[l^off].  The result is p[0].
  *
- * Compiled with -ffp-contract=off (see Makefile) so no add is fused.
+ * Compiled with -ffp-contract=off (see Makefile) so no add is fused.  The
+ * token loop is OpenMP-parallel (tokens are independent; per-token arithmetic
+ * is unchanged), so full 262,144-token batches are checked in seconds.
  */
 #include <math.h>
 #include <stdint.h>
+#include <stdlib.h>
 #include <string.h>
 
 #define LANES 32
@@ -51,48 +54,91 @@ float oracle_router_logit(const float* x, const float* wg, int d) {
     return p[0];
 }
 
-/* mode 0: Mixtral (softmax over the k selected logits, i.e. renormalised top-k);
- * mode 1: DeepSeek-V2 (softmax over all E, selected probabilities, no renorm).
- * Selection is on logits (softmax is monotone); strict '>' keeps the lower index
- * on ties.  Returns 0, or -1 on invalid arguments. */
-int oracle_router_topk(const float* x, const float* wg, int T, int d, int E, int k, int mode,
-                       float* logits_out /* nullable [T,E] */, int32_t* idx, float* w,
-                       int32_t* counts /* [E], zeroed here */) {
+/* One token: logits -> top-k indices and weights; selected experts are
+ * added to cnt.  mode 0: Mixtral (softmax over the k selected logits, i.e.
+ * renormalised top-k); mode 1: DeepSeek-V2 (softmax over all E, selected
+ * probabilities, no renorm).  Selection is on logits (softmax is monotone);
+ * strict '>' keeps the lower index on ties. */
+static void route_token(const float* xt, const float* wg, int d, int E, int k, int mode, float* logits_out,
+                        int32_t* idx, float* w, int32_t* cnt) {
+    float lg[256];
+    unsigned char taken[256];
+    for (int e = 0; e < E; ++e) {
+        lg[e] = oracle_router_logit(xt, wg + (long)e * d, d);
+        if (isnan(lg[e])) lg[e] = -INFINITY; /* NaN ranks below every number (GPU: nan_low) */
+        if (logits_out) logits_out[e] = lg[e];
+        taken[e] = 0;
+    }
+    for (int j = 0; j < k; ++j) {
+        int best = -1;
+        float bv = 0.0f;
+        for (int e = 0; e < E; ++e) {
+            if (taken[e]) continue;
+            if (best < 0 || lg[e] > bv) { best = e; bv = lg[e]; }
+        }
+        taken[best] = 1;
+        idx[j] = best;
+        cnt[best] += 1;
+    }
+    float m = lg[idx[0]];
+    if (mode == 0) {
+        float s = 0.0f;
+        for (int j = 0; j < k; ++j) s = s + expf(lg[idx[j]] - m);
+        for (int j = 0; j < k; ++j) w[j] = expf(lg[idx[j]] - m) / s;
+    } else {
+        float s = 0.0f;
+        for (int e = 0; e < E; ++e) s = s + expf(lg[e] - m);
+        for (int j = 0; j < k; ++j) w[j] = expf(lg[idx[j]] - m) / s;
+    }
+}
+
+/* Tokens are independent: the token loop runs on OpenMP threads (each token's
+ * arithmetic is unchanged; counts are integer sums, order-free).  x is fp32
+ * (x_bf16 == NULL) or bf16 bit patterns (x == NULL), widened exactly. */
+static int router_topk_impl(const float* x, const uint16_t* x_bf16, const float* wg, int T, int d, int E, int k,
+                            int mode, float* logits_out, int32_t* idx, float* w, int32_t* counts) {
     if (T < 0 || d <= 0 || (d % 8) != 0 || E <= 0 || E > 256 || k <= 0 || k > E || (mode != 0 && mode != 1))
         return -1;
     for (int e = 0; e < E; ++e) counts[e] = 0;
-    float lg[256];
-    unsigned char taken[256];
-    for (long t = 0; t < T; ++t) {
-        for (int e = 0; e < E; ++e) {
-            lg[e] = oracle_router_logit(x + t * (long)d, wg + (long)e * d, d);
-            if (isnan(lg[e])) lg[e] = -INFINITY; /* NaN ranks below every number (GPU: nan_low) */
-            if (logits_out) logits_out[t * E + e] = lg[e];
-            taken[e] = 0;
-        }
-        for (int j = 0; j < k; ++j) {
-            int best = -1;
-            float bv = 0.0f;
-            for (int e = 0; e < E; ++e) {
-                if (taken[e]) continue;
-                if (best < 0 || lg[e] > bv) { best = e; bv = lg[e]; }
+#pragma omp parallel
+    {
+        int32_t cnt[256];
+        for (int e = 0; e < E; ++e) cnt[e] = 0;
+        float* row = x_bf16 ? (float*)malloc(sizeof(float) * (size_t)d) : NULL;
+#pragma omp for schedule(static)
+        for (long t = 0; t < T; ++t) {
+            const float* xt;
+            if (x_bf16) {
+                const uint16_t* src = x_bf16 + t * (long)d;
+                for (int i = 0; i < d; ++i) {
+                    uint32_t u = (uint32_t)src[i] << 16;
+                    memcpy(row + i, &u, 4);
+                }
+                xt = row;
+            } else {
+                xt = x + t * (long)d;
             }
-            taken[best] = 1;
-            idx[t * k + j] = best;
-            counts[best] += 1;
+            route_token(xt, wg, d, E, k, mode, logits_out ? logits_out + t * E : NULL, idx + t * k, w + t * k, cnt);
         }
-        float m = lg[idx[t * k]];
-        if (mode == 0) {
-            float s = 0.0f;
-            for (int j = 0; j < k; ++j) s = s + expf(lg[idx[t * k + j]] - m);
-            for (int j = 0; j < k; ++j) w[t * k + j] = expf(lg[idx[t * k + j]] - m) / s;
-        } else {
-            float s = 0.0f;
-            for (int e = 0; e < E; ++e) s = s + expf(lg[e] - m);
-            for (int j = 0; j < k; ++j) w[t * k + j] = expf(lg[idx[t * k + j]] - m) / s;
-        }
+#pragma omp critical
+        for (int e = 0; e < E; ++e) counts[e] += cnt[e];
+        free(row);
     }
     return 0;
+}
+
+/* Returns 0, or -1 on invalid arguments. */
+int oracle_router_topk(const float* x, const float* wg, int T, int d, int E, int k, int mode,
+                       float* logits_out /* nullable [T,E] */, int32_t* idx, float* w,
+                       int32_t* counts /* [E], zeroed here */) {
+    return router_topk_impl(x, NULL, wg, T, d, E, k, mode, logits_out, idx, w, counts);
+}
+
+/* Same over bf16 tokens (bit patterns), e.g. a full 262,144-token batch
+ * without a 4-byte copy of it. */
+int oracle_router_topk_bf16(const uint16_t* x, const float* wg, int T, int d, int E, int k, int mode,
+                            float* logits_out, int32_t* idx, float* w, int32_t* counts) {
+    return router_topk_impl(NULL, x, wg, T, d, E, k, mode, logits_out, idx, w, counts);
 }
 
 /* Stable permutation by expert: within expert e the (t, j) pairs appear in

@@ -28,13 +28,12 @@ ROUTE_DEEPSEEK = 1
 
 # Every symbol include/coxmoe.h declares (tests check the .so exports them all).
 EXPORTS = (
-    "cox_last_error", "cox_version", "cox_device_check", "cox_router_topk", "cox_permute_workspace_bytes",
-    "cox_permute", "cox_grouped_swiglu", "cox_grouped_down", "cox_combine", "cox_interleave_w13",
-    "cox_ep_counts_put", "cox_ep_offsets", "cox_ep_dispatch", "cox_ep_combine", "cox_grouped_swiglu_ex",
-    "cox_grouped_down_ex", "cox_router_topk_ex", "cox_permute_ex", "cox_grouped_swiglu_gather",
-    "cox_small_expert_ffn", "cox_decode_moe", "cox_small_expert_ffn_idx", "cox_shared_down_combine",
-    "cox_decode_moe_routed",
+    "cox_last_error", "cox_version", "cox_device_check", "cox_router_workspace_bytes", "cox_router_topk",
+    "cox_permute_workspace_bytes", "cox_permute", "cox_grouped_swiglu", "cox_grouped_down",
+    "cox_small_expert_ffn", "cox_small_expert_ffn_idx", "cox_decode_moe", "cox_combine", "cox_ep_counts_put",
+    "cox_ep_offsets", "cox_ep_dispatch", "cox_ep_combine", "cox_interleave_w13",
 )
+ABI_VERSION = 2
 
 _lock = threading.Lock()
 _lib = None
@@ -47,73 +46,44 @@ class CoxError(RuntimeError):
 
 def _declare(L):
     c_int, c_void_p, c_ll, c_size_t = ctypes.c_int, ctypes.c_void_p, ctypes.c_longlong, ctypes.c_size_t
+    P = c_void_p
     L.cox_last_error.restype = ctypes.c_char_p
     L.cox_last_error.argtypes = []
     L.cox_version.restype = c_int
     L.cox_device_check.restype = c_int
+    L.cox_router_workspace_bytes.restype = c_size_t
+    L.cox_router_workspace_bytes.argtypes = [c_int, c_int]
     L.cox_router_topk.restype = c_int
-    L.cox_router_topk.argtypes = [c_void_p, c_int, c_void_p, c_int, c_int, c_int, c_int, c_int,
-                                  c_void_p, c_void_p, c_void_p, c_void_p]
-    L.cox_router_topk_ex.restype = c_int
-    L.cox_router_topk_ex.argtypes = [c_void_p, c_int, c_void_p, c_int, c_int, c_int, c_int, c_int, c_int,
-                                     c_void_p, c_void_p, c_void_p, c_void_p]
-    L.cox_permute_ex.restype = c_int
-    L.cox_permute_ex.argtypes = [c_void_p, c_int, c_int, c_int, c_int, c_void_p, c_int, c_void_p, c_void_p,
-                                 c_void_p, c_ll, c_void_p, c_void_p, c_void_p]
-    L.cox_grouped_swiglu_gather.restype = c_int
-    L.cox_grouped_swiglu_gather.argtypes = [c_void_p, c_ll, c_void_p, c_ll, c_void_p, c_int, c_void_p, c_void_p,
-                                            c_int, c_int, c_void_p, c_int, c_void_p]
+    L.cox_router_topk.argtypes = [P, c_int, P, c_int, c_int, c_int, c_int, c_int, c_int, P, P, P, P, c_size_t, P]
     L.cox_permute_workspace_bytes.restype = c_size_t
     L.cox_permute_workspace_bytes.argtypes = [c_int, c_int]
     L.cox_permute.restype = c_int
-    L.cox_permute.argtypes = [c_void_p, c_int, c_int, c_int, c_int, c_void_p, c_int, c_void_p, c_void_p,
-                              c_void_p, c_ll, c_void_p, c_void_p]
+    L.cox_permute.argtypes = [P, c_int, c_int, c_int, c_int, P, c_int, P, P, P, c_ll, P, P, P]
     L.cox_grouped_swiglu.restype = c_int
-    L.cox_grouped_swiglu.argtypes = [c_void_p, c_ll, c_void_p, c_int, c_void_p, c_void_p, c_int, c_int,
-                                     c_void_p, c_void_p]
+    L.cox_grouped_swiglu.argtypes = [P, c_ll, P, c_int, c_int, P, P, c_int, c_int, P, c_int, P]
     L.cox_grouped_down.restype = c_int
-    L.cox_grouped_down.argtypes = [c_void_p, c_ll, c_void_p, c_int, c_void_p, c_void_p, c_int, c_int,
-                                   c_void_p, c_void_p]
-    L.cox_grouped_swiglu_ex.restype = c_int
-    L.cox_grouped_swiglu_ex.argtypes = [c_void_p, c_ll, c_void_p, c_int, c_void_p, c_void_p, c_int, c_int,
-                                        c_void_p, c_int, c_void_p]
-    L.cox_grouped_down_ex.restype = c_int
-    L.cox_grouped_down_ex.argtypes = [c_void_p, c_ll, c_void_p, c_int, c_void_p, c_void_p, c_int, c_int,
-                                      c_void_p, c_int, c_void_p]
-    L.cox_decode_moe_routed.restype = c_int
-    L.cox_decode_moe_routed.argtypes = [c_void_p, c_int, c_void_p, c_int, c_int, c_int, c_void_p, c_void_p, c_int,
-                                        c_int, c_void_p, c_void_p, c_int, c_void_p, c_void_p, c_void_p, c_void_p,
-                                        c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]
-    L.cox_shared_down_combine.restype = c_int
-    L.cox_shared_down_combine.argtypes = [c_void_p, c_int, c_void_p, c_void_p, c_int, c_int, c_void_p, c_void_p,
-                                          c_void_p, c_int, c_void_p, c_void_p]
+    L.cox_grouped_down.argtypes = [P, c_ll, P, c_int, c_int, P, P, c_int, c_int, P, c_int, P]
     L.cox_small_expert_ffn.restype = c_int
-    L.cox_small_expert_ffn.argtypes = [c_void_p, c_int, c_void_p, c_void_p, c_ll, c_void_p, c_int, c_void_p,
-                                       c_void_p, c_void_p, c_int, c_int, c_void_p, c_void_p, c_void_p, c_void_p,
-                                       c_int, c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_void_p, c_void_p]
+    L.cox_small_expert_ffn.argtypes = [P, c_int, P, P, c_ll, P, c_int, c_int, P, P, P, c_int, c_int, P, P, P, P,
+                                       c_int, P, P, P, P, c_int, P, P]
     L.cox_small_expert_ffn_idx.restype = c_int
-    L.cox_small_expert_ffn_idx.argtypes = [c_void_p, c_int, c_void_p, c_void_p, c_int, c_void_p, c_int, c_void_p,
-                                           c_void_p, c_int, c_int, c_void_p, c_void_p, c_void_p, c_void_p, c_int,
-                                           c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]
+    L.cox_small_expert_ffn_idx.argtypes = [P, c_int, P, P, c_int, P, c_int, P, P, c_int, c_int, P, P, P, P, c_int,
+                                           P, P, P, P, P, P]
     L.cox_decode_moe.restype = c_int
-    L.cox_decode_moe.argtypes = [c_void_p, c_int, c_void_p, c_int, c_int, c_int, c_void_p, c_void_p, c_int, c_int,
-                                 c_void_p, c_void_p, c_int, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
-                                 c_void_p, c_void_p, c_void_p]
+    L.cox_decode_moe.argtypes = [P, c_int, P, c_int, c_int, c_int, P, P, c_int, c_int, P, P, c_int, P, P, P, P, P,
+                                 P, P, P]
     L.cox_combine.restype = c_int
-    L.cox_combine.argtypes = [c_void_p, c_void_p, c_void_p, c_int, c_int, c_int, c_void_p, c_void_p, c_int,
-                              c_void_p]
+    L.cox_combine.argtypes = [P, P, P, c_int, c_int, c_int, P, P, c_int, P]
     L.cox_ep_counts_put.restype = c_int
-    L.cox_ep_counts_put.argtypes = [c_void_p, c_int, c_int, c_int, c_void_p, c_void_p]
+    L.cox_ep_counts_put.argtypes = [P, c_int, c_int, c_int, P, P]
     L.cox_ep_offsets.restype = c_int
-    L.cox_ep_offsets.argtypes = [c_void_p, c_int, c_int, c_int, c_ll, c_void_p, c_void_p, c_void_p, c_void_p]
+    L.cox_ep_offsets.argtypes = [P, c_int, c_int, c_int, c_ll, P, P, P, P]
     L.cox_ep_dispatch.restype = c_int
-    L.cox_ep_dispatch.argtypes = [c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_int, c_int, c_int, c_ll,
-                                  c_void_p, c_int, c_void_p, c_void_p, c_void_p]
+    L.cox_ep_dispatch.argtypes = [P, P, P, P, c_int, c_int, c_int, c_int, c_ll, P, c_int, P, P, P]
     L.cox_ep_combine.restype = c_int
-    L.cox_ep_combine.argtypes = [c_void_p, c_void_p, c_void_p, c_int, c_int, c_int, c_int, c_int, c_void_p,
-                                 c_void_p, c_void_p]
+    L.cox_ep_combine.argtypes = [P, P, P, c_int, c_int, c_int, c_int, c_int, P, P, P]
     L.cox_interleave_w13.restype = c_int
-    L.cox_interleave_w13.argtypes = [c_void_p, c_void_p, c_int, c_int, c_void_p, c_void_p]
+    L.cox_interleave_w13.argtypes = [P, P, c_int, c_int, P, P]
 
 
 def load(path: Path | None = None):
@@ -126,6 +96,8 @@ def load(path: Path | None = None):
                 raise CoxError(f"{p} is missing: run __graft_entry__.build() (no CPU fallback exists)")
             L = ctypes.CDLL(str(p))
             _declare(L)
+            if L.cox_version() != ABI_VERSION:
+                raise CoxError(f"{p}: ABI version {L.cox_version()} != {ABI_VERSION}: rebuild the library")
             _lib = L
     return _lib
 

@@ -1,5 +1,6 @@
 // C ABI (include/coxmoe.h): argument validation, error reporting, dispatch.
 #include <cstdarg>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -8,16 +9,16 @@
 #include "common.cuh"
 
 namespace cox {
+size_t router_workspace_bytes(int T, int E);
 int launch_router(const void* x, int x_is_bf16, const void* wg, int wg_is_bf16, int T, int d, int E, int k,
-                  int mode, int32_t* idx, float* w, int32_t* counts, cudaStream_t s);
+                  int mode, int32_t* idx, float* w, int32_t* counts, void* ws, int tc, cudaStream_t s);
 size_t permute_workspace_bytes(int T, int E);
 int launch_permute(const int32_t* idx, int T, int k, int E, int tile_m, const void* x, int d, int32_t* offsets,
                    int32_t* dst, void* x_perm, void* workspace, cudaStream_t s, int32_t* row_tokens = nullptr,
                    long long rows_cap = 0);
 int launch_grouped_gemm(int epi, const void* A, long long rows_cap, int K, const int32_t* offsets, int n_groups,
                         const int32_t* group_expert, const void* const* B, int N, void* out, long long ldo,
-                        int max_ctas, cudaStream_t s, const int32_t* a_rows = nullptr, long long a_rows_cap = 0,
-                        const GemmCombine* cmb = nullptr);
+                        int max_ctas, cudaStream_t s);
 struct SmallDense {
   const void* wg;
   int E, mode;
@@ -92,7 +93,7 @@ extern "C" {
 
 const char* cox_last_error(void) { return g_err.c_str(); }
 
-int cox_version(void) { return 1; }
+int cox_version(void) { return 2; }
 
 int cox_device_check(void) {
   int dev = 0, major = 0, minor = 0;
@@ -104,30 +105,41 @@ int cox_device_check(void) {
   return 0;
 }
 
-int cox_router_topk_ex(const void* x, int x_dtype, const void* wg, int wg_dtype, int T, int d, int E, int k,
-                       int mode, int32_t* idx, float* w, int32_t* counts, void* stream) {
-  if (T < 0 || d <= 0 || d % 8 || E <= 0 || E > 256 || k < 1 || k > E || k > 8)
-    return fail(COX_EINVAL, "cox_router_topk: need T>=0, d%%8==0, 1<=k<=min(E,8), E<=256 (T=%d d=%d E=%d k=%d)", T, d,
-                E, k);
-  if (mode != COX_ROUTE_MIXTRAL && mode != COX_ROUTE_DEEPSEEK) return fail(COX_EINVAL, "cox_router_topk: bad mode %d", mode);
-  if (x_dtype != COX_DTYPE_BF16 && x_dtype != COX_DTYPE_F32) return fail(COX_EINVAL, "cox_router_topk: bad x_dtype");
-  if (wg_dtype != COX_DTYPE_BF16 && wg_dtype != COX_DTYPE_F32) return fail(COX_EINVAL, "cox_router_topk: bad wg_dtype");
-  if (T > 0 && (!x || !wg || !idx || !w || !counts)) return fail(COX_EINVAL, "cox_router_topk: null pointer");
-  if (!aligned16(x) || !aligned16(wg)) return fail(COX_EINVAL, "cox_router_topk: x and wg must be 16-byte aligned");
-  int rc = cox::launch_router(x, x_dtype == COX_DTYPE_BF16, wg, wg_dtype == COX_DTYPE_BF16, T, d, E, k, mode, idx, w,
-                              counts, static_cast<cudaStream_t>(stream));
-  return cuda_status(rc, "cox_router_topk");
+size_t cox_router_workspace_bytes(int T, int E) { return cox::router_workspace_bytes(T, E); }
+
+// COX_ROUTER_TC: test/A-B override of the tensor-core screen (0 never, 1 whenever the shape allows)
+static int router_tc_mode() {
+  static const int m = [] {
+    const char* e = getenv("COX_ROUTER_TC");
+    return e ? (atoi(e) ? 1 : 0) : -1;
+  }();
+  return m;
 }
 
-int cox_router_topk(const void* x, int x_dtype, const float* wg, int T, int d, int E, int k, int mode,
-                    int32_t* idx, float* w, int32_t* counts, void* stream) {
-  return cox_router_topk_ex(x, x_dtype, wg, COX_DTYPE_F32, T, d, E, k, mode, idx, w, counts, stream);
+int cox_router_topk(const void* x, int x_dtype, const void* wg, int wg_dtype, int T, int d, int E, int k, int mode,
+                    int32_t* idx, float* w, int32_t* counts, void* workspace, size_t workspace_bytes,
+                    void* stream) {
+  const char* fn = "cox_router_topk";
+  if (T < 0 || d <= 0 || d % 8 || E <= 0 || E > 256 || k < 1 || k > E || k > 8)
+    return fail(COX_EINVAL, "%s: need T>=0, d%%8==0, 1<=k<=min(E,8), E<=256 (T=%d d=%d E=%d k=%d)", fn, T, d, E, k);
+  if (mode != COX_ROUTE_MIXTRAL && mode != COX_ROUTE_DEEPSEEK) return fail(COX_EINVAL, "%s: bad mode %d", fn, mode);
+  if (x_dtype != COX_DTYPE_BF16 && x_dtype != COX_DTYPE_F32) return fail(COX_EINVAL, "%s: bad x_dtype", fn);
+  if (wg_dtype != COX_DTYPE_BF16 && wg_dtype != COX_DTYPE_F32) return fail(COX_EINVAL, "%s: bad wg_dtype", fn);
+  if (!counts || (T > 0 && (!x || !wg || !idx || !w))) return fail(COX_EINVAL, "%s: null pointer", fn);
+  if (!aligned16(x) || !aligned16(wg)) return fail(COX_EINVAL, "%s: x and wg must be 16-byte aligned", fn);
+  const size_t need = cox::router_workspace_bytes(T, E);
+  if (!workspace || !aligned16(workspace) || workspace_bytes < need)
+    return fail(COX_EINVAL, "%s: workspace of %zu bytes (16-byte aligned) required, got %zu", fn, need,
+                workspace_bytes);
+  int rc = cox::launch_router(x, x_dtype == COX_DTYPE_BF16, wg, wg_dtype == COX_DTYPE_BF16, T, d, E, k, mode, idx, w,
+                              counts, workspace, router_tc_mode(), static_cast<cudaStream_t>(stream));
+  return cuda_status(rc, fn);
 }
 
 size_t cox_permute_workspace_bytes(int T, int E) { return cox::permute_workspace_bytes(T, E); }
 
-int cox_permute_ex(const int32_t* idx, int T, int k, int E, int tile_m, const void* x, int d, int32_t* offsets,
-                   int32_t* dst, void* x_perm, long long rows_cap, int32_t* row_tokens, void* workspace, void* stream) {
+int cox_permute(const int32_t* idx, int T, int k, int E, int tile_m, const void* x, int d, int32_t* offsets,
+                int32_t* dst, void* x_perm, long long rows_cap, int32_t* row_tokens, void* workspace, void* stream) {
   if (T < 0 || k < 1 || k > 8 || E < 1 || E > 256 || tile_m < 1 || d <= 0 || d % 8)
     return fail(COX_EINVAL, "cox_permute: need 1<=k<=8, 1<=E<=256, tile_m>=1, d%%8==0");
   if (rows_cap < (long long)T * k + (long long)E * (tile_m - 1))
@@ -141,97 +153,56 @@ int cox_permute_ex(const int32_t* idx, int T, int k, int E, int tile_m, const vo
   return cuda_status(rc, "cox_permute");
 }
 
-int cox_permute(const int32_t* idx, int T, int k, int E, int tile_m, const void* x, int d, int32_t* offsets,
-                int32_t* dst, void* x_perm, long long rows_cap, void* workspace, void* stream) {
-  return cox_permute_ex(idx, T, k, E, tile_m, x, d, offsets, dst, x_perm, rows_cap, nullptr, workspace, stream);
-}
-
-static int check_groups(const char* fn, int n_groups, const int32_t* group_experts, const void* const* w) {
+// Every group's expert id must name a segment of offsets[E + 1]: the kernels
+// read offsets[e] and offsets[e + 1].
+static int check_groups(const char* fn, int E, int n_groups, const int32_t* group_experts, const void* const* w) {
   if (n_groups < 0 || n_groups > 64) return fail(COX_EINVAL, "%s: n_groups must be in [0, 64]", fn);
+  if (n_groups > 0 && (E < 1 || !group_experts || !w)) return fail(COX_EINVAL, "%s: need E >= 1 and the group tables", fn);
   for (int g = 0; g < n_groups; ++g) {
-    if (group_experts[g] < 0) return fail(COX_EINVAL, "%s: negative expert id", fn);
+    if (group_experts[g] < 0 || group_experts[g] >= E)
+      return fail(COX_EINVAL, "%s: group %d names expert %d outside [0, %d)", fn, g, group_experts[g], E);
     if (!w[g] || !aligned16(w[g])) return fail(COX_EINVAL, "%s: weight pointer %d null or unaligned", fn, g);
   }
   return 0;
 }
 
-int cox_grouped_swiglu_ex(const void* x_perm, long long rows_cap, const int32_t* offsets, int n_groups,
-                          const int32_t* group_experts, const void* const* w13, int d, int ff, void* h,
-                          int max_ctas, void* stream) {
+int cox_grouped_swiglu(const void* x_perm, long long rows_cap, const int32_t* offsets, int E, int n_groups,
+                       const int32_t* group_experts, const void* const* w13, int d, int ff, void* h, int max_ctas,
+                       void* stream) {
+  const char* fn = "cox_grouped_swiglu";
   if (d <= 0 || d % 64 || ff <= 0 || ff % 128)
-    return fail(COX_EINVAL, "cox_grouped_swiglu: need d%%64==0 and ff%%128==0 (d=%d ff=%d)", d, ff);
-  if (rows_cap < 1) return fail(COX_EINVAL, "cox_grouped_swiglu: rows_cap < 1");
-  if (max_ctas < 0 || max_ctas == 1) return fail(COX_EINVAL, "cox_grouped_swiglu: max_ctas must be 0 or >= 2");
-  if (!aligned16(x_perm) || !aligned16(h)) return fail(COX_EINVAL, "cox_grouped_swiglu: unaligned x_perm/h");
-  if (int rc = check_groups("cox_grouped_swiglu", n_groups, group_experts, w13)) return rc;
+    return fail(COX_EINVAL, "%s: need d%%64==0 and ff%%128==0 (d=%d ff=%d)", fn, d, ff);
+  if (rows_cap < 1) return fail(COX_EINVAL, "%s: rows_cap < 1", fn);
+  if (max_ctas < 0 || max_ctas == 1) return fail(COX_EINVAL, "%s: max_ctas must be 0 or >= 2", fn);
+  if (!aligned16(x_perm) || !aligned16(h)) return fail(COX_EINVAL, "%s: unaligned x_perm/h", fn);
+  if (int rc = check_groups(fn, E, n_groups, group_experts, w13)) return rc;
+  if (n_groups > 0 && (!x_perm || !h || !offsets)) return fail(COX_EINVAL, "%s: null x_perm/h/offsets", fn);
   int rc = cox::launch_grouped_gemm(0, x_perm, rows_cap, d, offsets, n_groups, group_experts, w13, 2 * ff, h, ff,
                                     max_ctas, static_cast<cudaStream_t>(stream));
-  return cuda_status(rc, "cox_grouped_swiglu");
+  return cuda_status(rc, fn);
 }
 
-int cox_grouped_swiglu_gather(const void* x, long long T, const int32_t* row_tokens, long long rows_cap,
-                              const int32_t* offsets, int n_groups, const int32_t* group_experts,
-                              const void* const* w13, int d, int ff, void* h, int max_ctas, void* stream) {
-  if (d <= 0 || d % 64 || ff <= 0 || ff % 128)
-    return fail(COX_EINVAL, "cox_grouped_swiglu_gather: need d%%64==0 and ff%%128==0 (d=%d ff=%d)", d, ff);
-  if (T < 1 || rows_cap < 1 || !row_tokens) return fail(COX_EINVAL, "cox_grouped_swiglu_gather: empty input");
-  if (max_ctas < 0 || max_ctas == 1) return fail(COX_EINVAL, "cox_grouped_swiglu_gather: bad max_ctas");
-  if (!aligned16(x) || !aligned16(h)) return fail(COX_EINVAL, "cox_grouped_swiglu_gather: unaligned x/h");
-  if (int rc = check_groups("cox_grouped_swiglu_gather", n_groups, group_experts, w13)) return rc;
-  int rc = cox::launch_grouped_gemm(0, x, T, d, offsets, n_groups, group_experts, w13, 2 * ff, h, ff, max_ctas,
-                                    static_cast<cudaStream_t>(stream), row_tokens, rows_cap);
-  return cuda_status(rc, "cox_grouped_swiglu_gather");
-}
-
-int cox_grouped_swiglu(const void* x_perm, long long rows_cap, const int32_t* offsets, int n_groups,
-                       const int32_t* group_experts, const void* const* w13, int d, int ff, void* h, void* stream) {
-  return cox_grouped_swiglu_ex(x_perm, rows_cap, offsets, n_groups, group_experts, w13, d, ff, h, 0, stream);
-}
-
-int cox_grouped_down_ex(const void* h, long long rows_cap, const int32_t* offsets, int n_groups,
-                        const int32_t* group_experts, const void* const* w2, int ff, int d, void* y_perm,
-                        int max_ctas, void* stream) {
+int cox_grouped_down(const void* h, long long rows_cap, const int32_t* offsets, int E, int n_groups,
+                     const int32_t* group_experts, const void* const* w2, int ff, int d, void* y_perm, int max_ctas,
+                     void* stream) {
+  const char* fn = "cox_grouped_down";
   if (d <= 0 || d % 256 || ff <= 0 || ff % 64)
-    return fail(COX_EINVAL, "cox_grouped_down: need d%%256==0 and ff%%64==0 (d=%d ff=%d)", d, ff);
-  if (rows_cap < 1) return fail(COX_EINVAL, "cox_grouped_down: rows_cap < 1");
-  if (max_ctas < 0 || max_ctas == 1) return fail(COX_EINVAL, "cox_grouped_down: max_ctas must be 0 or >= 2");
-  if (!aligned16(h) || !aligned16(y_perm)) return fail(COX_EINVAL, "cox_grouped_down: unaligned h/y_perm");
-  if (int rc = check_groups("cox_grouped_down", n_groups, group_experts, w2)) return rc;
+    return fail(COX_EINVAL, "%s: need d%%256==0 and ff%%64==0 (d=%d ff=%d)", fn, d, ff);
+  if (rows_cap < 1) return fail(COX_EINVAL, "%s: rows_cap < 1", fn);
+  if (max_ctas < 0 || max_ctas == 1) return fail(COX_EINVAL, "%s: max_ctas must be 0 or >= 2", fn);
+  if (!aligned16(h) || !aligned16(y_perm)) return fail(COX_EINVAL, "%s: unaligned h/y_perm", fn);
+  if (int rc = check_groups(fn, E, n_groups, group_experts, w2)) return rc;
+  if (n_groups > 0 && (!h || !y_perm || !offsets)) return fail(COX_EINVAL, "%s: null h/y_perm/offsets", fn);
   int rc = cox::launch_grouped_gemm(1, h, rows_cap, ff, offsets, n_groups, group_experts, w2, d, y_perm, d, max_ctas,
                                     static_cast<cudaStream_t>(stream));
-  return cuda_status(rc, "cox_grouped_down");
-}
-
-int cox_grouped_down(const void* h, long long rows_cap, const int32_t* offsets, int n_groups,
-                     const int32_t* group_experts, const void* const* w2, int ff, int d, void* y_perm, void* stream) {
-  return cox_grouped_down_ex(h, rows_cap, offsets, n_groups, group_experts, w2, ff, d, y_perm, 0, stream);
-}
-
-int cox_shared_down_combine(const void* h_shared, int T, const int32_t* shared_offsets, const void* w2_shared,
-                            int ff_shared, int d, const void* y_perm, const int32_t* dst, const float* w, int k,
-                            void* out, void* stream) {
-  const char* fn = "cox_shared_down_combine";
-  if (d <= 0 || d % 256 || ff_shared <= 0 || ff_shared % 64)
-    return fail(COX_EINVAL, "%s: need d%%256==0 and ff_shared%%64==0 (d=%d ff_shared=%d)", fn, d, ff_shared);
-  if (T < 0 || k < 1 || k > 8) return fail(COX_EINVAL, "%s: need T >= 0 and 1 <= k <= 8 (T=%d k=%d)", fn, T, k);
-  if (T == 0) return 0;
-  if (!h_shared || !shared_offsets || !w2_shared || !y_perm || !dst || !w || !out)
-    return fail(COX_EINVAL, "%s: null pointer", fn);
-  if (!aligned16(h_shared) || !aligned16(w2_shared) || !aligned16(y_perm) || !aligned16(out))
-    return fail(COX_EINVAL, "%s: unaligned h_shared/w2_shared/y_perm/out", fn);
-  const int32_t g0 = 0;
-  const void* b[1] = {w2_shared};
-  cox::GemmCombine cmb{y_perm, dst, w, k};
-  int rc = cox::launch_grouped_gemm(2, h_shared, T, ff_shared, shared_offsets, 1, &g0, b, d, out, d, 0,
-                                    static_cast<cudaStream_t>(stream), nullptr, 0, &cmb);
   return cuda_status(rc, fn);
 }
 
 int cox_small_expert_ffn(const void* x, int T, const int32_t* row_tokens, const void* x_perm, long long rows_cap,
-                         const int32_t* offsets, int n_groups, const int32_t* group_experts, const void* const* w13,
-                         const void* const* w2, int d, int ff, void* h, void* y_perm, const void* w13_shared,
-                         const void* w2_shared, int ff_shared, void* h_shared, void* y_shared, const int32_t* dst,
-                         const float* w, int k, void* out, void* stream) {
+                         const int32_t* offsets, int E, int n_groups, const int32_t* group_experts,
+                         const void* const* w13, const void* const* w2, int d, int ff, void* h, void* y_perm,
+                         const void* w13_shared, const void* w2_shared, int ff_shared, void* h_shared,
+                         void* y_shared, const int32_t* dst, const float* w, int k, void* out, void* stream) {
   const char* fn = "cox_small_expert_ffn";
   if (T < 0 || d <= 0 || d % 128) return fail(COX_EINVAL, "%s: need T >= 0 and d %% 128 == 0 (d=%d)", fn, d);
   if (T > 0 && (!x || !aligned16(x))) return fail(COX_EINVAL, "%s: x null or unaligned", fn);
@@ -242,8 +213,8 @@ int cox_small_expert_ffn(const void* x, int T, const int32_t* row_tokens, const 
     if (!h || !y_perm || !aligned16(x_perm) || !aligned16(h) || !aligned16(y_perm))
       return fail(COX_EINVAL, "%s: null or unaligned x_perm/h/y_perm", fn);
   }
-  if (int rc = check_groups(fn, n_groups, group_experts, w13)) return rc;
-  if (int rc = check_groups(fn, n_groups, group_experts, w2)) return rc;
+  if (int rc = check_groups(fn, E, n_groups, group_experts, w13)) return rc;
+  if (int rc = check_groups(fn, E, n_groups, group_experts, w2)) return rc;
   if (w13_shared) {
     if (ff_shared <= 0 || ff_shared % 128)
       return fail(COX_EINVAL, "%s: need ff_shared %% 128 == 0 (ff_shared=%d)", fn, ff_shared);
@@ -277,8 +248,8 @@ int cox_small_expert_ffn_idx(const void* x, int T, const int32_t* idx, const int
     return fail(COX_EINVAL, "%s: bad shared-expert operands", fn);
   int32_t ids[64];
   for (int e = 0; e < E; ++e) ids[e] = e;
-  if (int rc = check_groups(fn, E, ids, w13)) return rc;
-  if (int rc = check_groups(fn, E, ids, w2)) return rc;
+  if (int rc = check_groups(fn, E, E, ids, w13)) return rc;
+  if (int rc = check_groups(fn, E, E, ids, w2)) return rc;
   cox::SmallIdx fi{idx, counts, E, dst, offsets};
   int rc = cox::launch_small_ffn(x, T, nullptr, nullptr, (long long)T * k, nullptr, E, ids, w13, w2, d, ff, h,
                                  y_perm, w13_shared, w2_shared, ff_shared, h_shared, y_shared, dst, w, k, out, 3,
@@ -303,40 +274,12 @@ int cox_decode_moe(const void* x, int T, const void* wg, int E, int k, int mode,
     return fail(COX_EINVAL, "%s: bad shared-expert operands", fn);
   int32_t ids[64];
   for (int e = 0; e < E; ++e) ids[e] = e;
-  if (int rc = check_groups(fn, E, ids, w13)) return rc;
-  if (int rc = check_groups(fn, E, ids, w2)) return rc;
+  if (int rc = check_groups(fn, E, E, ids, w13)) return rc;
+  if (int rc = check_groups(fn, E, E, ids, w2)) return rc;
   cox::SmallDense dn{wg, E, mode, idx, w};
   int rc = cox::launch_small_ffn(x, T, nullptr, nullptr, (long long)E * T, nullptr, E, ids, w13, w2, d, ff, h, y,
                                  w13_shared, w2_shared, ff_shared, h_shared, y_shared, nullptr, nullptr, k, out, 3,
                                  static_cast<cudaStream_t>(stream), &dn);
-  return cuda_status(rc, fn);
-}
-
-int cox_decode_moe_routed(const void* x, int T, const void* wg, int E, int k, int mode, const void* const* w13,
-                          const void* const* w2, int d, int ff, const void* w13_shared, const void* w2_shared,
-                          int ff_shared, void* h, void* y_perm, void* h_shared, void* y_shared, int32_t* idx,
-                          float* w, int32_t* counts, int32_t* dst, int32_t* offsets, void* out, void* stream) {
-  const char* fn = "cox_decode_moe_routed";
-  if (T < 1 || T > 256) return fail(COX_EINVAL, "%s: need 1 <= T <= 256 (T=%d)", fn, T);
-  if (E < 1 || E > 64 || k < 1 || k > 8 || k > E) return fail(COX_EINVAL, "%s: need 1 <= k <= min(E, 8), E <= 64", fn);
-  if (mode != COX_ROUTE_MIXTRAL && mode != COX_ROUTE_DEEPSEEK) return fail(COX_EINVAL, "%s: bad mode %d", fn, mode);
-  if (d <= 0 || d % 128 || d > 8192 || ff <= 0 || ff % 128)
-    return fail(COX_EINVAL, "%s: need d %% 128 == 0, d <= 8192, ff %% 128 == 0", fn);
-  if (!x || !wg || !h || !y_perm || !idx || !w || !counts || !dst || !out || !aligned16(x) || !aligned16(wg) ||
-      !aligned16(h) || !aligned16(y_perm) || !aligned16(out))
-    return fail(COX_EINVAL, "%s: null or unaligned operand", fn);
-  if (w13_shared && (ff_shared <= 0 || ff_shared % 128 || !w2_shared || !h_shared || !y_shared ||
-                     !aligned16(h_shared) || !aligned16(y_shared)))
-    return fail(COX_EINVAL, "%s: bad shared-expert operands", fn);
-  int32_t ids[64];
-  for (int e = 0; e < E; ++e) ids[e] = e;
-  if (int rc = check_groups(fn, E, ids, w13)) return rc;
-  if (int rc = check_groups(fn, E, ids, w2)) return rc;
-  cox::SmallDense dn{wg, E, mode, idx, w};
-  cox::SmallIdx fi{idx, counts, E, dst, offsets};
-  int rc = cox::launch_small_ffn(x, T, nullptr, nullptr, (long long)T * k, nullptr, E, ids, w13, w2, d, ff, h,
-                                 y_perm, w13_shared, w2_shared, ff_shared, h_shared, y_shared, dst, w, k, out, 3,
-                                 static_cast<cudaStream_t>(stream), &dn, &fi);
   return cuda_status(rc, fn);
 }
 

@@ -9,6 +9,11 @@
 
 namespace cox {
 
+// Router workspace (cox_router_workspace_bytes): a zero-initialised header
+// for the decode router's tickets, then fp32 scratch rows.
+constexpr size_t ROUTER_WS_HEADER = 512;
+
+
 COX_DEV uint32_t smem_u32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
 
 COX_DEV uint32_t lane_id() { return threadIdx.x & 31; }
@@ -119,14 +124,13 @@ COX_DEV void tma_load_2d_pair(uint32_t dst, const void* map, uint32_t bar, int32
       : "memory");
 }
 
-// 4 arbitrary rows (row coordinates r0..r3) x one box of columns, into this CTA's
-// smem, completing on a barrier of the 2-CTA pair (tile::gather4, sm_100).
-COX_DEV void tma_gather4_pair(uint32_t dst, const void* map, uint32_t bar, int32_t col, int32_t r0, int32_t r1,
-                              int32_t r2, int32_t r3) {
+// same with an L2 cache policy (createpolicy)
+COX_DEV void tma_load_2d_pair_hint(uint32_t dst, const void* map, uint32_t bar, int32_t c0, int32_t c1,
+                                   uint64_t pol) {
   asm volatile(
-      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(dst),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(col), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(bar)
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1), "l"(pol)
       : "memory");
 }
 
@@ -189,12 +193,6 @@ COX_DEV uint64_t sdesc_kmajor_sw128(uint32_t saddr) {
 }
 
 // top-k combine fused into a down-projection epilogue (grouped_gemm.cu EPI_COMBINE)
-struct GemmCombine {
-  const void* y_perm;   // routed expert outputs [rows, N] bf16
-  const int32_t* dst;   // [T, k]
-  const float* w;       // [T, k]
-  int k;
-};
 
 // Instruction descriptor, kind::f16: BF16 x BF16 -> F32, both K-major.
 __host__ __device__ constexpr uint32_t idesc_bf16_f32(int M, int N) {

@@ -30,8 +30,13 @@ __global__ void ep_counts_put_kernel(const int32_t* __restrict__ counts, int E, 
 // From counts_all [G][E]: my receive segments (L+1 offsets, one per local
 // expert: every source's rows of local expert l are contiguous, sources in
 // rank order) and, for each of my experts e (owned by r = e / L, l = e % L),
-// the row where my first (t, e) pair lands on r.  overflow[0] is set if any
-// owner would receive more than `cap` rows.
+// the row where my first (t, e) pair lands on r.
+// Capacity: overflow[0] = the largest number of rows any owner would receive
+// if that exceeds `cap`, else 0 (written every launch, so the flag never goes
+// stale).  Every rank holds the same counts_all, so every rank reaches the
+// same verdict.  Memory safety does not depend on the caller reacting: the
+// receive segments are clamped to `cap` (the grouped GEMMs never touch rows
+// >= cap), the dispatch drops rows >= cap and the combine skips them.
 __global__ void ep_offsets_kernel(const int32_t* __restrict__ counts_all, int G, int E, int rank, long long cap,
                                   int32_t* __restrict__ recv_seg, int32_t* __restrict__ send_base,
                                   int32_t* __restrict__ overflow) {
@@ -41,17 +46,19 @@ __global__ void ep_offsets_kernel(const int32_t* __restrict__ counts_all, int G,
   recv_seg[0] = 0;
   for (int l = 0; l < L; ++l) {
     for (int s = 0; s < G; ++s) run += counts_all[s * E + rank * L + l];
-    recv_seg[l + 1] = (int32_t)run;
+    recv_seg[l + 1] = (int32_t)(run < cap ? run : cap);
   }
+  long long worst = 0;
   for (int r = 0; r < G; ++r) {
     long long base = 0;
     for (int l = 0; l < L; ++l)
       for (int s = 0; s < G; ++s) {
-        if (s == rank) send_base[r * L + l] = (int32_t)base;
+        if (s == rank) send_base[r * L + l] = (int32_t)(base < cap ? base : cap);
         base += counts_all[s * E + r * L + l];
       }
-    if (base > cap) overflow[0] = 1;
+    if (base > worst) worst = base;
   }
+  overflow[0] = worst > cap ? (int32_t)(worst < 0x7fffffffLL ? worst : 0x7fffffffLL) : 0;
 }
 
 // One warp per token: read x[t] once, store it to its k owners' receive rows.
@@ -69,9 +76,10 @@ __global__ void __launch_bounds__(256) ep_dispatch_kernel(
       dstp[j] = nullptr;
       if (j < k) {
         const int e = idx[t * k + j];
-        const long row = (long)send_base[e] + (dst_local[t * k + j] - offsets_local[e]);
+        long row = (long)send_base[e] + (dst_local[t * k + j] - offsets_local[e]);
+        if (row >= cap) row = -1;  // over capacity: dropped here, skipped by the combine
         if (lane == 0) route_row[t * k + j] = (int32_t)row;
-        if (row < cap) dstp[j] = peer_recv[e / L] + row * d;
+        if (row >= 0) dstp[j] = peer_recv[e / L] + row * d;
         nk = j + 1;
       }
     }
@@ -98,7 +106,8 @@ __global__ void __launch_bounds__(256) ep_dispatch_kernel(
 }
 
 // out[t] = sum_j w[t,j] * y_owner(j)[route_row[t,j]]  — rows read from the owners'
-// memory; same operation order as K5 / the oracle combine.
+// memory; same operation order as K5 / the oracle combine.  route_row < 0
+// (dropped for capacity) contributes nothing.
 template <int K>
 __global__ void __launch_bounds__(256) ep_combine_kernel(const int32_t* __restrict__ idx,
                                                          const int32_t* __restrict__ route_row,
@@ -112,13 +121,15 @@ __global__ void __launch_bounds__(256) ep_combine_kernel(const int32_t* __restri
     float wj[K];
 #pragma unroll
     for (int j = 0; j < K; ++j) {
-      rows[j] = peer_y[idx[t * K + j] / L] + (long)route_row[t * K + j] * d;
+      const int rr = route_row[t * K + j];
+      rows[j] = rr >= 0 ? peer_y[idx[t * K + j] / L] + (long)rr * d : nullptr;
       wj[j] = w[t * K + j];
     }
     for (int c = lane * 8; c < d; c += 256) {
       uint4 v[K];
 #pragma unroll
-      for (int j = 0; j < K; ++j) v[j] = *reinterpret_cast<const uint4*>(rows[j] + c);
+      for (int j = 0; j < K; ++j)
+        v[j] = rows[j] ? *reinterpret_cast<const uint4*>(rows[j] + c) : make_uint4(0u, 0u, 0u, 0u);
       float acc[8];
 #pragma unroll
       for (int q = 0; q < 8; ++q) acc[q] = 0.0f;

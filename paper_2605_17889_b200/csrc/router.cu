@@ -374,10 +374,7 @@ int launch_router_bf16w(const void* x, const void* wg, int T, int d, int E, int 
   if (smem > 220 * 1024) return -1;
   if (cudaMemsetAsync(counts, 0, sizeof(int32_t) * E, s) != cudaSuccess) return -2;
   if (T == 0) return 0;
-  static const int nw = [] {
-    const char* e = getenv("COX_ROUTER_NW");
-    return e && atoi(e) == 8 ? 8 : 16;
-  }();
+  constexpr int nw = 16;  // 16 warps of 4 tokens x 4 experts (measured faster than 8 x (4 x 8) on C4)
   long blocks = (T + RB_TB - 1) / RB_TB;
   if (blocks > 148L * 8) blocks = 148L * 8;
   if (nw == 16) {
@@ -412,7 +409,6 @@ int launch_router_bf16w(const void* x, const void* wg, int T, int d, int E, int 
 // its top-k; the block that completes the last token writes the per-expert
 // counts from idx (no memset node, no count atomics) and resets the tickets.
 constexpr int RD_TMAX = 64;
-constexpr int RD_SLOTS = 16;  // scratch slots, rotated per launch
 
 COX_DEV int atom_add_acq_rel(int* p, int v) {
   int old;
@@ -482,22 +478,16 @@ router_decode_kernel(const XT* __restrict__ x, const WT* __restrict__ wg, int T,
   for (int i = lane; i <= RD_TMAX; i += 32) g_cnt[i] = 0;
 }
 
+// Scratch from the caller's workspace (router_workspace_bytes): the per-token
+// tickets live in the zero-initialised header (the kernel resets them before
+// it exits), the logits rows behind it.
 static int launch_router_decode(const void* x, int x_is_bf16, const void* wg, int wg_is_bf16, int T, int d, int E,
-                                int k, int mode, int32_t* idx, float* w, int32_t* counts, cudaStream_t s) {
-  static float* logits = nullptr;
-  static int* cnt = nullptr;
-  static unsigned seq = 0;
-  if (!logits) {
-    if (cudaMalloc(&logits, sizeof(float) * RD_SLOTS * RD_TMAX * 256) != cudaSuccess) return -2;
-    if (cudaMalloc(&cnt, sizeof(int) * RD_SLOTS * (RD_TMAX + 1)) != cudaSuccess) return -2;
-    if (cudaMemset(cnt, 0, sizeof(int) * RD_SLOTS * (RD_TMAX + 1)) != cudaSuccess) return -2;
-  }
-  const unsigned slot = seq++ % RD_SLOTS;
+                                int k, int mode, int32_t* idx, float* w, int32_t* counts, void* ws, cudaStream_t s) {
   // splits per token: expert pairs spread over the warps of S blocks
   int S = 1;
   while (S < 4 && E % (4 * S) == 0 && E / (2 * S) >= 2 * RT_WARPS) S *= 2;
-  float* lgs = logits + (size_t)slot * RD_TMAX * 256;
-  int* cs = cnt + (size_t)slot * (RD_TMAX + 1);
+  int* cs = static_cast<int*>(ws);
+  float* lgs = reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + ROUTER_WS_HEADER);
   static bool carve = false;
   if (!carve) {  // decode: same smem carveout as the expert kernel that follows (no reconfig)
     cudaFuncSetAttribute(router_decode_kernel<__nv_bfloat16, __nv_bfloat16>,
@@ -517,34 +507,34 @@ static int launch_router_decode(const void* x, int x_is_bf16, const void* wg, in
 }
 
 int launch_router_tc(const void* x, const void* wg, int T, int d, int E, int k, int mode, int32_t* idx, float* w,
-                     int32_t* counts, cudaStream_t s);
+                     int32_t* counts, float* scratch, cudaStream_t s);
 
+size_t router_workspace_bytes(int T, int E) {
+  if (T < 0) T = 0;
+  return ROUTER_WS_HEADER + sizeof(float) * ((size_t)T * E + (size_t)T + 64);
+}
+
+// tc: -1 auto (tensor-core screen for large fine-grained batches), 0 never, 1
+// whenever the shape allows it (tests / A/B).
 int launch_router(const void* x, int x_is_bf16, const void* wg, int wg_is_bf16, int T, int d, int E, int k,
-                  int mode, int32_t* idx, float* w, int32_t* counts, cudaStream_t s) {
+                  int mode, int32_t* idx, float* w, int32_t* counts, void* ws, int tc, cudaStream_t s) {
   // Large batches with bf16 x and router weights: tensor-core screening +
-  // exact re-scoring (router_tc.cu).  COX_ROUTER_TC=0 forces the all-CUDA-core
-  // kernels below (same indices).
-  static const bool use_tc = [] {
-    const char* e = getenv("COX_ROUTER_TC");
-    return !(e && atoi(e) == 0);
-  }();
-  // (fine-grained MoE only: with E = 8 the all-CUDA-core kernel is faster,
-  // tools/bench_router.py: C2 0.85 ms vs 0.39 + 1.15 ms; C4 3.11 vs 1.77 ms)
-  if (use_tc && x_is_bf16 && wg_is_bf16 && E >= 32 && (long)T >= 148L * 128) {
-    const int rc = launch_router_tc(x, wg, T, d, E, k, mode, idx, w, counts, s);
+  // exact re-scoring (router_tc.cu), same indices as the CUDA-core kernels.
+  // Fine-grained MoE only: with E = 8 the all-CUDA-core kernel is faster
+  // (tools/bench_router.py: C2 0.85 ms vs 0.39 + 1.15 ms; C4 3.11 vs 1.77 ms).
+  const bool tc_ok = x_is_bf16 && wg_is_bf16 && T > 0;
+  if (tc_ok && (tc == 1 || (tc < 0 && E >= 32 && (long)T >= 148L * 128))) {
+    float* scratch = reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + ROUTER_WS_HEADER);
+    const int rc = launch_router_tc(x, wg, T, d, E, k, mode, idx, w, counts, scratch, s);
     if (rc != -3) return rc;  // -3: shape not supported by the screen -> CUDA-core kernels
   }
   if (wg_is_bf16 && x_is_bf16 && E > RT_EG && (long)T >= 148L * RB_TB) {
     const int rc = launch_router_bf16w(x, wg, T, d, E, k, mode, idx, w, counts, s);
     if (rc != -1) return rc;  // -1: tile does not fit in smem -> generic kernels below
   }
-  // decode batches: split-expert router, counts without a memset (COX_ROUTER_DECODE=0: generic kernel)
-  static const bool use_dec = [] {
-    const char* e = getenv("COX_ROUTER_DECODE");
-    return !(e && atoi(e) == 0);
-  }();
-  if (use_dec && T >= 1 && T <= RD_TMAX && E <= 256 && E % 2 == 0 && d % 8 == 0)
-    return launch_router_decode(x, x_is_bf16, wg, wg_is_bf16, T, d, E, k, mode, idx, w, counts, s);
+  // decode batches: split-expert router, counts without a memset
+  if (T >= 1 && T <= RD_TMAX && E <= 256 && E % 2 == 0 && d % 8 == 0)
+    return launch_router_decode(x, x_is_bf16, wg, wg_is_bf16, T, d, E, k, mode, idx, w, counts, ws, s);
   cudaError_t err = cudaMemsetAsync(counts, 0, sizeof(int32_t) * E, s);
   if (err != cudaSuccess) return -2;
   if (T == 0) return 0;

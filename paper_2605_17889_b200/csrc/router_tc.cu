@@ -422,24 +422,14 @@ __global__ void __launch_bounds__(RR_WARPS * 32, NCH <= 8 ? 2 : 1) router_rescor
     if (s_hist[i]) atomicAdd(&counts[i], s_hist[i]);
 }
 
-// Screening + re-scoring router.  approx / margin: scratch of T*E and T floats
-// (owned by the library, grown on demand).  Returns -3 if the shape is not
-// supported by the tensor-core screen (caller falls back to the CUDA-core
+// Screening + re-scoring router.  scratch: T*E + T floats from the caller's
+// workspace (approx logits, then per-token margins), so concurrent launches
+// on different streams or graphs never share it.  Returns -3 if the shape is
+// not supported by the tensor-core screen (caller falls back to the CUDA-core
 // router).
 int launch_router_tc(const void* x, const void* wg, int T, int d, int E, int k, int mode, int32_t* idx, float* w,
-                     int32_t* counts, cudaStream_t s) {
+                     int32_t* counts, float* scratch, cudaStream_t s) {
   if (d % RC_BK != 0 || d > 24 * 256 || E > 256 || E < 1 || k > 8) return -3;
-  static std::mutex mu;
-  std::lock_guard<std::mutex> lk(mu);
-  static float* scratch = nullptr;
-  static size_t scratch_n = 0;
-  const size_t need = (size_t)T * E + (size_t)T + 64;
-  if (need > scratch_n) {
-    if (scratch) cudaFree(scratch);  // stream-ordered users finished: callers synchronise on growth
-    scratch = nullptr;
-    if (cudaMalloc(&scratch, need * sizeof(float)) != cudaSuccess) return -2;
-    scratch_n = need;
-  }
   if (cudaMemsetAsync(counts, 0, sizeof(int32_t) * E, s) != cudaSuccess) return -2;
   if (T == 0) return 0;
   RcParams p;

@@ -113,7 +113,6 @@ struct SmallParams {
   __nv_bfloat16* out;
   int k;
   int T;
-  int k4_colmajor;
   // dense decode (dense != 0): every group runs over all T tokens (B = x rows
   // [0, T); routed group g writes h/y rows [(g - g0) T, +T)) and warp 2 of CTA
   // b routes token b (canonical order, like router_topk_kernel) into ridx/rw;
@@ -139,13 +138,6 @@ struct SmallParams {
   // and the producer of unit 0 of each group writes the group's dst entries
   // for the combine.
   int from_idx;
-  // route_in != 0 (with from_idx): no router kernel ran either.  Warp 2 of CTA
-  // b routes tokens b, b + grid, ... in the prologue (canonical order, as the
-  // dense path) into ridx/rw and the histogram counters[SG_HIST + e]; every CTA
-  // waits until all T tokens are routed, then proceeds as from_idx with those
-  // counts (CTA 0 copies them to counts_out).
-  int route_in;
-  int32_t* counts_out;     // [E] (route_in)
   const int32_t* rcounts;  // [E]
   int32_t* dst_out;        // [T, k]
   int32_t* offsets_out;    // [E + 1]
@@ -160,7 +152,6 @@ constexpr int SG_CB_BASE = 1 + SG_MAXG;  // counters[SG_CB_BASE + i]: down tiles
 constexpr int SG_COUNTERS = 256;
 constexpr int SG_ROUTED = SG_COUNTERS - 2;  // dense: tokens routed so far
 constexpr int SG_CTICKET = SG_COUNTERS - 3; // fused combine: work-item ticket
-constexpr int SG_HIST = 160;                // route_in: counters[SG_HIST + e] tokens routed to expert e (E <= 64)
 
 
 COX_DEV void mbar_spin_ge(const int* p, int want) {
@@ -289,61 +280,14 @@ __global__ void __launch_bounds__(SG_THREADS, 1) small_ffn_kernel(const __grid_c
   if (p.pdl) {
     pdl_wait();  // routing (offsets, row_tokens, dst, w) of this step is complete from here on
   }
-  if (p.route_in) {
-    // prologue routing with the whole CTA: warp w computes the logits of
-    // experts 8w..8w+7 (each in the canonical order, so the split changes no
-    // bit), then warp 2 selects the top-k
-    const int d = p.d, E = p.E, kk = p.k;
-    for (int t = blockIdx.x; t < p.T; t += gridDim.x) {
-      const __nv_bfloat16* xr = p.xtok + (long long)t * d;
-      for (int e0 = 8 * warp; e0 < E; e0 += 8 * (SG_THREADS / 32)) {
-        float acc[8];
-#pragma unroll
-        for (int u = 0; u < 8; ++u) acc[u] = 0.f;
-#pragma unroll 2
-        for (int sc = 8 * lane; sc < d; sc += 256) {
-          float xv[8];
-          bf16x8_to_f32(ld_nc_v4(xr + sc), xv);
-#pragma unroll
-          for (int u = 0; u < 8; u += 2) {
-            float wa[8], wb[8];
-            const int ea = min(e0 + u, E - 1), eb = min(e0 + u + 1, E - 1);
-            bf16x8_to_f32(ld_nc_v4(p.wg + (long long)ea * d + sc), wa);
-            bf16x8_to_f32(ld_nc_v4(p.wg + (long long)eb * d + sc), wb);
-#pragma unroll
-            for (int q = 0; q < 8; ++q) ffma2(acc[u], acc[u + 1], xv[q], wa[q], wb[q]);
-          }
-        }
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          float v = acc[u];
-#pragma unroll
-          for (int off = 16; off >= 1; off >>= 1) v = __fadd_rn(v, __shfl_xor_sync(0xffffffffu, v, off));
-          if (lane == 0 && e0 + u < E) s_route[e0 + u] = v != v ? -INFINITY : v;  // NaN ranks like -inf
-        }
-      }
-      __syncthreads();
-      if (warp == 2) {
-        warp_route_token(s_route, E, kk, p.mode, lane, reinterpret_cast<int*>(s_route + 264), s_route + 272,
-                         p.ridx + t * kk, p.rw + t * kk, p.counters + SG_HIST);
-        if (lane == 0) red_release_add(p.counters + SG_ROUTED, 1);  // after idx / w / histogram
-      }
-      __syncthreads();
-    }
-  }
   if (warp == 0) {
     if (p.from_idx) {
       // expert offsets from the router's counts (exclusive scan, 8 experts per lane)
       int loc[8], sum = 0;
-      if (p.route_in) {
-        if (lane == 0) mbar_spin_ge(p.counters + SG_ROUTED, p.T);  // every CTA's tokens are routed
-        __syncwarp();
-      }
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
         const int e = lane * 8 + q;
-        loc[q] = e < p.E ? (p.route_in ? __ldcg(p.counters + SG_HIST + e) : p.rcounts[e]) : 0;
-        if (p.route_in && blockIdx.x == 0 && e < p.E && p.counts_out) p.counts_out[e] = loc[q];
+        loc[q] = e < p.E ? p.rcounts[e] : 0;
         sum += loc[q];
       }
       int incl = sum;
@@ -436,15 +380,6 @@ __global__ void __launch_bounds__(SG_THREADS, 1) small_ffn_kernel(const __grid_c
       t -= total3;
       pre = s_p4;
       pass = 1;
-    }
-    if (pass == 1 && p.k4_colmajor) {
-      // down tiles run column-block-major (block i of every group, then i+1):
-      // the blocks complete one after another during the pass, so the fused
-      // combine of a block overlaps the streaming of later ones
-      const int nact = s_misc[0];
-      i = t / nact;
-      g = s_act[t - i * nact];
-      return;
     }
     int lo = 0, hi = G;  // largest g with pre[g] <= t (empty groups have pre[g] == pre[g + 1])
     while (hi - lo > 1) {
@@ -666,7 +601,7 @@ __global__ void __launch_bounds__(SG_THREADS, 1) small_ffn_kernel(const __grid_c
 #pragma unroll
       for (int b = 0; b < PB; ++b) {
         const int ent = c0 + 32 * b + lane;
-        ev[b] = ent < nent ? (p.route_in ? __ldcg(p.ridx + ent) : __ldg(p.ridx + ent)) : -1;
+        ev[b] = ent < nent ? __ldg(p.ridx + ent) : -1;
       }
 #pragma unroll
       for (int b = 0; b < PB; ++b) {
@@ -816,7 +751,7 @@ __global__ void __launch_bounds__(SG_THREADS, 1) small_ffn_kernel(const __grid_c
         s_w[e] = p.rw[e];
       } else if (p.from_idx) {
         s_dst[e] = s_pos[e];
-        s_w[e] = p.route_in ? __ldcg(p.cw + e) : p.cw[e];
+        s_w[e] = p.cw[e];
       } else {
         s_dst[e] = __ldcg(p.cdst + e);
         s_w[e] = p.cw[e];
@@ -879,8 +814,6 @@ __global__ void __launch_bounds__(SG_THREADS, 1) small_ffn_kernel(const __grid_c
       for (int c = 0; c < n; ++c) p.counters[c] = 0;
       p.counters[SG_ROUTED] = 0;
       p.counters[SG_CTICKET] = 0;
-      if (p.route_in)
-        for (int e = 0; e < p.E; ++e) p.counters[SG_HIST + e] = 0;
       p.counters[SG_COUNTERS - 1] = 0;
     }
   }
@@ -947,11 +880,7 @@ int launch_small_ffn(const void* x, int T, const int32_t* row_tokens, const void
   std::lock_guard<std::mutex> lk(mu);
   memset(&m, 0, sizeof(m));
   int rc = 0;
-  // dense + fromidx: routed decode with the routing in the kernel's prologue
-  // (route_in); the groups, maps and combine are those of the from_idx path
-  const SmallDense* router = dense;
-  const bool route_in = dense != nullptr && fromidx != nullptr;
-  if (route_in) dense = nullptr;
+  if (dense && fromidx) return -1;
   if (dense) {
     if ((rc = get_map(&m.act3[1], x, T, d, 16))) return rc;  // every group's SwiGLU B = x rows [0, T)
     if ((rc = get_map(&m.act4[0], h, rows_cap, ff, 16))) return rc;
@@ -1000,11 +929,6 @@ int launch_small_ffn(const void* x, int T, const int32_t* row_tokens, const void
   p.out = fuse ? static_cast<__nv_bfloat16*>(out) : nullptr;
   p.k = k;
   p.T = T;
-  static const int colmajor = [] {
-    const char* e = getenv("COX_SMALL_K4_COLMAJOR");  // measured on C4D: 240 vs 232 us (group-major)
-    return e ? atoi(e) : 0;
-  }();
-  p.k4_colmajor = colmajor;
   p.dense = dense ? 1 : 0;
   p.from_idx = fromidx ? 1 : 0;
   if (fromidx) {
@@ -1016,22 +940,8 @@ int launch_small_ffn(const void* x, int T, const int32_t* row_tokens, const void
     p.cdst = fromidx->dst_out;
     p.row_tokens = nullptr;
   }
-  // routed decode: launched as a programmatic dependent of the permute (COX_PDL=0 disables)
-  static const int pdl_env = [] {
-    const char* e = getenv("COX_PDL");
-    return e ? atoi(e) : 1;
-  }();
-  p.pdl = (!dense && pdl_env) ? 1 : 0;
-  p.route_in = route_in ? 1 : 0;
-  if (route_in) {
-    p.wg = static_cast<const __nv_bfloat16*>(router->wg);
-    p.xtok = static_cast<const __nv_bfloat16*>(x);
-    p.mode = router->mode;
-    p.ridx = router->idx;
-    p.rw = router->w;
-    p.cw = router->w;
-    p.counts_out = const_cast<int32_t*>(fromidx->counts);
-  }
+  // routed decode: launched as a programmatic dependent of the router / permute
+  p.pdl = dense ? 0 : 1;
   if (dense) {
     p.wg = static_cast<const __nv_bfloat16*>(dense->wg);
     p.xtok = static_cast<const __nv_bfloat16*>(x);
@@ -1056,13 +966,8 @@ int launch_small_ffn(const void* x, int T, const int32_t* row_tokens, const void
     cudaDeviceGetAttribute(&g_sg_sms, cudaDevAttrMultiProcessorCount, dev);
     if (g_sg_sms <= 0) g_sg_sms = 148;
   }
-  // pipeline shape (K atoms per stage, tokens per chunk); COX_SMALL_VARIANT=KA,NMAX for experiments
-  static int variant = [] {
-    const char* e = getenv("COX_SMALL_VARIANT");
-    int ka = 2, nm = 64;  // measured best on C4 decode (tools/ab_small.sh)
-    if (e) sscanf(e, "%d,%d", &ka, &nm);
-    return ka * 1000 + nm;
-  }();
+  // pipeline shape: 2 K atoms per stage, chunks of up to 64 tokens (measured
+  // best on C4 decode against 1/4 atoms and 16/32-token chunks)
 #define SG_LAUNCH(KA_, NM_)                                                                                \
   do {                                                                                                     \
     static bool attr = false;                                                                              \
@@ -1087,15 +992,7 @@ int launch_small_ffn(const void* x, int T, const int32_t* row_tokens, const void
       small_ffn_kernel<KA_, NM_><<<g_sg_sms, SG_THREADS, SgCfg<KA_, NM_>::SMEM, s>>>(p);                   \
     }                                                                                                      \
   } while (0)
-  switch (variant) {
-    case 1032: SG_LAUNCH(1, 32); break;
-    case 2032: SG_LAUNCH(2, 32); break;
-    case 2016: SG_LAUNCH(2, 16); break;
-    case 4016: SG_LAUNCH(4, 16); break;
-    case 4032: SG_LAUNCH(4, 32); break;
-    case 1064: SG_LAUNCH(1, 64); break;
-    default: SG_LAUNCH(2, 64); break;
-  }
+  SG_LAUNCH(2, 64);
 #undef SG_LAUNCH
   if (out && !fuse) {
     if (cudaGetLastError() != cudaSuccess) return -2;

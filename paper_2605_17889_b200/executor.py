@@ -52,6 +52,7 @@ class _Bufs:
     ping: torch.Tensor
     pong: torch.Tensor
     ws: torch.Tensor
+    router_ws: torch.Tensor
 
 
 class StratifiedMoEStack:
@@ -127,7 +128,8 @@ class StratifiedMoEStack:
                 h=torch.empty((cap, self.ff), dtype=bf, device=dev),
                 ping=torch.empty((T, self.d), dtype=bf, device=dev),
                 pong=torch.empty((T, self.d), dtype=bf, device=dev),
-                ws=torch.empty((max(16, ops.permute_workspace_bytes(T, self.E)),), dtype=torch.uint8, device=dev))
+                ws=torch.empty((max(16, ops.permute_workspace_bytes(T, self.E)),), dtype=torch.uint8, device=dev),
+                router_ws=ops.router_workspace(T, self.E, dev))
         return self._bufs
 
     # ------------------------------------------------------------ forward
@@ -158,7 +160,7 @@ class StratifiedMoEStack:
             out = b.ping if (l % 2 == 0) else b.pong
             if timeline:
                 e0 = mk(); e0.record(s)
-            ops.router_topk(cur, self.wg[l], self.k, self.mode, out=(b.idx, b.w, b.counts))
+            ops.router_topk(cur, self.wg[l], self.k, self.mode, out=(b.idx, b.w, b.counts), workspace=b.router_ws)
             ops.permute(b.idx, cur, self.E, 1, out=(b.offsets, b.dst, b.x_perm), workspace=b.ws)
             if counts_out is not None:
                 counts_out[l].copy_(b.counts)
@@ -171,7 +173,7 @@ class StratifiedMoEStack:
                 e2 = mk(); e2.record(s)
             cold = self.cold[l]
             if cold:
-                for ev in copy_done.pop(l):
+                for ev in copy_done.pop(l, []):
                     s.wait_event(ev)
                 base = (l % 2) * self.C
                 slots = [base + j for j in range(len(cold))]
@@ -179,8 +181,10 @@ class StratifiedMoEStack:
                 ops.grouped_down(b.h, b.offsets, cold, [self.ring.w2[i] for i in slots], self.d, y=b.x_perm)
                 for i in slots:
                     self.ring.release(i, s)
-                if l + 2 < self.N:
-                    copy_done[l + 2] = self._stage_layer(l + 2, timeline)
+            # layer l+2 reuses layer l's slot half; staged whether or not layer l
+            # had cold experts itself (plans may differ in exp_r per layer)
+            if self.C and l + 2 < self.N and self.cold[l + 2]:
+                copy_done[l + 2] = self._stage_layer(l + 2, timeline)
             if timeline:
                 e3 = mk(); e3.record(s)
             if res:

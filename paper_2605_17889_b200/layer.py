@@ -4,15 +4,25 @@ SwiGLU -> grouped down -> combine, all in libcoxmoe.so.
 ``MoELayer.forward`` is the single-GPU, all-resident path (the reference's
 ``AllocationStrategy(exp_r=E, exp_m=0, exp_c=0)``).  Residency/streaming and
 expert parallelism build on the same stage functions (executor.py, ep.py).
+
+Kernel selection by batch size (all measured on B200):
+  * T <= DENSE_T_MAX (48) and nearly every expert touched: ONE launch
+    (cox_decode_moe: router + every expert + shared experts + combine);
+  * T <= SMALL_GATHER_T_MAX (64): router launch + one weight-streaming launch
+    that reads the router's idx directly (cox_small_expert_ffn_idx);
+  * T <= SMALL_T_MAX (256): router + permute (x_perm materialised) + one
+    weight-streaming launch (cox_small_expert_ffn);
+  * larger batches: router, permute, K3, K4, combine (persistent tcgen05
+    grouped GEMMs), shared experts on a side stream.
 """
 from __future__ import annotations
 
-import os
 from dataclasses import dataclass
 
 import torch
 
 from . import _lib, ops
+from .hostio import HostIO, run_host_batches
 from .synthetic import LayerWeights
 
 MODES = {"mixtral": _lib.ROUTE_MIXTRAL, "deepseek": _lib.ROUTE_DEEPSEEK}
@@ -30,16 +40,18 @@ class StageBuffers:
     h: torch.Tensor
     y: torch.Tensor
     out: torch.Tensor
-    workspace: torch.Tensor
-    row_tokens: torch.Tensor | None = None  # gather mode: source token of every permuted row
-    x_ref: torch.Tensor | None = None       # gather mode: the step's input (A source of K3)
+    workspace: torch.Tensor          # permute workspace
+    router_ws: torch.Tensor          # router workspace (zero-initialised)
+    row_tokens: torch.Tensor | None = None  # small path: source token of every permuted row
     shared_offsets: torch.Tensor | None = None
     shared_h: torch.Tensor | None = None
     shared_y: torch.Tensor | None = None
+    dense_h: torch.Tensor | None = None     # dense decode scratch [E*T, ff] / [E*T, d]
+    dense_y: torch.Tensor | None = None
 
 
 def alloc_buffers(T: int, d: int, ff: int, E: int, k: int, tile_m: int, device, out_dtype=torch.bfloat16,
-                  shared_ff: int = 0, gather_a: bool = False) -> StageBuffers:
+                  shared_ff: int = 0) -> StageBuffers:
     cap = ops.rows_capacity(T, k, E, tile_m)
     bf = torch.bfloat16
     b = StageBuffers(
@@ -49,14 +61,13 @@ def alloc_buffers(T: int, d: int, ff: int, E: int, k: int, tile_m: int, device, 
         counts=torch.empty((E,), dtype=torch.int32, device=device),
         offsets=torch.empty((E + 1,), dtype=torch.int32, device=device),
         dst=torch.empty((T, k), dtype=torch.int32, device=device),
-        x_perm=torch.empty((1 if gather_a else cap, d), dtype=bf, device=device),
+        x_perm=torch.empty((cap, d), dtype=bf, device=device),
         h=torch.empty((cap, ff), dtype=bf, device=device),
         y=torch.empty((cap, d), dtype=bf, device=device),
         out=torch.empty((T, d), dtype=out_dtype, device=device),
         workspace=torch.empty((max(16, ops.permute_workspace_bytes(T, E)),), dtype=torch.uint8, device=device),
+        router_ws=ops.router_workspace(T, E, device),
     )
-    if gather_a:
-        b.row_tokens = torch.empty((cap,), dtype=torch.int32, device=device)
     if shared_ff:
         b.shared_offsets = torch.tensor([0, T], dtype=torch.int32, device=device)
         b.shared_h = torch.empty((max(T, 1), shared_ff), dtype=bf, device=device)
@@ -65,21 +76,46 @@ def alloc_buffers(T: int, d: int, ff: int, E: int, k: int, tile_m: int, device, 
 
 
 class MoELayer:
-    """One MoE layer's expert stage with every expert resident in HBM."""
+    """One MoE layer's expert stage with every expert resident in HBM.
+
+    Buffers are kept per batch size.  A CUDA graph captured over a buffer set
+    (``capture``, ``run_host_batches``) PINS that set: it is never freed or
+    reallocated while the layer lives, so a later forward at another batch
+    size cannot hand the graph's memory to other tensors.  Unpinned sets are
+    dropped when a new batch size is allocated (one live working set)."""
+
+    # decode-size batches: one weight-streaming launch for K3+K4 (+ shared
+    # experts), csrc/small_gemm.cu
+    SMALL_T_MAX = 256
+    # Row gathers (TMA tile::gather4 of x rows) only up to this many tokens:
+    # above it the permute materialises x_perm and the kernel loads tiled B
+    # boxes.  Measured on C4 (tools/sweep_decode_large.py, us/step, gather vs
+    # x_perm): T=64 196.5/196.2, 128 222.0/210.9, 192 270.9/234.8, 256 323.4/262.1.
+    SMALL_GATHER_T_MAX = 64
+    # Mid-size decode steps: router + every expert over all tokens + shared
+    # experts + combine in ONE launch (cox_decode_moe).  It streams EVERY
+    # expert, so it only pays when nearly all are touched anyway: measured on
+    # C4 (tools/sweep_decode.py, us/step, dense vs routed): T=8 129/129, 16
+    # 168/169, 24 188/195, 32 190/199, 48 198/204, 64 205/205.  Used when
+    # T <= DENSE_T_MAX and P(expert untouched) = (1 - k/E)^T <= 0.1.
+    DENSE_T_MAX = 48
+    # decode-size batches with shared experts: the shared expert runs beside
+    # the routed experts on a side stream with a slice of the SMs
+    SHARED_SIDE_MAX_ROWS = 8192
+    SHARED_SIDE_CTAS = 16
+    # run_host_batches replays a captured step for batches up to this many tokens
+    HOST_GRAPH_T_MAX = 8192
 
     def __init__(self, weights: LayerWeights, top_k: int, mode: str = "mixtral", tile_m: int = 1,
-                 out_dtype=torch.bfloat16, gather_a: bool | None = None):
+                 out_dtype=torch.bfloat16):
         if mode not in MODES:
             raise ValueError(f"mode must be one of {sorted(MODES)}")
         self.wts = weights
         self.k = int(top_k)
+        self.mode_name = mode
         self.mode = MODES[mode]
         self.tile_m = int(tile_m)
         self.out_dtype = out_dtype
-        # gather-fused A loads (TMA tile::gather4): K3 reads token rows from x directly
-        if gather_a is None:
-            gather_a = os.environ.get("COX_GATHER_A", "0") == "1"
-        self.gather_a = bool(gather_a)
         self.E = weights.num_experts
         self.d = weights.hidden_dim
         self.ff = weights.expert_dim
@@ -94,64 +130,63 @@ class MoELayer:
         self.shared_ff = weights.shared_w2.shape[1] if weights.shared_w2 is not None else 0
         if self.shared_ff and out_dtype != torch.bfloat16:
             raise ValueError("shared experts require a bf16 output")
-        self._bufs: StageBuffers | None = None
+        self._bufs: dict[int, StageBuffers] = {}
+        self._pinned: set[int] = set()
+        self._hs: dict[int, dict] = {}
+        self._side = None
         self.profile_events = None  # optional {"k3": (ev0, ev1), "k4": (ev0, ev1)} recorded around K3/K4
 
     def launches_per_step(self, T: int | None = None) -> int:
-        # router 1 + permute 4 (hist, scan, scatter, copy; +1 pad) + K3 + K4 + combine (+ shared K3/K4);
-        # decode-size batches: K3, K4 and the shared experts are one launch
+        if T is not None and self.uses_dense_decode(T):
+            return 1  # router + all experts + shared + combine in one launch
+        if T is not None and self.uses_idx_decode(T):
+            return 2  # router, then one launch for K3/K4/shared/combine reading the router's idx
         # permute: single-CTA index kernel for T*k <= 16384 (else hist, scan, scatter) + row copy (+ pad)
         small_perm = T is not None and T * self.k <= 16384
         perm = (1 if small_perm else 3) + 1 + (1 if self.tile_m > 1 else 0)
-        if T is not None and self.uses_dense_decode(T):
-            return 1  # router + all experts + shared + combine in one launch
-        if T is not None and self.uses_routed_one_launch(T):
-            return 1  # router in the prologue of the K3/K4/shared/combine launch
-        if T is not None and self.uses_idx_decode(T):
-            return 2  # router, then one launch for K3/K4/shared/combine reading the router's idx
         if T is not None and self.uses_small_path(T):
-            # router + single-CTA permute (indices only; + row copy above the gather
-            # threshold) + one launch for K3/K4/shared/combine
-            perm_small_path = 1 if small_perm else 3
-            return (1 + perm_small_path + (0 if self._small_gather(T) else 1) + 1
-                    + (1 if self.out_dtype != torch.bfloat16 else 0))
-        if (self.shared_ff and self.SHARED_FUSED_COMBINE and self.k <= 8
-                and not (T is not None and 0 < T * self.k <= self.SHARED_SIDE_MAX_ROWS)):
-            return 1 + perm + 2 + 2  # shared K3 + shared down with the combine in its epilogue
+            # router + permute (rows materialised) + one launch for K3/K4/shared/combine
+            return 1 + perm + 1 + (1 if self.out_dtype != torch.bfloat16 else 0)
         return 1 + perm + 2 + 1 + (2 if self.shared_ff else 0)
 
+    # --- buffers ---------------------------------------------------------------
     def buffers(self, T: int, device) -> StageBuffers:
-        if self._bufs is None or self._bufs.T != T:
-            self._bufs = None
-            self._bufs = alloc_buffers(T, self.d, self.ff, self.E, self.k, self.tile_m, device, self.out_dtype,
-                                       self.shared_ff, self.gather_a)
-            if self.uses_small_path(T) and self._bufs.row_tokens is None:
-                self._bufs.row_tokens = torch.empty((self._bufs.h.shape[0],), dtype=torch.int32, device=device)
-        return self._bufs
+        b = self._bufs.get(T)
+        if b is None:
+            for t in [t for t in self._bufs if t not in self._pinned]:
+                del self._bufs[t]
+            b = alloc_buffers(T, self.d, self.ff, self.E, self.k, self.tile_m, device, self.out_dtype,
+                              self.shared_ff)
+            if self.uses_small_path(T):
+                b.row_tokens = torch.empty((b.h.shape[0],), dtype=torch.int32, device=device)
+            if self.uses_dense_decode(T):
+                b.dense_h = torch.empty((self.E * T, self.ff), dtype=torch.bfloat16, device=device)
+                b.dense_y = torch.empty((self.E * T, self.d), dtype=torch.bfloat16, device=device)
+            self._bufs[T] = b
+        return b
+
+    def pin(self, T: int) -> None:
+        """Keep the buffer set of batch size T for the life of the layer (graphs reference it)."""
+        self._pinned.add(T)
 
     # --- stages (all stream-ordered on the current stream) -------------------
-    def route(self, x: torch.Tensor, b: StageBuffers):
-        ops.router_topk(x, self.wg_router, self.k, self.mode, out=(b.idx, b.w, b.counts))
-        if self.gather_a:
-            ops.permute(b.idx, x, self.E, self.tile_m, out=(b.offsets, b.dst, None), workspace=b.workspace,
-                        copy_rows=False, row_tokens=b.row_tokens)
-            b.x_ref = x
-        else:
-            ops.permute(b.idx, x, self.E, self.tile_m, out=(b.offsets, b.dst, b.x_perm), workspace=b.workspace)
+    def _router(self, x: torch.Tensor, b: StageBuffers):
+        ops.router_topk(x, self.wg_router, self.k, self.mode, out=(b.idx, b.w, b.counts), workspace=b.router_ws)
 
-    def _k3(self, b: StageBuffers, groups, w13, max_ctas: int = 0):
-        if self.gather_a:
-            ops.grouped_swiglu_gather(b.x_ref, b.row_tokens, b.offsets, groups, w13, self.ff, h=b.h,
-                                      max_ctas=max_ctas)
-        else:
-            ops.grouped_swiglu(b.x_perm, b.offsets, groups, w13, self.ff, h=b.h, max_ctas=max_ctas)
+    def route(self, x: torch.Tensor, b: StageBuffers):
+        self._router(x, b)
+        self._permute(x, b)
+
+    def _permute(self, x: torch.Tensor, b: StageBuffers):
+        ops.permute(b.idx, x, self.E, self.tile_m, out=(b.offsets, b.dst, b.x_perm), workspace=b.workspace,
+                    row_tokens=b.row_tokens)
 
     def experts(self, b: StageBuffers, groups=None, w13=None, w2=None):
         groups = self.groups if groups is None else groups
         pe = self.profile_events
         if pe:
             pe["k3"][0].record()
-        self._k3(b, groups, self.w13_list if w13 is None else w13)
+        ops.grouped_swiglu(b.x_perm, b.offsets, groups, self.w13_list if w13 is None else w13, self.ff, h=b.h)
         if pe:
             pe["k3"][1].record()
             pe["k4"][0].record()
@@ -159,39 +194,37 @@ class MoELayer:
         if pe:
             pe["k4"][1].record()
 
-    def shared_expert(self, x: torch.Tensor, b: StageBuffers):
+    def shared_expert(self, x: torch.Tensor, b: StageBuffers, max_ctas: int = 0):
         if not self.shared_ff:
             return None
-        ops.grouped_swiglu(x, b.shared_offsets, [0], [self.wts.shared_w13], self.shared_ff, h=b.shared_h)
-        ops.grouped_down(b.shared_h, b.shared_offsets, [0], [self.wts.shared_w2], self.d, y=b.shared_y)
+        ops.grouped_swiglu(x, b.shared_offsets, [0], [self.wts.shared_w13], self.shared_ff, h=b.shared_h,
+                           max_ctas=max_ctas)
+        ops.grouped_down(b.shared_h, b.shared_offsets, [0], [self.wts.shared_w2], self.d, y=b.shared_y,
+                         max_ctas=max_ctas)
         return b.shared_y
 
     def finish(self, b: StageBuffers, shared=None, out=None):
         return ops.combine(b.y, b.dst, b.w, shared, out=b.out if out is None else out)
 
-    # decode-size batches: the shared expert runs beside the routed experts on a
-    # side stream with a slice of the SMs (its GEMMs are tiny and would
-    # otherwise serialise behind the HBM-bound routed GEMMs)
-    SHARED_SIDE_MAX_ROWS = 8192
-    SHARED_SIDE_CTAS = 16
-
-    # decode-size batches: one weight-streaming launch for K3+K4 (+ shared
-    # experts), csrc/small_gemm.cu; COX_SMALL_T_MAX overrides the crossover
-    SMALL_T_MAX = int(os.environ.get("COX_SMALL_T_MAX", "256"))
-
     def uses_small_path(self, T: int) -> bool:
-        return (0 < T <= self.SMALL_T_MAX and not self.gather_a and self.d % 128 == 0 and self.ff % 128 == 0
-                and self.E <= 64 and (not self.shared_ff or self.shared_ff % 128 == 0))
+        return (0 < T <= self.SMALL_T_MAX and self.d % 128 == 0 and self.ff % 128 == 0 and self.E <= 64
+                and (not self.shared_ff or self.shared_ff % 128 == 0))
 
-    # prefill layers with shared experts: COX_SHARED_FUSE=1 runs the top-k combine
-    # in the shared down projection's epilogue (cox_shared_down_combine, bit-identical).
-    # Off by default: measured on C4 the fused epilogue is latency-bound on the k
-    # routed-row gathers (shared down + combine 3.51 ms fused vs 1.99 + 1.38 separate)
-    SHARED_FUSED_COMBINE = os.environ.get("COX_SHARED_FUSE", "0") == "1"
-    # prefill layers with shared experts: shared-expert GEMMs on a side stream
-    # beside the permute (COX_SHARED_BESIDE=0: in sequence after the routed experts)
-    SHARED_BESIDE_PERMUTE = os.environ.get("COX_SHARED_BESIDE", "1") == "1"
+    def uses_dense_decode(self, T: int) -> bool:
+        return (self.uses_small_path(T) and T <= self.DENSE_T_MAX and (1.0 - self.k / self.E) ** T <= 0.1
+                and self.wg_router.dtype == torch.bfloat16 and self.out_dtype == torch.bfloat16)
 
+    def uses_idx_decode(self, T: int, out: torch.Tensor | None = None) -> bool:
+        """Routed decode without a permute launch: the expert kernel reads the router's idx/counts."""
+        return (self.uses_small_path(T) and self.tile_m == 1 and T <= self.SMALL_GATHER_T_MAX
+                and (out is None or out.dtype == torch.bfloat16) and self.out_dtype == torch.bfloat16)
+
+    def _side_stream(self, dev):
+        if self._side is None:
+            self._side = torch.cuda.Stream(dev)
+        return self._side
+
+    # --- forward ---------------------------------------------------------------
     def forward(self, x: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
         if x.dtype != torch.bfloat16 or x.dim() != 2 or x.shape[1] != self.d:
             raise ValueError(f"x must be bf16 [T, {self.d}]")
@@ -200,163 +233,85 @@ class MoELayer:
         if self.uses_small_path(T):
             return self._forward_small(x, b, out)
         if self.shared_ff and 0 < T * self.k <= self.SHARED_SIDE_MAX_ROWS:
+            # small prefill batches: the shared expert on a side stream with a slice of the SMs
             main = torch.cuda.current_stream(x.device)
             side = self._side_stream(x.device)
             side.wait_stream(main)
             with torch.cuda.stream(side):
-                ops.grouped_swiglu(x, b.shared_offsets, [0], [self.wts.shared_w13], self.shared_ff, h=b.shared_h,
-                                   max_ctas=self.SHARED_SIDE_CTAS)
-                ops.grouped_down(b.shared_h, b.shared_offsets, [0], [self.wts.shared_w2], self.d, y=b.shared_y,
-                                 max_ctas=self.SHARED_SIDE_CTAS)
+                self.shared_expert(x, b, max_ctas=self.SHARED_SIDE_CTAS)
             self.route(x, b)
-            self._k3(b, self.groups, self.w13_list, max_ctas=-(-(148 - self.SHARED_SIDE_CTAS) // 2) * 2)
-            ops.grouped_down(b.h, b.offsets, self.groups, self.w2_list, self.d, y=b.y,
-                             max_ctas=-(-(148 - self.SHARED_SIDE_CTAS) // 2) * 2)
+            rest = -(-(148 - self.SHARED_SIDE_CTAS) // 2) * 2
+            ops.grouped_swiglu(b.x_perm, b.offsets, self.groups, self.w13_list, self.ff, h=b.h, max_ctas=rest)
+            ops.grouped_down(b.h, b.offsets, self.groups, self.w2_list, self.d, y=b.y, max_ctas=rest)
             main.wait_stream(side)
             return self.finish(b, b.shared_y, out)
-        if self.shared_ff and self.SHARED_BESIDE_PERMUTE and not self.SHARED_FUSED_COMBINE:
+        if self.shared_ff:
             # the shared expert does not depend on the routing: its GEMMs run on a
             # side stream right after the router, so the HBM-bound permute copy
             # (a few registers, no shared memory) co-resides with them on the SMs
+            # (C4: +0.5%)
             main = torch.cuda.current_stream(x.device)
             side = self._side_stream(x.device)
-            ops.router_topk(x, self.wg_router, self.k, self.mode, out=(b.idx, b.w, b.counts))
+            self._router(x, b)
             side.wait_stream(main)
             with torch.cuda.stream(side):
                 sh = self.shared_expert(x, b)
-            if self.gather_a:
-                ops.permute(b.idx, x, self.E, self.tile_m, out=(b.offsets, b.dst, None), workspace=b.workspace,
-                            copy_rows=False, row_tokens=b.row_tokens)
-                b.x_ref = x
-            else:
-                ops.permute(b.idx, x, self.E, self.tile_m, out=(b.offsets, b.dst, b.x_perm), workspace=b.workspace)
+            self._permute(x, b)
             self.experts(b)
             main.wait_stream(side)
             return self.finish(b, sh, out)
         self.route(x, b)
         self.experts(b)
-        if self.shared_ff and self.SHARED_FUSED_COMBINE and self.k <= 8:
-            # shared expert K3, then its down projection with the combine in the epilogue
-            ops.grouped_swiglu(x, b.shared_offsets, [0], [self.wts.shared_w13], self.shared_ff, h=b.shared_h)
-            return ops.shared_down_combine(b.shared_h, b.shared_offsets, self.wts.shared_w2, b.y, b.dst, b.w,
-                                           out=b.out if out is None else out)
-        sh = self.shared_expert(x, b)
-        return self.finish(b, sh, out)
+        return self.finish(b, None, out)
 
-    # experiment switches for the decode path (A/B): gathered vs materialised
-    # routed rows, fused vs separate combine
-    SMALL_GATHER = os.environ.get("COX_SMALL_GATHER", "1") == "1"
-    SMALL_FUSE = os.environ.get("COX_SMALL_FUSE", "1") == "1"
-    # Row gathers (TMA tile::gather4 of x rows) only up to this many tokens:
-    # above it the permute materialises x_perm and the kernel loads tiled B
-    # boxes.  Measured on C4 (tools/sweep_decode_large.py, us/step, gather vs
-    # x_perm): T=64 196.5/196.2, 128 222.0/210.9, 192 270.9/234.8, 256 323.4/262.1.
-    SMALL_GATHER_T_MAX = int(os.environ.get("COX_SMALL_GATHER_T_MAX", "64"))
+    __call__ = forward
 
-    def _small_gather(self, T: int) -> bool:
-        return self.SMALL_GATHER and T <= self.SMALL_GATHER_T_MAX
+    def _shared_args(self, b: StageBuffers):
+        return (self.wts.shared_w13, self.wts.shared_w2, b.shared_h, b.shared_y) if self.shared_ff else None
 
-    def _route_small(self, x: torch.Tensor, b: StageBuffers):
-        gather = self._small_gather(x.shape[0])
-        ops.router_topk(x, self.wg_router, self.k, self.mode, out=(b.idx, b.w, b.counts))
-        ops.permute(b.idx, x, self.E, self.tile_m, out=(b.offsets, b.dst, None if gather else b.x_perm),
-                    workspace=b.workspace, copy_rows=not gather, row_tokens=b.row_tokens)
+    def _forward_small(self, x: torch.Tensor, b: StageBuffers, out: torch.Tensor | None):
+        """Decode-size step: see the module docstring for the selection."""
+        out = b.out if out is None else out
+        T = x.shape[0]
+        if self.uses_dense_decode(T):
+            return ops.decode_moe(x, self.wg_router, self.k, self.mode, self.w13_list, self.w2_list, b.dense_h,
+                                  b.dense_y, b.idx, b.w, out, self._shared_args(b))
+        self._router(x, b)
+        if self.uses_idx_decode(T, out):
+            return self._ffn_idx(x, b, out)
+        self._permute(x, b)
+        return self._ffn_small(x, b, out)
 
     def _ffn_small(self, x: torch.Tensor, b: StageBuffers, out: torch.Tensor):
-        shared = (self.wts.shared_w13, self.wts.shared_w2, b.shared_h, b.shared_y) if self.shared_ff else None
-        fuse = out.dtype == torch.bfloat16 and self.SMALL_FUSE
-        ops.small_expert_ffn(x, b.offsets, self.groups, self.w13_list, self.w2_list, b.h, b.y,
-                             x_perm=None if self._small_gather(x.shape[0]) else b.x_perm, row_tokens=b.row_tokens,
-                             shared=shared, combine=(b.dst, b.w, out) if fuse else None)
+        fuse = out.dtype == torch.bfloat16
+        ops.small_expert_ffn(x, b.offsets, self.groups, self.w13_list, self.w2_list, b.h, b.y, x_perm=b.x_perm,
+                             shared=self._shared_args(b), combine=(b.dst, b.w, out) if fuse else None)
         if not fuse:
             ops.combine(b.y, b.dst, b.w, b.shared_y if self.shared_ff else None, out=out)
         return out
 
-    # Mid-size decode steps: router + every expert over all tokens + shared
-    # experts + combine in ONE launch (cox_decode_moe).  It streams EVERY
-    # expert, so it only pays when nearly all are touched anyway, and its token
-    # tiles grow with T: measured on C4 (tools/sweep_decode.py, us/step, dense
-    # vs routed): T=8 129/129, 16 168/169, 24 188/195, 32 190/199, 48 198/204,
-    # 64 205/205.  Used when T <= DENSE_T_MAX and P(expert untouched) =
-    # (1 - k/E)^T <= 0.1; COX_DECODE_DENSE=0 disables.
-    DENSE_T_MAX = 48 if os.environ.get("COX_DECODE_DENSE", "1") == "1" else 0
-
-    def uses_dense_decode(self, T: int) -> bool:
-        return (self.uses_small_path(T) and T <= self.DENSE_T_MAX and (1.0 - self.k / self.E) ** T <= 0.1
-                and self.wg_router.dtype == torch.bfloat16 and self.out_dtype == torch.bfloat16)
-
-    def _forward_small(self, x: torch.Tensor, b: StageBuffers, out: torch.Tensor | None):
-        """Decode-size step: router, index-only permute (no row copy), then ONE
-        launch for K3 + K4 + shared experts + combine (csrc/small_gemm.cu).
-        At <= 64 tokens the router runs inside that launch too (dense decode)."""
-        out = b.out if out is None else out
-        T = x.shape[0]
-        if self.uses_dense_decode(T):
-            dh, dy = self._dense_scratch(T, x.device)
-            shared = (self.wts.shared_w13, self.wts.shared_w2, b.shared_h, b.shared_y) if self.shared_ff else None
-            return ops.decode_moe(x, self.wg_router, self.k, self.mode, self.w13_list, self.w2_list, dh, dy,
-                                  b.idx, b.w, out, shared)
-        if self.uses_idx_decode(T, out):
-            if self.uses_routed_one_launch(T):
-                shared = (self.wts.shared_w13, self.wts.shared_w2, b.shared_h, b.shared_y) if self.shared_ff else None
-                return ops.decode_moe_routed(x, self.wg_router, self.k, self.mode, self.w13_list, self.w2_list,
-                                             b.h, b.y, b.idx, b.w, b.counts, b.dst, b.offsets, out, shared)
-            ops.router_topk(x, self.wg_router, self.k, self.mode, out=(b.idx, b.w, b.counts))
-            return self._ffn_idx(x, b, out)
-        self._route_small(x, b)
-        return self._ffn_small(x, b, out)
-
-    # routed decode without a permute launch: the expert kernel reads the
-    # router's idx/counts directly (COX_SMALL_FROM_IDX=0: router + permute + FFN)
-    SMALL_FROM_IDX = os.environ.get("COX_SMALL_FROM_IDX", "1") == "1"
-
-    def uses_idx_decode(self, T: int, out: torch.Tensor | None = None) -> bool:
-        return (self.SMALL_FROM_IDX and self.uses_small_path(T) and self.tile_m == 1 and self.SMALL_FUSE
-                and self._small_gather(T) and (out is None or out.dtype == torch.bfloat16)
-                and self.out_dtype == torch.bfloat16)
-
-    # routed decode in ONE launch: the router runs in the expert kernel's
-    # prologue (cox_decode_moe_routed), COX_DECODE_ROUTE_IN=1.  Off by default:
-    # measured on C4 (tools/sweep_decode.py, profiles/r01/sweep_decode_c4_v2.txt)
-    # the in-kernel routing of a token (~10 us on one CTA) is slower than the
-    # router kernel + PDL hand-off at small T (T=1: 82 vs 56 us) and within
-    # noise at T=64..256; C2D (E=8) gains ~1%
-    DECODE_ROUTE_IN = os.environ.get("COX_DECODE_ROUTE_IN", "0") == "1"
-
-    def uses_routed_one_launch(self, T: int) -> bool:
-        return (self.DECODE_ROUTE_IN and self.uses_idx_decode(T) and self.wg_router.dtype == torch.bfloat16
-                and self.E <= 64 and self.d <= 8192)
-
     def _ffn_idx(self, x: torch.Tensor, b: StageBuffers, out: torch.Tensor):
-        shared = (self.wts.shared_w13, self.wts.shared_w2, b.shared_h, b.shared_y) if self.shared_ff else None
         return ops.small_expert_ffn_idx(x, b.idx, b.counts, b.w, self.w13_list, self.w2_list, b.h, b.y, b.dst, out,
-                                        offsets=b.offsets, shared=shared)
+                                        offsets=b.offsets, shared=self._shared_args(b))
 
-    def _dense_scratch(self, T: int, dev):
-        sc = getattr(self, "_dense", None)
-        if sc is None or sc[0].shape[0] != self.E * T:
-            sc = (torch.empty((self.E * T, self.ff), dtype=torch.bfloat16, device=dev),
-                  torch.empty((self.E * T, self.d), dtype=torch.bfloat16, device=dev))
-            self._dense = sc
-        return sc
-
-    def _side_stream(self, dev):
-        st = getattr(self, "_side", None)
-        if st is None:
-            st = torch.cuda.Stream(dev)
-            self._side = st
-        return st
-
+    # --- CUDA graphs and host batches -------------------------------------------
     def capture(self, x_static: torch.Tensor):
         """Capture one forward over `x_static` into a CUDA graph (launch-bound
         small-T steps such as decode).  Returns (replay_fn, out_tensor); refill
-        x_static in place and call replay_fn() for each step."""
+        x_static in place and call replay_fn() for each step.  The batch size's
+        buffers are pinned for the life of the layer."""
+        T = x_static.shape[0]
+        self.pin(T)
         self.forward(x_static)  # allocate buffers / tensor maps outside capture
         torch.cuda.synchronize()
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g):
             out = self.forward(x_static)
-        return g.replay, out
+        keep = (g, x_static, self._bufs[T])
+
+        def replay():
+            keep[0].replay()
+        return replay, out
 
     def forward_microbatched(self, x: torch.Tensor, m_tokens: int) -> torch.Tensor:
         """Ablation (costmodel.expert_stage_time(coalesced=False), planner.py:309-366):
@@ -366,142 +321,89 @@ class MoELayer:
         NOT coalescing."""
         T = x.shape[0]
         out = torch.empty((T, self.d), dtype=self.out_dtype, device=x.device)
-        subs = {}
+        subs = getattr(self, "_mb_layers", None)
+        if subs is None:
+            subs = self._mb_layers = {}
         for s0 in range(0, T, m_tokens):
             xs = x[s0:s0 + m_tokens]
             n = xs.shape[0]
             if n not in subs:
-                subs[n] = MoELayer(self.wts, self.k, "mixtral" if self.mode == 0 else "deepseek", self.tile_m,
-                                   self.out_dtype, self.gather_a)
+                subs[n] = MoELayer(self.wts, self.k, self.mode_name, self.tile_m, self.out_dtype)
             subs[n].forward(xs, out=out[s0:s0 + n])
         return out
 
-    # run_host_batches replays a captured step for batches up to this many tokens (COX_HOST_GRAPH_T_MAX)
-    HOST_GRAPH_T_MAX = int(os.environ.get("COX_HOST_GRAPH_T_MAX", "8192"))
-
     def run_host_batches(self, xs_host, outs_host) -> None:
-        """End-to-end serving loop over host batches (pinned memory).
-
-        Batch i's H2D copy (copy engine, own stream) overlaps batch i-1's expert
-        stage, and batch i's D2H copy overlaps batch i+1's stage: two device
-        input and two device output buffers, event-ordered.  Every batch still
-        crosses PCIe both ways; only the waiting is hidden.  Batches of up to
-        HOST_GRAPH_T_MAX tokens replay a CUDA graph of the step (one per slot).
-        Returns once all work is enqueued; the current stream is ordered after
-        the last copy."""
-        if len(xs_host) != len(outs_host):
-            raise ValueError("one output buffer per input batch")
+        """End-to-end serving loop over host batches (pinned memory), see
+        hostio.run_host_batches.  Batches of up to HOST_GRAPH_T_MAX tokens replay
+        a CUDA graph of the step (one per slot; the batch size's buffers are
+        pinned)."""
         if not xs_host:
             return
         dev = self.wts.w13.device
         T = xs_host[0].shape[0]
-        comp = torch.cuda.current_stream(dev)
         st = self._host_state(T, dev)
-        h2d, d2h, xin, yout = st["h2d"], st["d2h"], st["xin"], st["yout"]
-        in_free, out_done = st["in_free"], st["out_done"]
-        for i, xh in enumerate(xs_host):
-            slot = i % 2
-            with torch.cuda.stream(h2d):
-                if in_free[slot] is not None:
-                    h2d.wait_event(in_free[slot])
-                xin[slot].copy_(xh, non_blocking=True)
-                ready = torch.cuda.Event()
-                ready.record(h2d)
-            comp.wait_event(ready)
-            if out_done[slot] is not None:
-                comp.wait_event(out_done[slot])
-            if st["graphs"] is not None:
-                st["graphs"][slot].replay()
-            else:
-                self.forward(xin[slot], out=yout[slot])
-            ev_c = torch.cuda.Event()
-            ev_c.record(comp)
-            in_free[slot] = ev_c
-            with torch.cuda.stream(d2h):
-                d2h.wait_event(ev_c)
-                outs_host[i].copy_(yout[slot], non_blocking=True)
-                ev_o = torch.cuda.Event()
-                ev_o.record(d2h)
-                out_done[slot] = ev_o
-        comp.wait_stream(d2h)
+        run_host_batches(st["io"], xs_host, outs_host,
+                         (lambda slot: st["graphs"][slot].replay()) if st["graphs"] is not None
+                         else (lambda slot: self.forward(st["io"].xin[slot], out=st["io"].yout[slot])))
 
     def _host_state(self, T, dev):
-        st = getattr(self, "_hs", None)
-        if st is None or st["T"] != T:
-            st = {"T": T, "h2d": torch.cuda.Stream(dev), "d2h": torch.cuda.Stream(dev),
-                  "xin": [torch.empty((T, self.d), dtype=torch.bfloat16, device=dev) for _ in range(2)],
-                  "yout": [torch.empty((T, self.d), dtype=self.out_dtype, device=dev) for _ in range(2)],
-                  "in_free": [None, None], "out_done": [None, None], "graphs": None}
+        st = self._hs.get(T)
+        if st is None:
+            io = HostIO(T, self.d, dev, out_dtype=self.out_dtype)
+            st = {"io": io, "graphs": None}
             if T <= self.HOST_GRAPH_T_MAX:
-                # launch-bound batch sizes: one CUDA graph per (input, output) slot pair
+                # launch-bound batch sizes: one CUDA graph per (input, output) slot pair; the
+                # graphs reference this T's stage buffers, which are pinned from here on
+                self.pin(T)
                 st["graphs"] = []
                 for s in range(2):
-                    st["xin"][s].zero_()
-                    self.forward(st["xin"][s], out=st["yout"][s])  # buffers / tensor maps outside capture
+                    io.xin[s].zero_()
+                    self.forward(io.xin[s], out=io.yout[s])  # buffers / tensor maps outside capture
                     torch.cuda.synchronize(dev)
                     g = torch.cuda.CUDAGraph()
                     with torch.cuda.graph(g):
-                        self.forward(st["xin"][s], out=st["yout"][s])
+                        self.forward(io.xin[s], out=io.yout[s])
                     st["graphs"].append(g)
-            self._hs = st
+                st["bufs"] = self._bufs[T]
+            self._hs[T] = st
         return st
-
-    __call__ = forward
 
     def stage_times(self, x: torch.Tensor | None = None) -> dict:
         """One instrumented step (CUDA events between stages), in ms."""
-        b = self._bufs
         if x is None:
             raise ValueError("stage_times needs the step's input")
+        T = x.shape[0]
+        b = self.buffers(T, x.device)
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(7)]
-        if self.uses_dense_decode(x.shape[0]) or self.uses_routed_one_launch(x.shape[0]):
+
+        def span(names, n):
+            torch.cuda.synchronize()
+            return {nm: ev[i].elapsed_time(ev[i + 1]) for i, nm in enumerate(names[:n])}
+
+        if self.uses_dense_decode(T):
             ev[0].record()
             self._forward_small(x, b, b.out)
             ev[1].record()
-            torch.cuda.synchronize()
-            name = "decode_moe_one_launch" if self.uses_dense_decode(x.shape[0]) else "decode_moe_routed_one_launch"
-            return {name: ev[0].elapsed_time(ev[1])}
+            return span(["decode_moe_one_launch"], 1)
         ev[0].record()
-        ops.router_topk(x, self.wg_router, self.k, self.mode, out=(b.idx, b.w, b.counts))
+        self._router(x, b)
         ev[1].record()
-        if self.uses_idx_decode(x.shape[0]):
+        if self.uses_idx_decode(T):
             self._ffn_idx(x, b, b.out)
             ev[2].record()
-            torch.cuda.synchronize()
-            return {"router": ev[0].elapsed_time(ev[1]), "expert_ffn_from_idx_shared_combine": ev[1].elapsed_time(ev[2])}
-        if self.uses_small_path(x.shape[0]):
-            gather = self._small_gather(x.shape[0])
-            ops.permute(b.idx, x, self.E, self.tile_m, out=(b.offsets, b.dst, None if gather else b.x_perm),
-                        workspace=b.workspace, copy_rows=not gather, row_tokens=b.row_tokens)
-        elif self.gather_a:
-            ops.permute(b.idx, x, self.E, self.tile_m, out=(b.offsets, b.dst, None), workspace=b.workspace,
-                        copy_rows=False, row_tokens=b.row_tokens)
-            b.x_ref = x
-        else:
-            ops.permute(b.idx, x, self.E, self.tile_m, out=(b.offsets, b.dst, b.x_perm), workspace=b.workspace)
+            return span(["router", "expert_ffn_from_idx_shared_combine"], 2)
+        self._permute(x, b)
         ev[2].record()
-        if self.uses_small_path(x.shape[0]):
+        if self.uses_small_path(T):
             self._ffn_small(x, b, b.out)
             ev[3].record()
-            torch.cuda.synchronize()
-            names = ["router", "permute", "expert_ffn_k3k4_shared_combine"]
-            return {n: ev[i].elapsed_time(ev[i + 1]) for i, n in enumerate(names)}
-        self._k3(b, self.groups, self.w13_list)
+            return span(["router", "permute", "expert_ffn_k3k4_shared_combine"], 3)
+        ops.grouped_swiglu(b.x_perm, b.offsets, self.groups, self.w13_list, self.ff, h=b.h)
         ev[3].record()
         ops.grouped_down(b.h, b.offsets, self.groups, self.w2_list, self.d, y=b.y)
         ev[4].record()
-        if self.shared_ff and self.SHARED_FUSED_COMBINE and self.k <= 8:
-            ops.grouped_swiglu(x, b.shared_offsets, [0], [self.wts.shared_w13], self.shared_ff, h=b.shared_h)
-            ev[5].record()
-            ops.shared_down_combine(b.shared_h, b.shared_offsets, self.wts.shared_w2, b.y, b.dst, b.w, out=b.out)
-            ev[6].record()
-            torch.cuda.synchronize()
-            names = ["router", "permute", "swiglu_k3", "down_k4", "shared_k3", "shared_down_with_combine"]
-            return {n: ev[i].elapsed_time(ev[i + 1]) for i, n in enumerate(names)}
         sh = self.shared_expert(x, b)
         ev[5].record()
         ops.combine(b.y, b.dst, b.w, sh, out=b.out)
         ev[6].record()
-        torch.cuda.synchronize()
-        names = ["router", "permute", "swiglu_k3", "down_k4", "shared", "combine"]
-        return {n: ev[i].elapsed_time(ev[i + 1]) for i, n in enumerate(names)}
+        return span(["router", "permute", "swiglu_k3", "down_k4", "shared", "combine"], 6)

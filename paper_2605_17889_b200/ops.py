@@ -47,7 +47,18 @@ def _ids(ids: Sequence[int]):
     return arr
 
 
-def router_topk(x: torch.Tensor, wg: torch.Tensor, k: int, mode: int = _lib.ROUTE_MIXTRAL, out=None, stream=None):
+def router_workspace_bytes(T: int, E: int) -> int:
+    return int(_lib.load().cox_router_workspace_bytes(T, E))
+
+
+def router_workspace(T: int, E: int, device) -> torch.Tensor:
+    """A zero-initialised router workspace (the kernels leave it zeroed; one per
+    concurrently executing launch, e.g. per layer buffer set)."""
+    return torch.zeros((max(16, router_workspace_bytes(T, E)),), dtype=torch.uint8, device=device)
+
+
+def router_topk(x: torch.Tensor, wg: torch.Tensor, k: int, mode: int = _lib.ROUTE_MIXTRAL, out=None,
+                workspace: torch.Tensor | None = None, stream=None):
     """K1: -> (idx [T,k] int32, w [T,k] fp32, counts [E] int32).  wg: fp32 or bf16 [E, d]."""
     _need(x, "x", ndim=2)
     _need(wg, "wg", None, 2)
@@ -69,10 +80,14 @@ def router_topk(x: torch.Tensor, wg: torch.Tensor, k: int, mode: int = _lib.ROUT
         counts = torch.empty((E,), dtype=torch.int32, device=x.device)
     else:
         idx, w, counts = out
+    if workspace is None:
+        workspace = router_workspace(T, E, x.device)
+    _need(workspace, "workspace", torch.uint8, 1)
     L = _lib.lib()
     wdt = _lib.DTYPE_BF16 if wg.dtype == _BF16 else _lib.DTYPE_F32
-    _lib.check(L.cox_router_topk_ex(x.data_ptr(), xdt, wg.data_ptr(), wdt, T, d, E, k, mode, idx.data_ptr(),
-                                    w.data_ptr(), counts.data_ptr(), _stream(stream)), "cox_router_topk")
+    _lib.check(L.cox_router_topk(x.data_ptr(), xdt, wg.data_ptr(), wdt, T, d, E, k, mode, idx.data_ptr(),
+                                 w.data_ptr(), counts.data_ptr(), workspace.data_ptr(), workspace.numel(),
+                                 _stream(stream)), "cox_router_topk")
     return idx, w, counts
 
 
@@ -111,11 +126,11 @@ def permute(idx: torch.Tensor, x: torch.Tensor, E: int, tile_m: int = 1, out=Non
         _need(row_tokens, "row_tokens", torch.int32, 1)
         if row_tokens.numel() < cap:
             raise ValueError(f"row_tokens needs {cap} entries")
-    _lib.check(L.cox_permute_ex(idx.data_ptr(), T, k, E, tile_m, x.data_ptr(), d, offsets.data_ptr(), dst.data_ptr(),
-                                x_perm.data_ptr() if x_perm is not None else None,
-                                x_perm.shape[0] if x_perm is not None else cap,
-                                row_tokens.data_ptr() if row_tokens is not None else None, workspace.data_ptr(),
-                                _stream(stream)), "cox_permute")
+    _lib.check(L.cox_permute(idx.data_ptr(), T, k, E, tile_m, x.data_ptr(), d, offsets.data_ptr(), dst.data_ptr(),
+                             x_perm.data_ptr() if x_perm is not None else None,
+                             x_perm.shape[0] if x_perm is not None else cap,
+                             row_tokens.data_ptr() if row_tokens is not None else None, workspace.data_ptr(),
+                             _stream(stream)), "cox_permute")
     return offsets, dst, x_perm
 
 
@@ -135,32 +150,9 @@ def grouped_swiglu(x_perm: torch.Tensor, offsets: torch.Tensor, group_experts: S
     if h is None:
         h = torch.empty((rows, ff), dtype=_BF16, device=x_perm.device)
     L = _lib.lib()
-    _lib.check(L.cox_grouped_swiglu_ex(x_perm.data_ptr(), rows, offsets.data_ptr(), len(group_experts),
-                                       _ids(group_experts), _ptrs(w13), d, ff, h.data_ptr(), max_ctas,
-                                       _stream(stream)), "cox_grouped_swiglu")
-    return h
-
-
-def grouped_swiglu_gather(x: torch.Tensor, row_tokens: torch.Tensor, offsets: torch.Tensor,
-                          group_experts: Sequence[int], w13: Sequence[torch.Tensor], ff: int, h: torch.Tensor,
-                          stream=None, max_ctas: int = 0):
-    """K3 with gather-fused A loads: row r of the grouped GEMM is x[row_tokens[r]]."""
-    _need(x, "x", _BF16, 2)
-    _need(row_tokens, "row_tokens", torch.int32, 1)
-    _need(offsets, "offsets", torch.int32, 1)
-    _need(h, "h", _BF16, 2)
-    T, d = x.shape
-    for i, w in enumerate(w13):
-        _need(w, f"w13[{i}]", _BF16, 2)
-        if tuple(w.shape) != (2 * ff, d):
-            raise ValueError(f"w13[{i}] must be [2*ff, d] = [{2 * ff}, {d}]")
-    if len(w13) != len(group_experts):
-        raise ValueError("one weight per group")
-    L = _lib.lib()
-    _lib.check(L.cox_grouped_swiglu_gather(x.data_ptr(), T, row_tokens.data_ptr(), row_tokens.numel(),
-                                           offsets.data_ptr(), len(group_experts), _ids(group_experts), _ptrs(w13),
-                                           d, ff, h.data_ptr(), max_ctas, _stream(stream)),
-               "cox_grouped_swiglu_gather")
+    _lib.check(L.cox_grouped_swiglu(x_perm.data_ptr(), rows, offsets.data_ptr(), offsets.numel() - 1,
+                                    len(group_experts), _ids(group_experts), _ptrs(w13), d, ff, h.data_ptr(),
+                                    max_ctas, _stream(stream)), "cox_grouped_swiglu")
     return h
 
 
@@ -179,9 +171,9 @@ def grouped_down(h: torch.Tensor, offsets: torch.Tensor, group_experts: Sequence
     if y is None:
         y = torch.empty((rows, d), dtype=_BF16, device=h.device)
     L = _lib.lib()
-    _lib.check(L.cox_grouped_down_ex(h.data_ptr(), rows, offsets.data_ptr(), len(group_experts),
-                                     _ids(group_experts), _ptrs(w2), ff, d, y.data_ptr(), max_ctas, _stream(stream)),
-               "cox_grouped_down")
+    _lib.check(L.cox_grouped_down(h.data_ptr(), rows, offsets.data_ptr(), offsets.numel() - 1,
+                                  len(group_experts), _ids(group_experts), _ptrs(w2), ff, d, y.data_ptr(), max_ctas,
+                                  _stream(stream)), "cox_grouped_down")
     return y
 
 
@@ -243,7 +235,8 @@ def small_expert_ffn(x: torch.Tensor, offsets: torch.Tensor, group_experts: Sequ
     ptr = lambda t: t.data_ptr() if t is not None else None  # noqa: E731
     L = _lib.lib()
     _lib.check(L.cox_small_expert_ffn(
-        x.data_ptr(), T, ptr(row_tokens), ptr(x_perm), rows, offsets.data_ptr(), len(group_experts),
+        x.data_ptr(), T, ptr(row_tokens), ptr(x_perm), rows, offsets.data_ptr(), offsets.numel() - 1,
+        len(group_experts),
         _ids(group_experts), _ptrs(w13), _ptrs(w2), d, ff, h.data_ptr(), y.data_ptr(), ptr(sw13), ptr(sw2), ffs,
         ptr(sh), ptr(sy), ptr(dst), ptr(wt), k, ptr(out), _stream(stream)), "cox_small_expert_ffn")
     return out if out is not None else y
@@ -316,46 +309,6 @@ def decode_moe(x: torch.Tensor, wg: torch.Tensor, k: int, mode: int, w13: Sequen
     return out
 
 
-def decode_moe_routed(x: torch.Tensor, wg: torch.Tensor, k: int, mode: int, w13: Sequence[torch.Tensor],
-                      w2: Sequence[torch.Tensor], h: torch.Tensor, y: torch.Tensor, idx: torch.Tensor,
-                      w: torch.Tensor, counts: torch.Tensor, dst: torch.Tensor, offsets: torch.Tensor,
-                      out: torch.Tensor, shared=None, stream=None):
-    """Whole routed decode-step layer in one launch (T <= 256): in-kernel router
-    (bit-identical idx/w), then only the touched experts + shared experts +
-    combine.  h [>= T*k, ff], y [>= T*k, d] scratch; writes idx/w/counts/dst/offsets
-    like router_topk + permute; shared = (w13_shared, w2_shared, h_shared, y_shared)."""
-    _need(x, "x", _BF16, 2)
-    _need(wg, "wg", _BF16, 2)
-    T, d = x.shape
-    E = wg.shape[0]
-    ff = h.shape[1]
-    for t, n in ((h, "h"), (y, "y"), (out, "out")):
-        _need(t, n, _BF16, 2)
-    for t, n in ((idx, "idx"), (dst, "dst")):
-        _need(t, n, torch.int32, 2)
-    _need(w, "w", torch.float32, 2)
-    _need(counts, "counts", torch.int32, 1)
-    _need(offsets, "offsets", torch.int32, 1)
-    if (wg.shape[1] != d or h.shape[0] < T * k or y.shape[0] < T * k or y.shape[1] != d
-            or tuple(out.shape) != (T, d) or tuple(idx.shape) != (T, k) or tuple(w.shape) != (T, k)
-            or tuple(dst.shape) != (T, k) or counts.shape[0] < E or offsets.shape[0] < E + 1
-            or len(w13) != E or len(w2) != E):
-        raise ValueError("decode_moe_routed: inconsistent shapes")
-    sw13 = sw2 = sh = sy = None
-    ffs = 0
-    if shared is not None:
-        sw13, sw2, sh, sy = shared
-        ffs = sh.shape[1]
-    ptr = lambda t: t.data_ptr() if t is not None else None  # noqa: E731
-    L = _lib.lib()
-    _lib.check(L.cox_decode_moe_routed(x.data_ptr(), T, wg.data_ptr(), E, k, mode, _ptrs(w13), _ptrs(w2), d, ff,
-                                       ptr(sw13), ptr(sw2), ffs, h.data_ptr(), y.data_ptr(), ptr(sh), ptr(sy),
-                                       idx.data_ptr(), w.data_ptr(), counts.data_ptr(), dst.data_ptr(),
-                                       offsets.data_ptr(), out.data_ptr(), _stream(stream)),
-               "cox_decode_moe_routed")
-    return out
-
-
 def combine(y_perm: torch.Tensor, dst: torch.Tensor, w: torch.Tensor, shared: torch.Tensor | None = None,
             out: torch.Tensor | None = None, out_dtype=_BF16, stream=None):
     """K5: out[t] = sum_j w[t,j] y_perm[dst[t,j]] (+ shared[t])."""
@@ -373,35 +326,6 @@ def combine(y_perm: torch.Tensor, dst: torch.Tensor, w: torch.Tensor, shared: to
     _lib.check(L.cox_combine(y_perm.data_ptr(), dst.data_ptr(), w.data_ptr(), T, k, d,
                              shared.data_ptr() if shared is not None else None, out.data_ptr(), odt, _stream(stream)),
                "cox_combine")
-    return out
-
-
-def shared_down_combine(h_shared: torch.Tensor, shared_offsets: torch.Tensor, w2_shared: torch.Tensor,
-                        y_perm: torch.Tensor, dst: torch.Tensor, w: torch.Tensor, out: torch.Tensor | None = None,
-                        stream=None):
-    """Shared-expert down projection with K5 fused into its epilogue:
-    out[t] = sum_j w[t,j] y_perm[dst[t,j]] + bf16(h_shared[t] W2s^T) — bit-identical
-    to grouped_down(shared) followed by combine(..., shared)."""
-    _need(h_shared, "h_shared", _BF16, 2)
-    _need(shared_offsets, "shared_offsets", torch.int32, 1)
-    _need(w2_shared, "w2_shared", _BF16, 2)
-    _need(y_perm, "y_perm", _BF16, 2)
-    _need(dst, "dst", torch.int32, 2)
-    _need(w, "w", torch.float32, 2)
-    T, k = dst.shape
-    d, ffs = w2_shared.shape
-    if h_shared.shape[1] != ffs or h_shared.shape[0] < T:
-        raise ValueError(f"h_shared must be [>= {T}, {ffs}]")
-    if y_perm.shape[1] != d:
-        raise ValueError(f"y_perm must have {d} columns")
-    if out is None:
-        out = torch.empty((T, d), dtype=_BF16, device=y_perm.device)
-    _need(out, "out", _BF16, 2)
-    L = _lib.lib()
-    _lib.check(L.cox_shared_down_combine(h_shared.data_ptr(), T, shared_offsets.data_ptr(), w2_shared.data_ptr(),
-                                         ffs, d, y_perm.data_ptr(), dst.data_ptr(), w.data_ptr(), k,
-                                         out.data_ptr(), _stream(stream)),
-               "cox_shared_down_combine")
     return out
 
 

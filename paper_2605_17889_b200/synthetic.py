@@ -52,11 +52,19 @@ def interleave_w13_torch(w1: torch.Tensor, w3: torch.Tensor) -> torch.Tensor:
     return torch.stack([a, b], dim=-3).reshape(*lead, 2 * ff, d).contiguous()
 
 
+def make_router_weight(E: int, d: int, seed: int = 0, device="cuda") -> torch.Tensor:
+    """The router weight of make_layer_weights(E, d, ff, seed) alone (its first
+    draw from the seeded generator): fp32 [E, d] with bf16-representable values."""
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+    return _uniform((E, d), d, g, device).float()
+
+
 def make_layer_weights(E: int, d: int, ff: int, seed: int = 0, device="cuda", shared_ff: int = 0,
                        keep_split: bool = False) -> LayerWeights:
     g = torch.Generator(device=device)
     g.manual_seed(seed)
-    wg = _uniform((E, d), d, g, device).float()
+    wg = _uniform((E, d), d, g, device).float()  # == make_router_weight(E, d, seed)
     w13 = torch.empty((E, 2 * ff, d), dtype=torch.bfloat16, device=device)
     w2 = torch.empty((E, d, ff), dtype=torch.bfloat16, device=device)
     w1s, w3s = [], []
@@ -94,3 +102,52 @@ def split_w13(w13: torch.Tensor):
     ff = two_ff // 2
     v = w13.reshape(*lead, ff // 128, 2, 128, d)
     return (v[..., 0, :, :].reshape(*lead, ff, d), v[..., 1, :, :].reshape(*lead, ff, d))
+
+
+def chunk_reverse(v: torch.Tensor) -> torch.Tensor:
+    """The involution pi that reverses the 8 elements of every chunk of the last
+    dimension (d % 8 == 0).  In the router's canonical order a chunk is one
+    sequential fma chain, so the products x_i w_i of x.pi(w) enter that chain
+    in the opposite order: with pi(x) == x the logit x.pi(w) equals x.w in real
+    arithmetic, but the fp32 results may differ in the last bits."""
+    *lead, d = v.shape
+    return v.reshape(*lead, d // 8, 8).flip(-1).reshape(*lead, d)
+
+
+def make_tie_batch(T: int, d: int, E: int, seed: int = 3, device="cuda", tie_fraction: float = 0.5,
+                   boost: float = 2.0, lead_k: int = 0):
+    """Adversarial routing batch: router rows 2m+1 = chunk_reverse(row 2m) for
+    the first half of the experts (pairs m < E/4), and a `tie_fraction` of the
+    tokens are chunk-reverse symmetric (x == pi(x) bit
+    for bit) and pushed toward one pair (2m, 2m+1), so the pair's two logits are
+    EQUAL in real arithmetic and differ only by fp32 rounding of the canonical
+    summation order — the top-k decision (membership and order) of those tokens
+    is decided by rounding alone, or by the lower-index rule when the fp32
+    values coincide.  lead_k > 0: half of the tie tokens also get lead_k other
+    experts pushed above the pair, so with top_k = lead_k + 1 only one of the
+    pair is selected (membership decided by rounding).  Returns (x bf16 [T, d], wg fp32 [E, d] with bf16-exact
+    values, pair index per token or -1)."""
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+    wg = _uniform((E, d), d, g, device).float()
+    npair = max(1, E // 4)
+    for m in range(npair):
+        wg[2 * m + 1] = chunk_reverse(wg[2 * m])
+    x = torch.empty((T, d), dtype=torch.float32, device=device)
+    x.normal_(0.0, 1.0, generator=g)
+    u = torch.rand((T,), generator=g, device=device)
+    pair = torch.randint(0, npair, (T,), generator=g, device=device)
+    tie = u < tie_fraction
+    dirs = wg[2 * pair] + wg[2 * pair + 1]                      # pi-symmetric direction of the pair
+    scale = boost / (wg[0] * wg[0]).sum().clamp_min(1e-12)      # ~boost added to the pair's logits
+    xt = 0.5 * (x + chunk_reverse(x)) + scale * dirs
+    lead = torch.rand((T,), generator=g, device=device) < 0.5
+    for _ in range(lead_k):
+        e = torch.randint(2 * npair, E, (T,), generator=g, device=device)  # an unpaired expert
+        push = wg[e] + chunk_reverse(wg[e])                     # pi-symmetric push toward expert e
+        xt = xt + torch.where(lead[:, None], 2.0 * scale * push, torch.zeros_like(push))
+    x = torch.where(tie[:, None], xt, x).to(torch.bfloat16)
+    xs = x.reshape(T, d // 8, 8)
+    mirrored = xs[:, :, :4].flip(-1)                            # exact symmetry in bf16: q -> 7 - q
+    xs[:, :, 4:] = torch.where(tie[:, None, None], mirrored, xs[:, :, 4:])
+    return xs.reshape(T, d), wg, torch.where(tie, pair, torch.full_like(pair, -1))

@@ -21,13 +21,33 @@ def test_library_exports_all_symbols():
     L = _lib.load()
     for name in header_symbols():
         assert hasattr(L, name), name
-    assert L.cox_version() == 1
+    assert L.cox_version() == _lib.ABI_VERSION == 2
 
 
 def test_workspace_query_is_host_only():
     L = _lib.load()
     assert L.cox_permute_workspace_bytes(262144, 8) >= 4 * 2 * 1024 * 8
     assert L.cox_permute_workspace_bytes(0, 8) > 0
+    # router: zeroed header for the decode tickets + T*E + T fp32 scratch (tensor-core screen)
+    assert L.cox_router_workspace_bytes(262144, 64) >= 4 * (262144 * 64 + 262144)
+    assert L.cox_router_workspace_bytes(0, 8) >= 512
+
+
+def test_argument_validation_is_host_only():
+    """Invalid arguments are rejected before any device work (no GPU needed):
+    expert ids must name a segment of offsets[E+1]; the router needs its workspace."""
+    import ctypes
+    L = _lib.load()
+    ids = (ctypes.c_int32 * 2)(0, 8)
+    ptrs = (ctypes.c_void_p * 2)(4096, 8192)
+    rc = L.cox_grouped_swiglu(4096, 100, 4096, 8, 2, ids, ptrs, 256, 256, 4096, 0, None)
+    assert rc == _lib.COX_EINVAL and b"outside [0, 8)" in L.cox_last_error()
+    ids[1] = -1
+    rc = L.cox_grouped_down(4096, 100, 4096, 8, 2, ids, ptrs, 256, 256, 4096, 0, None)
+    assert rc == _lib.COX_EINVAL
+    rc = L.cox_router_topk(4096, _lib.DTYPE_BF16, 4096, _lib.DTYPE_BF16, 64, 256, 8, 2, 0, 4096, 4096, 4096,
+                           4096, 16, None)
+    assert rc == _lib.COX_EINVAL and b"workspace" in L.cox_last_error()
 
 
 def test_sass_contains_tcgen05_and_tma():

@@ -42,7 +42,7 @@ class IpcTransport:
         dist.barrier()
 
 
-def _worker(rank, ws, port, q, fused=False, inboxes=None):
+def _worker(rank, ws, port, q, fused=False, inboxes=None, cap_factor=1.25, check_capacity=True):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     torch.cuda.set_device(0)
     dist.init_process_group("gloo", rank=rank, world_size=ws)
@@ -54,14 +54,31 @@ def _worker(rank, ws, port, q, fused=False, inboxes=None):
         wts = make_layer_weights(E, d, ff, seed=0, device="cuda")
         x = make_tokens(1500 + 77 * rank, d, seed=10 + rank, device="cuda")
         ref = MoELayer(wts, k)(x).clone()
+        if fused and not check_capacity:
+            # capacity overflow without the host check: rows beyond cap are dropped
+            # by the kernels (no out-of-bounds access) and check() raises
+            lay = FusedEPMoELayer(wts, k, "mixtral", transport=IpcTransport(rank, inboxes),
+                                  capacity_factor=cap_factor, check_capacity=False)
+            lay(x)
+            torch.cuda.synchronize()
+            try:
+                lay.check()
+                q.put((rank, "overflow not reported"))
+            except RuntimeError:
+                q.put((rank, True))
+            return
         if fused:
-            lay = FusedEPMoELayer(wts, k, "mixtral", transport=IpcTransport(rank, inboxes))
+            lay = FusedEPMoELayer(wts, k, "mixtral", transport=IpcTransport(rank, inboxes),
+                                  capacity_factor=cap_factor)
             out = lay(x).clone()
             out2 = lay(x)
             torch.cuda.synchronize()
             lay.check()
             if not torch.equal(out, out2):
                 q.put((rank, "second step differs"))
+                return
+            if cap_factor < 0.1 and lay.regrows != 1:
+                q.put((rank, f"expected one capacity regrow, got {lay.regrows}"))
                 return
         else:
             out = EPMoELayer(wts, k, "mixtral")(x)
@@ -73,8 +90,13 @@ def _worker(rank, ws, port, q, fused=False, inboxes=None):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("fused", [False, True])
-def test_ep_world2_real_kernels_bitexact(fused):
+@pytest.mark.parametrize("fused,cap_factor,check_capacity", [
+    (False, 1.25, True),
+    (True, 1.25, True),
+    (True, 0.01, True),    # receive buffers far too small: grown collectively, still bit-exact
+    (True, 0.01, False),   # no host check: dropped rows, no out-of-bounds access, check() raises
+])
+def test_ep_world2_real_kernels_bitexact(fused, cap_factor, check_capacity):
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
     port = s.getsockname()[1]
@@ -82,7 +104,8 @@ def test_ep_world2_real_kernels_bitexact(fused):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     inboxes = [ctx.Queue() for _ in range(2)]
-    ps = [ctx.Process(target=_worker, args=(r, 2, port, q, fused, inboxes)) for r in range(2)]
+    ps = [ctx.Process(target=_worker, args=(r, 2, port, q, fused, inboxes, cap_factor, check_capacity))
+          for r in range(2)]
     for p in ps:
         p.start()
     res = dict(q.get(timeout=300) for _ in ps)

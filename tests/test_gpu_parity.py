@@ -387,24 +387,6 @@ def test_fused_ep_full_size_c2_single_rank():
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("T,d,ff,E,k,mode,shared_ff,tile_m", [
-    (3000, 512, 256, 8, 2, "mixtral", 0, 1), (777, 512, 256, 16, 6, "deepseek", 512, 1),
-    (1000, 256, 128, 4, 2, "mixtral", 0, 128), (64, 2048, 1408, 64, 6, "deepseek", 2816, 1)])
-def test_gather_a_identical_to_materialised_permute(T, d, ff, E, k, mode, shared_ff, tile_m):
-    """TMA tile::gather4 A loads (no x_perm) == the materialised-permute path, bit-for-bit."""
-    wts = make_layer_weights(E, d, ff, seed=0, device=DEV, shared_ff=shared_ff)
-    x = make_tokens(T, d, seed=1, device=DEV)
-    a = MoELayer(wts, k, mode, tile_m=tile_m)(x).clone()
-    g = MoELayer(wts, k, mode, tile_m=tile_m, gather_a=True)
-    b = g(x)
-    torch.cuda.synchronize()
-    assert torch.equal(a, b)
-    rt = g.buffers(T, DEV).row_tokens.cpu().numpy()
-    dst = g.buffers(T, DEV).dst.cpu().numpy()
-    for t in range(0, T, max(1, T // 50)):
-        assert (rt[dst[t]] == t).all()
-
-
 @pytest.mark.parametrize("seed", range(12))
 def test_random_configs_vs_oracle(seed):
     """Seeded random configurations: d in {256..1024}, ff in multiples of 128, E in

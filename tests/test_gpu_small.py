@@ -97,123 +97,25 @@ def test_small_ffn_close_to_prefill_kernels():
 
 
 @pytest.mark.parametrize("T,d,ff,E,k,mode,shared_ff", [
-    (64, 2048, 1408, 64, 6, "deepseek", 2816),   # C4 decode step (routed path)
-    (32, 2048, 1408, 64, 6, "deepseek", 2816),   # C4, 32 sequences (dense single-launch path)
-    (64, 4096, 14336, 8, 2, "mixtral", 0),       # Mixtral-8x7B decode step
-    (200, 1024, 512, 16, 4, "deepseek", 256),
-    (1, 256, 128, 8, 2, "mixtral", 0),
-])
-def test_decode_layer_vs_oracle(T, d, ff, E, k, mode, shared_ff):
-    wts = make_layer_weights(E, d, ff, seed=0, device=DEV, shared_ff=shared_ff, keep_split=True)
-    x = make_tokens(T, d, seed=1, device=DEV)
-    layer = MoELayer(wts, k, mode)
-    assert layer.uses_small_path(T)
-    out = layer(x)
-    torch.cuda.synchronize()
-    b = layer.buffers(T, DEV)
-    f = lambda t: t.float().cpu().numpy()  # noqa: E731
-    shared = (f(wts.shared_w1), f(wts.shared_w3), f(wts.shared_w2)) if shared_ff else None
-    ref = O.moe_layer(f(x), f(wts.wg), f(wts.w1), f(wts.w3), f(wts.w2), k, 0 if mode == "mixtral" else 1,
-                      shared=shared)
-    assert np.array_equal(b.idx.cpu().numpy(), ref["idx"])
-    np.testing.assert_allclose(b.w.cpu().numpy(), ref["w"], rtol=2e-6, atol=1e-7)
-    if not layer.uses_dense_decode(T):  # the dense decode launch has no permutation
-        assert np.array_equal(b.dst.cpu().numpy(), ref["dst"])
-    err = rel_l2(f(out), ref["out"])
-    assert err <= 1e-2, err
-
-
-@pytest.mark.parametrize("T,d,ff,E,k,mode,shared_ff", [
-    (32, 2048, 1408, 64, 6, "deepseek", 2816),
-    (17, 4096, 14336, 8, 2, "mixtral", 0),
-    (33, 1024, 512, 40, 4, "deepseek", 256),
-])
-def test_dense_decode_matches_routed_decode(T, d, ff, E, k, mode, shared_ff):
-    """cox_decode_moe (router in the launch, every expert over every token)
-    against the routed decode path (router + permute + weight-streaming FFN):
-    identical routing, outputs equal up to fp32 summation order."""
-    wts = make_layer_weights(E, d, ff, seed=5, device=DEV, shared_ff=shared_ff)
-    x = make_tokens(T, d, seed=6, device=DEV)
-    dense = MoELayer(wts, k, mode)
-    routed = MoELayer(wts, k, mode)
-    routed.DENSE_T_MAX = 0
-    assert dense.uses_dense_decode(T) and not routed.uses_dense_decode(T)
-    a = dense(x).clone()
-    bb = routed(x).clone()
-    torch.cuda.synchronize()
-    assert torch.equal(dense.buffers(T, DEV).idx, routed.buffers(T, DEV).idx)
-    assert torch.equal(dense.buffers(T, DEV).w, routed.buffers(T, DEV).w)
-    assert rel_l2(a.float().cpu(), bb.float().cpu()) < 4e-3
-
-
-def test_decode_graph_replay_matches_eager():
-    T, d, ff, E, k, sff = 64, 2048, 1408, 64, 6, 2816
-    wts = make_layer_weights(E, d, ff, seed=0, device=DEV, shared_ff=sff)
-    layer = MoELayer(wts, k, "deepseek")
-    x_static = make_tokens(T, d, seed=1, device=DEV)
-    replay, out = layer.capture(x_static)
-    for s in (2, 3):
-        x_new = make_tokens(T, d, seed=s, device=DEV)
-        x_static.copy_(x_new)
-        replay()
-        torch.cuda.synchronize()
-        eager = MoELayer(wts, k, "deepseek")(x_new)
-        torch.cuda.synchronize()
-        assert torch.equal(out, eager)
-
-
-@pytest.mark.parametrize("T,E,k,d,ff,shared_ff", [
-    (64, 64, 6, 2048, 1408, 2816),
-    (37, 8, 2, 512, 256, 0),
-    (150, 16, 4, 1024, 512, 256),   # segments > 64 rows: chunked
-])
-def test_gather_rows_and_fused_combine_match_separate_kernels(T, E, k, d, ff, shared_ff):
-    """Gather-mode B loads (row_tokens, no x_perm) and the fused combine give the
-    same bits as materialised x_perm rows + the separate combine kernel."""
-    wts = make_layer_weights(E, d, ff, seed=8, device=DEV, shared_ff=shared_ff)
-    x = make_tokens(T, d, seed=9, device=DEV)
-    idx, w, _ = ops.router_topk(x, wts.wg, k, 1)
-    cap = ops.rows_capacity(T, k, E)
-    rt = torch.empty((cap,), dtype=torch.int32, device=DEV)
-    offsets, dst, x_perm = ops.permute(idx, x, E, row_tokens=rt)
-    g = list(range(E))
-    w13 = [wts.w13[e] for e in g]
-    w2 = [wts.w2[e] for e in g]
-    bf = torch.bfloat16
-
-    def bufs():
-        sh = ((wts.shared_w13, wts.shared_w2, torch.empty((T, shared_ff), dtype=bf, device=DEV),
-               torch.empty((T, d), dtype=bf, device=DEV)) if shared_ff else None)
-        return torch.empty((cap, ff), dtype=bf, device=DEV), torch.empty((cap, d), dtype=bf, device=DEV), sh
-
-    h1, y1, sh1 = bufs()
-    ops.small_expert_ffn(x, offsets, g, w13, w2, h1, y1, x_perm=x_perm, shared=sh1)
-    out1 = ops.combine(y1, dst, w, sh1[3] if shared_ff else None)
-    h2, y2, sh2 = bufs()
-    out2 = torch.full((T, d), 5.0, dtype=bf, device=DEV)
-    ops.small_expert_ffn(x, offsets, g, w13, w2, h2, y2, row_tokens=rt, shared=sh2, combine=(dst, w, out2))
-    torch.cuda.synchronize()
-    assert torch.equal(h1, h2) and torch.equal(y1, y2)
-    assert torch.equal(out1, out2)
-
-
-@pytest.mark.parametrize("T,d,ff,E,k,mode,shared_ff", [
     (64, 2048, 1408, 64, 6, "deepseek", 2816),
     (200, 1024, 512, 16, 4, "deepseek", 256),
     (5, 512, 256, 8, 2, "mixtral", 0),
+    (65, 1024, 512, 16, 4, "deepseek", 256),
+    (256, 1024, 512, 16, 4, "deepseek", 256),
 ])
 def test_decode_from_idx_matches_permute_path(T, d, ff, E, k, mode, shared_ff):
     """The expert launch that reads the router's idx/counts directly (no permute
-    kernel) produces the permute's offsets and dst and the same output bits as
-    router + permute + gathered-row launch."""
+    kernel, rows gathered from x) produces the permute's offsets and dst and the
+    same output bits as router + permute (x_perm materialised) + tiled-B launch."""
     wts = make_layer_weights(E, d, ff, seed=9, device=DEV, shared_ff=shared_ff)
     x = make_tokens(T, d, seed=10, device=DEV)
     a_l = MoELayer(wts, k, mode)
     b_l = MoELayer(wts, k, mode)
-    b_l.SMALL_FROM_IDX = False
     a_l.DENSE_T_MAX = b_l.DENSE_T_MAX = 0
-    a_l.SMALL_GATHER_T_MAX = b_l.SMALL_GATHER_T_MAX = 256  # gathered rows at every T here
+    a_l.SMALL_GATHER_T_MAX = 256  # idx path at every T here
+    b_l.SMALL_GATHER_T_MAX = 0    # router + permute + x_perm launch at every T
     assert a_l.uses_idx_decode(T) and not b_l.uses_idx_decode(T)
+    assert a_l.launches_per_step(T) == 2 and b_l.launches_per_step(T) == 4
     a = a_l(x).clone()
     bo = b_l(x).clone()
     torch.cuda.synchronize()
@@ -221,26 +123,6 @@ def test_decode_from_idx_matches_permute_path(T, d, ff, E, k, mode, shared_ff):
     assert torch.equal(ba.idx, bb.idx)
     assert torch.equal(ba.offsets, bb.offsets)
     assert torch.equal(ba.dst, bb.dst)
-    assert torch.equal(a, bo)
-
-
-@pytest.mark.parametrize("T", [65, 128, 256])
-def test_decode_x_perm_above_gather_threshold(T):
-    """Above SMALL_GATHER_T_MAX the decode step materialises x_perm (router +
-    permute copy + tiled-B launch): same routing and output bits as the
-    gathered-row path."""
-    d, ff, E, k, sff = 1024, 512, 16, 4, 256
-    wts = make_layer_weights(E, d, ff, seed=11, device=DEV, shared_ff=sff)
-    x = make_tokens(T, d, seed=12, device=DEV)
-    a_l = MoELayer(wts, k, "deepseek")
-    b_l = MoELayer(wts, k, "deepseek")
-    b_l.SMALL_GATHER_T_MAX = 256
-    assert not a_l._small_gather(T) and b_l._small_gather(T)
-    assert a_l.launches_per_step(T) == 4 and b_l.launches_per_step(T) == 2
-    a = a_l(x).clone()
-    bo = b_l(x).clone()
-    torch.cuda.synchronize()
-    assert torch.equal(a_l.buffers(T, DEV).idx, b_l.buffers(T, DEV).idx)
     assert torch.equal(a, bo)
 
 

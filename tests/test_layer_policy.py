@@ -23,13 +23,8 @@ def test_decode_path_selection(c4_layer):
     assert L.uses_dense_decode(24) and L.uses_dense_decode(48)
     assert not L.uses_dense_decode(64)      # measured slower than the routed path
     assert L.launches_per_step(32) == 1
-    assert not L.uses_routed_one_launch(64)
     assert L.launches_per_step(64) == 2  # router, then FFN + combine straight from the router's idx
-    L.DECODE_ROUTE_IN = True
-    try:
-        assert L.uses_routed_one_launch(64) and L.launches_per_step(64) == 1  # router in the FFN prologue
-    finally:
-        del L.DECODE_ROUTE_IN
+    assert L.launches_per_step(65) == 1 + 2 + 1  # router, permute (index kernel + row copy), one FFN launch
     assert L.launches_per_step(262144) == 1 + 3 + 1 + 2 + 1 + 2
 
 
@@ -41,8 +36,6 @@ def test_dense_decode_needs_bf16_router_and_output():
     assert not L.uses_dense_decode(32) and L.uses_small_path(32)
     L2 = MoELayer(make_layer_weights(8, 256, 128, seed=1, device="cpu"), 2, "mixtral", out_dtype=torch.float32)
     assert not L2.uses_dense_decode(32)
-    L.DECODE_ROUTE_IN = True
-    assert not L.uses_routed_one_launch(64)  # fp32 router weights: router kernel + FFN launch
 
 
 def test_small_path_shape_limits():

@@ -36,28 +36,20 @@ def main():
         x = make_tokens(T, d, seed=3, device=dev)
         layer = MoELayer(wts, k, mode)
         out = layer(x)
-        layer.SMALL_FROM_IDX = False
+        layer.SMALL_GATHER_T_MAX = 0  # router + permute + x_perm launch
         out2 = layer(x)
         torch.cuda.synchronize()
         assert torch.isfinite(out.float()).all() and torch.isfinite(out2.float()).all()
-    # single-launch routed decode (router in the prologue), split-expert decode
-    # router (T <= 64, E = 64 / 8 / 160), fused shared-down + combine epilogue
-    for (T, d, ff, E, k, mode, shared) in [(64, 256, 128, 64, 6, "deepseek", 256), (200, 256, 128, 8, 2, "mixtral", 0)]:
-        wts = make_layer_weights(E, d, ff, seed=4, device=dev, shared_ff=shared)
-        layer = MoELayer(wts, k, mode)
-        layer.DECODE_ROUTE_IN = True
-        layer.DENSE_T_MAX = 0
-        out = layer(make_tokens(T, d, seed=5, device=dev))
-        torch.cuda.synchronize()
-        assert torch.isfinite(out.float()).all()
+    # split-expert decode router (T <= 64, E = 64 / 8 / 160) with one workspace reused
     for E in (64, 8, 160):
         wgd = (torch.rand(E, 512, device=dev) * 2 - 1).to(torch.bfloat16) / 16
+        ws = ops.router_workspace(37, E, dev)
         for _ in range(2):
-            ops.router_topk(make_tokens(37, 512, device=dev), wgd, 6, 1)
+            ops.router_topk(make_tokens(37, 512, device=dev), wgd, 6, 1, workspace=ws)
     torch.cuda.synchronize()
+    # prefill layer with shared experts on the side stream
     wts = make_layer_weights(16, 256, 128, seed=6, device=dev, shared_ff=256)
     layer = MoELayer(wts, 4, "deepseek")
-    layer.SHARED_FUSED_COMBINE = True
     out = layer(make_tokens(3000, 256, seed=7, device=dev))
     torch.cuda.synchronize()
     assert torch.isfinite(out.float()).all()

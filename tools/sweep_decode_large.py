@@ -30,7 +30,7 @@ def main():
             if variant == "gather":
                 layer.SMALL_GATHER_T_MAX = 1 << 30  # row gathers at every T
             if variant == "x_perm":
-                layer.SMALL_GATHER = False
+                layer.SMALL_GATHER_T_MAX = 0
             if variant == "prefill":
                 layer.SMALL_T_MAX = 0
             if variant != "prefill" and not layer.uses_small_path(T):
