@@ -11,7 +11,7 @@
 namespace cox {
 size_t router_workspace_bytes(int T, int E);
 int launch_router(const void* x, int x_is_bf16, const void* wg, int wg_is_bf16, int T, int d, int E, int k,
-                  int mode, int32_t* idx, float* w, int32_t* counts, void* ws, int tc, cudaStream_t s);
+                  int mode, int32_t* idx, float* w, int32_t* counts, void* ws, int tc, int e8, cudaStream_t s);
 size_t permute_workspace_bytes(int T, int E);
 int launch_permute(const int32_t* idx, int T, int k, int E, int tile_m, const void* x, int d, int32_t* offsets,
                    int32_t* dst, void* x_perm, void* workspace, cudaStream_t s, int32_t* row_tokens = nullptr,
@@ -107,11 +107,16 @@ int cox_device_check(void) {
 
 size_t cox_router_workspace_bytes(int T, int E) { return cox::router_workspace_bytes(T, E); }
 
-// COX_ROUTER_TC: test/A-B override of the tensor-core screen (0 never, 1 whenever the shape allows)
-static int router_tc_mode() {
+// COX_ROUTER (A/B and tests): "generic" = the CUDA-core kernels of router.cu only
+// (no tensor-core screen, no E <= 8 TMA kernel); "tc" = the tensor-core screen
+// whenever the shape allows it; unset = automatic choice.
+static int router_env() {
   static const int m = [] {
-    const char* e = getenv("COX_ROUTER_TC");
-    return e ? (atoi(e) ? 1 : 0) : -1;
+    const char* e = getenv("COX_ROUTER");
+    if (!e) return 0;
+    if (!strcmp(e, "generic")) return 1;
+    if (!strcmp(e, "tc")) return 2;
+    return 0;
   }();
   return m;
 }
@@ -132,7 +137,8 @@ int cox_router_topk(const void* x, int x_dtype, const void* wg, int wg_dtype, in
     return fail(COX_EINVAL, "%s: workspace of %zu bytes (16-byte aligned) required, got %zu", fn, need,
                 workspace_bytes);
   int rc = cox::launch_router(x, x_dtype == COX_DTYPE_BF16, wg, wg_dtype == COX_DTYPE_BF16, T, d, E, k, mode, idx, w,
-                              counts, workspace, router_tc_mode(), static_cast<cudaStream_t>(stream));
+                              counts, workspace, router_env() == 1 ? 0 : router_env() == 2 ? 1 : -1,
+                              router_env() == 1 ? 0 : 1, static_cast<cudaStream_t>(stream));
   return cuda_status(rc, fn);
 }
 

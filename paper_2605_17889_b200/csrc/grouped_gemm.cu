@@ -474,6 +474,22 @@ int get_map(CUtensorMap* out, const void* ptr, unsigned long long rows, unsigned
   return 0;
 }
 
+// bf16 row-major [rows, cols] -> TMA map with a {box_cols, box_rows} box, no swizzle or 128B swizzle
+// (not cached: for kernels that build their map per launch).
+int get_map_box(CUtensorMap* out, const void* ptr, unsigned long long rows, unsigned long long cols,
+                unsigned box_cols, unsigned box_rows, bool swizzle128) {
+  auto enc = get_encode_fn();
+  if (!enc) return -2;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {cols * 2};
+  cuuint32_t box[2] = {box_cols, box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? 0 : -1;
+}
+
 static int env_int(const char* name, int dflt) {
   const char* e = getenv(name);
   return e ? atoi(e) : dflt;
@@ -538,6 +554,19 @@ int launch_grouped_gemm(int epi, const void* A, long long rows_cap, int K, const
   p.band = pick_band(epi, p.n_tiles, K);
   static const int l2_env[2] = {env_int("COX_GEMM_L2_K3", 0), env_int("COX_GEMM_L2_K4", 0)};
   p.l2_mode = l2_env[epi ? 1 : 0];
+  // evict_last lines live in the persisting set-aside of the L2 (cudaLimitPersistingL2CacheSize;
+  // 0 by default, which turns evict_last into evict_normal): COX_L2_PERSIST_MB sets it once
+  static const bool persist_set = [] {
+    const int mb = env_int("COX_L2_PERSIST_MB", 0);
+    if (mb <= 0) return false;
+    int dev = 0, mx = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&mx, cudaDevAttrMaxPersistingL2CacheSize, dev);
+    size_t want = (size_t)mb << 20;
+    if (want > (size_t)mx) want = (size_t)mx;
+    return cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want) == cudaSuccess;
+  }();
+  (void)persist_set;
   if (g_num_sms == 0) {
     int dev = 0;
     cudaGetDevice(&dev);

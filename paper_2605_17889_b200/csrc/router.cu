@@ -508,6 +508,8 @@ static int launch_router_decode(const void* x, int x_is_bf16, const void* wg, in
 
 int launch_router_tc(const void* x, const void* wg, int T, int d, int E, int k, int mode, int32_t* idx, float* w,
                      int32_t* counts, float* scratch, cudaStream_t s);
+int launch_router_e8(const void* x, const void* wg, int wg_is_bf16, int T, int d, int E, int k, int mode,
+                     int32_t* idx, float* w, int32_t* counts, cudaStream_t s);
 
 size_t router_workspace_bytes(int T, int E) {
   if (T < 0) T = 0;
@@ -515,9 +517,9 @@ size_t router_workspace_bytes(int T, int E) {
 }
 
 // tc: -1 auto (tensor-core screen for large fine-grained batches), 0 never, 1
-// whenever the shape allows it (tests / A/B).
+// whenever the shape allows it; e8: 0 never use the E <= 8 TMA kernel (A/B).
 int launch_router(const void* x, int x_is_bf16, const void* wg, int wg_is_bf16, int T, int d, int E, int k,
-                  int mode, int32_t* idx, float* w, int32_t* counts, void* ws, int tc, cudaStream_t s) {
+                  int mode, int32_t* idx, float* w, int32_t* counts, void* ws, int tc, int e8, cudaStream_t s) {
   // Large batches with bf16 x and router weights: tensor-core screening +
   // exact re-scoring (router_tc.cu), same indices as the CUDA-core kernels.
   // Fine-grained MoE only: with E = 8 the all-CUDA-core kernel is faster
@@ -527,6 +529,12 @@ int launch_router(const void* x, int x_is_bf16, const void* wg, int wg_is_bf16, 
     float* scratch = reinterpret_cast<float*>(static_cast<uint8_t*>(ws) + ROUTER_WS_HEADER);
     const int rc = launch_router_tc(x, wg, T, d, E, k, mode, idx, w, counts, scratch, s);
     if (rc != -3) return rc;  // -3: shape not supported by the screen -> CUDA-core kernels
+  }
+  // coarse-grained MoE (E <= 8) on large batches: TMA-fed kernel with the router
+  // rows in shared memory (router_e8.cu)
+  if (x_is_bf16 && E <= 8 && e8 != 0 && (long)T >= 148L * 64) {
+    const int rc = launch_router_e8(x, wg, wg_is_bf16, T, d, E, k, mode, idx, w, counts, s);
+    if (rc != -3) return rc;  // -3: shape not covered -> general kernels
   }
   if (wg_is_bf16 && x_is_bf16 && E > RT_EG && (long)T >= 148L * RB_TB) {
     const int rc = launch_router_bf16w(x, wg, T, d, E, k, mode, idx, w, counts, s);

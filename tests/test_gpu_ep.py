@@ -20,6 +20,7 @@ class IpcTransport:
 
     def __init__(self, rank, inboxes):
         self.rank, self.inboxes = rank, inboxes
+        self._keep = []
 
     def alloc(self, spec, dev):
         mine = {n: torch.zeros(shape, dtype=dt, device=dev) for n, (shape, dt) in spec.items()}
@@ -30,7 +31,7 @@ class IpcTransport:
         for _ in range(len(self.inboxes) - 1):
             r, t = self.inboxes[self.rank].get(timeout=120)
             peers[r] = t
-        self._keep = peers
+        self._keep.append(peers)  # every allocation's peer mappings stay alive
         out = {}
         for n in spec:
             ptrs = [peers[r][n].data_ptr() for r in range(len(self.inboxes))]

@@ -158,3 +158,25 @@ def test_random_decode_configs_vs_oracle(seed):
         assert np.array_equal(b.dst.cpu().numpy(), ref["dst"])
         assert np.array_equal(b.offsets.cpu().numpy(), ref["offsets"])
     assert rel_l2(f(out), ref["out"]) <= 1e-2
+
+
+def test_captured_graph_survives_other_batch_sizes():
+    """A CUDA graph captured at one batch size keeps its buffers (pinned per T):
+    forwards at other batch sizes in between must not reallocate them, so the
+    replay still produces the eager result (graph replay into freed
+    memory)."""
+    d, ff, E, k, sff = 1024, 512, 16, 4, 256
+    wts = make_layer_weights(E, d, ff, seed=13, device=DEV, shared_ff=sff)
+    layer = MoELayer(wts, k, "deepseek")
+    xs = make_tokens(64, d, seed=14, device=DEV)
+    replay, out = layer.capture(xs)
+    for T in (200, 5000, 37, 3000):  # other paths and batch sizes, fresh allocations
+        layer(make_tokens(T, d, seed=T, device=DEV))
+    junk = [torch.full((1 << 20,), 7.0, device=DEV) for _ in range(64)]  # reuse freed blocks
+    xs.copy_(make_tokens(64, d, seed=15, device=DEV))
+    replay()
+    torch.cuda.synchronize()
+    ref = MoELayer(wts, k, "deepseek")(xs)
+    torch.cuda.synchronize()
+    assert torch.equal(out, ref)
+    del junk
