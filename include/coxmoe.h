@@ -170,6 +170,18 @@ int cox_decode_moe(const void* x, int T, const void* wg, int E, int k, int mode,
                    void* h, void* y, void* h_shared, void* y_shared, int32_t* idx, float* w, void* out,
                    void* stream);
 
+/* K6' — cold-expert fetch decided on the device (decode-size steps,
+ * SURVEY.md §8 f1).  For each listed cold expert i
+ * (expert_ids[i] in [0, E)), if counts[expert_ids[i]] > 0 (the layer's router
+ * routed tokens to it) copy `bytes` from pinned host memory host_src[i] to the
+ * device slot dst[i]; untouched cold experts cost no PCIe bytes and the
+ * decision needs no host round trip (graph-capturable).  Replaces the
+ * unconditional `mig_load` of costmodel.py:252.  fetched [n] (nullable): 1 for
+ * every entry copied by this launch.  n <= 64, max_ctas: CTAs used (0 = one
+ * per SM). */
+int cox_fetch_experts(const int32_t* counts, int E, int n, const int32_t* expert_ids, const void* const* host_src,
+                      void* const* dst, const long long* bytes, int max_ctas, int32_t* fetched, void* stream);
+
 /* K5 — weighted top-k combine back to token order (+ optional shared-expert
  * output, DeepSeek-V2):  out[t] = sum_j w[t,j] * y_perm[dst[t,j]] (+ shared[t]).
  * out/shared dtype = out_dtype (bf16 or fp32). */

@@ -31,7 +31,7 @@ EXPORTS = (
     "cox_last_error", "cox_version", "cox_device_check", "cox_router_workspace_bytes", "cox_router_topk",
     "cox_permute_workspace_bytes", "cox_permute", "cox_grouped_swiglu", "cox_grouped_down",
     "cox_small_expert_ffn", "cox_small_expert_ffn_idx", "cox_decode_moe", "cox_combine", "cox_ep_counts_put",
-    "cox_ep_offsets", "cox_ep_dispatch", "cox_ep_combine", "cox_interleave_w13",
+    "cox_ep_offsets", "cox_ep_dispatch", "cox_ep_combine", "cox_interleave_w13", "cox_fetch_experts",
 )
 ABI_VERSION = 2
 
@@ -72,6 +72,8 @@ def _declare(L):
     L.cox_decode_moe.restype = c_int
     L.cox_decode_moe.argtypes = [P, c_int, P, c_int, c_int, c_int, P, P, c_int, c_int, P, P, c_int, P, P, P, P, P,
                                  P, P, P]
+    L.cox_fetch_experts.restype = c_int
+    L.cox_fetch_experts.argtypes = [P, c_int, c_int, P, P, P, P, c_int, P, P]
     L.cox_combine.restype = c_int
     L.cox_combine.argtypes = [P, P, P, c_int, c_int, c_int, P, P, c_int, P]
     L.cox_ep_counts_put.restype = c_int

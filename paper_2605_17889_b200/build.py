@@ -17,7 +17,7 @@ PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 ROOT = PKG.parent
 LIB = PKG / "libcoxmoe.so"
-SOURCES = ["capi.cu", "router.cu", "permute.cu", "combine.cu", "grouped_gemm.cu", "small_gemm.cu", "router_tc.cu", "router_e8.cu", "ep.cu"]
+SOURCES = ["capi.cu", "router.cu", "permute.cu", "combine.cu", "grouped_gemm.cu", "small_gemm.cu", "router_tc.cu", "router_e8.cu", "fetch.cu", "ep.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

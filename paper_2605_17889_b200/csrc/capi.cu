@@ -38,6 +38,8 @@ int launch_small_ffn(const void* x, int T, const int32_t* row_tokens, const void
                      int ffs, void* hs, void* ys, const int32_t* cdst, const float* cw, int k, void* out,
                      int phases, cudaStream_t s, const SmallDense* dense = nullptr,
                      const SmallIdx* fromidx = nullptr);
+int launch_fetch_experts(const int32_t* counts, int n, const int32_t* expert_ids, const void* const* src,
+                         void* const* dst, const long long* bytes, int max_ctas, int32_t* fetched, cudaStream_t s);
 int launch_combine(const void* y_perm, const int32_t* dst, const float* w, int T, int k, int d, const void* shared,
                    void* out, int out_is_bf16, cudaStream_t s);
 
@@ -81,6 +83,8 @@ static int cuda_status(int rc, const char* what) {
   if (rc == 0) return 0;
   if (rc == COX_ECUDA) {
     cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) e = cox::g_last_cuda_error;
+    cox::g_last_cuda_error = cudaSuccess;
     return fail(COX_ECUDA, "%s: CUDA error: %s", what, cudaGetErrorString(e));
   }
   if (rc == COX_EINVAL) return fail(COX_EINVAL, "%s: invalid argument (tensor map encode rejected the operand)", what);
@@ -289,6 +293,25 @@ int cox_decode_moe(const void* x, int T, const void* wg, int E, int k, int mode,
   return cuda_status(rc, fn);
 }
 
+int cox_fetch_experts(const int32_t* counts, int E, int n, const int32_t* expert_ids, const void* const* host_src,
+                      void* const* dst, const long long* bytes, int max_ctas, int32_t* fetched, void* stream) {
+  const char* fn = "cox_fetch_experts";
+  if (n < 0 || n > 64 || E < 1 || max_ctas < 0)
+    return fail(COX_EINVAL, "%s: need 0 <= n <= 64, E >= 1 (n=%d E=%d)", fn, n, E);
+  if (n == 0) return 0;
+  if (!counts || !expert_ids || !host_src || !dst || !bytes) return fail(COX_EINVAL, "%s: null pointer", fn);
+  for (int i = 0; i < n; ++i) {
+    if (expert_ids[i] < 0 || expert_ids[i] >= E)
+      return fail(COX_EINVAL, "%s: expert %d outside [0, %d)", fn, expert_ids[i], E);
+    if (!host_src[i] || !dst[i] || !aligned16(host_src[i]) || !aligned16(dst[i]) || bytes[i] < 0 || bytes[i] % 16)
+      return fail(COX_EINVAL, "%s: entry %d null, unaligned or not a multiple of 16 bytes", fn, i);
+  }
+  int rc = cox::launch_fetch_experts(counts, n, expert_ids, host_src, dst, bytes, max_ctas, fetched,
+                                     static_cast<cudaStream_t>(stream));
+  if (rc == -1) return fail(COX_EINVAL, "%s: a source is not pinned (mapped) host memory", fn);
+  return cuda_status(rc, fn);
+}
+
 int cox_combine(const void* y_perm, const int32_t* dst, const float* w, int T, int k, int d, const void* shared_out,
                 void* out, int out_dtype, void* stream) {
   if (T < 0 || k < 1 || k > 8 || d <= 0 || d % 8) return fail(COX_EINVAL, "cox_combine: need 1<=k<=8, d%%8==0");
@@ -348,7 +371,7 @@ int cox_interleave_w13(const void* w1, const void* w3, int ff, int d, void* w13,
   if (!aligned16(w1) || !aligned16(w3) || !aligned16(w13)) return fail(COX_EINVAL, "cox_interleave_w13: unaligned");
   cox::interleave_w13_kernel<<<1184, 256, 0, static_cast<cudaStream_t>(stream)>>>(
       static_cast<const uint4*>(w1), static_cast<const uint4*>(w3), ff, d, static_cast<uint4*>(w13));
-  return cuda_status(cudaGetLastError() == cudaSuccess ? 0 : COX_ECUDA, "cox_interleave_w13");
+  return cuda_status(cox::launch_status(), "cox_interleave_w13");
 }
 
 }  // extern "C"

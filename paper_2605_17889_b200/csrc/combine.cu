@@ -115,7 +115,7 @@ int launch_combine(const void* y_perm, const int32_t* dst, const float* w, int T
                             static_cast<__nv_bfloat16*>(out));
   else
     launch_k<float>(k, (int)blocks, s, y, dst, w, T, d, static_cast<const float*>(shared), static_cast<float*>(out));
-  return cudaGetLastError() == cudaSuccess ? 0 : -2;
+  return launch_status();
 }
 
 }  // namespace cox

@@ -13,6 +13,16 @@ namespace cox {
 // for the decode router's tickets, then fp32 scratch rows.
 constexpr size_t ROUTER_WS_HEADER = 512;
 
+// The CUDA error behind the last -2 a launcher returned on this thread
+// (cudaGetLastError clears the sticky state, so it is kept for cox_last_error).
+inline thread_local cudaError_t g_last_cuda_error = cudaSuccess;
+inline int launch_status() {
+  const cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) return 0;
+  g_last_cuda_error = e;
+  return -2;
+}
+
 
 COX_DEV uint32_t smem_u32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
 

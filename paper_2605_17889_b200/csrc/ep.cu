@@ -150,13 +150,13 @@ __global__ void __launch_bounds__(256) ep_combine_kernel(const int32_t* __restri
 int launch_ep_counts_put(const int32_t* counts, int E, int rank, int world, int32_t* const* peer_counts,
                          cudaStream_t s) {
   ep_counts_put_kernel<<<1, 256, 0, s>>>(counts, E, rank, world, peer_counts);
-  return cudaGetLastError() == cudaSuccess ? 0 : -2;
+  return launch_status();
 }
 
 int launch_ep_offsets(const int32_t* counts_all, int G, int E, int rank, long long cap, int32_t* recv_seg,
                       int32_t* send_base, int32_t* overflow, cudaStream_t s) {
   ep_offsets_kernel<<<1, 32, 0, s>>>(counts_all, G, E, rank, cap, recv_seg, send_base, overflow);
-  return cudaGetLastError() == cudaSuccess ? 0 : -2;
+  return launch_status();
 }
 
 int launch_ep_dispatch(const int32_t* idx, const int32_t* dst_local, const int32_t* offsets_local,
@@ -168,7 +168,7 @@ int launch_ep_dispatch(const int32_t* idx, const int32_t* dst_local, const int32
   ep_dispatch_kernel<<<(int)blocks, 256, 0, s>>>(idx, dst_local, offsets_local, send_base, T, k, L, cap,
                                                  static_cast<const __nv_bfloat16*>(x), d,
                                                  reinterpret_cast<__nv_bfloat16* const*>(peer_recv), route_row);
-  return cudaGetLastError() == cudaSuccess ? 0 : -2;
+  return launch_status();
 }
 
 int launch_ep_combine(const int32_t* idx, const int32_t* route_row, const float* w, int T, int k, int d, int L,
@@ -186,7 +186,7 @@ int launch_ep_combine(const int32_t* idx, const int32_t* route_row, const float*
     default:
       return -1;
   }
-  return cudaGetLastError() == cudaSuccess ? 0 : -2;
+  return launch_status();
 }
 
 }  // namespace cox

@@ -598,7 +598,7 @@ int launch_grouped_gemm(int epi, const void* A, long long rows_cap, int K, const
     else GM_LAUNCH(EPI_STORE, 1);
   }
 #undef GM_LAUNCH
-  return cudaGetLastError() == cudaSuccess ? 0 : -2;
+  return launch_status();
 }
 
 }  // namespace cox

@@ -309,7 +309,7 @@ int launch_permute(const int32_t* idx, int T, int k, int E, int tile_m, const vo
   if (x_perm) perm_copy<<<(int)cb, 256, 0, s>>>(dst, T, k, static_cast<const __nv_bfloat16*>(x), d,
                                     static_cast<__nv_bfloat16*>(x_perm));
   if (tile_m > 1 && x_perm) perm_zero_pad<<<dim3(8, E), 256, 0, s>>>(offsets, seg_counts, E, d, static_cast<__nv_bfloat16*>(x_perm));
-  return cudaGetLastError() == cudaSuccess ? 0 : -2;
+  return launch_status();
 }
 
 }  // namespace cox

@@ -398,7 +398,7 @@ int launch_router_bf16w(const void* x, const void* wg, int T, int d, int E, int 
         static_cast<const __nv_bfloat16*>(x), static_cast<const __nv_bfloat16*>(wg), T, d, E, k, mode, idx, w,
         counts);
   }
-  return cudaGetLastError() == cudaSuccess ? 0 : -2;
+  return launch_status();
 }
 
 // ---------------------------------------------------------------- decode router
@@ -503,7 +503,7 @@ static int launch_router_decode(const void* x, int x_is_bf16, const void* wg, in
     if (wg_is_bf16) RD_LAUNCH(float, __nv_bfloat16); else RD_LAUNCH(float, float);
   }
 #undef RD_LAUNCH
-  return cudaGetLastError() == cudaSuccess ? 0 : -2;
+  return launch_status();
 }
 
 int launch_router_tc(const void* x, const void* wg, int T, int d, int E, int k, int mode, int32_t* idx, float* w,
@@ -557,7 +557,7 @@ int launch_router(const void* x, int x_is_bf16, const void* wg, int wg_is_bf16, 
     if (blocks > 148L * 8) blocks = 148L * 8;
     router_topk_staged_kernel<<<(int)blocks, RT_WARPS * 32, staged_smem, s>>>(
         static_cast<const __nv_bfloat16*>(x), static_cast<const float*>(wg), T, d, E, k, mode, idx, w, counts);
-    return cudaGetLastError() == cudaSuccess ? 0 : -2;
+    return launch_status();
   }
   int groups = (E + RT_EG - 1) / RT_EG;
   int egn = 1;
@@ -589,7 +589,7 @@ int launch_router(const void* x, int x_is_bf16, const void* wg, int wg_is_bf16, 
   }
 #undef RT_BY_W
 #undef RT_LAUNCH
-  return cudaGetLastError() == cudaSuccess ? 0 : -2;
+  return launch_status();
 }
 
 }  // namespace cox

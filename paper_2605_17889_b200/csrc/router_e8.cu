@@ -42,7 +42,7 @@ constexpr int R8_SLAB = 256;                // d columns per stage: one 8-elemen
 constexpr uint32_t R8_STAGE_BYTES = R8_TILE * R8_SLAB * 2;  // 32 KB
 constexpr int R8_MAX_STAGES = 6;
 constexpr int R8_THREADS = (R8_WARPS + 1) * 32;  // + producer warp
-constexpr size_t R8_SMEM_LIMIT = 227 * 1024;
+constexpr size_t R8_SMEM_LIMIT = 227 * 1024 - 256;  // beside the static s_hist
 
 // bf16 pair -> fp32 on the ALU pipe (PRMT / LOP3), keeping the FMA pipe for the FFMA2s
 COX_DEV float bf16_lo(uint32_t u) {
@@ -89,7 +89,7 @@ __global__ void __launch_bounds__(R8_THREADS, 1)
 router_e8_kernel(const __grid_constant__ CUtensorMap xmap, const WT* __restrict__ wg, int T, int d, int E, int k,
                  int mode, int stages, int32_t* __restrict__ idx, float* __restrict__ wout,
                  int32_t* __restrict__ counts) {
-  extern __shared__ __align__(1024) uint8_t r8_smem[];
+  extern __shared__ __align__(128) uint8_t r8_smem[];
   uint8_t* sx = r8_smem;                                                         // [stages][64][256] bf16
   WT* sw = reinterpret_cast<WT*>(r8_smem + (size_t)stages * R8_STAGE_BYTES);     // [8][d]
   float* s_logit = reinterpret_cast<float*>(sw + 8 * (size_t)d);                 // [8 warps][64]
@@ -264,24 +264,19 @@ int launch_router_e8(const void* x, const void* wg, int wg_is_bf16, int T, int d
   const int grid = ntiles < num_sms ? ntiles : num_sms;
   const size_t smem = router_e8_smem(d, wg_is_bf16, stages);
   if (wg_is_bf16) {
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(router_e8_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)R8_SMEM_LIMIT);
-      attr = true;
-    }
+    if (cudaFuncSetAttribute(router_e8_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem) != cudaSuccess)
+      return launch_status();
     router_e8_kernel<__nv_bfloat16><<<grid, R8_THREADS, smem, s>>>(
         xmap, static_cast<const __nv_bfloat16*>(wg), T, d, E, k, mode, stages, idx, w, counts);
   } else {
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(router_e8_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)R8_SMEM_LIMIT);
-      attr = true;
-    }
+    if (cudaFuncSetAttribute(router_e8_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+        cudaSuccess)
+      return launch_status();
     router_e8_kernel<float><<<grid, R8_THREADS, smem, s>>>(xmap, static_cast<const float*>(wg), T, d, E, k, mode,
                                                           stages, idx, w, counts);
   }
-  return cudaGetLastError() == cudaSuccess ? 0 : -2;
+  return launch_status();
 }
 
 }  // namespace cox

@@ -491,7 +491,7 @@ int launch_router_tc(const void* x, const void* wg, int T, int d, int E, int k, 
   else return -3;
 #undef RR_BY_NE
 #undef RR_LAUNCH
-  return cudaGetLastError() == cudaSuccess ? 0 : -2;
+  return launch_status();
 }
 
 }  // namespace cox

@@ -995,10 +995,10 @@ int launch_small_ffn(const void* x, int T, const int32_t* row_tokens, const void
   SG_LAUNCH(2, 64);
 #undef SG_LAUNCH
   if (out && !fuse) {
-    if (cudaGetLastError() != cudaSuccess) return -2;
+    if (launch_status()) return -2;
     return launch_combine(y, cdst, cw, T, k, d, shared ? ys : nullptr, out, 1, s);
   }
-  return cudaGetLastError() == cudaSuccess ? 0 : -2;
+  return launch_status();
 }
 
 }  // namespace cox

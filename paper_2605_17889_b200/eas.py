@@ -11,6 +11,8 @@ algorithms exactly (pinned against the reference in tests/).
 """
 from __future__ import annotations
 
+from dataclasses import dataclass
+
 import numpy as np
 
 from .config import ActivationMap, ResidencyPlan
@@ -82,3 +84,105 @@ class Calibrator:
 
     def residency(self, capacity_per_layer: int) -> ResidencyPlan:
         return select_resident_experts(self.activation_map(), capacity_per_layer)
+
+
+# ---------------------------------------------------------------------------
+# Prototype selection (which batches calibrate the map).  Restated from the
+# reference so the GPU box needs no moeplan; pinned bit-for-bit against it in
+# tests/test_host.py (tests/golden/reference_golden.json).
+
+
+@dataclass(frozen=True)
+class Clustering:
+    """eas.Clustering (eas.py:225-240): assignments, centroids, the clustered
+    points and the inertia after every assignment step."""
+    assignments: np.ndarray
+    centroids: np.ndarray
+    embeddings: np.ndarray
+    iteration_inertia: tuple
+
+    @property
+    def num_clusters(self) -> int:
+        return self.centroids.shape[0]
+
+
+def _nearest(points: np.ndarray, centroids: np.ndarray):
+    """eas._nearest (eas.py:256-260): nearest centroid (ties -> lower id) and its squared distance."""
+    d2 = ((points[:, None, :] - centroids[None, :, :]) ** 2).sum(axis=2)
+    assign = d2.argmin(axis=1)
+    return assign, d2[np.arange(len(points)), assign]
+
+
+def _farthest_point_seeds(x: np.ndarray, k: int, seed: int) -> np.ndarray:
+    """eas._farthest_point_seeds (eas.py:263-272), same RNG stream."""
+    rng = np.random.default_rng(seed)
+    first = int(rng.integers(len(x)))
+    chosen = [first]
+    min_d2 = ((x - x[first]) ** 2).sum(axis=1)
+    for _ in range(k - 1):
+        nxt = int(min_d2.argmax())
+        chosen.append(nxt)
+        min_d2 = np.minimum(min_d2, ((x - x[nxt]) ** 2).sum(axis=1))
+    return x[chosen].copy()
+
+
+def cluster(embeddings, num_clusters: int, seed: int = 0, max_iters: int = 100, tolerance: float = 1e-6) -> Clustering:
+    """eas.cluster (eas.py:275-317): Lloyd iterations from farthest-point seeds;
+    empty clusters reseeded with the point farthest from its centroid.
+    Defaults = StratificationConfig's max_kmeans_iters / tolerance."""
+    x = np.asarray(embeddings, dtype=np.float64)
+    k = int(num_clusters)
+    if k < 1 or k > len(x):
+        raise ValueError("num_clusters must be in 1..number of samples")
+    centroids = _farthest_point_seeds(x, k, seed)
+    inertia_log = []
+    assign = np.zeros(len(x), dtype=np.int64)
+    for _ in range(max_iters):
+        assign, d2 = _nearest(x, centroids)
+        for c in range(k):
+            if not np.any(assign == c):
+                outlier = int(d2.argmax())
+                centroids = centroids.copy()
+                centroids[c] = x[outlier]
+                assign[outlier] = c
+                d2 = d2.copy()
+                d2[outlier] = 0.0
+        inertia_log.append(float(d2.sum()))
+        new_centroids = centroids.copy()
+        for c in range(k):
+            members = assign == c
+            if np.any(members):
+                new_centroids[c] = x[members].mean(axis=0)
+        shift = float(np.sqrt(((new_centroids - centroids) ** 2).sum(axis=1)).max())
+        centroids = new_centroids
+        if shift < tolerance:
+            break
+    assign, d2 = _nearest(x, centroids)
+    inertia_log.append(float(d2.sum()))
+    return Clustering(assignments=assign, centroids=centroids, embeddings=x, iteration_inertia=tuple(inertia_log))
+
+
+def select_prototypes(clustering: Clustering, sample_ratio: float) -> list:
+    """eas.select_prototypes (eas.py:320-339): per cluster the
+    round(sample_ratio * n_k) members nearest its centroid (>= 1 per non-empty
+    cluster), ties by index; sorted sample ids."""
+    if not (0.0 < sample_ratio <= 1.0):
+        raise ValueError("sample_ratio must be in (0, 1]")
+    chosen = []
+    for c in range(clustering.num_clusters):
+        members = np.flatnonzero(clustering.assignments == c)
+        if len(members) == 0:
+            continue
+        quota = max(1, int(sample_ratio * len(members) + 0.5))
+        d2 = ((clustering.embeddings[members] - clustering.centroids[c]) ** 2).sum(axis=1)
+        order = np.lexsort((members, d2))
+        chosen.extend(int(i) for i in members[order[:quota]])
+    return sorted(chosen)
+
+
+def random_hit_ratio(counts, experts_per_layer: int, capacity: int, seeds=range(50)) -> float:
+    """Mean hit ratio of eas.random_baseline plans over `seeds` (the CLI's
+    hitratio baseline averages 50 plans, cli.py:442-448)."""
+    counts = np.asarray(counts, dtype=float)
+    return float(np.mean([hit_ratio_from_counts(counts, random_baseline(experts_per_layer, capacity,
+                                                                        counts.shape[0], s)) for s in seeds]))

@@ -309,6 +309,30 @@ def decode_moe(x: torch.Tensor, wg: torch.Tensor, k: int, mode: int, w13: Sequen
     return out
 
 
+def fetch_experts(counts: torch.Tensor, expert_ids: Sequence[int], host_src: Sequence[torch.Tensor],
+                  dst: Sequence[torch.Tensor], max_ctas: int = 0, fetched: torch.Tensor | None = None, stream=None):
+    """K6': copy host_src[i] (pinned host) -> dst[i] (device) for every listed
+    entry whose expert has router count > 0; decided on the device, no host sync."""
+    _need(counts, "counts", torch.int32, 1)
+    if not (len(expert_ids) == len(host_src) == len(dst)):
+        raise ValueError("one source and one slot per entry")
+    nbytes = (ctypes.c_longlong * max(1, len(dst)))()
+    for i, (a, b) in enumerate(zip(host_src, dst)):
+        if a.is_cuda or not a.is_pinned() or not a.is_contiguous():
+            raise ValueError(f"host_src[{i}] must be contiguous pinned host memory")
+        _need(b, f"dst[{i}]")
+        if a.numel() * a.element_size() != b.numel() * b.element_size():
+            raise ValueError(f"entry {i}: source and slot sizes differ")
+        nbytes[i] = a.numel() * a.element_size()
+    if fetched is not None:
+        _need(fetched, "fetched", torch.int32, 1)
+    L = _lib.lib()
+    _lib.check(L.cox_fetch_experts(counts.data_ptr(), counts.numel(), len(expert_ids), _ids(expert_ids),
+                                   _ptrs(host_src), _ptrs(dst), nbytes, max_ctas,
+                                   fetched.data_ptr() if fetched is not None else None, _stream(stream)),
+               "cox_fetch_experts")
+
+
 def combine(y_perm: torch.Tensor, dst: torch.Tensor, w: torch.Tensor, shared: torch.Tensor | None = None,
             out: torch.Tensor | None = None, out_dtype=_BF16, stream=None):
     """K5: out[t] = sum_j w[t,j] y_perm[dst[t,j]] (+ shared[t])."""

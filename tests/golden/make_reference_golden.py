@@ -111,7 +111,15 @@ def main():
            "resident": [list(x) for x in plan.resident], "capacity": 16, "hit_ratio": eas.hit_ratio(trace, plan),
            "random_hit_ratio": eas.hit_ratio(trace, eas.random_baseline(64, 16, 4, 0))}
 
-    OUT.write_text(json.dumps({"systems": {k: sysd(v) for k, v in systems.items()},
+    # prototype selection (cluster + select_prototypes) on a small trace
+    ptrace = eas.generate_synthetic_trace(600, 12, 2, 16, 2, 5, 1.2, seed=11)
+    pcfg = eas.StratificationConfig(num_clusters=5, sample_ratio=0.04, seed=11)
+    pcl = eas.cluster(ptrace, pcfg)
+    protos = {"embeddings": ptrace.embeddings.tolist(), "num_clusters": 5, "sample_ratio": 0.04, "seed": 11,
+              "assignments": pcl.assignments.tolist(), "centroids": pcl.centroids.tolist(),
+              "inertia": list(pcl.iteration_inertia), "prototypes": eas.select_prototypes(pcl, 0.04, 11)}
+
+    OUT.write_text(json.dumps({"prototypes": protos, "systems": {k: sysd(v) for k, v in systems.items()},
                                "models": {k: [v.num_layers, v.hidden_dim, v.expert_dim, v.experts_per_layer, v.top_k,
                                               v.dtype_bytes] for k, v in models.items()},
                                "batches": {k: [v.batch_size, v.input_len, v.output_len] for k, v in batches.items()},

@@ -93,6 +93,17 @@ def test_hit_ratio_and_calibrator_vs_reference():
     assert h["hit_ratio"] > h["random_hit_ratio"] + 0.3
 
 
+def test_cluster_and_prototypes_vs_reference():
+    """Prototype selection for calibration: eas.cluster (Lloyd + farthest-point
+    seeds) and eas.select_prototypes restated bit-for-bit (eas.py:263-339)."""
+    g = GOLD["prototypes"]
+    cl = eas.cluster(np.asarray(g["embeddings"]), g["num_clusters"], seed=g["seed"])
+    assert cl.assignments.tolist() == g["assignments"]
+    assert cl.centroids.tolist() == g["centroids"]
+    assert list(cl.iteration_inertia) == g["inertia"]
+    assert eas.select_prototypes(cl, g["sample_ratio"]) == g["prototypes"]
+
+
 def test_mirror_validation_matches_reference_rules():
     with pytest.raises(ValueError):
         C.ModelConfig(1, 8, 8, 4, 5)
