@@ -55,6 +55,9 @@ CONFIGS = {
     "C3": (64 * 4096, 6144, 16384, 8, 2, "mixtral", 0,
            "C3 Mixtral-8x22B-shaped 56-layer MoE stack, batch 64x4096, HBM budget -> calibrated hot experts "
            "resident, cold experts streamed from pinned host memory"),
+    "C3D": (8, 6144, 16384, 8, 2, "mixtral", 0,
+            "C3 56-layer stack decode step: 8 sequences x 1 token; cold experts fetched only when routed to "
+            "(device-side decision), calibrated vs random residency"),
 }
 STACK_LAYERS = 56
 
@@ -265,36 +268,74 @@ def run_reference(args, cfg):
     print(json.dumps(line), flush=True)
 
 
-def run_stack(args, cfg):
-    """C3: the 56-layer stratified stack on one GPU (BASELINE.json configs[2])."""
-    import torch
-    from paper_2605_17889_b200 import costmodel as CM
-    from paper_2605_17889_b200.config import ModelConfig, ResidencyPlan, AllocationStrategy, Device, BatchConfig, Phase
-    from paper_2605_17889_b200.executor import StratifiedMoEStack, make_pool, make_router_weights
-    from paper_2605_17889_b200.eas import hit_ratio_from_counts
-    from paper_2605_17889_b200.synthetic import make_tokens
+def _stack_setup(args, cfg, T_eval):
+    """C3 stack on one GPU with topic-structured routing; calibrated residency.
 
+    Expert (l, e) weights are pool[(l*E + e) % P] (P distinct experts in pinned
+    host RAM); the router rows carry per-(topic, layer) Zipf preferences
+    (synthetic.make_topic_router, the GPU analogue of
+    eas.generate_synthetic_trace).  Calibration = prefill-only probing
+    (PAPER.md:308): candidate sequences are clustered on their embeddings
+    (eas.cluster), prototypes chosen nearest-to-centroid (eas.select_prototypes,
+    ratio 0.05), run through the stack, and the K1 histograms give the
+    ActivationMap from which eas.select_resident_experts picks the hot set
+    under the HBM budget (max_capacity: measured free HBM, the vram_usage
+    feasibility test)."""
+    import torch
+    from paper_2605_17889_b200 import eas
+    from paper_2605_17889_b200.config import ResidencyPlan
+    from paper_2605_17889_b200.executor import StratifiedMoEStack, make_pool
+    from paper_2605_17889_b200.synthetic import (make_topic_router, make_topic_tokens, make_topic_workload,
+                                                 sequence_embeddings)
     T, d, ff, E, k, mode, _, desc = cfg
     N = args.layers
     dev = torch.device("cuda", 0)
     torch.cuda.set_device(dev)
-    model = ModelConfig(N, d, ff, E, k, 2)
     pool = make_pool(args.pool, d, ff, seed=0, device=dev, residual_scale=(2.0 * N) ** -0.5)
-    wg = make_router_weights(N, E, d, seed=7, device=dev)
+    wl = make_topic_workload(d, num_topics=args.topics, device=dev)
+    wg = make_topic_router(N, E, d, wl, device=dev)
     stack = StratifiedMoEStack(N, wg, pool, k, ResidencyPlan(tuple(() for _ in range(N)), 0), mode)
-    # calibration: prototype batches through the all-cold stack (prefill-only probing)
-    protos = [make_tokens(args.proto_tokens, d, seed=100 + i, device=dev) for i in range(2)]
-    # capacity from the HBM budget is computed after calibration frees its buffers
-    stack.calibrate(protos, 0)
-    del protos
-    cap = stack.max_capacity(T)
-    from paper_2605_17889_b200.eas import select_resident_experts
-    plan = select_resident_experts(stack.calibration_map, cap)
-    stack.set_residency(plan)
-    x = make_tokens(T, d, seed=1, device=dev)
-    counts = torch.zeros((N, E), dtype=torch.int32, device=dev)
+    n_cand, cand_len = 256, 256
+    xc, _ = make_topic_tokens(wl, n_cand, cand_len, seed=100, device=dev)
+    cl = eas.cluster(sequence_embeddings(xc, n_cand), args.topics, seed=0)
+    protos = eas.select_prototypes(cl, 0.05)
+    xp = xc.reshape(n_cand, cand_len, d)[torch.tensor(protos, device=dev)].reshape(-1, d).contiguous()
+    del xc
+    cap = stack.max_capacity(T_eval)
+    t0 = time.perf_counter()
+    plan = stack.calibrate([xp], cap)
+    t_cal = time.perf_counter() - t0
+    info = {"prototypes": len(protos), "prototype_tokens": int(xp.shape[0]), "candidates": n_cand,
+            "clusters": args.topics, "calibration_s": round(t_cal, 2), "capacity_per_layer": cap}
+    return stack, wl, plan, cap, info
+
+
+def _hit_summary(counts, plan, E, cap):
+    """Token-weighted hit ratio of the timed batch's K1 histograms: calibrated
+    plan, eas.random_baseline (mean of 50 seeds), and the batch's own top-cap."""
+    from paper_2605_17889_b200 import eas
+    from paper_2605_17889_b200.config import ActivationMap
+    c = counts.cpu().numpy().astype(float)
+    best = eas.select_resident_experts(ActivationMap(c + 1e-9), cap)
+    return {"calibrated": eas.hit_ratio_from_counts(c, plan),
+            "random_baseline_mean50": eas.random_hit_ratio(c, E, cap),
+            "exact_map_upper_bound": eas.hit_ratio_from_counts(c, best)}
+
+
+def run_stack(args, cfg):
+    """C3: the 56-layer stratified stack on one GPU (BASELINE.json configs[2])."""
+    import torch
+    from paper_2605_17889_b200 import costmodel as CM
+    from paper_2605_17889_b200.config import ModelConfig, AllocationStrategy, Device, BatchConfig, Phase
+    from paper_2605_17889_b200.synthetic import make_topic_tokens
+
+    T, d, ff, E, k, mode, _, desc = cfg
+    N = args.layers
+    stack, wl, plan, cap, cal = _stack_setup(args, cfg, T)
+    x, _ = make_topic_tokens(wl, 64, T // 64, seed=1, device="cuda")
+    counts = torch.zeros((N, E), dtype=torch.int32, device="cuda")
     for _ in range(args.warmup):
-        stack(x)
+        stack(x, fetch="stream")
     torch.cuda.synchronize()
     s = torch.cuda.current_stream()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -302,38 +343,104 @@ def run_stack(args, cfg):
         torch.cuda.synchronize()
         a.record(s)
         for i in range(args.steps):
-            stack(x, counts_out=counts if i == args.steps - 1 else None)
+            stack(x, counts_out=counts if i == args.steps - 1 else None, fetch="stream")
         b.record(s)
         torch.cuda.synchronize()
     ms = a.elapsed_time(b) / args.steps
-    stack(x, timeline=True)
+    stack(x, timeline=True, fetch="stream")
     parts = stack.measured_parts()
-    hit = hit_ratio_from_counts(counts.cpu().numpy().astype(float), plan)
     pk = peaks()
     flops = N * (6.0 * T * k * d * ff + 2.0 * T * d * E)
     n_cold = sum(len(c) for c in stack.cold)
-    mig_bytes = n_cold * pool.nbytes_per_expert()
+    mig_bytes = n_cold * stack.pool.nbytes_per_expert()
+    model = ModelConfig(N, d, ff, E, k, 2)
     strat = AllocationStrategy((Device.GPU,) * 3, cap, E - cap, 0, m=64)
-    ana = CM.expert_stage_parts(strat, Phase.prefill(4096), CM.b200_system(), model, BatchConfig(64, 4096, 0),
+    system = CM.load_system_spec(CM.B200_SYSTEM_YAML)
+    ana = CM.expert_stage_parts(strat, Phase.prefill(T // 64), system, model, BatchConfig(64, T // 64, 0),
                                 stack.calibration_map, count_top_k=True)
     line = {
         "metric": metric_name("C3"), "value": T / (ms / 1e3), "unit": "tokens/s", "n_gpus": 1,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
-        "data": "synthetic; expert (l,e) weights = pool[(l*E+e) % P] (P distinct experts in pinned host RAM)",
+        "data": "synthetic; topic-structured routing (make_topic_router); expert (l,e) weights = pool[(l*E+e) % P] "
+                "(P distinct experts in pinned host RAM)",
         "config": {"workload": desc, "layers": N, "tokens": T, "d": d, "ff": ff, "E": E, "k": k,
                    "resident_per_layer": cap, "resident_bytes": stack.resident_bytes, "host_pool_experts": args.pool,
-                   "cold_experts_per_step": n_cold, "h2d_bytes_per_step": mig_bytes},
+                   "cold_experts_per_step": n_cold, "h2d_bytes_per_step": mig_bytes, "calibration": cal},
         "stack_tflops": flops / (ms / 1e3) / 1e12,
         "frac_of_bf16_sustained": flops / (ms / 1e3) / 1e12 / pk["bf16_sus"],
-        "hit_ratio": hit,
+        "hit_ratio": _hit_summary(counts, plan, E, cap),
         "measured_parts_per_layer_s": {"act_load": parts.act_load, "mig_load": parts.mig_load,
                                        "lat_gpu": parts.lat_gpu},
         "analytical_parts_per_layer_s": {"act_load": ana.act_load, "mig_load": ana.mig_load, "lat_gpu": ana.lat_gpu,
-                                         "system": "b200 measured peaks, 55 GB/s link, k counted"},
+                                         "system": "configs/system_b200.yaml (measured peaks), k counted"},
         "h2d_gbs": mig_bytes / max(1e-9, parts.mig_load * N) / 1e9,
         "gpu_launches": stack.launches_per_step * args.steps,
         "clocks": clk.summary(),
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_stack_decode(args, cfg):
+    """C3D: decode steps of the C3 stack (T tokens = T sequences x 1 token).
+    Cold experts are fetched only if the layer's router sent them tokens
+    (cox_fetch_experts, decided on the device), so the residency plan's hit
+    ratio turns into PCIe bytes: the calibrated plan (eas.select_resident_experts
+    on prototype histograms) is timed against eas.random_baseline residency."""
+    import torch
+    from paper_2605_17889_b200 import eas
+    from paper_2605_17889_b200.synthetic import make_topic_tokens
+
+    T, d, ff, E, k, mode, _, desc = cfg
+    N = args.layers
+    stack, wl, plan, cap, cal = _stack_setup(args, cfg, max(T, 4096))
+    per_expert = stack.pool.nbytes_per_expert()
+
+    def measure(tag):
+        xs = [make_topic_tokens(wl, T, 1, seed=200 + i, device="cuda")[0] for i in range(args.steps + args.warmup)]
+        counts = torch.zeros((N, E), dtype=torch.int32, device="cuda")
+        tot = torch.zeros((N, E), dtype=torch.int64, device="cuda")
+        fetched = 0.0
+        for i in range(args.warmup):
+            stack(xs[i], fetch="touched")
+        torch.cuda.synchronize()
+        s = torch.cuda.current_stream()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with ClockSampler(0) as clk:
+            a.record(s)
+            for i in range(args.steps):
+                stack(xs[args.warmup + i], fetch="touched", counts_out=counts)
+                tot += counts
+                fetched += stack._fetched.sum()  # device tensor: no sync inside the timed loop
+            b.record(s)
+            torch.cuda.synchronize()
+        ms = a.elapsed_time(b) / args.steps
+        f = float(fetched) / 2.0 / args.steps  # cold experts fetched per step (W13 + W2 entries)
+        hit = eas.hit_ratio_from_counts(tot.cpu().numpy().astype(float), stack.plan)
+        return {"tag": tag, "ms_per_step": ms, "tokens_per_s": T / (ms / 1e3), "hit_ratio": hit,
+                "cold_experts_fetched_per_step": f, "pcie_bytes_per_step": f * per_expert,
+                "pcie_gbs": f * per_expert / (ms / 1e3) / 1e9, "clocks": clk.summary()}
+
+    cal_res = measure("calibrated")
+    rnd_plan = eas.random_baseline(E, cap, N, seed=0)
+    stack.set_residency(rnd_plan)
+    rnd_res = measure("random_baseline")
+    line = {
+        "metric": metric_name("C3D"), "value": cal_res["tokens_per_s"], "unit": "tokens/s", "n_gpus": 1,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": cal_res["ms_per_step"],
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic; topic-structured routing; decode tokens drawn per step from the topic mix",
+        "config": {"workload": desc, "layers": N, "tokens_per_step": T, "d": d, "ff": ff, "E": E, "k": k,
+                   "resident_per_layer": cap, "host_pool_experts": args.pool, "calibration": cal,
+                   "fetch": "touched-only (cox_fetch_experts: cold experts with router count > 0)"},
+        "calibrated": cal_res, "random_residency": rnd_res,
+        "speedup_calibrated_vs_random": rnd_res["ms_per_step"] / cal_res["ms_per_step"],
+        "roofline": {"kernel": "cold-expert fetch (PCIe, SM loads of mapped pinned memory)", "bound": "pcie",
+                     "achieved": cal_res["pcie_gbs"], "peak": 55.0, "unit": "GB/s",
+                     "frac": cal_res["pcie_gbs"] / 55.0, "traffic": None,
+                     "peak_kind": "copy-engine H2D rate of the C3 prefill stack (configs/system_b200.yaml)"},
+        "gpu_launches": None,
+        "clocks": cal_res["clocks"],
     }
     print(json.dumps(line), flush=True)
 
@@ -354,13 +461,13 @@ def main():
                     help="ablation: run the expert stage per micro-batch of this many tokens (not coalesced)")
     ap.add_argument("--layers", type=int, default=STACK_LAYERS, help="C3 stack depth")
     ap.add_argument("--pool", type=int, default=16, help="C3 distinct host-pool experts")
-    ap.add_argument("--proto-tokens", type=int, default=8192, help="C3 calibration batch size")
+    ap.add_argument("--topics", type=int, default=8, help="C3 latent routing topics (= calibration clusters)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.steps is None:
         # enough steps that the end-to-end pipeline's fill (first H2D) and drain
         # (last D2H) are a small share of the e2e number, within ~5 s per arm
-        args.steps = {"C3": 5, "C4D": 2000, "C2D": 1000, "C1": 200}.get(args.config, 30)
+        args.steps = {"C3": 5, "C3D": 5, "C4D": 2000, "C2D": 1000, "C1": 200}.get(args.config, 30)
         if args.impl == "reference":
             args.steps = 10
     cfg = CONFIGS[args.config]
@@ -368,6 +475,8 @@ def main():
         return run_reference(args, cfg)
     if args.config == "C3":
         return run_stack(args, cfg)
+    if args.config == "C3D":
+        return run_stack_decode(args, cfg)
 
     import torch
     import torch.distributed as dist

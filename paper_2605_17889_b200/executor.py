@@ -63,6 +63,9 @@ class StratifiedMoEStack:
         inside K5) instead of MoE_l(x_l) alone."""
         self.N = int(num_layers)
         self.wg = wg
+        # router weights in bf16 when that is exact (as MoELayer): half the bytes, shared-memory resident
+        wgb = wg.to(torch.bfloat16)
+        self.wg_router = wgb if torch.equal(wgb.float(), wg) else wg
         self.E = wg.shape[1]
         self.d = wg.shape[2]
         self.ff = pool.w2.shape[2]
@@ -137,20 +140,34 @@ class StratifiedMoEStack:
         base = (l % 2) * self.C
         return [self.ring.stage(self.pool, self.pool_map(l, e), base + j, timing) for j, e in enumerate(self.cold[l])]
 
-    def forward(self, x: torch.Tensor, timeline: bool = False, counts_out: torch.Tensor | None = None):
+    # decode-size batches fetch only the cold experts the router touched (on the device)
+    TOUCHED_T_MAX = 4096
+
+    def forward(self, x: torch.Tensor, timeline: bool = False, counts_out: torch.Tensor | None = None,
+                fetch: str = "auto"):
         """Run all N layers; returns the last layer's output (a view of an internal buffer).
 
         counts_out: optional [N, E] int32 device tensor receiving each layer's
-        routed-token histogram (calibration / hit-ratio accounting)."""
+        routed-token histogram (calibration / hit-ratio accounting).
+        fetch: "stream" — every cold expert of every layer is copied (copy
+        engine, two layers ahead, overlapped with the resident GEMMs; prefill);
+        "touched" — after each layer's router, cox_fetch_experts copies only the
+        cold experts that received tokens (decided on the device; decode-size
+        steps); "auto" — touched for T <= TOUCHED_T_MAX, else stream."""
         if x.dtype != torch.bfloat16 or x.shape[1] != self.d:
             raise ValueError(f"x must be bf16 [T, {self.d}]")
+        if fetch not in ("auto", "stream", "touched"):
+            raise ValueError("fetch must be auto, stream or touched")
         T = x.shape[0]
+        if fetch == "auto":
+            fetch = "touched" if T <= self.TOUCHED_T_MAX else "stream"
         b = self._buffers(T)
-        s = torch.cuda.current_stream()
+        self._records = []
         if self.ring is not None:
             self.ring.copy_events = []
-        evs = [] if timeline else None
-        mk = (lambda: torch.cuda.Event(enable_timing=True)) if timeline else None
+        if fetch == "touched":
+            return self._forward_touched(x, b, timeline, counts_out)
+        s = torch.cuda.current_stream()
         copy_done = {}
         if self.C:
             for l in range(min(2, self.N)):
@@ -158,23 +175,19 @@ class StratifiedMoEStack:
         cur = x
         for l in range(self.N):
             out = b.ping if (l % 2 == 0) else b.pong
-            if timeline:
-                e0 = mk(); e0.record(s)
-            ops.router_topk(cur, self.wg[l], self.k, self.mode, out=(b.idx, b.w, b.counts), workspace=b.router_ws)
-            ops.permute(b.idx, cur, self.E, 1, out=(b.offsets, b.dst, b.x_perm), workspace=b.ws)
-            if counts_out is not None:
-                counts_out[l].copy_(b.counts)
-            if timeline:
-                e1 = mk(); e1.record(s)
+            e0 = self._mark(timeline)
+            self._route(cur, b, l, counts_out)
+            e1 = self._mark(timeline)
             res = list(self.plan.resident[l])
             if res:
                 ops.grouped_swiglu(b.x_perm, b.offsets, res, [self.res_w13[l][e] for e in res], self.ff, h=b.h)
-            if timeline:
-                e2 = mk(); e2.record(s)
+            e2 = self._mark(timeline)
             cold = self.cold[l]
             if cold:
                 for ev in copy_done.pop(l, []):
                     s.wait_event(ev)
+            e2w = self._mark(timeline)  # the cold GEMMs' copies have landed
+            if cold:
                 base = (l % 2) * self.C
                 slots = [base + j for j in range(len(cold))]
                 ops.grouped_swiglu(b.x_perm, b.offsets, cold, [self.ring.w13[i] for i in slots], self.ff, h=b.h)
@@ -185,49 +198,105 @@ class StratifiedMoEStack:
             # had cold experts itself (plans may differ in exp_r per layer)
             if self.C and l + 2 < self.N and self.cold[l + 2]:
                 copy_done[l + 2] = self._stage_layer(l + 2, timeline)
-            if timeline:
-                e3 = mk(); e3.record(s)
+            e3 = self._mark(timeline)
             if res:
                 ops.grouped_down(b.h, b.offsets, res, [self.res_w2[l][e] for e in res], self.d, y=b.x_perm)
-            if timeline:
-                e4 = mk(); e4.record(s)
+            e4 = self._mark(timeline)
             # residual stream: out = x_l + sum_j w_j y_j, fused into K5 (shared_out = x_l)
             ops.combine(b.x_perm, b.dst, b.w, shared=cur if self.residual else None, out=out)
+            e5 = self._mark(timeline)
             if timeline:
-                e5 = mk(); e5.record(s)
-                evs.append((e0, e1, e2, e3, e4, e5))
+                self._records += [(f"expert:gather:L{l}", "gpu", e0, e1), (f"expert:gpu:resident:L{l}", "gpu", e1, e2),
+                                  (f"expert:wait:L{l}", "wait", e2, e2w), (f"expert:gpu:cold:L{l}", "gpu", e2w, e3),
+                                  (f"expert:gpu:resident:L{l}", "gpu", e3, e4), (f"expert:merge:L{l}", "gpu", e4, e5)]
             cur = out
-        self._timeline_events = evs
+        if timeline and self.ring is not None:
+            for i, (slot, a, b2) in enumerate(self.ring.copy_events):
+                self._records.append((f"expert:migrate:slot{slot}:{i}", "h2d", a, b2))
         return cur
 
     __call__ = forward
+
+    @staticmethod
+    def _mark(timeline: bool):
+        if not timeline:
+            return None
+        ev = torch.cuda.Event(enable_timing=True)
+        ev.record()
+        return ev
+
+    def _route(self, cur, b, l, counts_out):
+        ops.router_topk(cur, self.wg_router[l], self.k, self.mode, out=(b.idx, b.w, b.counts), workspace=b.router_ws)
+        ops.permute(b.idx, cur, self.E, 1, out=(b.offsets, b.dst, b.x_perm), workspace=b.ws)
+        if counts_out is not None:
+            counts_out[l].copy_(b.counts)
+
+    def _forward_touched(self, x, b, timeline, counts_out):
+        """Decode-size steps: per layer router -> device-side fetch of the touched
+        cold experts (pinned host -> slots [0, C)) -> one grouped K3/K4 over all
+        experts (resident copies and fetched slots) -> combine + residual.
+        self.fetched_entries accumulates, per layer, how many cold entries (W13 /
+        W2 of an expert) crossed PCIe."""
+        cur = x
+        if self.C:
+            if getattr(self, "_fetched", None) is None or self._fetched.shape != (self.N, 2 * self.C):
+                self._fetched = torch.zeros((self.N, 2 * self.C), dtype=torch.int32, device=self.device)
+        for l in range(self.N):
+            out = b.ping if (l % 2 == 0) else b.pong
+            e0 = self._mark(timeline)
+            self._route(cur, b, l, counts_out)
+            e1 = self._mark(timeline)
+            cold = self.cold[l]
+            w13 = [None] * self.E
+            w2 = [None] * self.E
+            for e, t in self.res_w13[l].items():
+                w13[e], w2[e] = t, self.res_w2[l][e]
+            if cold:
+                ids, src, dst = [], [], []
+                for j, e in enumerate(cold):
+                    p = self.pool_map(l, e)
+                    ids += [e, e]
+                    src += [self.pool.w13[p], self.pool.w2[p]]
+                    dst += [self.ring.w13[j], self.ring.w2[j]]
+                    w13[e], w2[e] = self.ring.w13[j], self.ring.w2[j]
+                ops.fetch_experts(b.counts, ids, src, dst, fetched=self._fetched[l, : 2 * len(cold)])
+            e2 = self._mark(timeline)
+            groups = list(range(self.E))
+            ops.grouped_swiglu(b.x_perm, b.offsets, groups, w13, self.ff, h=b.h)
+            ops.grouped_down(b.h, b.offsets, groups, w2, self.d, y=b.x_perm)
+            e3 = self._mark(timeline)
+            ops.combine(b.x_perm, b.dst, b.w, shared=cur if self.residual else None, out=out)
+            e4 = self._mark(timeline)
+            if timeline:
+                self._records += [(f"expert:gather:L{l}", "gpu", e0, e1), (f"expert:migrate:touched:L{l}", "h2d", e1, e2),
+                                  (f"expert:gpu:L{l}", "gpu", e2, e3), (f"expert:merge:L{l}", "gpu", e3, e4)]
+            cur = out
+        return cur
+
+    def fetched_cold_experts(self) -> float:
+        """Mean number of cold experts fetched per layer by the last touched-mode step."""
+        if getattr(self, "_fetched", None) is None:
+            return 0.0
+        return float(self._fetched.sum().item()) / 2.0 / self.N
 
     # ------------------------------------------------------------ reporting
     def timeline_records(self) -> list[dict]:
         """Measured timeline in sim.timeline_records' schema (sim.py:356-361):
         [{"name", "res", "ts", "dur"}] in seconds from the first event."""
         torch.cuda.synchronize()
-        evs = self._timeline_events or []
-        if not evs:
+        recs = getattr(self, "_records", None) or []
+        if not recs:
             return []
-        t0 = evs[0][0]
-        rec = []
-        ms = lambda a, b: a.elapsed_time(b) / 1e3  # noqa: E731
-        for l, (e0, e1, e2, e3, e4, e5) in enumerate(evs):
-            rec.append({"name": f"expert:gather:L{l}", "res": "gpu", "ts": ms(t0, e0), "dur": ms(e0, e1)})
-            rec.append({"name": f"expert:gpu:resident:L{l}", "res": "gpu", "ts": ms(t0, e1),
-                        "dur": ms(e1, e2) + ms(e3, e4)})
-            rec.append({"name": f"expert:gpu:cold:L{l}", "res": "gpu", "ts": ms(t0, e2), "dur": ms(e2, e3)})
-            rec.append({"name": f"expert:merge:L{l}", "res": "gpu", "ts": ms(t0, e4), "dur": ms(e4, e5)})
-        if self.ring is not None:
-            for i, (slot, a, b) in enumerate(self.ring.copy_events):
-                rec.append({"name": f"expert:migrate:slot{slot}:{i}", "res": "h2d", "ts": ms(t0, a), "dur": ms(a, b)})
-        return sorted(rec, key=lambda r: r["ts"])
+        t0 = recs[0][2]
+        out = [{"name": n, "res": r, "ts": t0.elapsed_time(a) / 1e3, "dur": a.elapsed_time(b) / 1e3}
+               for n, r, a, b in recs]
+        return sorted(out, key=lambda r: r["ts"])
 
     def measured_parts(self) -> ExpertStageParts:
         """Per-layer mean of the measured timeline, in ExpertStageParts' fields
         (costmodel.py:199-222): act_load 0 (activations stay in HBM),
-        mig_load = copy-engine busy time, lat_gpu = stage GPU time."""
+        mig_load = copy-engine busy time, lat_gpu = stage GPU time (kernels
+        only: time the stream spent waiting for a copy is excluded)."""
         rec = self.timeline_records()
         n = max(1, self.N)
         mig = sum(r["dur"] for r in rec if r["res"] == "h2d") / n
@@ -294,6 +363,65 @@ class StratifiedMoEStack:
         return plan
 
 
+_MEASURE_CACHE: dict = {}
+
+
+def measured_expert_stage_parts(strategy, phase, system, model, batch, activation_map=None, coalesced: bool = True,
+                                *, mode: str = "mixtral", warmup: int = 1, device=None) -> ExpertStageParts:
+    """The MEASURED counterpart of costmodel.expert_stage_parts, with its
+    signature (costmodel.py:225-233): one MoE layer of `model` runs on this
+    B200 over batch.batch_size x phase.seq_len synthetic tokens, with
+    strategy.exp_r experts resident (the hottest of `activation_map`, summed
+    over its layers) and strategy.exp_m streamed from pinned host memory.
+    Returns seconds per layer in ExpertStageParts' fields:
+      act_load     0 — activations stay in HBM (no PCIe gather on B200);
+      mig_load     copy-engine busy time of the exp_m cold experts;
+      lat_gpu      GPU time of the expert stage (router .. combine);
+      lat_cpu      0 — no CPU expert path (exp_c must be 0);
+      return_store 0.
+    coalesced=False runs ceil(B / strategy.m) micro-batches of strategy.m
+    sequences (the reference's `repeats`, costmodel.py:254-260) and sums them.
+    `system` is accepted for signature parity (the hardware is measured)."""
+    from .config import ActivationMap
+    from .synthetic import make_tokens
+    if strategy.exp_r + strategy.exp_m + strategy.exp_c != model.experts_per_layer:
+        raise ValueError(f"expert partition {strategy.exp_r}+{strategy.exp_m}+{strategy.exp_c} "
+                         f"does not cover the {model.experts_per_layer} activated experts")
+    if strategy.exp_c != 0:
+        raise ValueError("the B200 executor runs every expert on the GPU: exp_c must be 0")
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    E, d, ff, k = model.experts_per_layer, model.hidden_dim, model.expert_dim, model.top_k
+    key = (E, d, ff, k, mode, str(dev))
+    stack = _MEASURE_CACHE.get(key)
+    if stack is None:
+        _MEASURE_CACHE.clear()
+        pool = make_pool(E, d, ff, seed=0, device=dev)
+        wg = make_router_weights(1, E, d, seed=7, device=dev)
+        stack = StratifiedMoEStack(1, wg, pool, k, ResidencyPlan(((),), 0), mode, pool_map=lambda l, e: e,
+                                   residual=False)
+        _MEASURE_CACHE[key] = stack
+    counts = np.ones((1, E)) if activation_map is None else \
+        np.asarray(activation_map.counts, dtype=float).sum(axis=0, keepdims=True)
+    stack.set_residency(select_resident_experts(ActivationMap(counts), strategy.exp_r))
+    L = int(phase.seq_len)
+    B = int(batch.batch_size)
+    m = B if coalesced else int(strategy.m)
+    sizes = [min(m, B - s0) for s0 in range(0, B, m)]
+    mig = gpu = 0.0
+    for nseq in sorted(set(sizes)):
+        x = make_tokens(nseq * L, d, seed=1, device=dev)
+        for _ in range(warmup):
+            stack(x, fetch="stream")
+        stack(x, timeline=True, fetch="stream")
+        parts = stack.measured_parts()
+        reps = sizes.count(nseq)
+        mig += reps * parts.mig_load
+        gpu += reps * parts.lat_gpu
+        del x
+    stack._bufs = None
+    return ExpertStageParts(act_load=0.0, mig_load=mig, lat_gpu=gpu, lat_cpu=0.0, return_store=0.0)
+
+
 def make_pool(P: int, d: int, ff: int, seed: int = 0, device="cuda", residual_scale: float = 1.0) -> HostExpertPool:
     """P distinct random experts generated on the device, copied to pinned host memory.
 
@@ -328,4 +456,5 @@ def hit_ratio_of_counts(counts: np.ndarray, plan: ResidencyPlan) -> float:
     return hit_ratio_from_counts(counts, plan)
 
 
-__all__ = ["StratifiedMoEStack", "make_pool", "make_router_weights", "HostExpertPool", "hit_ratio_of_counts"]
+__all__ = ["StratifiedMoEStack", "make_pool", "make_router_weights", "HostExpertPool", "hit_ratio_of_counts",
+           "measured_expert_stage_parts"]

@@ -151,3 +151,83 @@ def make_tie_batch(T: int, d: int, E: int, seed: int = 3, device="cuda", tie_fra
     mirrored = xs[:, :, :4].flip(-1)                            # exact symmetry in bf16: q -> 7 - q
     xs[:, :, 4:] = torch.where(tie[:, None, None], mirrored, xs[:, :, 4:])
     return xs.reshape(T, d), wg, torch.where(tie, pair, torch.full_like(pair, -1))
+
+
+@dataclass
+class TopicWorkload:
+    """Topic-structured routing for a deep MoE stack (the GPU counterpart of
+    eas.generate_synthetic_trace, eas.py:180-240): every sequence belongs to
+    one of K latent topics (topic sizes skewed ~ 1/rank), its tokens carry the
+    topic's unit direction u_topic (x = noise + amp * u_topic; the residual
+    stream keeps it from layer to layer), and each layer's router rows hold a
+    per-(topic, layer) Zipf preference over a random expert permutation:
+    wg_l[e] = base_l[e] + sum_topic beta * log(E * pref[topic, l, e]) * u_topic / amp,
+    so a topic's tokens prefer that topic's hot experts in every layer.
+    Calibrating on prototype sequences (eas.cluster / select_prototypes on
+    sequence embeddings) therefore predicts which experts are hot."""
+    dirs: torch.Tensor          # [K, d] fp32 unit vectors
+    topic_weights: list         # [K] sampling probabilities
+    amp: float
+
+    @property
+    def num_topics(self) -> int:
+        return self.dirs.shape[0]
+
+
+def make_topic_workload(d: int, num_topics: int = 8, amp: float = 8.0, seed: int = 31, device="cuda") -> TopicWorkload:
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+    u = torch.empty((num_topics, d), dtype=torch.float32, device=device)
+    u.normal_(0.0, 1.0, generator=g)
+    u /= u.norm(dim=1, keepdim=True)
+    w = [1.0 / (i + 1) for i in range(num_topics)]
+    s = sum(w)
+    return TopicWorkload(dirs=u, topic_weights=[v / s for v in w], amp=amp)
+
+
+def make_topic_router(N: int, E: int, d: int, wl: TopicWorkload, zipf: float = 1.2, beta: float = 1.0,
+                      seed: int = 7, device="cuda") -> torch.Tensor:
+    """Router weights [N, E, d] fp32 (bf16-exact values) with the topic preferences."""
+    import numpy as np
+    rng = np.random.default_rng(seed)
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+    wg = torch.empty((N, E, d), dtype=torch.float32, device=device)
+    wg.uniform_(-d ** -0.5, d ** -0.5, generator=g)
+    rank_w = 1.0 / np.arange(1, E + 1, dtype=float) ** zipf
+    rank_w /= rank_w.sum()
+    K = wl.num_topics
+    bias = np.empty((K, N, E))
+    for t in range(K):
+        for layer in range(N):
+            pref = np.empty(E)
+            pref[rng.permutation(E)] = rank_w
+            bias[t, layer] = beta * np.log(E * pref)
+    b = torch.from_numpy(bias).to(device=device, dtype=torch.float32)       # [K, N, E]
+    wg += torch.einsum("kne,kd->ned", b, wl.dirs) / wl.amp
+    return wg.to(torch.bfloat16).float()
+
+
+def make_topic_tokens(wl: TopicWorkload, n_seq: int, seq_len: int, seed: int, device="cuda"):
+    """x [n_seq * seq_len, d] bf16 (sequence-major) and the topic of every sequence."""
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+    w = torch.tensor(wl.topic_weights, device=device)
+    topics = torch.multinomial(w, n_seq, replacement=True, generator=g)
+    d = wl.dirs.shape[1]
+    x = torch.empty((n_seq, seq_len, d), dtype=torch.float32, device=device)
+    x.normal_(0.0, 1.0, generator=g)
+    x += wl.amp * wl.dirs[topics][:, None, :]
+    return x.reshape(n_seq * seq_len, d).to(torch.bfloat16), topics
+
+
+def sequence_embeddings(x: torch.Tensor, n_seq: int, proj_dim: int = 32, seed: int = 5):
+    """Per-sequence embedding for prototype clustering: the mean token, randomly
+    projected to proj_dim dims (numpy float64 [n_seq, proj_dim])."""
+    d = x.shape[1]
+    g = torch.Generator(device=x.device)
+    g.manual_seed(seed)
+    P = torch.empty((d, proj_dim), dtype=torch.float32, device=x.device)
+    P.normal_(0.0, d ** -0.5, generator=g)
+    m = x.float().reshape(n_seq, -1, d).mean(dim=1)
+    return (m @ P).double().cpu().numpy()

@@ -24,6 +24,7 @@ from moeplan import configio, eas  # noqa: E402
 from moeplan.costmodel import AllocationStrategy, expert_stage_parts, vram_usage  # noqa: E402
 from moeplan.hardware import Device, DeviceSpec, LinkSpec, SystemSpec  # noqa: E402
 from moeplan.planner import PlanRequest, sweep_microbatch  # noqa: E402
+from moeplan.planner import plan as planner_plan  # noqa: E402
 from moeplan.workload import BatchConfig, ModelConfig, Phase, PhaseKind  # noqa: E402
 
 OUT = Path(__file__).resolve().parent / "reference_golden.json"
@@ -119,7 +120,21 @@ def main():
               "assignments": pcl.assignments.tolist(), "centroids": pcl.centroids.tolist(),
               "inertia": list(pcl.iteration_inertia), "prototypes": eas.select_prototypes(pcl, 0.04, 11)}
 
-    OUT.write_text(json.dumps({"prototypes": protos, "systems": {k: sysd(v) for k, v in systems.items()},
+    # planner.plan on this repo's B200 system triple (configs/system_b200.yaml, the reference's YAML schema)
+    repo = Path(__file__).resolve().parents[2]
+    bsys = configio.load_system_spec(repo / "paper_2605_17889_b200" / "configs" / "system_b200.yaml")
+    c3 = ModelConfig(56, 6144, 16384, 8, 2, 2)
+    c3b = BatchConfig(64, 4096, 16)
+    pl = planner_plan(PlanRequest(system=bsys, model=c3, batch=c3b))
+
+    def strat(st):
+        return {"placement": [p.value for p in st.placement], "exp_r": st.exp_r, "exp_m": st.exp_m,
+                "exp_c": st.exp_c, "m": st.m}
+    plan_c3 = {"system": sysd(bsys), "model": [56, 6144, 16384, 8, 2, 2], "batch": [64, 4096, 16],
+               "prefill": strat(pl.prefill_strategy), "decode": strat(pl.decode_strategy),
+               "vram_prefill_resident_bytes": pl.vram_prefill.resident_expert_bytes}
+
+    OUT.write_text(json.dumps({"plan_c3_b200": plan_c3, "prototypes": protos, "systems": {k: sysd(v) for k, v in systems.items()},
                                "models": {k: [v.num_layers, v.hidden_dim, v.expert_dim, v.experts_per_layer, v.top_k,
                                               v.dtype_bytes] for k, v in models.items()},
                                "batches": {k: [v.batch_size, v.input_len, v.output_len] for k, v in batches.items()},

@@ -83,3 +83,65 @@ def test_apply_strategy_from_orchestrator():
     assert torch.equal(ref, out)
     with pytest.raises(ValueError):
         stack.apply_strategy(AllocationStrategy((Device.GPU,) * 3, exp_r=4, exp_m=2, exp_c=2, m=4))
+
+
+def test_touched_fetch_matches_stream_and_skips_untouched():
+    """fetch="touched" (cox_fetch_experts after each router) gives the same bits
+    as fetch="stream" and copies no bytes for cold experts the router left
+    untouched: expert 7's router row is pushed far down, so it never wins."""
+    pool = make_pool(P, d, ff, seed=0, device=DEV)
+    wg = make_router_weights(N, E, d, seed=7, device=DEV)
+    wg[:, 7] = -wg[:, 7].abs() - 0.5
+    wg = wg.to(torch.bfloat16).float()
+    plan = ResidencyPlan(tuple((0, 1, 2) for _ in range(N)), 3)
+    stack = StratifiedMoEStack(N, wg, pool, k, plan, "mixtral")
+    x = make_tokens(300, d, seed=4, device=DEV)
+    a = stack(x, fetch="stream").clone()
+    counts = torch.zeros((N, E), dtype=torch.int32, device=DEV)
+    b = stack(x, fetch="touched", counts_out=counts).clone()
+    torch.cuda.synchronize()
+    assert torch.equal(a, b)
+    assert int(counts[:, 7].sum()) == 0
+    fetched = stack._fetched.cpu().numpy()
+    for l in range(N):
+        for j, e in enumerate(stack.cold[l]):
+            want = 1 if int(counts[l, e]) > 0 else 0
+            assert fetched[l, 2 * j] == want and fetched[l, 2 * j + 1] == want, (l, e)
+    assert stack.fetched_cold_experts() < len(stack.cold[0])
+
+
+def test_golden_c3_plan_runs_and_measured_parts():
+    """The plan moeplan.planner.plan makes for C3 on configs/system_b200.yaml
+    (committed golden, tests/test_reference_interop.py) drives a C3-shaped
+    stack (3 layers), and measured_expert_stage_parts (costmodel.py:225-233's
+    signature) returns hardware-measured parts next to the analytical row."""
+    import json
+    from pathlib import Path
+    from paper_2605_17889_b200 import costmodel as CM
+    from paper_2605_17889_b200.config import AllocationStrategy, BatchConfig, Device, ModelConfig, Phase
+    from paper_2605_17889_b200.executor import measured_expert_stage_parts
+    g = json.loads((Path(__file__).resolve().parent / "golden" / "reference_golden.json").read_text())["plan_c3_b200"]
+    pf = g["prefill"]
+    strat = AllocationStrategy(tuple(Device(p) for p in pf["placement"]), pf["exp_r"], pf["exp_m"], pf["exp_c"],
+                               m=pf["m"])
+    Nl, dd, fff = 3, 6144, 16384
+    pool = make_pool(8, dd, fff, seed=0, device=DEV, residual_scale=(2.0 * Nl) ** -0.5)
+    st = StratifiedMoEStack(Nl, make_router_weights(Nl, E, dd, seed=7, device=DEV), pool, k,
+                            ResidencyPlan(tuple(() for _ in range(Nl)), 0), "mixtral", pool_map=lambda l, e: e)
+    plan = st.apply_strategy(strat)
+    assert all(len(r) == pf["exp_r"] for r in plan.resident) and all(len(c) == pf["exp_m"] for c in st.cold)
+    out = st(make_tokens(8192, dd, seed=5, device=DEV), fetch="stream")
+    torch.cuda.synchronize()
+    assert torch.isfinite(out.float()).all()
+    del st, pool
+    torch.cuda.empty_cache()
+    model = ModelConfig(56, dd, fff, 8, 2, 2)
+    batch = BatchConfig(2, 4096, 0)
+    ph = Phase.prefill(4096)
+    meas = measured_expert_stage_parts(strat, ph, CM.load_system_spec(CM.B200_SYSTEM_YAML), model, batch)
+    ana = CM.expert_stage_parts(strat, ph, CM.load_system_spec(CM.B200_SYSTEM_YAML), model, batch,
+                                count_top_k=True)
+    assert meas.act_load == 0.0 and meas.lat_cpu == 0.0 and meas.return_store == 0.0
+    # 4 cold experts x 604 MB over PCIe; the analytical row charges the same bytes at 55 GB/s
+    assert 0.5 < meas.mig_load / ana.mig_load < 2.0, (meas, ana)
+    assert 0.2 < meas.lat_gpu / ana.lat_gpu < 5.0, (meas, ana)

@@ -130,3 +130,14 @@ def test_capacity_per_layer():
     assert CM.capacity_per_layer(model, 4 * per * 56 - 1) == 3
     assert CM.capacity_per_layer(model, 0) == 0
     assert CM.capacity_per_layer(model, 1e15) == 8
+
+
+def test_b200_system_yaml_loads():
+    """configs/system_b200.yaml parses into the reference's SystemSpec shape
+    (the same YAML is read by moeplan.configio in tests/test_reference_interop.py)."""
+    s = CM.load_system_spec(CM.B200_SYSTEM_YAML)
+    assert s.gpu.mem_bandwidth == 6.4528e12 and s.gpu.peak_compute == 1430.7e12
+    assert s.link.bandwidth == 55e9 and s.link.duplex and s.link.efficiency == 1.0
+    g = GOLD["plan_c3_b200"]["system"]
+    assert [s.gpu.mem_bandwidth, s.gpu.peak_compute, s.gpu.mem_capacity] == g["gpu"]
+    assert [s.cpu.mem_bandwidth, s.cpu.peak_compute, s.cpu.mem_capacity] == g["cpu"]

@@ -58,3 +58,30 @@ def test_planner_plan_drives_residency(moeplan):
     for layer, res in enumerate(ours.resident):
         order = np.argsort(-amap.counts[layer], kind="stable")[: s.exp_r]
         assert set(res) == set(int(e) for e in order)
+
+
+def test_b200_system_yaml_replans_c3(moeplan):
+    """configs/system_b200.yaml (the reference's YAML schema, measured B200
+    numbers) is read identically by moeplan.configio and by costmodel.
+    load_system_spec, and moeplan.planner.plan on it reproduces the committed
+    C3 plan that tests/test_gpu_stack.py runs on the GPU."""
+    import json
+    from pathlib import Path
+    from moeplan import configio
+    from moeplan.planner import PlanRequest, plan
+    from moeplan.workload import BatchConfig, ModelConfig
+    ref = configio.load_system_spec(CM.B200_SYSTEM_YAML)
+    ours = CM.load_system_spec(CM.B200_SYSTEM_YAML)
+    for a, b in ((ref.gpu, ours.gpu), (ref.cpu, ours.cpu)):
+        assert (a.mem_bandwidth, a.peak_compute, a.mem_capacity) == (b.mem_bandwidth, b.peak_compute, b.mem_capacity)
+    assert (ref.link.bandwidth, ref.link.duplex, ref.link.efficiency) == \
+           (ours.link.bandwidth, ours.link.duplex, ours.link.efficiency)
+    g = json.loads((Path(__file__).resolve().parent / "golden" / "reference_golden.json").read_text())["plan_c3_b200"]
+    p = plan(PlanRequest(system=ref, model=ModelConfig(*g["model"]), batch=BatchConfig(*g["batch"])))
+    for ph, st in (("prefill", p.prefill_strategy), ("decode", p.decode_strategy)):
+        assert [x.value for x in st.placement] == g[ph]["placement"]
+        assert (st.exp_r, st.exp_m, st.exp_c, st.m) == (g[ph]["exp_r"], g[ph]["exp_m"], g[ph]["exp_c"], g[ph]["m"])
+    # the prefill partition runs on the B200 executor (no CPU experts); the
+    # decode partition's CPU experts are replaced by device-side touched-only
+    # fetches (executor.StratifiedMoEStack, fetch="touched"; DESIGN.md)
+    assert g["prefill"]["exp_c"] == 0
