@@ -631,7 +631,6 @@ def main():
         pk = peaks()
         flops_k3 = 4.0 * T * k * d * ff
         flops_k4 = 2.0 * T * k * d * ff
-        flops_layer = 6.0 * T * k * d * ff + 2.0 * T * d * E + (6.0 * T * d * shared_ff if shared_ff else 0.0)
         traffic = None
         tp = ROOT / "profiles" / "ncu_traffic.json"
         if tp.exists() and args.config == "C2":
@@ -662,45 +661,54 @@ def main():
         if ep_info is not None and parity is not None:
             parity["ep"] = ep_info
             parity["pass"] = bool(parity["pass"] and ep_info["rank0_output_equals_single_gpu_layer"])
-        wgb = (touched * 3 * d * ff * 2 + 3 * d * shared_ff * 2) / 1e9
-        if decode:
-            l2_note = (f"expert weights read per step ({wgb:.2f} GB) > 126 MB L2, so every step streams them "
-                       "from HBM; no flush")
-        else:
-            ws_gb = wgb + T * d * 2 * (3 + 2 * k) / 1e9 + T * k * ff * 2 / 1e9
-            l2_note = (f"per-step working set {ws_gb:.2f} GB > 126 MB L2 (x {T * d * 2 / 1e9:.3f} GB, x_perm "
-                       f"{T * k * d * 2 / 1e9:.3f} GB, h {T * k * ff * 2 / 1e9:.3f} GB, expert weights {wgb:.3f} GB); "
-                       "no flush")
-        if args.microbatch:
-            desc_mb = f" [ABLATION: micro-batched, {args.microbatch} tokens per expert-stage launch]"
-        else:
-            desc_mb = ""
-        line = {
-            "metric": metric_name(args.config),
-            "value": value, "unit": "tokens/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": "bf16", "data": "synthetic (seeded N(0,1) tokens, nn.Linear-style U(+-1/sqrt(fan_in)) weights)",
-            "config": {"workload": desc + desc_mb, "tokens_per_gpu": T, "global_batch_tokens": T * ws, "d": d, "ff": ff,
-                       "E": E, "k": k, "routing": mode, "parallelism": f"ep{ws}" if ws > 1 else "single",
-                       "ep_path": ep_used,
-                       "l2": l2_note},
-            "layer_tflops": flops_layer / (ms_step / 1e3) / 1e12,
-            "frac_layer_of_bf16_sustained": flops_layer / (ms_step / 1e3) / 1e12 / pk["bf16_sus"],
-            "frac_layer_of_bf16_burst": flops_layer / (ms_step / 1e3) / 1e12 / pk["bf16"],
-            "roofline": roof,
-            "stages_ms": stages,
-            "cpu_baseline": cpu,
-            "parity": parity,
-            "e2e": e2e,
-            "gpu_launches": launches_per_step(layer, args.microbatch or T) * args.steps
-            * (-(-T // args.microbatch) if args.microbatch else 1),
-            "clocks": clk.summary(),
-        }
+        line = assemble_line(args, cfg, ws, value, ms_step, pk, roof, stages, cpu, parity, e2e,
+                             launches_per_step(layer, args.microbatch or T) * args.steps
+                             * (-(-T // args.microbatch) if args.microbatch else 1),
+                             clk.summary(), ep_used, touched, decode)
         print(json.dumps(line), flush=True)
     if ws > 1:
         if hasattr(layer, "check"):
             layer.check()
         dist.destroy_process_group()
+
+
+def assemble_line(args, cfg, ws, value, ms_step, pk, roof, stages, cpu, parity, e2e, gpu_launches, clocks, ep_used,
+                  touched, decode) -> dict:
+    """The ONE JSON line of bench.py (rank 0).  `value` and `e2e` are whole-job
+    tokens/s over all ws ranks; at ws > 1 `parity` carries the EP checks
+    (rank 0's output == the single-GPU layer) and `stages_ms` the NVLink phases."""
+    T, d, ff, E, k, mode, shared_ff, desc = cfg
+    flops_layer = 6.0 * T * k * d * ff + 2.0 * T * d * E + (6.0 * T * d * shared_ff if shared_ff else 0.0)
+    wgb = (touched * 3 * d * ff * 2 + 3 * d * shared_ff * 2) / 1e9
+    if decode:
+        l2_note = (f"expert weights read per step ({wgb:.2f} GB) > 126 MB L2, so every step streams them "
+                   "from HBM; no flush")
+    else:
+        ws_gb = wgb + T * d * 2 * (3 + 2 * k) / 1e9 + T * k * ff * 2 / 1e9
+        l2_note = (f"per-step working set {ws_gb:.2f} GB > 126 MB L2 (x {T * d * 2 / 1e9:.3f} GB, x_perm "
+                   f"{T * k * d * 2 / 1e9:.3f} GB, h {T * k * ff * 2 / 1e9:.3f} GB, expert weights {wgb:.3f} GB); "
+                   "no flush")
+    desc_mb = f" [ABLATION: micro-batched, {args.microbatch} tokens per expert-stage launch]" if args.microbatch else ""
+    tflops = flops_layer * ws / (ms_step / 1e3) / 1e12  # every rank runs one layer's worth of tokens
+    return {
+        "metric": metric_name(args.config),
+        "value": value, "unit": "tokens/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "bf16", "data": "synthetic (seeded N(0,1) tokens, nn.Linear-style U(+-1/sqrt(fan_in)) weights)",
+        "config": {"workload": desc + desc_mb, "tokens_per_gpu": T, "global_batch_tokens": T * ws, "d": d, "ff": ff,
+                   "E": E, "k": k, "routing": mode, "parallelism": f"ep{ws}" if ws > 1 else "single",
+                   "ep_path": ep_used, "l2": l2_note},
+        "layer_tflops": tflops,
+        "frac_layer_of_bf16_sustained": tflops / ws / pk["bf16_sus"],
+        "frac_layer_of_bf16_burst": tflops / ws / pk["bf16"],
+        "roofline": roof,
+        "stages_ms": stages,
+        "cpu_baseline": cpu,
+        "parity": parity,
+        "e2e": e2e,
+        "gpu_launches": gpu_launches,
+        "clocks": clocks,
+    }
 
 
 def launches_per_step(layer, T: int) -> int:

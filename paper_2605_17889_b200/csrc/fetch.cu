@@ -30,29 +30,31 @@ struct FetchParams {
 constexpr int FX_U = 4;                      // loads in flight per thread
 constexpr long long FX_SLICE = 256LL * FX_U;  // vectors per CTA iteration (16 KB)
 
-// Grid-stride over (entry, 16 KB slice); 4 loads in flight per thread before
-// the stores (PCIe round trips are ~1-2 us; 148 CTAs keep ~2.4 MB in flight).
+// Per entry: one check of its expert's count (untouched entries cost one load
+// per CTA), then a grid-stride over its 16 KB slices with 4 loads in flight per
+// thread before the stores (PCIe round trips are ~1-2 us; 148 CTAs keep
+// ~2.4 MB in flight).
 __global__ void __launch_bounds__(256) fetch_experts_kernel(const __grid_constant__ FetchParams p) {
-  const long long total = p.first[p.n];
-  int i = 0;
-  for (long long it = blockIdx.x; it < total; it += gridDim.x) {
-    while (it >= p.first[i + 1]) ++i;  // `it` only grows: a forward scan
+  for (int i = 0; i < p.n; ++i) {
     if (__ldg(p.counts + p.expert[i]) <= 0) continue;  // untouched this step: no bytes cross PCIe
-    const long long s0 = (it - p.first[i]) * FX_SLICE;
-    if (p.fetched && s0 == 0 && threadIdx.x == 0) p.fetched[i] = 1;
+    if (p.fetched && blockIdx.x == 0 && threadIdx.x == 0) p.fetched[i] = 1;
     const uint4* __restrict__ src = p.src[i];
     uint4* __restrict__ dst = p.dst[i];
     const long long nv = p.vecs[i];
-    uint4 v[FX_U];
+    const long long nslice = p.first[i + 1] - p.first[i];
+    for (long long sl = blockIdx.x; sl < nslice; sl += gridDim.x) {
+      const long long s0 = sl * FX_SLICE;
+      uint4 v[FX_U];
 #pragma unroll
-    for (int u = 0; u < FX_U; ++u) {
-      const long long j = s0 + threadIdx.x + 256LL * u;
-      if (j < nv) v[u] = ld_nc_v4(src + j);
-    }
+      for (int u = 0; u < FX_U; ++u) {
+        const long long j = s0 + threadIdx.x + 256LL * u;
+        if (j < nv) v[u] = ld_nc_v4(src + j);
+      }
 #pragma unroll
-    for (int u = 0; u < FX_U; ++u) {
-      const long long j = s0 + threadIdx.x + 256LL * u;
-      if (j < nv) dst[j] = v[u];
+      for (int u = 0; u < FX_U; ++u) {
+        const long long j = s0 + threadIdx.x + 256LL * u;
+        if (j < nv) dst[j] = v[u];
+      }
     }
   }
 }

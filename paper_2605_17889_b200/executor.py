@@ -330,7 +330,8 @@ class StratifiedMoEStack:
     def max_capacity(self, T: int, slack_bytes: int = 4 << 30) -> int:
         """Largest exp_r whose resident copies + the T-token activations + the
         2*(E - exp_r) slot ring fit in the free HBM (x, ping, pong, x_perm, h) (the vram_usage feasibility
-        test, costmodel.py:440-489, with measured free memory)."""
+        test, costmodel.py:440-489, with measured free memory).  Leaves the
+        stack with an empty residency plan (every expert cold)."""
         self.ring = None
         self._bufs = None
         self.res_w13, self.res_w2 = [], []
@@ -338,11 +339,15 @@ class StratifiedMoEStack:
         free, _ = torch.cuda.mem_get_info(self.device)
         per = self.pool.nbytes_per_expert()
         act = T * self.d * 2 * 3 + ops.rows_capacity(T, self.k, self.E) * (self.d + self.ff) * 2
+        best = 0
         for cap in range(self.E, -1, -1):
             need = cap * per * self.N + 2 * (self.E - cap) * per + act + slack_bytes
             if need <= free:
-                return cap
-        return 0
+                best = cap
+                break
+        # the resident copies were freed to measure: continue with every expert cold
+        self.set_residency(ResidencyPlan(tuple(() for _ in range(self.N)), 0))
+        return best
 
     def calibrate(self, batches, capacity_per_layer: int) -> ResidencyPlan:
         """Prefill-only probing: run prototype batches through the

@@ -88,26 +88,28 @@ def test_apply_strategy_from_orchestrator():
 def test_touched_fetch_matches_stream_and_skips_untouched():
     """fetch="touched" (cox_fetch_experts after each router) gives the same bits
     as fetch="stream" and copies no bytes for cold experts the router left
-    untouched: expert 7's router row is pushed far down, so it never wins."""
+    untouched (3 tokens x top-2: at most 6 of 8 experts touched per layer)."""
     pool = make_pool(P, d, ff, seed=0, device=DEV)
     wg = make_router_weights(N, E, d, seed=7, device=DEV)
-    wg[:, 7] = -wg[:, 7].abs() - 0.5
-    wg = wg.to(torch.bfloat16).float()
     plan = ResidencyPlan(tuple((0, 1, 2) for _ in range(N)), 3)
     stack = StratifiedMoEStack(N, wg, pool, k, plan, "mixtral")
-    x = make_tokens(300, d, seed=4, device=DEV)
-    a = stack(x, fetch="stream").clone()
-    counts = torch.zeros((N, E), dtype=torch.int32, device=DEV)
-    b = stack(x, fetch="touched", counts_out=counts).clone()
-    torch.cuda.synchronize()
-    assert torch.equal(a, b)
-    assert int(counts[:, 7].sum()) == 0
-    fetched = stack._fetched.cpu().numpy()
-    for l in range(N):
-        for j, e in enumerate(stack.cold[l]):
-            want = 1 if int(counts[l, e]) > 0 else 0
-            assert fetched[l, 2 * j] == want and fetched[l, 2 * j + 1] == want, (l, e)
-    assert stack.fetched_cold_experts() < len(stack.cold[0])
+    for T in (3, 300):
+        x = make_tokens(T, d, seed=4, device=DEV)
+        a = stack(x, fetch="stream").clone()
+        counts = torch.zeros((N, E), dtype=torch.int32, device=DEV)
+        b = stack(x, fetch="touched", counts_out=counts).clone()
+        torch.cuda.synchronize()
+        assert torch.equal(a, b)
+        fetched = stack._fetched.cpu().numpy()
+        c = counts.cpu().numpy()
+        untouched = 0
+        for l in range(N):
+            for j, e in enumerate(stack.cold[l]):
+                want = 1 if c[l, e] > 0 else 0
+                untouched += 1 - want
+                assert fetched[l, 2 * j] == want and fetched[l, 2 * j + 1] == want, (l, e)
+        if T == 3:
+            assert untouched > 0 and stack.fetched_cold_experts() < len(stack.cold[0])
 
 
 def test_golden_c3_plan_runs_and_measured_parts():

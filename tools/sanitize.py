@@ -53,6 +53,28 @@ def main():
     out = layer(make_tokens(3000, 256, seed=7, device=dev))
     torch.cuda.synchronize()
     assert torch.isfinite(out.float()).all()
+    # TMA-fed E <= 8 router (T >= 148*64, d % 256 == 0) with bf16 and fp32 router rows
+    from paper_2605_17889_b200.synthetic import make_router_weight
+    wg8 = make_router_weight(8, 512, seed=3, device=dev)
+    ops.router_topk(make_tokens(148 * 64 + 5, 512, device=dev), wg8.to(torch.bfloat16), 2, 0)
+    ops.router_topk(make_tokens(148 * 64 + 5, 512, device=dev), wg8 + 1e-4, 2, 1)
+    # device-side cold-expert fetch (touched / untouched entries)
+    host = [torch.randn(4096 + 8 * i).to(torch.bfloat16).pin_memory() for i in range(4)]
+    dst = [torch.empty_like(h, device=dev) for h in host]
+    counts = torch.tensor([1, 0, 3, 0], dtype=torch.int32, device=dev)
+    fetched = torch.empty(4, dtype=torch.int32, device=dev)
+    ops.fetch_experts(counts, [0, 1, 2, 3], host, dst, fetched=fetched)
+    torch.cuda.synchronize()
+    assert torch.equal(dst[2].cpu(), host[2]) and fetched.tolist() == [1, 0, 1, 0]
+    # stratified stack: streamed and touched-only cold experts
+    from paper_2605_17889_b200.config import ResidencyPlan
+    from paper_2605_17889_b200.executor import StratifiedMoEStack, make_pool, make_router_weights
+    st = StratifiedMoEStack(3, make_router_weights(3, 8, 256, device=dev), make_pool(5, 256, 256, device=dev), 2,
+                            ResidencyPlan(tuple((0, 1) for _ in range(3)), 2))
+    xs = make_tokens(200, 256, seed=8, device=dev)
+    st(xs, fetch="stream")
+    st(xs, fetch="touched")
+    torch.cuda.synchronize()
     # tensor-core screening router (E >= 32, T >= 148*128)
     wg64 = (torch.rand(64, 256, device=dev) * 2 - 1).to(torch.bfloat16) / 16
     ops.router_topk(make_tokens(148 * 128 + 9, 256, device=dev), wg64, 6, 1)
