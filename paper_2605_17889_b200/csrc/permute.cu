@@ -7,9 +7,12 @@
 // ascending token order; segments are padded to a multiple of tile_m rows
 // (padding rows are zero-filled).  No atomics decide placement:
 //   1. perm_hist    — per-block (256 tokens) expert histogram (smem atomics on
-//                     integers: order-independent result);
-//   2. perm_scan    — per-expert exclusive scan over blocks (one warp per
-//                     expert, shuffle scan) and the padded segment offsets;
+//                     integers: order-independent result), stored expert-major
+//                     ([E][nb]) so each expert's block counts are contiguous;
+//   2. perm_scan    — per-expert exclusive scan over blocks: one warp per
+//                     expert walks its row 32 blocks at a time (coalesced
+//                     loads, shuffle scan, carried running sum), then the
+//                     padded segment offsets;
 //   3. perm_scatter — in-block ranks from warp ballots (lane = token, so
 //                     popc(ballot & lanemask_lt) is the ascending-token rank);
 //   4. perm_copy    — grid-wide, one warp per token: each row is read ONCE
@@ -32,32 +35,43 @@ __global__ void __launch_bounds__(PM_TB) perm_hist(const int32_t* __restrict__ i
       if ((unsigned)e < (unsigned)E) atomicAdd(&s_h[e], 1);  // invalid ids are dropped (dst = -1)
     }
   __syncthreads();
-  for (int i = threadIdx.x; i < E; i += blockDim.x) block_counts[(long)blockIdx.x * E + i] = s_h[i];
+  for (int i = threadIdx.x; i < E; i += blockDim.x) block_counts[(long)i * gridDim.x + blockIdx.x] = s_h[i];
 }
 
-// One block of 1024 threads; warp w scans experts w, w+32, ...
+// One block of 1024 threads; warp w scans experts w, w+32, ... over their
+// contiguous [nb] rows of block counts (expert-major), 32 blocks per step with
+// every step's loads issued before the carried scans.
 __global__ void __launch_bounds__(1024) perm_scan(const int32_t* __restrict__ block_counts, int nb, int E, int tile_m,
                                                   int32_t* __restrict__ block_base, int32_t* __restrict__ offsets,
                                                   int32_t* __restrict__ seg_counts) {
   __shared__ int s_tot[1024];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int per = (nb + 31) / 32;
+  constexpr int U = 8;  // 32-block steps whose loads are in flight together
   for (int e = warp; e < E; e += 32) {
-    const int b0 = lane * per, b1 = min(nb, b0 + per);
-    int local = 0;
-    for (int b = b0; b < b1; ++b) local += block_counts[(long)b * E + e];
-    int incl = local;
+    const int32_t* row = block_counts + (long)e * nb;
+    int32_t* base = block_base + (long)e * nb;
+    int carry = 0;
+    for (int b0 = 0; b0 < nb; b0 += 32 * U) {
+      int v[U];
 #pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-      int v = __shfl_up_sync(0xffffffffu, incl, off);
-      if (lane >= off) incl += v;
+      for (int u = 0; u < U; ++u) {
+        const int b = b0 + 32 * u + lane;
+        v[u] = b < nb ? row[b] : 0;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        int incl = v[u];
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+          const int y = __shfl_up_sync(0xffffffffu, incl, off);
+          if (lane >= off) incl += y;
+        }
+        const int b = b0 + 32 * u + lane;
+        if (b < nb) base[b] = carry + incl - v[u];
+        carry += __shfl_sync(0xffffffffu, incl, 31);
+      }
     }
-    int run = incl - local;
-    for (int b = b0; b < b1; ++b) {
-      block_base[(long)b * E + e] = run;
-      run += block_counts[(long)b * E + e];
-    }
-    if (lane == 31) s_tot[e] = incl;
+    if (lane == 0) s_tot[e] = carry;
   }
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -101,7 +115,7 @@ __global__ void __launch_bounds__(PM_TB) perm_scatter(const int32_t* __restrict_
   }
   __syncthreads();
   for (int e = threadIdx.x; e < E; e += blockDim.x) {
-    int run = offsets[e] + block_base[(long)blockIdx.x * E + e];
+    int run = offsets[e] + block_base[(long)e * gridDim.x + blockIdx.x];
     for (int w = 0; w < PM_TB / 32; ++w) {
       s_wbase[w][e] = run;
       run += s_wcnt[w][e];
