@@ -76,9 +76,12 @@ struct TileCoord {
   int g, m, n;
 };
 
-COX_DEV TileCoord decode_tile(int t, const int* s_prefix, const int* s_rows, int band) {
+// g: the caller's group cursor.  Every role sees increasing tile ids (first
+// wave static, then an atomic counter), so the group search resumes where the
+// previous tile's ended instead of scanning from group 0 (C4: 64 groups, a
+// serial smem scan of ~32 steps per tile delayed the producer's TMA issue).
+COX_DEV TileCoord decode_tile(int t, const int* s_prefix, const int* s_rows, int band, int& g) {
   TileCoord c;
-  int g = 0;
   while (t >= s_prefix[g + 1]) ++g;
   const int local = t - s_prefix[g];
   const int mt = (s_rows[g] + 2 * GM_BM - 1) / (2 * GM_BM);
@@ -259,10 +262,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GM_THREADS, 1)
       l2_policies(p.l2_mode, pol_a, pol_b);
       const bool hint = p.l2_mode != 0;
       uint32_t stage = 0, phase = 0;
-      int si = 0;
+      int si = 0, gcur = 0;
       int t = fetch_tile(si, true);
       while (t < total) {
-        const TileCoord c = decode_tile(t, s_prefix, s_rows, p.band);
+        const TileCoord c = decode_tile(t, s_prefix, s_rows, p.band, gcur);
         const int a_row = s_row0[c.g] + c.m * 2 * GM_BM + (int)rank * GM_BM;
         const int b_row = c.n * GM_BN + (int)rank * (GM_BN / 2);
         const CUtensorMap* bmap = &p.b_map[c.g];
@@ -332,11 +335,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GM_THREADS, 1)
     const uint32_t tempty_leader0 = mapa(smem_u32(&tempty[0]), 0);
     const uint32_t tempty_leader1 = mapa(smem_u32(&tempty[1]), 0);
     __nv_bfloat16* out = static_cast<__nv_bfloat16*>(p.out);
-    int si = 0;
+    int si = 0, gcur = 0;
     for (int it = 0;; ++it) {
       const int t = fetch_tile(si, lane == 0);
       if (t >= total) break;
-      const TileCoord c = decode_tile(t, s_prefix, s_rows, p.band);
+      const TileCoord c = decode_tile(t, s_prefix, s_rows, p.band, gcur);
       const int acc = it & 1;
       const uint32_t acc_phase = (it >> 1) & 1;
       mbar_wait(smem_u32(&tfull[acc]), acc_phase);

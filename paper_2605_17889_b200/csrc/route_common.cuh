@@ -11,6 +11,19 @@
 
 namespace cox {
 
+// Recursive-halving step: lane keeps the half of `v` selected by (lane & off)
+// and adds the partner's copy of the same logits.
+template <int N>
+COX_DEV void rs_step(float (&v)[2 * N], float (&o)[N], int lane, int off) {
+  const bool upper = (lane & off) != 0;
+#pragma unroll
+  for (int m = 0; m < N; ++m) {
+    const float keep = upper ? v[N + m] : v[m];
+    const float send = upper ? v[m] : v[N + m];
+    o[m] = __fadd_rn(keep, __shfl_xor_sync(0xffffffffu, send, off));
+  }
+}
+
 // lg: the token's E logits in shared memory (overwritten with the exp terms in
 // mode 1); s_sel / s_selv: this warp's [8] shared scratch; idx / w: the
 // token's k outputs; hist: optional shared/global histogram (+1 per selected

@@ -29,6 +29,7 @@
 #include <cuda.h>
 
 #include "common.cuh"
+#include "route_common.cuh"
 
 namespace cox {
 
@@ -70,19 +71,6 @@ struct WRow<float> {
     f[0] = a.x; f[1] = a.y; f[2] = a.z; f[3] = a.w; f[4] = b.x; f[5] = b.y; f[6] = b.z; f[7] = b.w;
   }
 };
-
-// Recursive-halving step: lane keeps the half of `v` selected by (lane & off)
-// and adds the partner's copy of the same logits.
-template <int N>
-COX_DEV void rs_step(float (&v)[2 * N], float (&o)[N], int lane, int off) {
-  const bool upper = (lane & off) != 0;
-#pragma unroll
-  for (int m = 0; m < N; ++m) {
-    const float keep = upper ? v[N + m] : v[m];
-    const float send = upper ? v[m] : v[N + m];
-    o[m] = __fadd_rn(keep, __shfl_xor_sync(0xffffffffu, send, off));
-  }
-}
 
 template <typename WT>
 __global__ void __launch_bounds__(R8_THREADS, 1)

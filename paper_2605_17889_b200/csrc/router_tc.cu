@@ -30,6 +30,7 @@
 #include <mutex>
 
 #include "common.cuh"
+#include "route_common.cuh"
 
 namespace cox {
 
@@ -266,12 +267,17 @@ __global__ void __launch_bounds__(RC_THREADS, 1) router_screen_kernel(const __gr
 }
 
 // ---------------------------------------------------------------------------- R2
-// One warp per token.  The exact logits of the candidates are computed four at
-// a time (two FFMA2 per x element: four independent canonical FMA chains per
-// lane, each logit's operation sequence unchanged), x row and router rows read
-// through L1 (the kernel uses no shared memory for data, so the whole router
-// weight of a fine-grained MoE stays L1-resident).
+// One warp per token.  The candidates' exact logits are computed with the x
+// chunk loop outermost: each x chunk is widened once and feeds up to 8
+// candidate chains (slot pairs share one FFMA2 with the x element broadcast),
+// so the widening cost is per token, not per candidate.  The 8 per-lane
+// partial sums are combined by a recursive-halving reduce-scatter over the
+// xor butterfly's exact pairs (9 shuffles instead of 40), and the top-k,
+// routing weights and histogram are warp_route_token's (route_common.cuh) on
+// the token's logits: exact for the candidates, screened for the rest (which
+// are provably below k exact candidate logits, so they are never selected).
 constexpr int RR_WARPS = 8;
+constexpr int RR_SLOTS = 8;  // candidate chains per pass
 
 // L1-allocating read-only load (the router rows are re-read by every token)
 COX_DEV uint4 ldg_v4(const void* p) { return __ldg(reinterpret_cast<const uint4*>(p)); }
@@ -283,9 +289,10 @@ __global__ void __launch_bounds__(RR_WARPS * 32, NCH <= 8 ? 2 : 1) router_rescor
     const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ wg, const float* __restrict__ approx,
     const float* __restrict__ margin, int T, int d, int E, int k, int mode, int32_t* __restrict__ idx,
     float* __restrict__ wout, int32_t* __restrict__ counts) {
-  __shared__ float s_l[RR_WARPS][256];     // per warp: approx logits, exact for the candidates
+  __shared__ float s_l[RR_WARPS][256];  // per warp: screened logits, exact for the candidates
   __shared__ uint8_t s_cand[RR_WARPS][256];
-  __shared__ int s_win[RR_WARPS][8];       // exact winners by rank
+  __shared__ int s_sel[RR_WARPS][8];
+  __shared__ float s_selv[RR_WARPS][8];
   __shared__ int s_hist[256];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int i = threadIdx.x; i < E; i += blockDim.x) s_hist[i] = 0;
@@ -293,32 +300,36 @@ __global__ void __launch_bounds__(RR_WARPS * 32, NCH <= 8 ? 2 : 1) router_rescor
   float* lg = s_l[warp];
   uint8_t* cand = s_cand[warp];
   for (long long t = (long long)blockIdx.x * RR_WARPS + warp; t < T; t += (long long)gridDim.x * RR_WARPS) {
+    const __nv_bfloat16* xr = x + t * d;
+    uint4 xq[NCH];
+#pragma unroll
+    for (int j = 0; j < NCH; ++j) {
+      const int s = 8 * lane + 256 * j;
+      xq[j] = s < d ? ld_nc_v4(xr + s) : make_uint4(0, 0, 0, 0);
+    }
     float av[NE];
+    uint32_t key[NE];
 #pragma unroll
     for (int i = 0; i < NE; ++i) {
       const int e = lane + 32 * i;
       av[i] = e < E ? approx[t * E + e] : -INFINITY;
       av[i] = av[i] != av[i] ? -INFINITY : av[i];  // NaN ranks like -inf (router.cu nan_low)
       if (e < E) lg[e] = av[i];
+      key[i] = e < E ? route_key(av[i]) : 0u;
     }
-    // k-th largest approx VALUE: k rounds of a value-only warp max; equal
-    // values leave together (that can only lower the threshold: a superset)
-    float kth = -INFINITY;
-    {
-      uint32_t taken = 0;
-      for (int j = 0; j < k; ++j) {
-        float bv = -INFINITY;
+    // k-th largest screened VALUE: k rounds of a warp max over order keys;
+    // equal values leave together (that can only lower the threshold: a superset)
+    uint32_t mk = 0;
+    for (int j = 0; j < k; ++j) {
+      uint32_t bk = 0;
 #pragma unroll
-        for (int i = 0; i < NE; ++i)
-          if (!(taken & (1u << i))) bv = fmaxf(bv, av[i]);
+      for (int i = 0; i < NE; ++i) bk = key[i] > bk ? key[i] : bk;
+      mk = __reduce_max_sync(0xffffffffu, bk);
 #pragma unroll
-        for (int off = 16; off >= 1; off >>= 1) bv = fmaxf(bv, __shfl_xor_sync(0xffffffffu, bv, off));
-#pragma unroll
-        for (int i = 0; i < NE; ++i)
-          if (av[i] == bv) taken |= 1u << i;
-        kth = bv;
-      }
+      for (int i = 0; i < NE; ++i)
+        if (key[i] == mk) key[i] = 0;
     }
+    const float kth = __uint_as_float((mk & 0x80000000u) ? (mk & 0x7fffffffu) : ~mk);
     const float thr = kth - 2.0f * margin[t];
     int nc = 0;
 #pragma unroll
@@ -330,92 +341,52 @@ __global__ void __launch_bounds__(RR_WARPS * 32, NCH <= 8 ? 2 : 1) router_rescor
       nc += __popc(bal);
     }
     __syncwarp();
-    const __nv_bfloat16* xr = x + t * d;
-    uint4 xq[NCH];
+    for (int c0 = 0; c0 < nc; c0 += RR_SLOTS) {
+      const int ns = nc - c0 < RR_SLOTS ? nc - c0 : RR_SLOTS;  // warp-uniform
+      int wo[RR_SLOTS];  // element offsets of the slots' router rows (E * d < 2^31)
+      float a[RR_SLOTS];
 #pragma unroll
-    for (int j = 0; j < NCH; ++j) {
-      const int s = 8 * lane + 256 * j;
-      xq[j] = s < d ? ld_nc_v4(xr + s) : make_uint4(0, 0, 0, 0);
-    }
-    constexpr int CG = NCH >= 16 ? 2 : 4;  // candidates per pass (registers: x row + CG weight chunks)
-    for (int c = 0; c < nc; c += CG) {
-      int ec[CG];
-      const __nv_bfloat16* wr[CG];
-      float a[CG];
-#pragma unroll
-      for (int u = 0; u < CG; ++u) {
-        ec[u] = cand[c + u < nc ? c + u : nc - 1];
-        wr[u] = wg + (long long)ec[u] * d;
+      for (int u = 0; u < RR_SLOTS; ++u) {
+        wo[u] = (int)cand[c0 + (u < ns ? u : ns - 1)] * d + 8 * lane;
         a[u] = 0.f;
       }
 #pragma unroll
       for (int j = 0; j < NCH; ++j) {
-        const int s = 8 * lane + 256 * j;
-        if (s >= d) break;
-        float xv[8], f[CG][8];
-        bf16x8_to_f32(xq[j], xv);
+        if (8 * lane + 256 * j < d) {
+          uint4 wq[RR_SLOTS];
 #pragma unroll
-        for (int u = 0; u < CG; ++u) bf16x8_to_f32(ldg_v4(wr[u] + s), f[u]);
+          for (int u = 0; u < RR_SLOTS; u += 2)
+            if (u < ns) {
+              wq[u] = ldg_v4(wg + wo[u] + 256 * j);
+              wq[u + 1] = ldg_v4(wg + wo[u + 1] + 256 * j);
+            }
+          float xv[8];
+          bf16x8_to_f32(xq[j], xv);
 #pragma unroll
-        for (int q = 0; q < 8; ++q)
+          for (int u = 0; u < RR_SLOTS; u += 2)
+            if (u < ns) {
+              float fa[8], fb[8];
+              bf16x8_to_f32(wq[u], fa);
+              bf16x8_to_f32(wq[u + 1], fb);
 #pragma unroll
-          for (int u = 0; u < CG; u += 2) ffma2(a[u], a[u + 1], xv[q], f[u][q], f[u + 1][q]);
+              for (int q = 0; q < 8; ++q) ffma2(a[u], a[u + 1], xv[q], fa[q], fb[q]);
+            }
+        }
       }
-#pragma unroll
-      for (int off = 16; off >= 1; off >>= 1)
-#pragma unroll
-        for (int u = 0; u < CG; ++u) a[u] = __fadd_rn(a[u], __shfl_xor_sync(0xffffffffu, a[u], off));
-      if (lane == 0) {
-#pragma unroll
-        for (int u = 0; u < CG; ++u) lg[ec[u]] = a[u] != a[u] ? -INFINITY : a[u];
-      }
+      // butterfly sums of the 8 slots: reduce-scatter (16, 8, 4), then 2, 1;
+      // slot s ends in lanes 4 s .. 4 s + 3
+      float v4[4], v2[2], v1[1];
+      rs_step<4>(a, v4, lane, 16);
+      rs_step<2>(v4, v2, lane, 8);
+      rs_step<1>(v2, v1, lane, 4);
+      float r = v1[0];
+      r = __fadd_rn(r, __shfl_xor_sync(0xffffffffu, r, 2));
+      r = __fadd_rn(r, __shfl_xor_sync(0xffffffffu, r, 1));
+      const int s = lane >> 2;
+      if ((lane & 3) == 0 && s < ns) lg[cand[c0 + s]] = r != r ? -INFINITY : r;
     }
     __syncwarp();
-    // exact top-k among the candidates: the rank of candidate slot c is the
-    // number of candidates with a larger exact logit, or an equal one and a
-    // lower expert index (the tie rule); slots are spread over the lanes
-    for (int c0 = 0; c0 < nc; c0 += 32) {
-      const int c = c0 + lane;
-      const int e = c < nc ? cand[c] : 0;
-      const float v = c < nc ? lg[e] : 0.f;
-      int rank = 0;
-      for (int o = 0; o < nc; ++o) {
-        const int eo = cand[o];
-        const float vo = lg[eo];
-        rank += (vo > v || (vo == v && eo < e)) ? 1 : 0;
-      }
-      if (c < nc && rank < k) s_win[warp][rank] = e;
-    }
-    __syncwarp();
-    int sel[8];
-    float selv[8];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      if (j < k) {
-        sel[j] = s_win[warp][j];
-        selv[j] = lg[sel[j]];
-      }
-    }
-    __syncwarp();
-    if (mode != 0) {  // full-softmax denominator terms in parallel
-      for (int e = lane; e < E; e += 32) lg[e] = expf(__fsub_rn(lg[e], selv[0]));
-      __syncwarp();
-    }
-    if (lane == 0) {
-      const float m = selv[0];
-      float ssum = 0.0f;
-      if (mode == 0) {
-        for (int j = 0; j < k; ++j) ssum = __fadd_rn(ssum, expf(__fsub_rn(selv[j], m)));
-      } else {
-        for (int e = 0; e < E; ++e) ssum = __fadd_rn(ssum, lg[e]);  // ascending e, as the oracle
-      }
-      for (int j = 0; j < k; ++j) {
-        idx[t * k + j] = sel[j];
-        wout[t * k + j] = __fdiv_rn(expf(__fsub_rn(selv[j], m)), ssum);
-        atomicAdd(&s_hist[sel[j]], 1);
-      }
-    }
-    __syncwarp();
+    warp_route_token(lg, E, k, mode, lane, s_sel[warp], s_selv[warp], idx + t * k, wout + t * k, s_hist);
   }
   __syncthreads();
   for (int i = threadIdx.x; i < E; i += blockDim.x)
