@@ -250,6 +250,17 @@ COX_DEV void tmem_ld_32x32b_x32(uint32_t taddr, uint32_t (&r)[32]) {
 }
 COX_DEV void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
+// a = fma(x.lo, w.lo, a); a = fma(x.hi, w.hi, a) for two packed bf16 pairs:
+// mixed-precision fma.rn.f32.bf16 (FHFMA.BF16, sm_100) reads the bf16 halves
+// straight from the 32-bit registers.  The product of two bf16 values is exact
+// in fp32, so each step equals fmaf on the widened operands (one rounding) —
+// bit-identical to the widen-then-FFMA sequence, without the widening.
+COX_DEV void fma_bf16x2_seq(float& a, uint32_t x2, uint32_t w2) {
+  asm("{\n\t.reg .b16 xl, xh, wl, wh;\n\tmov.b32 {xl, xh}, %1;\n\tmov.b32 {wl, wh}, %2;\n\t"
+      "fma.rn.f32.bf16 %0, xl, wl, %0;\n\tfma.rn.f32.bf16 %0, xh, wh, %0;\n\t}"
+      : "+f"(a) : "r"(x2), "r"(w2));
+}
+
 // Two independent fp32 FMAs in one FFMA2 (fma.rn.f32x2, sm_100): a0 = fma(x, w0, a0),
 // a1 = fma(x, w1, a1), each correctly rounded — bit-identical to two fmaf.  ptxas
 // folds the duplicated x into a broadcast operand.

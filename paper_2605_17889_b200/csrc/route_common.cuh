@@ -37,13 +37,15 @@ COX_DEV uint32_t route_key(float v) {
   return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
 }
 
+// NI = logits per lane held as keys (E <= 32 NI): callers that know E is small
+// pass a smaller NI (each selection round scans NI registers per lane).
+template <int NI = 8>
 COX_DEV void warp_route_token(float* lg, int E, int k, int mode, int lane, int* s_sel, float* s_selv,
                               int32_t* idx, float* w, int* hist) {
   // the lane's logits (experts lane + 32 i) in registers, selected ones knocked
   // out; each round: the lane's best (lowest index among equals), then two
   // warp-wide redux steps: max key, then min index among the lanes holding it
   // (= the old shuffle butterfly's choice: largest value, ties -> lower index)
-  constexpr int NI = 8;  // E <= 256
   uint32_t key[NI];
 #pragma unroll
   for (int i = 0; i < NI; ++i) key[i] = (lane + 32 * i < E) ? route_key(lg[lane + 32 * i]) : 0u;

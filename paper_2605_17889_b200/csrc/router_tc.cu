@@ -268,9 +268,9 @@ __global__ void __launch_bounds__(RC_THREADS, 1) router_screen_kernel(const __gr
 
 // ---------------------------------------------------------------------------- R2
 // One warp per token.  The candidates' exact logits are computed with the x
-// chunk loop outermost: each x chunk is widened once and feeds up to 8
-// candidate chains (slot pairs share one FFMA2 with the x element broadcast),
-// so the widening cost is per token, not per candidate.  The 8 per-lane
+// chunk loop outermost, up to 8 candidate chains per pass, each step one
+// mixed-precision FMA on the packed bf16 operands (fma_bf16x2_seq: no
+// widening instructions, bit-identical to fmaf on the widened values).  The 8 per-lane
 // partial sums are combined by a recursive-halving reduce-scatter over the
 // xor butterfly's exact pairs (9 shuffles instead of 40), and the top-k,
 // routing weights and histogram are warp_route_token's (route_common.cuh) on
@@ -343,11 +343,11 @@ __global__ void __launch_bounds__(RR_WARPS * 32, NCH <= 8 ? 2 : 1) router_rescor
     __syncwarp();
     for (int c0 = 0; c0 < nc; c0 += RR_SLOTS) {
       const int ns = nc - c0 < RR_SLOTS ? nc - c0 : RR_SLOTS;  // warp-uniform
-      int wo[RR_SLOTS];  // element offsets of the slots' router rows (E * d < 2^31)
+      const __nv_bfloat16* wr[RR_SLOTS];
       float a[RR_SLOTS];
 #pragma unroll
       for (int u = 0; u < RR_SLOTS; ++u) {
-        wo[u] = (int)cand[c0 + (u < ns ? u : ns - 1)] * d + 8 * lane;
+        wr[u] = wg + (long long)cand[c0 + (u < ns ? u : ns - 1)] * d + 8 * lane;
         a[u] = 0.f;
       }
 #pragma unroll
@@ -355,21 +355,15 @@ __global__ void __launch_bounds__(RR_WARPS * 32, NCH <= 8 ? 2 : 1) router_rescor
         if (8 * lane + 256 * j < d) {
           uint4 wq[RR_SLOTS];
 #pragma unroll
-          for (int u = 0; u < RR_SLOTS; u += 2)
-            if (u < ns) {
-              wq[u] = ldg_v4(wg + wo[u] + 256 * j);
-              wq[u + 1] = ldg_v4(wg + wo[u + 1] + 256 * j);
-            }
-          float xv[8];
-          bf16x8_to_f32(xq[j], xv);
+          for (int u = 0; u < RR_SLOTS; ++u)
+            if (u < ns) wq[u] = ldg_v4(wr[u] + 256 * j);
 #pragma unroll
-          for (int u = 0; u < RR_SLOTS; u += 2)
+          for (int u = 0; u < RR_SLOTS; ++u)
             if (u < ns) {
-              float fa[8], fb[8];
-              bf16x8_to_f32(wq[u], fa);
-              bf16x8_to_f32(wq[u + 1], fb);
-#pragma unroll
-              for (int q = 0; q < 8; ++q) ffma2(a[u], a[u + 1], xv[q], fa[q], fb[q]);
+              fma_bf16x2_seq(a[u], xq[j].x, wq[u].x);
+              fma_bf16x2_seq(a[u], xq[j].y, wq[u].y);
+              fma_bf16x2_seq(a[u], xq[j].z, wq[u].z);
+              fma_bf16x2_seq(a[u], xq[j].w, wq[u].w);
             }
         }
       }
@@ -386,7 +380,7 @@ __global__ void __launch_bounds__(RR_WARPS * 32, NCH <= 8 ? 2 : 1) router_rescor
       if ((lane & 3) == 0 && s < ns) lg[cand[c0 + s]] = r != r ? -INFINITY : r;
     }
     __syncwarp();
-    warp_route_token(lg, E, k, mode, lane, s_sel[warp], s_selv[warp], idx + t * k, wout + t * k, s_hist);
+    warp_route_token<NE>(lg, E, k, mode, lane, s_sel[warp], s_selv[warp], idx + t * k, wout + t * k, s_hist);
   }
   __syncthreads();
   for (int i = threadIdx.x; i < E; i += blockDim.x)
