@@ -267,17 +267,16 @@ __global__ void __launch_bounds__(RC_THREADS, 1) router_screen_kernel(const __gr
 }
 
 // ---------------------------------------------------------------------------- R2
-// One warp per token.  The candidates' exact logits are computed with the x
-// chunk loop outermost, up to 8 candidate chains per pass, each step one
-// mixed-precision FMA on the packed bf16 operands (fma_bf16x2_seq: no
-// widening instructions, bit-identical to fmaf on the widened values).  The 8 per-lane
-// partial sums are combined by a recursive-halving reduce-scatter over the
-// xor butterfly's exact pairs (9 shuffles instead of 40), and the top-k,
+// One warp per token.  The candidates' exact logits are computed two chains
+// at a time, each step one mixed-precision FMA on the packed bf16 operands
+// (fma_bf16x2_seq: no widening instructions, bit-identical to fmaf on the
+// widened values); a pair's per-lane partial sums are combined over the xor
+// butterfly's exact pairs (reduce-scatter at 16, then 8..1), and the top-k,
 // routing weights and histogram are warp_route_token's (route_common.cuh) on
 // the token's logits: exact for the candidates, screened for the rest (which
 // are provably below k exact candidate logits, so they are never selected).
 constexpr int RR_WARPS = 8;
-constexpr int RR_SLOTS = 8;  // candidate chains per pass
+constexpr int RR_CH = 2;  // candidate chains in flight per warp (4: +2% time, more discarded chains)
 
 // L1-allocating read-only load (the router rows are re-read by every token)
 COX_DEV uint4 ldg_v4(const void* p) { return __ldg(reinterpret_cast<const uint4*>(p)); }
@@ -285,12 +284,12 @@ COX_DEV uint4 ldg_v4(const void* p) { return __ldg(reinterpret_cast<const uint4*
 // NCH = x chunks per lane held in registers (d <= 256 NCH): the token's whole
 // x row is requested at once, so a token costs one DRAM round trip.
 template <int NCH, int NE>
-__global__ void __launch_bounds__(RR_WARPS * 32, NCH <= 8 ? 2 : 1) router_rescore_kernel(
+__global__ void __launch_bounds__(RR_WARPS * 32, NCH <= 8 ? 3 : 1) router_rescore_kernel(
     const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ wg, const float* __restrict__ approx,
     const float* __restrict__ margin, int T, int d, int E, int k, int mode, int32_t* __restrict__ idx,
     float* __restrict__ wout, int32_t* __restrict__ counts) {
-  __shared__ float s_l[RR_WARPS][256];  // per warp: screened logits, exact for the candidates
-  __shared__ uint8_t s_cand[RR_WARPS][256];
+  __shared__ float s_l[RR_WARPS][32 * NE];  // per warp: screened logits, exact for the candidates
+  __shared__ uint8_t s_cand[RR_WARPS][32 * NE];
   __shared__ int s_sel[RR_WARPS][8];
   __shared__ float s_selv[RR_WARPS][8];
   __shared__ int s_hist[256];
@@ -341,43 +340,43 @@ __global__ void __launch_bounds__(RR_WARPS * 32, NCH <= 8 ? 2 : 1) router_rescor
       nc += __popc(bal);
     }
     __syncwarp();
-    for (int c0 = 0; c0 < nc; c0 += RR_SLOTS) {
-      const int ns = nc - c0 < RR_SLOTS ? nc - c0 : RR_SLOTS;  // warp-uniform
-      const __nv_bfloat16* wr[RR_SLOTS];
-      float a[RR_SLOTS];
+    // candidates RR_CH at a time (a runtime loop: only real candidates cost
+    // FMAs; a short last group runs beside discarded duplicates)
+    for (int c = 0; c < nc; c += RR_CH) {
+      const __nv_bfloat16* wr[RR_CH];
+      float a[RR_CH];
 #pragma unroll
-      for (int u = 0; u < RR_SLOTS; ++u) {
-        wr[u] = wg + (long long)cand[c0 + (u < ns ? u : ns - 1)] * d + 8 * lane;
+      for (int u = 0; u < RR_CH; ++u) {
+        wr[u] = wg + (long long)cand[c + u < nc ? c + u : c] * d + 8 * lane;
         a[u] = 0.f;
       }
 #pragma unroll
       for (int j = 0; j < NCH; ++j) {
         if (8 * lane + 256 * j < d) {
-          uint4 wq[RR_SLOTS];
+          uint4 p[RR_CH];
 #pragma unroll
-          for (int u = 0; u < RR_SLOTS; ++u)
-            if (u < ns) wq[u] = ldg_v4(wr[u] + 256 * j);
+          for (int u = 0; u < RR_CH; ++u) p[u] = ldg_v4(wr[u] + 256 * j);
 #pragma unroll
-          for (int u = 0; u < RR_SLOTS; ++u)
-            if (u < ns) {
-              fma_bf16x2_seq(a[u], xq[j].x, wq[u].x);
-              fma_bf16x2_seq(a[u], xq[j].y, wq[u].y);
-              fma_bf16x2_seq(a[u], xq[j].z, wq[u].z);
-              fma_bf16x2_seq(a[u], xq[j].w, wq[u].w);
-            }
+          for (int u = 0; u < RR_CH; ++u) fma_bf16x2_seq(a[u], xq[j].x, p[u].x);
+#pragma unroll
+          for (int u = 0; u < RR_CH; ++u) fma_bf16x2_seq(a[u], xq[j].y, p[u].y);
+#pragma unroll
+          for (int u = 0; u < RR_CH; ++u) fma_bf16x2_seq(a[u], xq[j].z, p[u].z);
+#pragma unroll
+          for (int u = 0; u < RR_CH; ++u) fma_bf16x2_seq(a[u], xq[j].w, p[u].w);
         }
       }
-      // butterfly sums of the 8 slots: reduce-scatter (16, 8, 4), then 2, 1;
-      // slot s ends in lanes 4 s .. 4 s + 3
-      float v4[4], v2[2], v1[1];
-      rs_step<4>(a, v4, lane, 16);
-      rs_step<2>(v4, v2, lane, 8);
-      rs_step<1>(v2, v1, lane, 4);
+      // butterfly sums of the group over the xor butterfly's exact pairs:
+      // reduce-scatter at 16, then plain levels 8, 4, 2, 1; chain u ends in
+      // lanes 16 u .. 16 u + 15
+      static_assert(RR_CH == 2, "reduce-scatter below is written for 2 chains");
+      float v1[1];
+      rs_step<1>(a, v1, lane, 16);
       float r = v1[0];
-      r = __fadd_rn(r, __shfl_xor_sync(0xffffffffu, r, 2));
-      r = __fadd_rn(r, __shfl_xor_sync(0xffffffffu, r, 1));
-      const int s = lane >> 2;
-      if ((lane & 3) == 0 && s < ns) lg[cand[c0 + s]] = r != r ? -INFINITY : r;
+#pragma unroll
+      for (int off = 8; off >= 1; off >>= 1) r = __fadd_rn(r, __shfl_xor_sync(0xffffffffu, r, off));
+      const int u = lane >> 4;
+      if ((lane & 15) == 0 && c + u < nc) lg[cand[c + u]] = r != r ? -INFINITY : r;
     }
     __syncwarp();
     warp_route_token<NE>(lg, E, k, mode, lane, s_sel[warp], s_selv[warp], idx + t * k, wout + t * k, s_hist);
