@@ -102,6 +102,19 @@ int cox_grouped_swiglu(const void* x_perm, long long rows_cap, const int32_t* of
                        const int32_t* group_experts, const void* const* w13, int d, int ff, void* h, int max_ctas,
                        void* stream);
 
+/* K3 with the permuted rows gathered from x (no x_perm copy): identical
+ * results to cox_grouped_swiglu on x_perm[r] = x[row_tokens[r]].  row_tokens
+ * [T*k]: the source token of every permuted row (cox_permute with x_perm ==
+ * NULL writes it, with offsets and dst and no row copy).  Four extra warps per
+ * CTA fill the A stages by cp.async in the 128B-swizzled layout the tensor
+ * core reads; B (the weights) still streams by TMA.  Replaces the permute's
+ * row copy (T*k*d*2 bytes written, T*d*2 read) in the reference's
+ * expert:dispatch step (sim.py:149-202, costmodel.py:266-273).
+ * d % 64 == 0, ff % 128 == 0. */
+int cox_grouped_swiglu_gather(const void* x, long long T, const int32_t* row_tokens, const int32_t* offsets, int E,
+                              int n_groups, const int32_t* group_experts, const void* const* w13, int d, int ff,
+                              void* h, int max_ctas, void* stream);
+
 /* K4 — grouped down projection: y_perm[r] = h[r] W2_e^T.  w2[g]: [d, ff] bf16.
  * Same grouping arguments as cox_grouped_swiglu.  ff % 64 == 0, d % 256 == 0. */
 int cox_grouped_down(const void* h, long long rows_cap, const int32_t* offsets, int E, int n_groups,

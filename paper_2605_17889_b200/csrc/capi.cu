@@ -18,7 +18,8 @@ int launch_permute(const int32_t* idx, int T, int k, int E, int tile_m, const vo
                    long long rows_cap = 0);
 int launch_grouped_gemm(int epi, const void* A, long long rows_cap, int K, const int32_t* offsets, int n_groups,
                         const int32_t* group_expert, const void* const* B, int N, void* out, long long ldo,
-                        int max_ctas, cudaStream_t s);
+                        int max_ctas, cudaStream_t s, const void* gx = nullptr, const int32_t* row_tokens = nullptr,
+                        long long gx_ld = 0);
 struct SmallDense {
   const void* wg;
   int E, mode;
@@ -189,6 +190,23 @@ int cox_grouped_swiglu(const void* x_perm, long long rows_cap, const int32_t* of
   if (n_groups > 0 && (!x_perm || !h || !offsets)) return fail(COX_EINVAL, "%s: null x_perm/h/offsets", fn);
   int rc = cox::launch_grouped_gemm(0, x_perm, rows_cap, d, offsets, n_groups, group_experts, w13, 2 * ff, h, ff,
                                     max_ctas, static_cast<cudaStream_t>(stream));
+  return cuda_status(rc, fn);
+}
+
+int cox_grouped_swiglu_gather(const void* x, long long T, const int32_t* row_tokens, const int32_t* offsets, int E,
+                              int n_groups, const int32_t* group_experts, const void* const* w13, int d, int ff,
+                              void* h, int max_ctas, void* stream) {
+  const char* fn = "cox_grouped_swiglu_gather";
+  if (d <= 0 || d % 64 || ff <= 0 || ff % 128)
+    return fail(COX_EINVAL, "%s: need d%%64==0 and ff%%128==0 (d=%d ff=%d)", fn, d, ff);
+  if (T < 0) return fail(COX_EINVAL, "%s: T < 0", fn);
+  if (max_ctas < 0 || max_ctas == 1) return fail(COX_EINVAL, "%s: max_ctas must be 0 or >= 2", fn);
+  if (!aligned16(x) || !aligned16(h)) return fail(COX_EINVAL, "%s: unaligned x/h", fn);
+  if (int rc = check_groups(fn, E, n_groups, group_experts, w13)) return rc;
+  if (n_groups > 0 && (!x || !h || !offsets || !row_tokens))
+    return fail(COX_EINVAL, "%s: null x/h/offsets/row_tokens", fn);
+  int rc = cox::launch_grouped_gemm(0, nullptr, 0, d, offsets, n_groups, group_experts, w13, 2 * ff, h, ff, max_ctas,
+                                    static_cast<cudaStream_t>(stream), x, row_tokens, d);
   return cuda_status(rc, fn);
 }
 

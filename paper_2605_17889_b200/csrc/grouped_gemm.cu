@@ -50,6 +50,7 @@ constexpr int GM_BK = 64;   // one 128-byte swizzle atom of bf16
 constexpr int GM_STAGES = 6;
 constexpr int GM_MAXG = 64;
 constexpr int GM_THREADS = 256;
+constexpr int GM_GATHER_WARPS = 4;  // gather mode: A rows by cp.async (warps 8..11)
 constexpr uint32_t GM_A_BYTES = GM_BM * GM_BK * 2;         // 16 KB
 constexpr uint32_t GM_B_BYTES = (GM_BN / 2) * GM_BK * 2;   // 16 KB
 constexpr uint32_t GM_TMEM_COLS = 512;
@@ -70,6 +71,11 @@ struct alignas(64) GemmParams {
   int n_tiles;
   int band;
   int l2_mode;  // L2 cache policy of the operand loads, see l2_policies()
+  // gather mode (K3 without x_perm): A row r of group g is token
+  // row_tokens[row0_g + r] of gx [*, K] (row pitch gx_ld elements)
+  const __nv_bfloat16* gx;
+  const int32_t* row_tokens;
+  long long gx_ld;
 };
 
 struct TileCoord {
@@ -124,8 +130,13 @@ COX_DEV void l2_policies(int mode, uint64_t& pa, uint64_t& pb) {
   pa = mode == 2 ? first : normal;
 }
 
-template <int EPI, int KA>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GM_THREADS, 1)
+// 16-byte cp.async into shared memory (L2 only); src_bytes 0 zero-fills
+COX_DEV void cp_async_cg16(uint32_t dst, const void* src, uint32_t src_bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(src_bytes) : "memory");
+}
+
+template <int EPI, int KA, bool GATHER = false>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GM_THREADS + (GATHER ? 32 * GM_GATHER_WARPS : 0), 1)
     grouped_gemm_kernel(const __grid_constant__ GemmParams p) {
   constexpr int BK = GM_BK * KA;
   constexpr int STAGES = GmRing<KA>::STAGES;
@@ -143,7 +154,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GM_THREADS, 1)
   uint64_t* tempty = bars + 2 * NB + 2;
   uint64_t* sfull = bars + 2 * NB + 4;                           // [DEPTH] tile id published
   uint64_t* sempty = sfull + GM_SCHED_DEPTH;                     // [DEPTH] (leader) slot consumed
-  int* s_tile = reinterpret_cast<int*>(sempty + GM_SCHED_DEPTH);  // [DEPTH]
+  uint64_t* afull = sempty + GM_SCHED_DEPTH;                     // [NB] gather mode: this CTA's A copies landed
+  int* s_tile = reinterpret_cast<int*>(afull + NB);              // [DEPTH]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_tile + GM_SCHED_DEPTH);
   int* s_prefix = reinterpret_cast<int*>(tmem_slot + 4);
   int* s_rows = s_prefix + GM_MAXG + 1;
@@ -157,8 +169,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GM_THREADS, 1)
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
-      mbar_init(smem_u32(&full[s]), 1);
+      // gather mode: + one relay arrive per CTA (its A copies landed)
+      mbar_init(smem_u32(&full[s]), GATHER ? 3 : 1);
       mbar_init(smem_u32(&empty[s]), 1);
+      if (GATHER) mbar_init(smem_u32(&afull[s]), 32 * GM_GATHER_WARPS);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(smem_u32(&tfull[a]), 1);
@@ -166,7 +180,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GM_THREADS, 1)
     }
     for (int i = 0; i < GM_SCHED_DEPTH; ++i) {
       mbar_init(smem_u32(&sfull[i]), 1);
-      mbar_init(smem_u32(&sempty[i]), 11);  // producers x2 + MMA + epilogue warps x8
+      // producers x2 + MMA + epilogue warps x8 (+ gather warps x8 + relays x2)
+      mbar_init(smem_u32(&sempty[i]), GATHER ? 11 + 2 * GM_GATHER_WARPS + 2 : 11);
     }
     fence_mbar_init();
   }
@@ -197,7 +212,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GM_THREADS, 1)
     if (lane == 0) s_prefix[p.n_groups] = acc;
   }
   if (warp == 0 && lane == 0) {
-    tma_prefetch_desc(&p.a_map);
+    if (!GATHER) tma_prefetch_desc(&p.a_map);
     for (int g = 0; g < p.n_groups; ++g) tma_prefetch_desc(&p.b_map[g]);
   }
   if (warp == 2) tmem_alloc<2>(smem_u32(tmem_slot), GM_TMEM_COLS);
@@ -274,17 +289,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GM_THREADS, 1)
           mbar_wait(smem_u32(&empty[stage]), phase ^ 1);
           const uint32_t fb_local = smem_u32(&full[stage]);
           const uint32_t fb = mapa(fb_local, 0);
-          if (rank == 0) mbar_arrive_expect_tx(fb_local, 2 * (A_STAGE + B_STAGE));
+          if (rank == 0) mbar_arrive_expect_tx(fb_local, 2 * ((GATHER ? 0u : A_STAGE) + B_STAGE));
 #pragma unroll
           for (int a = 0; a < KA; ++a) {
             const uint32_t da = smem_u32(sA + stage * A_STAGE + a * GM_A_BYTES);
             const uint32_t db = smem_u32(sB + stage * B_STAGE + a * GM_B_BYTES);
             const int kc = kb * BK + a * GM_BK;
             if (hint) {
-              tma_load_2d_pair_hint(da, &p.a_map, fb, kc, a_row, pol_a);
+              if (!GATHER) tma_load_2d_pair_hint(da, &p.a_map, fb, kc, a_row, pol_a);
               tma_load_2d_pair_hint(db, bmap, fb, kc, b_row, pol_b);
             } else {
-              tma_load_2d_pair(da, &p.a_map, fb, kc, a_row);
+              if (!GATHER) tma_load_2d_pair(da, &p.a_map, fb, kc, a_row);
               tma_load_2d_pair(db, bmap, fb, kc, b_row);
             }
           }
@@ -310,7 +325,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GM_THREADS, 1)
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * GM_BN;
         for (int kb = 0; kb < nk; ++kb) {
-          mbar_wait(smem_u32(&full[stage]), phase);
+          if (GATHER) mbar_wait_cluster(smem_u32(&full[stage]), phase);  // peer gather warps arrive remotely
+          else mbar_wait(smem_u32(&full[stage]), phase);
           tc_fence_after();
           const uint32_t a_base = smem_u32(sA + stage * A_STAGE);
           const uint32_t b_base = smem_u32(sB + stage * B_STAGE);
@@ -329,7 +345,78 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GM_THREADS, 1)
       }
     }
     __syncwarp();
-  } else if (warp >= 4) {
+  } else if (GATHER && warp == 2) {
+    // ------------------------------------------------------------ A relay (gather mode)
+    // Waits until this CTA's gather threads' copies of a stage have landed
+    // (cp.async.mbarrier.arrive on afull), makes them visible to the tensor
+    // core's async proxy, and arrives on the leader's full barrier (cluster
+    // scope, release) — the MMA waits there with a cluster-scope acquire.
+    if (lane == 0) {
+      const uint32_t full0 = mapa(smem_u32(&full[0]), 0);
+      uint32_t stage = 0, phase = 0;
+      int si = 0;
+      int t = fetch_tile(si, true);
+      while (t < total) {
+        int t_next = total;
+        for (int kb = 0; kb < nk; ++kb) {
+          mbar_wait(smem_u32(&afull[stage]), phase);
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          mbar_arrive_cluster(full0 + stage * 8);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+          if (kb == 0) t_next = fetch_tile(si, true);
+        }
+        t = t_next;
+      }
+    }
+    __syncwarp();
+  } else if (GATHER && warp >= 8) {
+    // ------------------------------------------------------------ A gather (cp.async)
+    // 4 warps fill this CTA's 128 A rows of every stage straight from x: lane
+    // (gw, l) copies 16-byte chunk l%8 of rows 4 gw + l/8 + 16 w (w < 8) of
+    // each 64-column swizzle atom (a warp instruction = 4 rows x 128 B), into
+    // the 128B-swizzled K-major layout TMA would write (chunk c of row r at
+    // (c ^ (r & 7)) * 16).  Completion is tracked without blocking: each
+    // thread's cp.async.mbarrier.arrive.noinc fires on afull[stage] once its
+    // copies have landed (the relay warp publishes the stage).  Rows past the
+    // group end are zero-filled.
+    const int gw = warp - 8;
+    const int c8 = lane & 7;
+    uint32_t stage = 0, phase = 0;
+    int si = 0, gcur = 0;
+    int t = fetch_tile(si, lane == 0);
+    while (t < total) {
+      const TileCoord c = decode_tile(t, s_prefix, s_rows, p.band, gcur);
+      const int lrow0 = c.m * 2 * GM_BM + (int)rank * GM_BM;  // first A row of this CTA in the group
+      const __nv_bfloat16* src[8];
+      uint32_t sbytes[8];
+#pragma unroll
+      for (int w = 0; w < 8; ++w) {
+        const int r = 4 * gw + (lane >> 3) + 16 * w;
+        const bool ok = lrow0 + r < s_rows[c.g];
+        const int tok = ok ? __ldg(p.row_tokens + s_row0[c.g] + lrow0 + r) : 0;
+        src[w] = p.gx + (long long)tok * p.gx_ld + 8 * c8;
+        sbytes[w] = ok ? 16u : 0u;
+      }
+      int t_next = total;
+      for (int kb = 0; kb < nk; ++kb) {
+        mbar_wait(smem_u32(&empty[stage]), phase ^ 1);
+#pragma unroll
+        for (int a = 0; a < KA; ++a) {
+          const uint32_t atom = smem_u32(sA + stage * A_STAGE + a * GM_A_BYTES);
+          const int kc = kb * BK + a * GM_BK;
+#pragma unroll
+          for (int w = 0; w < 8; ++w) {
+            const int r = 4 * gw + (lane >> 3) + 16 * w;
+            cp_async_cg16(atom + r * 128 + ((c8 ^ (r & 7)) << 4), src[w] + kc, sbytes[w]);
+          }
+        }
+        asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(&afull[stage])) : "memory");
+        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        if (kb == 0) t_next = fetch_tile(si, lane == 0);
+      }
+      t = t_next;
+    }
+  } else if (warp >= 4 && warp < 8) {
     // ------------------------------------------------------------ epilogue
     const int ew = warp - 4;
     const uint32_t tempty_leader0 = mapa(smem_u32(&tempty[0]), 0);
@@ -524,15 +611,22 @@ static int g_num_sms = 0;
 
 // epi: EPI_SWIGLU (B = W13 interleaved [2ff, K], out = h [rows_cap, ff])
 //      EPI_STORE  (B = W2 [N, K],                out = y [rows_cap, N])
+// gx != nullptr (EPI_SWIGLU only): gather mode, A row r of a group is row
+// row_tokens[r] of gx [*, K] (pitch gx_ld); A / rows_cap are unused.
 int launch_grouped_gemm(int epi, const void* A, long long rows_cap, int K, const int32_t* offsets, int n_groups,
                         const int32_t* group_expert, const void* const* B, int N, void* out, long long ldo,
-                        int max_ctas, cudaStream_t s) {
+                        int max_ctas, cudaStream_t s, const void* gx, const int32_t* row_tokens, long long gx_ld) {
   if (n_groups <= 0) return 0;
   static GemmParams p;  // large (8.6 KB): built in static storage, copied at launch
   static std::mutex mu;
   std::lock_guard<std::mutex> lk(mu);
-  int rc = get_map(&p.a_map, A, (unsigned long long)rows_cap, (unsigned long long)K, (unsigned)GM_BM);
+  const bool gather = gx != nullptr;
+  if (gather && epi != EPI_SWIGLU) return -1;
+  int rc = gather ? 0 : get_map(&p.a_map, A, (unsigned long long)rows_cap, (unsigned long long)K, (unsigned)GM_BM);
   if (rc) return rc;
+  p.gx = static_cast<const __nv_bfloat16*>(gx);
+  p.row_tokens = row_tokens;
+  p.gx_ld = gx_ld;
   for (int g = 0; g < n_groups; ++g) {
     rc = get_map(&p.b_map[g], B[g], (unsigned long long)N, (unsigned long long)K, GM_BN / 2);
     if (rc) return rc;
@@ -583,22 +677,28 @@ int launch_grouped_gemm(int epi, const void* A, long long rows_cap, int K, const
   // stages (42.6 vs 43.6 ms).
   int ka = epi == EPI_SWIGLU ? 2 : 1;
   if (K % (ka * GM_BK) != 0) ka = 1;
-#define GM_LAUNCH(E_, KA_)                                                                                     \
+#define GM_LAUNCH(E_, KA_, G_)                                                                                 \
   do {                                                                                                         \
     static bool attr = false;                                                                                  \
     if (!attr) {                                                                                               \
-      cudaFuncSetAttribute(grouped_gemm_kernel<E_, KA_>, cudaFuncAttributeMaxDynamicSharedMemorySize,          \
+      cudaFuncSetAttribute(grouped_gemm_kernel<E_, KA_, G_>, cudaFuncAttributeMaxDynamicSharedMemorySize,      \
                            (int)GmRing<KA_>::SMEM);                                                            \
       attr = true;                                                                                             \
     }                                                                                                          \
-    grouped_gemm_kernel<E_, KA_><<<grid, GM_THREADS, GmRing<KA_>::SMEM, s>>>(p);                               \
+    grouped_gemm_kernel<E_, KA_, G_><<<grid, GM_THREADS + (G_ ? 32 * GM_GATHER_WARPS : 0), GmRing<KA_>::SMEM,   \
+                                       s>>>(p);                                                                \
   } while (0)
   if (epi == EPI_SWIGLU) {
-    if (ka == 2) GM_LAUNCH(EPI_SWIGLU, 2);
-    else GM_LAUNCH(EPI_SWIGLU, 1);
+    if (gather) {
+      if (ka == 2) GM_LAUNCH(EPI_SWIGLU, 2, true);
+      else GM_LAUNCH(EPI_SWIGLU, 1, true);
+    } else {
+      if (ka == 2) GM_LAUNCH(EPI_SWIGLU, 2, false);
+      else GM_LAUNCH(EPI_SWIGLU, 1, false);
+    }
   } else {
-    if (ka == 2) GM_LAUNCH(EPI_STORE, 2);
-    else GM_LAUNCH(EPI_STORE, 1);
+    if (ka == 2) GM_LAUNCH(EPI_STORE, 2, false);
+    else GM_LAUNCH(EPI_STORE, 1, false);
   }
 #undef GM_LAUNCH
   return launch_status();

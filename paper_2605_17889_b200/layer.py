@@ -51,7 +51,7 @@ class StageBuffers:
 
 
 def alloc_buffers(T: int, d: int, ff: int, E: int, k: int, tile_m: int, device, out_dtype=torch.bfloat16,
-                  shared_ff: int = 0) -> StageBuffers:
+                  shared_ff: int = 0, gather_a: bool = False) -> StageBuffers:
     cap = ops.rows_capacity(T, k, E, tile_m)
     bf = torch.bfloat16
     b = StageBuffers(
@@ -61,13 +61,15 @@ def alloc_buffers(T: int, d: int, ff: int, E: int, k: int, tile_m: int, device, 
         counts=torch.empty((E,), dtype=torch.int32, device=device),
         offsets=torch.empty((E + 1,), dtype=torch.int32, device=device),
         dst=torch.empty((T, k), dtype=torch.int32, device=device),
-        x_perm=torch.empty((cap, d), dtype=bf, device=device),
+        x_perm=torch.empty((0 if gather_a else cap, d), dtype=bf, device=device),
         h=torch.empty((cap, ff), dtype=bf, device=device),
         y=torch.empty((cap, d), dtype=bf, device=device),
         out=torch.empty((T, d), dtype=out_dtype, device=device),
         workspace=torch.empty((max(16, ops.permute_workspace_bytes(T, E)),), dtype=torch.uint8, device=device),
         router_ws=ops.router_workspace(T, E, device),
     )
+    if gather_a:
+        b.row_tokens = torch.empty((cap,), dtype=torch.int32, device=device)
     if shared_ff:
         b.shared_offsets = torch.tensor([0, T], dtype=torch.int32, device=device)
         b.shared_h = torch.empty((max(T, 1), shared_ff), dtype=bf, device=device)
@@ -105,9 +107,15 @@ class MoELayer:
     SHARED_SIDE_CTAS = 16
     # run_host_batches replays a captured step for batches up to this many tokens
     HOST_GRAPH_T_MAX = 8192
+    # prefill K3 reading its A rows from x by cp.async gathers (no x_perm copy,
+    # saves the T*k*d*2-byte x_perm buffer): bit-identical, but measured slower
+    # on B200 (C4 31.9 vs 30.8 ms, C2 154.8 vs 136.1 ms per step: the gathered
+    # stages keep the tensor pipe 73% busy vs 88% for TMA-fed x_perm tiles), so
+    # off by default; DESIGN.md §3 "Gather-fused A, round 2"
+    GATHER_A_DEFAULT = False
 
     def __init__(self, weights: LayerWeights, top_k: int, mode: str = "mixtral", tile_m: int = 1,
-                 out_dtype=torch.bfloat16):
+                 out_dtype=torch.bfloat16, gather_a: bool | None = None):
         if mode not in MODES:
             raise ValueError(f"mode must be one of {sorted(MODES)}")
         self.wts = weights
@@ -116,6 +124,11 @@ class MoELayer:
         self.mode = MODES[mode]
         self.tile_m = int(tile_m)
         self.out_dtype = out_dtype
+        # prefill K3 gathers its A rows from x (cp.async) instead of a
+        # materialised x_perm: the permute writes indices only
+        self.gather_a = self.GATHER_A_DEFAULT if gather_a is None else bool(gather_a)
+        if self.gather_a and self.tile_m != 1:
+            raise ValueError("gather_a needs tile_m == 1")
         self.E = weights.num_experts
         self.d = weights.hidden_dim
         self.ff = weights.expert_dim
@@ -147,7 +160,8 @@ class MoELayer:
         if T is not None and self.uses_small_path(T):
             # router + permute (rows materialised) + one launch for K3/K4/shared/combine
             return 1 + perm + 1 + (1 if self.out_dtype != torch.bfloat16 else 0)
-        return 1 + perm + 2 + 1 + (2 if self.shared_ff else 0)
+        # prefill: the gather path drops the permute's row copy
+        return 1 + perm - (1 if self.gather_a else 0) + 2 + 1 + (2 if self.shared_ff else 0)
 
     # --- buffers ---------------------------------------------------------------
     def buffers(self, T: int, device) -> StageBuffers:
@@ -155,8 +169,9 @@ class MoELayer:
         if b is None:
             for t in [t for t in self._bufs if t not in self._pinned]:
                 del self._bufs[t]
+            gather = self.gather_a and not self.uses_small_path(T)
             b = alloc_buffers(T, self.d, self.ff, self.E, self.k, self.tile_m, device, self.out_dtype,
-                              self.shared_ff)
+                              self.shared_ff, gather_a=gather)
             if self.uses_small_path(T):
                 b.row_tokens = torch.empty((b.h.shape[0],), dtype=torch.int32, device=device)
             if self.uses_dense_decode(T):
@@ -177,16 +192,26 @@ class MoELayer:
         self._router(x, b)
         self._permute(x, b)
 
+    def _gathers(self, b: StageBuffers) -> bool:
+        return b.x_perm.shape[0] == 0  # prefill buffers of a gather_a layer
+
     def _permute(self, x: torch.Tensor, b: StageBuffers):
         ops.permute(b.idx, x, self.E, self.tile_m, out=(b.offsets, b.dst, b.x_perm), workspace=b.workspace,
-                    row_tokens=b.row_tokens)
+                    row_tokens=b.row_tokens, copy_rows=not self._gathers(b))
+        self._x = x  # the gather K3 reads the permuted rows straight from the step's input
+
+    def _swiglu(self, b: StageBuffers, groups, w13, max_ctas: int = 0):
+        if self._gathers(b):
+            ops.grouped_swiglu_gather(self._x, b.row_tokens, b.offsets, groups, w13, self.ff, b.h, max_ctas=max_ctas)
+        else:
+            ops.grouped_swiglu(b.x_perm, b.offsets, groups, w13, self.ff, h=b.h, max_ctas=max_ctas)
 
     def experts(self, b: StageBuffers, groups=None, w13=None, w2=None):
         groups = self.groups if groups is None else groups
         pe = self.profile_events
         if pe:
             pe["k3"][0].record()
-        ops.grouped_swiglu(b.x_perm, b.offsets, groups, self.w13_list if w13 is None else w13, self.ff, h=b.h)
+        self._swiglu(b, groups, self.w13_list if w13 is None else w13)
         if pe:
             pe["k3"][1].record()
             pe["k4"][0].record()
@@ -241,7 +266,7 @@ class MoELayer:
                 self.shared_expert(x, b, max_ctas=self.SHARED_SIDE_CTAS)
             self.route(x, b)
             rest = -(-(148 - self.SHARED_SIDE_CTAS) // 2) * 2
-            ops.grouped_swiglu(b.x_perm, b.offsets, self.groups, self.w13_list, self.ff, h=b.h, max_ctas=rest)
+            self._swiglu(b, self.groups, self.w13_list, max_ctas=rest)
             ops.grouped_down(b.h, b.offsets, self.groups, self.w2_list, self.d, y=b.y, max_ctas=rest)
             main.wait_stream(side)
             return self.finish(b, b.shared_y, out)
@@ -328,7 +353,7 @@ class MoELayer:
             xs = x[s0:s0 + m_tokens]
             n = xs.shape[0]
             if n not in subs:
-                subs[n] = MoELayer(self.wts, self.k, self.mode_name, self.tile_m, self.out_dtype)
+                subs[n] = MoELayer(self.wts, self.k, self.mode_name, self.tile_m, self.out_dtype, self.gather_a)
             subs[n].forward(xs, out=out[s0:s0 + n])
         return out
 
@@ -398,7 +423,7 @@ class MoELayer:
             self._ffn_small(x, b, b.out)
             ev[3].record()
             return span(["router", "permute", "expert_ffn_k3k4_shared_combine"], 3)
-        ops.grouped_swiglu(b.x_perm, b.offsets, self.groups, self.w13_list, self.ff, h=b.h)
+        self._swiglu(b, self.groups, self.w13_list)
         ev[3].record()
         ops.grouped_down(b.h, b.offsets, self.groups, self.w2_list, self.d, y=b.y)
         ev[4].record()

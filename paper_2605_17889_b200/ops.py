@@ -156,6 +156,31 @@ def grouped_swiglu(x_perm: torch.Tensor, offsets: torch.Tensor, group_experts: S
     return h
 
 
+def grouped_swiglu_gather(x: torch.Tensor, row_tokens: torch.Tensor, offsets: torch.Tensor,
+                          group_experts: Sequence[int], w13: Sequence[torch.Tensor], ff: int, h: torch.Tensor,
+                          stream=None, max_ctas: int = 0):
+    """K3 with the permuted rows gathered from x: h[r] = SwiGLU_e(x[row_tokens[r]]) —
+    the same bits as grouped_swiglu on x_perm, without the permute's row copy."""
+    _need(x, "x", _BF16, 2)
+    _need(row_tokens, "row_tokens", torch.int32, 1)
+    _need(offsets, "offsets", torch.int32, 1)
+    _need(h, "h", _BF16, 2)
+    T, d = x.shape
+    for i, w in enumerate(w13):
+        _need(w, f"w13[{i}]", _BF16, 2)
+        if tuple(w.shape) != (2 * ff, d):
+            raise ValueError(f"w13[{i}] must be [2*ff, d] = [{2 * ff}, {d}]")
+    if len(w13) != len(group_experts):
+        raise ValueError("one weight per group")
+    if h.shape[1] != ff or h.shape[0] > row_tokens.numel():
+        raise ValueError("h must be [rows, ff] with a row_tokens entry per row")
+    L = _lib.lib()
+    _lib.check(L.cox_grouped_swiglu_gather(x.data_ptr(), T, row_tokens.data_ptr(), offsets.data_ptr(),
+                                           offsets.numel() - 1, len(group_experts), _ids(group_experts), _ptrs(w13),
+                                           d, ff, h.data_ptr(), max_ctas, _stream(stream)), "cox_grouped_swiglu_gather")
+    return h
+
+
 def grouped_down(h: torch.Tensor, offsets: torch.Tensor, group_experts: Sequence[int], w2: Sequence[torch.Tensor],
                  d: int, y: torch.Tensor | None = None, stream=None, max_ctas: int = 0):
     """K4: y[r] = h[r] W2_e^T for the listed groups."""

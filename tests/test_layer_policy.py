@@ -25,7 +25,10 @@ def test_decode_path_selection(c4_layer):
     assert L.launches_per_step(32) == 1
     assert L.launches_per_step(64) == 2  # router, then FFN + combine straight from the router's idx
     assert L.launches_per_step(65) == 1 + 2 + 1  # router, permute (index kernel + row copy), one FFN launch
+    # prefill: router, permute (hist, scan, scatter, row copy), K3, K4, combine, shared x2
     assert L.launches_per_step(262144) == 1 + 3 + 1 + 2 + 1 + 2
+    G = MoELayer(L.wts, L.k, L.mode_name, gather_a=True)
+    assert G.launches_per_step(262144) == 1 + 3 + 2 + 1 + 2  # K3 gathers the rows: no copy launch
 
 
 def test_dense_decode_needs_bf16_router_and_output():

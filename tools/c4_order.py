@@ -29,7 +29,7 @@ def serial(layer, x, b, ev=None):
     mark(1)
     layer._permute(x, b)
     mark(2)
-    ops.grouped_swiglu(b.x_perm, b.offsets, layer.groups, layer.w13_list, layer.ff, h=b.h)
+    layer._swiglu(b, layer.groups, layer.w13_list)
     mark(3)
     ops.grouped_down(b.h, b.offsets, layer.groups, layer.w2_list, layer.d, y=b.y)
     mark(4)
@@ -77,23 +77,23 @@ def main():
 
 
 
-def ablate(rounds=3, steps=10, config="C4"):
+def ablate(rounds=3, steps=10, config="C4", gather=None):
     """What-if: step time with a stage left out (its outputs stale from an earlier
     step), to measure what each non-GEMM stage costs inside the power-capped step."""
     shapes = {"C4": (64 * 4096, 2048, 1408, 64, 6, "deepseek", 2816), "C2": (64 * 4096, 4096, 14336, 8, 2, "mixtral", 0)}
     T, d, ff, E, k, mode, sff = shapes[config]
     wts = make_layer_weights(E, d, ff, seed=0, device="cuda", shared_ff=sff)
     x = make_tokens(T, d, seed=1, device="cuda")
-    layer = MoELayer(wts, k, mode)
+    layer = MoELayer(wts, k, mode, gather_a=gather)
     b = layer.buffers(T, x.device)
+    layer._permute(x, b)
 
     def run(skip):
         if "router" not in skip:
             layer._router(x, b)
         if "permute" not in skip:
             layer._permute(x, b)
-        ops.grouped_swiglu(b.x_perm, b.offsets, layer.groups, layer.w13_list, layer.ff, h=b.h)
-        ops.grouped_down(b.h, b.offsets, layer.groups, layer.w2_list, layer.d, y=b.y)
+        layer.experts(b)
         sh = layer.shared_expert(x, b)
         if "combine" not in skip:
             ops.combine(b.y, b.dst, b.w, sh, out=b.out)
@@ -113,11 +113,60 @@ def ablate(rounds=3, steps=10, config="C4"):
             torch.cuda.synchronize()
             res[n].append(a.elapsed_time(z) / steps)
     for n, v in res.items():
-        print(f"{config} {n:9s} ms/step " + " ".join(f"{t:.3f}" for t in v), flush=True)
+        print(f"{config}{' gather' if layer.gather_a else ' x_perm'} {n:9s} ms/step " + " ".join(f"{t:.3f}" for t in v),
+              flush=True)
+
+
+def beside_sweep(rounds=3, steps=10):
+    """C4: the shared experts on a side stream beside the router/permute, with the
+    shared GEMMs limited to `max_ctas` SMs so that the HBM-bound permute keeps
+    some SMs; serial order as the reference."""
+    T, d, ff, E, k, sff = 64 * 4096, 2048, 1408, 64, 6, 2816
+    wts = make_layer_weights(E, d, ff, seed=0, device="cuda", shared_ff=sff)
+    x = make_tokens(T, d, seed=1, device="cuda")
+    layer = MoELayer(wts, k, "deepseek")
+    b = layer.buffers(T, x.device)
+    main = torch.cuda.current_stream()
+    side = torch.cuda.Stream()
+
+    def beside(mc, early):
+        if not early:
+            layer._router(x, b)
+        side.wait_stream(main)
+        with torch.cuda.stream(side):
+            sh = layer.shared_expert(x, b, max_ctas=mc)
+        if early:
+            layer._router(x, b)
+        layer._permute(x, b)
+        layer.experts(b)
+        main.wait_stream(side)
+        ops.combine(b.y, b.dst, b.w, sh, out=b.out)
+    variants = {"serial": lambda: serial(layer, x, b)}
+    for mc in (0, 128, 112, 96):
+        variants[f"beside{mc}"] = (lambda mc=mc: beside(mc, False))
+        variants[f"early{mc}"] = (lambda mc=mc: beside(mc, True))
+    for f in variants.values():
+        f()
+    torch.cuda.synchronize()
+    res = {n: [] for n in variants}
+    for r in range(rounds):
+        for n, f in variants.items():
+            a, z = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            for _ in range(steps):
+                f()
+            z.record()
+            torch.cuda.synchronize()
+            res[n].append(a.elapsed_time(z) / steps)
+    for n, v in res.items():
+        print(f"C4 {n:10s} ms/step " + " ".join(f"{t:.3f}" for t in v), flush=True)
 
 
 if __name__ == "__main__":
-    if len(sys.argv) > 1 and sys.argv[1] == "ablate":
-        ablate(config=sys.argv[2] if len(sys.argv) > 2 else "C4")
+    if len(sys.argv) > 1 and sys.argv[1] == "beside":
+        beside_sweep()
+    elif len(sys.argv) > 1 and sys.argv[1] == "ablate":
+        ablate(config=sys.argv[2] if len(sys.argv) > 2 else "C4",
+               gather={"gather": True, "xperm": False}.get(sys.argv[3]) if len(sys.argv) > 3 else None)
     else:
         main()
