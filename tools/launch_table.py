@@ -12,7 +12,7 @@ tot = 0.0
 for k, v in sorted(by.items()):
     t = float(v.get("gpu__time_duration.sum", "0").replace(",", ""))
     tot += t
-    extra = v.get("sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed", "")
+    extra = v.get("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed", v.get("sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed", ""))
     print(f"{k:3d} {v['k'][:60]:60s} {t / 1e3:9.1f} us  rd {float(v.get('dram__bytes_read.sum', '0')) / 1e9:7.3f} GB"
           f"  wr {float(v.get('dram__bytes_write.sum', '0')) / 1e9:7.3f} GB  {extra}")
 print(f"total {tot / 1e6:.3f} ms")
