@@ -1,13 +1,15 @@
 """Time the prefill layer with K3 on materialised x_perm vs K3 gathering its A
 rows from x (MoELayer(gather_a=True)), interleaved, CUDA events, steady state.
-The gather split (rows by cp.async vs TMA tile::gather4) is COX_GATHER_CP_WAVES
-(read once per process), so sweep it with one process per value:
 
-    for w in 8 6 5 4; do COX_GATHER_CP_WAVES=$w python tools/gather_sweep.py C4; done
+    python tools/gather_sweep.py C4|C2|C3L
+
+Measured (round 2): a hybrid that moved part of each CTA's A rows to TMA
+tile::gather4 was slower the more rows the TMA took (C4: 34.0 ms with all rows
+by cp.async, 37.4 with 3/8 by gather4, 55.3 with all by gather4, vs 30.3 on
+x_perm), so the library gathers by cp.async only.
 """
 from __future__ import annotations
 
-import os
 import sys
 from pathlib import Path
 
@@ -42,8 +44,7 @@ def main():
             z.record()
             torch.cuda.synchronize()
             res[n].append(a.elapsed_time(z) / steps)
-    w = os.environ.get("COX_GATHER_CP_WAVES", "6 (default)")
-    print(f"{cfg} cp_waves={w} outputs bit-identical: {same}  " +
+    print(f"{cfg} outputs bit-identical: {same}  " +
           "  ".join(f"{n} " + " ".join(f"{t:.2f}" for t in v) + " ms" for n, v in res.items()), flush=True)
 
 
