@@ -79,6 +79,14 @@ def main():
     wg64 = (torch.rand(64, 256, device=dev) * 2 - 1).to(torch.bfloat16) / 16
     ops.router_topk(make_tokens(148 * 128 + 9, 256, device=dev), wg64, 6, 1)
     torch.cuda.synchronize()
+    # K3 gather mode (A rows by cp.async from x), incl. partial tiles and shared experts
+    for (T, d, ff, E, k, mode, shared) in [(3000, 256, 128, 8, 2, "mixtral", 0), (2500, 512, 256, 16, 4, "deepseek", 256)]:
+        wts = make_layer_weights(E, d, ff, seed=4, device=dev, shared_ff=shared)
+        x = make_tokens(T, d, seed=5, device=dev)
+        a = MoELayer(wts, k, mode, gather_a=True)(x)
+        b = MoELayer(wts, k, mode, gather_a=False)(x)
+        torch.cuda.synchronize()
+        assert torch.equal(a, b)
     print("sanitize run ok")
 
 
