@@ -33,7 +33,7 @@ EXPORTS = (
     "cox_small_expert_ffn", "cox_small_expert_ffn_idx", "cox_decode_moe", "cox_combine", "cox_ep_counts_put",
     "cox_ep_offsets", "cox_ep_dispatch", "cox_ep_combine", "cox_interleave_w13", "cox_fetch_experts",
 )
-ABI_VERSION = 2
+ABI_VERSION = 3
 
 _lock = threading.Lock()
 _lib = None

@@ -98,7 +98,7 @@ extern "C" {
 
 const char* cox_last_error(void) { return g_err.c_str(); }
 
-int cox_version(void) { return 2; }
+int cox_version(void) { return 3; }
 
 int cox_device_check(void) {
   int dev = 0, major = 0, minor = 0;

@@ -21,7 +21,7 @@ def test_library_exports_all_symbols():
     L = _lib.load()
     for name in header_symbols():
         assert hasattr(L, name), name
-    assert L.cox_version() == _lib.ABI_VERSION == 2
+    assert L.cox_version() == _lib.ABI_VERSION == 3
 
 
 def test_workspace_query_is_host_only():
