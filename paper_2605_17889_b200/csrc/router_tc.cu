@@ -284,7 +284,7 @@ COX_DEV uint4 ldg_v4(const void* p) { return __ldg(reinterpret_cast<const uint4*
 // NCH = x chunks per lane held in registers (d <= 256 NCH): the token's whole
 // x row is requested at once, so a token costs one DRAM round trip.
 template <int NCH, int NE>
-__global__ void __launch_bounds__(RR_WARPS * 32, NCH <= 8 ? 3 : 1) router_rescore_kernel(
+__global__ void __launch_bounds__(RR_WARPS * 32, NCH <= 8 ? 2 : 1) router_rescore_kernel(
     const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ wg, const float* __restrict__ approx,
     const float* __restrict__ margin, int T, int d, int E, int k, int mode, int32_t* __restrict__ idx,
     float* __restrict__ wout, int32_t* __restrict__ counts) {
@@ -298,20 +298,40 @@ __global__ void __launch_bounds__(RR_WARPS * 32, NCH <= 8 ? 3 : 1) router_rescor
   __syncthreads();
   float* lg = s_l[warp];
   uint8_t* cand = s_cand[warp];
-  for (long long t = (long long)blockIdx.x * RR_WARPS + warp; t < T; t += (long long)gridDim.x * RR_WARPS) {
-    const __nv_bfloat16* xr = x + t * d;
-    uint4 xq[NCH];
+  // the next token's x row, screened logits and margin are requested while
+  // the current token is scored (one DRAM round trip hidden per token)
+  const long long tstep = (long long)gridDim.x * RR_WARPS;
+  long long t = (long long)blockIdx.x * RR_WARPS + warp;
+  uint4 xn[NCH];
+  float an[NE], mn = 0.f;
+  auto fetch = [&](long long tt) {
+    if (tt >= T) return;
 #pragma unroll
     for (int j = 0; j < NCH; ++j) {
       const int s = 8 * lane + 256 * j;
-      xq[j] = s < d ? ld_nc_v4(xr + s) : make_uint4(0, 0, 0, 0);
+      xn[j] = s < d ? ld_nc_v4(x + tt * d + s) : make_uint4(0, 0, 0, 0);
     }
+#pragma unroll
+    for (int i = 0; i < NE; ++i) {
+      const int e = lane + 32 * i;
+      an[i] = e < E ? approx[tt * E + e] : -INFINITY;
+    }
+    mn = margin[tt];
+  };
+  fetch(t);
+  for (; t < T; t += tstep) {
+    uint4 xq[NCH];
     float av[NE];
+#pragma unroll
+    for (int j = 0; j < NCH; ++j) xq[j] = xn[j];
+#pragma unroll
+    for (int i = 0; i < NE; ++i) av[i] = an[i];
+    const float mt = mn;
+    fetch(t + tstep);
     uint32_t key[NE];
 #pragma unroll
     for (int i = 0; i < NE; ++i) {
       const int e = lane + 32 * i;
-      av[i] = e < E ? approx[t * E + e] : -INFINITY;
       av[i] = av[i] != av[i] ? -INFINITY : av[i];  // NaN ranks like -inf (router.cu nan_low)
       if (e < E) lg[e] = av[i];
       key[i] = e < E ? route_key(av[i]) : 0u;
@@ -329,7 +349,7 @@ __global__ void __launch_bounds__(RR_WARPS * 32, NCH <= 8 ? 3 : 1) router_rescor
         if (key[i] == mk) key[i] = 0;
     }
     const float kth = __uint_as_float((mk & 0x80000000u) ? (mk & 0x7fffffffu) : ~mk);
-    const float thr = kth - 2.0f * margin[t];
+    const float thr = kth - 2.0f * mt;
     int nc = 0;
 #pragma unroll
     for (int i = 0; i < NE; ++i) {
