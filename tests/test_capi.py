@@ -48,6 +48,15 @@ def test_argument_validation_is_host_only():
     rc = L.cox_router_topk(4096, _lib.DTYPE_BF16, 4096, _lib.DTYPE_BF16, 64, 256, 8, 2, 0, 4096, 4096, 4096,
                            4096, 16, None)
     assert rc == _lib.COX_EINVAL and b"workspace" in L.cox_last_error()
+    # K3 gather mode: needs row_tokens, d % 64 == 0, expert ids inside [0, E)
+    ids[1] = 3
+    rc = L.cox_grouped_swiglu_gather(4096, 100, None, 4096, 8, 2, ids, ptrs, 256, 256, 4096, 0, None)
+    assert rc == _lib.COX_EINVAL and b"row_tokens" in L.cox_last_error()
+    rc = L.cox_grouped_swiglu_gather(4096, 100, 4096, 4096, 8, 2, ids, ptrs, 96, 256, 4096, 0, None)
+    assert rc == _lib.COX_EINVAL and b"d%64" in L.cox_last_error()
+    ids[1] = 9
+    rc = L.cox_grouped_swiglu_gather(4096, 100, 4096, 4096, 8, 2, ids, ptrs, 256, 256, 4096, 0, None)
+    assert rc == _lib.COX_EINVAL and b"outside [0, 8)" in L.cox_last_error()
 
 
 def test_sass_contains_tcgen05_and_tma():
@@ -60,4 +69,5 @@ def test_sass_contains_tcgen05_and_tma():
         pytest.skip("cuobjdump not available")
     sass = subprocess.run([exe, "-sass", str(_lib.LIB_PATH)], capture_output=True, text=True).stdout
     assert "UTCHMMA" in sass and "UTMALDG" in sass and "LDTM" in sass
+    assert "LDGSTS" in sass and "FHFMA" in sass  # K3 gather mode (cp.async), mixed-precision re-score FMAs
     assert "HMMA" not in sass.replace("UTCHMMA", "")  # no legacy mma.sync path
