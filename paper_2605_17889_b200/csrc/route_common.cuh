@@ -104,4 +104,15 @@ COX_DEV void warp_route_token(float* lg, int E, int k, int mode, int lane, int* 
   __syncwarp();
 }
 
+// warp_route_token with the key scan sized to E at run time (E is uniform
+// across the launch, so the branch is too): E <= 64 scans 2 registers per lane
+// per selection round instead of 8.
+COX_DEV void warp_route_token_e(float* lg, int E, int k, int mode, int lane, int* s_sel, float* s_selv, int32_t* idx,
+                                float* w, int* hist) {
+  if (E <= 32) warp_route_token<1>(lg, E, k, mode, lane, s_sel, s_selv, idx, w, hist);
+  else if (E <= 64) warp_route_token<2>(lg, E, k, mode, lane, s_sel, s_selv, idx, w, hist);
+  else if (E <= 128) warp_route_token<4>(lg, E, k, mode, lane, s_sel, s_selv, idx, w, hist);
+  else warp_route_token<8>(lg, E, k, mode, lane, s_sel, s_selv, idx, w, hist);
+}
+
 }  // namespace cox

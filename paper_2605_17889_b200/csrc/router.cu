@@ -146,7 +146,7 @@ router_topk_kernel(const XT* __restrict__ x, const WT* __restrict__ wg, int T, i
       const long t = tb0 + tl;
       if (t >= T) break;
       float* lg = s_logits + tl * E;
-      warp_route_token(lg, E, k, mode, lane, s_sel[warp], s_selv[warp], idx + t * k, wout + t * k, s_hist);
+      warp_route_token_e(lg, E, k, mode, lane, s_sel[warp], s_selv[warp], idx + t * k, wout + t * k, s_hist);
     }
     __syncthreads();
   }
@@ -253,7 +253,7 @@ router_topk_staged_kernel(const __nv_bfloat16* __restrict__ x, const float* __re
       const long t = tb0 + tl;
       if (t >= T) break;
       float* lg = s_logits + tl * E;
-      warp_route_token(lg, E, k, mode, lane, s_sel[warp], s_selv[warp], idx + t * k, wout + t * k, s_hist);
+      warp_route_token_e(lg, E, k, mode, lane, s_sel[warp], s_selv[warp], idx + t * k, wout + t * k, s_hist);
       __syncwarp();
     }
   }
@@ -359,7 +359,7 @@ router_topk_staged_bf16w_kernel(const __nv_bfloat16* __restrict__ x, const __nv_
       const long t = tb0 + tl;
       if (t >= T) break;
       float* lg = s_logits + tl * E;
-      warp_route_token(lg, E, k, mode, lane, s_sel[warp], s_selv[warp], idx + t * k, wout + t * k, s_hist);
+      warp_route_token_e(lg, E, k, mode, lane, s_sel[warp], s_selv[warp], idx + t * k, wout + t * k, s_hist);
       __syncwarp();
     }
   }
@@ -461,7 +461,7 @@ router_decode_kernel(const XT* __restrict__ x, const WT* __restrict__ wg, int T,
   // last block of token t: its top-k
   for (int e = lane; e < E; e += 32) lg[e] = __ldcg(g_logits + (long)t * E + e);
   __syncwarp();
-  warp_route_token(lg, E, k, mode, lane, s_sel, s_selv, idx + (long)t * k, wout + (long)t * k, nullptr);
+  warp_route_token_e(lg, E, k, mode, lane, s_sel, s_selv, idx + (long)t * k, wout + (long)t * k, nullptr);
   int last_tok = 0;
   if (lane == 0) last_tok = atom_add_acq_rel(g_cnt + RD_TMAX, 1) == T - 1;
   last_tok = __shfl_sync(0xffffffffu, last_tok, 0);

@@ -268,7 +268,7 @@ __global__ void __launch_bounds__(SG_THREADS, 1) small_ffn_kernel(const __grid_c
         }
       }
       __syncwarp();
-      warp_route_token(s_route, E, kk, p.mode, lane, reinterpret_cast<int*>(s_route + 264), s_route + 272,
+      warp_route_token_e(s_route, E, kk, p.mode, lane, reinterpret_cast<int*>(s_route + 264), s_route + 272,
                        p.ridx + t * kk, p.rw + t * kk, nullptr);
       if (lane == 0) red_release_add(p.counters + SG_ROUTED, 1);  // after idx / w / histogram
       __syncwarp();
