@@ -288,16 +288,94 @@ __global__ void __launch_bounds__(RR_WARPS * 32, NCH <= 8 ? 2 : 1) router_rescor
     const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ wg, const float* __restrict__ approx,
     const float* __restrict__ margin, int T, int d, int E, int k, int mode, int32_t* __restrict__ idx,
     float* __restrict__ wout, int32_t* __restrict__ counts) {
-  __shared__ float s_l[RR_WARPS][32 * NE];  // per warp: screened logits, exact for the candidates
+  // Tokens are scored one per warp (exact candidate logits need the whole
+  // warp's lanes: the canonical lane-chunk order), but the per-token top-k and
+  // softmax are serial work, so they run one token per LANE over a batch of
+  // TB tokens: per warp, TB logit rows (screened, exact for the candidates;
+  // pitch 32 NE + 1 so the lanes' row scans hit distinct banks) and each
+  // token's candidate bit mask.
+  constexpr int TB = 32 / NE < 4 ? 4 : 32 / NE;
+  constexpr int PITCH = 32 * NE + 1;
+  __shared__ float s_l[RR_WARPS][TB * PITCH];
+  __shared__ uint32_t s_mask[RR_WARPS][TB][NE];
+  __shared__ long long s_tok[RR_WARPS][TB];
   __shared__ uint8_t s_cand[RR_WARPS][32 * NE];
-  __shared__ int s_sel[RR_WARPS][8];
-  __shared__ float s_selv[RR_WARPS][8];
   __shared__ int s_hist[256];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int i = threadIdx.x; i < E; i += blockDim.x) s_hist[i] = 0;
   __syncthreads();
-  float* lg = s_l[warp];
   uint8_t* cand = s_cand[warp];
+  // lane b < nb selects and weighs batch token b (same operations, in the same
+  // order, as warp_route_token: largest value first, ties -> lower index; the
+  // top-k lies among the candidates, which hold exact logits)
+  auto finish_batch = [&](int nb) {
+    __syncwarp();
+    if (lane < nb) {
+      const float* lr = s_l[warp] + lane * PITCH;
+      const long long t = s_tok[warp][lane];
+      uint32_t msk[NE];
+      int nc = 0;
+#pragma unroll
+      for (int i = 0; i < NE; ++i) {
+        msk[i] = s_mask[warp][lane][i];
+        nc += __popc(msk[i]);
+      }
+      if (nc < k) {  // only with non-finite margins (no candidates): select among all E screened values
+#pragma unroll
+        for (int i = 0; i < NE; ++i) msk[i] = (32 * i + 32 <= E) ? 0xffffffffu : ((1u << (E - 32 * i)) - 1u);
+      }
+      int sel[8];
+      float selv[8];
+      uint32_t taken[NE];
+#pragma unroll
+      for (int i = 0; i < NE; ++i) taken[i] = 0u;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {  // k <= 8; unrolled so sel / selv stay in registers
+        sel[j] = 0;
+        selv[j] = 0.f;
+        if (j < k) {
+          int be = -1, bw = 0, bb = 0;
+          float bv = 0.f;
+#pragma unroll
+          for (int i = 0; i < NE; ++i) {
+            for (uint32_t m = msk[i] & ~taken[i]; m; m &= m - 1u) {  // ascending expert order
+              const int bit = __ffs(m) - 1;
+              const float v = lr[32 * i + bit];
+              if (be < 0 || v > bv) {
+                be = 32 * i + bit;
+                bv = v;
+                bw = i;
+                bb = bit;
+              }
+            }
+          }
+#pragma unroll
+          for (int i = 0; i < NE; ++i)
+            if (i == bw) taken[i] |= 1u << bb;
+          sel[j] = be;
+          selv[j] = bv;
+        }
+      }
+      const float m = selv[0];
+      float ssum = 0.0f;
+      if (mode == 0) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          if (j < k) ssum = __fadd_rn(ssum, expf(__fsub_rn(selv[j], m)));
+      } else {
+        for (int e = 0; e < E; ++e) ssum = __fadd_rn(ssum, expf(__fsub_rn(lr[e], m)));  // ascending e, as the oracle
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (j < k) {
+          idx[t * k + j] = sel[j];
+          wout[t * k + j] = __fdiv_rn(expf(__fsub_rn(selv[j], m)), ssum);
+          atomicAdd(&s_hist[sel[j]], 1);
+        }
+    }
+    __syncwarp();
+  };
+  int nb = 0;
   // the next token's x row, screened logits and margin are requested while
   // the current token is scored (one DRAM round trip hidden per token)
   const long long tstep = (long long)gridDim.x * RR_WARPS;
@@ -328,6 +406,7 @@ __global__ void __launch_bounds__(RR_WARPS * 32, NCH <= 8 ? 2 : 1) router_rescor
     for (int i = 0; i < NE; ++i) av[i] = an[i];
     const float mt = mn;
     fetch(t + tstep);
+    float* lg = s_l[warp] + nb * PITCH;
     uint32_t key[NE];
 #pragma unroll
     for (int i = 0; i < NE; ++i) {
@@ -358,7 +437,9 @@ __global__ void __launch_bounds__(RR_WARPS * 32, NCH <= 8 ? 2 : 1) router_rescor
       const uint32_t bal = __ballot_sync(0xffffffffu, c);
       if (c) cand[nc + __popc(bal & ((1u << lane) - 1u))] = (uint8_t)e;
       nc += __popc(bal);
+      if (lane == 0) s_mask[warp][nb][i] = bal;
     }
+    if (lane == 0) s_tok[warp][nb] = t;
     __syncwarp();
     // candidates RR_CH at a time (a runtime loop: only real candidates cost
     // FMAs; a short last group runs beside discarded duplicates)
@@ -398,9 +479,12 @@ __global__ void __launch_bounds__(RR_WARPS * 32, NCH <= 8 ? 2 : 1) router_rescor
       const int u = lane >> 4;
       if ((lane & 15) == 0 && c + u < nc) lg[cand[c + u]] = r != r ? -INFINITY : r;
     }
-    __syncwarp();
-    warp_route_token<NE>(lg, E, k, mode, lane, s_sel[warp], s_selv[warp], idx + t * k, wout + t * k, s_hist);
+    if (++nb == TB) {
+      finish_batch(nb);
+      nb = 0;
+    }
   }
+  if (nb) finish_batch(nb);
   __syncthreads();
   for (int i = threadIdx.x; i < E; i += blockDim.x)
     if (s_hist[i]) atomicAdd(&counts[i], s_hist[i]);
@@ -452,8 +536,8 @@ int launch_router_tc(const void* x, const void* wg, int T, int d, int E, int k, 
 #define RR_LAUNCH(NCH_, NE_)                                                                                     \
   do {                                                                                                           \
     static bool carve = false;                                                                                   \
-    if (!carve) { /* data flows through L1: keep the L1 share large */                                           \
-      cudaFuncSetAttribute(router_rescore_kernel<NCH_, NE_>, cudaFuncAttributePreferredSharedMemoryCarveout, 10); \
+    if (!carve) { /* router rows flow through L1: the smallest carveout that fits 2 CTAs (~37 KB each) */          \
+      cudaFuncSetAttribute(router_rescore_kernel<NCH_, NE_>, cudaFuncAttributePreferredSharedMemoryCarveout, 40); \
       carve = true;                                                                                              \
     }                                                                                                            \
     router_rescore_kernel<NCH_, NE_><<<(int)blocks, RR_WARPS * 32, 0, s>>>(                                      \
