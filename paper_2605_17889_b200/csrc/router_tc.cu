@@ -38,7 +38,7 @@ int get_map(CUtensorMap* out, const void* ptr, unsigned long long rows, unsigned
 
 constexpr int RC_BM = 128;  // tokens per tile (MMA M, TMEM lanes)
 constexpr int RC_BK = 64;   // K per stage: one 128-byte swizzle atom
-constexpr int RC_STAGES = 4;
+constexpr int RC_MAX_STAGES = 8;  // ring depth: as many 64-column stages as fit ~200 KB (8 at E <= 64)
 constexpr int RC_THREADS = 256;
 constexpr uint32_t RC_A_BYTES = RC_BM * RC_BK * 2;  // 16 KB
 
@@ -51,8 +51,14 @@ struct RcParams {
   float gamma;
 };
 
+__host__ __device__ constexpr int rc_stages(int Epad) {
+  return (int)(200u * 1024u / (RC_A_BYTES + (uint32_t)Epad * 128u)) > RC_MAX_STAGES
+             ? RC_MAX_STAGES
+             : (int)(200u * 1024u / (RC_A_BYTES + (uint32_t)Epad * 128u));
+}
+
 constexpr size_t rc_smem_bytes(int Epad) {
-  return 1024 + (size_t)RC_STAGES * (RC_A_BYTES + (size_t)Epad * 128) + 1024 + 2 * RC_BM * 4 + 256 * 4 + 64;
+  return 1024 + (size_t)rc_stages(Epad) * (RC_A_BYTES + (size_t)Epad * 128) + 1024 + 2 * RC_BM * 4 + 256 * 4 + 64;
 }
 
 COX_DEV float bf16_abs_max8(const uint4& v, float m) {
@@ -79,6 +85,7 @@ __global__ void __launch_bounds__(RC_THREADS, 1) router_screen_kernel(const __gr
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const uint32_t B_BYTES = (uint32_t)p.Epad * 128;
   uint8_t* sA = smem;
+  const int RC_STAGES = rc_stages(p.Epad);
   uint8_t* sB = smem + RC_STAGES * RC_A_BYTES;
   uint64_t* full = reinterpret_cast<uint64_t*>(sB + RC_STAGES * B_BYTES);
   uint64_t* empty = full + RC_STAGES;
