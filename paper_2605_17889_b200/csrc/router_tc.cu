@@ -290,7 +290,7 @@ COX_DEV uint4 ldg_v4(const void* p) { return __ldg(reinterpret_cast<const uint4*
 
 // NCH = x chunks per lane held in registers (d <= 256 NCH): the token's whole
 // x row is requested at once, so a token costs one DRAM round trip.
-template <int NCH, int NE>
+template <int NCH, int NE, bool FULL>
 __global__ void __launch_bounds__(RR_WARPS * 32, NCH <= 8 ? 2 : 1) router_rescore_kernel(
     const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ wg, const float* __restrict__ approx,
     const float* __restrict__ margin, int T, int d, int E, int k, int mode, int32_t* __restrict__ idx,
@@ -394,7 +394,7 @@ __global__ void __launch_bounds__(RR_WARPS * 32, NCH <= 8 ? 2 : 1) router_rescor
 #pragma unroll
     for (int j = 0; j < NCH; ++j) {
       const int s = 8 * lane + 256 * j;
-      xn[j] = s < d ? ld_nc_v4(x + tt * d + s) : make_uint4(0, 0, 0, 0);
+      xn[j] = (FULL || s < d) ? ld_nc_v4(x + tt * d + s) : make_uint4(0, 0, 0, 0);
     }
 #pragma unroll
     for (int i = 0; i < NE; ++i) {
@@ -460,7 +460,7 @@ __global__ void __launch_bounds__(RR_WARPS * 32, NCH <= 8 ? 2 : 1) router_rescor
       }
 #pragma unroll
       for (int j = 0; j < NCH; ++j) {
-        if (8 * lane + 256 * j < d) {
+        if (FULL || 8 * lane + 256 * j < d) {  // FULL: d == 256 NCH, every lane owns NCH chunks
           uint4 p[RR_CH];
 #pragma unroll
           for (int u = 0; u < RR_CH; ++u) p[u] = ldg_v4(wr[u] + 256 * j);
@@ -540,16 +540,22 @@ int launch_router_tc(const void* x, const void* wg, int T, int d, int E, int k, 
   router_screen_kernel<<<grid, RC_THREADS, smem, s>>>(p);
   long long blocks = ((long long)T + RR_WARPS - 1) / RR_WARPS;
   if (blocks > (long long)num_sms * 8) blocks = (long long)num_sms * 8;
-#define RR_LAUNCH(NCH_, NE_)                                                                                     \
-  do {                                                                                                           \
-    static bool carve = false;                                                                                   \
+#define RR_LAUNCH3(NCH_, NE_, F_)                                                                                 \
+  do {                                                                                                             \
+    static bool carve = false;                                                                                     \
     if (!carve) { /* router rows flow through L1: the smallest carveout that fits 2 CTAs (~37 KB each) */          \
-      cudaFuncSetAttribute(router_rescore_kernel<NCH_, NE_>, cudaFuncAttributePreferredSharedMemoryCarveout, 40); \
-      carve = true;                                                                                              \
-    }                                                                                                            \
-    router_rescore_kernel<NCH_, NE_><<<(int)blocks, RR_WARPS * 32, 0, s>>>(                                      \
-        static_cast<const __nv_bfloat16*>(x), static_cast<const __nv_bfloat16*>(wg), p.approx, p.margin, T, d, E, \
-        k, mode, idx, w, counts);                                                                                \
+      cudaFuncSetAttribute(router_rescore_kernel<NCH_, NE_, F_>, cudaFuncAttributePreferredSharedMemoryCarveout,   \
+                           40);                                                                                    \
+      carve = true;                                                                                                \
+    }                                                                                                              \
+    router_rescore_kernel<NCH_, NE_, F_><<<(int)blocks, RR_WARPS * 32, 0, s>>>(                                    \
+        static_cast<const __nv_bfloat16*>(x), static_cast<const __nv_bfloat16*>(wg), p.approx, p.margin, T, d, E,   \
+        k, mode, idx, w, counts);                                                                                  \
+  } while (0)
+#define RR_LAUNCH(NCH_, NE_)                       \
+  do {                                             \
+    if (d == 256 * (NCH_)) RR_LAUNCH3(NCH_, NE_, true); \
+    else RR_LAUNCH3(NCH_, NE_, false);             \
   } while (0)
 #define RR_BY_NE(NCH_)                          \
   do {                                          \
@@ -566,6 +572,7 @@ int launch_router_tc(const void* x, const void* wg, int T, int d, int E, int k, 
   else return -3;
 #undef RR_BY_NE
 #undef RR_LAUNCH
+#undef RR_LAUNCH3
   return launch_status();
 }
 
