@@ -459,9 +459,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GM_THREADS + (GATHER
 #pragma unroll 1
         for (int cc = 0; cc < (GM_BN / 2) / 32; ++cc) {
           uint32_t gr[32], ur[32];
-          tmem_ld_32x32b_x32(tbase + cc * 32, gr);
-          tmem_ld_32x32b_x32(tbase + (GM_BN / 2) + cc * 32, ur);
-          tmem_ld_wait();
+          tmem_ld2_32x32b_x32(tbase + cc * 32, gr, tbase + (GM_BN / 2) + cc * 32, ur);
           uint32_t pk[16];
 #pragma unroll
           for (int q = 0; q < 16; ++q) {
@@ -479,7 +477,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GM_THREADS + (GATHER
         for (int cc = 0; cc < GM_BN / 32; ++cc) {
           uint32_t r[32];
           tmem_ld_32x32b_x32(tbase + cc * 32, r);
-          tmem_ld_wait();
           uint32_t pk[16];
 #pragma unroll
           for (int q = 0; q < 16; ++q) pk[q] = pack_bf16x2(__uint_as_float(r[2 * q]), __uint_as_float(r[2 * q + 1]));

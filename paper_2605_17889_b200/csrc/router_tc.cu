@@ -244,7 +244,6 @@ __global__ void __launch_bounds__(RC_THREADS, 1) router_screen_kernel(const __gr
       for (int c0 = 0; c0 < p.E; c0 += 32) {
         uint32_t v[32];
         tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * acc_stride + c0, v);
-        tmem_ld_wait();
         if (t < p.T) {
           const int n = min(32, p.E - c0);
           if ((p.E & 3) == 0) {
@@ -252,7 +251,9 @@ __global__ void __launch_bounds__(RC_THREADS, 1) router_screen_kernel(const __gr
             for (int j = 0; j < 32; j += 4)
               if (j < n) st_global_v4(dst + c0 + j, v[j], v[j + 1], v[j + 2], v[j + 3]);
           } else {
-            for (int j = 0; j < n; ++j) dst[c0 + j] = __uint_as_float(v[j]);
+#pragma unroll
+            for (int j = 0; j < 32; ++j)  // static indices: v stays in registers
+              if (j < n) dst[c0 + j] = __uint_as_float(v[j]);
           }
         }
       }

@@ -654,7 +654,6 @@ __global__ void __launch_bounds__(SG_THREADS, 1) small_ffn_kernel(const __grid_c
         for (int c32 = 0; c32 < nrem; c32 += 32) {
           uint32_t v[32];
           tmem_ld_32x32b_x32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * SG_NMAX + c32, v);
-          tmem_ld_wait();
 #pragma unroll
           for (int j = 0; j < 32; ++j) stg[r * SG_PITCH + j] = __uint_as_float(v[j]);
           named_bar_epi();
