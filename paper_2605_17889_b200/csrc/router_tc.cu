@@ -51,10 +51,11 @@ struct RcParams {
   float gamma;
 };
 
+// two CTAs per SM, each with ~100 KB of ring (latency hiding from 16 warps)
 __host__ __device__ constexpr int rc_stages(int Epad) {
-  return (int)(200u * 1024u / (RC_A_BYTES + (uint32_t)Epad * 128u)) > RC_MAX_STAGES
+  return (int)(100u * 1024u / (RC_A_BYTES + (uint32_t)Epad * 128u)) > RC_MAX_STAGES
              ? RC_MAX_STAGES
-             : (int)(200u * 1024u / (RC_A_BYTES + (uint32_t)Epad * 128u));
+             : (int)(100u * 1024u / (RC_A_BYTES + (uint32_t)Epad * 128u));
 }
 
 constexpr size_t rc_smem_bytes(int Epad) {
@@ -80,7 +81,7 @@ COX_DEV float bf16_abs_sum8(const uint4& v, float s) {
   return s;
 }
 
-__global__ void __launch_bounds__(RC_THREADS, 1) router_screen_kernel(const __grid_constant__ RcParams p) {
+__global__ void __launch_bounds__(RC_THREADS, 2) router_screen_kernel(const __grid_constant__ RcParams p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const uint32_t B_BYTES = (uint32_t)p.Epad * 128;
@@ -531,12 +532,16 @@ int launch_router_tc(const void* x, const void* wg, int T, int d, int E, int k, 
     cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev);
   }
   const int ntiles = (T + RC_BM - 1) / RC_BM;
-  const int grid = ntiles < num_sms ? ntiles : num_sms;
+  const int grid = ntiles < 2 * num_sms ? ntiles : 2 * num_sms;
   const size_t smem = rc_smem_bytes(Epad);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(router_screen_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rc_smem_bytes(256));
-    attr = true;
+  // the ring depth depends on E, so the largest footprint is not at E = 256:
+  // raise the kernel's dynamic shared-memory limit whenever a launch needs more
+  static size_t attr_bytes = 0;
+  if (smem > attr_bytes) {
+    if (cudaFuncSetAttribute(router_screen_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+        cudaSuccess)
+      return -2;
+    attr_bytes = smem;
   }
   router_screen_kernel<<<grid, RC_THREADS, smem, s>>>(p);
   long long blocks = ((long long)T + RR_WARPS - 1) / RR_WARPS;
