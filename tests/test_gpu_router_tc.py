@@ -43,6 +43,9 @@ def _check(x, wg, k, mode, wtol):
     (4096, 40, 2, 0),    # E not a multiple of 16, C2-sized rows
     (1024, 36, 3, 1),
     (512, 160, 8, 0),
+    (1024, 96, 4, 1),    # the screen's largest ring footprint (E in (80, 96])
+    (768, 256, 8, 1),    # widest E: 32-column router tiles, 4-stage ring
+    (4096, 32, 2, 1),    # narrowest E: 8-stage ring, NCH = 16 re-score
 ])
 def test_tc_router_bitexact_indices(d, E, k, mode):
     x = make_tokens(T_TC, d, seed=11, device=DEV)
