@@ -107,24 +107,13 @@ int cox_grouped_swiglu(const void* x_perm, long long rows_cap, const int32_t* of
  * [T*k]: the source token of every permuted row (cox_permute with x_perm ==
  * NULL writes it, with offsets and dst and no row copy).  Four extra warps per
  * CTA fill the A stages by cp.async in the 128B-swizzled layout the tensor
- * core reads; B (the weights) still streams by TMA.  Half mode
- * (x_perm_half != NULL, [rows_cap, d]): the first 64 of every 128 rows of a
- * segment are read from x_perm_half by TMA (cox_permute_half materialises only
- * those) and the other 64 are gathered, halving both the permute's writes and
- * the cp.async traffic.  Replaces the permute's row copy (T*k*d*2 bytes
- * written, or half of it) in the reference's expert:dispatch step
- * (sim.py:149-202, costmodel.py:266-273).  d % 64 == 0, ff % 128 == 0. */
-int cox_grouped_swiglu_gather(const void* x, long long T, const int32_t* row_tokens, const void* x_perm_half,
-                              long long rows_cap, const int32_t* offsets, int E, int n_groups,
-                              const int32_t* group_experts, const void* const* w13, int d, int ff, void* h,
-                              int max_ctas, void* stream);
-
-/* cox_permute (tile_m = 1) that copies only the rows a half-mode
- * cox_grouped_swiglu_gather loads from x_perm: local row i of an expert
- * segment is written iff (i mod 128) < 64.  offsets, dst and row_tokens are
- * complete.  x_perm and row_tokens are required. */
-int cox_permute_half(const int32_t* idx, int T, int k, int E, const void* x, int d, int32_t* offsets, int32_t* dst,
-                     void* x_perm, long long rows_cap, int32_t* row_tokens, void* workspace, void* stream);
+ * core reads; B (the weights) still streams by TMA.  Replaces the permute's
+ * row copy (T*k*d*2 bytes written, T*d*2 read) in the reference's
+ * expert:dispatch step (sim.py:149-202, costmodel.py:266-273).
+ * d % 64 == 0, ff % 128 == 0. */
+int cox_grouped_swiglu_gather(const void* x, long long T, const int32_t* row_tokens, const int32_t* offsets, int E,
+                              int n_groups, const int32_t* group_experts, const void* const* w13, int d, int ff,
+                              void* h, int max_ctas, void* stream);
 
 /* K4 — grouped down projection: y_perm[r] = h[r] W2_e^T.  w2[g]: [d, ff] bf16.
  * Same grouping arguments as cox_grouped_swiglu.  ff % 64 == 0, d % 256 == 0. */

@@ -29,7 +29,7 @@ ROUTE_DEEPSEEK = 1
 # Every symbol include/coxmoe.h declares (tests check the .so exports them all).
 EXPORTS = (
     "cox_last_error", "cox_version", "cox_device_check", "cox_router_workspace_bytes", "cox_router_topk",
-    "cox_permute_workspace_bytes", "cox_permute", "cox_grouped_swiglu", "cox_grouped_swiglu_gather", "cox_permute_half", "cox_grouped_down",
+    "cox_permute_workspace_bytes", "cox_permute", "cox_grouped_swiglu", "cox_grouped_swiglu_gather", "cox_grouped_down",
     "cox_small_expert_ffn", "cox_small_expert_ffn_idx", "cox_decode_moe", "cox_combine", "cox_ep_counts_put",
     "cox_ep_offsets", "cox_ep_dispatch", "cox_ep_combine", "cox_interleave_w13", "cox_fetch_experts",
 )
@@ -62,9 +62,7 @@ def _declare(L):
     L.cox_grouped_swiglu.restype = c_int
     L.cox_grouped_swiglu.argtypes = [P, c_ll, P, c_int, c_int, P, P, c_int, c_int, P, c_int, P]
     L.cox_grouped_swiglu_gather.restype = c_int
-    L.cox_grouped_swiglu_gather.argtypes = [P, c_ll, P, P, c_ll, P, c_int, c_int, P, P, c_int, c_int, P, c_int, P]
-    L.cox_permute_half.restype = c_int
-    L.cox_permute_half.argtypes = [P, c_int, c_int, c_int, P, c_int, P, P, P, c_ll, P, P, P]
+    L.cox_grouped_swiglu_gather.argtypes = [P, c_ll, P, P, c_int, c_int, P, P, c_int, c_int, P, c_int, P]
     L.cox_grouped_down.restype = c_int
     L.cox_grouped_down.argtypes = [P, c_ll, P, c_int, c_int, P, P, c_int, c_int, P, c_int, P]
     L.cox_small_expert_ffn.restype = c_int

@@ -15,11 +15,11 @@ int launch_router(const void* x, int x_is_bf16, const void* wg, int wg_is_bf16, 
 size_t permute_workspace_bytes(int T, int E);
 int launch_permute(const int32_t* idx, int T, int k, int E, int tile_m, const void* x, int d, int32_t* offsets,
                    int32_t* dst, void* x_perm, void* workspace, cudaStream_t s, int32_t* row_tokens = nullptr,
-                   long long rows_cap = 0, int copy_half = 0);
+                   long long rows_cap = 0);
 int launch_grouped_gemm(int epi, const void* A, long long rows_cap, int K, const int32_t* offsets, int n_groups,
                         const int32_t* group_expert, const void* const* B, int N, void* out, long long ldo,
                         int max_ctas, cudaStream_t s, const void* gx = nullptr, const int32_t* row_tokens = nullptr,
-                        long long gx_ld = 0, long long gx_rows = 0);
+                        long long gx_ld = 0);
 struct SmallDense {
   const void* wg;
   int E, mode;
@@ -164,20 +164,6 @@ int cox_permute(const int32_t* idx, int T, int k, int E, int tile_m, const void*
   return cuda_status(rc, "cox_permute");
 }
 
-int cox_permute_half(const int32_t* idx, int T, int k, int E, const void* x, int d, int32_t* offsets, int32_t* dst,
-                     void* x_perm, long long rows_cap, int32_t* row_tokens, void* workspace, void* stream) {
-  if (!x_perm || !row_tokens) return fail(COX_EINVAL, "cox_permute_half: needs x_perm and row_tokens");
-  if (T < 0 || k < 1 || k > 8 || E < 1 || E > 256 || d <= 0 || d % 8)
-    return fail(COX_EINVAL, "cox_permute_half: need 1<=k<=8, 1<=E<=256, d%%8==0");
-  if (rows_cap < (long long)T * k)
-    return fail(COX_EINVAL, "cox_permute_half: rows_cap %lld < T*k = %lld", rows_cap, (long long)T * k);
-  if (!aligned16(x) || !aligned16(x_perm)) return fail(COX_EINVAL, "cox_permute_half: x/x_perm must be 16-byte aligned");
-  if (!workspace || !offsets) return fail(COX_EINVAL, "cox_permute_half: null workspace/offsets");
-  int rc = cox::launch_permute(idx, T, k, E, 1, x, d, offsets, dst, x_perm, workspace,
-                               static_cast<cudaStream_t>(stream), row_tokens, rows_cap, 1);
-  return cuda_status(rc, "cox_permute_half");
-}
-
 // Every group's expert id must name a segment of offsets[E + 1]: the kernels
 // read offsets[e] and offsets[e + 1].
 static int check_groups(const char* fn, int E, int n_groups, const int32_t* group_experts, const void* const* w) {
@@ -207,10 +193,9 @@ int cox_grouped_swiglu(const void* x_perm, long long rows_cap, const int32_t* of
   return cuda_status(rc, fn);
 }
 
-int cox_grouped_swiglu_gather(const void* x, long long T, const int32_t* row_tokens, const void* x_perm_half,
-                              long long rows_cap, const int32_t* offsets, int E, int n_groups,
-                              const int32_t* group_experts, const void* const* w13, int d, int ff, void* h,
-                              int max_ctas, void* stream) {
+int cox_grouped_swiglu_gather(const void* x, long long T, const int32_t* row_tokens, const int32_t* offsets, int E,
+                              int n_groups, const int32_t* group_experts, const void* const* w13, int d, int ff,
+                              void* h, int max_ctas, void* stream) {
   const char* fn = "cox_grouped_swiglu_gather";
   if (d <= 0 || d % 64 || ff <= 0 || ff % 128)
     return fail(COX_EINVAL, "%s: need d%%64==0 and ff%%128==0 (d=%d ff=%d)", fn, d, ff);
@@ -220,10 +205,8 @@ int cox_grouped_swiglu_gather(const void* x, long long T, const int32_t* row_tok
   if (int rc = check_groups(fn, E, n_groups, group_experts, w13)) return rc;
   if (n_groups > 0 && (!x || !h || !offsets || !row_tokens))
     return fail(COX_EINVAL, "%s: null x/h/offsets/row_tokens", fn);
-  if (x_perm_half && (!aligned16(x_perm_half) || rows_cap < 1))
-    return fail(COX_EINVAL, "%s: x_perm_half unaligned or rows_cap < 1", fn);
-  int rc = cox::launch_grouped_gemm(0, x_perm_half, rows_cap, d, offsets, n_groups, group_experts, w13, 2 * ff, h, ff,
-                                    max_ctas, static_cast<cudaStream_t>(stream), x, row_tokens, d, T);
+  int rc = cox::launch_grouped_gemm(0, nullptr, 0, d, offsets, n_groups, group_experts, w13, 2 * ff, h, ff, max_ctas,
+                                    static_cast<cudaStream_t>(stream), x, row_tokens, d);
   return cuda_status(rc, fn);
 }
 

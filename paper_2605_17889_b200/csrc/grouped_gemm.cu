@@ -76,7 +76,6 @@ struct alignas(64) GemmParams {
   const __nv_bfloat16* gx;
   const int32_t* row_tokens;
   long long gx_ld;
-  int a_half;  // gather mode: rows [0, 64) of every CTA tile by TMA from a_map (x_perm, box of 64 rows)
 };
 
 struct TileCoord {
@@ -213,7 +212,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GM_THREADS + (GATHER
     if (lane == 0) s_prefix[p.n_groups] = acc;
   }
   if (warp == 0 && lane == 0) {
-    if (!GATHER || p.a_half) tma_prefetch_desc(&p.a_map);
+    if (!GATHER) tma_prefetch_desc(&p.a_map);
     for (int g = 0; g < p.n_groups; ++g) tma_prefetch_desc(&p.b_map[g]);
   }
   if (warp == 2) tmem_alloc<2>(smem_u32(tmem_slot), GM_TMEM_COLS);
@@ -290,18 +289,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GM_THREADS + (GATHER
           mbar_wait(smem_u32(&empty[stage]), phase ^ 1);
           const uint32_t fb_local = smem_u32(&full[stage]);
           const uint32_t fb = mapa(fb_local, 0);
-          if (rank == 0)
-            mbar_arrive_expect_tx(fb_local, 2 * ((GATHER ? (p.a_half ? A_STAGE / 2 : 0u) : A_STAGE) + B_STAGE));
+          if (rank == 0) mbar_arrive_expect_tx(fb_local, 2 * ((GATHER ? 0u : A_STAGE) + B_STAGE));
 #pragma unroll
           for (int a = 0; a < KA; ++a) {
             const uint32_t da = smem_u32(sA + stage * A_STAGE + a * GM_A_BYTES);
             const uint32_t db = smem_u32(sB + stage * B_STAGE + a * GM_B_BYTES);
             const int kc = kb * BK + a * GM_BK;
             if (hint) {
-              if (!GATHER || p.a_half) tma_load_2d_pair_hint(da, &p.a_map, fb, kc, a_row, pol_a);
+              if (!GATHER) tma_load_2d_pair_hint(da, &p.a_map, fb, kc, a_row, pol_a);
               tma_load_2d_pair_hint(db, bmap, fb, kc, b_row, pol_b);
             } else {
-              if (!GATHER || p.a_half) tma_load_2d_pair(da, &p.a_map, fb, kc, a_row);
+              if (!GATHER) tma_load_2d_pair(da, &p.a_map, fb, kc, a_row);
               tma_load_2d_pair(db, bmap, fb, kc, b_row);
             }
           }
@@ -392,10 +390,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GM_THREADS + (GATHER
       const __nv_bfloat16* src[8];
       uint32_t sbytes[8];
 #pragma unroll
-      const int w0 = p.a_half ? 4 : 0;  // half mode: rows [0, 64) come by TMA
       for (int w = 0; w < 8; ++w) {
         const int r = 4 * gw + (lane >> 3) + 16 * w;
-        const bool ok = w >= w0 && lrow0 + r < s_rows[c.g];
+        const bool ok = lrow0 + r < s_rows[c.g];
         const int tok = ok ? __ldg(p.row_tokens + s_row0[c.g] + lrow0 + r) : 0;
         src[w] = p.gx + (long long)tok * p.gx_ld + 8 * c8;
         sbytes[w] = ok ? 16u : 0u;
@@ -410,7 +407,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GM_THREADS + (GATHER
 #pragma unroll
           for (int w = 0; w < 8; ++w) {
             const int r = 4 * gw + (lane >> 3) + 16 * w;
-            if (w >= w0) cp_async_cg16(atom + r * 128 + ((c8 ^ (r & 7)) << 4), src[w] + kc, sbytes[w]);
+            cp_async_cg16(atom + r * 128 + ((c8 ^ (r & 7)) << 4), src[w] + kc, sbytes[w]);
           }
         }
         asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(&afull[stage])) : "memory");
@@ -615,22 +612,15 @@ static int g_num_sms = 0;
 // row_tokens[r] of gx [*, K] (pitch gx_ld); A / rows_cap are unused.
 int launch_grouped_gemm(int epi, const void* A, long long rows_cap, int K, const int32_t* offsets, int n_groups,
                         const int32_t* group_expert, const void* const* B, int N, void* out, long long ldo,
-                        int max_ctas, cudaStream_t s, const void* gx, const int32_t* row_tokens, long long gx_ld,
-                        long long gx_rows) {
+                        int max_ctas, cudaStream_t s, const void* gx, const int32_t* row_tokens, long long gx_ld) {
   if (n_groups <= 0) return 0;
   static GemmParams p;  // large (8.6 KB): built in static storage, copied at launch
   static std::mutex mu;
   std::lock_guard<std::mutex> lk(mu);
   const bool gather = gx != nullptr;
   if (gather && epi != EPI_SWIGLU) return -1;
-  // gather mode with A != nullptr: half mode, A = x_perm holding the first 64 rows of every 128 (box of 64 rows)
-  p.a_half = gather && A != nullptr ? 1 : 0;
-  int rc = (gather && !p.a_half)
-               ? 0
-               : get_map(&p.a_map, A, (unsigned long long)rows_cap, (unsigned long long)K,
-                         (unsigned)(p.a_half ? GM_BM / 2 : GM_BM));
+  int rc = gather ? 0 : get_map(&p.a_map, A, (unsigned long long)rows_cap, (unsigned long long)K, (unsigned)GM_BM);
   if (rc) return rc;
-  (void)gx_rows;
   p.gx = static_cast<const __nv_bfloat16*>(gx);
   p.row_tokens = row_tokens;
   p.gx_ld = gx_ld;

@@ -236,25 +236,15 @@ __global__ void __launch_bounds__(PS_THREADS) perm_small(const int32_t* __restri
 
 // Row copies, grid-wide: one warp per token; each row is read once (16 B
 // vectors, 4 chunks in flight per lane) and written to its k destinations.
-// HALF: copy only the rows in the first 64 of every 128-row block of their
-// expert segment (the rows a half-gather K3 loads by TMA; it gathers the rest
-// from x itself, cox_grouped_swiglu_gather).
-template <bool HALF>
 __global__ void __launch_bounds__(256) perm_copy(const int32_t* __restrict__ dst, int T, int k,
                                                  const __nv_bfloat16* __restrict__ x, int d,
-                                                 __nv_bfloat16* __restrict__ x_perm, const int32_t* __restrict__ idx,
-                                                 const int32_t* __restrict__ offsets) {
+                                                 __nv_bfloat16* __restrict__ x_perm) {
   const int lane = threadIdx.x & 31;
   const long nwarps = (long)gridDim.x * (blockDim.x >> 5);
   for (long t = (long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); t < T; t += nwarps) {
     int di[8];
 #pragma unroll
     for (int j = 0; j < 8; ++j) di[j] = j < k ? dst[t * k + j] : 0;
-    if (HALF) {
-#pragma unroll
-      for (int j = 0; j < 8; ++j)
-        if (j < k && di[j] >= 0 && ((di[j] - offsets[idx[t * k + j]]) & 127) >= 64) di[j] = -1;
-    }
     const __nv_bfloat16* src = x + t * (long)d;
     for (int c0 = lane * 8; c0 < d; c0 += 32 * 8 * 4) {
       uint4 v[4];
@@ -295,7 +285,7 @@ size_t permute_workspace_bytes(int T, int E) {
 
 int launch_permute(const int32_t* idx, int T, int k, int E, int tile_m, const void* x, int d, int32_t* offsets,
                    int32_t* dst, void* x_perm, void* workspace, cudaStream_t s, int32_t* row_tokens,
-                   long long rows_cap, int copy_half) {
+                   long long rows_cap) {
   long nb = (T + PM_TB - 1) / PM_TB;
   int32_t* block_counts = static_cast<int32_t*>(workspace);
   int32_t* block_base = block_counts + (nb > 0 ? nb : 1) * E;
@@ -330,12 +320,8 @@ int launch_permute(const int32_t* idx, int T, int k, int E, int tile_m, const vo
   }
   long cb = (T + 7) / 8;
   if (cb > 148L * 16) cb = 148L * 16;
-  if (x_perm && copy_half && tile_m == 1)
-    perm_copy<true><<<(int)cb, 256, 0, s>>>(dst, T, k, static_cast<const __nv_bfloat16*>(x), d,
-                                            static_cast<__nv_bfloat16*>(x_perm), idx, offsets);
-  else if (x_perm)
-    perm_copy<false><<<(int)cb, 256, 0, s>>>(dst, T, k, static_cast<const __nv_bfloat16*>(x), d,
-                                             static_cast<__nv_bfloat16*>(x_perm), idx, offsets);
+  if (x_perm) perm_copy<<<(int)cb, 256, 0, s>>>(dst, T, k, static_cast<const __nv_bfloat16*>(x), d,
+                                    static_cast<__nv_bfloat16*>(x_perm));
   if (tile_m > 1 && x_perm) perm_zero_pad<<<dim3(8, E), 256, 0, s>>>(offsets, seg_counts, E, d, static_cast<__nv_bfloat16*>(x_perm));
   return launch_status();
 }

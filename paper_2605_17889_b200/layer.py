@@ -51,7 +51,7 @@ class StageBuffers:
 
 
 def alloc_buffers(T: int, d: int, ff: int, E: int, k: int, tile_m: int, device, out_dtype=torch.bfloat16,
-                  shared_ff: int = 0, gather_a: bool | str = False) -> StageBuffers:
+                  shared_ff: int = 0, gather_a: bool = False) -> StageBuffers:
     cap = ops.rows_capacity(T, k, E, tile_m)
     bf = torch.bfloat16
     b = StageBuffers(
@@ -61,7 +61,7 @@ def alloc_buffers(T: int, d: int, ff: int, E: int, k: int, tile_m: int, device, 
         counts=torch.empty((E,), dtype=torch.int32, device=device),
         offsets=torch.empty((E + 1,), dtype=torch.int32, device=device),
         dst=torch.empty((T, k), dtype=torch.int32, device=device),
-        x_perm=torch.empty((0 if gather_a is True else cap, d), dtype=bf, device=device),
+        x_perm=torch.empty((0 if gather_a else cap, d), dtype=bf, device=device),
         h=torch.empty((cap, ff), dtype=bf, device=device),
         y=torch.empty((cap, d), dtype=bf, device=device),
         out=torch.empty((T, d), dtype=out_dtype, device=device),
@@ -115,7 +115,7 @@ class MoELayer:
     GATHER_A_DEFAULT = False
 
     def __init__(self, weights: LayerWeights, top_k: int, mode: str = "mixtral", tile_m: int = 1,
-                 out_dtype=torch.bfloat16, gather_a: bool | str | None = None):
+                 out_dtype=torch.bfloat16, gather_a: bool | None = None):
         if mode not in MODES:
             raise ValueError(f"mode must be one of {sorted(MODES)}")
         self.wts = weights
@@ -126,10 +126,7 @@ class MoELayer:
         self.out_dtype = out_dtype
         # prefill K3 gathers its A rows from x (cp.async) instead of a
         # materialised x_perm: the permute writes indices only
-        ga = self.GATHER_A_DEFAULT if gather_a is None else gather_a
-        if ga not in (False, True, "half"):
-            raise ValueError("gather_a must be False, True or 'half'")
-        self.gather_a = ga
+        self.gather_a = self.GATHER_A_DEFAULT if gather_a is None else bool(gather_a)
         if self.gather_a and self.tile_m != 1:
             raise ValueError("gather_a needs tile_m == 1")
         self.E = weights.num_experts
@@ -164,7 +161,7 @@ class MoELayer:
             # router + permute (rows materialised) + one launch for K3/K4/shared/combine
             return 1 + perm + 1 + (1 if self.out_dtype != torch.bfloat16 else 0)
         # prefill: the gather path drops the permute's row copy
-        return 1 + perm - (1 if self.gather_a is True else 0) + 2 + 1 + (2 if self.shared_ff else 0)
+        return 1 + perm - (1 if self.gather_a else 0) + 2 + 1 + (2 if self.shared_ff else 0)
 
     # --- buffers ---------------------------------------------------------------
     def buffers(self, T: int, device) -> StageBuffers:
@@ -172,7 +169,7 @@ class MoELayer:
         if b is None:
             for t in [t for t in self._bufs if t not in self._pinned]:
                 del self._bufs[t]
-            gather = False if self.uses_small_path(T) else self.gather_a  # False | True | "half"
+            gather = self.gather_a and not self.uses_small_path(T)
             b = alloc_buffers(T, self.d, self.ff, self.E, self.k, self.tile_m, device, self.out_dtype,
                               self.shared_ff, gather_a=gather)
             if self.uses_small_path(T):
@@ -196,21 +193,16 @@ class MoELayer:
         self._permute(x, b)
 
     def _gathers(self, b: StageBuffers) -> bool:
-        return b.row_tokens is not None and not self.uses_small_path(b.T)  # prefill buffers of a gather_a layer
+        return b.x_perm.shape[0] == 0  # prefill buffers of a gather_a layer
 
     def _permute(self, x: torch.Tensor, b: StageBuffers):
-        if self._gathers(b) and self.gather_a == "half":
-            ops.permute_half(b.idx, x, self.E, out=(b.offsets, b.dst, b.x_perm), workspace=b.workspace,
-                             row_tokens=b.row_tokens)
-        else:
-            ops.permute(b.idx, x, self.E, self.tile_m, out=(b.offsets, b.dst, b.x_perm), workspace=b.workspace,
-                        row_tokens=b.row_tokens, copy_rows=not self._gathers(b))
+        ops.permute(b.idx, x, self.E, self.tile_m, out=(b.offsets, b.dst, b.x_perm), workspace=b.workspace,
+                    row_tokens=b.row_tokens, copy_rows=not self._gathers(b))
         self._x = x  # the gather K3 reads the permuted rows straight from the step's input
 
     def _swiglu(self, b: StageBuffers, groups, w13, max_ctas: int = 0):
         if self._gathers(b):
-            ops.grouped_swiglu_gather(self._x, b.row_tokens, b.offsets, groups, w13, self.ff, b.h, max_ctas=max_ctas,
-                                      x_perm_half=b.x_perm if self.gather_a == "half" else None)
+            ops.grouped_swiglu_gather(self._x, b.row_tokens, b.offsets, groups, w13, self.ff, b.h, max_ctas=max_ctas)
         else:
             ops.grouped_swiglu(b.x_perm, b.offsets, groups, w13, self.ff, h=b.h, max_ctas=max_ctas)
 

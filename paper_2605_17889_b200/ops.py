@@ -158,11 +158,9 @@ def grouped_swiglu(x_perm: torch.Tensor, offsets: torch.Tensor, group_experts: S
 
 def grouped_swiglu_gather(x: torch.Tensor, row_tokens: torch.Tensor, offsets: torch.Tensor,
                           group_experts: Sequence[int], w13: Sequence[torch.Tensor], ff: int, h: torch.Tensor,
-                          stream=None, max_ctas: int = 0, x_perm_half: torch.Tensor | None = None):
+                          stream=None, max_ctas: int = 0):
     """K3 with the permuted rows gathered from x: h[r] = SwiGLU_e(x[row_tokens[r]]) —
-    the same bits as grouped_swiglu on x_perm, without (x_perm_half=None) or with
-    half of the permute's row copy (x_perm_half from permute_half: the first 64 of
-    every 128 rows of a segment come from it by TMA)."""
+    the same bits as grouped_swiglu on x_perm, without the permute's row copy."""
     _need(x, "x", _BF16, 2)
     _need(row_tokens, "row_tokens", torch.int32, 1)
     _need(offsets, "offsets", torch.int32, 1)
@@ -176,35 +174,11 @@ def grouped_swiglu_gather(x: torch.Tensor, row_tokens: torch.Tensor, offsets: to
         raise ValueError("one weight per group")
     if h.shape[1] != ff or h.shape[0] > row_tokens.numel():
         raise ValueError("h must be [rows, ff] with a row_tokens entry per row")
-    if x_perm_half is not None:
-        _need(x_perm_half, "x_perm_half", _BF16, 2)
-        if x_perm_half.shape[1] != d:
-            raise ValueError("x_perm_half must be [rows_cap, d]")
     L = _lib.lib()
-    _lib.check(L.cox_grouped_swiglu_gather(x.data_ptr(), T, row_tokens.data_ptr(),
-                                           x_perm_half.data_ptr() if x_perm_half is not None else None,
-                                           x_perm_half.shape[0] if x_perm_half is not None else 0,
-                                           offsets.data_ptr(), offsets.numel() - 1, len(group_experts),
-                                           _ids(group_experts), _ptrs(w13), d, ff, h.data_ptr(), max_ctas,
-                                           _stream(stream)), "cox_grouped_swiglu_gather")
+    _lib.check(L.cox_grouped_swiglu_gather(x.data_ptr(), T, row_tokens.data_ptr(), offsets.data_ptr(),
+                                           offsets.numel() - 1, len(group_experts), _ids(group_experts), _ptrs(w13),
+                                           d, ff, h.data_ptr(), max_ctas, _stream(stream)), "cox_grouped_swiglu_gather")
     return h
-
-
-def permute_half(idx: torch.Tensor, x: torch.Tensor, E: int, out, workspace, row_tokens: torch.Tensor, stream=None):
-    """K2 for the half-gather K3: complete offsets / dst / row_tokens, but x_perm
-    holds only the first 64 of every 128 rows of each expert segment."""
-    _need(idx, "idx", torch.int32, 2)
-    _need(x, "x", _BF16, 2)
-    _need(row_tokens, "row_tokens", torch.int32, 1)
-    T, k = idx.shape
-    offsets, dst, x_perm = out
-    if x_perm is None or x_perm.shape[0] < T * k or row_tokens.numel() < T * k:
-        raise ValueError("permute_half needs x_perm and row_tokens of T*k rows")
-    L = _lib.lib()
-    _lib.check(L.cox_permute_half(idx.data_ptr(), T, k, E, x.data_ptr(), x.shape[1], offsets.data_ptr(),
-                                  dst.data_ptr(), x_perm.data_ptr(), x_perm.shape[0], row_tokens.data_ptr(),
-                                  workspace.data_ptr(), _stream(stream)), "cox_permute_half")
-    return offsets, dst, x_perm
 
 
 def grouped_down(h: torch.Tensor, offsets: torch.Tensor, group_experts: Sequence[int], w2: Sequence[torch.Tensor],

@@ -50,17 +50,13 @@ def test_argument_validation_is_host_only():
     assert rc == _lib.COX_EINVAL and b"workspace" in L.cox_last_error()
     # K3 gather mode: needs row_tokens, d % 64 == 0, expert ids inside [0, E)
     ids[1] = 3
-    rc = L.cox_grouped_swiglu_gather(4096, 100, None, None, 0, 4096, 8, 2, ids, ptrs, 256, 256, 4096, 0, None)
+    rc = L.cox_grouped_swiglu_gather(4096, 100, None, 4096, 8, 2, ids, ptrs, 256, 256, 4096, 0, None)
     assert rc == _lib.COX_EINVAL and b"row_tokens" in L.cox_last_error()
-    rc = L.cox_grouped_swiglu_gather(4096, 100, 4096, None, 0, 4096, 8, 2, ids, ptrs, 96, 256, 4096, 0, None)
+    rc = L.cox_grouped_swiglu_gather(4096, 100, 4096, 4096, 8, 2, ids, ptrs, 96, 256, 4096, 0, None)
     assert rc == _lib.COX_EINVAL and b"d%64" in L.cox_last_error()
-    rc = L.cox_grouped_swiglu_gather(4096, 100, 4096, 4100, 200, 4096, 8, 2, ids, ptrs, 256, 256, 4096, 0, None)
-    assert rc == _lib.COX_EINVAL and b"x_perm_half" in L.cox_last_error()
     ids[1] = 9
-    rc = L.cox_grouped_swiglu_gather(4096, 100, 4096, None, 0, 4096, 8, 2, ids, ptrs, 256, 256, 4096, 0, None)
+    rc = L.cox_grouped_swiglu_gather(4096, 100, 4096, 4096, 8, 2, ids, ptrs, 256, 256, 4096, 0, None)
     assert rc == _lib.COX_EINVAL and b"outside [0, 8)" in L.cox_last_error()
-    rc = L.cox_permute_half(4096, 100, 2, 8, 4096, 256, 4096, 4096, None, 200, 4096, 4096, None)
-    assert rc == _lib.COX_EINVAL and b"x_perm and row_tokens" in L.cox_last_error()
 
 
 def test_sass_contains_tcgen05_and_tma():
