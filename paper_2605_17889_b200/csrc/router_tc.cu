@@ -14,12 +14,14 @@
 //      rounding of d/16 tensor-core accumulation steps plus d/32 + 5 canonical
 //      fp32 steps, x4 safety; SURVEY.md §0.5 explains why the canonical order
 //      is needed at all).
-//   R2 router_rescore_kernel (one warp per token): k-th largest approx value a_k;
-//      candidates C = {e : approx_e >= a_k - 2 margin_t}.  Every e outside C has
-//      exact_e < a_k - margin_t <= exact_s for all k screened winners s, so the
-//      exact top-k lies in C.  Exact canonical logits for C (FFMA2 pairs, lane
-//      chunk order + xor butterfly), top-k with ties to the lower index, weights
-//      from the exact logits (Mixtral: softmax over the k: bit-exact; DeepSeek:
+//   R2 router_rescore_kernel (one warp per token scores, one lane per token
+//      selects): k-th largest approx value a_k; candidates C = {e : approx_e >=
+//      a_k - 2 margin_t}.  Every e outside C has exact_e < a_k - margin_t <=
+//      exact_s for all k screened winners s, so the exact top-k lies in C.
+//      Exact canonical logits for C (mixed-precision FHFMA.BF16 chains in the
+//      lane chunk order + the xor butterfly's sums), then per lane over a
+//      batch of tokens: top-k with ties to the lower index, weights from the
+//      exact logits (Mixtral: softmax over the k: bit-exact; DeepSeek:
 //      full-softmax denominator uses exact logits for C and the tensor-core
 //      logits for the rest).
 // Used when x and the router weight are bf16 (the checkpoint dtypes).
