@@ -240,10 +240,16 @@ def run_reference(args, cfg):
     from paper_2605_17889_b200.synthetic import make_layer_weights, make_tokens
     T, d, ff, E, k, mode, shared_ff, desc = cfg
     sample = min(T, args.ref_tokens)
-    wts = make_layer_weights(E, d, ff, seed=0, device="cpu", shared_ff=shared_ff)
-    x = make_tokens(sample, d, seed=1, device="cpu").float().numpy()
+    # the same seeded generators (and so the same bits) as the GPU arm's inputs:
+    # drawn on the GPU when there is one (data generation only, no kernels of
+    # ours), then moved to host memory for the CPU oracle
+    gen_dev = "cuda" if torch.cuda.is_available() else "cpu"
+    wts = make_layer_weights(E, d, ff, seed=0, device=gen_dev, shared_ff=shared_ff)
+    x = make_tokens(T if gen_dev == "cuda" else sample, d, seed=1, device=gen_dev)[:sample].float().cpu().numpy()
     hw, shared = host_weights(wts)
     del wts
+    if gen_dev == "cuda":
+        torch.cuda.empty_cache()
     threads = len(os.sched_getaffinity(0))
     O.set_num_threads(threads)
     mode_id = 0 if mode == "mixtral" else 1
@@ -257,7 +263,8 @@ def run_reference(args, cfg):
     line = {
         "impl": "reference", "metric": metric_name(args.config), "value": value, "unit": "tokens/s",
         "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": f"synthetic (the GPU arm's seeded inputs, generated on {gen_dev})",
         "config": {"workload": desc, "tokens_per_step": sample, "d": d, "ff": ff, "E": E, "k": k},
         "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": threads, "kind": "port",
                          "sample": f"first {sample} of {T} tokens per step, full-size weights, fp32 oracle "
