@@ -10,8 +10,8 @@ Kernel selection by batch size (all measured on B200):
     (cox_decode_moe: router + every expert + shared experts + combine);
   * T <= SMALL_GATHER_T_MAX (64): router launch + one weight-streaming launch
     that reads the router's idx directly (cox_small_expert_ffn_idx);
-  * T <= SMALL_T_MAX (256): router + permute (x_perm materialised) + one
-    weight-streaming launch (cox_small_expert_ffn);
+  * T <= SMALL_T_MAX (256) and T*k <= 48 E: router + permute (x_perm
+    materialised) + one weight-streaming launch (cox_small_expert_ffn);
   * larger batches: router, permute, K3, K4, combine (persistent tcgen05
     grouped GEMMs), shared experts on a side stream.
 """
@@ -89,6 +89,12 @@ class MoELayer:
     # decode-size batches: one weight-streaming launch for K3+K4 (+ shared
     # experts), csrc/small_gemm.cu
     SMALL_T_MAX = 256
+    # ... and while an expert averages at most this many rows (the kernel runs
+    # segments in 64-token chunks).  Measured with tools/sweep_tokens.py
+    # (graph replay, us, weight-streaming vs prefill kernels): C2 (E=8, k=2)
+    # T=192 (48 rows) 511 vs 590, T=256 (64 rows) 734 vs 601; C4 (E=64, k=6)
+    # T=256 (24 rows) 278 vs 287, T=384 (36 rows) 356 vs 302.
+    SMALL_ROWS_PER_EXPERT_MAX = 48
     # Row gathers (TMA tile::gather4 of x rows) only up to this many tokens:
     # above it the permute materialises x_perm and the kernel loads tiled B
     # boxes.  Measured on C4 (tools/sweep_decode_large.py, us/step, gather vs
@@ -232,7 +238,8 @@ class MoELayer:
         return ops.combine(b.y, b.dst, b.w, shared, out=b.out if out is None else out)
 
     def uses_small_path(self, T: int) -> bool:
-        return (0 < T <= self.SMALL_T_MAX and self.d % 128 == 0 and self.ff % 128 == 0 and self.E <= 64
+        return (0 < T <= self.SMALL_T_MAX and T * self.k <= self.SMALL_ROWS_PER_EXPERT_MAX * self.E
+                and self.d % 128 == 0 and self.ff % 128 == 0 and self.E <= 64
                 and (not self.shared_ff or self.shared_ff % 128 == 0))
 
     def uses_dense_decode(self, T: int) -> bool:

@@ -145,6 +145,7 @@ def test_random_decode_configs_vs_oracle(seed):
         x += 2.0 * d ** 0.5 * wts.wg[int(rng.integers(0, E))]
     x = x.to(torch.bfloat16)
     layer = MoELayer(wts, k, mode)
+    layer.SMALL_ROWS_PER_EXPERT_MAX = 1 << 30  # exercise the weight-streaming kernel at any rows/expert
     assert layer.uses_small_path(T)
     out = layer(x)
     torch.cuda.synchronize()

@@ -54,7 +54,31 @@ def time_step(layer, x, reps):
     return ts[len(ts) // 2]
 
 
+def compare_paths(cfg):
+    """Weight-streaming (small) path vs prefill kernels for T = 64 ... 2048."""
+    d, ff, E, k, mode, sff = SHAPES[cfg]
+    wts = make_layer_weights(E, d, ff, seed=0, device="cuda", shared_ff=sff)
+    for T in (64, 128, 192, 256, 384, 512, 768, 1024, 1536, 2048):
+        x = make_tokens(T, d, seed=1, device="cuda")
+        row = []
+        for name, tmax in (("small", 1 << 30), ("prefill", 0)):
+            layer = MoELayer(wts, k, mode)
+            layer.SMALL_T_MAX = tmax
+            layer.SMALL_GATHER_T_MAX = min(layer.SMALL_GATHER_T_MAX, tmax)
+            layer.DENSE_T_MAX = 0
+            try:
+                row.append(f"{name} {time_step(layer, x, 100) * 1e3:8.1f} us")
+            except Exception as exc:  # noqa: BLE001
+                row.append(f"{name} failed ({type(exc).__name__})")
+            del layer
+            torch.cuda.empty_cache()
+        print(f"{cfg} T={T:5d} rows/expert {T * k / E:6.1f}:  " + "   ".join(row), flush=True)
+
+
 def main():
+    if len(sys.argv) > 2 and sys.argv[2] == "paths":
+        compare_paths(sys.argv[1])
+        return
     cfg = sys.argv[1] if len(sys.argv) > 1 else "C4"
     d, ff, E, k, mode, sff = SHAPES[cfg]
     wts = make_layer_weights(E, d, ff, seed=0, device="cuda", shared_ff=sff)
