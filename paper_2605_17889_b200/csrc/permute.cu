@@ -139,7 +139,9 @@ __global__ void __launch_bounds__(PM_TB) perm_scatter(const int32_t* __restrict_
 // ballots, warp prefix per expert in shared memory, running per-expert base
 // across chunks.
 constexpr int PS_THREADS = 1024;
-constexpr long PS_MAX_PAIRS = 16384;
+// up to 2,048 pairs (decode-size steps, T <= 256): above, the three parallel
+// kernels win (C1, T*k = 8,192: 7 us faster per step under graph replay)
+constexpr long PS_MAX_PAIRS = 2048;
 
 __global__ void __launch_bounds__(PS_THREADS) perm_small(const int32_t* __restrict__ idx, int T, int k, int E,
                                                          int tile_m, int32_t* __restrict__ offsets,

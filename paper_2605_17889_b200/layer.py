@@ -160,8 +160,8 @@ class MoELayer:
             return 1  # router + all experts + shared + combine in one launch
         if T is not None and self.uses_idx_decode(T):
             return 2  # router, then one launch for K3/K4/shared/combine reading the router's idx
-        # permute: single-CTA index kernel for T*k <= 16384 (else hist, scan, scatter) + row copy (+ pad)
-        small_perm = T is not None and T * self.k <= 16384
+        # permute: single-CTA index kernel for T*k <= 2048 (else hist, scan, scatter) + row copy (+ pad)
+        small_perm = T is not None and T * self.k <= 2048
         perm = (1 if small_perm else 3) + 1 + (1 if self.tile_m > 1 else 0)
         if T is not None and self.uses_small_path(T):
             # router + permute (rows materialised) + one launch for K3/K4/shared/combine

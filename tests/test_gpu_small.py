@@ -112,6 +112,7 @@ def test_decode_from_idx_matches_permute_path(T, d, ff, E, k, mode, shared_ff):
     a_l = MoELayer(wts, k, mode)
     b_l = MoELayer(wts, k, mode)
     a_l.DENSE_T_MAX = b_l.DENSE_T_MAX = 0
+    a_l.SMALL_ROWS_PER_EXPERT_MAX = b_l.SMALL_ROWS_PER_EXPERT_MAX = 1 << 30  # kernel equivalence at any rows/expert
     a_l.SMALL_GATHER_T_MAX = 256  # idx path at every T here
     b_l.SMALL_GATHER_T_MAX = 0    # router + permute + x_perm launch at every T
     assert a_l.uses_idx_decode(T) and not b_l.uses_idx_decode(T)
