@@ -157,7 +157,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GM_THREADS + (GATHER
   uint64_t* afull = sempty + GM_SCHED_DEPTH;                     // [NB] gather mode: this CTA's A copies landed
   int* s_tile = reinterpret_cast<int*>(afull + NB);              // [DEPTH]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_tile + GM_SCHED_DEPTH);
-  int* s_prefix = reinterpret_cast<int*>(tmem_slot + 4);
+  uint32_t* tx_scratch = tmem_slot + 4;  // [12] gather mode: the relays' 16-byte completion copies
+  int* s_prefix = reinterpret_cast<int*>(tx_scratch + 12);
   int* s_rows = s_prefix + GM_MAXG + 1;
   int* s_row0 = s_rows + GM_MAXG;
   uint32_t* s_stage = reinterpret_cast<uint32_t*>(
@@ -169,8 +170,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GM_THREADS + (GATHER
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
-      // gather mode: + one relay arrive per CTA (its A copies landed)
-      mbar_init(smem_u32(&full[s]), GATHER ? 3 : 1);
+      // gather mode: the relays signal "A landed" as 16 transaction bytes each (see below)
+      mbar_init(smem_u32(&full[s]), 1);
       mbar_init(smem_u32(&empty[s]), 1);
       if (GATHER) mbar_init(smem_u32(&afull[s]), 32 * GM_GATHER_WARPS);
     }
@@ -289,7 +290,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GM_THREADS + (GATHER
           mbar_wait(smem_u32(&empty[stage]), phase ^ 1);
           const uint32_t fb_local = smem_u32(&full[stage]);
           const uint32_t fb = mapa(fb_local, 0);
-          if (rank == 0) mbar_arrive_expect_tx(fb_local, 2 * ((GATHER ? 0u : A_STAGE) + B_STAGE));
+          if (rank == 0) mbar_arrive_expect_tx(fb_local, 2 * ((GATHER ? 16u : A_STAGE) + B_STAGE));
 #pragma unroll
           for (int a = 0; a < KA; ++a) {
             const uint32_t da = smem_u32(sA + stage * A_STAGE + a * GM_A_BYTES);
@@ -325,8 +326,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GM_THREADS + (GATHER
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * GM_BN;
         for (int kb = 0; kb < nk; ++kb) {
-          if (GATHER) mbar_wait_cluster(smem_u32(&full[stage]), phase);  // peer gather warps arrive remotely
-          else mbar_wait(smem_u32(&full[stage]), phase);
+          mbar_wait(smem_u32(&full[stage]), phase);
           tc_fence_after();
           const uint32_t a_base = smem_u32(sA + stage * A_STAGE);
           const uint32_t b_base = smem_u32(sB + stage * B_STAGE);
@@ -348,11 +348,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GM_THREADS + (GATHER
   } else if (GATHER && warp == 2) {
     // ------------------------------------------------------------ A relay (gather mode)
     // Waits until this CTA's gather threads' copies of a stage have landed
-    // (cp.async.mbarrier.arrive on afull), makes them visible to the tensor
-    // core's async proxy, and arrives on the leader's full barrier (cluster
-    // scope, release) — the MMA waits there with a cluster-scope acquire.
+    // (cp.async.mbarrier.arrive on afull), orders them before the async proxy
+    // (fence.proxy.async), and signals the pair leader's full barrier with a
+    // 16-byte async-proxy bulk copy into the leader's shared memory that
+    // completes as transaction bytes on that barrier — the same completion
+    // path as the TMA loads, so the MMA waits exactly as for TMA-fed tiles.
+    // (An mbarrier.arrive.release.cluster here compiles to a GPU-scope memory
+    // barrier per stage and made the gathered K3 ~8% slower.)
     if (lane == 0) {
       const uint32_t full0 = mapa(smem_u32(&full[0]), 0);
+      const uint32_t dst = mapa(smem_u32(tx_scratch + 4 * rank), 0);
+      const uint32_t src = smem_u32(tx_scratch + 8);
       uint32_t stage = 0, phase = 0;
       int si = 0;
       int t = fetch_tile(si, true);
@@ -361,7 +367,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GM_THREADS + (GATHER
         for (int kb = 0; kb < nk; ++kb) {
           mbar_wait(smem_u32(&afull[stage]), phase);
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-          mbar_arrive_cluster(full0 + stage * 8);
+          asm volatile(
+              "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], 16, [%2];" ::"r"(dst),
+              "r"(src), "r"(full0 + stage * 8)
+              : "memory");
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
           if (kb == 0) t_next = fetch_tile(si, true);
         }

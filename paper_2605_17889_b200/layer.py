@@ -114,10 +114,10 @@ class MoELayer:
     # run_host_batches replays a captured step for batches up to this many tokens
     HOST_GRAPH_T_MAX = 8192
     # prefill K3 reading its A rows from x by cp.async gathers (no x_perm copy,
-    # saves the T*k*d*2-byte x_perm buffer): bit-identical, but measured slower
-    # on B200 (C4 31.9 vs 30.8 ms, C2 154.8 vs 136.1 ms per step: the gathered
-    # stages keep the tensor pipe 73% busy vs 88% for TMA-fed x_perm tiles), so
-    # off by default; DESIGN.md §3 "Gather-fused A, round 2"
+    # saves the T*k*d*2-byte x_perm buffer): bit-identical, measured within
+    # 1-2% of (not faster than) the x_perm path on B200 (C4 30.1-30.7 vs
+    # 29.9-30.0 ms, C2 137.6-138.1 vs 134.0-135.4 ms per step), so opt-in;
+    # DESIGN.md §4 "Gather-fused A loads"
     GATHER_A_DEFAULT = False
 
     def __init__(self, weights: LayerWeights, top_k: int, mode: str = "mixtral", tile_m: int = 1,
