@@ -249,7 +249,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GM_THREADS + (GATHER
       mbar_wait_cluster(smem_u32(&sfull[slot]), ph);
       t = reinterpret_cast<volatile int*>(s_tile)[slot];
       __syncwarp(__activemask());
-      if (do_arrive) mbar_arrive_cluster(mapa(smem_u32(&sempty[slot]), 0));
+      if (do_arrive) {
+        // relaxed arrive (a release.cluster arrive is a GPU-scope membar that
+        // would wait for this warp's outstanding global stores); the slot read
+        // is ordered before it by a data dependency of the arrive's address
+        uint32_t z;
+        asm volatile("and.b32 %0, %1, 0;" : "=r"(z) : "r"(t));
+        mbar_arrive_cluster_relaxed(mapa(smem_u32(&sempty[slot]), 0) + z);
+      }
     }
     ++si;
     return t;
