@@ -170,8 +170,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GM_THREADS + (GATHER
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
-      // gather mode: the relays signal "A landed" as 16 transaction bytes each (see below)
-      mbar_init(smem_u32(&full[s]), 1);
+      // gather mode: + the leader's relay arrive; the peer's relay signals as 16 tx bytes (see below)
+      mbar_init(smem_u32(&full[s]), GATHER ? 2 : 1);
       mbar_init(smem_u32(&empty[s]), 1);
       if (GATHER) mbar_init(smem_u32(&afull[s]), 32 * GM_GATHER_WARPS);
     }
@@ -297,7 +297,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GM_THREADS + (GATHER
           mbar_wait(smem_u32(&empty[stage]), phase ^ 1);
           const uint32_t fb_local = smem_u32(&full[stage]);
           const uint32_t fb = mapa(fb_local, 0);
-          if (rank == 0) mbar_arrive_expect_tx(fb_local, 2 * ((GATHER ? 16u : A_STAGE) + B_STAGE));
+          if (rank == 0) mbar_arrive_expect_tx(fb_local, GATHER ? 2 * B_STAGE + 16u : 2 * (A_STAGE + B_STAGE));
 #pragma unroll
           for (int a = 0; a < KA; ++a) {
             const uint32_t da = smem_u32(sA + stage * A_STAGE + a * GM_A_BYTES);
@@ -355,16 +355,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GM_THREADS + (GATHER
   } else if (GATHER && warp == 2) {
     // ------------------------------------------------------------ A relay (gather mode)
     // Waits until this CTA's gather threads' copies of a stage have landed
-    // (cp.async.mbarrier.arrive on afull), orders them before the async proxy
-    // (fence.proxy.async), and signals the pair leader's full barrier with a
+    // (cp.async.mbarrier.arrive on afull) and orders them before the async
+    // proxy (fence.proxy.async).  The leader's relay then arrives on its own
+    // full barrier (CTA scope); the peer's relay signals the leader with a
     // 16-byte async-proxy bulk copy into the leader's shared memory that
     // completes as transaction bytes on that barrier — the same completion
-    // path as the TMA loads, so the MMA waits exactly as for TMA-fed tiles.
-    // (An mbarrier.arrive.release.cluster here compiles to a GPU-scope memory
-    // barrier per stage and made the gathered K3 ~8% slower.)
+    // path as the peer's TMA loads.  (An mbarrier.arrive.release.cluster here
+    // compiles to a GPU-scope memory barrier per stage and made the gathered
+    // K3 ~8% slower.)
     if (lane == 0) {
       const uint32_t full0 = mapa(smem_u32(&full[0]), 0);
-      const uint32_t dst = mapa(smem_u32(tx_scratch + 4 * rank), 0);
+      const uint32_t dst = mapa(smem_u32(tx_scratch), 0);
       const uint32_t src = smem_u32(tx_scratch + 8);
       uint32_t stage = 0, phase = 0;
       int si = 0;
@@ -374,10 +375,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GM_THREADS + (GATHER
         for (int kb = 0; kb < nk; ++kb) {
           mbar_wait(smem_u32(&afull[stage]), phase);
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-          asm volatile(
-              "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], 16, [%2];" ::"r"(dst),
-              "r"(src), "r"(full0 + stage * 8)
-              : "memory");
+          if (rank == 0)
+            mbar_arrive(smem_u32(&full[stage]));
+          else
+            asm volatile(
+                "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], 16, [%2];" ::"r"(
+                    dst),
+                "r"(src), "r"(full0 + stage * 8)
+                : "memory");
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
           if (kb == 0) t_next = fetch_tile(si, true);
         }
