@@ -490,6 +490,7 @@ __global__ void __launch_bounds__(RR_WARPS * 32, NCH <= 8 ? 2 : 1) router_rescor
       const int u = lane >> 4;
       if ((lane & 15) == 0 && c + u < nc) lg[cand[c + u]] = r != r ? -INFINITY : r;
     }
+    __syncwarp();  // this token's cand / lg accesses before the next token's writes
     if (++nb == TB) {
       finish_batch(nb);
       nb = 0;
