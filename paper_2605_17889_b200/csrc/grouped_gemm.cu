@@ -690,11 +690,11 @@ int launch_grouped_gemm(int epi, const void* A, long long rows_cap, int K, const
   }
   int grid = (g_num_sms / 2) * 2;
   if (max_ctas >= 2 && max_ctas < grid) grid = (max_ctas / 2) * 2;
-  // K per stage: measured on C2, the SwiGLU GEMM is faster with BK=128 (3 stages;
-  // K3 92.2 -> 89.6 ms) while the long-K down projection prefers BK=64 with 6
-  // stages (42.6 vs 43.6 ms).
-  int ka = epi == EPI_SWIGLU ? 2 : 1;
-  if (K % (ka * GM_BK) != 0) ka = 1;
+  // K per stage: BK = 128 (3 stages) wherever K allows it.  Measured: C2 K3
+  // 92.2 -> 89.6 ms against BK = 64 / 6 stages; the down projection, same box,
+  // interleaved: C4's routed K4 (K = 1408) 6.96 -> 6.63 ms, C2's (K = 14336)
+  // 43.9 either way (tools/ab_k4ka.sh, round 2).
+  const int ka = K % (2 * GM_BK) == 0 ? 2 : 1;
 #define GM_LAUNCH(E_, KA_, G_)                                                                                 \
   do {                                                                                                         \
     static bool attr = false;                                                                                  \
