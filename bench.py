@@ -329,6 +329,85 @@ def _hit_summary(counts, plan, E, cap):
             "exact_map_upper_bound": eas.hit_ratio_from_counts(c, best)}
 
 
+def stack_parity_and_cpu(args, stack, T, mode):
+    """C3 / C3D: parity and CPU baseline on the stack's LAST layer of the last
+    step (its input is layer N-2's output, still in the ping/pong buffer).
+    parity: that layer's routing of the FULL batch (idx, counts, offsets, dst)
+    against the oracle router, bit for bit, and its output (residual included)
+    on the first n tokens against the fp32 oracle layer (rel-L2 <= 1e-2).
+    cpu_baseline: the oracle's rate through that one layer, divided by the
+    stack depth (the stack's tokens/s on the host)."""
+    import numpy as np
+    import torch
+    from oracle import oracle as O
+    from paper_2605_17889_b200.synthetic import split_w13
+    b = stack._bufs
+    N, E, k = stack.N, stack.E, stack.k
+    if N < 2 or b is None:
+        return None, None
+    l = N - 1
+    x_in = b.ping if (N - 2) % 2 == 0 else b.pong
+    out = b.ping if l % 2 == 0 else b.pong
+    mode_id = 0 if mode == "mixtral" else 1
+    wg = stack.wg[l].float().cpu().numpy()
+    gi, gc, go, gd = (t.cpu().numpy() for t in (b.idx, b.counts, b.offsets, b.dst))
+    t0 = time.perf_counter()
+    oi, _, oc = O.router_topk_bf16(x_in.view(torch.int16).cpu().numpy().view(np.uint16), wg, k, mode_id)
+    oo, od = O.permute(oi, E, 1)
+    t_route = time.perf_counter() - t0
+    routing_ok = bool(np.array_equal(gi, oi) and np.array_equal(gc, oc) and np.array_equal(go, oo)
+                      and np.array_equal(gd, od))
+    n = min(T, args.cpu_tokens)
+    ps = [stack.pool_map(l, e) for e in range(E)]
+    w1, w3 = split_w13(torch.stack([stack.pool.w13[p] for p in ps]))
+    w2 = torch.stack([stack.pool.w2[p] for p in ps])
+    f = lambda t: t.float().numpy()  # noqa: E731
+    threads = len(os.sched_getaffinity(0))
+    O.set_num_threads(threads)
+    xs = x_in[:n].float().cpu().numpy()
+    t0 = time.perf_counter()
+    ref = O.moe_layer(xs, wg, f(w1), f(w3), f(w2), k, mode_id, shared=None)
+    dt = time.perf_counter() - t0
+    ref_out = ref["out"] + (xs.astype(np.float64) if stack.residual else 0.0)
+    gout = out[:n].float().cpu().numpy().astype(np.float64)
+    err = float(np.linalg.norm(gout - ref_out) / max(np.linalg.norm(ref_out), 1e-30))
+    cpu = {"value": n / dt / N, "unit": "tokens/s", "cores": threads, "kind": "port",
+           "sample": f"first {n} of {T} tokens through one layer (layer {l}: its router rows and experts, "
+                     f"full size), fp32 oracle (oracle/, OpenMP x{threads}) on {cpu_model_name()}: {dt:.2f} s; "
+                     f"value = that per-layer rate / {N} layers"}
+    parity = {"layer_checked": l, "routing_tokens_checked": T, "routing_bitexact": routing_ok,
+              "routing_checked": "idx, counts, offsets, dst", "routing_oracle_s": round(t_route, 2),
+              "tokens_checked": n, "routing_indices_bitexact": bool(np.array_equal(gi[:n], ref["idx"])),
+              "out_rel_l2_vs_fp32_oracle": err, "tolerance": 1e-2, "pass": bool(routing_ok and err <= 1e-2)}
+    return cpu, parity
+
+
+def stack_e2e(stack, xs_dev, steps, fetch):
+    """End to end through StratifiedMoEStack.forward with host buffers: each
+    step copies its tokens from pinned host memory, runs every layer and reads
+    the last layer's output back to pinned host memory, inside the timed region."""
+    import torch
+    xs_host = [x.cpu().pin_memory() for x in xs_dev]
+    T, d = xs_dev[0].shape
+    x_dev = torch.empty_like(xs_dev[0])
+    out_host = torch.empty((T, d), dtype=torch.bfloat16).pin_memory()
+    s = torch.cuda.current_stream()
+    torch.cuda.synchronize()
+    a, z = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(s)
+    for i in range(steps):
+        x_dev.copy_(xs_host[i % len(xs_host)], non_blocking=True)
+        o = stack(x_dev, fetch=fetch)
+        out_host.copy_(o, non_blocking=True)
+    z.record(s)
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(z) / steps
+    return {"value": T / (ms / 1e3), "unit": "tokens/s", "h2d_bytes_per_step": T * d * 2,
+            "d2h_bytes_per_step": T * d * 2, "steps": steps,
+            "api": "StratifiedMoEStack.forward (pinned host tokens in, last layer's output out, inside the timed "
+                   "region)"}
+
+
 def run_stack(args, cfg):
     """C3: the 56-layer stratified stack on one GPU (BASELINE.json configs[2])."""
     import torch
@@ -356,6 +435,11 @@ def run_stack(args, cfg):
     ms = a.elapsed_time(b) / args.steps
     stack(x, timeline=True, fetch="stream")
     parts = stack.measured_parts()
+    cpu = parity = e2e = None
+    if not args.no_cpu_baseline:
+        cpu, parity = stack_parity_and_cpu(args, stack, T, mode)
+    if not args.no_e2e:
+        e2e = stack_e2e(stack, [x], 1, "stream")
     pk = peaks()
     flops = N * (6.0 * T * k * d * ff + 2.0 * T * d * E)
     n_cold = sum(len(c) for c in stack.cold)
@@ -382,6 +466,13 @@ def run_stack(args, cfg):
         "analytical_parts_per_layer_s": {"act_load": ana.act_load, "mig_load": ana.mig_load, "lat_gpu": ana.lat_gpu,
                                          "system": "configs/system_b200.yaml (measured peaks), k counted"},
         "h2d_gbs": mig_bytes / max(1e-9, parts.mig_load * N) / 1e9,
+        "roofline": {"kernel": f"whole {N}-layer stack step (K3/K4 of every layer + router/permute/combine)",
+                     "bound": "tensor", "achieved": flops / (ms / 1e3) / 1e12, "peak": pk["bf16_sus"],
+                     "unit": "TFLOP/s", "frac": flops / (ms / 1e3) / 1e12 / pk["bf16_sus"], "traffic": None,
+                     "peak_kind": f"bf16_tflops_sustained ({pk['src']}); burst {pk['bf16']}"},
+        "cpu_baseline": cpu,
+        "parity": parity,
+        "e2e": e2e,
         "gpu_launches": stack.launches_per_step * args.steps,
         "clocks": clk.summary(),
     }
@@ -429,6 +520,13 @@ def run_stack_decode(args, cfg):
                 "pcie_gbs": f * per_expert / (ms / 1e3) / 1e9, "clocks": clk.summary()}
 
     cal_res = measure("calibrated")
+    cpu = parity = e2e = None
+    if not args.no_cpu_baseline:
+        cpu, parity = stack_parity_and_cpu(args, stack, T, mode)
+    if not args.no_e2e:
+        xs = [make_topic_tokens(wl, T, 1, seed=200 + i, device="cuda")[0] for i in range(args.steps)]
+        e2e = stack_e2e(stack, xs, args.steps, "touched")
+        e2e["residency"] = "calibrated"
     rnd_plan = eas.random_baseline(E, cap, N, seed=0)
     stack.set_residency(rnd_plan)
     rnd_res = measure("random_baseline")
@@ -446,7 +544,10 @@ def run_stack_decode(args, cfg):
                      "achieved": cal_res["pcie_gbs"], "peak": 55.0, "unit": "GB/s",
                      "frac": cal_res["pcie_gbs"] / 55.0, "traffic": None,
                      "peak_kind": "copy-engine H2D rate of the C3 prefill stack (configs/system_b200.yaml)"},
-        "gpu_launches": None,
+        "cpu_baseline": cpu,
+        "parity": parity,
+        "e2e": e2e,
+        "gpu_launches": stack.launches_per_step_at(T, "touched") * args.steps,
         "clocks": cal_res["clocks"],
     }
     print(json.dumps(line), flush=True)

@@ -112,8 +112,17 @@ class StratifiedMoEStack:
 
     @property
     def launches_per_step(self) -> int:
-        per = 1 + 4 + 1  # router, permute x4, combine
-        return sum(per + (2 if self.plan.resident[l] else 0) + (2 if self.cold[l] else 0) for l in range(self.N))
+        return self.launches_per_step_at(1 << 20, "stream")
+
+    def launches_per_step_at(self, T: int, fetch: str = "stream") -> int:
+        """Kernel launches of one forward over T tokens (router, permute index
+        kernel(s) + row copy, GEMMs, combine; touched mode: one fetch launch per
+        layer with cold experts and one K3/K4 over all experts)."""
+        perm = (1 if T * self.k <= 2048 else 3) + 1
+        if fetch == "touched":
+            return sum(1 + perm + (1 if self.cold[l] else 0) + 2 + 1 for l in range(self.N))
+        return sum(1 + perm + 1 + (2 if self.plan.resident[l] else 0) + (2 if self.cold[l] else 0)
+                   for l in range(self.N))
 
     def _buffers(self, T: int) -> _Bufs:
         if self._bufs is None or self._bufs.T != T:
