@@ -147,6 +147,30 @@ def test_grouped_gemms_vs_torch_fp32(E, d, ff, counts):
         assert rel_l2(y[r0:r1].float().cpu(), yref.cpu()) < 1e-2, f"y expert {e}"
 
 
+def test_grouped_gemms_with_64_wide_k_stages():
+    """K % 128 == 64 takes the BK = 64 pipeline (6 stages) of both GEMMs: the
+    SwiGLU GEMM at d = 320 and the down projection at K = ff = 192."""
+    E, d, ff = 2, 320, 256
+    wts, x, offs_t, offs = _gemm_case(E, d, ff, [300, 17])
+    h = ops.grouped_swiglu(x, offs_t, list(range(E)), [wts.w13[e] for e in range(E)], ff)
+    w1, w3 = split_w13(wts.w13)
+    for e in range(E):
+        r0, r1 = int(offs[e]), int(offs[e + 1])
+        xe = x[r0:r1].float()
+        href = torch.nn.functional.silu(xe @ w1[e].float().T) * (xe @ w3[e].float().T)
+        assert rel_l2(h[r0:r1].float().cpu(), href.cpu()) < 1e-2, f"h expert {e}"
+    d2, K = 256, 192
+    g = torch.Generator(device=DEV).manual_seed(5)
+    hk = (torch.randn((int(offs[-1]), K), generator=g, device=DEV) * 0.5).to(torch.bfloat16)
+    w2 = [(torch.randn((d2, K), generator=g, device=DEV) / K ** 0.5).to(torch.bfloat16) for _ in range(E)]
+    y = ops.grouped_down(hk, offs_t, list(range(E)), w2, d2)
+    torch.cuda.synchronize()
+    for e in range(E):
+        r0, r1 = int(offs[e]), int(offs[e + 1])
+        yref = hk[r0:r1].float() @ w2[e].float().T
+        assert rel_l2(y[r0:r1].float().cpu(), yref.cpu()) < 1e-2, f"y expert {e}"
+
+
 def test_grouped_subset_groups_only_touch_their_rows():
     E, d, ff = 4, 256, 256
     wts, x, offs_t, offs = _gemm_case(E, d, ff, [100, 200, 300, 50])
