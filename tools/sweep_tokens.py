@@ -64,6 +64,7 @@ def compare_paths(cfg):
         for name, tmax in (("small", 1 << 30), ("prefill", 0)):
             layer = MoELayer(wts, k, mode)
             layer.SMALL_T_MAX = tmax
+            layer.SMALL_ROWS_PER_EXPERT_MAX = tmax
             layer.SMALL_GATHER_T_MAX = min(layer.SMALL_GATHER_T_MAX, tmax)
             layer.DENSE_T_MAX = 0
             try:
