@@ -15,8 +15,8 @@
 //     CTA), N=256 (128 B rows per CTA), K=16 per instruction, fp32 accumulators
 //     in TMEM (2 x 256 columns: the epilogue of tile i overlaps the MMAs of i+1).
 //   * TMA (cp.async.bulk.tensor, 128B swizzle) streams K slices of A and B into
-//     a 192 KB smem ring guarded by mbarriers (K3: 3 stages of K = 128; K4: 6
-//     stages of K = 64); both CTAs' loads complete on the leader's "full"
+//     a 192 KB smem ring guarded by mbarriers (3 stages of K = 128, or 6 of
+//     K = 64 when K % 128 != 0); both CTAs' loads complete on the leader's "full"
 //     barrier, the leader's MMA commit frees the slot in both CTAs (multicast
 //     commit).
 //   * Warp roles: w0 TMA producer, w1 MMA issuer (leader CTA, one thread),
