@@ -86,11 +86,12 @@ struct TileCoord {
 // wave static, then an atomic counter), so the group search resumes where the
 // previous tile's ended instead of scanning from group 0 (C4: 64 groups, a
 // serial smem scan of ~32 steps per tile delayed the producer's TMA issue).
-COX_DEV TileCoord decode_tile(int t, const int* s_prefix, const int* s_rows, int band, int& g) {
+// mh: rows per m-tile of a pair (256; 128 in the M128 mode)
+COX_DEV TileCoord decode_tile(int t, const int* s_prefix, const int* s_rows, int band, int mh, int& g) {
   TileCoord c;
   while (t >= s_prefix[g + 1]) ++g;
   const int local = t - s_prefix[g];
-  const int mt = (s_rows[g] + 2 * GM_BM - 1) / (2 * GM_BM);
+  const int mt = (s_rows[g] + mh - 1) / mh;
   const int per_band = mt * band;
   const int b = local / per_band;
   const int r = local - b * per_band;
@@ -135,9 +136,19 @@ COX_DEV void cp_async_cg16(uint32_t dst, const void* src, uint32_t src_bytes) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(src_bytes) : "memory");
 }
 
-template <int EPI, int KA, bool GATHER = false>
+// M128 (medium batches, segments of <= ~128 rows): M = 128 per pair, 64 A
+// rows per CTA, so a segment that fits one 128-row m-tile keeps both SMs'
+// MMAs on it instead of one SM computing 128 rows past the segment end.  The
+// accumulator of cta_group::2 with M = 128 holds N columns [0, 128) in TMEM
+// lanes 0-63 and [128, 256) in lanes 64-127 (same column addresses); for the
+// SwiGLU GEMM each CTA's 128 B rows are 64 gate + the 64 matching up rows, so
+// every epilogue warp finds gate and up in its own lanes.
+template <int EPI, int KA, bool GATHER = false, bool M128 = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GM_THREADS + (GATHER ? 32 * GM_GATHER_WARPS : 0), 1)
     grouped_gemm_kernel(const __grid_constant__ GemmParams p) {
+  static_assert(!(GATHER && M128), "the gather mode uses 256-row pair tiles");
+  constexpr int MH = M128 ? GM_BM : 2 * GM_BM;      // rows per pair m-tile
+  constexpr int ROWS_CTA = MH / 2;                  // A rows per CTA
   constexpr int BK = GM_BK * KA;
   constexpr int STAGES = GmRing<KA>::STAGES;
   constexpr int NB = GM_STAGES;  // barrier / atom array length (>= STAGES)
@@ -199,7 +210,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GM_THREADS + (GATHER
         const int rows = p.offsets[e + 1] - r0;
         s_row0[g] = r0;
         s_rows[g] = rows;
-        tiles = ((rows + 2 * GM_BM - 1) / (2 * GM_BM)) * p.n_tiles;
+        tiles = ((rows + MH - 1) / MH) * p.n_tiles;
       }
       int incl = tiles;
 #pragma unroll
@@ -288,22 +299,29 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GM_THREADS + (GATHER
       int si = 0, gcur = 0;
       int t = fetch_tile(si, true);
       while (t < total) {
-        const TileCoord c = decode_tile(t, s_prefix, s_rows, p.band, gcur);
-        const int a_row = s_row0[c.g] + c.m * 2 * GM_BM + (int)rank * GM_BM;
+        const TileCoord c = decode_tile(t, s_prefix, s_rows, p.band, MH, gcur);
+        const int a_row = s_row0[c.g] + c.m * MH + (int)rank * ROWS_CTA;
         const int b_row = c.n * GM_BN + (int)rank * (GM_BN / 2);
+        // M128 SwiGLU: this CTA's B = gate rows [256 n + 64 rank, +64) over the matching up rows (+128)
+        const int b_gate = c.n * GM_BN + (int)rank * 64;
         const CUtensorMap* bmap = &p.b_map[c.g];
         int t_next = total;
         for (int kb = 0; kb < nk; ++kb) {
           mbar_wait(smem_u32(&empty[stage]), phase ^ 1);
           const uint32_t fb_local = smem_u32(&full[stage]);
           const uint32_t fb = mapa(fb_local, 0);
-          if (rank == 0) mbar_arrive_expect_tx(fb_local, GATHER ? 2 * B_STAGE + 16u : 2 * (A_STAGE + B_STAGE));
+          if (rank == 0)
+            mbar_arrive_expect_tx(fb_local, GATHER ? 2 * B_STAGE + 16u : 2 * ((M128 ? A_STAGE / 2 : A_STAGE) + B_STAGE));
 #pragma unroll
           for (int a = 0; a < KA; ++a) {
             const uint32_t da = smem_u32(sA + stage * A_STAGE + a * GM_A_BYTES);
             const uint32_t db = smem_u32(sB + stage * B_STAGE + a * GM_B_BYTES);
             const int kc = kb * BK + a * GM_BK;
-            if (hint) {
+            if (M128 && EPI == EPI_SWIGLU) {
+              tma_load_2d_pair(da, &p.a_map, fb, kc, a_row);
+              tma_load_2d_pair(db, bmap, fb, kc, b_gate);
+              tma_load_2d_pair(db + GM_B_BYTES / 2, bmap, fb, kc, b_gate + GM_BN / 2);
+            } else if (hint) {
               if (!GATHER) tma_load_2d_pair_hint(da, &p.a_map, fb, kc, a_row, pol_a);
               tma_load_2d_pair_hint(db, bmap, fb, kc, b_row, pol_b);
             } else {
@@ -321,7 +339,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GM_THREADS + (GATHER
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer (leader CTA)
     if (rank == 0 && lane == 0) {
-      const uint32_t idesc = idesc_bf16_f32(2 * GM_BM, GM_BN);
+      const uint32_t idesc = idesc_bf16_f32(MH, GM_BN);
       uint32_t stage = 0, phase = 0;
       int si = 0;
       int t = fetch_tile(si, true);
@@ -406,7 +424,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GM_THREADS + (GATHER
     int si = 0, gcur = 0;
     int t = fetch_tile(si, lane == 0);
     while (t < total) {
-      const TileCoord c = decode_tile(t, s_prefix, s_rows, p.band, gcur);
+      const TileCoord c = decode_tile(t, s_prefix, s_rows, p.band, MH, gcur);
       const int lrow0 = c.m * 2 * GM_BM + (int)rank * GM_BM;  // first A row of this CTA in the group
       const __nv_bfloat16* src[8];
       uint32_t sbytes[8];
@@ -447,7 +465,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GM_THREADS + (GATHER
     for (int it = 0;; ++it) {
       const int t = fetch_tile(si, lane == 0);
       if (t >= total) break;
-      const TileCoord c = decode_tile(t, s_prefix, s_rows, p.band, gcur);
+      const TileCoord c = decode_tile(t, s_prefix, s_rows, p.band, MH, gcur);
       const int acc = it & 1;
       const uint32_t acc_phase = (it >> 1) & 1;
       mbar_wait(smem_u32(&tfull[acc]), acc_phase);
@@ -458,7 +476,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GM_THREADS + (GATHER
       // conflict-free), then every st.global.v4 instruction of the warp writes
       // 4 rows x 128 contiguous bytes (full lines) instead of 32 scattered
       // 16-byte pieces.
-      const int wrow0 = c.m * 2 * GM_BM + (int)rank * GM_BM + ew * 32;  // first row of this warp in the group
+      // first row of this warp in the group (M128: warps 0,1 and 2,3 hold the same 64 rows, N halves)
+      const int wrow0 = M128 ? c.m * MH + (int)rank * ROWS_CTA + (ew & 1) * 32 : c.m * MH + (int)rank * GM_BM + ew * 32;
       const int vrows = s_rows[c.g] - wrow0;                               // rows of the warp that are stored
       const long long grow0 = (long long)s_row0[c.g] + wrow0;
       uint32_t* stg = s_stage + ew * (32 * 32);
@@ -475,7 +494,39 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GM_THREADS + (GATHER
         }
         __syncwarp();
       };
-      if constexpr (EPI == EPI_SWIGLU) {
+      if constexpr (EPI == EPI_SWIGLU && M128) {
+        // N columns 0-63 gate / 64-127 up of h block 2n (lanes 0-63) or 2n+1 (lanes 64-127)
+        __nv_bfloat16* ocol = out + (long long)c.n * (GM_BN / 2) + (ew >> 1) * 64;
+#pragma unroll 1
+        for (int cc = 0; cc < 2; ++cc) {
+          uint32_t gr[32], ur[32];
+          tmem_ld2_32x32b_x32(tbase + cc * 32, gr, tbase + 64 + cc * 32, ur);
+          uint32_t pk[16];
+#pragma unroll
+          for (int q = 0; q < 16; ++q) {
+            const float g0 = __uint_as_float(gr[2 * q]), g1 = __uint_as_float(gr[2 * q + 1]);
+            const float u0 = __uint_as_float(ur[2 * q]), u1 = __uint_as_float(ur[2 * q + 1]);
+            pk[q] = pack_bf16x2(silu_f(g0) * u0, silu_f(g1) * u1);
+          }
+#pragma unroll
+          for (int q = 0; q < 4; ++q) stage16(cc * 4 + q, pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+        }
+        flush64(ocol);
+      } else if constexpr (EPI == EPI_STORE && M128) {
+        // N columns [128 h, 128 h + 128) of the warp's rows, h = ew >> 1
+        __nv_bfloat16* ocol = out + (long long)c.n * GM_BN + (ew >> 1) * (GM_BN / 2);
+#pragma unroll 1
+        for (int cc = 0; cc < 4; ++cc) {
+          uint32_t r[32];
+          tmem_ld_32x32b_x32(tbase + cc * 32, r);
+          uint32_t pk[16];
+#pragma unroll
+          for (int q = 0; q < 16; ++q) pk[q] = pack_bf16x2(__uint_as_float(r[2 * q]), __uint_as_float(r[2 * q + 1]));
+#pragma unroll
+          for (int q = 0; q < 4; ++q) stage16((cc & 1) * 4 + q, pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+          if (cc & 1) flush64(ocol + (cc >> 1) * 64);
+        }
+      } else if constexpr (EPI == EPI_SWIGLU) {
         __nv_bfloat16* ocol = out + (long long)c.n * (GM_BN / 2);
 #pragma unroll 1
         for (int cc = 0; cc < (GM_BN / 2) / 32; ++cc) {
@@ -640,13 +691,23 @@ int launch_grouped_gemm(int epi, const void* A, long long rows_cap, int K, const
   std::lock_guard<std::mutex> lk(mu);
   const bool gather = gx != nullptr;
   if (gather && epi != EPI_SWIGLU) return -1;
-  int rc = gather ? 0 : get_map(&p.a_map, A, (unsigned long long)rows_cap, (unsigned long long)K, (unsigned)GM_BM);
+  // M128 mode when the segments average <= 64 rows (medium batches).  Measured
+  // (tools/sweep_tokens.py, same box): C4 T = 512 (48 rows per expert) 305 ->
+  // 283 us, C2 T = 256 (64 rows) 644 -> 555 us; at 96-128 rows it loses (C4
+  // T = 1024 347 -> 371 us: the pairs' B operand is fetched twice as often).
+  // COX_GEMM_M128=0/1 forces it (A/B, tests).
+  static const int m128_env = env_int("COX_GEMM_M128", -1);
+  const bool m128 = !gather && (m128_env >= 0 ? m128_env == 1 : rows_cap <= 64LL * n_groups);
+  int rc = gather ? 0
+                  : get_map(&p.a_map, A, (unsigned long long)rows_cap, (unsigned long long)K,
+                            (unsigned)(m128 ? GM_BM / 2 : GM_BM));
   if (rc) return rc;
   p.gx = static_cast<const __nv_bfloat16*>(gx);
   p.row_tokens = row_tokens;
   p.gx_ld = gx_ld;
   for (int g = 0; g < n_groups; ++g) {
-    rc = get_map(&p.b_map[g], B[g], (unsigned long long)N, (unsigned long long)K, GM_BN / 2);
+    rc = get_map(&p.b_map[g], B[g], (unsigned long long)N, (unsigned long long)K,
+                 (m128 && epi == EPI_SWIGLU) ? GM_BN / 4 : GM_BN / 2);
     if (rc) return rc;
     p.group_expert[g] = group_expert[g];
   }
@@ -695,28 +756,34 @@ int launch_grouped_gemm(int epi, const void* A, long long rows_cap, int K, const
   // interleaved: C4's routed K4 (K = 1408) 6.96 -> 6.63 ms, C2's (K = 14336)
   // 43.9 either way (tools/ab_k4ka.sh, round 2).
   const int ka = K % (2 * GM_BK) == 0 ? 2 : 1;
-#define GM_LAUNCH(E_, KA_, G_)                                                                                 \
+#define GM_LAUNCH(E_, KA_, G_, M_)                                                                             \
   do {                                                                                                         \
     static bool attr = false;                                                                                  \
     if (!attr) {                                                                                               \
-      cudaFuncSetAttribute(grouped_gemm_kernel<E_, KA_, G_>, cudaFuncAttributeMaxDynamicSharedMemorySize,      \
+      cudaFuncSetAttribute(grouped_gemm_kernel<E_, KA_, G_, M_>, cudaFuncAttributeMaxDynamicSharedMemorySize,  \
                            (int)GmRing<KA_>::SMEM);                                                            \
       attr = true;                                                                                             \
     }                                                                                                          \
-    grouped_gemm_kernel<E_, KA_, G_><<<grid, GM_THREADS + (G_ ? 32 * GM_GATHER_WARPS : 0), GmRing<KA_>::SMEM,   \
-                                       s>>>(p);                                                                \
+    grouped_gemm_kernel<E_, KA_, G_, M_><<<grid, GM_THREADS + (G_ ? 32 * GM_GATHER_WARPS : 0),                 \
+                                           GmRing<KA_>::SMEM, s>>>(p);                                         \
   } while (0)
   if (epi == EPI_SWIGLU) {
     if (gather) {
-      if (ka == 2) GM_LAUNCH(EPI_SWIGLU, 2, true);
-      else GM_LAUNCH(EPI_SWIGLU, 1, true);
+      if (ka == 2) GM_LAUNCH(EPI_SWIGLU, 2, true, false);
+      else GM_LAUNCH(EPI_SWIGLU, 1, true, false);
+    } else if (m128) {
+      if (ka == 2) GM_LAUNCH(EPI_SWIGLU, 2, false, true);
+      else GM_LAUNCH(EPI_SWIGLU, 1, false, true);
     } else {
-      if (ka == 2) GM_LAUNCH(EPI_SWIGLU, 2, false);
-      else GM_LAUNCH(EPI_SWIGLU, 1, false);
+      if (ka == 2) GM_LAUNCH(EPI_SWIGLU, 2, false, false);
+      else GM_LAUNCH(EPI_SWIGLU, 1, false, false);
     }
+  } else if (m128) {
+    if (ka == 2) GM_LAUNCH(EPI_STORE, 2, false, true);
+    else GM_LAUNCH(EPI_STORE, 1, false, true);
   } else {
-    if (ka == 2) GM_LAUNCH(EPI_STORE, 2, false);
-    else GM_LAUNCH(EPI_STORE, 1, false);
+    if (ka == 2) GM_LAUNCH(EPI_STORE, 2, false, false);
+    else GM_LAUNCH(EPI_STORE, 1, false, false);
   }
 #undef GM_LAUNCH
   return launch_status();
