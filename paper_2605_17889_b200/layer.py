@@ -10,7 +10,7 @@ Kernel selection by batch size (all measured on B200):
     (cox_decode_moe: router + every expert + shared experts + combine);
   * T <= SMALL_GATHER_T_MAX (64): router launch + one weight-streaming launch
     that reads the router's idx directly (cox_small_expert_ffn_idx);
-  * T <= SMALL_T_MAX (256) and T*k <= 48 E: router + permute (x_perm
+  * T <= SMALL_T_MAX (256) and T*k <= 32 E: router + permute (x_perm
     materialised) + one weight-streaming launch (cox_small_expert_ffn);
   * larger batches: router, permute, K3, K4, combine (persistent tcgen05
     grouped GEMMs), shared experts on a side stream.
@@ -90,11 +90,12 @@ class MoELayer:
     # experts), csrc/small_gemm.cu
     SMALL_T_MAX = 256
     # ... and while an expert averages at most this many rows (the kernel runs
-    # segments in 64-token chunks).  Measured with tools/sweep_tokens.py
-    # (graph replay, us, weight-streaming vs prefill kernels): C2 (E=8, k=2)
-    # T=192 (48 rows) 511 vs 590, T=256 (64 rows) 734 vs 601; C4 (E=64, k=6)
-    # T=256 (24 rows) 278 vs 287, T=384 (36 rows) 356 vs 302.
-    SMALL_ROWS_PER_EXPERT_MAX = 48
+    # segments in 64-token chunks and re-reads them per 128 weight rows).
+    # Measured with tools/sweep_tokens.py paths (graph replay, us,
+    # weight-streaming vs prefill kernels with their M = 128 pair tiles):
+    # C2 (E=8, k=2) T=128 (32 rows) 495 vs 530, T=192 (48 rows) 660 vs 534;
+    # C4 (E=64, k=6) T=192 (18 rows) 235 vs 256, T=256 (24 rows) 265 vs 258.
+    SMALL_ROWS_PER_EXPERT_MAX = 32
     # Row gathers (TMA tile::gather4 of x rows) only up to this many tokens:
     # above it the permute materialises x_perm and the kernel loads tiled B
     # boxes.  Measured on C4 (tools/sweep_decode_large.py, us/step, gather vs

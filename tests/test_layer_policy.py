@@ -15,10 +15,11 @@ def c4_layer():
 
 def test_small_path_needs_few_rows_per_expert():
     """Mixtral-shaped (E=8, k=2): the weight-streaming kernel only while an expert
-    averages <= 48 rows (T <= 192); measured slower than the prefill kernels at 64."""
+    averages <= 32 rows (T <= 128); measured slower than the prefill kernels
+    (M = 128 pair tiles) at 48."""
     wts = make_layer_weights(8, 256, 128, seed=0, device="cpu")
     L = MoELayer(wts, 2, "mixtral")
-    assert L.uses_small_path(192) and not L.uses_small_path(193) and not L.uses_small_path(256)
+    assert L.uses_small_path(128) and not L.uses_small_path(129) and not L.uses_small_path(192)
 
 
 def test_decode_path_selection(c4_layer):
