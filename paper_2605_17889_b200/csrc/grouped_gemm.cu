@@ -61,6 +61,7 @@ constexpr int EPI_STORE = 1;
 struct alignas(64) GemmParams {
   CUtensorMap a_map;
   CUtensorMap b_map[GM_MAXG];
+  CUtensorMap b_map64[GM_MAXG];  // SwiGLU half tiles: 64-row boxes (gate rows over up rows)
   const int32_t* offsets;
   int* tile_counter;  // zeroed before launch; dynamic tile scheduler
   void* out;
@@ -71,6 +72,7 @@ struct alignas(64) GemmParams {
   int n_tiles;
   int band;
   int l2_mode;  // L2 cache policy of the operand loads, see l2_policies()
+  int half_tiles;  // 1: a group's last m-tile with <= 128 rows runs as an M = 128 pair tile
   // gather mode (K3 without x_perm): A row r of group g is token
   // row_tokens[row0_g + r] of gx [*, K] (row pitch gx_ld elements)
   const __nv_bfloat16* gx;
@@ -80,24 +82,27 @@ struct alignas(64) GemmParams {
 
 struct TileCoord {
   int g, m, n;
+  bool half;  // M = 128 pair tile (64 A rows per CTA)
 };
 
 // g: the caller's group cursor.  Every role sees increasing tile ids (first
 // wave static, then an atomic counter), so the group search resumes where the
 // previous tile's ended instead of scanning from group 0 (C4: 64 groups, a
 // serial smem scan of ~32 steps per tile delayed the producer's TMA issue).
-// mh: rows per m-tile of a pair (256; 128 in the M128 mode)
-COX_DEV TileCoord decode_tile(int t, const int* s_prefix, const int* s_rows, int band, int mh, int& g) {
+// half_ok: the group's last m-tile runs as an M = 128 pair tile when at most
+// 128 of its rows are left (see grouped_gemm_kernel)
+COX_DEV TileCoord decode_tile(int t, const int* s_prefix, const int* s_rows, int band, bool half_ok, int& g) {
   TileCoord c;
   while (t >= s_prefix[g + 1]) ++g;
   const int local = t - s_prefix[g];
-  const int mt = (s_rows[g] + mh - 1) / mh;
+  const int mt = (s_rows[g] + 2 * GM_BM - 1) / (2 * GM_BM);
   const int per_band = mt * band;
   const int b = local / per_band;
   const int r = local - b * per_band;
   c.g = g;
   c.m = r / band;
   c.n = b * band + (r - c.m * band);
+  c.half = half_ok && c.m == mt - 1 && s_rows[g] - c.m * 2 * GM_BM <= GM_BM;  // compile-time false without HALF
   return c;
 }
 
@@ -136,19 +141,21 @@ COX_DEV void cp_async_cg16(uint32_t dst, const void* src, uint32_t src_bytes) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(src_bytes) : "memory");
 }
 
-// M128 (medium batches, segments of <= ~128 rows): M = 128 per pair, 64 A
-// rows per CTA, so a segment that fits one 128-row m-tile keeps both SMs'
-// MMAs on it instead of one SM computing 128 rows past the segment end.  The
-// accumulator of cta_group::2 with M = 128 holds N columns [0, 128) in TMEM
-// lanes 0-63 and [128, 256) in lanes 64-127 (same column addresses); for the
-// SwiGLU GEMM each CTA's 128 B rows are 64 gate + the 64 matching up rows, so
-// every epilogue warp finds gate and up in its own lanes.
-template <int EPI, int KA, bool GATHER = false, bool M128 = false>
+// Half tiles: the last m-tile of a group with at most 128 rows left (short
+// segments of medium batches; the few rows a segment spills past a multiple of
+// 256) runs as an M = 128 pair tile, 64 A rows per CTA, so one SM of the pair
+// does not multiply 128 rows past the segment end.  The accumulator of
+// cta_group::2 with M = 128 holds N columns [0, 128) in TMEM lanes 0-63 and
+// [128, 256) in lanes 64-127 (same column addresses); for the SwiGLU GEMM each
+// CTA's 128 B rows are then 64 gate rows over the 64 matching up rows, so every
+// epilogue warp finds gate and up in its own lanes (64-row boxes of a second
+// tensor map).  A half tile's A box is the usual 128 rows; the MMA reads the
+// first 64.
+template <int EPI, int KA, bool GATHER = false, bool HALF = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GM_THREADS + (GATHER ? 32 * GM_GATHER_WARPS : 0), 1)
     grouped_gemm_kernel(const __grid_constant__ GemmParams p) {
-  static_assert(!(GATHER && M128), "the gather mode uses 256-row pair tiles");
-  constexpr int MH = M128 ? GM_BM : 2 * GM_BM;      // rows per pair m-tile
-  constexpr int ROWS_CTA = MH / 2;                  // A rows per CTA
+  static_assert(!(GATHER && HALF), "the gather mode runs 256-row pair tiles only");
+  constexpr bool half_ok = HALF;
   constexpr int BK = GM_BK * KA;
   constexpr int STAGES = GmRing<KA>::STAGES;
   constexpr int NB = GM_STAGES;  // barrier / atom array length (>= STAGES)
@@ -210,7 +217,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GM_THREADS + (GATHER
         const int rows = p.offsets[e + 1] - r0;
         s_row0[g] = r0;
         s_rows[g] = rows;
-        tiles = ((rows + MH - 1) / MH) * p.n_tiles;
+        tiles = ((rows + 2 * GM_BM - 1) / (2 * GM_BM)) * p.n_tiles;
       }
       int incl = tiles;
 #pragma unroll
@@ -299,28 +306,29 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GM_THREADS + (GATHER
       int si = 0, gcur = 0;
       int t = fetch_tile(si, true);
       while (t < total) {
-        const TileCoord c = decode_tile(t, s_prefix, s_rows, p.band, MH, gcur);
-        const int a_row = s_row0[c.g] + c.m * MH + (int)rank * ROWS_CTA;
+        const TileCoord c = decode_tile(t, s_prefix, s_rows, p.band, half_ok, gcur);
+        const int a_row = s_row0[c.g] + c.m * 2 * GM_BM + (int)rank * (c.half ? GM_BM / 2 : GM_BM);
         const int b_row = c.n * GM_BN + (int)rank * (GM_BN / 2);
-        // M128 SwiGLU: this CTA's B = gate rows [256 n + 64 rank, +64) over the matching up rows (+128)
+        // half SwiGLU tile: 64 gate rows [256 n + 64 rank, +64) over the 64 matching up rows (+128)
+        const bool gate_up = HALF && EPI == EPI_SWIGLU && c.half;
         const int b_gate = c.n * GM_BN + (int)rank * 64;
         const CUtensorMap* bmap = &p.b_map[c.g];
+        const CUtensorMap* bmap64 = &p.b_map64[c.g];
         int t_next = total;
         for (int kb = 0; kb < nk; ++kb) {
           mbar_wait(smem_u32(&empty[stage]), phase ^ 1);
           const uint32_t fb_local = smem_u32(&full[stage]);
           const uint32_t fb = mapa(fb_local, 0);
-          if (rank == 0)
-            mbar_arrive_expect_tx(fb_local, GATHER ? 2 * B_STAGE + 16u : 2 * ((M128 ? A_STAGE / 2 : A_STAGE) + B_STAGE));
+          if (rank == 0) mbar_arrive_expect_tx(fb_local, GATHER ? 2 * B_STAGE + 16u : 2 * (A_STAGE + B_STAGE));
 #pragma unroll
           for (int a = 0; a < KA; ++a) {
             const uint32_t da = smem_u32(sA + stage * A_STAGE + a * GM_A_BYTES);
             const uint32_t db = smem_u32(sB + stage * B_STAGE + a * GM_B_BYTES);
             const int kc = kb * BK + a * GM_BK;
-            if (M128 && EPI == EPI_SWIGLU) {
+            if (HALF && gate_up) {
               tma_load_2d_pair(da, &p.a_map, fb, kc, a_row);
-              tma_load_2d_pair(db, bmap, fb, kc, b_gate);
-              tma_load_2d_pair(db + GM_B_BYTES / 2, bmap, fb, kc, b_gate + GM_BN / 2);
+              tma_load_2d_pair(db, bmap64, fb, kc, b_gate);
+              tma_load_2d_pair(db + GM_B_BYTES / 2, bmap64, fb, kc, b_gate + GM_BN / 2);
             } else if (hint) {
               if (!GATHER) tma_load_2d_pair_hint(da, &p.a_map, fb, kc, a_row, pol_a);
               tma_load_2d_pair_hint(db, bmap, fb, kc, b_row, pol_b);
@@ -339,12 +347,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GM_THREADS + (GATHER
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer (leader CTA)
     if (rank == 0 && lane == 0) {
-      const uint32_t idesc = idesc_bf16_f32(MH, GM_BN);
+      const uint32_t idesc_full = idesc_bf16_f32(2 * GM_BM, GM_BN);
+      const uint32_t idesc_half = idesc_bf16_f32(GM_BM, GM_BN);
       uint32_t stage = 0, phase = 0;
-      int si = 0;
+      int si = 0, gcur = 0;
       int t = fetch_tile(si, true);
+      // the tile's shape is decoded while the previous tile's MMAs run (the
+      // MMA issue gap between tiles is on the critical path)
+      uint32_t idesc_next = idesc_full;
+      if constexpr (HALF)
+        if (t < total && decode_tile(t, s_prefix, s_rows, p.band, half_ok, gcur).half) idesc_next = idesc_half;
       for (int it = 0; t < total; ++it) {
         int t_next = total;
+        const uint32_t idesc = idesc_next;
         const int acc = it & 1;
         const uint32_t acc_phase = (it >> 1) & 1;
         mbar_wait(smem_u32(&tempty[acc]), acc_phase ^ 1);
@@ -363,7 +378,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GM_THREADS + (GATHER
           }
           mma_commit<2>(smem_u32(&empty[stage]));
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
-          if (kb == 0) t_next = fetch_tile(si, true);  // look ahead while the tensor pipe is busy
+          if (kb == 0) {  // look ahead while the tensor pipe is busy
+            t_next = fetch_tile(si, true);
+            if constexpr (HALF)
+              if (t_next < total)
+                idesc_next = decode_tile(t_next, s_prefix, s_rows, p.band, half_ok, gcur).half ? idesc_half
+                                                                                              : idesc_full;
+          }
         }
         mma_commit<2>(smem_u32(&tfull[acc]));
         t = t_next;
@@ -424,7 +445,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GM_THREADS + (GATHER
     int si = 0, gcur = 0;
     int t = fetch_tile(si, lane == 0);
     while (t < total) {
-      const TileCoord c = decode_tile(t, s_prefix, s_rows, p.band, MH, gcur);
+      const TileCoord c = decode_tile(t, s_prefix, s_rows, p.band, false, gcur);
       const int lrow0 = c.m * 2 * GM_BM + (int)rank * GM_BM;  // first A row of this CTA in the group
       const __nv_bfloat16* src[8];
       uint32_t sbytes[8];
@@ -465,7 +486,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GM_THREADS + (GATHER
     for (int it = 0;; ++it) {
       const int t = fetch_tile(si, lane == 0);
       if (t >= total) break;
-      const TileCoord c = decode_tile(t, s_prefix, s_rows, p.band, MH, gcur);
+      const TileCoord c = decode_tile(t, s_prefix, s_rows, p.band, half_ok, gcur);
       const int acc = it & 1;
       const uint32_t acc_phase = (it >> 1) & 1;
       mbar_wait(smem_u32(&tfull[acc]), acc_phase);
@@ -476,8 +497,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GM_THREADS + (GATHER
       // conflict-free), then every st.global.v4 instruction of the warp writes
       // 4 rows x 128 contiguous bytes (full lines) instead of 32 scattered
       // 16-byte pieces.
-      // first row of this warp in the group (M128: warps 0,1 and 2,3 hold the same 64 rows, N halves)
-      const int wrow0 = M128 ? c.m * MH + (int)rank * ROWS_CTA + (ew & 1) * 32 : c.m * MH + (int)rank * GM_BM + ew * 32;
+      // first row of this warp in the group (half tile: warps 0,1 and 2,3 hold the same 64 rows, N halves)
+      const int wrow0 = c.half ? c.m * 2 * GM_BM + (int)rank * (GM_BM / 2) + (ew & 1) * 32
+                               : c.m * 2 * GM_BM + (int)rank * GM_BM + ew * 32;
       const int vrows = s_rows[c.g] - wrow0;                               // rows of the warp that are stored
       const long long grow0 = (long long)s_row0[c.g] + wrow0;
       uint32_t* stg = s_stage + ew * (32 * 32);
@@ -494,7 +516,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GM_THREADS + (GATHER
         }
         __syncwarp();
       };
-      if constexpr (EPI == EPI_SWIGLU && M128) {
+      if (HALF && EPI == EPI_SWIGLU && c.half) {
         // N columns 0-63 gate / 64-127 up of h block 2n (lanes 0-63) or 2n+1 (lanes 64-127)
         __nv_bfloat16* ocol = out + (long long)c.n * (GM_BN / 2) + (ew >> 1) * 64;
 #pragma unroll 1
@@ -512,7 +534,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GM_THREADS + (GATHER
           for (int q = 0; q < 4; ++q) stage16(cc * 4 + q, pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
         }
         flush64(ocol);
-      } else if constexpr (EPI == EPI_STORE && M128) {
+      } else if (HALF && EPI == EPI_STORE && c.half) {
         // N columns [128 h, 128 h + 128) of the warp's rows, h = ew >> 1
         __nv_bfloat16* ocol = out + (long long)c.n * GM_BN + (ew >> 1) * (GM_BN / 2);
 #pragma unroll 1
@@ -526,7 +548,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GM_THREADS + (GATHER
           for (int q = 0; q < 4; ++q) stage16((cc & 1) * 4 + q, pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
           if (cc & 1) flush64(ocol + (cc >> 1) * 64);
         }
-      } else if constexpr (EPI == EPI_SWIGLU) {
+      } else if (EPI == EPI_SWIGLU) {
         __nv_bfloat16* ocol = out + (long long)c.n * (GM_BN / 2);
 #pragma unroll 1
         for (int cc = 0; cc < (GM_BN / 2) / 32; ++cc) {
@@ -686,29 +708,31 @@ int launch_grouped_gemm(int epi, const void* A, long long rows_cap, int K, const
                         const int32_t* group_expert, const void* const* B, int N, void* out, long long ldo,
                         int max_ctas, cudaStream_t s, const void* gx, const int32_t* row_tokens, long long gx_ld) {
   if (n_groups <= 0) return 0;
-  static GemmParams p;  // large (8.6 KB): built in static storage, copied at launch
+  static GemmParams p;  // large (17 KB): built in static storage, copied at launch
   static std::mutex mu;
   std::lock_guard<std::mutex> lk(mu);
   const bool gather = gx != nullptr;
   if (gather && epi != EPI_SWIGLU) return -1;
-  // M128 mode when the segments average <= 64 rows (medium batches).  Measured
-  // (tools/sweep_tokens.py, same box): C4 T = 512 (48 rows per expert) 305 ->
-  // 283 us, C2 T = 256 (64 rows) 644 -> 555 us; at 96-128 rows it loses (C4
-  // T = 1024 347 -> 371 us: the pairs' B operand is fetched twice as often).
-  // COX_GEMM_M128=0/1 forces it (A/B, tests).
-  static const int m128_env = env_int("COX_GEMM_M128", -1);
-  const bool m128 = !gather && (m128_env >= 0 ? m128_env == 1 : rows_cap <= 64LL * n_groups);
-  int rc = gather ? 0
-                  : get_map(&p.a_map, A, (unsigned long long)rows_cap, (unsigned long long)K,
-                            (unsigned)(m128 ? GM_BM / 2 : GM_BM));
+  // half tiles (see grouped_gemm_kernel) for batches whose segments average
+  // <= 2,048 rows: there the last m-tile's padding is a visible share of the
+  // MMAs (C2 T = 1,024: ~256 +- 16 rows per expert, so half the experts spill a
+  // few rows into a second tile); above, the full-tile kernel (same-box A/B:
+  // the half-capable kernel costs 0.4-0.7% at T = 262,144).  COX_GEMM_HALF=0/1
+  // forbids / forces them (A/B, tests).
+  static const int half_env = env_int("COX_GEMM_HALF", -1);
+  p.half_tiles = !gather && (half_env >= 0 ? half_env == 1 : rows_cap <= 2048LL * n_groups);
+  int rc = gather ? 0 : get_map(&p.a_map, A, (unsigned long long)rows_cap, (unsigned long long)K, GM_BM);
   if (rc) return rc;
   p.gx = static_cast<const __nv_bfloat16*>(gx);
   p.row_tokens = row_tokens;
   p.gx_ld = gx_ld;
   for (int g = 0; g < n_groups; ++g) {
-    rc = get_map(&p.b_map[g], B[g], (unsigned long long)N, (unsigned long long)K,
-                 (m128 && epi == EPI_SWIGLU) ? GM_BN / 4 : GM_BN / 2);
+    rc = get_map(&p.b_map[g], B[g], (unsigned long long)N, (unsigned long long)K, GM_BN / 2);
     if (rc) return rc;
+    if (epi == EPI_SWIGLU && p.half_tiles) {
+      rc = get_map(&p.b_map64[g], B[g], (unsigned long long)N, (unsigned long long)K, GM_BN / 4);
+      if (rc) return rc;
+    }
     p.group_expert[g] = group_expert[g];
   }
   // per-launch tile counters: a ring of slots, each zeroed (stream-ordered) before its launch
@@ -756,29 +780,30 @@ int launch_grouped_gemm(int epi, const void* A, long long rows_cap, int K, const
   // interleaved: C4's routed K4 (K = 1408) 6.96 -> 6.63 ms, C2's (K = 14336)
   // 43.9 either way (tools/ab_k4ka.sh, round 2).
   const int ka = K % (2 * GM_BK) == 0 ? 2 : 1;
-#define GM_LAUNCH(E_, KA_, G_, M_)                                                                             \
+#define GM_LAUNCH(E_, KA_, G_, H_)                                                                             \
   do {                                                                                                         \
     static bool attr = false;                                                                                  \
     if (!attr) {                                                                                               \
-      cudaFuncSetAttribute(grouped_gemm_kernel<E_, KA_, G_, M_>, cudaFuncAttributeMaxDynamicSharedMemorySize,  \
+      cudaFuncSetAttribute(grouped_gemm_kernel<E_, KA_, G_, H_>, cudaFuncAttributeMaxDynamicSharedMemorySize,  \
                            (int)GmRing<KA_>::SMEM);                                                            \
       attr = true;                                                                                             \
     }                                                                                                          \
-    grouped_gemm_kernel<E_, KA_, G_, M_><<<grid, GM_THREADS + (G_ ? 32 * GM_GATHER_WARPS : 0),                 \
+    grouped_gemm_kernel<E_, KA_, G_, H_><<<grid, GM_THREADS + (G_ ? 32 * GM_GATHER_WARPS : 0),                 \
                                            GmRing<KA_>::SMEM, s>>>(p);                                         \
   } while (0)
+  const bool h = p.half_tiles != 0;
   if (epi == EPI_SWIGLU) {
     if (gather) {
       if (ka == 2) GM_LAUNCH(EPI_SWIGLU, 2, true, false);
       else GM_LAUNCH(EPI_SWIGLU, 1, true, false);
-    } else if (m128) {
+    } else if (h) {
       if (ka == 2) GM_LAUNCH(EPI_SWIGLU, 2, false, true);
       else GM_LAUNCH(EPI_SWIGLU, 1, false, true);
     } else {
       if (ka == 2) GM_LAUNCH(EPI_SWIGLU, 2, false, false);
       else GM_LAUNCH(EPI_SWIGLU, 1, false, false);
     }
-  } else if (m128) {
+  } else if (h) {
     if (ka == 2) GM_LAUNCH(EPI_STORE, 2, false, true);
     else GM_LAUNCH(EPI_STORE, 1, false, true);
   } else {
