@@ -128,7 +128,7 @@ def _gemm_case(E, d, ff, counts, seed=0):
     (2, 256, 256, [300, 17]),
     (4, 512, 384, [0, 256, 1, 700]),
     (3, 1024, 512, [1000, 513, 255]),
-    (8, 256, 256, [40, 0, 64, 1, 50, 63, 17, 30]),  # <= 64 rows per group on average: the M128 pair mode
+    (8, 256, 256, [40, 0, 64, 1, 50, 63, 17, 30]),  # short segments: M = 128 half tiles
 ])
 def test_grouped_gemms_vs_torch_fp32(E, d, ff, counts):
     wts, x, offs_t, offs = _gemm_case(E, d, ff, counts)
@@ -186,7 +186,7 @@ def test_grouped_subset_groups_only_touch_their_rows():
     (4096, 1024, 3584, 8, 2, "mixtral", 0),   # C1 shape (bf16 inputs on the GPU)
     (999, 512, 256, 8, 2, "mixtral", 0),
     (700, 512, 256, 16, 6, "deepseek", 512),  # fine-grained + shared experts
-    (300, 512, 256, 16, 2, "mixtral", 0),     # medium batch: prefill kernels in the M128 pair mode
+    (300, 512, 256, 16, 2, "mixtral", 0),     # medium batch: prefill kernels with M = 128 half tiles
     (300, 512, 256, 32, 4, "deepseek", 256),
 ])
 def test_layer_vs_oracle(T, d, ff, E, k, mode, shared_ff):
