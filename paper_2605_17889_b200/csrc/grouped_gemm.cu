@@ -778,7 +778,7 @@ int launch_grouped_gemm(int epi, const void* A, long long rows_cap, int K, const
   // K per stage: BK = 128 (3 stages) wherever K allows it.  Measured: C2 K3
   // 92.2 -> 89.6 ms against BK = 64 / 6 stages; the down projection, same box,
   // interleaved: C4's routed K4 (K = 1408) 6.96 -> 6.63 ms, C2's (K = 14336)
-  // 43.9 either way (tools/ab_k4ka.sh, round 2).
+  // 43.9 either way (same-box library A/B).
   const int ka = K % (2 * GM_BK) == 0 ? 2 : 1;
 #define GM_LAUNCH(E_, KA_, G_, H_)                                                                             \
   do {                                                                                                         \
