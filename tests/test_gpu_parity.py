@@ -172,6 +172,24 @@ def test_grouped_gemms_with_64_wide_k_stages():
         assert rel_l2(y[r0:r1].float().cpu(), yref.cpu()) < 1e-2, f"y expert {e}"
 
 
+def test_half_tiles_bit_identical_to_full_tiles():
+    """M = 128 half tiles (a segment's last m-tile with <= 128 rows) give the
+    same bits as 256-row tiles: tools/half_tile_equal.py with the mode forced
+    off and on (the switch is read once per process, so two processes)."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+    tool = Path(__file__).resolve().parents[1] / "tools" / "half_tile_equal.py"
+    out = []
+    for v in ("0", "1"):
+        env = dict(os.environ, COX_GEMM_HALF=v)
+        r = subprocess.run([sys.executable, str(tool)], env=env, capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        out.append(r.stdout.strip().splitlines()[-1])
+    assert out[0] == out[1]
+
+
 def test_grouped_subset_groups_only_touch_their_rows():
     E, d, ff = 4, 256, 256
     wts, x, offs_t, offs = _gemm_case(E, d, ff, [100, 200, 300, 50])
